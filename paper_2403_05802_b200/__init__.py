@@ -1,0 +1,387 @@
+"""ctypes binding of the B200 sparse hot path (include/sparseforge_b200.h).
+
+The product is the sm_100a library ``_lib/libsfg.so`` behind a C-ABI; this
+module is a thin host binding used by the tests and bench.py. It never
+computes anything itself: when the library (or a B200) is missing it raises.
+
+    import paper_2403_05802_b200 as sfg
+    ctx = sfg.Context(0)
+    coo = ctx.from_coo(m, n, rows, cols, vals)          # from_coo (tensor.hpp:156)
+    csr = ctx.convert(coo, "CSR")                        # convert_structure + materialize
+    y   = ctx.spmv(csr, x)                               # run_kernel(spmv_kernel(), ...)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libsfg.so")
+
+KINDS = {"COO": 0, "CSR": 1, "CSC": 2, "DCSR": 3, "ELL": 4, "BCSR": 5, "HYB": 6}
+KIND_NAMES = {v: k for k, v in KINDS.items()}
+F32, BF16 = 0, 1
+FLAG_SORTED, FLAG_SUM_DUPLICATES, FLAG_HOST = 1, 2, 4
+COMPUTE_HOST, COMPUTE_ACCUMULATE = 1, 2
+ERROR_KINDS = ["Parse", "NonAffine", "NonIntegral", "UnsupportedSource", "UnsupportedHeader",
+               "DuplicateCoordinate", "Collision", "InvalidOperation", "Singular", "Io"]
+
+
+class SfgError(RuntimeError):
+    """Status from the C-ABI: ``kind`` is the reference ErrorKind name
+    (errors.hpp:10-21) or "Cuda" / "OutOfMemory"."""
+
+    def __init__(self, status, msg):
+        if 1 <= status <= 10:
+            kind = ERROR_KINDS[status - 1]
+        else:
+            kind = {64: "Cuda", 65: "OutOfMemory"}.get(status, f"status{status}")
+        super().__init__(f"{kind}: {msg}")
+        self.kind = kind
+        self.status = status
+
+
+class Format(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("block_r", C.c_int32), ("block_c", C.c_int32),
+                ("value_dtype", C.c_int32), ("threshold", C.c_int64)]
+
+
+class LevelView(C.Structure):
+    _fields_ = [("storage", C.c_uint32), ("lo", C.c_int64), ("hi", C.c_int64),
+                ("node_count", C.c_int64), ("idx_len", C.c_int64), ("ptr_len", C.c_int64),
+                ("idx", C.c_void_p), ("ptr", C.c_void_p)]
+
+
+class TensorView(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("value_dtype", C.c_int32), ("rows", C.c_int64),
+                ("cols", C.c_int64), ("nlevels", C.c_int32), ("level", LevelView * 4),
+                ("nvals", C.c_int64), ("values", C.c_void_p), ("parts", C.c_void_p * 2)]
+
+
+@dataclass
+class Level:
+    """MaterializedLevel (storage.hpp:77-83) on the host."""
+    flags: int
+    lo: int
+    hi: int
+    node_count: int
+    idx: np.ndarray
+    ptr: np.ndarray
+
+    def explain(self) -> str:
+        names = ((1, "size"), (2, "ptr"), (4, "idx"), (8, "dense_vector"))
+        return ", ".join(n for f, n in names if self.flags & f)
+
+
+@dataclass
+class Materialized:
+    """MaterializedTensor (storage.hpp:85-91) on the host."""
+    fmt: str
+    shape: tuple
+    levels: list = field(default_factory=list)
+    values: np.ndarray = None
+
+    def explain(self) -> str:
+        return " | ".join(f"L{i}: {lv.explain()}" for i, lv in enumerate(self.levels)) + " | val"
+
+
+_lib = None
+
+
+def load():
+    """Load libsfg.so; fails loudly if it was not built (no CPU fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: the CUDA extension is not built "
+                          "(run __graft_entry__.build() or `make lib`)")
+    lib = C.CDLL(LIB_PATH)
+    vp, i64, i32, u32 = C.c_void_p, C.c_int64, C.c_int32, C.c_uint32
+    pp = C.POINTER(C.c_void_p)
+    sig = {
+        "sfg_last_error": (C.c_char_p, []),
+        "sfg_context_create": (C.c_int, [C.c_int, vp, pp]),
+        "sfg_context_set_stream": (C.c_int, [vp, vp]),
+        "sfg_context_destroy": (C.c_int, [vp]),
+        "sfg_context_synchronize": (C.c_int, [vp]),
+        "sfg_format_resolve": (C.c_int, [C.c_char_p, C.POINTER(Format)]),
+        "sfg_plan_text": (C.c_int, [C.POINTER(Format), C.POINTER(Format), C.c_char_p, i64]),
+        "sfg_storage_explain": (C.c_int, [C.POINTER(Format), C.c_char_p, i64]),
+        "sfg_from_coo": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, u32, pp]),
+        "sfg_convert": (C.c_int, [vp, vp, C.POINTER(Format), pp]),
+        "sfg_decompose_rows": (C.c_int, [vp, vp, i64, pp, pp, vp]),
+        "sfg_tensor_view_get": (C.c_int, [vp, vp, C.POINTER(TensorView)]),
+        "sfg_tensor_free": (C.c_int, [vp]),
+        "sfg_spmv": (C.c_int, [vp, vp, vp, vp, u32]),
+        "sfg_spmm": (C.c_int, [vp, vp, vp, i32, i64, i64, vp, i64, u32]),
+        "sfg_row_partition": (C.c_int, [vp, vp, i32, C.POINTER(C.c_int64)]),
+        "sfg_coo_slice_rows": (C.c_int, [vp, vp, i64, i64, pp]),
+        "sfgx_gen_uniform": (C.c_int, [vp, C.c_uint64, i64, i64, i32, pp]),
+        "sfgx_gen_rmat": (C.c_int, [vp, C.c_uint64, i32, i64, pp]),
+        "sfgx_gen_hypersparse": (C.c_int, [vp, C.c_uint64, i64, i64, i64, pp]),
+        "sfgx_gen_dense": (C.c_int, [vp, C.c_uint64, i64, vp]),
+        "sfgx_launch_count": (i64, []),
+        "sfgx_device_alloc": (C.c_int, [vp, i64, pp]),
+        "sfgx_device_free": (C.c_int, [vp, vp]),
+        "sfgx_copy": (C.c_int, [vp, vp, vp, i64, i32]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _check(st):
+    if st != 0:
+        raise SfgError(st, _lib.sfg_last_error().decode(errors="replace"))
+
+
+def resolve_format(text: str) -> Format:
+    lib = load()
+    f = Format()
+    _check(lib.sfg_format_resolve(text.encode(), C.byref(f)))
+    return f
+
+
+def plan_lines(src: str, dst: str):
+    lib = load()
+    buf = C.create_string_buffer(4096)
+    s, d = resolve_format(src), resolve_format(dst)
+    _check(lib.sfg_plan_text(C.byref(s), C.byref(d), buf, 4096))
+    return [l for l in buf.value.decode().split("\n") if l]
+
+
+def storage_explain(fmt: str) -> str:
+    lib = load()
+    buf = C.create_string_buffer(4096)
+    f = resolve_format(fmt)
+    _check(lib.sfg_storage_explain(C.byref(f), buf, 4096))
+    return buf.value.decode()
+
+
+def launch_count() -> int:
+    return int(load().sfgx_launch_count())
+
+
+class DeviceBuffer:
+    """Device allocation owned by a context (stream-ordered)."""
+
+    def __init__(self, ctx: "Context", nbytes: int):
+        self.ctx, self.nbytes = ctx, int(nbytes)
+        p = C.c_void_p()
+        _check(ctx.lib.sfgx_device_alloc(ctx.h, self.nbytes, C.byref(p)))
+        self.ptr = p.value
+
+    def free(self):
+        if self.ptr:
+            self.ctx.lib.sfgx_device_free(self.ctx.h, C.c_void_p(self.ptr))
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def upload(self, arr: np.ndarray):
+        arr = np.ascontiguousarray(arr)
+        assert arr.nbytes <= self.nbytes
+        _check(self.ctx.lib.sfgx_copy(self.ctx.h, C.c_void_p(self.ptr), arr.ctypes.data_as(C.c_void_p),
+                                      arr.nbytes, 0))
+        return self
+
+    def download(self, dtype, count) -> np.ndarray:
+        out = np.empty(int(count), dtype)
+        if out.nbytes:
+            _check(self.ctx.lib.sfgx_copy(self.ctx.h, out.ctypes.data_as(C.c_void_p),
+                                          C.c_void_p(self.ptr), out.nbytes, 1))
+        return out
+
+
+class Tensor:
+    """A device-resident materialized tensor (sfg_tensor handle)."""
+
+    def __init__(self, ctx: "Context", handle, owned=True):
+        self.ctx, self.h, self.owned = ctx, handle, owned
+
+    def __del__(self):
+        try:
+            if self.owned and self.h:
+                self.ctx.lib.sfg_tensor_free(self.h)
+        except Exception:
+            pass
+
+    def view(self) -> TensorView:
+        v = TensorView()
+        _check(self.ctx.lib.sfg_tensor_view_get(self.ctx.h, self.h, C.byref(v)))
+        return v
+
+    @property
+    def kind(self) -> str:
+        return KIND_NAMES[self.view().kind]
+
+    @property
+    def shape(self):
+        v = self.view()
+        return (v.rows, v.cols)
+
+    def parts(self):
+        v = self.view()
+        return [Tensor(self.ctx, C.c_void_p(p), owned=False) for p in v.parts if p]
+
+    def _dl(self, ptr, dtype, count):
+        out = np.empty(int(count), dtype)
+        if out.nbytes:
+            _check(self.ctx.lib.sfgx_copy(self.ctx.h, out.ctypes.data_as(C.c_void_p), C.c_void_p(ptr),
+                                          out.nbytes, 1))
+        return out
+
+    def download(self):
+        """Host copy shaped like the reference MaterializedTensor
+        (storage.hpp:77-91): int64 idx/ptr and f64 values, field for field
+        the layout the oracle returns."""
+        v = self.view()
+        out = Materialized(KIND_NAMES[v.kind], (v.rows, v.cols))
+        for i in range(v.nlevels):
+            lv = v.level[i]
+            idx = self._dl(lv.idx, np.int32, lv.idx_len).astype(np.int64)
+            ptr = self._dl(lv.ptr, np.int32, lv.ptr_len).astype(np.int64)
+            out.levels.append(Level(int(lv.storage), int(lv.lo), int(lv.hi),
+                                           int(lv.node_count), idx, ptr))
+        if v.value_dtype == BF16:
+            raw = self._dl(v.values, np.uint16, v.nvals).astype(np.uint32) << 16
+            out.values = raw.view(np.float32).astype(np.float64)
+        else:
+            out.values = self._dl(v.values, np.float32, v.nvals).astype(np.float64)
+        return out
+
+    def coo_arrays(self):
+        v = self.view()
+        assert v.kind == KINDS["COO"]
+        return (self._dl(v.level[0].idx, np.int32, v.level[0].idx_len),
+                self._dl(v.level[1].idx, np.int32, v.level[1].idx_len),
+                self._dl(v.values, np.float32, v.nvals))
+
+
+class Context:
+    def __init__(self, device: int = 0, stream: int | None = None):
+        self.lib = load()
+        h = C.c_void_p()
+        _check(self.lib.sfg_context_create(device, C.c_void_p(stream or 0), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            self.lib.sfg_context_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream: int):
+        _check(self.lib.sfg_context_set_stream(self.h, C.c_void_p(stream)))
+
+    def synchronize(self):
+        _check(self.lib.sfg_context_synchronize(self.h))
+
+    def buffer(self, nbytes) -> DeviceBuffer:
+        return DeviceBuffer(self, nbytes)
+
+    # ---------------------------------------------------------------- ingest
+    def from_coo(self, m, n, row, col, val, sorted=False, sum_duplicates=False) -> Tensor:
+        """from_coo (tensor.hpp:156) from host arrays."""
+        row = np.ascontiguousarray(row, np.int32)
+        col = np.ascontiguousarray(col, np.int32)
+        val = np.ascontiguousarray(val, np.float32)
+        flags = FLAG_HOST | (FLAG_SORTED if sorted else 0) | (FLAG_SUM_DUPLICATES if sum_duplicates else 0)
+        h = C.c_void_p()
+        vp = lambda a: a.ctypes.data_as(C.c_void_p)
+        _check(self.lib.sfg_from_coo(self.h, m, n, len(val), vp(row), vp(col), vp(val), flags, C.byref(h)))
+        return Tensor(self, h)
+
+    def from_coo_device(self, m, n, nnz, row_ptr, col_ptr, val_ptr, flags=0) -> Tensor:
+        h = C.c_void_p()
+        _check(self.lib.sfg_from_coo(self.h, m, n, nnz, C.c_void_p(row_ptr), C.c_void_p(col_ptr),
+                                     C.c_void_p(val_ptr), flags, C.byref(h)))
+        return Tensor(self, h)
+
+    # ------------------------------------------------------------ conversion
+    def convert(self, src: Tensor, fmt: str, value_dtype: int = F32) -> Tensor:
+        f = resolve_format(fmt)
+        f.value_dtype = value_dtype
+        h = C.c_void_p()
+        _check(self.lib.sfg_convert(self.h, src.h, C.byref(f), C.byref(h)))
+        return Tensor(self, h)
+
+    def decompose_rows(self, coo: Tensor, min_sum: int, totals_ptr: int = 0):
+        s, r = C.c_void_p(), C.c_void_p()
+        _check(self.lib.sfg_decompose_rows(self.h, coo.h, min_sum, C.byref(s), C.byref(r),
+                                           C.c_void_p(totals_ptr)))
+        return Tensor(self, s), Tensor(self, r)
+
+    def row_partition(self, coo: Tensor, parts: int):
+        b = (C.c_int64 * (parts + 1))()
+        _check(self.lib.sfg_row_partition(self.h, coo.h, parts, b))
+        return list(b)
+
+    def slice_rows(self, coo: Tensor, r0: int, r1: int) -> Tensor:
+        h = C.c_void_p()
+        _check(self.lib.sfg_coo_slice_rows(self.h, coo.h, r0, r1, C.byref(h)))
+        return Tensor(self, h)
+
+    # --------------------------------------------------------------- compute
+    def spmv(self, a: Tensor, x: np.ndarray) -> np.ndarray:
+        """y = A x from host x (copies inside, like the reference API)."""
+        x = np.ascontiguousarray(x, np.float32)
+        y = np.zeros(a.shape[0], np.float32)
+        _check(self.lib.sfg_spmv(self.h, a.h, x.ctypes.data_as(C.c_void_p),
+                                 y.ctypes.data_as(C.c_void_p), COMPUTE_HOST))
+        return y
+
+    def spmv_device(self, a: Tensor, x_ptr: int, y_ptr: int, accumulate=False):
+        _check(self.lib.sfg_spmv(self.h, a.h, C.c_void_p(x_ptr), C.c_void_p(y_ptr),
+                                 COMPUTE_ACCUMULATE if accumulate else 0))
+
+    def spmm(self, a: Tensor, b: np.ndarray, b_dtype=F32) -> np.ndarray:
+        if b_dtype == F32:
+            b = np.ascontiguousarray(b, np.float32)
+        else:
+            b = np.ascontiguousarray(b, np.uint16)  # raw bf16 bits
+        nd = b.shape[1]
+        c = np.zeros((a.shape[0], nd), np.float32)
+        _check(self.lib.sfg_spmm(self.h, a.h, b.ctypes.data_as(C.c_void_p), b_dtype, nd, nd,
+                                 c.ctypes.data_as(C.c_void_p), nd, COMPUTE_HOST))
+        return c
+
+    def spmm_device(self, a: Tensor, b_ptr: int, b_dtype: int, nd: int, c_ptr: int,
+                    ldb=None, ldc=None, accumulate=False):
+        _check(self.lib.sfg_spmm(self.h, a.h, C.c_void_p(b_ptr), b_dtype, nd, ldb or nd,
+                                 C.c_void_p(c_ptr), ldc or nd, COMPUTE_ACCUMULATE if accumulate else 0))
+
+    # ------------------------------------------------------------ generators
+    def gen_uniform(self, seed, m, n, per_row) -> Tensor:
+        h = C.c_void_p()
+        _check(self.lib.sfgx_gen_uniform(self.h, seed, m, n, per_row, C.byref(h)))
+        return Tensor(self, h)
+
+    def gen_rmat(self, seed, scale, edges) -> Tensor:
+        h = C.c_void_p()
+        _check(self.lib.sfgx_gen_rmat(self.h, seed, scale, edges, C.byref(h)))
+        return Tensor(self, h)
+
+    def gen_hypersparse(self, seed, m, n, draws) -> Tensor:
+        h = C.c_void_p()
+        _check(self.lib.sfgx_gen_hypersparse(self.h, seed, m, n, draws, C.byref(h)))
+        return Tensor(self, h)
+
+    def gen_dense(self, seed, count, out_ptr):
+        _check(self.lib.sfgx_gen_dense(self.h, seed, count, C.c_void_p(out_ptr)))

@@ -1,0 +1,529 @@
+// abi.cu — the extern "C" boundary (include/sparseforge_b200.h).
+//
+// Each entry point converts C++ failures into a status code (1 + ErrorKind,
+// or SFG_ERR_CUDA / SFG_ERR_OOM) and a thread-local message, mirroring the
+// reference's Error(ErrorKind) convention (errors.hpp:10-36).
+#include <cctype>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "internal.cuh"
+
+namespace sfg {
+const char* last_error();
+}
+
+namespace {
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return SFG_OK;
+  } catch (const sfg::Failure& e) {
+    sfg::set_last_error(e.msg);
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    sfg::set_last_error("host allocation failed");
+    return SFG_ERR_OOM;
+  } catch (const std::exception& e) {
+    sfg::set_last_error(e.what());
+    return SFG_ERR_INVALID_OPERATION;
+  }
+}
+
+void require(bool ok, int code, const char* msg) {
+  if (!ok) sfg::raise(code, msg);
+}
+
+void copy_text(const std::string& s, char* buf, int64_t len) {
+  if (!buf || len <= 0) return;
+  size_t n = std::min<size_t>(s.size(), static_cast<size_t>(len - 1));
+  std::memcpy(buf, s.data(), n);
+  buf[n] = 0;
+}
+
+std::string fmt_name(const sfg_format& f) {
+  switch (f.kind) {
+    case SFG_COO: return "COO";
+    case SFG_CSR: return "CSR";
+    case SFG_CSC: return "CSC";
+    case SFG_DCSR: return "DCSR";
+    case SFG_ELL: return "ELL";
+    case SFG_BCSR: return "BCSR(" + std::to_string(f.block_r) + "," + std::to_string(f.block_c) + ")";
+    case SFG_HYB: return "HYB(" + std::to_string(f.threshold) + ")";
+  }
+  return "?";
+}
+
+// plan_conversion output for a COO source (planner.hpp:95-252), as the
+// reference prints it (plan_lines, planner.hpp:22-27).
+std::string plan_for(const sfg_format& dst) {
+  switch (dst.kind) {
+    case SFG_COO: return "";
+    case SFG_CSR: return "Fill(0)\nMerge(0)\n";
+    case SFG_CSC: return "Swap(0,1)\nSort\nFill(0)\nMerge(0)\n";
+    case SFG_DCSR: return "Merge(0)\n";
+    case SFG_ELL: return "Sum(0)\nEnumerate(0)\nSort\nFill(1)\nMerge(0)\n";
+    case SFG_BCSR:
+      return "TileSplit(0," + std::to_string(dst.block_r) + ")\nTileSplit(2," +
+             std::to_string(dst.block_c) + ")\nSwap(1,2)\nSort\nFill(3)\nFill(2)\nFill(0)\n" +
+             "Vectorize(2)\nMerge(0)\n";
+    case SFG_HYB:
+      return "Decompose(sum(value) groupBy (d0, d1) -> (d0) with value ne 0 -> 1 | otherwise -> 0, " +
+             std::to_string(dst.threshold) +
+             ")\nremainder: Sum(0)\nremainder: Enumerate(0)\nremainder: Sort\nremainder: Fill(1)\n"
+             "remainder: Merge(0)\n";
+  }
+  return "";
+}
+
+// explain_storage(infer_storage(...)) (storage.hpp:35-75; oracle_data.hpp:128-148).
+std::string explain_for(const sfg_format& f) {
+  switch (f.kind) {
+    case SFG_COO: return "L0: idx | L1: idx | val";
+    case SFG_CSR:
+    case SFG_CSC: return "L0: size | L1: ptr, idx | val";
+    case SFG_DCSR: return "L0: idx | L1: ptr, idx | val";
+    case SFG_ELL: return "L0: idx | L1: size | L2: idx | val";
+    case SFG_BCSR:
+      return "L0: size | L1: ptr, idx | L2: size, dense_vector | L3: size, dense_vector | val";
+    case SFG_HYB: return "ELL(L0: idx | L1: size | L2: idx | val) + COO(L0: idx | L1: idx | val)";
+  }
+  return "";
+}
+
+void validate_format(const sfg_format& f) {
+  require(f.kind >= SFG_COO && f.kind <= SFG_HYB, SFG_ERR_PARSE, "unknown format kind");
+  if (f.kind == SFG_BCSR)
+    require(f.block_r > 0 && f.block_c > 0, SFG_ERR_INVALID_OPERATION,
+            "TileSplit factor must be positive");
+  require(f.value_dtype == SFG_F32 || (f.value_dtype == SFG_BF16 && f.kind == SFG_BCSR),
+          SFG_ERR_INVALID_OPERATION, "bf16 values are supported for BCSR only");
+}
+
+sfg_level_view level(uint32_t storage, int64_t lo, int64_t hi, int64_t nodes, int64_t idx_len,
+                     const int32_t* idx, int64_t ptr_len, const int32_t* ptr) {
+  sfg_level_view v;
+  v.storage = storage;
+  v.lo = lo;
+  v.hi = hi;
+  v.node_count = nodes;
+  v.idx_len = idx_len;
+  v.ptr_len = ptr_len;
+  v.idx = idx;
+  v.ptr = ptr;
+  return v;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sfg_last_error(void) { return sfg::last_error(); }
+
+int sfg_context_create(int device, void* stream, sfg_context** out) {
+  return guard([&] {
+    require(out != nullptr, SFG_ERR_INVALID_OPERATION, "null output");
+    *out = nullptr;
+    SFG_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    SFG_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      sfg::raise(SFG_ERR_CUDA, std::string("sm_100a build needs a Blackwell (cc 10.x) device, got ") +
+                                   prop.name);
+    auto* ctx = new sfg_context;
+    ctx->device = device;
+    ctx->stream = static_cast<cudaStream_t>(stream);
+    ctx->sms = prop.multiProcessorCount;
+    SFG_CUDA(cudaMallocHost(&ctx->pinned, 4096));
+    // Keep freed blocks in the pool: conversions allocate and free per call.
+    cudaMemPool_t pool;
+    SFG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t threshold = UINT64_MAX;
+    SFG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+    *out = ctx;
+  });
+}
+
+int sfg_context_set_stream(sfg_context* ctx, void* stream) {
+  return guard([&] {
+    require(ctx, SFG_ERR_INVALID_OPERATION, "null context");
+    ctx->stream = static_cast<cudaStream_t>(stream);
+  });
+}
+
+int sfg_context_synchronize(sfg_context* ctx) {
+  return guard([&] { SFG_CUDA(cudaStreamSynchronize(ctx->stream)); });
+}
+
+int sfg_context_destroy(sfg_context* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    if (ctx->scratch) sfg::dfree(ctx, ctx->scratch);
+    cudaStreamSynchronize(ctx->stream);
+    cudaFreeHost(ctx->pinned);
+    delete ctx;
+  });
+}
+
+int sfg_format_resolve(const char* text, sfg_format* out) {
+  return guard([&] {
+    require(text && out, SFG_ERR_INVALID_OPERATION, "null argument");
+    std::string t;
+    for (const char* p = text; *p; ++p)
+      if (!std::isspace(static_cast<unsigned char>(*p))) t += *p;
+    require(!t.empty(), SFG_ERR_PARSE, "empty format");
+    std::string name = t;
+    int64_t args[2] = {0, 0};
+    int nargs = 0;
+    auto open = t.find('(');
+    if (open != std::string::npos) {
+      require(t.back() == ')', SFG_ERR_PARSE, "malformed format name");
+      name = t.substr(0, open);
+      std::string inner = t.substr(open + 1, t.size() - open - 2);
+      size_t pos = 0;
+      while (pos <= inner.size() && nargs < 3) {
+        size_t next = inner.find(',', pos);
+        if (next == std::string::npos) next = inner.size();
+        std::string piece = inner.substr(pos, next - pos);
+        require(!piece.empty() && piece.find_first_not_of("0123456789") == std::string::npos,
+                SFG_ERR_PARSE, "format arguments must be positive integers");
+        require(nargs < 2, SFG_ERR_PARSE, "too many format arguments");
+        args[nargs++] = std::stoll(piece);
+        pos = next + 1;
+        if (next == inner.size()) break;
+      }
+    }
+    sfg_format f{};
+    f.value_dtype = SFG_F32;
+    if (name == "COO") f.kind = SFG_COO;
+    else if (name == "CSR") f.kind = SFG_CSR;
+    else if (name == "CSC") f.kind = SFG_CSC;
+    else if (name == "DCSR") f.kind = SFG_DCSR;
+    else if (name == "ELL") f.kind = SFG_ELL;
+    else if (name == "BCSR") {
+      // formats.hpp:49-53: r defaults to 2, c defaults to r
+      f.kind = SFG_BCSR;
+      f.block_r = static_cast<int32_t>(nargs > 0 ? args[0] : 2);
+      f.block_c = static_cast<int32_t>(nargs > 1 ? args[1] : f.block_r);
+    } else if (name == "HYB") {
+      f.kind = SFG_HYB;
+      f.threshold = nargs > 0 ? args[0] : 8;
+    } else {
+      sfg::raise(SFG_ERR_PARSE, "unknown format name: " + name);
+    }
+    validate_format(f);
+    *out = f;
+  });
+}
+
+int sfg_plan_text(const sfg_format* src, const sfg_format* dst, char* buf, int64_t len) {
+  return guard([&] {
+    require(src && dst, SFG_ERR_INVALID_OPERATION, "null format");
+    validate_format(*dst);
+    if (src->kind != SFG_COO)
+      sfg::raise(SFG_ERR_UNSUPPORTED_SOURCE, "the device planner converts from COO sources");
+    copy_text(plan_for(*dst), buf, len);
+  });
+}
+
+int sfg_storage_explain(const sfg_format* f, char* buf, int64_t len) {
+  return guard([&] {
+    require(f != nullptr, SFG_ERR_INVALID_OPERATION, "null format");
+    validate_format(*f);
+    copy_text(explain_for(*f), buf, len);
+  });
+}
+
+int sfg_from_coo(sfg_context* ctx, int64_t rows, int64_t cols, int64_t nnz, const int32_t* row,
+                 const int32_t* col, const float* val, uint32_t flags, sfg_tensor** out) {
+  return guard([&] {
+    require(ctx && out, SFG_ERR_INVALID_OPERATION, "null argument");
+    *out = nullptr;
+    require(nnz >= 0 && rows >= 0 && cols >= 0, SFG_ERR_INVALID_OPERATION,
+            "coordinate rank mismatch");
+    require(rows < INT32_MAX && cols < INT32_MAX && nnz < INT32_MAX, SFG_ERR_INVALID_OPERATION,
+            "extent or nnz exceeds the int32 index range");
+    const int32_t* drow = row;
+    const int32_t* dcol = col;
+    const float* dval = val;
+    int32_t* tmp[3] = {nullptr, nullptr, nullptr};
+    if (flags & SFG_FLAG_HOST) {
+      tmp[0] = sfg::dalloc_n<int32_t>(ctx, nnz);
+      tmp[1] = sfg::dalloc_n<int32_t>(ctx, nnz);
+      tmp[2] = sfg::dalloc_n<int32_t>(ctx, nnz);
+      SFG_CUDA(cudaMemcpyAsync(tmp[0], row, nnz * 4, cudaMemcpyHostToDevice, ctx->stream));
+      SFG_CUDA(cudaMemcpyAsync(tmp[1], col, nnz * 4, cudaMemcpyHostToDevice, ctx->stream));
+      SFG_CUDA(cudaMemcpyAsync(tmp[2], val, nnz * 4, cudaMemcpyHostToDevice, ctx->stream));
+      drow = tmp[0];
+      dcol = tmp[1];
+      dval = reinterpret_cast<const float*>(tmp[2]);
+    }
+    sfg_tensor* t = nullptr;
+    try {
+      if (flags & SFG_FLAG_SORTED) {
+        sfg::check_coo_canonical(ctx, drow, dcol, rows, cols, nnz);
+        t = sfg::new_tensor(ctx, SFG_COO, rows, cols);
+        t->nnz = nnz;
+        t->row = sfg::dalloc_n<int32_t>(ctx, nnz);
+        t->idx = sfg::dalloc_n<int32_t>(ctx, nnz);
+        t->val = sfg::dalloc_n<float>(ctx, nnz);
+        SFG_CUDA(cudaMemcpyAsync(t->row, drow, nnz * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+        SFG_CUDA(cudaMemcpyAsync(t->idx, dcol, nnz * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+        SFG_CUDA(cudaMemcpyAsync(t->val, dval, nnz * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+      } else {
+        t = sfg::sort_coo(ctx, rows, cols, nnz, drow, dcol, dval,
+                          (flags & SFG_FLAG_SUM_DUPLICATES) != 0);
+      }
+    } catch (...) {
+      for (auto* p : tmp) sfg::dfree(ctx, p);
+      throw;
+    }
+    for (auto* p : tmp) sfg::dfree(ctx, p);
+    *out = t;
+  });
+}
+
+int sfg_convert(sfg_context* ctx, const sfg_tensor* src, const sfg_format* dst, sfg_tensor** out) {
+  return guard([&] {
+    require(ctx && src && dst && out, SFG_ERR_INVALID_OPERATION, "null argument");
+    *out = nullptr;
+    validate_format(*dst);
+    if (src->kind != SFG_COO)
+      sfg::raise(SFG_ERR_UNSUPPORTED_SOURCE, "the device planner converts from COO sources");
+    if (src->m <= 0 || src->n <= 0)
+      sfg::raise(SFG_ERR_INVALID_OPERATION, "empty bounds at extent-only level");
+    switch (dst->kind) {
+      case SFG_COO: *out = sfg::coo_to_coo(ctx, src); break;
+      case SFG_CSR: *out = sfg::coo_to_csr(ctx, src); break;
+      case SFG_CSC: *out = sfg::coo_to_csc(ctx, src); break;
+      case SFG_DCSR: *out = sfg::coo_to_dcsr(ctx, src); break;
+      case SFG_ELL: *out = sfg::coo_to_ell(ctx, src); break;
+      case SFG_BCSR:
+        *out = sfg::coo_to_bcsr(ctx, src, dst->block_r, dst->block_c, dst->value_dtype);
+        break;
+      case SFG_HYB: *out = sfg::coo_to_hyb(ctx, src, dst->threshold); break;
+    }
+  });
+}
+
+int sfg_decompose_rows(sfg_context* ctx, const sfg_tensor* coo, int64_t min_sum,
+                       sfg_tensor** selected, sfg_tensor** remainder, int32_t* totals) {
+  return guard([&] {
+    require(ctx && coo && selected && remainder, SFG_ERR_INVALID_OPERATION, "null argument");
+    require(coo->kind == SFG_COO, SFG_ERR_INVALID_OPERATION,
+            "decompose expects coordinate-form input");
+    *selected = *remainder = nullptr;
+    sfg::decompose_rows(ctx, coo, min_sum, selected, remainder, totals);
+  });
+}
+
+int sfg_tensor_view_get(sfg_context* ctx, const sfg_tensor* t, sfg_tensor_view* out) {
+  return guard([&] {
+    require(t && out, SFG_ERR_INVALID_OPERATION, "null argument");
+    (void)ctx;
+    sfg_tensor_view v;
+    std::memset(&v, 0, sizeof v);
+    v.kind = t->kind;
+    v.value_dtype = t->dtype;
+    v.rows = t->m;
+    v.cols = t->n;
+    v.values = t->val;
+    const int S = SFG_LEVEL_SIZE, P = SFG_LEVEL_PTR, I = SFG_LEVEL_IDX, D = SFG_LEVEL_DENSE_VECTOR;
+    switch (t->kind) {
+      case SFG_COO:
+        v.nlevels = 2;
+        v.level[0] = level(I, 0, t->m - 1, t->nnz, t->nnz, t->row, 0, nullptr);
+        v.level[1] = level(I, 0, t->n - 1, t->nnz, t->nnz, t->idx, 0, nullptr);
+        v.nvals = t->nnz;
+        break;
+      case SFG_CSR:
+        v.nlevels = 2;
+        v.level[0] = level(S, 0, t->m - 1, t->m, 0, nullptr, 0, nullptr);
+        v.level[1] = level(P | I, 0, t->n - 1, t->nnz, t->nnz, t->idx, t->m + 1, t->ptr);
+        v.nvals = t->nnz;
+        break;
+      case SFG_CSC:
+        v.nlevels = 2;
+        v.level[0] = level(S, 0, t->n - 1, t->n, 0, nullptr, 0, nullptr);
+        v.level[1] = level(P | I, 0, t->m - 1, t->nnz, t->nnz, t->idx, t->n + 1, t->ptr);
+        v.nvals = t->nnz;
+        break;
+      case SFG_DCSR:
+        v.nlevels = 2;
+        v.level[0] = level(I, 0, t->m - 1, t->nnr, t->nnr, t->row, 0, nullptr);
+        v.level[1] = level(P | I, 0, t->n - 1, t->nnz, t->nnz, t->idx, t->nnr + 1, t->ptr);
+        v.nvals = t->nnz;
+        break;
+      case SFG_ELL:
+        v.nlevels = 3;
+        v.level[0] = level(I, 0, t->k - 1, t->k, t->k, t->slots, 0, nullptr);
+        v.level[1] = level(S, 0, t->m - 1, t->k * t->m, 0, nullptr, 0, nullptr);
+        v.level[2] = level(I, 0, t->n - 1, t->k * t->m, t->k * t->m, t->idx, 0, nullptr);
+        v.nvals = t->k * t->m;
+        break;
+      case SFG_BCSR:
+        v.nlevels = 4;
+        v.level[0] = level(S, 0, t->nbr - 1, t->nbr, 0, nullptr, 0, nullptr);
+        v.level[1] = level(P | I, 0, t->nbc - 1, t->nnz, t->nnz, t->idx, t->nbr + 1, t->ptr);
+        v.level[2] = level(S | D, 0, t->rb - 1, t->nnz * t->rb, 0, nullptr, 0, nullptr);
+        v.level[3] = level(S | D, 0, t->cb - 1, t->nnz * t->rb * t->cb, 0, nullptr, 0, nullptr);
+        v.nvals = t->nnz * t->rb * t->cb;
+        break;
+      case SFG_HYB:
+        v.nlevels = 0;
+        v.parts[0] = t->part[0];
+        v.parts[1] = t->part[1];
+        break;
+    }
+    *out = v;
+  });
+}
+
+int sfg_tensor_free(sfg_tensor* t) {
+  return guard([&] {
+    if (!t) return;
+    for (auto* p : t->part)
+      if (p) {
+        sfg::free_tensor_arrays(p);
+        delete p;
+      }
+    sfg::free_tensor_arrays(t);
+    delete t;
+  });
+}
+
+int sfg_spmv(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, uint32_t flags) {
+  return guard([&] {
+    require(ctx && a && x && y, SFG_ERR_INVALID_OPERATION, "null argument");
+    if (flags & SFG_COMPUTE_HOST) {
+      float* dx = sfg::dalloc_n<float>(ctx, a->n);
+      float* dy = sfg::dalloc_n<float>(ctx, a->m);
+      try {
+        SFG_CUDA(cudaMemcpyAsync(dx, x, a->n * 4, cudaMemcpyHostToDevice, ctx->stream));
+        if (flags & SFG_COMPUTE_ACCUMULATE)
+          SFG_CUDA(cudaMemcpyAsync(dy, y, a->m * 4, cudaMemcpyHostToDevice, ctx->stream));
+        sfg::spmv(ctx, a, dx, dy, (flags & SFG_COMPUTE_ACCUMULATE) != 0);
+        SFG_CUDA(cudaMemcpyAsync(y, dy, a->m * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        SFG_CUDA(cudaStreamSynchronize(ctx->stream));
+      } catch (...) {
+        sfg::dfree(ctx, dx);
+        sfg::dfree(ctx, dy);
+        throw;
+      }
+      sfg::dfree(ctx, dx);
+      sfg::dfree(ctx, dy);
+    } else {
+      sfg::spmv(ctx, a, x, y, (flags & SFG_COMPUTE_ACCUMULATE) != 0);
+    }
+  });
+}
+
+int sfg_spmm(sfg_context* ctx, const sfg_tensor* a, const void* b, int32_t b_dtype, int64_t nd,
+             int64_t ldb, float* c, int64_t ldc, uint32_t flags) {
+  return guard([&] {
+    require(ctx && a && b && c, SFG_ERR_INVALID_OPERATION, "null argument");
+    require(nd > 0 && ldb >= nd && ldc >= nd, SFG_ERR_INVALID_OPERATION, "bad dense shape");
+    require(b_dtype == SFG_F32 || b_dtype == SFG_BF16, SFG_ERR_INVALID_OPERATION, "bad dtype");
+    bool acc = (flags & SFG_COMPUTE_ACCUMULATE) != 0;
+    if (flags & SFG_COMPUTE_HOST) {
+      size_t esz = b_dtype == SFG_F32 ? 4 : 2;
+      void* db = sfg::dalloc(ctx, a->n * ldb * esz);
+      float* dc = sfg::dalloc_n<float>(ctx, a->m * ldc);
+      try {
+        SFG_CUDA(cudaMemcpyAsync(db, b, a->n * ldb * esz, cudaMemcpyHostToDevice, ctx->stream));
+        if (acc)
+          SFG_CUDA(cudaMemcpyAsync(dc, c, a->m * ldc * 4, cudaMemcpyHostToDevice, ctx->stream));
+        sfg::spmm(ctx, a, db, b_dtype, nd, ldb, dc, ldc, acc);
+        SFG_CUDA(cudaMemcpyAsync(c, dc, a->m * ldc * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        SFG_CUDA(cudaStreamSynchronize(ctx->stream));
+      } catch (...) {
+        sfg::dfree(ctx, db);
+        sfg::dfree(ctx, dc);
+        throw;
+      }
+      sfg::dfree(ctx, db);
+      sfg::dfree(ctx, dc);
+    } else {
+      sfg::spmm(ctx, a, b, b_dtype, nd, ldb, c, ldc, acc);
+    }
+  });
+}
+
+int sfg_row_partition(sfg_context* ctx, const sfg_tensor* coo, int32_t parts, int64_t* bounds) {
+  return guard([&] {
+    require(ctx && coo && bounds && parts > 0, SFG_ERR_INVALID_OPERATION, "bad argument");
+    require(coo->kind == SFG_COO, SFG_ERR_INVALID_OPERATION, "row partition expects COO");
+    sfg::row_partition(ctx, coo, parts, bounds);
+  });
+}
+
+int sfg_coo_slice_rows(sfg_context* ctx, const sfg_tensor* coo, int64_t r0, int64_t r1,
+                       sfg_tensor** out) {
+  return guard([&] {
+    require(ctx && coo && out, SFG_ERR_INVALID_OPERATION, "null argument");
+    require(coo->kind == SFG_COO, SFG_ERR_INVALID_OPERATION, "row slice expects COO");
+    require(0 <= r0 && r0 <= r1 && r1 <= coo->m, SFG_ERR_INVALID_OPERATION, "bad row range");
+    *out = sfg::coo_slice_rows(ctx, coo, r0, r1);
+  });
+}
+
+int sfgx_gen_uniform(sfg_context* ctx, uint64_t seed, int64_t rows, int64_t cols, int32_t per_row,
+                     sfg_tensor** out) {
+  return guard([&] {
+    require(per_row > 0 && per_row <= 64 && per_row <= cols, SFG_ERR_INVALID_OPERATION,
+            "per_row must be in [1, min(64, cols)]");
+    require(rows * per_row < INT32_MAX, SFG_ERR_INVALID_OPERATION, "too many entries");
+    *out = sfg::gen_uniform(ctx, seed, rows, cols, per_row);
+  });
+}
+
+int sfgx_gen_rmat(sfg_context* ctx, uint64_t seed, int32_t scale, int64_t edges, sfg_tensor** out) {
+  return guard([&] {
+    require(scale > 0 && scale <= 30 && edges > 0 && edges < INT32_MAX, SFG_ERR_INVALID_OPERATION,
+            "bad R-MAT size");
+    *out = sfg::gen_from_keys(ctx, seed, 0, scale, int64_t(1) << scale, int64_t(1) << scale, edges);
+  });
+}
+
+int sfgx_gen_hypersparse(sfg_context* ctx, uint64_t seed, int64_t rows, int64_t cols,
+                         int64_t draws, sfg_tensor** out) {
+  return guard([&] {
+    require(rows > 0 && cols > 0 && rows < INT32_MAX && cols < INT32_MAX && draws > 0 &&
+                draws < INT32_MAX,
+            SFG_ERR_INVALID_OPERATION, "bad hypersparse size");
+    *out = sfg::gen_from_keys(ctx, seed, 1, 0, rows, cols, draws);
+  });
+}
+
+int sfgx_gen_dense(sfg_context* ctx, uint64_t seed, int64_t count, float* out) {
+  return guard([&] { sfg::gen_dense(ctx, seed, count, out); });
+}
+
+int64_t sfgx_launch_count(void) { return sfg::g_launches.load(); }
+
+int sfgx_device_alloc(sfg_context* ctx, int64_t bytes, void** out) {
+  return guard([&] {
+    require(ctx && out && bytes >= 0, SFG_ERR_INVALID_OPERATION, "bad argument");
+    *out = sfg::dalloc(ctx, static_cast<size_t>(bytes));
+  });
+}
+
+int sfgx_device_free(sfg_context* ctx, void* p) {
+  return guard([&] { sfg::dfree(ctx, p); });
+}
+
+int sfgx_copy(sfg_context* ctx, void* dst, const void* src, int64_t bytes, int32_t kind) {
+  return guard([&] {
+    require(ctx && bytes >= 0 && kind >= 0 && kind <= 2, SFG_ERR_INVALID_OPERATION, "bad argument");
+    if (bytes == 0) return;
+    cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice
+                                 : (kind == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice);
+    SFG_CUDA(cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), k, ctx->stream));
+    if (kind == 1) SFG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,337 @@
+// convert_csr.cu — canonical-COO checks and the row-compressed conversions
+// COO -> COO / CSR / DCSR, plus row partitioning and row slicing.
+//
+// Reference semantics (paths relative to proj/include/sparseforge/):
+//   CSR  = plan Fill(0) Merge(0)   (planner.hpp:242-249; operators.hpp:346-391)
+//          materialize: L0 size, L1 ptr[m+1] + idx[nnz] (storage.hpp:156-200);
+//          empty rows are dangling prefixes -> empty ptr runs.
+//   DCSR = plan Merge(0); L0 is fused (one node per distinct row,
+//          storage.hpp:142-149), L1 ptr[nnr+1] + idx[nnz].
+// The canonical COO handed in is (row, col)-sorted and unique
+// (from_coo, tensor.hpp:156-200), so both are pure streaming passes.
+#include <vector>
+
+#include "devutil.cuh"
+#include "internal.cuh"
+
+namespace sfg {
+
+namespace {
+
+constexpr int kBlock = 256;
+
+// ---------------------------------------------------------------- checks
+enum { kBadRange = 1, kDuplicate = 2, kUnsorted = 4 };
+
+__global__ void __launch_bounds__(kBlock) k_check_canonical(const int32_t* __restrict__ row,
+                                                             const int32_t* __restrict__ col,
+                                                             int64_t nnz, int32_t m, int32_t n,
+                                                             int* __restrict__ flags) {
+  int f = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int r = row[e], c = col[e];
+    if (r < 0 || r >= m || c < 0 || c >= n) f |= kBadRange;
+    if (e > 0) {
+      int pr = row[e - 1], pc = col[e - 1];
+      if (pr == r && pc == c) f |= kDuplicate;
+      else if (pr > r || (pr == r && pc > c)) f |= kUnsorted;
+    }
+  }
+  f = __reduce_or_sync(kFull, f);
+  if ((threadIdx.x & 31) == 0 && f) atomicOr(flags, f);
+}
+
+// ----------------------------------------------------------- COO -> CSR
+// One thread owns 4 consecutive entries (128-bit loads/stores of row, col,
+// val). Row boundaries inside its run write ptr[q] = e for every row q in
+// (row[e-1], row[e]]; the owner of the last entry closes ptr up to m.
+// Empty-row gaps longer than a warp are filled cooperatively by the warp.
+__global__ void __launch_bounds__(kBlock) k_coo_to_csr(const int32_t* __restrict__ row,
+                                                        const int32_t* __restrict__ col,
+                                                        const float* __restrict__ val, int64_t nnz,
+                                                        int32_t m, int32_t* __restrict__ ptr,
+                                                        int32_t* __restrict__ ocol,
+                                                        float* __restrict__ oval) {
+  const int64_t nvec = (nnz + 3) >> 2;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // uniform trip count across the warp (fill_gaps uses warp collectives)
+  const int64_t base0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+  for (int64_t wbase = base0; wbase < nvec; wbase += stride) {
+    int64_t v = wbase + (threadIdx.x & 31);
+    Gap g[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) g[i] = {1, 0, 0};
+    if (v < nvec) {
+      int64_t e0 = v << 2;
+      int r[4];
+      if (e0 + 4 <= nnz) {
+        int4 rr = ld_stream(reinterpret_cast<const int4*>(row + e0));
+        int4 cc = ld_stream(reinterpret_cast<const int4*>(col + e0));
+        float4 vv = ld_stream(reinterpret_cast<const float4*>(val + e0));
+        st_stream(reinterpret_cast<int4*>(ocol + e0), cc);
+        st_stream(reinterpret_cast<float4*>(oval + e0), vv);
+        r[0] = rr.x; r[1] = rr.y; r[2] = rr.z; r[3] = rr.w;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (e0 + i < nnz) {
+            r[i] = row[e0 + i];
+            ocol[e0 + i] = col[e0 + i];
+            oval[e0 + i] = val[e0 + i];
+          } else {
+            r[i] = -1;
+          }
+        }
+      }
+      int prev = e0 == 0 ? -1 : row[e0 - 1];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (e0 + i < nnz) {
+          g[i] = {prev + 1, r[i], (int32_t)(e0 + i)};
+          prev = r[i];
+        }
+      }
+      if (e0 + 4 >= nnz) g[4] = {prev + 1, m, (int32_t)nnz};
+    }
+    fill_gaps(g, ptr);
+  }
+}
+
+// nnz == 0: every row is empty.
+__global__ void k_fill_i32(int32_t* __restrict__ p, int64_t n, int32_t v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+// ---------------------------------------------------------- COO -> DCSR
+// Row heads (e == 0 or row[e] != row[e-1]) are compacted with a single-pass
+// decoupled look-back scan: tile t learns how many heads precede it and
+// writes L0.idx[pos] = row, L1.ptr[pos] = e directly. col/val are copied in
+// the same pass.
+constexpr int kDcsrItems = 16;  // 4 x int4 per thread
+constexpr int kDcsrTile = kBlock * kDcsrItems;
+
+__global__ void __launch_bounds__(kBlock) k_coo_to_dcsr(
+    const int32_t* __restrict__ row, const int32_t* __restrict__ col,
+    const float* __restrict__ val, int64_t nnz, int32_t* __restrict__ orow,
+    int32_t* __restrict__ optr, int32_t* __restrict__ ocol, float* __restrict__ oval,
+    unsigned long long* __restrict__ status, uint32_t epoch, int32_t* __restrict__ nnr_out) {
+  __shared__ uint32_t smem[34];
+  __shared__ uint32_t slot;
+  const int tile = blockIdx.x;
+  const int64_t e_base = (int64_t)tile * kDcsrTile + (int64_t)threadIdx.x * kDcsrItems;
+  int r[kDcsrItems];
+  bool full = e_base + kDcsrItems <= nnz;
+  if (full) {
+#pragma unroll
+    for (int q = 0; q < kDcsrItems / 4; ++q) {
+      int4 rr = ld_stream(reinterpret_cast<const int4*>(row + e_base) + q);
+      int4 cc = ld_stream(reinterpret_cast<const int4*>(col + e_base) + q);
+      float4 vv = ld_stream(reinterpret_cast<const float4*>(val + e_base) + q);
+      st_stream(reinterpret_cast<int4*>(ocol + e_base) + q, cc);
+      st_stream(reinterpret_cast<float4*>(oval + e_base) + q, vv);
+      r[4 * q] = rr.x; r[4 * q + 1] = rr.y; r[4 * q + 2] = rr.z; r[4 * q + 3] = rr.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kDcsrItems; ++i) {
+      int64_t e = e_base + i;
+      if (e < nnz) {
+        r[i] = row[e];
+        ocol[e] = col[e];
+        oval[e] = val[e];
+      } else {
+        r[i] = -2;
+      }
+    }
+  }
+  int prev = (e_base == 0 || e_base >= nnz) ? -1 : row[e_base - 1];
+  uint32_t heads = 0;
+  uint32_t hmask = 0;
+#pragma unroll
+  for (int i = 0; i < kDcsrItems; ++i) {
+    bool valid = e_base + i < nnz;
+    bool h = valid && r[i] != prev;
+    hmask |= (h ? 1u : 0u) << i;
+    heads += h;
+    if (valid) prev = r[i];
+  }
+  uint32_t total;
+  uint32_t excl = block_exclusive_scan<uint32_t, kBlock>(heads, smem, &total);
+  uint32_t tile_prefix = lookback_prefix(status, epoch, tile, total, &slot);
+  uint32_t pos = tile_prefix + excl;
+#pragma unroll
+  for (int i = 0; i < kDcsrItems; ++i) {
+    if (hmask >> i & 1u) {
+      orow[pos] = r[i];
+      optr[pos] = (int32_t)(e_base + i);
+      ++pos;
+    }
+  }
+  if (tile == gridDim.x - 1 && threadIdx.x == 0) {
+    uint32_t nnr = tile_prefix + total;
+    optr[nnr] = (int32_t)nnz;
+    *nnr_out = (int32_t)nnr;
+  }
+}
+
+// ------------------------------------------------------- row partitioning
+__global__ void k_lower_bound_rows(const int32_t* __restrict__ row, int64_t nnz,
+                                   const int64_t* __restrict__ keys, int nkeys,
+                                   int64_t* __restrict__ out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nkeys) return;
+  int64_t lo = 0, hi = nnz, key = keys[i];
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (row[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  out[i] = lo;
+}
+
+__global__ void k_gather_rows(const int32_t* __restrict__ row, const int64_t* __restrict__ pos,
+                              int nkeys, int64_t nnz, int32_t m, int64_t* __restrict__ out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nkeys) return;
+  out[i] = pos[i] < nnz ? row[pos[i]] : m;
+}
+
+__global__ void k_slice_rows(const int32_t* __restrict__ row, const int32_t* __restrict__ col,
+                             const float* __restrict__ val, int64_t e0, int64_t count, int32_t r0,
+                             int32_t* __restrict__ orow, int32_t* __restrict__ ocol,
+                             float* __restrict__ oval) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    orow[i] = row[e0 + i] - r0;
+    ocol[i] = col[e0 + i];
+    oval[i] = val[e0 + i];
+  }
+}
+
+}  // namespace
+
+void check_coo_canonical(sfg_context* ctx, const int32_t* row, const int32_t* col, int64_t m,
+                         int64_t n, int64_t nnz) {
+  if (nnz == 0) return;
+  int* flags = static_cast<int*>(scratch(ctx, 64));
+  SFG_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), ctx->stream));
+  SFG_LAUNCH(k_check_canonical, stream_grid(ctx, nnz, kBlock, 4), kBlock, 0, ctx->stream, row, col,
+             nnz, (int32_t)m, (int32_t)n, flags);
+  int f = 0;
+  read_back(ctx, flags, sizeof f, &f);
+  if (f & kBadRange) raise(SFG_ERR_INVALID_OPERATION, "coordinate out of range");
+  if (f & kUnsorted)
+    raise(SFG_ERR_INVALID_OPERATION, "input flagged SORTED is not (row, col)-sorted");
+  if (f & kDuplicate) raise(SFG_ERR_DUPLICATE_COORDINATE, "duplicate coordinate");
+}
+
+sfg_tensor* coo_to_coo(sfg_context* ctx, const sfg_tensor* s) {
+  sfg_tensor* t = new_tensor(ctx, SFG_COO, s->m, s->n);
+  t->nnz = s->nnz;
+  t->row = dalloc_n<int32_t>(ctx, s->nnz);
+  t->idx = dalloc_n<int32_t>(ctx, s->nnz);
+  t->val = dalloc_n<float>(ctx, s->nnz);
+  SFG_CUDA(cudaMemcpyAsync(t->row, s->row, s->nnz * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+  SFG_CUDA(cudaMemcpyAsync(t->idx, s->idx, s->nnz * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+  SFG_CUDA(cudaMemcpyAsync(t->val, s->val, s->nnz * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+  return t;
+}
+
+sfg_tensor* coo_to_csr(sfg_context* ctx, const sfg_tensor* s) {
+  sfg_tensor* t = new_tensor(ctx, SFG_CSR, s->m, s->n);
+  t->nnz = s->nnz;
+  t->ptr = dalloc_n<int32_t>(ctx, s->m + 1);
+  t->idx = dalloc_n<int32_t>(ctx, s->nnz);
+  t->val = dalloc_n<float>(ctx, s->nnz);
+  if (s->nnz == 0) {
+    SFG_LAUNCH(k_fill_i32, stream_grid(ctx, s->m + 1, kBlock, 4), kBlock, 0, ctx->stream, t->ptr,
+               s->m + 1, 0);
+    return t;
+  }
+  int64_t nvec = ceil_div(s->nnz, 4);
+  SFG_LAUNCH(k_coo_to_csr, stream_grid(ctx, nvec, kBlock, 1, 8), kBlock, 0, ctx->stream, s->row,
+             s->idx, static_cast<const float*>(s->val), s->nnz, (int32_t)s->m, t->ptr, t->idx,
+             static_cast<float*>(t->val));
+  return t;
+}
+
+sfg_tensor* coo_to_dcsr(sfg_context* ctx, const sfg_tensor* s) {
+  sfg_tensor* t = new_tensor(ctx, SFG_DCSR, s->m, s->n);
+  t->nnz = s->nnz;
+  int64_t cap = s->nnz < s->m ? s->nnz : s->m;  // nnr <= min(nnz, m)
+  t->row = dalloc_n<int32_t>(ctx, cap);
+  t->ptr = dalloc_n<int32_t>(ctx, cap + 1);
+  t->idx = dalloc_n<int32_t>(ctx, s->nnz);
+  t->val = dalloc_n<float>(ctx, s->nnz);
+  if (s->nnz == 0) {
+    SFG_LAUNCH(k_fill_i32, 1, 32, 0, ctx->stream, t->ptr, 1, 0);
+    t->nnr = 0;
+    return t;
+  }
+  int tiles = (int)ceil_div(s->nnz, kDcsrTile);
+  auto* status = static_cast<unsigned long long*>(scratch(ctx, (size_t)tiles * 8 + 64));
+  int32_t* nnr_dev = reinterpret_cast<int32_t*>(status + tiles);
+  SFG_LAUNCH(k_coo_to_dcsr, tiles, kBlock, 0, ctx->stream, s->row, s->idx,
+             static_cast<const float*>(s->val), s->nnz, t->row, t->ptr, t->idx,
+             static_cast<float*>(t->val), status, ctx->epoch++, nnr_dev);
+  int32_t nnr = 0;
+  read_back(ctx, nnr_dev, sizeof nnr, &nnr);
+  t->nnr = nnr;
+  return t;
+}
+
+void row_partition(sfg_context* ctx, const sfg_tensor* coo, int parts, int64_t* bounds) {
+  // Partition p starts at the row holding entry floor(p * nnz / P): nnz
+  // balanced to within one row.
+  std::vector<int64_t> keys(parts + 1);
+  bounds[0] = 0;
+  bounds[parts] = coo->m;
+  if (parts == 1) return;
+  if (coo->nnz == 0) {
+    for (int p = 1; p < parts; ++p) bounds[p] = coo->m * p / parts;
+    return;
+  }
+  int64_t* dpos = dalloc_n<int64_t>(ctx, parts);
+  std::vector<int64_t> pos(parts - 1);
+  for (int p = 1; p < parts; ++p) pos[p - 1] = coo->nnz * p / parts;
+  SFG_CUDA(cudaMemcpyAsync(dpos, pos.data(), (parts - 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
+  int64_t* drows = dalloc_n<int64_t>(ctx, parts);
+  SFG_LAUNCH(k_gather_rows, 1, 256, 0, ctx->stream, coo->row, dpos, parts - 1, coo->nnz,
+             (int32_t)coo->m, drows);
+  std::vector<int64_t> rows(parts - 1);
+  SFG_CUDA(cudaMemcpyAsync(rows.data(), drows, (parts - 1) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  SFG_CUDA(cudaStreamSynchronize(ctx->stream));
+  dfree(ctx, dpos);
+  dfree(ctx, drows);
+  for (int p = 1; p < parts; ++p) {
+    int64_t b = rows[p - 1];
+    if (b < bounds[p - 1]) b = bounds[p - 1];
+    bounds[p] = b;
+  }
+}
+
+sfg_tensor* coo_slice_rows(sfg_context* ctx, const sfg_tensor* coo, int64_t r0, int64_t r1) {
+  int64_t keys[2] = {r0, r1};
+  int64_t* dk = dalloc_n<int64_t>(ctx, 4);
+  SFG_CUDA(cudaMemcpyAsync(dk, keys, 16, cudaMemcpyHostToDevice, ctx->stream));
+  SFG_LAUNCH(k_lower_bound_rows, 1, 32, 0, ctx->stream, coo->row, coo->nnz, dk, 2, dk + 2);
+  int64_t pos[2];
+  read_back(ctx, dk + 2, 16, pos);
+  dfree(ctx, dk);
+  sfg_tensor* t = new_tensor(ctx, SFG_COO, r1 - r0, coo->n);
+  int64_t count = pos[1] - pos[0];
+  t->nnz = count;
+  t->row = dalloc_n<int32_t>(ctx, count);
+  t->idx = dalloc_n<int32_t>(ctx, count);
+  t->val = dalloc_n<float>(ctx, count);
+  if (count)
+    SFG_LAUNCH(k_slice_rows, stream_grid(ctx, count, kBlock, 4), kBlock, 0, ctx->stream, coo->row,
+               coo->idx, static_cast<const float*>(coo->val), pos[0], count, (int32_t)r0, t->row,
+               t->idx, static_cast<float*>(t->val));
+  return t;
+}
+
+}  // namespace sfg

@@ -1,0 +1,141 @@
+// internal.cuh — shared host/device plumbing for the sm_100a sparse path.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <string>
+
+#include "../../include/sparseforge_b200.h"
+
+namespace sfg {
+
+// ------------------------------------------------------------------ errors
+struct Failure {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void raise(int code, const std::string& msg);
+[[noreturn]] void raise_cuda(cudaError_t e, const char* what, const char* file, int line);
+void set_last_error(const std::string& msg);
+
+#define SFG_CUDA(call)                                                      \
+  do {                                                                      \
+    cudaError_t e__ = (call);                                               \
+    if (e__ != cudaSuccess) ::sfg::raise_cuda(e__, #call, __FILE__, __LINE__); \
+  } while (0)
+
+extern std::atomic<int64_t> g_launches;
+
+// Every kernel launch goes through here: counted (bench gpu_launches) and
+// checked for launch-configuration errors.
+#define SFG_LAUNCH(kernel, grid, block, smem, stream, ...)                   \
+  do {                                                                      \
+    kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);             \
+    ::sfg::g_launches.fetch_add(1, std::memory_order_relaxed);              \
+    SFG_CUDA(cudaPeekAtLastError());                                        \
+  } while (0)
+
+}  // namespace sfg
+
+// ---------------------------------------------------------------- context
+struct sfg_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sms = 148;
+  int64_t* pinned = nullptr;   // small host scratch for size read-backs
+  void* scratch = nullptr;     // device scratch (look-back status words, counters)
+  size_t scratch_bytes = 0;
+  uint32_t epoch = 1;          // look-back status generation
+};
+
+// ------------------------------------------------------------------ tensor
+// Device-resident materialized tensor. Array roles per format (the level
+// arrays of MaterializedTensor, storage.hpp:77-91):
+//   COO : row[nnz] (L0 idx), idx[nnz] (L1 idx)
+//   CSR : ptr[m+1], idx[nnz]              CSC: ptr[n+1], idx[nnz] (rows)
+//   DCSR: row[nnr] (L0 idx), ptr[nnr+1], idx[nnz]
+//   ELL : slots[K] (L0 idx), idx[K*m] (L2 idx, slot-major), val[K*m]
+//   BCSR: ptr[nbr+1], idx[nblocks] (bcol), val[nblocks*rb*cb] block-major
+//   HYB : part[0] = ELL of the remainder, part[1] = COO of the selection
+struct sfg_tensor {
+  sfg_context* ctx = nullptr;
+  int32_t kind = SFG_COO;
+  int32_t dtype = SFG_F32;
+  int64_t m = 0, n = 0;
+  int64_t nnz = 0;       // stored coordinates (COO/CSR/CSC/DCSR), cells (ELL), blocks (BCSR)
+  int64_t nnr = 0;       // DCSR nonempty rows
+  int64_t k = 0;         // ELL slots
+  int64_t br = 0, bc = 0;        // BCSR block shape (r, c)
+  int64_t rb = 0, cb = 0;        // BCSR level-2/3 extents (== r, c except one-tile edge)
+  int64_t nbr = 0, nbc = 0;      // BCSR block grid
+  int64_t threshold = 0;         // HYB min_sum
+  int32_t* row = nullptr;
+  int32_t* ptr = nullptr;
+  int32_t* idx = nullptr;
+  int32_t* slots = nullptr;
+  void* val = nullptr;
+  sfg_tensor* part[2] = {nullptr, nullptr};
+};
+
+namespace sfg {
+
+// Stream-ordered device allocation from the context's pool.
+void* dalloc(sfg_context* ctx, size_t bytes);
+void dfree(sfg_context* ctx, void* p);
+template <class T>
+T* dalloc_n(sfg_context* ctx, int64_t n) {
+  return static_cast<T*>(dalloc(ctx, static_cast<size_t>(n > 0 ? n : 1) * sizeof(T)));
+}
+
+// Scratch with at least `bytes` bytes (grows; contents undefined).
+void* scratch(sfg_context* ctx, size_t bytes);
+// Copy `count` int64 values device->host through pinned memory and sync.
+void read_back(sfg_context* ctx, const void* dev, size_t bytes, void* host);
+
+sfg_tensor* new_tensor(sfg_context* ctx, int kind, int64_t m, int64_t n);
+void free_tensor_arrays(sfg_tensor* t);
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Grid for a grid-stride streaming kernel: a few waves of resident CTAs.
+inline int stream_grid(const sfg_context* ctx, int64_t work_items, int block, int per_thread,
+                       int ctas_per_sm = 8) {
+  int64_t want = ceil_div(work_items, static_cast<int64_t>(block) * per_thread);
+  int64_t cap = static_cast<int64_t>(ctx->sms) * ctas_per_sm;
+  if (want < 1) want = 1;
+  return static_cast<int>(want < cap ? want : cap);
+}
+
+// ----------------------------------------------------- kernel entry points
+// (defined in the per-area .cu files, called from abi.cu)
+void check_coo_canonical(sfg_context* ctx, const int32_t* row, const int32_t* col, int64_t m,
+                         int64_t n, int64_t nnz);
+sfg_tensor* sort_coo(sfg_context* ctx, int64_t m, int64_t n, int64_t nnz, const int32_t* row,
+                     const int32_t* col, const float* val, bool sum_duplicates);
+void sort_u64_keys(sfg_context* ctx, uint64_t* keys, int64_t n, int key_bits, uint64_t** sorted_out);
+
+sfg_tensor* coo_to_coo(sfg_context* ctx, const sfg_tensor* s);
+sfg_tensor* coo_to_csr(sfg_context* ctx, const sfg_tensor* s);
+sfg_tensor* coo_to_csc(sfg_context* ctx, const sfg_tensor* s);
+sfg_tensor* coo_to_dcsr(sfg_context* ctx, const sfg_tensor* s);
+sfg_tensor* coo_to_ell(sfg_context* ctx, const sfg_tensor* s);
+sfg_tensor* coo_to_bcsr(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_t c, int dtype);
+sfg_tensor* coo_to_hyb(sfg_context* ctx, const sfg_tensor* s, int64_t min_sum);
+void decompose_rows(sfg_context* ctx, const sfg_tensor* s, int64_t min_sum, sfg_tensor** sel,
+                    sfg_tensor** rem, int32_t* totals);
+void row_partition(sfg_context* ctx, const sfg_tensor* coo, int parts, int64_t* bounds);
+sfg_tensor* coo_slice_rows(sfg_context* ctx, const sfg_tensor* coo, int64_t r0, int64_t r1);
+
+void spmv(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, bool accumulate);
+void spmm(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dtype, int64_t nd,
+          int64_t ldb, float* c, int64_t ldc, bool accumulate);
+
+sfg_tensor* gen_uniform(sfg_context* ctx, uint64_t seed, int64_t m, int64_t n, int per_row);
+sfg_tensor* gen_from_keys(sfg_context* ctx, uint64_t seed, int kind, int scale, int64_t m,
+                          int64_t n, int64_t draws);
+void gen_dense(sfg_context* ctx, uint64_t seed, int64_t count, float* out);
+
+}  // namespace sfg

@@ -1,0 +1,378 @@
+// sort.cu — from_coo on the device: range check, stable LSD radix sort of
+// packed (row, col) keys, duplicate rejection or f64 summation.
+//
+// Reference: from_coo (tensor.hpp:156-200) = range check (171-174), stable
+// lexicographic sort_entries (136-152, std::stable_sort), duplicates ->
+// DuplicateCoordinate (185-191) or summed in sorted order (192).
+//
+// Radix sort: one-sweep LSD with 8-bit digits. An upfront pass histograms
+// every digit position; each sort pass then streams tiles of 4096 keys:
+// per-warp match_any ranking (stable: rounds of 32 consecutive keys in
+// input order), per-digit decoupled look-back across tiles for the tile's
+// digit offsets, scatter. Digit positions where every key has the same
+// digit are skipped.
+#include <cuda_bf16.h>
+
+#include <vector>
+
+#include "devutil.cuh"
+#include "internal.cuh"
+
+namespace sfg {
+
+namespace {
+
+constexpr int kBlock = 256;
+constexpr int kWarps = kBlock / 32;
+constexpr int kRounds = 16;                       // keys per lane
+constexpr int kTile = kBlock * kRounds;           // 4096 keys per tile
+constexpr int kMaxPasses = 8;
+
+__global__ void __launch_bounds__(kBlock) k_global_hist(const uint64_t* __restrict__ keys, int64_t n,
+                                                         int passes, uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[kMaxPasses][256];
+  for (int i = threadIdx.x; i < kMaxPasses * 256; i += blockDim.x) (&h[0][0])[i] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k = keys[i];
+    for (int p = 0; p < passes; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 0xff], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) {
+    uint32_t v = (&h[0][0])[i];
+    if (v) atomicAdd(hist + i, v);
+  }
+}
+
+template <bool kPayload>
+__global__ void __launch_bounds__(kBlock) k_onesweep(const uint64_t* __restrict__ kin,
+                                                      const uint32_t* __restrict__ pin,
+                                                      uint64_t* __restrict__ kout,
+                                                      uint32_t* __restrict__ pout, int64_t n,
+                                                      int shift, const uint32_t* __restrict__ goff,
+                                                      unsigned long long* __restrict__ status,
+                                                      uint32_t epoch) {
+  __shared__ uint32_t wcnt[kWarps][256];
+  __shared__ uint32_t base_d[256];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tile = blockIdx.x;
+  for (int i = threadIdx.x; i < kWarps * 256; i += blockDim.x) (&wcnt[0][0])[i] = 0;
+  __syncthreads();
+
+  const int64_t wbase = (int64_t)tile * kTile + (int64_t)warp * (32 * kRounds);
+  uint64_t key[kRounds];
+  uint32_t pay[kRounds];
+  uint32_t rank[kRounds];
+#pragma unroll
+  for (int j = 0; j < kRounds; ++j) {
+    int64_t i = wbase + j * 32 + lane;
+    key[j] = i < n ? kin[i] : 0;
+    if (kPayload) pay[j] = i < n ? pin[i] : 0;
+  }
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int j = 0; j < kRounds; ++j) {
+    int64_t i = wbase + j * 32 + lane;
+    uint32_t d = i < n ? (uint32_t)((key[j] >> shift) & 0xff) : 256u;
+    unsigned peers = __match_any_sync(kFull, d);
+    int leader = __ffs(peers) - 1;
+    uint32_t b = 0;
+    if (lane == leader && d < 256) {
+      b = wcnt[warp][d];
+      wcnt[warp][d] = b + __popc(peers);
+    }
+    b = __shfl_sync(kFull, b, leader);
+    rank[j] = b + __popc(peers & lt);
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit: exclusive prefix over warps, tile total, look-back
+  {
+    const int d = threadIdx.x;
+    uint32_t s = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      uint32_t c = wcnt[w][d];
+      wcnt[w][d] = s;
+      s += c;
+    }
+    unsigned long long* st = status + (size_t)tile * 256 + d;
+    uint32_t ep = epoch & 0x3fffffffu;
+    uint32_t excl = 0;
+    if (tile == 0) {
+      st_relaxed(st, lb_pack(epoch, 2, s));
+    } else {
+      st_relaxed(st, lb_pack(epoch, 1, s));
+      for (int t = tile - 1; t >= 0; --t) {
+        unsigned long long w;
+        uint32_t state;
+        do {
+          w = ld_relaxed(status + (size_t)t * 256 + d);
+          uint32_t hi = (uint32_t)(w >> 32);
+          state = (hi >> 2) == ep ? (hi & 3u) : 0u;
+        } while (state == 0);
+        excl += (uint32_t)w;
+        if (state == 2) break;
+      }
+      st_relaxed(st, lb_pack(epoch, 2, excl + s));
+    }
+    base_d[d] = goff[d] + excl;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kRounds; ++j) {
+    int64_t i = wbase + j * 32 + lane;
+    if (i < n) {
+      uint32_t d = (uint32_t)((key[j] >> shift) & 0xff);
+      uint32_t o = base_d[d] + wcnt[warp][d] + rank[j];
+      kout[o] = key[j];
+      if (kPayload) pout[o] = pay[j];
+    }
+  }
+}
+
+__global__ void k_digit_offsets(uint32_t* __restrict__ hist, int passes) {
+  // one warp per pass: exclusive scan of 256 counts, in place
+  int p = blockIdx.x;
+  if (p >= passes) return;
+  uint32_t* h = hist + p * 256;
+  int lane = threadIdx.x;
+  uint32_t run = 0;
+  for (int c = 0; c < 256; c += 32) {
+    uint32_t v = h[c + lane];
+    uint32_t inc = warp_inclusive_scan(v);
+    h[c + lane] = run + inc - v;
+    run += __shfl_sync(kFull, inc, 31);
+  }
+}
+
+// Head flags of sorted keys -> compaction positions (exclusive scan).
+constexpr int kUItems = 16;
+constexpr int kUTile = kBlock * kUItems;
+
+__global__ void __launch_bounds__(kBlock) k_unique_pos(const uint64_t* __restrict__ keys, int64_t n,
+                                                        int32_t* __restrict__ pos,
+                                                        unsigned long long* __restrict__ status,
+                                                        uint32_t epoch, int32_t* __restrict__ total,
+                                                        unsigned long long* __restrict__ first_dup) {
+  __shared__ uint32_t smem[34];
+  __shared__ uint32_t slot;
+  const int64_t e0 = (int64_t)blockIdx.x * kUTile + (int64_t)threadIdx.x * kUItems;
+  uint32_t heads = 0, hm = 0;
+  uint64_t prev = e0 > 0 && e0 < n ? keys[e0 - 1] : ~0ull;
+  unsigned long long dup = ~0ull;
+#pragma unroll
+  for (int i = 0; i < kUItems; ++i) {
+    int64_t e = e0 + i;
+    if (e < n) {
+      uint64_t k = keys[e];
+      bool h = e == 0 || k != prev;
+      if (!h && k < dup) dup = k;
+      hm |= (h ? 1u : 0u) << i;
+      heads += h;
+      prev = k;
+    }
+  }
+  if (dup != ~0ull) atomicMin(first_dup, dup);
+  uint32_t tot;
+  uint32_t excl = block_exclusive_scan<uint32_t, kBlock>(heads, smem, &tot);
+  uint32_t tp = lookback_prefix(status, epoch, blockIdx.x, tot, &slot);
+  uint32_t p = tp + excl;
+#pragma unroll
+  for (int i = 0; i < kUItems; ++i) {
+    int64_t e = e0 + i;
+    if (e < n) {
+      p += (hm >> i) & 1u;
+      pos[e] = (int32_t)(p - 1);  // position of this key's unique slot
+    }
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *total = (int32_t)(tp + tot);
+}
+
+enum { kBadRange = 1 };
+
+__global__ void __launch_bounds__(kBlock) k_make_keys(const int32_t* __restrict__ row,
+                                                       const int32_t* __restrict__ col,
+                                                       const float* __restrict__ val, int64_t nnz,
+                                                       int32_t m, int32_t n, int cbits,
+                                                       uint64_t* __restrict__ keys,
+                                                       uint32_t* __restrict__ pay,
+                                                       int* __restrict__ flags) {
+  int f = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int r = row[e], c = col[e];
+    if (r < 0 || r >= m || c < 0 || c >= n) f = kBadRange;
+    keys[e] = ((uint64_t)(uint32_t)r << cbits) | (uint32_t)c;
+    pay[e] = __float_as_uint(val[e]);
+  }
+  if (__reduce_or_sync(kFull, f) && (threadIdx.x & 31) == 0) atomicOr(flags, f);
+}
+
+// Unique keys -> canonical COO. With sum_duplicates, the head of each run
+// adds the run's values in sorted (= stable input) order in f64, like
+// `out.values.back() += t.values[e]` over doubles (tensor.hpp:192), and
+// rounds once to fp32.
+__global__ void __launch_bounds__(kBlock) k_emit_coo(const uint64_t* __restrict__ keys,
+                                                      const uint32_t* __restrict__ pay,
+                                                      const int32_t* __restrict__ pos, int64_t n,
+                                                      int cbits, int32_t* __restrict__ row,
+                                                      int32_t* __restrict__ col,
+                                                      float* __restrict__ val) {
+  const uint64_t cmask = (1ull << cbits) - 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k = keys[i];
+    if (i > 0 && keys[i - 1] == k) continue;
+    double s = (double)__uint_as_float(pay[i]);
+    for (int64_t j = i + 1; j < n && keys[j] == k; ++j) s += (double)__uint_as_float(pay[j]);
+    int32_t o = pos[i];
+    row[o] = (int32_t)(k >> cbits);
+    col[o] = (int32_t)(k & cmask);
+    val[o] = (float)s;
+  }
+}
+
+int bits_for(int64_t extent) {
+  int b = 0;
+  while ((int64_t(1) << b) < extent) ++b;
+  return b;
+}
+
+}  // namespace
+
+// LSD radix sort of (key, payload) by the low `key_bits` bits. The result
+// lands in either the input or the alternate buffer; *kres / *pres say which.
+static void radix_sort(sfg_context* ctx, uint64_t* keys, uint32_t* pay, int64_t n, int key_bits,
+                       uint64_t** kres, uint32_t** pres, uint64_t** kalt_out, uint32_t** palt_out) {
+  int passes = (key_bits + 7) / 8;
+  if (passes > kMaxPasses) passes = kMaxPasses;
+  uint64_t* kalt = dalloc_n<uint64_t>(ctx, n);
+  uint32_t* palt = pay ? dalloc_n<uint32_t>(ctx, n) : nullptr;
+  *kalt_out = kalt;
+  *palt_out = palt;
+  uint64_t* kin = keys;
+  uint32_t* pin = pay;
+  uint64_t* kout = kalt;
+  uint32_t* pout = palt;
+  if (n > 1 && passes > 0) {
+    int tiles = (int)ceil_div(n, kTile);
+    size_t status_bytes = (size_t)tiles * 256 * 8;
+    char* scr = static_cast<char*>(scratch(ctx, status_bytes + kMaxPasses * 256 * 4 + 256));
+    auto* status = reinterpret_cast<unsigned long long*>(scr);
+    auto* hist = reinterpret_cast<uint32_t*>(scr + status_bytes);
+    SFG_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * 256 * 4, ctx->stream));
+    SFG_LAUNCH(k_global_hist, stream_grid(ctx, n, kBlock, 8, 4), kBlock, 0, ctx->stream, keys, n,
+               passes, hist);
+    std::vector<uint32_t> h(passes * 256);
+    SFG_CUDA(cudaMemcpyAsync(h.data(), hist, passes * 256 * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    SFG_LAUNCH(k_digit_offsets, passes, 32, 0, ctx->stream, hist, passes);
+    SFG_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int p = 0; p < passes; ++p) {
+      bool constant = false;
+      for (int d = 0; d < 256; ++d) constant |= (h[p * 256 + d] == (uint32_t)n);
+      if (constant) continue;
+      if (pay)
+        SFG_LAUNCH(k_onesweep<true>, tiles, kBlock, 0, ctx->stream, kin, pin, kout, pout, n, 8 * p,
+                   hist + p * 256, status, ctx->epoch++);
+      else
+        SFG_LAUNCH(k_onesweep<false>, tiles, kBlock, 0, ctx->stream, kin, nullptr, kout, nullptr, n,
+                   8 * p, hist + p * 256, status, ctx->epoch++);
+      std::swap(kin, kout);
+      std::swap(pin, pout);
+    }
+  }
+  *kres = kin;
+  *pres = pin;
+}
+
+void sort_u64_keys(sfg_context* ctx, uint64_t* keys, int64_t n, int key_bits, uint64_t** sorted_out) {
+  uint64_t *kres, *kalt;
+  uint32_t *pres, *palt;
+  radix_sort(ctx, keys, nullptr, n, key_bits, &kres, &pres, &kalt, &palt);
+  if (kres == keys) dfree(ctx, kalt);
+  *sorted_out = kres;
+}
+
+int64_t unique_positions(sfg_context* ctx, const uint64_t* keys, int64_t n, int32_t* pos) {
+  if (n == 0) return 0;
+  int tiles = (int)ceil_div(n, kUTile);
+  char* scr = static_cast<char*>(scratch(ctx, (size_t)tiles * 8 + 64));
+  auto* status = reinterpret_cast<unsigned long long*>(scr);
+  auto* tail = reinterpret_cast<unsigned long long*>(scr + (size_t)tiles * 8);
+  SFG_CUDA(cudaMemsetAsync(tail, 0xff, 16, ctx->stream));
+  SFG_LAUNCH(k_unique_pos, tiles, kBlock, 0, ctx->stream, keys, n, pos, status, ctx->epoch++,
+             reinterpret_cast<int32_t*>(tail + 1), tail);
+  int32_t total[4];
+  read_back(ctx, tail, 16, total);
+  return total[2];
+}
+
+sfg_tensor* sort_coo(sfg_context* ctx, int64_t m, int64_t n, int64_t nnz, const int32_t* row,
+                     const int32_t* col, const float* val, bool sum_duplicates) {
+  sfg_tensor* t = new_tensor(ctx, SFG_COO, m, n);
+  if (nnz == 0) {
+    t->row = dalloc_n<int32_t>(ctx, 0);
+    t->idx = dalloc_n<int32_t>(ctx, 0);
+    t->val = dalloc_n<float>(ctx, 0);
+    return t;
+  }
+  int cbits = bits_for(n), rbits = bits_for(m);
+  uint64_t* keys = dalloc_n<uint64_t>(ctx, nnz);
+  uint32_t* pay = dalloc_n<uint32_t>(ctx, nnz);
+  int* flags = static_cast<int*>(dalloc(ctx, 16));
+  SFG_CUDA(cudaMemsetAsync(flags, 0, 4, ctx->stream));
+  SFG_LAUNCH(k_make_keys, stream_grid(ctx, nnz, kBlock, 4), kBlock, 0, ctx->stream, row, col, val,
+             nnz, (int32_t)m, (int32_t)n, cbits, keys, pay, flags);
+  int f = 0;
+  read_back(ctx, flags, 4, &f);
+  dfree(ctx, flags);
+  if (f & kBadRange) {
+    dfree(ctx, keys);
+    dfree(ctx, pay);
+    delete t;
+    raise(SFG_ERR_INVALID_OPERATION, "coordinate out of range");
+  }
+  uint64_t *kres, *kalt;
+  uint32_t *pres, *palt;
+  radix_sort(ctx, keys, pay, nnz, cbits + rbits, &kres, &pres, &kalt, &palt);
+  int32_t* pos = dalloc_n<int32_t>(ctx, nnz);
+  // unique_positions also records the smallest duplicated key
+  int tiles = (int)ceil_div(nnz, kUTile);
+  char* scr = static_cast<char*>(scratch(ctx, (size_t)tiles * 8 + 64));
+  auto* status = reinterpret_cast<unsigned long long*>(scr);
+  auto* tail = reinterpret_cast<unsigned long long*>(scr + (size_t)tiles * 8);
+  SFG_CUDA(cudaMemsetAsync(tail, 0xff, 16, ctx->stream));
+  SFG_LAUNCH(k_unique_pos, tiles, kBlock, 0, ctx->stream, kres, nnz, pos, status, ctx->epoch++,
+             reinterpret_cast<int32_t*>(tail + 1), tail);
+  unsigned long long res[2];
+  read_back(ctx, tail, 16, res);
+  int64_t uniq = static_cast<int32_t>(res[1] & 0xffffffffu);
+  if (res[0] != ~0ull && !sum_duplicates) {
+    uint64_t k = res[0];
+    dfree(ctx, keys);
+    dfree(ctx, pay);
+    dfree(ctx, kalt);
+    dfree(ctx, palt);
+    dfree(ctx, pos);
+    delete t;
+    raise(SFG_ERR_DUPLICATE_COORDINATE,
+          "duplicate coordinate (" + std::to_string(k >> cbits) + "," +
+              std::to_string(k & ((1ull << cbits) - 1)) + ")");
+  }
+  t->nnz = uniq;
+  t->row = dalloc_n<int32_t>(ctx, uniq);
+  t->idx = dalloc_n<int32_t>(ctx, uniq);
+  t->val = dalloc_n<float>(ctx, uniq);
+  SFG_LAUNCH(k_emit_coo, stream_grid(ctx, nnz, kBlock, 4), kBlock, 0, ctx->stream, kres, pres, pos,
+             nnz, cbits, t->row, t->idx, static_cast<float*>(t->val));
+  dfree(ctx, pos);
+  dfree(ctx, keys);
+  dfree(ctx, pay);
+  dfree(ctx, kalt);
+  dfree(ctx, palt);
+  return t;
+}
+
+}  // namespace sfg

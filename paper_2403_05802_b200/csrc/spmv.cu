@@ -1,0 +1,327 @@
+// spmv.cu — y = A x over every materialized format.
+//
+// Reference: run_kernel(spmv_kernel(), {A, x}) (kernel.hpp:236-384, 32-40).
+// The reference walks every stored slot in storage order (walk_slots,
+// storage.hpp:238-280), padding included, restores logical coordinates
+// through the inverse map, drops slots outside the logical shape (bounds
+// guard, kernel.hpp:290-302) and accumulates value * x[col] into y[row].
+// The kernels below compute the same sums in fp32 with a different (tree)
+// association order; padded ELL slots are multiplied like the reference
+// (0 * x[0]); BCSR slots past M/N are guarded out.
+#include <cuda_bf16.h>
+
+#include "devutil.cuh"
+#include "internal.cuh"
+
+namespace sfg {
+
+namespace {
+
+constexpr int kBlock = 256;
+
+__device__ __forceinline__ float ldx(const float* __restrict__ x, int c) { return __ldg(x + c); }
+
+// ---------------------------------------------------------------- CSR
+// G lanes per row (G = power of two, 2..32): lanes stride the row's
+// entries (coalesced idx/val streams), gather x through the read-only
+// path, then reduce inside the lane group with shuffles.
+template <int G>
+__global__ void __launch_bounds__(kBlock) k_spmv_csr(const int32_t* __restrict__ ptr,
+                                                      const int32_t* __restrict__ col,
+                                                      const float* __restrict__ val,
+                                                      const float* __restrict__ x,
+                                                      float* __restrict__ y, int32_t m, int acc) {
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << (lane & ~(G - 1)));
+  const int64_t groups = (int64_t)gridDim.x * (blockDim.x / G);
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; r < m; r += groups) {
+    int s = __ldg(ptr + r), e = __ldg(ptr + r + 1);
+    float sum = 0.f;
+    int k = s + gl;
+    // two independent gathers in flight per lane
+    for (; k + G < e; k += 2 * G) {
+      int c0 = ld_stream(col + k), c1 = ld_stream(col + k + G);
+      float v0 = ld_stream(val + k), v1 = ld_stream(val + k + G);
+      sum = fmaf(v0, ldx(x, c0), sum);
+      sum = fmaf(v1, ldx(x, c1), sum);
+    }
+    if (k < e) sum = fmaf(ld_stream(val + k), ldx(x, ld_stream(col + k)), sum);
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(gmask, sum, o);
+    if (gl == 0) y[r] = acc ? y[r] + sum : sum;
+  }
+}
+
+// ---------------------------------------------------------------- DCSR
+template <int G>
+__global__ void __launch_bounds__(kBlock) k_spmv_dcsr(const int32_t* __restrict__ rows,
+                                                       const int32_t* __restrict__ ptr,
+                                                       const int32_t* __restrict__ col,
+                                                       const float* __restrict__ val,
+                                                       const float* __restrict__ x,
+                                                       float* __restrict__ y, int64_t nnr) {
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << (lane & ~(G - 1)));
+  const int64_t groups = (int64_t)gridDim.x * (blockDim.x / G);
+  for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; p < nnr; p += groups) {
+    int s = __ldg(ptr + p), e = __ldg(ptr + p + 1);
+    float sum = 0.f;
+    for (int k = s + gl; k < e; k += G) sum = fmaf(ld_stream(val + k), ldx(x, ld_stream(col + k)), sum);
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(gmask, sum, o);
+    if (gl == 0) {
+      int r = __ldg(rows + p);
+      y[r] += sum;  // y pre-zeroed (or accumulating); rows are distinct
+    }
+  }
+}
+
+// ---------------------------------------------------------------- ELL
+// Thread per row; slot-major arrays make each slot a coalesced stream.
+__global__ void __launch_bounds__(kBlock) k_spmv_ell(const int32_t* __restrict__ idx,
+                                                      const float* __restrict__ val,
+                                                      const float* __restrict__ x,
+                                                      float* __restrict__ y, int32_t m, int32_t k,
+                                                      int acc) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    float sum = 0.f;
+    int s = 0;
+    for (; s + 1 < k; s += 2) {
+      int c0 = ld_stream(idx + (int64_t)s * m + r), c1 = ld_stream(idx + (int64_t)(s + 1) * m + r);
+      float v0 = ld_stream(val + (int64_t)s * m + r), v1 = ld_stream(val + (int64_t)(s + 1) * m + r);
+      sum = fmaf(v0, ldx(x, c0), sum);
+      sum = fmaf(v1, ldx(x, c1), sum);
+    }
+    if (s < k) sum = fmaf(ld_stream(val + (int64_t)s * m + r), ldx(x, ld_stream(idx + (int64_t)s * m + r)), sum);
+    y[r] = acc ? y[r] + sum : sum;
+  }
+}
+
+// ---------------------------------------------------------------- COO
+// Row-sorted entries, segmented warp reduction. Each warp owns a chunk of
+// kCooIters*32 consecutive entries; every 32-entry step does a segmented
+// inclusive scan keyed by row, closes finished rows with a plain add, and
+// carries the open row into the next step. Only the first and last row of
+// a chunk can be shared with another warp; those use atomicAdd.
+constexpr int kCooIters = 8;
+
+__global__ void __launch_bounds__(kBlock) k_spmv_coo(const int32_t* __restrict__ row,
+                                                      const int32_t* __restrict__ col,
+                                                      const float* __restrict__ val,
+                                                      const float* __restrict__ x,
+                                                      float* __restrict__ y, int64_t nnz) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t chunk = 32 * kCooIters;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w * chunk < nnz; w += warps) {
+    const int64_t c0 = w * chunk;
+    const int64_t c1 = c0 + chunk < nnz ? c0 + chunk : nnz;
+    const int first_row = __ldg(row + c0);
+    int carry_row = -1;
+    float carry = 0.f;
+    for (int64_t base = c0; base < c1; base += 32) {
+      int64_t e = base + lane;
+      bool valid = e < c1;
+      int r = valid ? ld_stream(row + e) : -1;
+      float p = valid ? ld_stream(val + e) * ldx(x, ld_stream(col + e)) : 0.f;
+      // fold the carried row into its first occurrence
+      if (lane == 0 && r == carry_row) p += carry;
+      // segmented inclusive scan keyed by row
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        float q = __shfl_up_sync(kFull, p, o);
+        int rq = __shfl_up_sync(kFull, r, o);
+        if (lane >= o && rq == r) p += q;
+      }
+      int rnext = __shfl_down_sync(kFull, r, 1);
+      bool tail = valid && (lane == 31 || rnext != r);
+      bool last_lane_open = lane == 31 || !__shfl_down_sync(kFull, (int)valid, 1);
+      // carried row that did not reappear in this step is finished
+      if (lane == 0 && carry_row >= 0 && r != carry_row) {
+        if (carry_row == first_row) atomicAdd(y + carry_row, carry);
+        else y[carry_row] += carry;
+      }
+      carry_row = -1;
+      // segment ends that are not the step's last valid entry close now
+      bool closes = tail && !(valid && last_lane_open);
+      if (closes) {
+        if (r == first_row) atomicAdd(y + r, p);
+        else y[r] += p;
+      }
+      // the last valid lane's segment may continue: carry it
+      int src = 31 - __clz(__ballot_sync(kFull, valid));
+      carry_row = __shfl_sync(kFull, r, src);
+      carry = __shfl_sync(kFull, p, src);
+    }
+    if (lane == 0 && carry_row >= 0) atomicAdd(y + carry_row, carry);
+  }
+}
+
+// ---------------------------------------------------------------- CSC
+// Column-major walk: warp per column, scatter-add into y.
+__global__ void __launch_bounds__(kBlock) k_spmv_csc(const int32_t* __restrict__ ptr,
+                                                      const int32_t* __restrict__ rowi,
+                                                      const float* __restrict__ val,
+                                                      const float* __restrict__ x,
+                                                      float* __restrict__ y, int32_t n) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < n; c += warps) {
+    int s = __ldg(ptr + c), e = __ldg(ptr + c + 1);
+    float xc = ldx(x, (int)c);
+    for (int k = s + lane; k < e; k += 32) atomicAdd(y + ld_stream(rowi + k), ld_stream(val + k) * xc);
+  }
+}
+
+// ---------------------------------------------------------------- BCSR
+// Warp per block row; lanes own (row-in-block) x (col-in-block) slots of
+// each block in turn. Slots past M/N are guarded out like the reference.
+template <typename T>
+__device__ __forceinline__ float to_f(T v);
+template <>
+__device__ __forceinline__ float to_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ float to_f<__nv_bfloat16_raw>(__nv_bfloat16_raw v) {
+  return __uint_as_float(static_cast<uint32_t>(v.x) << 16);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_spmv_bcsr(const int32_t* __restrict__ ptr,
+                                                       const int32_t* __restrict__ bcol,
+                                                       const T* __restrict__ val,
+                                                       const float* __restrict__ x,
+                                                       float* __restrict__ y, int64_t nbr, int32_t m,
+                                                       int32_t n, int32_t br, int32_t bc, int32_t rb,
+                                                       int32_t cb, int acc) {
+  extern __shared__ float sh_rows[];  // [warps][rb]
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  float* mine = sh_rows + wid * rb;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int slots = rb * cb;
+  for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nbr; b += warps) {
+    for (int i = lane; i < rb; i += 32) mine[i] = 0.f;
+    __syncwarp();
+    int s = __ldg(ptr + b), e = __ldg(ptr + b + 1);
+    for (int k = s; k < e; ++k) {
+      int c0 = __ldg(bcol + k) * bc;
+      const T* blk = val + (int64_t)k * slots;
+      for (int q = lane; q < slots; q += 32) {
+        int i = q / cb, j = q - i * cb;
+        int cc = c0 + j;
+        if (cc < n) atomicAdd(mine + i, to_f(blk[q]) * ldx(x, cc));
+      }
+    }
+    __syncwarp();
+    for (int i = lane; i < rb; i += 32) {
+      int64_t r = b * br + i;
+      if (r < m) y[r] = acc ? y[r] + mine[i] : mine[i];
+    }
+    __syncwarp();
+  }
+}
+
+int pick_group(double avg) {
+  if (avg <= 2) return 2;
+  if (avg <= 4) return 4;
+  if (avg <= 8) return 8;
+  if (avg <= 24) return 16;
+  return 32;
+}
+
+void spmv_csr(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, bool acc) {
+  if (a->m == 0) return;
+  int g = pick_group(a->m ? double(a->nnz) / double(a->m) : 0);
+  int rows_per_cta = kBlock / g;
+  int grid = (int)std::min<int64_t>(ceil_div(a->m, rows_per_cta), (int64_t)ctx->sms * 16);
+  auto v = static_cast<const float*>(a->val);
+  switch (g) {
+    case 2: SFG_LAUNCH(k_spmv_csr<2>, grid, kBlock, 0, ctx->stream, a->ptr, a->idx, v, x, y, (int)a->m, acc); break;
+    case 4: SFG_LAUNCH(k_spmv_csr<4>, grid, kBlock, 0, ctx->stream, a->ptr, a->idx, v, x, y, (int)a->m, acc); break;
+    case 8: SFG_LAUNCH(k_spmv_csr<8>, grid, kBlock, 0, ctx->stream, a->ptr, a->idx, v, x, y, (int)a->m, acc); break;
+    case 16: SFG_LAUNCH(k_spmv_csr<16>, grid, kBlock, 0, ctx->stream, a->ptr, a->idx, v, x, y, (int)a->m, acc); break;
+    default: SFG_LAUNCH(k_spmv_csr<32>, grid, kBlock, 0, ctx->stream, a->ptr, a->idx, v, x, y, (int)a->m, acc); break;
+  }
+}
+
+void zero_y(sfg_context* ctx, float* y, int64_t m) {
+  if (m) SFG_CUDA(cudaMemsetAsync(y, 0, m * sizeof(float), ctx->stream));
+}
+
+void spmv_coo(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, bool acc) {
+  if (!acc) zero_y(ctx, y, a->m);
+  if (a->nnz == 0) return;
+  int64_t chunks = ceil_div(a->nnz, 32 * kCooIters);
+  int grid = (int)std::min<int64_t>(ceil_div(chunks, kBlock / 32), (int64_t)ctx->sms * 16);
+  SFG_LAUNCH(k_spmv_coo, grid, kBlock, 0, ctx->stream, a->row, a->idx,
+             static_cast<const float*>(a->val), x, y, a->nnz);
+}
+
+void spmv_ell(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, bool acc) {
+  if (a->m == 0) return;
+  if (a->k == 0) {
+    if (!acc) zero_y(ctx, y, a->m);
+    return;
+  }
+  SFG_LAUNCH(k_spmv_ell, (int)ceil_div(a->m, kBlock), kBlock, 0, ctx->stream, a->idx,
+             static_cast<const float*>(a->val), x, y, (int)a->m, (int)a->k, acc);
+}
+
+}  // namespace
+
+void spmv(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, bool acc) {
+  switch (a->kind) {
+    case SFG_CSR: spmv_csr(ctx, a, x, y, acc); break;
+    case SFG_COO: spmv_coo(ctx, a, x, y, acc); break;
+    case SFG_ELL: spmv_ell(ctx, a, x, y, acc); break;
+    case SFG_DCSR: {
+      if (!acc) zero_y(ctx, y, a->m);
+      if (a->nnr == 0) break;
+      int g = pick_group(double(a->nnz) / double(a->nnr));
+      int grid = (int)std::min<int64_t>(ceil_div(a->nnr, kBlock / g), (int64_t)ctx->sms * 16);
+      auto v = static_cast<const float*>(a->val);
+      switch (g) {
+        case 2: SFG_LAUNCH(k_spmv_dcsr<2>, grid, kBlock, 0, ctx->stream, a->row, a->ptr, a->idx, v, x, y, a->nnr); break;
+        case 4: SFG_LAUNCH(k_spmv_dcsr<4>, grid, kBlock, 0, ctx->stream, a->row, a->ptr, a->idx, v, x, y, a->nnr); break;
+        case 8: SFG_LAUNCH(k_spmv_dcsr<8>, grid, kBlock, 0, ctx->stream, a->row, a->ptr, a->idx, v, x, y, a->nnr); break;
+        case 16: SFG_LAUNCH(k_spmv_dcsr<16>, grid, kBlock, 0, ctx->stream, a->row, a->ptr, a->idx, v, x, y, a->nnr); break;
+        default: SFG_LAUNCH(k_spmv_dcsr<32>, grid, kBlock, 0, ctx->stream, a->row, a->ptr, a->idx, v, x, y, a->nnr); break;
+      }
+      break;
+    }
+    case SFG_CSC: {
+      if (!acc) zero_y(ctx, y, a->m);
+      if (a->nnz == 0) break;
+      int grid = (int)std::min<int64_t>(ceil_div(a->n, kBlock / 32), (int64_t)ctx->sms * 16);
+      SFG_LAUNCH(k_spmv_csc, grid, kBlock, 0, ctx->stream, a->ptr, a->idx,
+                 static_cast<const float*>(a->val), x, y, (int)a->n);
+      break;
+    }
+    case SFG_BCSR: {
+      if (a->nbr == 0) break;
+      int grid = (int)std::min<int64_t>(ceil_div(a->nbr, kBlock / 32), (int64_t)ctx->sms * 16);
+      size_t smem = (kBlock / 32) * a->rb * sizeof(float);
+      if (a->dtype == SFG_BF16)
+        SFG_LAUNCH(k_spmv_bcsr<__nv_bfloat16_raw>, grid, kBlock, smem, ctx->stream, a->ptr, a->idx,
+                   static_cast<const __nv_bfloat16_raw*>(a->val), x, y, a->nbr, (int)a->m, (int)a->n,
+                   (int)a->br, (int)a->bc, (int)a->rb, (int)a->cb, acc);
+      else
+        SFG_LAUNCH(k_spmv_bcsr<float>, grid, kBlock, smem, ctx->stream, a->ptr, a->idx,
+                   static_cast<const float*>(a->val), x, y, a->nbr, (int)a->m, (int)a->n,
+                   (int)a->br, (int)a->bc, (int)a->rb, (int)a->cb, acc);
+      break;
+    }
+    case SFG_HYB:
+      // y = ELL(remainder) x, then += COO(selection) x: the caller-side sum
+      // of two run_kernel outputs in the reference.
+      spmv(ctx, a->part[0], x, y, acc);
+      spmv(ctx, a->part[1], x, y, true);
+      break;
+    default: raise(SFG_ERR_INVALID_OPERATION, "spmv: unsupported format");
+  }
+}
+
+}  // namespace sfg

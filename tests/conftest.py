@@ -32,3 +32,9 @@ def ref():
     if not oracle.ref_available():
         pytest.skip("reference shim (oracle/_ref/libsfref.so) not built here")
     return oracle.Ref()
+
+
+@pytest.fixture(scope="session")
+def ctx():
+    import paper_2403_05802_b200 as sfg
+    return sfg.Context(0)

@@ -1,0 +1,290 @@
+// convert_bcsr.cu — COO -> BCSR(r, c).
+//
+// Reference: plan TileSplit(0,r) TileSplit(2,c) Swap(1,2) Sort Fill(3)
+// Fill(2) Fill(0) Vectorize(2) Merge(0). TileSplit
+// (operators.hpp:263-285) maps (d0, d1) -> (d0/r, d1/c, d0%r, d1%c); the
+// mod level's bounds are [0, r-1] unless the whole range lies in one tile,
+// in which case they are [lo%r, hi%r] — a single block row is only M rows
+// tall (likewise for columns). Fill(3), Fill(2) complete every touched
+// block with zeros, positions past M/N included (operators.hpp:346-379);
+// Fill(0) leaves empty block rows as empty ptr runs. Materialized: L0 size
+// (block rows), L1 ptr[nbr+1] + idx[nblocks] (block columns, ascending),
+// L2/L3 dense, values block-major and row-major inside a block
+// (storage.hpp:142-218).
+//
+// Device plan: (1) block-row pointers from the sorted rows; (2) one CTA per
+// block row marks its block columns in a shared-memory bitmap (restricted
+// to the row's [min, max] block-column range) and counts them; (3)
+// look-back scan of the counts -> L1.ptr; (4) zero-fill the value array;
+// (5) each CTA rebuilds its bitmap, ranks the set bits (block index =
+// prefix popcount), writes L1.idx and scatters every entry into its block.
+#include <cuda_bf16.h>
+
+#include "devutil.cuh"
+#include "internal.cuh"
+
+namespace sfg {
+
+namespace {
+
+constexpr int kBlock = 256;
+constexpr int kMaxWords = 40 * 1024;  // 160 KB bitmap => <= 1.31 M block columns per row span
+
+__global__ void __launch_bounds__(kBlock) k_brow_ptr(const int32_t* __restrict__ row, int64_t nnz,
+                                                      int32_t r, int32_t nbr,
+                                                      int32_t* __restrict__ bptr) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t base0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+  for (int64_t wbase = base0; wbase < nnz; wbase += stride) {
+    int64_t e = wbase + (threadIdx.x & 31);
+    Gap g[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) g[i] = {1, 0, 0};
+    if (e < nnz) {
+      int b = __ldg(row + e) / r;
+      int prev = e == 0 ? -1 : __ldg(row + e - 1) / r;
+      g[0] = {prev + 1, b, (int32_t)e};
+      if (e == nnz - 1) g[1] = {b + 1, nbr, (int32_t)nnz};
+    }
+    fill_gaps(g, bptr);
+  }
+}
+
+// Bitmap of the block columns present in block row `br` over [lo, hi].
+__device__ __forceinline__ void mark(const int32_t* __restrict__ col, int32_t s, int32_t e,
+                                     int32_t c, int32_t lo, uint32_t* bm) {
+  for (int32_t k = s + threadIdx.x; k < e; k += blockDim.x) {
+    int b = __ldg(col + k) / c - lo;
+    atomicOr(bm + (b >> 5), 1u << (b & 31));
+  }
+}
+
+__device__ __forceinline__ void col_range(const int32_t* __restrict__ col, int32_t s, int32_t e,
+                                          int32_t c, int* smin, int* smax, int32_t* lo,
+                                          int32_t* hi) {
+  int mn = INT32_MAX, mx = -1;
+  for (int32_t k = s + threadIdx.x; k < e; k += blockDim.x) {
+    int b = __ldg(col + k) / c;
+    mn = min(mn, b);
+    mx = max(mx, b);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(kFull, mn, o));
+    mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+  }
+  if (threadIdx.x == 0) {
+    *smin = INT32_MAX;
+    *smax = -1;
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(smin, mn);
+    atomicMax(smax, mx);
+  }
+  __syncthreads();
+  *lo = *smin;
+  *hi = *smax;
+}
+
+__global__ void __launch_bounds__(kBlock) k_count_blocks(const int32_t* __restrict__ bptr,
+                                                          const int32_t* __restrict__ col,
+                                                          int32_t c, int32_t nbr,
+                                                          int32_t* __restrict__ cnt,
+                                                          int* __restrict__ too_wide) {
+  extern __shared__ uint32_t bm[];
+  __shared__ int smin, smax, ssum;
+  for (int32_t br = blockIdx.x; br < nbr; br += gridDim.x) {
+    int32_t s = __ldg(bptr + br), e = __ldg(bptr + br + 1);
+    if (s == e) {
+      if (threadIdx.x == 0) cnt[br] = 0;
+      continue;
+    }
+    int32_t lo, hi;
+    col_range(col, s, e, c, &smin, &smax, &lo, &hi);
+    int words = ((hi - lo) >> 5) + 1;
+    if (words > kMaxWords) {
+      if (threadIdx.x == 0) atomicOr(too_wide, 1);
+      continue;
+    }
+    for (int w = threadIdx.x; w < words; w += blockDim.x) bm[w] = 0;
+    if (threadIdx.x == 0) ssum = 0;
+    __syncthreads();
+    mark(col, s, e, c, lo, bm);
+    __syncthreads();
+    int pc = 0;
+    for (int w = threadIdx.x; w < words; w += blockDim.x) pc += __popc(bm[w]);
+    pc = warp_sum(pc);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&ssum, pc);
+    __syncthreads();
+    if (threadIdx.x == 0) cnt[br] = ssum;
+    __syncthreads();
+  }
+}
+
+constexpr int kItems = 16;
+constexpr int kTile = kBlock * kItems;
+
+__global__ void __launch_bounds__(kBlock) k_scan_i32(const int32_t* __restrict__ cnt, int32_t n,
+                                                      int32_t* __restrict__ ptr,
+                                                      unsigned long long* __restrict__ status,
+                                                      uint32_t epoch) {
+  __shared__ uint32_t smem[34];
+  __shared__ uint32_t slot;
+  const int64_t c0 = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kItems;
+  uint32_t v[kItems], sum = 0;
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    v[i] = c0 + i < n ? (uint32_t)__ldg(cnt + c0 + i) : 0u;
+    sum += v[i];
+  }
+  uint32_t total;
+  uint32_t excl = block_exclusive_scan<uint32_t, kBlock>(sum, smem, &total);
+  uint32_t p = lookback_prefix(status, epoch, blockIdx.x, total, &slot) + excl;
+#pragma unroll
+  for (int i = 0; i < kItems; ++i)
+    if (c0 + i < n) {
+      ptr[c0 + i] = (int32_t)p;
+      p += v[i];
+    }
+  if (c0 + kItems >= n && c0 < n) ptr[n] = (int32_t)p;
+}
+
+template <typename T>
+__device__ __forceinline__ T to_val(float v);
+template <>
+__device__ __forceinline__ float to_val<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 to_val<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_fill_blocks(
+    const int32_t* __restrict__ bptr, const int32_t* __restrict__ row,
+    const int32_t* __restrict__ col, const float* __restrict__ val, int32_t r, int32_t c,
+    int32_t rb, int32_t cb, int32_t nbr, const int32_t* __restrict__ blk_ptr,
+    int32_t* __restrict__ bidx, T* __restrict__ bval) {
+  extern __shared__ uint32_t bm[];  // [words] bitmap, then [words] prefix
+  __shared__ int smin, smax;
+  __shared__ uint32_t wsum[34];
+  for (int32_t br = blockIdx.x; br < nbr; br += gridDim.x) {
+    int32_t s = __ldg(bptr + br), e = __ldg(bptr + br + 1);
+    if (s == e) continue;
+    int32_t lo, hi;
+    col_range(col, s, e, c, &smin, &smax, &lo, &hi);
+    int words = ((hi - lo) >> 5) + 1;
+    uint32_t* pre = bm + words;
+    for (int w = threadIdx.x; w < words; w += blockDim.x) bm[w] = 0;
+    __syncthreads();
+    mark(col, s, e, c, lo, bm);
+    __syncthreads();
+    // exclusive prefix of popcounts over the words: each thread owns a
+    // contiguous run of words
+    int per = (words + blockDim.x - 1) / blockDim.x;
+    int w0 = threadIdx.x * per, w1 = min(words, w0 + per);
+    uint32_t mine = 0;
+    for (int w = w0; w < w1; ++w) mine += __popc(bm[w]);
+    uint32_t tot;
+    uint32_t ex = block_exclusive_scan<uint32_t, kBlock>(mine, wsum, &tot);
+    for (int w = w0; w < w1; ++w) {
+      pre[w] = ex;
+      ex += __popc(bm[w]);
+    }
+    __syncthreads();
+    const int32_t base = __ldg(blk_ptr + br);
+    // L1.idx: block columns in ascending order
+    for (int w = threadIdx.x; w < words; w += blockDim.x) {
+      uint32_t bits = bm[w];
+      uint32_t k = pre[w];
+      while (bits) {
+        int b = __ffs(bits) - 1;
+        bits &= bits - 1;
+        bidx[base + k++] = lo + (w << 5) + b;
+      }
+    }
+    // scatter the entries into their dense blocks
+    for (int32_t k = s + threadIdx.x; k < e; k += blockDim.x) {
+      int cc = __ldg(col + k), rr = __ldg(row + k);
+      int b = cc / c - lo;
+      uint32_t rank = pre[b >> 5] + __popc(bm[b >> 5] & ((1u << (b & 31)) - 1u));
+      int64_t blk = (int64_t)base + rank;
+      int i = rr - br * r, j = cc - (cc / c) * c;
+      bval[(blk * rb + i) * cb + j] = to_val<T>(__ldg(val + k));
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+sfg_tensor* coo_to_bcsr(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_t c, int dtype) {
+  const int64_t m = s->m, n = s->n, nnz = s->nnz;
+  sfg_tensor* t = new_tensor(ctx, SFG_BCSR, m, n);
+  t->dtype = dtype;
+  t->br = r;
+  t->bc = c;
+  t->nbr = (m - 1) / r + 1;
+  t->nbc = (n - 1) / c + 1;
+  t->rb = t->nbr == 1 ? m : r;  // one-tile bounds (operators.hpp:275-278)
+  t->cb = t->nbc == 1 ? n : c;
+  const int32_t nbr = (int32_t)t->nbr;
+  int32_t* bptr = dalloc_n<int32_t>(ctx, nbr + 1);
+  int32_t* cnt = dalloc_n<int32_t>(ctx, nbr);
+  t->ptr = dalloc_n<int32_t>(ctx, nbr + 1);
+  if (nnz == 0) {
+    SFG_CUDA(cudaMemsetAsync(t->ptr, 0, (nbr + 1) * sizeof(int32_t), ctx->stream));
+    t->idx = dalloc_n<int32_t>(ctx, 0);
+    t->val = dalloc(ctx, 4);
+    dfree(ctx, bptr);
+    dfree(ctx, cnt);
+    return t;
+  }
+  SFG_LAUNCH(k_brow_ptr, stream_grid(ctx, nnz, kBlock, 1, 8), kBlock, 0, ctx->stream, s->row, nnz,
+             (int32_t)r, nbr, bptr);
+  int tiles = (int)ceil_div(nbr, kTile);
+  char* scr = static_cast<char*>(scratch(ctx, (size_t)tiles * 8 + 64));
+  auto* status = reinterpret_cast<unsigned long long*>(scr);
+  auto* tail = reinterpret_cast<int32_t*>(scr + (size_t)tiles * 8);
+  SFG_CUDA(cudaMemsetAsync(tail, 0, 16, ctx->stream));
+  const size_t smem_count = kMaxWords * 4;
+  const size_t smem_fill = kMaxWords * 8 > 227 * 1024 ? 227 * 1024 : kMaxWords * 8;
+  static bool attr_set = false;
+  if (!attr_set) {
+    SFG_CUDA(cudaFuncSetAttribute(k_count_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem_count));
+    SFG_CUDA(cudaFuncSetAttribute(k_fill_blocks<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem_fill));
+    SFG_CUDA(cudaFuncSetAttribute(k_fill_blocks<__nv_bfloat16>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fill));
+    attr_set = true;
+  }
+  // bitmap words actually needed: the widest possible row span
+  int64_t words = (t->nbc + 31) / 32;
+  if (words * 8 > (int64_t)smem_fill)
+    raise(SFG_ERR_INVALID_OPERATION,
+          "BCSR: block-column range wider than the device bitmap (" + std::to_string(t->nbc) +
+              " block columns)");
+  int grid = (int)std::min<int64_t>(nbr, (int64_t)ctx->sms * 8);
+  SFG_LAUNCH(k_count_blocks, grid, kBlock, words * 4, ctx->stream, bptr, s->idx, (int32_t)c, nbr,
+             cnt, tail + 1);
+  SFG_LAUNCH(k_scan_i32, tiles, kBlock, 0, ctx->stream, cnt, nbr, t->ptr, status, ctx->epoch++);
+  int32_t nblocks = 0;
+  read_back(ctx, t->ptr + nbr, sizeof nblocks, &nblocks);
+  t->nnz = nblocks;
+  int64_t nvals = (int64_t)nblocks * t->rb * t->cb;
+  size_t esz = dtype == SFG_BF16 ? 2 : 4;
+  t->idx = dalloc_n<int32_t>(ctx, nblocks);
+  t->val = dalloc(ctx, nvals * esz);
+  SFG_CUDA(cudaMemsetAsync(t->val, 0, nvals * esz, ctx->stream));
+  if (dtype == SFG_BF16)
+    SFG_LAUNCH(k_fill_blocks<__nv_bfloat16>, grid, kBlock, words * 8, ctx->stream, bptr, s->row,
+               s->idx, static_cast<const float*>(s->val), (int32_t)r, (int32_t)c, (int32_t)t->rb,
+               (int32_t)t->cb, nbr, t->ptr, t->idx, static_cast<__nv_bfloat16*>(t->val));
+  else
+    SFG_LAUNCH(k_fill_blocks<float>, grid, kBlock, words * 8, ctx->stream, bptr, s->row, s->idx,
+               static_cast<const float*>(s->val), (int32_t)r, (int32_t)c, (int32_t)t->rb,
+               (int32_t)t->cb, nbr, t->ptr, t->idx, static_cast<float*>(t->val));
+  dfree(ctx, bptr);
+  dfree(ctx, cnt);
+  return t;
+}
+
+}  // namespace sfg

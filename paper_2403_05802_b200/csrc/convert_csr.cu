@@ -240,6 +240,17 @@ sfg_tensor* coo_to_coo(sfg_context* ctx, const sfg_tensor* s) {
   return t;
 }
 
+void compress_sorted(sfg_context* ctx, const int32_t* key, const int32_t* other, const float* val,
+                     int64_t nnz, int64_t extent, int32_t* ptr, int32_t* oidx, float* oval) {
+  if (nnz == 0) {
+    SFG_LAUNCH(k_fill_i32, stream_grid(ctx, extent + 1, kBlock, 4), kBlock, 0, ctx->stream, ptr,
+               extent + 1, 0);
+    return;
+  }
+  SFG_LAUNCH(k_coo_to_csr, stream_grid(ctx, ceil_div(nnz, 4), kBlock, 1, 8), kBlock, 0, ctx->stream,
+             key, other, val, nnz, (int32_t)extent, ptr, oidx, oval);
+}
+
 sfg_tensor* coo_to_csr(sfg_context* ctx, const sfg_tensor* s) {
   sfg_tensor* t = new_tensor(ctx, SFG_CSR, s->m, s->n);
   t->nnz = s->nnz;

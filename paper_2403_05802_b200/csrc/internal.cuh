@@ -115,6 +115,11 @@ void check_coo_canonical(sfg_context* ctx, const int32_t* row, const int32_t* co
                          int64_t n, int64_t nnz);
 sfg_tensor* sort_coo(sfg_context* ctx, int64_t m, int64_t n, int64_t nnz, const int32_t* row,
                      const int32_t* col, const float* val, bool sum_duplicates);
+void radix_sort(sfg_context* ctx, uint64_t* keys, uint32_t* pay, int64_t n, int key_bits,
+                uint64_t** kres, uint32_t** pres, uint64_t** kalt, uint32_t** palt);
+// ptr[extent+1] + copies of (other, val) from entries sorted by `key`.
+void compress_sorted(sfg_context* ctx, const int32_t* key, const int32_t* other, const float* val,
+                     int64_t nnz, int64_t extent, int32_t* ptr, int32_t* oidx, float* oval);
 void sort_u64_keys(sfg_context* ctx, uint64_t* keys, int64_t n, int key_bits, uint64_t** sorted_out);
 
 sfg_tensor* coo_to_coo(sfg_context* ctx, const sfg_tensor* s);

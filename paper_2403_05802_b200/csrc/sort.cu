@@ -244,7 +244,7 @@ int bits_for(int64_t extent) {
 
 // LSD radix sort of (key, payload) by the low `key_bits` bits. The result
 // lands in either the input or the alternate buffer; *kres / *pres say which.
-static void radix_sort(sfg_context* ctx, uint64_t* keys, uint32_t* pay, int64_t n, int key_bits,
+void radix_sort(sfg_context* ctx, uint64_t* keys, uint32_t* pay, int64_t n, int key_bits,
                        uint64_t** kres, uint32_t** pres, uint64_t** kalt_out, uint32_t** palt_out) {
   int passes = (key_bits + 7) / 8;
   if (passes > kMaxPasses) passes = kMaxPasses;

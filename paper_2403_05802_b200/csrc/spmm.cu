@@ -1,0 +1,380 @@
+// spmm.cu — C[M x nd] = A B over every materialized format (CUDA cores).
+//
+// Reference: run_kernel(spmm_kernel(), {A, B}) (kernel.hpp:236-384, 42-51):
+// every stored slot (padding included) restores (d0, d1), is bounds-guarded,
+// and for each d2 accumulates value * B[d1][d2] into C[d0][d2]. Here a warp
+// owns a row (or a row-sorted run of entries) and its lanes own 32*V
+// consecutive output columns: each stored entry is broadcast across the
+// warp and multiplies one coalesced row of B. fp32 accumulate; B may be
+// fp32 or bf16. The BCSR tensor-core path lives in bcsr_tc.cu.
+#include <cuda_bf16.h>
+
+#include "devutil.cuh"
+#include "internal.cuh"
+
+namespace sfg {
+
+namespace {
+
+constexpr int kBlock = 256;
+
+template <typename TB>
+struct BRow;
+
+template <>
+struct BRow<float> {
+  template <int V>
+  __device__ __forceinline__ static void load(const float* __restrict__ p, float (&v)[V]) {
+    if constexpr (V == 4) {
+      float4 q = __ldg(reinterpret_cast<const float4*>(p));
+      v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else if constexpr (V == 2) {
+      float2 q = __ldg(reinterpret_cast<const float2*>(p));
+      v[0] = q.x; v[1] = q.y;
+    } else {
+#pragma unroll
+      for (int i = 0; i < V; ++i) v[i] = __ldg(p + i);
+    }
+  }
+};
+
+template <>
+struct BRow<__nv_bfloat16> {
+  template <int V>
+  __device__ __forceinline__ static void load(const __nv_bfloat16* __restrict__ p, float (&v)[V]) {
+    if constexpr (V == 4) {
+      uint2 q = __ldg(reinterpret_cast<const uint2*>(p));
+      v[0] = __uint_as_float(q.x << 16); v[1] = __uint_as_float(q.x & 0xffff0000u);
+      v[2] = __uint_as_float(q.y << 16); v[3] = __uint_as_float(q.y & 0xffff0000u);
+    } else if constexpr (V == 2) {
+      uint32_t q = __ldg(reinterpret_cast<const unsigned int*>(p));
+      v[0] = __uint_as_float(q << 16); v[1] = __uint_as_float(q & 0xffff0000u);
+    } else {
+#pragma unroll
+      for (int i = 0; i < V; ++i) v[i] = __bfloat162float(p[i]);
+    }
+  }
+};
+
+// Geometry of the dense operands shared by every kernel.
+struct Dense {
+  const void* b;
+  int64_t ldb;
+  float* c;
+  int64_t ldc;
+  int32_t nd;
+  int acc;
+};
+
+// Accumulate `val * B[col][cols of this lane]` for the lane's column chunk.
+template <typename TB, int V>
+__device__ __forceinline__ void fma_row(const Dense& d, int col, float val, int c0, bool vec,
+                                        float (&acc)[V]) {
+  const TB* brow = static_cast<const TB*>(d.b) + (int64_t)col * d.ldb + c0;
+  float v[V];
+  if (vec) {
+    BRow<TB>::template load<V>(brow, v);
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; ++i) v[i] = c0 + i < d.nd ? (float)brow[i] : 0.f;
+  }
+#pragma unroll
+  for (int i = 0; i < V; ++i) acc[i] = fmaf(val, v[i], acc[i]);
+}
+
+template <int V>
+__device__ __forceinline__ void store_row(const Dense& d, int64_t row, int c0, bool atomic,
+                                          const float (&acc)[V]) {
+  float* crow = d.c + row * d.ldc + c0;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    if (c0 + i >= d.nd) break;
+    if (atomic) atomicAdd(crow + i, acc[i]);
+    else crow[i] = d.acc ? crow[i] + acc[i] : acc[i];
+  }
+}
+
+// -------------------------------------------------------------- CSR/DCSR
+// rows == nullptr: CSR (row p is row p); otherwise DCSR (row = rows[p]).
+template <typename TB, int V>
+__global__ void __launch_bounds__(kBlock) k_spmm_rows(const int32_t* __restrict__ rows,
+                                                       const int32_t* __restrict__ ptr,
+                                                       const int32_t* __restrict__ col,
+                                                       const float* __restrict__ val, int64_t nrows,
+                                                       Dense d) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int chunks = (d.nd + 32 * V - 1) / (32 * V);
+  const bool vec_ok = (d.nd % (32 * V) == 0) && (d.ldb % V == 0);
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nrows * chunks;
+       w += warps) {
+    int64_t p = w / chunks;
+    int c0 = (int)(w - p * chunks) * 32 * V + lane * V;
+    int s = __ldg(ptr + p), e = __ldg(ptr + p + 1);
+    float acc[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[i] = 0.f;
+    for (int base = s; base < e; base += 32) {
+      int k = base + lane;
+      int mc = k < e ? ld_stream(col + k) : 0;
+      float mv = k < e ? ld_stream(val + k) : 0.f;
+      int cnt = min(32, e - base);
+      int j = 0;
+      for (; j + 2 <= cnt; j += 2) {
+        int c1 = __shfl_sync(kFull, mc, j), c2 = __shfl_sync(kFull, mc, j + 1);
+        float v1 = __shfl_sync(kFull, mv, j), v2 = __shfl_sync(kFull, mv, j + 1);
+        fma_row<TB, V>(d, c1, v1, c0, vec_ok, acc);
+        fma_row<TB, V>(d, c2, v2, c0, vec_ok, acc);
+      }
+      if (j < cnt) fma_row<TB, V>(d, __shfl_sync(kFull, mc, j), __shfl_sync(kFull, mv, j), c0, vec_ok, acc);
+    }
+    int64_t r = rows ? __ldg(rows + p) : p;
+    store_row<V>(d, r, c0, false, acc);
+  }
+}
+
+// ------------------------------------------------------------------- ELL
+template <typename TB, int V>
+__global__ void __launch_bounds__(kBlock) k_spmm_ell(const int32_t* __restrict__ idx,
+                                                      const float* __restrict__ val, int32_t m,
+                                                      int32_t k, Dense d) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int chunks = (d.nd + 32 * V - 1) / (32 * V);
+  const bool vec_ok = (d.nd % (32 * V) == 0) && (d.ldb % V == 0);
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < (int64_t)m * chunks;
+       w += warps) {
+    int64_t r = w / chunks;
+    int c0 = (int)(w - r * chunks) * 32 * V + lane * V;
+    float acc[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[i] = 0.f;
+    for (int s = 0; s < k; ++s) {
+      int64_t cell = (int64_t)s * m + r;
+      fma_row<TB, V>(d, __ldg(idx + cell), __ldg(val + cell), c0, vec_ok, acc);
+    }
+    store_row<V>(d, r, c0, false, acc);
+  }
+}
+
+// ------------------------------------------------------------------- COO
+// A warp owns 32*kCooIters consecutive row-sorted entries; it accumulates a
+// row while the row stays the same and flushes on change. Only the first and
+// last rows of a chunk may be shared with neighbouring warps (atomicAdd).
+constexpr int kCooIters = 4;
+
+template <typename TB, int V>
+__global__ void __launch_bounds__(kBlock) k_spmm_coo(const int32_t* __restrict__ row,
+                                                      const int32_t* __restrict__ col,
+                                                      const float* __restrict__ val, int64_t nnz,
+                                                      Dense d) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int chunks = (d.nd + 32 * V - 1) / (32 * V);
+  const bool vec_ok = (d.nd % (32 * V) == 0) && (d.ldb % V == 0);
+  const int64_t span = 32 * kCooIters;
+  const int64_t nchunks = (nnz + span - 1) / span;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nchunks * chunks;
+       w += warps) {
+    int64_t q = w / chunks;
+    int c0 = (int)(w - q * chunks) * 32 * V + lane * V;
+    int64_t e0 = q * span, e1 = min(nnz, e0 + span);
+    int first = __ldg(row + e0);
+    int last = __ldg(row + e1 - 1);
+    int cur = first;
+    float acc[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[i] = 0.f;
+    for (int64_t base = e0; base < e1; base += 32) {
+      int64_t k = base + lane;
+      int mr = k < e1 ? __ldg(row + k) : -1;
+      int mc = k < e1 ? __ldg(col + k) : 0;
+      float mv = k < e1 ? __ldg(val + k) : 0.f;
+      int cnt = (int)min<int64_t>(32, e1 - base);
+      for (int j = 0; j < cnt; ++j) {
+        int rj = __shfl_sync(kFull, mr, j);
+        if (rj != cur) {
+          store_row<V>(d, cur, c0, cur == first, acc);
+#pragma unroll
+          for (int i = 0; i < V; ++i) acc[i] = 0.f;
+          cur = rj;
+        }
+        fma_row<TB, V>(d, __shfl_sync(kFull, mc, j), __shfl_sync(kFull, mv, j), c0, vec_ok, acc);
+      }
+    }
+    store_row<V>(d, cur, c0, cur == first || cur == last, acc);
+  }
+}
+
+// ------------------------------------------------------------------- CSC
+template <typename TB, int V>
+__global__ void __launch_bounds__(kBlock) k_spmm_csc(const int32_t* __restrict__ ptr,
+                                                      const int32_t* __restrict__ rowi,
+                                                      const float* __restrict__ val, int32_t n,
+                                                      Dense d) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int chunks = (d.nd + 32 * V - 1) / (32 * V);
+  const bool vec_ok = (d.nd % (32 * V) == 0) && (d.ldb % V == 0);
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < (int64_t)n * chunks;
+       w += warps) {
+    int64_t c = w / chunks;
+    int c0 = (int)(w - c * chunks) * 32 * V + lane * V;
+    int s = __ldg(ptr + c), e = __ldg(ptr + c + 1);
+    if (s == e) continue;
+    float b[V], zero[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) zero[i] = 0.f, b[i] = 0.f;
+    fma_row<TB, V>(d, (int)c, 1.f, c0, vec_ok, b);
+    for (int k = s; k < e; ++k) {
+      float v = __ldg(val + k);
+      float a[V];
+#pragma unroll
+      for (int i = 0; i < V; ++i) a[i] = v * b[i];
+      store_row<V>(d, __ldg(rowi + k), c0, true, a);
+    }
+    (void)zero;
+  }
+}
+
+// ------------------------------------------------------------------ BCSR
+// Warp per (block row, column chunk): lanes keep rb accumulators (one per
+// row of the block row) for their V columns; every stored slot of every
+// block is applied; rows/cols past M/N are guarded out (kernel.hpp:290-302).
+template <typename TB, typename TA, int V, int RB>
+__global__ void __launch_bounds__(kBlock) k_spmm_bcsr(const int32_t* __restrict__ ptr,
+                                                       const int32_t* __restrict__ bcol,
+                                                       const TA* __restrict__ val, int64_t nbr,
+                                                       int32_t m, int32_t n, int32_t br, int32_t bc,
+                                                       int32_t rb, int32_t cb, Dense d) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int chunks = (d.nd + 32 * V - 1) / (32 * V);
+  const bool vec_ok = (d.nd % (32 * V) == 0) && (d.ldb % V == 0);
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nbr * chunks;
+       w += warps) {
+    int64_t b = w / chunks;
+    int c0 = (int)(w - b * chunks) * 32 * V + lane * V;
+    float acc[RB][V];
+#pragma unroll
+    for (int i = 0; i < RB; ++i)
+#pragma unroll
+      for (int v = 0; v < V; ++v) acc[i][v] = 0.f;
+    int s = __ldg(ptr + b), e = __ldg(ptr + b + 1);
+    for (int k = s; k < e; ++k) {
+      int colbase = __ldg(bcol + k) * bc;
+      const TA* blk = val + (int64_t)k * rb * cb;
+      for (int j = 0; j < cb; ++j) {
+        if (colbase + j >= n) break;
+        float bv[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) bv[v] = 0.f;
+        fma_row<TB, V>(d, colbase + j, 1.f, c0, vec_ok, bv);
+#pragma unroll
+        for (int i = 0; i < RB; ++i) {
+          if (i < rb) {
+            float a = (float)blk[i * cb + j];
+#pragma unroll
+            for (int v = 0; v < V; ++v) acc[i][v] = fmaf(a, bv[v], acc[i][v]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < RB; ++i) {
+      int64_t r = b * br + i;
+      if (i < rb && r < m) store_row<V>(d, r, c0, false, acc[i]);
+    }
+  }
+}
+
+template <typename TB, int V>
+void launch_fmt(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
+  int64_t chunks = ceil_div(d.nd, 32 * V);
+  auto grid_for = [&](int64_t warps_needed) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(warps_needed, kBlock / 32),
+                                                      (int64_t)ctx->sms * 16));
+  };
+  const float* fv = static_cast<const float*>(a->val);
+  switch (a->kind) {
+    case SFG_CSR:
+      SFG_LAUNCH((k_spmm_rows<TB, V>), grid_for(a->m * chunks), kBlock, 0, ctx->stream, nullptr,
+                 a->ptr, a->idx, fv, a->m, d);
+      break;
+    case SFG_DCSR:
+      if (a->nnr)
+        SFG_LAUNCH((k_spmm_rows<TB, V>), grid_for(a->nnr * chunks), kBlock, 0, ctx->stream, a->row,
+                   a->ptr, a->idx, fv, a->nnr, d);
+      break;
+    case SFG_ELL:
+      SFG_LAUNCH((k_spmm_ell<TB, V>), grid_for(a->m * chunks), kBlock, 0, ctx->stream, a->idx, fv,
+                 (int32_t)a->m, (int32_t)a->k, d);
+      break;
+    case SFG_COO:
+      if (a->nnz)
+        SFG_LAUNCH((k_spmm_coo<TB, V>), grid_for(ceil_div(a->nnz, 32 * kCooIters) * chunks), kBlock,
+                   0, ctx->stream, a->row, a->idx, fv, a->nnz, d);
+      break;
+    case SFG_CSC:
+      if (a->nnz)
+        SFG_LAUNCH((k_spmm_csc<TB, V>), grid_for(a->n * chunks), kBlock, 0, ctx->stream, a->ptr,
+                   a->idx, fv, (int32_t)a->n, d);
+      break;
+    case SFG_BCSR: {
+      if (a->nbr == 0 || a->nnz == 0) break;
+      if (a->rb > 16) raise(SFG_ERR_INVALID_OPERATION, "BCSR SpMM: block rows > 16 not supported");
+      int g = grid_for(a->nbr * chunks);
+#define SFG_BCSR_CASE(RB)                                                                          \
+  if (a->dtype == SFG_BF16)                                                                        \
+    SFG_LAUNCH((k_spmm_bcsr<TB, __nv_bfloat16, V, RB>), g, kBlock, 0, ctx->stream, a->ptr, a->idx, \
+               static_cast<const __nv_bfloat16*>(a->val), a->nbr, (int)a->m, (int)a->n,           \
+               (int)a->br, (int)a->bc, (int)a->rb, (int)a->cb, d);                                 \
+  else                                                                                             \
+    SFG_LAUNCH((k_spmm_bcsr<TB, float, V, RB>), g, kBlock, 0, ctx->stream, a->ptr, a->idx, fv,     \
+               a->nbr, (int)a->m, (int)a->n, (int)a->br, (int)a->bc, (int)a->rb, (int)a->cb, d);
+      if (a->rb <= 4) { SFG_BCSR_CASE(4) }
+      else if (a->rb <= 8) { SFG_BCSR_CASE(8) }
+      else { SFG_BCSR_CASE(16) }
+#undef SFG_BCSR_CASE
+      break;
+    }
+    default: raise(SFG_ERR_INVALID_OPERATION, "spmm: unsupported format");
+  }
+}
+
+template <typename TB>
+void launch_v(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
+  if (d.nd >= 128) launch_fmt<TB, 4>(ctx, a, d);
+  else if (d.nd >= 64) launch_fmt<TB, 2>(ctx, a, d);
+  else launch_fmt<TB, 1>(ctx, a, d);
+}
+
+}  // namespace
+
+// Tensor-core BCSR path (bcsr_tc.cu); returns false when not applicable.
+bool spmm_bcsr_tc(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dtype, int64_t nd,
+                  int64_t ldb, float* c, int64_t ldc, bool accumulate);
+
+void spmm(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dtype, int64_t nd,
+          int64_t ldb, float* c, int64_t ldc, bool accumulate) {
+  if (a->kind == SFG_HYB) {
+    spmm(ctx, a->part[0], b, b_dtype, nd, ldb, c, ldc, accumulate);
+    spmm(ctx, a->part[1], b, b_dtype, nd, ldb, c, ldc, true);
+    return;
+  }
+  if (a->kind == SFG_BCSR && spmm_bcsr_tc(ctx, a, b, b_dtype, nd, ldb, c, ldc, accumulate)) return;
+  bool zero_first = !accumulate && (a->kind == SFG_COO || a->kind == SFG_CSC || a->kind == SFG_DCSR ||
+                                    a->kind == SFG_BCSR);
+  if (zero_first && a->m > 0) {
+    if (ldc == nd)
+      SFG_CUDA(cudaMemsetAsync(c, 0, a->m * ldc * sizeof(float), ctx->stream));
+    else
+      SFG_CUDA(cudaMemset2DAsync(c, ldc * sizeof(float), 0, nd * sizeof(float), a->m, ctx->stream));
+  }
+  // kernels that own whole rows write with accumulate semantics after zeroing
+  Dense d{b, ldb, c, ldc, (int32_t)nd, (accumulate || zero_first) ? 1 : 0};
+  if (b_dtype == SFG_BF16) launch_v<__nv_bfloat16>(ctx, a, d);
+  else launch_v<float>(ctx, a, d);
+}
+
+}  // namespace sfg

@@ -1,0 +1,92 @@
+"""GPU parity: SpMM C = A B over every format (fp32 and bf16 B) vs the f64
+oracle, |C_hat - C| <= 1e-5 * sum_j |a_ij| |B_jk| per output."""
+import numpy as np
+import pytest
+
+import paper_2403_05802_b200 as sfg
+from gpu_common import TOL
+from matrices import power_law_coo, random_coo
+
+pytestmark = pytest.mark.gpu
+
+FORMATS = ["COO", "CSR", "CSC", "DCSR", "ELL", "BCSR(2,2)", "BCSR(4,4)", "BCSR(16,16)", "HYB(3)"]
+
+
+def oracle_spmm(port, p, fmt, b):
+    if fmt.startswith("BCSR"):
+        rr, cc = (int(t) for t in fmt[5:-1].split(","))
+        return port.spmm(port.convert(p, "BCSR", rr, cc), b)
+    if fmt.startswith("HYB"):
+        t = int(fmt[4:-1])
+        s, r, _ = port.decompose_rows(p, t)
+        return port.spmm(port.convert(r, "ELL"), b) + port.spmm(port.convert(s, "COO"), b)
+    return port.spmm(port.convert(p, fmt), b)
+
+
+def abs_bound(r, c, v, m, b):
+    out = np.zeros((m, b.shape[1]))
+    np.add.at(out, r, np.abs(v)[:, None] * np.abs(b[c]))
+    return out
+
+
+def check(cd, cr, bound, ctx):
+    err = np.abs(cd.astype(np.float64) - cr)
+    bad = err > TOL * bound + 1e-30
+    assert not bad.any(), (ctx, np.argwhere(bad)[:3], err[bad][:3])
+
+
+@pytest.mark.parametrize("nd", [1, 7, 32, 64, 128])
+@pytest.mark.parametrize("fmt", FORMATS)
+def test_spmm_formats(ctx, port, fmt, nd):
+    m, n = 130, 97
+    r, c, v = random_coo(nd, m, n, 0.2, zeros=0.1)
+    rng = np.random.default_rng(nd)
+    b = (rng.random((n, nd)) * 2 - 1).astype(np.float32)
+    d, p = ctx.from_coo(m, n, r, c, v), port.from_coo(m, n, r, c, v)
+    cd = ctx.spmm(ctx.convert(d, fmt), b)
+    cr = oracle_spmm(port, p, fmt, b.astype(np.float64))
+    check(cd, cr, abs_bound(r, c, v, m, b.astype(np.float64)), (fmt, nd))
+
+
+@pytest.mark.parametrize("fmt", ["CSR", "COO", "DCSR", "HYB(8)"])
+def test_spmm_power_law_nd64(ctx, port, fmt):
+    m, n = 3000, 2000
+    r, c, v = power_law_coo(1, m, n, avg=15, alpha=1.2)
+    b = (np.random.default_rng(0).random((n, 64)) * 2 - 1).astype(np.float32)
+    d, p = ctx.from_coo(m, n, r, c, v), port.from_coo(m, n, r, c, v)
+    cd = ctx.spmm(ctx.convert(d, fmt), b)
+    cr = oracle_spmm(port, p, fmt, b.astype(np.float64))
+    check(cd, cr, abs_bound(r, c, v, m, b.astype(np.float64)), fmt)
+
+
+def to_bf16_bits(a):
+    f = np.asarray(a, np.float32).view(np.uint32).astype(np.uint64)
+    return (((f + 0x7FFF + ((f >> 16) & 1)) >> 16)).astype(np.uint16)
+
+
+def bits_to_f64(bits):
+    return (bits.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+@pytest.mark.parametrize("fmt", ["CSR", "BCSR(16,16)", "BCSR(4,4)", "ELL"])
+def test_spmm_bf16_b(ctx, port, fmt):
+    """bf16 B: the oracle runs on the bf16-rounded operand."""
+    m, n, nd = 256, 192, 128
+    r, c, v = random_coo(9, m, n, 0.15)
+    b = (np.random.default_rng(2).random((n, nd)) * 2 - 1).astype(np.float32)
+    bb = to_bf16_bits(b)
+    d, p = ctx.from_coo(m, n, r, c, v), port.from_coo(m, n, r, c, v)
+    cd = ctx.spmm(ctx.convert(d, fmt), bb, b_dtype=sfg.BF16)
+    b64 = bits_to_f64(bb)
+    cr = oracle_spmm(port, p, fmt, b64)
+    check(cd, cr, abs_bound(r, c, v, m, b64), fmt)
+
+
+def test_spmm_accumulate_and_ld(ctx):
+    t = ctx.convert(ctx.from_coo(2, 2, [0, 1], [1, 0], [2.0, 3.0]), "CSR")
+    b = np.array([[1, 2, 0], [3, 4, 0]], np.float32)  # ldb = 3, nd = 2
+    cbuf = ctx.buffer(2 * 4 * 4).upload(np.full((2, 4), 10, np.float32))
+    bbuf = ctx.buffer(b.nbytes).upload(b)
+    ctx.spmm_device(t, bbuf.ptr, sfg.F32, 2, cbuf.ptr, ldb=3, ldc=4, accumulate=True)
+    out = cbuf.download(np.float32, 8).reshape(2, 4)
+    assert out.tolist() == [[16, 18, 10, 10], [13, 16, 10, 10]]

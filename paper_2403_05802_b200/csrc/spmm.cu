@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(kBlock) k_spmm_coo(const int32_t* __restrict__
       int mr = k < e1 ? __ldg(row + k) : -1;
       int mc = k < e1 ? __ldg(col + k) : 0;
       float mv = k < e1 ? __ldg(val + k) : 0.f;
-      int cnt = (int)min<int64_t>(32, e1 - base);
+      int cnt = (int)(e1 - base < 32 ? e1 - base : 32);
       for (int j = 0; j < cnt; ++j) {
         int rj = __shfl_sync(kFull, mr, j);
         if (rj != cur) {

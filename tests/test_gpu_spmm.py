@@ -90,3 +90,35 @@ def test_spmm_accumulate_and_ld(ctx):
     ctx.spmm_device(t, bbuf.ptr, sfg.F32, 2, cbuf.ptr, ldb=3, ldc=4, accumulate=True)
     out = cbuf.download(np.float32, 8).reshape(2, 4)
     assert out.tolist() == [[16, 18, 10, 10], [13, 16, 10, 10]]
+
+
+def bf16_round(a):
+    return bits_to_f64(to_bf16_bits(a))
+
+
+@pytest.mark.parametrize("shape", [(256, 256), (250, 200), (16, 16), (1000, 3000), (4096, 512)])
+@pytest.mark.parametrize("density", [0.02, 0.3])
+def test_bcsr16_bf16_tensor_core(ctx, port, shape, density):
+    """BCSR(16,16) with bf16 values and bf16 B, nd = 128: the tcgen05 path
+    (bcsr_tc.cu). The oracle runs on the bf16-rounded values and B."""
+    m, n = shape
+    rng = np.random.default_rng(m + n)
+    nbr, nbc = (m + 15) // 16, (n + 15) // 16
+    mask = rng.random((nbr, nbc)) < density
+    mask[nbr // 2] = False  # an empty block row
+    br, bc = np.nonzero(mask)
+    ii, jj = np.meshgrid(np.arange(16), np.arange(16), indexing="ij")
+    rows = (br[:, None] * 16 + ii.ravel()[None, :]).ravel()
+    cols = (bc[:, None] * 16 + jj.ravel()[None, :]).ravel()
+    keep = (rows < m) & (cols < n)
+    rows, cols = rows[keep], cols[keep]
+    vals = (0.5 + rng.integers(0, 1 << 23, rows.size) / 2.0 ** 23) * np.where(rng.random(rows.size) < .5, -1, 1)
+    vals = bf16_round(vals)
+    b = (rng.random((n, 128)) * 2 - 1).astype(np.float32)
+    bb = to_bf16_bits(b)
+    d = ctx.convert(ctx.from_coo(m, n, rows, cols, vals), "BCSR(16,16)", value_dtype=sfg.BF16)
+    cd = ctx.spmm(d, bb, b_dtype=sfg.BF16)
+    p = port.from_coo(m, n, rows, cols, vals)
+    b64 = bits_to_f64(bb)
+    cr = port.spmm(port.convert(p, "BCSR", 16, 16), b64)
+    check(cd, cr, abs_bound(rows, cols, vals, m, b64), ("bcsr-tc", shape, density))

@@ -1,5 +1,6 @@
 // core.cu — context, allocation, tensor lifetime and error plumbing.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.cuh"
@@ -7,6 +8,19 @@
 namespace sfg {
 
 std::atomic<int64_t> g_launches{0};
+
+bool debug_launches() {
+  static const bool on = [] {
+    const char* v = std::getenv("SFG_DEBUG");
+    return v && *v && *v != '0';
+  }();
+  return on;
+}
+
+void trace_launch(const char* name, cudaStream_t stream) {
+  std::fprintf(stderr, "[sfg] launch %s (stream %p)\n", name, (void*)stream);
+  std::fflush(stderr);
+}
 
 static thread_local std::string g_last_error;
 

@@ -28,14 +28,18 @@ void set_last_error(const std::string& msg);
   } while (0)
 
 extern std::atomic<int64_t> g_launches;
+bool debug_launches();  // SFG_DEBUG=1: trace and synchronize every launch
+void trace_launch(const char* name, cudaStream_t stream);
 
 // Every kernel launch goes through here: counted (bench gpu_launches) and
 // checked for launch-configuration errors.
 #define SFG_LAUNCH(kernel, grid, block, smem, stream, ...)                   \
   do {                                                                      \
+    if (::sfg::debug_launches()) ::sfg::trace_launch(#kernel, (stream));    \
     kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);             \
     ::sfg::g_launches.fetch_add(1, std::memory_order_relaxed);              \
     SFG_CUDA(cudaPeekAtLastError());                                        \
+    if (::sfg::debug_launches()) SFG_CUDA(cudaStreamSynchronize(stream));   \
   } while (0)
 
 }  // namespace sfg

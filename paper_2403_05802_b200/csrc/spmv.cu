@@ -101,62 +101,65 @@ __global__ void __launch_bounds__(kBlock) k_spmv_ell(const int32_t* __restrict__
 }
 
 // ---------------------------------------------------------------- COO
-// Row-sorted entries, segmented warp reduction. Each warp owns a chunk of
-// kCooIters*32 consecutive entries; every 32-entry step does a segmented
-// inclusive scan keyed by row, closes finished rows with a plain add, and
-// carries the open row into the next step. Only the first and last row of
-// a chunk can be shared with another warp; those use atomicAdd.
-constexpr int kCooIters = 8;
+// Row-sorted entries, thread-sequential segmented reduction: each lane owns
+// kCooRun consecutive entries (128-bit loads of row/col/val), sums runs of
+// equal rows in registers, and writes a row with a plain add when the row
+// lies strictly inside its run (no other lane can touch it); the lane's
+// first and last rows may continue in a neighbouring lane or warp and use
+// atomicAdd. y must be zeroed (or hold a partial result) beforehand.
+constexpr int kCooRun = 8;
+
+__device__ __forceinline__ void coo_flush(float* __restrict__ y, int r, float s, bool shared) {
+  if (shared) atomicAdd(y + r, s);
+  else y[r] += s;
+}
 
 __global__ void __launch_bounds__(kBlock) k_spmv_coo(const int32_t* __restrict__ row,
                                                       const int32_t* __restrict__ col,
                                                       const float* __restrict__ val,
                                                       const float* __restrict__ x,
                                                       float* __restrict__ y, int64_t nnz) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t chunk = 32 * kCooIters;
-  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w * chunk < nnz; w += warps) {
-    const int64_t c0 = w * chunk;
-    const int64_t c1 = c0 + chunk < nnz ? c0 + chunk : nnz;
-    const int first_row = __ldg(row + c0);
-    int carry_row = -1;
-    float carry = 0.f;
-    for (int64_t base = c0; base < c1; base += 32) {
-      int64_t e = base + lane;
-      bool valid = e < c1;
-      int r = valid ? ld_stream(row + e) : -1;
-      float p = valid ? ld_stream(val + e) * ldx(x, ld_stream(col + e)) : 0.f;
-      // fold the carried row into its first occurrence
-      if (lane == 0 && r == carry_row) p += carry;
-      // segmented inclusive scan keyed by row
+  const int64_t threads = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t * kCooRun < nnz; t += threads) {
+    const int64_t e0 = t * kCooRun;
+    int r[kCooRun], c[kCooRun];
+    float v[kCooRun];
+    if (e0 + kCooRun <= nnz) {
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        float q = __shfl_up_sync(kFull, p, o);
-        int rq = __shfl_up_sync(kFull, r, o);
-        if (lane >= o && rq == r) p += q;
+      for (int q = 0; q < kCooRun / 4; ++q) {
+        int4 rr = ld_stream(reinterpret_cast<const int4*>(row + e0) + q);
+        int4 cc = ld_stream(reinterpret_cast<const int4*>(col + e0) + q);
+        float4 vv = ld_stream(reinterpret_cast<const float4*>(val + e0) + q);
+        r[4 * q] = rr.x; r[4 * q + 1] = rr.y; r[4 * q + 2] = rr.z; r[4 * q + 3] = rr.w;
+        c[4 * q] = cc.x; c[4 * q + 1] = cc.y; c[4 * q + 2] = cc.z; c[4 * q + 3] = cc.w;
+        v[4 * q] = vv.x; v[4 * q + 1] = vv.y; v[4 * q + 2] = vv.z; v[4 * q + 3] = vv.w;
       }
-      int rnext = __shfl_down_sync(kFull, r, 1);
-      bool tail = valid && (lane == 31 || rnext != r);
-      bool last_lane_open = lane == 31 || !__shfl_down_sync(kFull, (int)valid, 1);
-      // carried row that did not reappear in this step is finished
-      if (lane == 0 && carry_row >= 0 && r != carry_row) {
-        if (carry_row == first_row) atomicAdd(y + carry_row, carry);
-        else y[carry_row] += carry;
+    } else {
+#pragma unroll
+      for (int i = 0; i < kCooRun; ++i) {
+        bool ok = e0 + i < nnz;
+        r[i] = ok ? row[e0 + i] : -1;
+        c[i] = ok ? col[e0 + i] : 0;
+        v[i] = ok ? val[e0 + i] : 0.f;
       }
-      carry_row = -1;
-      // segment ends that are not the step's last valid entry close now
-      bool closes = tail && !(valid && last_lane_open);
-      if (closes) {
-        if (r == first_row) atomicAdd(y + r, p);
-        else y[r] += p;
-      }
-      // the last valid lane's segment may continue: carry it
-      int src = 31 - __clz(__ballot_sync(kFull, valid));
-      carry_row = __shfl_sync(kFull, r, src);
-      carry = __shfl_sync(kFull, p, src);
     }
-    if (lane == 0 && carry_row >= 0) atomicAdd(y + carry_row, carry);
+    float p[kCooRun];
+#pragma unroll
+    for (int i = 0; i < kCooRun; ++i) p[i] = v[i] * ldx(x, c[i]);
+    const int first = r[0];
+    int cur = r[0];
+    float s = p[0];
+#pragma unroll
+    for (int i = 1; i < kCooRun; ++i) {
+      if (r[i] < 0) break;
+      if (r[i] != cur) {
+        coo_flush(y, cur, s, cur == first);
+        cur = r[i];
+        s = 0.f;
+      }
+      s += p[i];
+    }
+    coo_flush(y, cur, s, true);  // the run's last row may continue
   }
 }
 
@@ -254,8 +257,7 @@ void zero_y(sfg_context* ctx, float* y, int64_t m) {
 void spmv_coo(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, bool acc) {
   if (!acc) zero_y(ctx, y, a->m);
   if (a->nnz == 0) return;
-  int64_t chunks = ceil_div(a->nnz, 32 * kCooIters);
-  int grid = (int)std::min<int64_t>(ceil_div(chunks, kBlock / 32), (int64_t)ctx->sms * 16);
+  int grid = stream_grid(ctx, ceil_div(a->nnz, kCooRun), kBlock, 1, 8);
   SFG_LAUNCH(k_spmv_coo, grid, kBlock, 0, ctx->stream, a->row, a->idx,
              static_cast<const float*>(a->val), x, y, a->nnz);
 }

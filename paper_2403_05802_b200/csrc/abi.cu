@@ -162,6 +162,7 @@ int sfg_context_destroy(sfg_context* ctx) {
   return guard([&] {
     if (!ctx) return;
     if (ctx->scratch) sfg::dfree(ctx, ctx->scratch);
+    if (ctx->status) sfg::dfree(ctx, ctx->status);
     cudaStreamSynchronize(ctx->stream);
     cudaFreeHost(ctx->pinned);
     delete ctx;

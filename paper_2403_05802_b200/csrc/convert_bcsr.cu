@@ -28,7 +28,7 @@ namespace sfg {
 namespace {
 
 constexpr int kBlock = 256;
-constexpr int kMaxWords = 40 * 1024;  // 160 KB bitmap => <= 1.31 M block columns per row span
+constexpr int kMaxWords = 24 * 1024;  // 96 KB bitmap (+96 KB prefix) => <= 786K block columns
 
 __global__ void __launch_bounds__(kBlock) k_brow_ptr(const int32_t* __restrict__ row, int64_t nnz,
                                                       int32_t r, int32_t nbr,
@@ -240,12 +240,11 @@ sfg_tensor* coo_to_bcsr(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_
   SFG_LAUNCH(k_brow_ptr, stream_grid(ctx, nnz, kBlock, 1, 8), kBlock, 0, ctx->stream, s->row, nnz,
              (int32_t)r, nbr, bptr);
   int tiles = (int)ceil_div(nbr, kTile);
-  char* scr = static_cast<char*>(scratch(ctx, (size_t)tiles * 8 + 64));
-  auto* status = reinterpret_cast<unsigned long long*>(scr);
-  auto* tail = reinterpret_cast<int32_t*>(scr + (size_t)tiles * 8);
+  auto* status = lookback_status(ctx, tiles);
+  auto* tail = static_cast<int32_t*>(scratch(ctx, 64));
   SFG_CUDA(cudaMemsetAsync(tail, 0, 16, ctx->stream));
   const size_t smem_count = kMaxWords * 4;
-  const size_t smem_fill = kMaxWords * 8 > 227 * 1024 ? 227 * 1024 : kMaxWords * 8;
+  const size_t smem_fill = kMaxWords * 8;
   static bool attr_set = false;
   if (!attr_set) {
     SFG_CUDA(cudaFuncSetAttribute(k_count_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -156,9 +156,8 @@ sfg_tensor* coo_to_csc(sfg_context* ctx, const sfg_tensor* s) {
   int32_t* cnt = dalloc_n<int32_t>(ctx, n);
   int32_t* cursor = dalloc_n<int32_t>(ctx, n);
   int tiles = (int)ceil_div(n, kTile);
-  char* scr = static_cast<char*>(scratch(ctx, (size_t)tiles * 8 + 64));
-  auto* status = reinterpret_cast<unsigned long long*>(scr);
-  auto* maxcnt = reinterpret_cast<int32_t*>(scr + (size_t)tiles * 8);
+  auto* status = lookback_status(ctx, tiles);
+  auto* maxcnt = static_cast<int32_t*>(scratch(ctx, 64));
   SFG_CUDA(cudaMemsetAsync(cnt, 0, n * sizeof(int32_t), ctx->stream));
   SFG_CUDA(cudaMemsetAsync(maxcnt, 0, sizeof(int32_t), ctx->stream));
   SFG_LAUNCH(k_col_hist, stream_grid(ctx, nnz, kBlock, 4), kBlock, 0, ctx->stream, s->idx, nnz, cnt);

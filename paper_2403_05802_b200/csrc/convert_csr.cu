@@ -283,8 +283,8 @@ sfg_tensor* coo_to_dcsr(sfg_context* ctx, const sfg_tensor* s) {
     return t;
   }
   int tiles = (int)ceil_div(s->nnz, kDcsrTile);
-  auto* status = static_cast<unsigned long long*>(scratch(ctx, (size_t)tiles * 8 + 64));
-  int32_t* nnr_dev = reinterpret_cast<int32_t*>(status + tiles);
+  auto* status = lookback_status(ctx, tiles);
+  int32_t* nnr_dev = static_cast<int32_t*>(scratch(ctx, 64));
   SFG_LAUNCH(k_coo_to_dcsr, tiles, kBlock, 0, ctx->stream, s->row, s->idx,
              static_cast<const float*>(s->val), s->nnz, t->row, t->ptr, t->idx,
              static_cast<float*>(t->val), status, ctx->epoch++, nnr_dev);

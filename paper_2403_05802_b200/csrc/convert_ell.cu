@@ -289,9 +289,8 @@ RowInfo row_info(sfg_context* ctx, const sfg_tensor* s, int64_t min_sum, int32_t
   ri.zcnt = dalloc_n<int32_t>(ctx, m);
   ri.off = dalloc_n<uint32_t>(ctx, m);
   int tiles = (int)ceil_div(m, kScanTile);
-  char* scr = static_cast<char*>(scratch(ctx, (size_t)tiles * 8 + 64));
-  auto* status = reinterpret_cast<unsigned long long*>(scr);
-  auto* tail = reinterpret_cast<int32_t*>(scr + (size_t)tiles * 8);  // [any_zero, nnz_sel, k_max]
+  auto* status = lookback_status(ctx, tiles);
+  auto* tail = static_cast<int32_t*>(scratch(ctx, 64));  // [any_zero, nnz_sel, k_max]
   SFG_CUDA(cudaMemsetAsync(tail, 0, 16, ctx->stream));
   SFG_CUDA(cudaMemsetAsync(ri.zcnt, 0, m * sizeof(int32_t), ctx->stream));
   if (s->nnz == 0) {

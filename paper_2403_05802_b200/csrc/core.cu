@@ -61,6 +61,17 @@ void* scratch(sfg_context* ctx, size_t bytes) {
   return ctx->scratch;
 }
 
+unsigned long long* lookback_status(sfg_context* ctx, size_t words) {
+  if (words > ctx->status_words) {
+    if (ctx->status) dfree(ctx, ctx->status);
+    size_t want = words < 4096 ? 4096 : words + words / 4;
+    ctx->status = dalloc(ctx, want * 8);
+    SFG_CUDA(cudaMemsetAsync(ctx->status, 0, want * 8, ctx->stream));
+    ctx->status_words = want;
+  }
+  return static_cast<unsigned long long*>(ctx->status);
+}
+
 void read_back(sfg_context* ctx, const void* dev, size_t bytes, void* host) {
   if (bytes > 4096) raise(SFG_ERR_INVALID_OPERATION, "read_back too large");
   SFG_CUDA(cudaMemcpyAsync(ctx->pinned, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));

@@ -50,8 +50,10 @@ struct sfg_context {
   cudaStream_t stream = nullptr;
   int sms = 148;
   int64_t* pinned = nullptr;   // small host scratch for size read-backs
-  void* scratch = nullptr;     // device scratch (look-back status words, counters)
+  void* scratch = nullptr;     // device scratch (counters, histograms, flags)
   size_t scratch_bytes = 0;
+  void* status = nullptr;      // look-back status words only
+  size_t status_words = 0;
   uint32_t epoch = 1;          // look-back status generation
 };
 
@@ -94,8 +96,13 @@ T* dalloc_n(sfg_context* ctx, int64_t n) {
   return static_cast<T*>(dalloc(ctx, static_cast<size_t>(n > 0 ? n : 1) * sizeof(T)));
 }
 
-// Scratch with at least `bytes` bytes (grows; contents undefined).
+// Scratch with at least `bytes` bytes (grows; contents undefined). Never
+// used for look-back status words.
 void* scratch(sfg_context* ctx, size_t bytes);
+// Dedicated look-back status words (>= `words`), zero-filled whenever the
+// buffer is (re)allocated and written only by look-back kernels, so a stale
+// word always carries an older epoch than the launch reading it.
+unsigned long long* lookback_status(sfg_context* ctx, size_t words);
 // Copy `count` int64 values device->host through pinned memory and sync.
 void read_back(sfg_context* ctx, const void* dev, size_t bytes, void* host);
 

@@ -259,9 +259,8 @@ void radix_sort(sfg_context* ctx, uint64_t* keys, uint32_t* pay, int64_t n, int 
   if (n > 1 && passes > 0) {
     int tiles = (int)ceil_div(n, kTile);
     size_t status_bytes = (size_t)tiles * 256 * 8;
-    char* scr = static_cast<char*>(scratch(ctx, status_bytes + kMaxPasses * 256 * 4 + 256));
-    auto* status = reinterpret_cast<unsigned long long*>(scr);
-    auto* hist = reinterpret_cast<uint32_t*>(scr + status_bytes);
+    auto* status = lookback_status(ctx, status_bytes / 8);
+    auto* hist = static_cast<uint32_t*>(scratch(ctx, kMaxPasses * 256 * 4 + 256));
     SFG_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * 256 * 4, ctx->stream));
     SFG_LAUNCH(k_global_hist, stream_grid(ctx, n, kBlock, 8, 4), kBlock, 0, ctx->stream, keys, n,
                passes, hist);
@@ -298,9 +297,8 @@ void sort_u64_keys(sfg_context* ctx, uint64_t* keys, int64_t n, int key_bits, ui
 int64_t unique_positions(sfg_context* ctx, const uint64_t* keys, int64_t n, int32_t* pos) {
   if (n == 0) return 0;
   int tiles = (int)ceil_div(n, kUTile);
-  char* scr = static_cast<char*>(scratch(ctx, (size_t)tiles * 8 + 64));
-  auto* status = reinterpret_cast<unsigned long long*>(scr);
-  auto* tail = reinterpret_cast<unsigned long long*>(scr + (size_t)tiles * 8);
+  auto* status = lookback_status(ctx, tiles);
+  auto* tail = static_cast<unsigned long long*>(scratch(ctx, 64));
   SFG_CUDA(cudaMemsetAsync(tail, 0xff, 16, ctx->stream));
   SFG_LAUNCH(k_unique_pos, tiles, kBlock, 0, ctx->stream, keys, n, pos, status, ctx->epoch++,
              reinterpret_cast<int32_t*>(tail + 1), tail);
@@ -340,9 +338,8 @@ sfg_tensor* sort_coo(sfg_context* ctx, int64_t m, int64_t n, int64_t nnz, const 
   int32_t* pos = dalloc_n<int32_t>(ctx, nnz);
   // unique_positions also records the smallest duplicated key
   int tiles = (int)ceil_div(nnz, kUTile);
-  char* scr = static_cast<char*>(scratch(ctx, (size_t)tiles * 8 + 64));
-  auto* status = reinterpret_cast<unsigned long long*>(scr);
-  auto* tail = reinterpret_cast<unsigned long long*>(scr + (size_t)tiles * 8);
+  auto* status = lookback_status(ctx, tiles);
+  auto* tail = static_cast<unsigned long long*>(scratch(ctx, 64));
   SFG_CUDA(cudaMemsetAsync(tail, 0xff, 16, ctx->stream));
   SFG_LAUNCH(k_unique_pos, tiles, kBlock, 0, ctx->stream, kres, nnz, pos, status, ctx->epoch++,
              reinterpret_cast<int32_t*>(tail + 1), tail);

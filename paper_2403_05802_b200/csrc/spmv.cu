@@ -22,34 +22,63 @@ constexpr int kBlock = 256;
 __device__ __forceinline__ float ldx(const float* __restrict__ x, int c) { return __ldg(x + c); }
 
 // ---------------------------------------------------------------- CSR
-// G lanes per row (G = power of two, 2..32): lanes stride the row's
-// entries (coalesced idx/val streams), gather x through the read-only
-// path, then reduce inside the lane group with shuffles.
-template <int G>
+// G lanes per row (G = power of two, 2..32), R consecutive rows per lane
+// group per iteration: the group loads the R+1 row pointers at once, then
+// walks the R rows side by side so every lane keeps R independent
+// col -> x gathers in flight (the gathers, not HBM, bound CSR SpMV on random
+// columns). Entries are strided by G inside a row (coalesced idx/val
+// streams); partial sums reduce inside the lane group with shuffles.
+template <int G, int R>
 __global__ void __launch_bounds__(kBlock) k_spmv_csr(const int32_t* __restrict__ ptr,
                                                       const int32_t* __restrict__ col,
                                                       const float* __restrict__ val,
                                                       const float* __restrict__ x,
                                                       float* __restrict__ y, int32_t m, int acc) {
+  static_assert(G >= R + 1 || G == 32, "pointer load needs R+1 lanes");
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
-  const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << (lane & ~(G - 1)));
+  const int gbase = lane & ~(G - 1);
+  const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << gbase);
   const int64_t groups = (int64_t)gridDim.x * (blockDim.x / G);
-  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; r < m; r += groups) {
-    int s = __ldg(ptr + r), e = __ldg(ptr + r + 1);
-    float sum = 0.f;
-    int k = s + gl;
-    // two independent gathers in flight per lane
-    for (; k + G < e; k += 2 * G) {
-      int c0 = ld_stream(col + k), c1 = ld_stream(col + k + G);
-      float v0 = ld_stream(val + k), v1 = ld_stream(val + k + G);
-      sum = fmaf(v0, ldx(x, c0), sum);
-      sum = fmaf(v1, ldx(x, c1), sum);
-    }
-    if (k < e) sum = fmaf(ld_stream(val + k), ldx(x, ld_stream(col + k)), sum);
+  for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; g * R < m; g += groups) {
+    const int64_t r0 = g * R;
+    const int nrows = (int)(m - r0 < R ? m - r0 : R);
+    int myp = gl <= nrows ? __ldg(ptr + r0 + gl) : 0;
+    int s[R], e[R];
+    float sum[R];
 #pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(gmask, sum, o);
-    if (gl == 0) y[r] = acc ? y[r] + sum : sum;
+    for (int i = 0; i < R; ++i) {
+      s[i] = __shfl_sync(gmask, myp, gbase + i) + gl;
+      e[i] = i < nrows ? __shfl_sync(gmask, myp, gbase + i + 1) : 0;
+      sum[i] = 0.f;
+    }
+    int len = 0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) len = max(len, e[i] - s[i] + gl);
+    for (int t = 0; t < len; t += G) {
+      int c[R];
+      float v[R];
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        bool ok = s[i] + t < e[i];
+        c[i] = ok ? ld_stream(col + s[i] + t) : 0;
+        v[i] = ok ? ld_stream(val + s[i] + t) : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+        if (s[i] + t < e[i]) sum[i] = fmaf(v[i], ldx(x, c[i]), sum[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) sum[i] += __shfl_xor_sync(gmask, sum[i], o);
+    if (gl < nrows) {
+      float out = sum[0];
+#pragma unroll
+      for (int i = 1; i < R; ++i)
+        if (gl == i) out = sum[i];
+      y[r0 + gl] = acc ? y[r0 + gl] + out : out;
+    }
   }
 }
 
@@ -238,15 +267,16 @@ int pick_group(double avg) {
 void spmv_csr(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, bool acc) {
   if (a->m == 0) return;
   int g = pick_group(a->m ? double(a->nnz) / double(a->m) : 0);
-  int rows_per_cta = kBlock / g;
-  int grid = (int)std::min<int64_t>(ceil_div(a->m, rows_per_cta), (int64_t)ctx->sms * 16);
+  const int R = 4;
+  int grid = (int)std::min<int64_t>(ceil_div(a->m, (int64_t)(kBlock / g) * R), (int64_t)ctx->sms * 16);
+  if (grid < 1) grid = 1;
   auto v = static_cast<const float*>(a->val);
   switch (g) {
-    case 2: SFG_LAUNCH(k_spmv_csr<2>, grid, kBlock, 0, ctx->stream, a->ptr, a->idx, v, x, y, (int)a->m, acc); break;
-    case 4: SFG_LAUNCH(k_spmv_csr<4>, grid, kBlock, 0, ctx->stream, a->ptr, a->idx, v, x, y, (int)a->m, acc); break;
-    case 8: SFG_LAUNCH(k_spmv_csr<8>, grid, kBlock, 0, ctx->stream, a->ptr, a->idx, v, x, y, (int)a->m, acc); break;
-    case 16: SFG_LAUNCH(k_spmv_csr<16>, grid, kBlock, 0, ctx->stream, a->ptr, a->idx, v, x, y, (int)a->m, acc); break;
-    default: SFG_LAUNCH(k_spmv_csr<32>, grid, kBlock, 0, ctx->stream, a->ptr, a->idx, v, x, y, (int)a->m, acc); break;
+    case 2: SFG_LAUNCH((k_spmv_csr<2, 1>), (int)std::min<int64_t>(ceil_div(a->m, kBlock / 2), (int64_t)ctx->sms * 16), kBlock, 0, ctx->stream, a->ptr, a->idx, v, x, y, (int)a->m, acc); break;
+    case 4: SFG_LAUNCH((k_spmv_csr<4, 3>), (int)std::min<int64_t>(ceil_div(a->m, (kBlock / 4) * 3), (int64_t)ctx->sms * 16), kBlock, 0, ctx->stream, a->ptr, a->idx, v, x, y, (int)a->m, acc); break;
+    case 8: SFG_LAUNCH((k_spmv_csr<8, R>), grid, kBlock, 0, ctx->stream, a->ptr, a->idx, v, x, y, (int)a->m, acc); break;
+    case 16: SFG_LAUNCH((k_spmv_csr<16, R>), grid, kBlock, 0, ctx->stream, a->ptr, a->idx, v, x, y, (int)a->m, acc); break;
+    default: SFG_LAUNCH((k_spmv_csr<32, R>), grid, kBlock, 0, ctx->stream, a->ptr, a->idx, v, x, y, (int)a->m, acc); break;
   }
 }
 

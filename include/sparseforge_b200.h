@@ -185,6 +185,10 @@ int sfgx_gen_rmat(sfg_context* ctx, uint64_t seed, int32_t scale, int64_t edges,
 int sfgx_gen_hypersparse(sfg_context* ctx, uint64_t seed, int64_t rows, int64_t cols,
                          int64_t draws, sfg_tensor** out);
 int sfgx_gen_dense(sfg_context* ctx, uint64_t seed, int64_t count, float* out);
+/* Config 4: BCSR(r,c) generated directly; block present with probability
+ * thresh / 2^32; value_dtype SFG_F32 or SFG_BF16. */
+int sfgx_gen_block_sparse(sfg_context* ctx, uint64_t seed, int64_t rows, int64_t cols, int32_t r,
+                          int32_t c, uint32_t thresh, int32_t value_dtype, sfg_tensor** out);
 /* Number of this library's kernels launched so far (bench gpu_launches). */
 int64_t sfgx_launch_count(void);
 /* Device buffers and stream-ordered copies for callers without a CUDA

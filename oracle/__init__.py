@@ -226,6 +226,13 @@ class Port(_Base):
                                                  C.c_int64(draws), C.byref(h)))
         return _Coo(self.lib, h, self.prefix, (m, n))
 
+    def gen_block_sparse(self, seed, m, n, r, c, density):
+        h = C.c_void_p()
+        thresh = min(int(density * 2 ** 32), 2 ** 32 - 1)
+        self._check(self.lib.sfo_gen_block_sparse(C.c_uint64(seed), C.c_int64(m), C.c_int64(n), C.c_int64(r),
+                                                  C.c_int64(c), C.c_uint32(thresh), C.byref(h)))
+        return _Coo(self.lib, h, self.prefix, (m, n))
+
     def gen_dense(self, seed, count):
         out = np.empty(count, np.float64)
         self.lib.sfo_gen_dense(C.c_uint64(seed), C.c_int64(count), _pf64(out))

@@ -695,6 +695,33 @@ int sfo_gen_hypersparse(uint64_t seed, int64_t m, int64_t n, int64_t draws, sfo_
   return SFO_OK;
 }
 
+/* COO expansion of the config-4 block-sparse matrix, (row, col)-sorted. */
+int sfo_gen_block_sparse(uint64_t seed, int64_t m, int64_t n, int64_t r, int64_t c, uint32_t thresh,
+                         sfo_coo** out) {
+  int64_t nbr = (m - 1) / r + 1, nbc = (n - 1) / c + 1, cnt = 0;
+  for (int64_t br = 0; br < nbr; ++br)
+    for (int64_t bc = 0; bc < nbc; ++bc)
+      if (sfg_block_present(seed, (uint32_t)br, (uint32_t)bc, thresh)) {
+        int64_t rows = (br + 1) * r <= m ? r : m - br * r, cols = (bc + 1) * c <= n ? c : n - bc * c;
+        cnt += rows * cols;
+      }
+  sfo_coo* t = coo_alloc(m, n, cnt);
+  int64_t k = 0;
+  for (int64_t row = 0; row < m; ++row) {
+    int64_t br = row / r;
+    for (int64_t bc = 0; bc < nbc; ++bc) {
+      if (!sfg_block_present(seed, (uint32_t)br, (uint32_t)bc, thresh)) continue;
+      for (int64_t col = bc * c; col < (bc + 1) * c && col < n; ++col) {
+        t->row[k] = row;
+        t->col[k] = col;
+        t->val[k++] = (double)sfg_coord_value(seed, (uint32_t)row, (uint32_t)col);
+      }
+    }
+  }
+  *out = t;
+  return SFO_OK;
+}
+
 void sfo_gen_dense(uint64_t seed, int64_t count, double* out) {
   for (int64_t i = 0; i < count; ++i)
     out[i] = (double)sfg_dense_value(sfg_hash3(seed, (uint64_t)i, 0x77));

@@ -85,6 +85,8 @@ int sfo_gen_uniform(uint64_t seed, int64_t m, int64_t n, int per_row, sfo_coo** 
 int sfo_gen_rmat(uint64_t seed, int scale, int64_t edges, sfo_coo** out);
 int sfo_gen_hypersparse(uint64_t seed, int64_t m, int64_t n, int64_t draws, sfo_coo** out);
 void sfo_gen_dense(uint64_t seed, int64_t count, double* out);
+int sfo_gen_block_sparse(uint64_t seed, int64_t m, int64_t n, int64_t r, int64_t c, uint32_t thresh,
+                         sfo_coo** out);
 
 #ifdef __cplusplus
 }

@@ -124,6 +124,7 @@ def load():
         "sfgx_gen_rmat": (C.c_int, [vp, C.c_uint64, i32, i64, pp]),
         "sfgx_gen_hypersparse": (C.c_int, [vp, C.c_uint64, i64, i64, i64, pp]),
         "sfgx_gen_dense": (C.c_int, [vp, C.c_uint64, i64, vp]),
+        "sfgx_gen_block_sparse": (C.c_int, [vp, C.c_uint64, i64, i64, i32, i32, u32, i32, pp]),
         "sfgx_launch_count": (i64, []),
         "sfgx_device_alloc": (C.c_int, [vp, i64, pp]),
         "sfgx_device_free": (C.c_int, [vp, vp]),
@@ -381,6 +382,12 @@ class Context:
     def gen_hypersparse(self, seed, m, n, draws) -> Tensor:
         h = C.c_void_p()
         _check(self.lib.sfgx_gen_hypersparse(self.h, seed, m, n, draws, C.byref(h)))
+        return Tensor(self, h)
+
+    def gen_block_sparse(self, seed, m, n, r, c, density, value_dtype=F32) -> Tensor:
+        h = C.c_void_p()
+        thresh = min(int(density * 2 ** 32), 2 ** 32 - 1)
+        _check(self.lib.sfgx_gen_block_sparse(self.h, seed, m, n, r, c, thresh, value_dtype, C.byref(h)))
         return Tensor(self, h)
 
     def gen_dense(self, seed, count, out_ptr):

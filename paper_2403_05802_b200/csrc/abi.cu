@@ -499,6 +499,16 @@ int sfgx_gen_hypersparse(sfg_context* ctx, uint64_t seed, int64_t rows, int64_t 
   });
 }
 
+int sfgx_gen_block_sparse(sfg_context* ctx, uint64_t seed, int64_t rows, int64_t cols, int32_t r,
+                          int32_t c, uint32_t thresh, int32_t value_dtype, sfg_tensor** out) {
+  return guard([&] {
+    require(ctx && out && rows > 0 && cols > 0 && r > 0 && c > 0 && rows < INT32_MAX && cols < INT32_MAX,
+            SFG_ERR_INVALID_OPERATION, "bad block-sparse shape");
+    require(value_dtype == SFG_F32 || value_dtype == SFG_BF16, SFG_ERR_INVALID_OPERATION, "bad dtype");
+    *out = sfg::gen_block_sparse(ctx, seed, rows, cols, r, c, thresh, value_dtype);
+  });
+}
+
 int sfgx_gen_dense(sfg_context* ctx, uint64_t seed, int64_t count, float* out) {
   return guard([&] { sfg::gen_dense(ctx, seed, count, out); });
 }

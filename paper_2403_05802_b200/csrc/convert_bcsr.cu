@@ -215,6 +215,12 @@ __global__ void __launch_bounds__(kBlock) k_fill_blocks(
 
 }  // namespace
 
+void scan_counts(sfg_context* ctx, const int32_t* cnt, int64_t n, int32_t* ptr) {
+  int tiles = (int)ceil_div(n, kTile);
+  auto* status = lookback_status(ctx, tiles);
+  SFG_LAUNCH(k_scan_i32, tiles, kBlock, 0, ctx->stream, cnt, (int32_t)n, ptr, status, ctx->epoch++);
+}
+
 sfg_tensor* coo_to_bcsr(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_t c, int dtype) {
   const int64_t m = s->m, n = s->n, nnz = s->nnz;
   sfg_tensor* t = new_tensor(ctx, SFG_BCSR, m, n);

@@ -110,19 +110,33 @@ __global__ void __launch_bounds__(kBlock) k_row_scan(const int32_t* __restrict__
                                                       uint32_t epoch, ScanOut* __restrict__ out) {
   __shared__ uint32_t smem[34];
   __shared__ uint32_t slot;
-  const int64_t r0 = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  // The tile's row pointers / zero counts / outputs go through shared memory
+  // (skewed by one word per 16 so the per-thread runs are conflict-free), so
+  // every global access is coalesced.
+  __shared__ int32_t sp[kScanTile + kScanTile / 16 + 2];
+  __shared__ int32_t sz[kScanTile + kScanTile / 16 + 1];
+  auto sk = [](int i) { return i + (i >> 4); };
+  const int64_t tile0 = (int64_t)blockIdx.x * kScanTile;
+  for (int i = threadIdx.x; i <= kScanTile; i += kBlock) {
+    int64_t r = tile0 + i;
+    sp[sk(i)] = r <= m ? __ldg(ptr + r) : 0;
+    if (i < kScanTile) sz[sk(i)] = r < m ? __ldg(zcnt + r) : 0;
+  }
+  __syncthreads();
+  const int t0 = threadIdx.x * kScanItems;
+  const int64_t r0 = tile0 + t0;
   uint32_t cnt[kScanItems];
   uint32_t selmask = 0, sum = 0;
   int32_t kmax = 0;
-  int32_t p_lo = r0 < m ? __ldg(ptr + r0) : 0;
+  int32_t p_lo = sp[sk(t0)];
 #pragma unroll
   for (int i = 0; i < kScanItems; ++i) {
     int64_t r = r0 + i;
     cnt[i] = 0;
     if (r < m) {
-      int32_t p_hi = __ldg(ptr + r + 1);
+      int32_t p_hi = sp[sk(t0 + i + 1)];
       int32_t c = p_hi - p_lo;
-      int32_t nz = has_zeros ? c - __ldg(zcnt + r) : c;
+      int32_t nz = has_zeros ? c - sz[sk(t0 + i)] : c;
       if (totals) totals[r] = nz;
       bool sel = (int64_t)nz >= min_sum;
       if (sel) {
@@ -141,63 +155,65 @@ __global__ void __launch_bounds__(kBlock) k_row_scan(const int32_t* __restrict__
   if ((threadIdx.x & 31) == 0 && kmax > 0) atomicMax(&out->k_max, kmax);
   uint32_t tp = lookback_prefix(status, epoch, blockIdx.x, total, &slot);
   uint32_t sel_before = tp + excl;
-  int32_t p = r0 < m ? __ldg(ptr + r0) : 0;
+  int32_t p = sp[sk(t0)];
+  uint32_t* so = reinterpret_cast<uint32_t*>(sz);  // reuse: per-row offsets
+  __syncthreads();
 #pragma unroll
   for (int i = 0; i < kScanItems; ++i) {
-    int64_t r = r0 + i;
-    if (r < m) {
-      bool sel = (selmask >> i) & 1u;
-      off[r] = sel ? (kSelBit | (uint32_t)(p - sel_before)) : sel_before;
-      if (sel) sel_before += cnt[i];
-      p += cnt[i];
-    }
+    bool sel = (selmask >> i) & 1u;
+    so[sk(t0 + i)] = sel ? (kSelBit | (uint32_t)(p - sel_before)) : sel_before;
+    if (sel) sel_before += cnt[i];
+    p += cnt[i];
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kScanTile; i += kBlock)
+    if (tile0 + i < m) off[tile0 + i] = so[sk(i)];
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out->nnz_sel = (int32_t)(tp + total);
 }
 
 // ---------------------------------------------------------------- 3. split
+constexpr int kSplitRun = 8;
+
 __global__ void __launch_bounds__(kBlock) k_split(
     const int32_t* __restrict__ row, const int32_t* __restrict__ col,
     const float* __restrict__ val, int64_t nnz, const uint32_t* __restrict__ off,
     int32_t* __restrict__ srow, int32_t* __restrict__ scol, float* __restrict__ sval,
     int32_t* __restrict__ rrow, int32_t* __restrict__ rcol, float* __restrict__ rval) {
-  const int64_t nvec = (nnz + 3) >> 2;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec;
+  // kSplitRun consecutive entries per thread; row, col and val are all
+  // loaded up front (independent 128-bit loads), then one `off` lookup per
+  // distinct row of the run (runs are mostly a single row), then stores.
+  constexpr int R = kSplitRun;
+  const int64_t nrun = (nnz + R - 1) / R;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nrun;
        v += (int64_t)gridDim.x * blockDim.x) {
-    int64_t e0 = v << 2;
-    int r[4];
-    uint32_t o[4];
-    bool full = e0 + 4 <= nnz;
-    if (full) {
-      int4 rr = ld_stream(reinterpret_cast<const int4*>(row + e0));
-      r[0] = rr.x; r[1] = rr.y; r[2] = rr.z; r[3] = rr.w;
+    int64_t e0 = v * R;
+    int r[R], c[R];
+    float x[R];
+    uint32_t o[R];
+    if (e0 + R <= nnz) {
+#pragma unroll
+      for (int q = 0; q < R / 4; ++q) {
+        int4 rr = ld_stream(reinterpret_cast<const int4*>(row + e0) + q);
+        int4 cc = ld_stream(reinterpret_cast<const int4*>(col + e0) + q);
+        float4 vv = ld_stream(reinterpret_cast<const float4*>(val + e0) + q);
+        r[4 * q] = rr.x; r[4 * q + 1] = rr.y; r[4 * q + 2] = rr.z; r[4 * q + 3] = rr.w;
+        c[4 * q] = cc.x; c[4 * q + 1] = cc.y; c[4 * q + 2] = cc.z; c[4 * q + 3] = cc.w;
+        x[4 * q] = vv.x; x[4 * q + 1] = vv.y; x[4 * q + 2] = vv.z; x[4 * q + 3] = vv.w;
+      }
     } else {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) r[i] = e0 + i < nnz ? row[e0 + i] : -1;
-    }
-    bool need = rrow != nullptr;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      o[i] = r[i] >= 0 ? __ldg(off + r[i]) : 0u;
-      need |= r[i] >= 0 && (o[i] & kSelBit);
-    }
-    if (!need) continue;
-    int c[4];
-    float x[4];
-    if (full) {
-      int4 cc = ld_stream(reinterpret_cast<const int4*>(col + e0));
-      float4 vv = ld_stream(reinterpret_cast<const float4*>(val + e0));
-      c[0] = cc.x; c[1] = cc.y; c[2] = cc.z; c[3] = cc.w;
-      x[0] = vv.x; x[1] = vv.y; x[2] = vv.z; x[3] = vv.w;
-    } else {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        c[i] = e0 + i < nnz ? col[e0 + i] : 0;
-        x[i] = e0 + i < nnz ? val[e0 + i] : 0.f;
+      for (int i = 0; i < R; ++i) {
+        bool ok = e0 + i < nnz;
+        r[i] = ok ? row[e0 + i] : -1;
+        c[i] = ok ? col[e0 + i] : 0;
+        x[i] = ok ? val[e0 + i] : 0.f;
       }
     }
+    o[0] = r[0] >= 0 ? __ldg(off + r[0]) : 0u;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 1; i < R; ++i) o[i] = r[i] == r[i - 1] ? o[i - 1] : (r[i] >= 0 ? __ldg(off + r[i]) : 0u);
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
       if (r[i] < 0) continue;
       int64_t pos = e0 + i - (int64_t)(o[i] & ~kSelBit);
       if (o[i] & kSelBit) {
@@ -354,7 +370,7 @@ void decompose_rows(sfg_context* ctx, const sfg_tensor* s, int64_t min_sum, sfg_
   sfg_tensor* a = coo_part(ctx, s->m, s->n, ri.nnz_sel);
   sfg_tensor* b = coo_part(ctx, s->m, s->n, s->nnz - ri.nnz_sel);
   if (s->nnz)
-    SFG_LAUNCH(k_split, stream_grid(ctx, ceil_div(s->nnz, 4), kBlock, 1, 8), kBlock, 0, ctx->stream,
+    SFG_LAUNCH(k_split, stream_grid(ctx, ceil_div(s->nnz, kSplitRun), kBlock, 1, 8), kBlock, 0, ctx->stream,
                s->row, s->idx, static_cast<const float*>(s->val), s->nnz, ri.off, a->row, a->idx,
                static_cast<float*>(a->val), b->row, b->idx, static_cast<float*>(b->val));
   free_row_info(ctx, ri);
@@ -376,7 +392,7 @@ sfg_tensor* coo_to_hyb(sfg_context* ctx, const sfg_tensor* s, int64_t min_sum) {
   h->threshold = min_sum;
   h->part[1] = coo_part(ctx, s->m, s->n, ri.nnz_sel);
   if (s->nnz)
-    SFG_LAUNCH(k_split, stream_grid(ctx, ceil_div(s->nnz, 4), kBlock, 1, 8), kBlock, 0, ctx->stream,
+    SFG_LAUNCH(k_split, stream_grid(ctx, ceil_div(s->nnz, kSplitRun), kBlock, 1, 8), kBlock, 0, ctx->stream,
                s->row, s->idx, static_cast<const float*>(s->val), s->nnz, ri.off, h->part[1]->row,
                h->part[1]->idx, static_cast<float*>(h->part[1]->val), nullptr, nullptr, nullptr);
   h->part[0] = ell_from(ctx, s, ri, true);

@@ -153,5 +153,7 @@ sfg_tensor* gen_uniform(sfg_context* ctx, uint64_t seed, int64_t m, int64_t n, i
 sfg_tensor* gen_from_keys(sfg_context* ctx, uint64_t seed, int kind, int scale, int64_t m,
                           int64_t n, int64_t draws);
 void gen_dense(sfg_context* ctx, uint64_t seed, int64_t count, float* out);
+sfg_tensor* gen_block_sparse(sfg_context* ctx, uint64_t seed, int64_t m, int64_t n, int64_t r,
+                             int64_t c, uint32_t thresh, int dtype);
 
 }  // namespace sfg

@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(kBlock) k_spmv_ell(const int32_t* __restrict__
 // lies strictly inside its run (no other lane can touch it); the lane's
 // first and last rows may continue in a neighbouring lane or warp and use
 // atomicAdd. y must be zeroed (or hold a partial result) beforehand.
-constexpr int kCooRun = 8;
+constexpr int kCooRun = 16;
 
 __device__ __forceinline__ void coo_flush(float* __restrict__ y, int r, float s, bool shared) {
   if (shared) atomicAdd(y + r, s);

@@ -104,3 +104,13 @@ SFG_HD float sfg_coord_value(uint64_t seed, uint32_t r, uint32_t c) {
 }
 
 #endif /* SFG_SYNTH_H */
+
+/* Config 4: block (br, bc) of a block-sparse matrix is present with
+ * probability p = thresh / 2^32; values are coordinate-hashed like the other
+ * generators, so the block-sparse matrix equals its COO expansion. */
+#ifndef SFG_SYNTH_BLOCKS
+#define SFG_SYNTH_BLOCKS
+SFG_HD int sfg_block_present(uint64_t seed, uint32_t br, uint32_t bc, uint32_t thresh) {
+  return (uint32_t)(sfg_hash3(seed ^ 0xB10CB10Cull, br, bc) >> 32) < thresh;
+}
+#endif

@@ -113,3 +113,18 @@ def test_bcsr_conversion_throughput_scale(ctx, port):
         d, p = ctx.from_coo(4096, 4096, rows, cols, vals), port.from_coo(4096, 4096, rows, cols, vals)
         assert_same_materialized(ctx.convert(d, f"BCSR({r_},{c_})").download(),
                                  port.convert(p, "BCSR", r_, c_).download(), (r_, c_))
+
+
+@pytest.mark.parametrize("rc", [(4, 4), (16, 16), (3, 5)])
+@pytest.mark.parametrize("shape", [(512, 512), (100, 77)])
+def test_block_sparse_generator_equals_conversion(ctx, port, rc, shape):
+    """Config-4 input generated directly as BCSR == convert(COO expansion)."""
+    import paper_2403_05802_b200 as sfg
+    m, n = shape
+    d = ctx.gen_block_sparse(9, m, n, rc[0], rc[1], 0.1).download()
+    p = port.gen_block_sparse(9, m, n, rc[0], rc[1], 0.1)
+    assert_same_materialized(d, port.convert(p, "BCSR", *rc).download(), (rc, shape))
+    db = ctx.gen_block_sparse(9, m, n, rc[0], rc[1], 0.1, value_dtype=sfg.BF16).download()
+    ora = port.convert(p, "BCSR", *rc).download()
+    ora.values = bf16_round(ora.values)
+    assert_same_materialized(db, ora, "bf16")

@@ -2,20 +2,23 @@
 """Benchmark of the B200 sparse hot path (BASELINE.json north star).
 
 A step = one pass of the hot path over one synthetic matrix resident in HBM:
-canonical (row-sorted) COO -> format conversion -> SpMV, i.e. the reference's
-convert_structure + materialize + run_kernel (planner.hpp:261, storage.hpp:97,
-kernel.hpp:236). Default workload: BASELINE config 2 (hybrid ELL+COO
-conversion + SpMV on R-MAT scale 22, edge factor 16, threshold T=8).
+canonical (row-sorted) COO -> format conversion -> SpMV/SpMM, i.e. the
+reference's convert_structure + materialize + run_kernel (planner.hpp:261,
+storage.hpp:97, kernel.hpp:236). Default workload: BASELINE config 2
+(hybrid ELL+COO conversion + SpMV on R-MAT scale 22, edge factor 16, T=8).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1|2|3]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5]
                   [--impl ours|reference]
 
 Prints ONE JSON line (rank 0). value = nnz converted+multiplied per second
-over all ranks (Mnnz/s). `e2e` runs the same step through the C-ABI with
-host buffers (from_coo from pinned host arrays, SpMV with host x / host y).
-`roofline` = dominant kernel's algorithmic bytes / CUDA-event time vs the
-measured HBM copy peak. `cpu_baseline` = the unmodified reference (oracle/_ref)
-on a bounded row-block sample, on this host's cores.
+over all ranks (Mnnz/s; config 4, which has no conversion in the step, is
+reported in GFLOP/s). `e2e` runs the same step through the C-ABI with host
+buffers (from_coo from pinned host arrays, SpMV with host x / host y).
+`roofline` = dominant kernel family's algorithmic bytes / CUDA-event time vs
+the measured HBM copy peak. `cpu_baseline` / --impl reference = the
+unmodified reference (oracle/_ref) on a bounded row-block sample.
+N > 1 (torchrun): nnz-balanced row blocks of a weak-scaled matrix (R-MAT
+scale 22 + log2 N), y reassembled with an NCCL all-gather.
 """
 from __future__ import annotations
 
@@ -23,8 +26,8 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
+import threading
 import time
 
 import numpy as np
@@ -33,7 +36,6 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "SpMV/SpMM GFLOP/s + achieved HBM GB/s; format conversion Mnnz/s"
-UNIT = "Mnnz/s"
 
 
 def load_peaks():
@@ -47,123 +49,259 @@ def load_peaks():
 
 # ----------------------------------------------------------------- workloads
 class Workload:
-    """Defines setup (device-resident canonical COO + dense operand), the
-    step, and the algorithmic bytes of each kernel family in the step."""
-
-    name = ""
+    """setup() builds the device-resident input; step() is one pass of the
+    path; kernels() lists the kernel families timed for the roofline as
+    (name, fn, algorithmic bytes, flops)."""
+    unit = "Mnnz/s"
     fmt = ""
+    has_cpu_sample = False
 
-    def __init__(self, args, rank, world):
-        self.args, self.rank, self.world = args, rank, world
+    def __init__(self, sfg, ctx, rank, world):
+        self.sfg, self.ctx, self.rank, self.world = sfg, ctx, rank, world
+        self.info = {}
 
-    # algorithmic bytes (SURVEY.md §8d): each array read once, written once
+    def rows_block(self, glob):
+        """This rank's nnz-balanced row block."""
+        if self.world == 1:
+            self.bounds = [0, glob.shape[0]]
+            return glob
+        self.bounds = self.ctx.row_partition(glob, self.world)
+        return self.ctx.slice_rows(glob, self.bounds[self.rank], self.bounds[self.rank + 1])
+
+    def work_units(self):
+        return self.nnz
+
+    def describe(self):
+        return self.__doc__.strip()
+
+
+class SpmvWorkload(Workload):
+    """conversion to self.fmt + SpMV"""
+
+    def setup_dense(self, torch):
+        m, n = self.coo.shape
+        self.m, self.n = m, n
+        self.nnz = int(self.coo.view().nvals)
+        self.x = torch.empty(n, dtype=torch.float32, device="cuda")
+        self.ctx.gen_dense(3, n, self.x.data_ptr())
+        self.y = torch.zeros(max(m, 1), dtype=torch.float32, device="cuda")
+
+    def step(self):
+        a = self.ctx.convert(self.coo, self.fmt)
+        self.ctx.spmv_device(a, self.x.data_ptr(), self.y.data_ptr())
+
+    def kernels(self):
+        a = self.ctx.convert(self.coo, self.fmt)
+        self.probe(a)
+        self.kept = a
+        return [("convert", lambda: self.ctx.convert(self.coo, self.fmt), self.convert_bytes(), 0),
+                ("spmv", lambda: self.ctx.spmv_device(a, self.x.data_ptr(), self.y.data_ptr()),
+                 self.spmv_bytes(), 2 * self.nnz)]
+
+    def probe(self, a):
+        pass
+
+    def out_rows(self):
+        return self.y
+
+
+class Cfg1(SpmvWorkload):
+    """COO->CSR conversion + CSR SpMV fp32, uniform 2^20 x 2^20, 16/row"""
+    fmt = "CSR"
+    has_cpu_sample = True
+
+    def setup(self, torch):
+        self.coo = self.rows_block(self.ctx.gen_uniform(1, (1 << 20) * self.world, 1 << 20, 16))
+        self.setup_dense(torch)
+
     def convert_bytes(self):
-        raise NotImplementedError
+        return 20 * self.nnz + 4 * (self.m + 1)
 
     def spmv_bytes(self):
-        raise NotImplementedError
+        return 8 * self.nnz + 4 * (self.m + 1) + 4 * self.n + 4 * self.m
 
 
-class Cfg1(Workload):
-    """COO->CSR conversion + CSR SpMV fp32, uniform 2^20 x 2^20, 16/row."""
-    fmt = "CSR"
-
-    def setup(self, ctx):
-        self.scale = 20
-        m = n = 1 << self.scale
-        glob = ctx.gen_uniform(1, m * self.world, n, 16) if self.world > 1 else ctx.gen_uniform(1, m, n, 16)
-        return glob
-
-    def convert_bytes(self, nnz, m, n, info):
-        return 20 * nnz + 4 * (m + 1)  # read row,col,val; write idx,val,ptr
-
-    def spmv_bytes(self, nnz, m, n, info):
-        return 8 * nnz + 4 * (m + 1) + 4 * n + 4 * m
-
-
-class Cfg2(Workload):
-    """Hybrid ELL+COO conversion (decompose T=8) + SpMV, R-MAT s22 ef16."""
+class Cfg2(SpmvWorkload):
+    """hybrid ELL+COO conversion (decompose, T=8) + SpMV, R-MAT scale 22 (+log2 N), edge factor 16"""
     fmt = "HYB(8)"
+    has_cpu_sample = True
 
-    def setup(self, ctx):
+    def setup(self, torch):
         self.scale = 22 + (self.world.bit_length() - 1 if self.world > 1 else 0)
-        return ctx.gen_rmat(7, self.scale, 16 << self.scale)
+        self.coo = self.rows_block(self.ctx.gen_rmat(7, self.scale, 16 << self.scale))
+        self.setup_dense(torch)
 
-    def convert_bytes(self, nnz, m, n, info):
-        # decompose: count pass (row + val) 8*nnz + 4M; split: read 12*nnz,
-        # write COO 12*nnz_sel; ELL: write 8*K*M (+ read 8*nnz_rem for the
-        # remainder entries, counted in the 12*nnz read)
-        return 8 * nnz + 4 * m + 12 * nnz + 12 * info["nnz_coo"] + 8 * info["ell_cells"]
+    def probe(self, a):
+        ell, cpart = a.parts()
+        ev, cv = ell.view(), cpart.view()
+        self.info = {"ell_cells": int(ev.nvals), "ell_k": int(ev.level[0].node_count),
+                     "nnz_coo": int(cv.nvals), "nnz_ell": self.nnz - int(cv.nvals), "threshold": 8}
 
-    def spmv_bytes(self, nnz, m, n, info):
-        return 8 * info["ell_cells"] + 12 * info["nnz_coo"] + 4 * n + 4 * m
+    def convert_bytes(self):
+        i = self.info
+        # count pass (row + val) + row pointers, split (row, col, val read;
+        # COO part written), ELL cells written
+        return 8 * self.nnz + 4 * self.m + 12 * self.nnz + 12 * i["nnz_coo"] + 8 * i["ell_cells"]
+
+    def spmv_bytes(self):
+        i = self.info
+        return 8 * i["ell_cells"] + 12 * i["nnz_coo"] + 4 * self.n + 4 * self.m
 
 
 class Cfg3(Workload):
-    """DCSR conversion + SpMV on hypersparse 4M x 4M, 2/row (SpMM later)."""
-    fmt = "DCSR"
+    """DCSR and CSC conversion + DCSR SpMM N=64 fp32, hypersparse 4M x 4M, 2/row (i.i.d., dedup)"""
+    nd = 64
 
-    def setup(self, ctx):
+    def setup(self, torch):
         m = 1 << 22
-        return ctx.gen_hypersparse(5, m, m, 2 * m)
+        self.coo = self.rows_block(self.ctx.gen_hypersparse(5, m * self.world, m, 2 * m * self.world))
+        self.m, self.n = self.coo.shape
+        self.nnz = int(self.coo.view().nvals)
+        self.b = torch.empty(self.n * self.nd, dtype=torch.float32, device="cuda")
+        self.ctx.gen_dense(3, self.n * self.nd, self.b.data_ptr())
+        self.c = torch.zeros(max(self.m, 1) * self.nd, dtype=torch.float32, device="cuda")
+        self.y = self.c
+        self.fmt = "DCSR"
 
-    def convert_bytes(self, nnz, m, n, info):
-        return 20 * nnz + 8 * info.get("nnr", 0) + 4
+    def step(self):
+        a = self.ctx.convert(self.coo, "DCSR")
+        self.ctx.convert(self.coo, "CSC")
+        self.ctx.spmm_device(a, self.b.data_ptr(), self.sfg.F32, self.nd, self.c.data_ptr())
 
-    def spmv_bytes(self, nnz, m, n, info):
-        return 8 * nnz + 8 * info.get("nnr", 0) + 4 * n + 4 * m
+    def kernels(self):
+        a = self.ctx.convert(self.coo, "DCSR")
+        nnr = int(a.view().level[0].node_count)
+        self.info = {"nnr": nnr, "nd": self.nd}
+        self.kept = a
+        nz, m, n, nd = self.nnz, self.m, self.n, self.nd
+        return [("convert_dcsr", lambda: self.ctx.convert(self.coo, "DCSR"), 20 * nz + 8 * nnr + 4, 0),
+                ("convert_csc", lambda: self.ctx.convert(self.coo, "CSC"), 20 * nz + 4 * (n + 1), 0),
+                ("spmm", lambda: self.ctx.spmm_device(a, self.b.data_ptr(), self.sfg.F32, nd, self.c.data_ptr()),
+                 8 * nz + 8 * nnr + 4 * n * nd + 4 * m * nd, 2 * nz * nd)]
+
+    def out_rows(self):
+        return self.c
 
 
-WORKLOADS = {1: Cfg1, 2: Cfg2, 3: Cfg3}
+class Cfg4(Workload):
+    """BCSR(16,16) bf16 SpMM N=128 (tcgen05), block-sparse 512K x 512K, 10% block density, generated as BCSR"""
+    unit = "GFLOP/s"
+    nd = 128
+
+    def setup(self, torch):
+        m = 1 << 19
+        self.m = self.n = m
+        self.a = self.ctx.gen_block_sparse(11, m, m, 16, 16, 0.1, value_dtype=self.sfg.BF16)
+        v = self.a.view()
+        self.nblocks = int(v.level[1].node_count)
+        self.nnz = self.nblocks * 256
+        self.b = torch.empty(m * self.nd, dtype=torch.bfloat16, device="cuda")
+        self.b.uniform_(-1, 1)
+        self.c = torch.zeros(m * self.nd, dtype=torch.float32, device="cuda")
+        self.y = self.c
+        self.fmt = "BCSR(16,16) bf16"
+        self.bounds = [0, m]
+        self.info = {"nblocks": self.nblocks, "nd": self.nd, "value_dtype": "bf16", "b_dtype": "bf16"}
+
+    def step(self):
+        self.ctx.spmm_device(self.a, self.b.data_ptr(), self.sfg.BF16, self.nd, self.c.data_ptr())
+
+    def work_units(self):
+        return 2 * self.nnz * self.nd / 1e3  # unit conversion below: (MFLOP) -> GFLOP/s
+
+    def kernels(self):
+        nb, m, n, nd = self.nblocks, self.m, self.n, self.nd
+        byts = nb * 256 * 2 + 4 * nb + 4 * (m // 16 + 1) + 2 * n * nd + 4 * m * nd
+        return [("spmm_bcsr_tc", self.step, byts, 2 * self.nnz * nd)]
+
+
+class Cfg5(SpmvWorkload):
+    """CSR conversion + CSR SpMM N=32 fp32, R-MAT scale 26 (row-partitioned over N GPUs)"""
+    fmt = "CSR"
+    nd = 32
+
+    def setup(self, torch):
+        self.scale = 26
+        self.coo = self.rows_block(self.ctx.gen_rmat(7, self.scale, 16 << self.scale))
+        m, n = self.coo.shape
+        self.m, self.n = m, n
+        self.nnz = int(self.coo.view().nvals)
+        self.b = torch.empty(n * self.nd, dtype=torch.float32, device="cuda")
+        self.ctx.gen_dense(3, n * self.nd, self.b.data_ptr())
+        self.c = torch.zeros(max(m, 1) * self.nd, dtype=torch.float32, device="cuda")
+        self.y = self.c
+
+    def step(self):
+        a = self.ctx.convert(self.coo, "CSR")
+        self.ctx.spmm_device(a, self.b.data_ptr(), self.sfg.F32, self.nd, self.c.data_ptr())
+
+    def kernels(self):
+        a = self.ctx.convert(self.coo, "CSR")
+        self.kept = a
+        nz, m, n, nd = self.nnz, self.m, self.n, self.nd
+        return [("convert", lambda: self.ctx.convert(self.coo, "CSR"), 20 * nz + 4 * (m + 1), 0),
+                ("spmm", lambda: self.ctx.spmm_device(a, self.b.data_ptr(), self.sfg.F32, nd, self.c.data_ptr()),
+                 8 * nz + 4 * (m + 1) + 4 * n * nd + 4 * m * nd, 2 * nz * nd)]
+
+    def out_rows(self):
+        return self.c
+
+
+WORKLOADS = {1: Cfg1, 2: Cfg2, 3: Cfg3, 4: Cfg4, 5: Cfg5}
 
 
 # ------------------------------------------------------------------- clocks
 class ClockSampler:
-    def __init__(self, device):
-        self.device = device
-        self.proc = None
-        self.path = os.path.join("/tmp", f"sfg_clocks_{os.getpid()}.csv")
+    """In-process NVML sampling of SM clocks and throttle reasons (a
+    background thread; lighter than an nvidia-smi subprocess)."""
+
+    def __init__(self, device, period=0.05):
+        self.device, self.period = device, period
+        self.samples, self.ok = [], False
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
         try:
-            self.f = open(self.path, "w")
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
-        except Exception:
-            self.proc = None
+            import pynvml as N
+            N.nvmlInit()
+            self.N, self.h = N, N.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)
+            return self
+        self.stop = threading.Event()
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
         return self
 
-    def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
+    def _run(self):
+        N = self.N
+        while not self.stop.is_set():
             try:
-                self.proc.wait(timeout=5)
+                self.samples.append((N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM),
+                                     N.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
             except Exception:
-                self.proc.kill()
-            self.f.close()
+                pass
+            self.stop.wait(self.period)
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self.stop.set()
+            self.th.join()
 
     def summary(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        rows = []
-        with open(self.path) as f:
-            for line in f:
-                parts = [p.strip() for p in line.split(",")]
-                if len(parts) == 6:
-                    try:
-                        rows.append((float(parts[0]), float(parts[1]), parts[2:]))
-                    except ValueError:
-                        pass
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for _, _, rs in rows for i, r in enumerate(rs) if r.lower() == "active"})
-        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
-                "reasons": reasons, "samples": len(rows)}
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [f"nvml unavailable: {self.err}"]}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["no samples"]}
+        N = self.N
+        names = {N.nvmlClocksThrottleReasonHwSlowdown: "hw_slowdown",
+                 N.nvmlClocksThrottleReasonHwThermalSlowdown: "hw_thermal_slowdown",
+                 N.nvmlClocksThrottleReasonSwThermalSlowdown: "sw_thermal_slowdown",
+                 N.nvmlClocksThrottleReasonSwPowerCap: "sw_power_cap"}
+        reasons = sorted({n for _, r in self.samples for bit, n in names.items() if r & bit})
+        return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples), "source": "NVML, 50 ms period"}
 
 
 # ---------------------------------------------------------------- our arm
@@ -172,6 +310,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_2403_05802_b200 as sfg
+    from paper_2403_05802_b200.rowpart import gather_rows, padded_chunk
 
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -181,54 +320,22 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
     ctx = sfg.Context(local, stream.cuda_stream)
-    wl = WORKLOADS[args.config](args, rank, world)
-
-    # ---- setup: canonical COO resident in HBM, this rank's row block
-    glob = wl.setup(ctx)
-    if world > 1:
-        bounds = ctx.row_partition(glob, world)
-        coo = ctx.slice_rows(glob, bounds[rank], bounds[rank + 1])
-        row0 = bounds[rank]
-        del glob
-    else:
-        coo, bounds, row0 = glob, [0, glob.shape[0]], 0
-    m, n = coo.shape
-    nnz = int(coo.view().nvals)
-    x = torch.empty(n, dtype=torch.float32, device="cuda")
-    ctx.gen_dense(3, n, x.data_ptr())
-    if world > 1:
-        # equal padded chunks for the all-gather
-        t = torch.tensor([m], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        chunk = int(t.item())
-    else:
-        chunk = m
-    y = torch.zeros(max(chunk, 1), dtype=torch.float32, device="cuda")
-    y_full = torch.empty(max(chunk, 1) * world, dtype=torch.float32, device="cuda") if world > 1 else y
+    wl = WORKLOADS[args.config](sfg, ctx, rank, world)
+    wl.setup(torch)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
-    # info for the algorithmic byte counts
-    a = ctx.convert(coo, wl.fmt)
-    info = {}
-    if wl.fmt.startswith("HYB"):
-        ell, cpart = a.parts()
-        ev, cv = ell.view(), cpart.view()
-        info = {"ell_cells": int(ev.nvals), "ell_k": int(ev.level[0].node_count),
-                "nnz_coo": int(cv.nvals), "nnz_ell": nnz - int(cv.nvals)}
-    elif wl.fmt == "DCSR":
-        info = {"nnr": int(a.view().level[0].node_count)}
-    del a
-
-    def gather_y():
-        if world > 1:
-            # reassemble y over NVLink: rank r's rows land at y_full[r*chunk:]
-            dist.all_gather_into_tensor(y_full, y)
+    if world > 1:
+        out_rows = wl.out_rows()
+        width = out_rows.numel() // max(wl.m, 1)
+        chunk = padded_chunk(wl.m)
+        ybuf = torch.zeros(chunk * width, dtype=torch.float32, device="cuda")
 
     def step():
-        a = ctx.convert(coo, wl.fmt)
-        ctx.spmv_device(a, x.data_ptr(), y.data_ptr())
-        del a
-        gather_y()
+        wl.step()
+        if world > 1:
+            # reassemble the output over NVLink: rank r's rows at r*chunk
+            ybuf[: wl.m * width].copy_(out_rows[: wl.m * width])
+            gather_rows(ybuf.view(chunk, width), chunk)
 
     def timed(fn, k, flush_between=True):
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
@@ -241,130 +348,154 @@ def run_ours(args):
         torch.cuda.synchronize()
         return [s.elapsed_time(e) for s, e in ev]
 
-    # ---- warmup
-    for _ in range(max(args.warmup, 3)):
+    warm = max(args.warmup, 3)
+    for _ in range(warm):
         step()
     torch.cuda.synchronize()
 
-    # ---- timed region: K steps, barrier + sync on both sides
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
+    # ---- timed region: K steps, barrier + sync on both sides; clocks sampled
     with ClockSampler(local) as clk:
-        # keep the GPU under this load long enough for nvidia-smi to sample
-        # the clocks; the timed steps follow inside the same sampling window
-        t_end = time.time() + (0 if args.profile else 1.5)
+        # keep the GPU under this load long enough for the sampler to see the
+        # clocks; the timed steps follow inside the same sampling window
+        t_end = time.time() + (0 if args.profile else 1.0)
         while time.time() < t_end:
             step()
             torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
         l0 = sfg.launch_count()
         step_ms = timed(step, args.steps)
-    launches = (sfg.launch_count() - l0)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
+        launches = sfg.launch_count() - l0
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
     total_ms = sum(step_ms)
+    units = float(wl.work_units())
     if world > 1:
         t = torch.tensor([total_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-        tn = torch.tensor([nnz], device="cuda", dtype=torch.float64)
+        tn = torch.tensor([units], device="cuda", dtype=torch.float64)
         dist.all_reduce(tn)
-        total_nnz = float(tn.item())
-    else:
-        total_nnz = float(nnz)
+        units = float(tn.item())
     ms_per_step = total_ms / args.steps
-    value = total_nnz / (ms_per_step * 1e-3) / 1e6
+    value = units / (ms_per_step * 1e-3) / 1e6
 
-    # ---- kernel-level roofline: convert alone, spmv alone (CUDA events)
+    # ---- kernel families alone (CUDA events on the launching stream)
     hbm, _, peak_src = load_peaks()
-    conv_ms = statistics.mean(timed(lambda: ctx.convert(coo, wl.fmt), args.steps))
-    a = ctx.convert(coo, wl.fmt)
-    spmv_ms = statistics.mean(timed(lambda: ctx.spmv_device(a, x.data_ptr(), y.data_ptr()),
-                                    args.steps))
-    cb = wl.convert_bytes(nnz, m, n, info)
-    sb = wl.spmv_bytes(nnz, m, n, info)
-    kernels = {
-        "convert": {"ms": conv_ms, "alg_bytes": cb, "GB/s": cb / conv_ms / 1e6,
-                    "Mnnz/s": nnz / conv_ms / 1e3},
-        "spmv": {"ms": spmv_ms, "alg_bytes": sb, "GB/s": sb / spmv_ms / 1e6,
-                 "GFLOP/s": 2 * nnz / spmv_ms / 1e6},
-    }
+    kernels = {}
+    for name, fn, byts, flops in wl.kernels():
+        for _ in range(2):
+            fn()
+        ms = statistics.median(timed(fn, max(args.steps, 5)))
+        d = {"ms": round(ms, 4), "alg_bytes": int(byts), "GB/s": round(byts / ms / 1e6, 1),
+             "hbm_frac": round(byts / ms / 1e6 / hbm, 4)}
+        if flops:
+            d["GFLOP/s"] = round(flops / ms / 1e6, 1)
+        kernels[name] = d
     dom = max(kernels, key=lambda k: kernels[k]["ms"])
     ach = kernels[dom]["GB/s"]
-    roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-            "frac": round(ach / hbm, 4), "traffic": None, "kernel": dom,
-            "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs"}
-
-    # ---- e2e through the C-ABI with host buffers (pinned)
-    r_h, c_h, v_h = coo.coo_arrays()
-    pin = lambda arr: torch.from_numpy(arr).pin_memory()
-    r_p, c_p, v_p = pin(r_h), pin(c_h), pin(v_h)
-    x_p = pin(x.cpu().numpy())
-    y_p = torch.empty(m, dtype=torch.float32).pin_memory()
-    import ctypes as C
-    lib = sfg.load()
-
-    def e2e_step():
-        h = C.c_void_p()
-        sfg._check(lib.sfg_from_coo(ctx.h, m, n, nnz, C.c_void_p(r_p.data_ptr()), C.c_void_p(c_p.data_ptr()),
-                                    C.c_void_p(v_p.data_ptr()), sfg.FLAG_HOST | sfg.FLAG_SORTED, C.byref(h)))
-        t = sfg.Tensor(ctx, h)
-        a2 = ctx.convert(t, wl.fmt)
-        sfg._check(lib.sfg_spmv(ctx.h, a2.h, C.c_void_p(x_p.data_ptr()), C.c_void_p(y_p.data_ptr()),
-                                sfg.COMPUTE_HOST))
+    roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4),
+            "traffic": None, "kernel": dom, "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs"}
 
     if args.profile:
-        print(json.dumps({"profile_run": True, "value": round(value, 2), "kernels": kernels}))
+        if rank == 0:
+            print(json.dumps({"profile_run": True, "value": round(value, 2), "kernels": kernels}))
         return
+
+    e2e = (e2e_measure(args, sfg, ctx, wl, timed, torch, dist, world) if not args.no_e2e
+           else {"value": None, "unit": wl.unit, "skipped": "--no-e2e"})
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(value, 2), "unit": wl.unit, "n_gpus": world,
+            "steps": args.steps, "warmup": warm, "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16" if args.config == 4 else "f32",
+            "data": "synthetic (seeded generators, csrc/synth.h)",
+            "config": {"workload": f"config {args.config}: {wl.describe()}", "format": wl.fmt,
+                       "rows": int(wl.bounds[-1]), "cols": int(wl.n), "nnz_per_rank": int(wl.nnz),
+                       "nnz_total": int(units) if wl.unit == "Mnnz/s" else None,
+                       "scale": getattr(wl, "scale", None),
+                       "l2": "flushed (256 MB write) before every timed step",
+                       "parallelism": f"row-partitioned x{world}, NCCL all-gather of the output"
+                       if world > 1 else "single GPU", **wl.info},
+            "step_ms": {"min": round(min(step_ms), 4), "median": round(statistics.median(step_ms), 4),
+                        "max": round(max(step_ms), 4)},
+            "roofline": roof, "kernels": kernels, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        if world == 1 and wl.has_cpu_sample and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(args.config, steps=1)
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def e2e_measure(args, sfg, ctx, wl, timed, torch, dist, world):
+    """Same step through the C-ABI with HOST buffers: from_coo from pinned
+    row/col/val, conversion, SpMV/SpMM with host x/B in and y/C out."""
+    import ctypes as C
+
+    lib = sfg.load()
+    if args.config == 4:
+        # no conversion in the config-4 step: host B in, host C out
+        b_p = torch.empty(wl.b.numel(), dtype=torch.bfloat16).pin_memory()
+        b_p.copy_(wl.b.cpu())
+        c_p = torch.empty(wl.c.numel(), dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            sfg._check(lib.sfg_spmm(ctx.h, wl.a.h, C.c_void_p(b_p.data_ptr()), sfg.BF16, wl.nd, wl.nd,
+                                    C.c_void_p(c_p.data_ptr()), wl.nd, sfg.COMPUTE_HOST))
+        h2d, d2h = b_p.numel() * 2, c_p.numel() * 4
+    else:
+        r_h, c_h, v_h = wl.coo.coo_arrays()
+        pin = lambda arr: torch.from_numpy(arr).pin_memory()
+        r_p, c_p, v_p = pin(r_h), pin(c_h), pin(v_h)
+        nd = getattr(wl, "nd", 1)
+        dense = wl.b if hasattr(wl, "b") else wl.x
+        x_p = pin(dense.cpu().numpy())
+        y_p = torch.empty(max(wl.m, 1) * nd, dtype=torch.float32).pin_memory()
+        fmt = wl.fmt
+
+        def e2e_step():
+            h = C.c_void_p()
+            sfg._check(lib.sfg_from_coo(ctx.h, wl.m, wl.n, wl.nnz, C.c_void_p(r_p.data_ptr()),
+                                        C.c_void_p(c_p.data_ptr()), C.c_void_p(v_p.data_ptr()),
+                                        sfg.FLAG_HOST | sfg.FLAG_SORTED, C.byref(h)))
+            t = sfg.Tensor(ctx, h)
+            a2 = ctx.convert(t, fmt)
+            if args.config == 3:
+                ctx.convert(t, "CSC")
+            if nd == 1:
+                sfg._check(lib.sfg_spmv(ctx.h, a2.h, C.c_void_p(x_p.data_ptr()), C.c_void_p(y_p.data_ptr()),
+                                        sfg.COMPUTE_HOST))
+            else:
+                sfg._check(lib.sfg_spmm(ctx.h, a2.h, C.c_void_p(x_p.data_ptr()), sfg.F32, nd, nd,
+                                        C.c_void_p(y_p.data_ptr()), nd, sfg.COMPUTE_HOST))
+        h2d, d2h = 12 * wl.nnz + x_p.numel() * 4, y_p.numel() * 4
     for _ in range(2):
         e2e_step()
     torch.cuda.synchronize()
-    e2e_ms = statistics.mean(timed(e2e_step, max(3, min(args.steps, 10)), flush_between=False))
+    ms = statistics.mean(timed(e2e_step, max(3, min(args.steps, 10)), flush_between=False))
+    units = float(wl.work_units())
     if world > 1:
-        t = torch.tensor([e2e_ms], device="cuda")
+        t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    e2e = {"value": round(total_nnz / (e2e_ms * 1e-3) / 1e6, 2), "unit": UNIT,
-           "h2d_bytes_per_step": int(12 * nnz + 4 * n), "d2h_bytes_per_step": int(4 * m),
-           "ms_per_step": round(e2e_ms, 4)}
-
-    out = None
-    if rank == 0:
-        out = {
-            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms_per_step, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded generators, csrc/synth.h)",
-            "config": {"workload": f"config {args.config}: {wl.__doc__.strip()}",
-                       "format": wl.fmt, "rows": int(bounds[-1]) if world > 1 else m, "cols": n,
-                       "nnz_per_rank": nnz, "nnz_total": int(total_nnz), "scale": getattr(wl, "scale", None),
-                       "step": f"canonical COO -> {wl.fmt} conversion -> SpMV" +
-                               (" -> NCCL all-gather of y" if world > 1 else ""),
-                       "l2": "flushed (256 MB write) before every timed step",
-                       "parallelism": f"row-partitioned x{world}" if world > 1 else "single GPU",
-                       **{k: v for k, v in info.items()}},
-            "roofline": roof,
-            "kernels": {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in d.items()}
-                        for k, d in kernels.items()},
-            "e2e": e2e,
-            "gpu_launches": int(launches),
-            "clocks": clk.summary(),
-        }
-    if world > 1:
-        dist.barrier()
-    if rank == 0 and args.config in (1, 2) and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(args.config, steps=1)
-    if rank == 0:
-        print(json.dumps(out), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+        ms = float(t.item())
+        tn = torch.tensor([units], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tn)
+        units = float(tn.item())
+    return {"value": round(units / (ms * 1e-3) / 1e6, 2), "unit": wl.unit, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms, 4)}
 
 
 # ------------------------------------------------------- reference (CPU) arm
 def reference_sample(config):
-    """Bounded row-block sample of the workload, from the oracle's
-    generator (identical matrix to the GPU arm's)."""
+    """Bounded row-block sample of the workload, from the oracle's generator
+    (the same matrix the GPU arm uses)."""
     import oracle
     port = oracle.Port()
     if config == 1:
@@ -372,7 +503,7 @@ def reference_sample(config):
         rows = (0, 1 << 16)  # 1/16 of the rows: 1,048,576 nnz
     else:
         full = port.gen_rmat(7, 22, 16 << 22)
-        rows = (1 << 20, (1 << 20) + (1 << 17))  # a mid-graph row block
+        rows = (1 << 20, (1 << 20) + (1 << 17))  # a mid-graph row block, ~5.2 M nnz
     r, c, v = full.arrays()
     sel = (r >= rows[0]) & (r < rows[1])
     r, c, v = r[sel] - rows[0], c[sel], v[sel]
@@ -382,9 +513,9 @@ def reference_sample(config):
     return m, n, r, c, v, x, desc
 
 
-def cpu_baseline(config, steps=1, kind="reference"):
+def cpu_baseline(config, steps=1):
     import oracle
-    lib = oracle.Ref() if (kind == "reference" and oracle.ref_available()) else oracle.Port()
+    lib = oracle.Ref() if oracle.ref_available() else oracle.Port()
     kind = "reference" if isinstance(lib, oracle.Ref) else "port"
     m, n, r, c, v, x, desc = reference_sample(config)
     threads = os.cpu_count() or 1
@@ -401,30 +532,27 @@ def cpu_baseline(config, steps=1, kind="reference"):
             lib.spmv(e, x, threads=threads) + lib.spmv(co, x, threads=threads)
         times.append(time.perf_counter() - t0)
     sec = statistics.mean(times)
-    return {"value": round(len(v) / sec / 1e6, 4), "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": desc + f"; convert single-threaded (reference), run_kernel threads={threads}",
+    return {"value": round(len(v) / sec / 1e6, 4), "unit": "Mnnz/s", "cores": threads, "kind": kind,
+            "sample": desc + f"; conversions single-threaded (as in the reference), run_kernel threads={threads}",
             "sec_per_step": round(sec, 3)}
 
 
 def run_reference(args):
-    rank = int(os.environ.get("RANK", 0))
-    if rank != 0:
+    if int(os.environ.get("RANK", 0)) != 0:
         return
     if args.config not in (1, 2):
-        print(json.dumps({"impl": "reference", "unavailable": f"config {args.config} has no CPU sample"}))
+        print(json.dumps({"impl": "reference", "unavailable": f"config {args.config} has no bounded CPU sample"}))
         return
-    for _ in range(args.warmup):
-        pass  # the reference has no warm-up effects worth timing twice
     cb = cpu_baseline(args.config, steps=args.steps)
-    wl = WORKLOADS[args.config]
+    doc = WORKLOADS[args.config].__doc__.strip()
     print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": 0,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["sec_per_step"] * 1e3,
+        "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "Mnnz/s", "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(cb["sec_per_step"] * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generators, csrc/synth.h)",
-        "config": {"workload": f"config {args.config}: {wl.__doc__.strip()}", "format": wl.fmt},
+        "config": {"workload": f"config {args.config}: {doc}", "format": WORKLOADS[args.config].fmt},
         "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
-        "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "e2e": {"value": cb["value"], "unit": "Mnnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
 
@@ -436,6 +564,7 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: no clock soak, no e2e, no CPU baseline")
     args = ap.parse_args()

@@ -127,11 +127,13 @@ __global__ void __launch_bounds__(kBlock) k_coo_to_dcsr(
   if (full) {
 #pragma unroll
     for (int q = 0; q < kDcsrItems / 4; ++q) {
-      int4 rr = ld_stream(reinterpret_cast<const int4*>(row + e_base) + q);
-      int4 cc = ld_stream(reinterpret_cast<const int4*>(col + e_base) + q);
-      float4 vv = ld_stream(reinterpret_cast<const float4*>(val + e_base) + q);
-      st_stream(reinterpret_cast<int4*>(ocol + e_base) + q, cc);
-      st_stream(reinterpret_cast<float4*>(oval + e_base) + q, vv);
+      // L1-allocating: lane runs are 64 B apart, so consecutive q steps
+      // share each 32 B sector
+      int4 rr = __ldg(reinterpret_cast<const int4*>(row + e_base) + q);
+      int4 cc = __ldg(reinterpret_cast<const int4*>(col + e_base) + q);
+      float4 vv = __ldg(reinterpret_cast<const float4*>(val + e_base) + q);
+      reinterpret_cast<int4*>(ocol + e_base)[q] = cc;  // halves of a sector: keep in L2
+      reinterpret_cast<float4*>(oval + e_base)[q] = vv;
       r[4 * q] = rr.x; r[4 * q + 1] = rr.y; r[4 * q + 2] = rr.z; r[4 * q + 3] = rr.w;
     }
   } else {

@@ -179,43 +179,36 @@ __global__ void __launch_bounds__(kBlock) k_split(
     const float* __restrict__ val, int64_t nnz, const uint32_t* __restrict__ off,
     int32_t* __restrict__ srow, int32_t* __restrict__ scol, float* __restrict__ sval,
     int32_t* __restrict__ rrow, int32_t* __restrict__ rcol, float* __restrict__ rval) {
-  // kSplitRun consecutive entries per thread; row, col and val are all
-  // loaded up front (independent 128-bit loads), then one `off` lookup per
-  // distinct row of the run (runs are mostly a single row), then stores.
+  // A warp owns 32*kSplitRun consecutive entries, lane-strided: at step i
+  // lane l handles entry base + 32 i + l, so loads are coalesced and, since
+  // consecutive entries of one part land at consecutive positions, so are
+  // the stores (blocked per-thread runs scattered 4-byte stores 32 B apart,
+  // which cost L2 partial-sector read-modify-writes). All loads of the
+  // warp's chunk are issued before the first store.
   constexpr int R = kSplitRun;
-  const int64_t nrun = (nnz + R - 1) / R;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nrun;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    int64_t e0 = v * R;
+  const int lane = threadIdx.x & 31;
+  const int64_t span = 32 * R;
+  const int64_t nchunk = (nnz + span - 1) / span;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nchunk; w += warps) {
+    const int64_t base = w * span + lane;
     int r[R], c[R];
     float x[R];
     uint32_t o[R];
-    if (e0 + R <= nnz) {
 #pragma unroll
-      for (int q = 0; q < R / 4; ++q) {
-        int4 rr = ld_stream(reinterpret_cast<const int4*>(row + e0) + q);
-        int4 cc = ld_stream(reinterpret_cast<const int4*>(col + e0) + q);
-        float4 vv = ld_stream(reinterpret_cast<const float4*>(val + e0) + q);
-        r[4 * q] = rr.x; r[4 * q + 1] = rr.y; r[4 * q + 2] = rr.z; r[4 * q + 3] = rr.w;
-        c[4 * q] = cc.x; c[4 * q + 1] = cc.y; c[4 * q + 2] = cc.z; c[4 * q + 3] = cc.w;
-        x[4 * q] = vv.x; x[4 * q + 1] = vv.y; x[4 * q + 2] = vv.z; x[4 * q + 3] = vv.w;
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < R; ++i) {
-        bool ok = e0 + i < nnz;
-        r[i] = ok ? row[e0 + i] : -1;
-        c[i] = ok ? col[e0 + i] : 0;
-        x[i] = ok ? val[e0 + i] : 0.f;
-      }
+    for (int i = 0; i < R; ++i) {
+      int64_t e = base + 32 * i;
+      bool ok = e < nnz;
+      r[i] = ok ? ld_stream(row + e) : -1;
+      c[i] = ok ? ld_stream(col + e) : 0;
+      x[i] = ok ? ld_stream(val + e) : 0.f;
     }
-    o[0] = r[0] >= 0 ? __ldg(off + r[0]) : 0u;
 #pragma unroll
-    for (int i = 1; i < R; ++i) o[i] = r[i] == r[i - 1] ? o[i - 1] : (r[i] >= 0 ? __ldg(off + r[i]) : 0u);
+    for (int i = 0; i < R; ++i) o[i] = r[i] >= 0 ? __ldg(off + r[i]) : 0u;
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       if (r[i] < 0) continue;
-      int64_t pos = e0 + i - (int64_t)(o[i] & ~kSelBit);
+      int64_t pos = base + 32 * i - (int64_t)(o[i] & ~kSelBit);
       if (o[i] & kSelBit) {
         srow[pos] = r[i];
         scol[pos] = c[i];

@@ -156,9 +156,11 @@ __global__ void __launch_bounds__(kBlock) k_spmv_coo(const int32_t* __restrict__
     if (e0 + kCooRun <= nnz) {
 #pragma unroll
       for (int q = 0; q < kCooRun / 4; ++q) {
-        int4 rr = ld_stream(reinterpret_cast<const int4*>(row + e0) + q);
-        int4 cc = ld_stream(reinterpret_cast<const int4*>(col + e0) + q);
-        float4 vv = ld_stream(reinterpret_cast<const float4*>(val + e0) + q);
+        // L1-allocating: lane runs are 64 B apart, so each 32 B sector is
+        // touched by two consecutive q steps
+        int4 rr = __ldg(reinterpret_cast<const int4*>(row + e0) + q);
+        int4 cc = __ldg(reinterpret_cast<const int4*>(col + e0) + q);
+        float4 vv = __ldg(reinterpret_cast<const float4*>(val + e0) + q);
         r[4 * q] = rr.x; r[4 * q + 1] = rr.y; r[4 * q + 2] = rr.z; r[4 * q + 3] = rr.w;
         c[4 * q] = cc.x; c[4 * q + 1] = cc.y; c[4 * q + 2] = cc.z; c[4 * q + 3] = cc.w;
         v[4 * q] = vv.x; v[4 * q + 1] = vv.y; v[4 * q + 2] = vv.z; v[4 * q + 3] = vv.w;

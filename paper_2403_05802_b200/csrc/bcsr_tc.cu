@@ -253,6 +253,179 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ------------------------------------------------------------------------
+// Grouped variant: a CTA owns kGroup consecutive block rows, all resident in
+// TMEM at once (kGroup x 16 fp32 columns = 512). The producer warp merges
+// the group's block-column lists (lane j holds block row j's cursor; warp
+// min + ballot per step), so each B tile is loaded ONCE per group and
+// multiplied into every block row that holds that block column. Per stage:
+// one B tile (4 KB, SW128) + up to kGroup value blocks (512 B each, SW32);
+// the stage's block-row mask travels in shared memory. At the end of the
+// group the epilogue drains all accumulators.
+constexpr int kGroup = 32;
+constexpr int kGStages = 8;
+constexpr int kGStageBytes = kTileBytes + kGroup * kABytes;  // 20 KB
+constexpr uint32_t kEndMask = 0;                             // end-of-group marker
+
+struct GShared {
+  uint64_t full[kGStages];
+  uint64_t empty[kGStages];
+  uint64_t acc_full;
+  uint64_t acc_empty;
+  uint32_t mask[kGStages];
+  uint32_t started;
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ void mbar_arrive_plain(uint64_t* bar) { mbar_arrive(bar); }
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_bcsr_tc_group(const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_a,
+                    const int32_t* __restrict__ ptr, const int32_t* __restrict__ bcol, int32_t nbr,
+                    int32_t m, float* __restrict__ c, int64_t ldc, int accumulate) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* stages = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  GShared* sh = reinterpret_cast<GShared*>(stages + kGStages * kGStageBytes);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t ngroups = (nbr + kGroup - 1) / kGroup;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kGStages; ++s) {
+      mbar_init(&sh->full[s], 1);
+      mbar_init(&sh->empty[s], 1);
+    }
+    mbar_init(&sh->acc_full, 1);
+    mbar_init(&sh->acc_empty, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 5) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sh->tmem_base)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sh->tmem_base;
+
+  if (warp == 4) {
+    // ------------------------------------------- producer: k-way merge
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int32_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+      const int32_t br = g * kGroup + lane;
+      int32_t cur = 0, end = 0;
+      if (br < nbr) {
+        cur = __ldg(ptr + br);
+        end = __ldg(ptr + br + 1);
+      }
+      uint32_t bc = cur < end ? (uint32_t)__ldg(bcol + cur) : 0xffffffffu;
+      while (true) {
+        uint32_t mn = __reduce_min_sync(kFull, bc);
+        uint32_t mask = __ballot_sync(kFull, bc == mn && mn != 0xffffffffu);
+        if (lane == 0) {
+          mbar_wait(&sh->empty[stage], phase ^ 1);
+          sh->mask[stage] = mask;
+          if (mask) {
+            uint8_t* st = stages + stage * kGStageBytes;
+            mbar_expect_tx(&sh->full[stage], kTileBytes + __popc(mask) * kABytes);
+            tma_2d(st, &tmap_b, &sh->full[stage], 0, (int)mn * kBlk);
+            tma_2d(st + 2048, &tmap_b, &sh->full[stage], 64, (int)mn * kBlk);
+          } else {
+            mbar_arrive_plain(&sh->full[stage]);  // end-of-group marker
+          }
+        }
+        __syncwarp();
+        if (mask >> lane & 1u) {
+          uint8_t* st = stages + stage * kGStageBytes;
+          tma_2d(st + kTileBytes + lane * kABytes, &tmap_a, &sh->full[stage], 0, cur * kBlk);
+          ++cur;
+          bc = cur < end ? (uint32_t)__ldg(bcol + cur) : 0xffffffffu;
+        }
+        if (++stage == kGStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+        if (!mask) break;
+      }
+    }
+  } else if (warp == 5) {
+    // ------------------------------------------- MMA issuer
+    int stage = 0, it = 0;
+    uint32_t phase = 0;
+    for (int32_t g = blockIdx.x; g < ngroups; g += gridDim.x, ++it) {
+      mbar_wait(&sh->acc_empty, (it & 1) ^ 1);
+      tc_fence_after();
+      uint32_t started = 0;
+      while (true) {
+        mbar_wait(&sh->full[stage], phase);
+        tc_fence_after();
+        uint32_t mask = sh->mask[stage];
+        if (lane == 0) {
+          if (mask) {
+            uint32_t base = smem_u32(stages + stage * kGStageBytes);
+            uint64_t adesc = smem_desc(base, 2048, 1024, 2);
+            uint32_t mm = mask;
+            while (mm) {
+              int j = __ffs(mm) - 1;
+              mm &= mm - 1;
+              uint64_t bdesc = smem_desc(base + kTileBytes + j * kABytes, 16, 256, 6);
+              tc_mma(tmem + j * kBlk, adesc, bdesc, kIdesc, (started >> j) & 1u);
+            }
+            tc_commit(&sh->empty[stage]);
+          } else {
+            tc_commit(&sh->acc_full);
+            mbar_arrive(&sh->empty[stage]);
+          }
+        }
+        started |= mask;
+        __syncwarp();
+        if (++stage == kGStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+        if (!mask) break;
+      }
+    }
+  } else {
+    // ------------------------------------------- epilogue
+    int it = 0;
+    const int col = warp * 32 + lane;
+    for (int32_t g = blockIdx.x; g < ngroups; g += gridDim.x, ++it) {
+      mbar_wait(&sh->acc_full, it & 1);
+      tc_fence_after();
+      for (int j = 0; j < kGroup; ++j) {
+        const int64_t r0 = ((int64_t)g * kGroup + j) * kBlk;
+        if (r0 >= m) break;
+        const int32_t br = g * kGroup + j;
+        float v[16];
+        if (__ldg(ptr + br) < __ldg(ptr + br + 1)) {  // accumulator j was written
+          tc_ld16(tmem + ((uint32_t)(warp * 32) << 16) + j * kBlk, v);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < kBlk; ++i) {
+          if (r0 + i < m) {
+            float* p = c + (r0 + i) * ldc + col;
+            *p = accumulate ? *p + v[i] : v[i];
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh->acc_empty);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -298,14 +471,26 @@ bool spmm_bcsr_tc(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dt
       raise(SFG_ERR_CUDA, "cuTensorMapEncodeTiled(A) failed");
   }
   const size_t smem = 1024 + kStages * kStageBytes + sizeof(Shared) + 64;
+  const size_t gsmem = 1024 + kGStages * kGStageBytes + sizeof(GShared) + 64;
   static bool attr = false;
   if (!attr) {
     SFG_CUDA(cudaFuncSetAttribute(k_bcsr_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SFG_CUDA(cudaFuncSetAttribute(k_bcsr_tc_group, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem));
     attr = true;
   }
-  int grid = (int)std::min<int64_t>(a->nbr, (int64_t)ctx->sms);
-  SFG_LAUNCH(k_bcsr_tc, grid, kThreads, smem, ctx->stream, tb, ta, a->ptr, a->idx, (int32_t)a->nbr,
-             (int32_t)a->m, c, ldc, accumulate ? 1 : 0);
+  static const bool per_row = [] {
+    const char* v = std::getenv("SFG_BCSR_TC_PER_ROW");  // A/B switch: one block row per accumulator
+    return v && *v == '1';
+  }();
+  if (per_row) {
+    int grid = (int)std::min<int64_t>(a->nbr, (int64_t)ctx->sms);
+    SFG_LAUNCH(k_bcsr_tc, grid, kThreads, smem, ctx->stream, tb, ta, a->ptr, a->idx, (int32_t)a->nbr,
+               (int32_t)a->m, c, ldc, accumulate ? 1 : 0);
+  } else {
+    int grid = (int)std::min<int64_t>(ceil_div(a->nbr, kGroup), (int64_t)ctx->sms);
+    SFG_LAUNCH(k_bcsr_tc_group, grid, kThreads, gsmem, ctx->stream, tb, ta, a->ptr, a->idx, (int32_t)a->nbr,
+               (int32_t)a->m, c, ldc, accumulate ? 1 : 0);
+  }
   return true;
 }
 

@@ -398,6 +398,18 @@ def run_ours(args):
     ach = kernels[dom]["GB/s"]
     roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4),
             "traffic": None, "kernel": dom, "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs"}
+    # DRAM bytes per launch of the dominant family, from the committed ncu
+    # launch list of this config (profiles/traffic_config<N>.json)
+    tpath = os.path.join(ROOT, "profiles", f"traffic_config{args.config}.json")
+    if os.path.exists(tpath):
+        try:
+            fam = json.load(open(tpath))["families"].get(dom)
+            if fam:
+                roof["traffic"] = fam["dram_bytes_per_launch"]
+                roof["traffic_alg_ratio"] = round(fam["dram_bytes_per_launch"] / kernels[dom]["alg_bytes"], 3)
+                roof["traffic_source"] = f"ncu dram__bytes_read+write, {os.path.relpath(tpath, ROOT)}"
+        except Exception:
+            pass
 
     if args.profile:
         if rank == 0:

@@ -259,13 +259,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 // the group's block-column lists (lane j holds block row j's cursor; warp
 // min + ballot per step), so each B tile is loaded ONCE per group and
 // multiplied into every block row that holds that block column. Per stage:
-// one B tile (4 KB, SW128) + up to kGroup value blocks (512 B each, SW32);
-// the stage's block-row mask travels in shared memory. At the end of the
-// group the epilogue drains all accumulators.
+// one B tile (4 KB, SW128) + up to kMaxA value blocks (512 B each, SW32,
+// packed in block-row order); a block column held by more than kMaxA of the
+// group's block rows spills into further stages that reload the tile. The
+// stage's block-row mask travels in shared memory. The ring is deep (26
+// stages, ~8 KB each): the kernel is bound by bytes in flight per SM, since
+// every stage round-trips through L2/HBM. At the end of the group the
+// epilogue drains all accumulators.
 constexpr int kGroup = 32;
-constexpr int kGStages = 8;
-constexpr int kGStageBytes = kTileBytes + kGroup * kABytes;  // 20 KB
-constexpr uint32_t kEndMask = 0;                             // end-of-group marker
+constexpr int kMaxA = 8;
+constexpr int kGStages = 26;
+constexpr int kGStageBytes = kTileBytes + kMaxA * kABytes;  // 8 KB
 
 struct GShared {
   uint64_t full[kGStages];
@@ -319,32 +323,71 @@ __global__ void __launch_bounds__(kThreads, 1)
         cur = __ldg(ptr + br);
         end = __ldg(ptr + br + 1);
       }
-      uint32_t bc = cur < end ? (uint32_t)__ldg(bcol + cur) : 0xffffffffu;
+      // Block-column window in registers, double-buffered: wa holds the
+      // next 8 block columns of this lane's block row, wb the 8 after, whose
+      // loads were issued 8 advances earlier — the merge never waits on a
+      // dependent global load.
+      uint32_t wa[8], wb[8];
+      int wi = 0;
+      int32_t next = cur + 16;  // first block index not yet requested
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        wa[k] = cur + k < end ? (uint32_t)__ldg(bcol + cur + k) : 0xffffffffu;
+        wb[k] = cur + 8 + k < end ? (uint32_t)__ldg(bcol + cur + 8 + k) : 0xffffffffu;
+      }
+      uint32_t bc = wa[0];
       while (true) {
         uint32_t mn = __reduce_min_sync(kFull, bc);
         uint32_t mask = __ballot_sync(kFull, bc == mn && mn != 0xffffffffu);
-        if (lane == 0) {
-          mbar_wait(&sh->empty[stage], phase ^ 1);
-          sh->mask[stage] = mask;
-          if (mask) {
-            uint8_t* st = stages + stage * kGStageBytes;
-            mbar_expect_tx(&sh->full[stage], kTileBytes + __popc(mask) * kABytes);
-            tma_2d(st, &tmap_b, &sh->full[stage], 0, (int)mn * kBlk);
-            tma_2d(st + 2048, &tmap_b, &sh->full[stage], 64, (int)mn * kBlk);
-          } else {
-            mbar_arrive_plain(&sh->full[stage]);  // end-of-group marker
+        uint32_t rest = mask;
+        do {
+          // next chunk: the lowest kMaxA block rows still pending
+          uint32_t chunk = 0, t = rest;
+#pragma unroll
+          for (int k = 0; k < kMaxA; ++k) {
+            uint32_t low = t & (0u - t);
+            chunk |= low;
+            t ^= low;
           }
-        }
-        __syncwarp();
+          rest ^= chunk;
+          if (lane == 0) {
+            mbar_wait(&sh->empty[stage], phase ^ 1);
+            sh->mask[stage] = chunk;
+            if (chunk) {
+              uint8_t* st = stages + stage * kGStageBytes;
+              mbar_expect_tx(&sh->full[stage], kTileBytes + __popc(chunk) * kABytes);
+              tma_2d(st, &tmap_b, &sh->full[stage], 0, (int)mn * kBlk);
+              tma_2d(st + 2048, &tmap_b, &sh->full[stage], 64, (int)mn * kBlk);
+            } else {
+              mbar_arrive_plain(&sh->full[stage]);  // end-of-group marker
+            }
+          }
+          __syncwarp();
+          if (chunk >> lane & 1u) {
+            uint8_t* st = stages + stage * kGStageBytes;
+            int slot = __popc(chunk & ((1u << lane) - 1u));
+            tma_2d(st + kTileBytes + slot * kABytes, &tmap_a, &sh->full[stage], 0, cur * kBlk);
+          }
+          if (++stage == kGStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        } while (rest);
         if (mask >> lane & 1u) {
-          uint8_t* st = stages + stage * kGStageBytes;
-          tma_2d(st + kTileBytes + lane * kABytes, &tmap_a, &sh->full[stage], 0, cur * kBlk);
           ++cur;
-          bc = cur < end ? (uint32_t)__ldg(bcol + cur) : 0xffffffffu;
-        }
-        if (++stage == kGStages) {
-          stage = 0;
-          phase ^= 1;
+          if (++wi == 8) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              wa[k] = wb[k];
+              wb[k] = next + k < end ? (uint32_t)__ldg(bcol + next + k) : 0xffffffffu;
+            }
+            next += 8;
+            wi = 0;
+          }
+          bc = wa[0];
+#pragma unroll
+          for (int k = 1; k < 8; ++k)
+            if (k == wi) bc = wa[k];
         }
         if (!mask) break;
       }
@@ -366,10 +409,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t base = smem_u32(stages + stage * kGStageBytes);
             uint64_t adesc = smem_desc(base, 2048, 1024, 2);
             uint32_t mm = mask;
-            while (mm) {
+            for (int slot = 0; mm; ++slot) {
               int j = __ffs(mm) - 1;
               mm &= mm - 1;
-              uint64_t bdesc = smem_desc(base + kTileBytes + j * kABytes, 16, 256, 6);
+              uint64_t bdesc = smem_desc(base + kTileBytes + slot * kABytes, 16, 256, 6);
               tc_mma(tmem + j * kBlk, adesc, bdesc, kIdesc, (started >> j) & 1u);
             }
             tc_commit(&sh->empty[stage]);

@@ -133,6 +133,68 @@ __global__ void __launch_bounds__(kBlock) k_spmm_rows(const int32_t* __restrict_
   }
 }
 
+// Short rows (a few entries each, e.g. hypersparse DCSR): a warp walks R
+// consecutive rows side by side so R independent B-row gathers are in flight
+// per step; entry (col, val) loads are warp-uniform (broadcast).
+template <typename TB, int V, int R>
+__global__ void __launch_bounds__(kBlock) k_spmm_rows_multi(const int32_t* __restrict__ rows,
+                                                             const int32_t* __restrict__ ptr,
+                                                             const int32_t* __restrict__ col,
+                                                             const float* __restrict__ val,
+                                                             int64_t nrows, Dense d) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int chunks = (d.nd + 32 * V - 1) / (32 * V);
+  const bool vec_ok = (d.nd % (32 * V) == 0) && (d.ldb % V == 0);
+  const int64_t groups = (nrows + R - 1) / R;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < groups * chunks; w += warps) {
+    const int64_t g = w / chunks;
+    const int c0 = (int)(w - g * chunks) * 32 * V + lane * V;
+    const int64_t p0 = g * R;
+    int s[R], e[R];
+    int len = 0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      bool ok = p0 + i < nrows;
+      s[i] = ok ? __ldg(ptr + p0 + i) : 0;
+      e[i] = ok ? __ldg(ptr + p0 + i + 1) : 0;
+      len = max(len, e[i] - s[i]);
+    }
+    float acc[R][V];
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+      for (int v = 0; v < V; ++v) acc[i][v] = 0.f;
+    for (int t = 0; t < len; ++t) {
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+        if (s[i] + t < e[i]) fma_row<TB, V>(d, __ldg(col + s[i] + t), __ldg(val + s[i] + t), c0, vec_ok, acc[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      if (p0 + i >= nrows) break;
+      int64_t r = rows ? __ldg(rows + p0 + i) : p0 + i;
+      store_row<V>(d, r, c0, false, acc[i]);
+    }
+  }
+}
+
+// DCSR: zero the rows that hold no entry (the gaps between consecutive
+// stored rows), instead of clearing all of C before the kernel writes the
+// stored rows. A warp per gap.
+__global__ void __launch_bounds__(kBlock) k_zero_gap_rows(const int32_t* __restrict__ rows, int64_t nnr,
+                                                           int64_t m, int32_t nd, float* __restrict__ c,
+                                                           int64_t ldc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q <= nnr; q += warps) {
+    int64_t lo = q == 0 ? 0 : (int64_t)__ldg(rows + q - 1) + 1;
+    int64_t hi = q == nnr ? m : (int64_t)__ldg(rows + q);
+    for (int64_t r = lo; r < hi; ++r)
+      for (int j = lane; j < nd; j += 32) c[r * ldc + j] = 0.f;
+  }
+}
+
 // ------------------------------------------------------------------- ELL
 template <typename TB, int V>
 __global__ void __launch_bounds__(kBlock) k_spmm_ell(const int32_t* __restrict__ idx,
@@ -296,16 +358,22 @@ void launch_fmt(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
                                                       (int64_t)ctx->sms * 16));
   };
   const float* fv = static_cast<const float*>(a->val);
+  const int64_t stored_rows = a->kind == SFG_DCSR ? a->nnr : a->m;
+  const bool short_rows = stored_rows > 0 && a->nnz <= 8 * stored_rows;  // <= 8 entries per row
+  constexpr int kR = 4;
   switch (a->kind) {
     case SFG_CSR:
-      SFG_LAUNCH((k_spmm_rows<TB, V>), grid_for(a->m * chunks), kBlock, 0, ctx->stream, nullptr,
-                 a->ptr, a->idx, fv, a->m, d);
+    case SFG_DCSR: {
+      if (stored_rows == 0) break;
+      const int32_t* rows = a->kind == SFG_DCSR ? a->row : nullptr;
+      if (short_rows)
+        SFG_LAUNCH((k_spmm_rows_multi<TB, V, kR>), grid_for(ceil_div(stored_rows, kR) * chunks), kBlock, 0,
+                   ctx->stream, rows, a->ptr, a->idx, fv, stored_rows, d);
+      else
+        SFG_LAUNCH((k_spmm_rows<TB, V>), grid_for(stored_rows * chunks), kBlock, 0, ctx->stream, rows,
+                   a->ptr, a->idx, fv, stored_rows, d);
       break;
-    case SFG_DCSR:
-      if (a->nnr)
-        SFG_LAUNCH((k_spmm_rows<TB, V>), grid_for(a->nnr * chunks), kBlock, 0, ctx->stream, a->row,
-                   a->ptr, a->idx, fv, a->nnr, d);
-      break;
+    }
     case SFG_ELL:
       SFG_LAUNCH((k_spmm_ell<TB, V>), grid_for(a->m * chunks), kBlock, 0, ctx->stream, a->idx, fv,
                  (int32_t)a->m, (int32_t)a->k, d);
@@ -363,8 +431,17 @@ void spmm(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dtype, int
     return;
   }
   if (a->kind == SFG_BCSR && spmm_bcsr_tc(ctx, a, b, b_dtype, nd, ldb, c, ldc, accumulate)) return;
-  bool zero_first = !accumulate && (a->kind == SFG_COO || a->kind == SFG_CSC || a->kind == SFG_DCSR ||
-                                    a->kind == SFG_BCSR);
+  if (a->kind == SFG_DCSR && !accumulate && a->m > 0) {
+    // stored rows are written whole by the kernel; only the gaps need zeros
+    SFG_LAUNCH(k_zero_gap_rows, (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a->nnr + 1, kBlock / 32),
+                                                                            (int64_t)ctx->sms * 16)),
+               kBlock, 0, ctx->stream, a->row, a->nnr, a->m, (int32_t)nd, c, ldc);
+    Dense d{b, ldb, c, ldc, (int32_t)nd, 0};
+    if (b_dtype == SFG_BF16) launch_v<__nv_bfloat16>(ctx, a, d);
+    else launch_v<float>(ctx, a, d);
+    return;
+  }
+  bool zero_first = !accumulate && (a->kind == SFG_COO || a->kind == SFG_CSC || a->kind == SFG_BCSR);
   if (zero_first && a->m > 0) {
     if (ldc == nd)
       SFG_CUDA(cudaMemsetAsync(c, 0, a->m * ldc * sizeof(float), ctx->stream));

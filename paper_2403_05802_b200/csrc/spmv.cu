@@ -143,40 +143,52 @@ __device__ __forceinline__ void coo_flush(float* __restrict__ y, int r, float s,
   else y[r] += s;
 }
 
+// Loads are lane-strided (entry base + 32 i + lane: one 128-byte line per
+// warp load, so L1 wavefronts go to the x gathers, not to the streams), the
+// products pass through shared memory (skewed by one word per 16, so both
+// the strided writes and the blocked reads are conflict-free), and each lane
+// then reduces its own kCooRun consecutive entries.
 __global__ void __launch_bounds__(kBlock) k_spmv_coo(const int32_t* __restrict__ row,
                                                       const int32_t* __restrict__ col,
                                                       const float* __restrict__ val,
                                                       const float* __restrict__ x,
                                                       float* __restrict__ y, int64_t nnz) {
-  const int64_t threads = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t * kCooRun < nnz; t += threads) {
-    const int64_t e0 = t * kCooRun;
-    int r[kCooRun], c[kCooRun];
-    float v[kCooRun];
-    if (e0 + kCooRun <= nnz) {
-#pragma unroll
-      for (int q = 0; q < kCooRun / 4; ++q) {
-        // L1-allocating: lane runs are 64 B apart, so each 32 B sector is
-        // touched by two consecutive q steps
-        int4 rr = __ldg(reinterpret_cast<const int4*>(row + e0) + q);
-        int4 cc = __ldg(reinterpret_cast<const int4*>(col + e0) + q);
-        float4 vv = __ldg(reinterpret_cast<const float4*>(val + e0) + q);
-        r[4 * q] = rr.x; r[4 * q + 1] = rr.y; r[4 * q + 2] = rr.z; r[4 * q + 3] = rr.w;
-        c[4 * q] = cc.x; c[4 * q + 1] = cc.y; c[4 * q + 2] = cc.z; c[4 * q + 3] = cc.w;
-        v[4 * q] = vv.x; v[4 * q + 1] = vv.y; v[4 * q + 2] = vv.z; v[4 * q + 3] = vv.w;
-      }
-    } else {
+  constexpr int kSpan = 32 * kCooRun;
+  constexpr int kSkew = kSpan + kSpan / 16;
+  __shared__ int s_row[kBlock / 32][kSkew];
+  __shared__ float s_p[kBlock / 32][kSkew];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  auto sk = [](int j) { return j + (j >> 4); };
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w * kSpan < nnz; w += warps) {
+    const int64_t base = w * kSpan;
+    {
+      int rr[kCooRun], cc[kCooRun];
+      float vv[kCooRun];
 #pragma unroll
       for (int i = 0; i < kCooRun; ++i) {
-        bool ok = e0 + i < nnz;
-        r[i] = ok ? row[e0 + i] : -1;
-        c[i] = ok ? col[e0 + i] : 0;
-        v[i] = ok ? val[e0 + i] : 0.f;
+        int64_t e = base + 32 * i + lane;
+        bool ok = e < nnz;
+        rr[i] = ok ? ld_stream(row + e) : -1;
+        cc[i] = ok ? ld_stream(col + e) : 0;
+        vv[i] = ok ? ld_stream(val + e) : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < kCooRun; ++i) {
+        s_row[wid][sk(32 * i + lane)] = rr[i];
+        s_p[wid][sk(32 * i + lane)] = vv[i] * ldx(x, cc[i]);
       }
     }
+    __syncwarp();
+    int r[kCooRun];
     float p[kCooRun];
 #pragma unroll
-    for (int i = 0; i < kCooRun; ++i) p[i] = v[i] * ldx(x, c[i]);
+    for (int i = 0; i < kCooRun; ++i) {
+      r[i] = s_row[wid][sk(lane * kCooRun + i)];
+      p[i] = s_p[wid][sk(lane * kCooRun + i)];
+    }
+    __syncwarp();
+    if (r[0] < 0) continue;
     const int first = r[0];
     int cur = r[0];
     float s = p[0];

@@ -30,6 +30,5 @@ def check_spmv(y_dev, y_ref, bound, ctx=""):
 
 def dense_abs_bound(r, c, v, m, x):
     """sum_j |a_ij| |x_j| from COO arrays (numpy, f64)."""
-    out = np.zeros(m, np.float64)
-    np.add.at(out, np.asarray(r, np.int64), np.abs(np.asarray(v, np.float64)) * np.abs(x[np.asarray(c, np.int64)]))
-    return out
+    w = np.abs(np.asarray(v, np.float64)) * np.abs(x[np.asarray(c, np.int64)])
+    return np.bincount(np.asarray(r, np.int64), weights=w, minlength=m)

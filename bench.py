@@ -276,10 +276,13 @@ class ClockSampler:
 
     def _run(self):
         N = self.N
+        self.call_ms = []
         while not self.stop.is_set():
             try:
+                t0 = time.perf_counter()
                 self.samples.append((N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM),
                                      N.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+                self.call_ms.append((time.perf_counter() - t0) * 1e3)
             except Exception:
                 pass
             self.stop.wait(self.period)
@@ -301,7 +304,8 @@ class ClockSampler:
                  N.nvmlClocksThrottleReasonSwPowerCap: "sw_power_cap"}
         reasons = sorted({n for _, r in self.samples for bit, n in names.items() if r & bit})
         return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": reasons, "samples": len(self.samples), "source": "NVML, 50 ms period"}
+                "reasons": reasons, "samples": len(self.samples), "source": "NVML, 50 ms period",
+                "nvml_call_ms_max": round(max(self.call_ms), 2) if self.call_ms else None}
 
 
 # ---------------------------------------------------------------- our arm
@@ -434,7 +438,7 @@ def run_ours(args):
                        "parallelism": f"row-partitioned x{world}, NCCL all-gather of the output"
                        if world > 1 else "single GPU", **wl.info},
             "step_ms": {"min": round(min(step_ms), 4), "median": round(statistics.median(step_ms), 4),
-                        "max": round(max(step_ms), 4)},
+                        "max": round(max(step_ms), 4), "all": [round(t, 4) for t in step_ms]},
             "roofline": roof, "kernels": kernels, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }

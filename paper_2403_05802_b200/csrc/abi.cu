@@ -265,9 +265,10 @@ int sfg_from_coo(sfg_context* ctx, int64_t rows, int64_t cols, int64_t nnz, cons
     sfg_tensor* t = nullptr;
     try {
       if (flags & SFG_FLAG_SORTED) {
-        sfg::check_coo_canonical(ctx, drow, dcol, rows, cols, nnz);
+        int zeros = sfg::check_coo_canonical(ctx, drow, dcol, dval, rows, cols, nnz);
         t = sfg::new_tensor(ctx, SFG_COO, rows, cols);
         t->nnz = nnz;
+        t->has_zeros = zeros;
         t->row = sfg::dalloc_n<int32_t>(ctx, nnz);
         t->idx = sfg::dalloc_n<int32_t>(ctx, nnz);
         t->val = sfg::dalloc_n<float>(ctx, nnz);

@@ -286,7 +286,8 @@ __device__ __forceinline__ void mbar_arrive_plain(uint64_t* bar) { mbar_arrive(b
 __global__ void __launch_bounds__(kThreads, 1)
     k_bcsr_tc_group(const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_a,
                     const int32_t* __restrict__ ptr, const int32_t* __restrict__ bcol, int32_t nbr,
-                    int32_t m, float* __restrict__ c, int64_t ldc, int accumulate) {
+                    int32_t m, float* __restrict__ c, int64_t ldc, int accumulate,
+                    const uint32_t* __restrict__ plan, int32_t nbc) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* stages = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   GShared* sh = reinterpret_cast<GShared*>(stages + kGStages * kGStageBytes);
@@ -312,7 +313,85 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = sh->tmem_base;
 
-  if (warp == 4) {
+  // One pipeline step: the B tile of block column `bc` and the value blocks
+  // of the block rows in `mask` (split into stages of <= kMaxA blocks).
+  // Lanes whose bit is set issue their own value-block load and advance.
+  auto issue = [&](uint32_t mask, uint32_t bc, int32_t& cur, int& stage, uint32_t& phase) {
+    uint32_t rest = mask;
+    do {
+      uint32_t chunk = rest;
+      if (__popc(rest) > kMaxA) {  // rare: more than kMaxA block rows share bc
+        chunk = 0;
+        uint32_t t = rest;
+#pragma unroll
+        for (int k = 0; k < kMaxA; ++k) {
+          uint32_t low = t & (0u - t);
+          chunk |= low;
+          t ^= low;
+        }
+      }
+      rest ^= chunk;
+      if (lane == 0) {
+        mbar_wait(&sh->empty[stage], phase ^ 1);
+        sh->mask[stage] = chunk;
+        uint8_t* st = stages + stage * kGStageBytes;
+        mbar_expect_tx(&sh->full[stage], kTileBytes + __popc(chunk) * kABytes);
+        tma_2d(st, &tmap_b, &sh->full[stage], 0, (int)bc * kBlk);
+        tma_2d(st + 2048, &tmap_b, &sh->full[stage], 64, (int)bc * kBlk);
+      }
+      __syncwarp();
+      if (chunk >> lane & 1u) {
+        uint8_t* st = stages + stage * kGStageBytes;
+        int slot = __popc(chunk & ((1u << lane) - 1u));
+        tma_2d(st + kTileBytes + slot * kABytes, &tmap_a, &sh->full[stage], 0, cur * kBlk);
+      }
+      if (++stage == kGStages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    } while (rest);
+    if (mask >> lane & 1u) ++cur;
+  };
+  auto end_group = [&](int& stage, uint32_t& phase) {
+    if (lane == 0) {
+      mbar_wait(&sh->empty[stage], phase ^ 1);
+      sh->mask[stage] = 0;
+      mbar_arrive_plain(&sh->full[stage]);  // end-of-group marker
+    }
+    __syncwarp();
+    if (++stage == kGStages) {
+      stage = 0;
+      phase ^= 1;
+    }
+  };
+
+  if (warp == 4 && plan != nullptr) {
+    // ------------------------------------ producer: stream the mask plan
+    // plan[g * nbc + bc] = bit j set iff block row g*32+j holds block
+    // column bc. Lane l reads the masks of 32 consecutive block columns
+    // (one coalesced load, the next batch prefetched); the nonzero ones are
+    // issued in order.
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int32_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+      const int32_t br = g * kGroup + lane;
+      int32_t cur = br < nbr ? __ldg(ptr + br) : 0;
+      const uint32_t* pg = plan + (int64_t)g * nbc;
+      uint32_t nxt = lane < nbc ? __ldg(pg + lane) : 0u;
+      for (int32_t bc0 = 0; bc0 < nbc; bc0 += 32) {
+        uint32_t mine = nxt;
+        nxt = bc0 + 32 + lane < nbc ? __ldg(pg + bc0 + 32 + lane) : 0u;
+        uint32_t nz = __ballot_sync(kFull, mine != 0);
+        while (nz) {
+          int src = __ffs(nz) - 1;
+          nz &= nz - 1;
+          uint32_t mask = __shfl_sync(kFull, mine, src);
+          issue(mask, (uint32_t)(bc0 + src), cur, stage, phase);
+        }
+      }
+      end_group(stage, phase);
+    }
+  } else if (warp == 4) {
     // ------------------------------------------- producer: k-way merge
     int stage = 0;
     uint32_t phase = 0;
@@ -339,42 +418,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       while (true) {
         uint32_t mn = __reduce_min_sync(kFull, bc);
         uint32_t mask = __ballot_sync(kFull, bc == mn && mn != 0xffffffffu);
-        uint32_t rest = mask;
-        do {
-          // next chunk: the lowest kMaxA block rows still pending
-          uint32_t chunk = 0, t = rest;
-#pragma unroll
-          for (int k = 0; k < kMaxA; ++k) {
-            uint32_t low = t & (0u - t);
-            chunk |= low;
-            t ^= low;
-          }
-          rest ^= chunk;
-          if (lane == 0) {
-            mbar_wait(&sh->empty[stage], phase ^ 1);
-            sh->mask[stage] = chunk;
-            if (chunk) {
-              uint8_t* st = stages + stage * kGStageBytes;
-              mbar_expect_tx(&sh->full[stage], kTileBytes + __popc(chunk) * kABytes);
-              tma_2d(st, &tmap_b, &sh->full[stage], 0, (int)mn * kBlk);
-              tma_2d(st + 2048, &tmap_b, &sh->full[stage], 64, (int)mn * kBlk);
-            } else {
-              mbar_arrive_plain(&sh->full[stage]);  // end-of-group marker
-            }
-          }
-          __syncwarp();
-          if (chunk >> lane & 1u) {
-            uint8_t* st = stages + stage * kGStageBytes;
-            int slot = __popc(chunk & ((1u << lane) - 1u));
-            tma_2d(st + kTileBytes + slot * kABytes, &tmap_a, &sh->full[stage], 0, cur * kBlk);
-          }
-          if (++stage == kGStages) {
-            stage = 0;
-            phase ^= 1;
-          }
-        } while (rest);
+        if (!mask) {
+          end_group(stage, phase);
+          break;
+        }
+        issue(mask, mn, cur, stage, phase);
         if (mask >> lane & 1u) {
-          ++cur;
           if (++wi == 8) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -469,6 +518,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// SpMM plan: plan[g * nbc + bc] |= 1 << (br % 32) for every stored block
+// (br, bc), g = br / 32. A warp per block row, one lane per block.
+__global__ void __launch_bounds__(256) k_bcsr_plan(const int32_t* __restrict__ ptr,
+                                                    const int32_t* __restrict__ bcol, int32_t nbr,
+                                                    int32_t nbc, uint32_t* __restrict__ plan) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t br = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; br < nbr; br += warps) {
+    uint32_t* pg = plan + (br / kGroup) * (int64_t)nbc;
+    const uint32_t bit = 1u << (br % kGroup);
+    for (int32_t k = __ldg(ptr + br) + lane; k < __ldg(ptr + br + 1); k += 32) atomicOr(pg + __ldg(bcol + k), bit);
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -530,9 +593,21 @@ bool spmm_bcsr_tc(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dt
     SFG_LAUNCH(k_bcsr_tc, grid, kThreads, smem, ctx->stream, tb, ta, a->ptr, a->idx, (int32_t)a->nbr,
                (int32_t)a->m, c, ldc, accumulate ? 1 : 0);
   } else {
-    int grid = (int)std::min<int64_t>(ceil_div(a->nbr, kGroup), (int64_t)ctx->sms);
+    // The mask plan (per 32-block-row group, per block column) is built once
+    // per matrix and cached on the tensor; it is used when the group masks
+    // are dense enough that streaming them beats the in-kernel merge.
+    const int64_t ngroups = ceil_div(a->nbr, kGroup);
+    const int64_t words = ngroups * a->nbc;
+    sfg_tensor* mut = const_cast<sfg_tensor*>(a);  // plan is a cache, not tensor state
+    if (!mut->tc_plan && a->nnz * 4 >= words && words <= (int64_t(1) << 30)) {
+      mut->tc_plan = dalloc_n<uint32_t>(ctx, words);
+      SFG_CUDA(cudaMemsetAsync(mut->tc_plan, 0, words * 4, ctx->stream));
+      SFG_LAUNCH(k_bcsr_plan, stream_grid(ctx, a->nbr * 32, 256, 1, 8), 256, 0, ctx->stream, a->ptr, a->idx,
+                 (int32_t)a->nbr, (int32_t)a->nbc, mut->tc_plan);
+    }
+    int grid = (int)std::min<int64_t>(ngroups, (int64_t)ctx->sms);
     SFG_LAUNCH(k_bcsr_tc_group, grid, kThreads, gsmem, ctx->stream, tb, ta, a->ptr, a->idx, (int32_t)a->nbr,
-               (int32_t)a->m, c, ldc, accumulate ? 1 : 0);
+               (int32_t)a->m, c, ldc, accumulate ? 1 : 0, mut->tc_plan, (int32_t)a->nbc);
   }
   return true;
 }

@@ -21,10 +21,11 @@ namespace {
 constexpr int kBlock = 256;
 
 // ---------------------------------------------------------------- checks
-enum { kBadRange = 1, kDuplicate = 2, kUnsorted = 4 };
+enum { kBadRange = 1, kDuplicate = 2, kUnsorted = 4, kZeroValue = 8 };
 
 __global__ void __launch_bounds__(kBlock) k_check_canonical(const int32_t* __restrict__ row,
                                                              const int32_t* __restrict__ col,
+                                                             const float* __restrict__ val,
                                                              int64_t nnz, int32_t m, int32_t n,
                                                              int* __restrict__ flags) {
   int f = 0;
@@ -32,6 +33,7 @@ __global__ void __launch_bounds__(kBlock) k_check_canonical(const int32_t* __res
        e += (int64_t)gridDim.x * blockDim.x) {
     int r = row[e], c = col[e];
     if (r < 0 || r >= m || c < 0 || c >= n) f |= kBadRange;
+    if (val[e] == 0.f) f |= kZeroValue;  // explicit zeros: recorded, not an error
     if (e > 0) {
       int pr = row[e - 1], pc = col[e - 1];
       if (pr == r && pc == c) f |= kDuplicate;
@@ -215,12 +217,12 @@ __global__ void k_slice_rows(const int32_t* __restrict__ row, const int32_t* __r
 
 }  // namespace
 
-void check_coo_canonical(sfg_context* ctx, const int32_t* row, const int32_t* col, int64_t m,
-                         int64_t n, int64_t nnz) {
-  if (nnz == 0) return;
+int check_coo_canonical(sfg_context* ctx, const int32_t* row, const int32_t* col, const float* val,
+                        int64_t m, int64_t n, int64_t nnz) {
+  if (nnz == 0) return 0;
   int* flags = static_cast<int*>(scratch(ctx, 64));
   SFG_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), ctx->stream));
-  SFG_LAUNCH(k_check_canonical, stream_grid(ctx, nnz, kBlock, 4), kBlock, 0, ctx->stream, row, col,
+  SFG_LAUNCH(k_check_canonical, stream_grid(ctx, nnz, kBlock, 4), kBlock, 0, ctx->stream, row, col, val,
              nnz, (int32_t)m, (int32_t)n, flags);
   int f = 0;
   read_back(ctx, flags, sizeof f, &f);
@@ -228,11 +230,13 @@ void check_coo_canonical(sfg_context* ctx, const int32_t* row, const int32_t* co
   if (f & kUnsorted)
     raise(SFG_ERR_INVALID_OPERATION, "input flagged SORTED is not (row, col)-sorted");
   if (f & kDuplicate) raise(SFG_ERR_DUPLICATE_COORDINATE, "duplicate coordinate");
+  return (f & kZeroValue) ? 1 : 0;
 }
 
 sfg_tensor* coo_to_coo(sfg_context* ctx, const sfg_tensor* s) {
   sfg_tensor* t = new_tensor(ctx, SFG_COO, s->m, s->n);
   t->nnz = s->nnz;
+  t->has_zeros = s->has_zeros;
   t->row = dalloc_n<int32_t>(ctx, s->nnz);
   t->idx = dalloc_n<int32_t>(ctx, s->nnz);
   t->val = dalloc_n<float>(ctx, s->nnz);
@@ -337,6 +341,7 @@ sfg_tensor* coo_slice_rows(sfg_context* ctx, const sfg_tensor* coo, int64_t r0, 
   sfg_tensor* t = new_tensor(ctx, SFG_COO, r1 - r0, coo->n);
   int64_t count = pos[1] - pos[0];
   t->nnz = count;
+  t->has_zeros = coo->has_zeros == 0 ? 0 : -1;
   t->row = dalloc_n<int32_t>(ctx, count);
   t->idx = dalloc_n<int32_t>(ctx, count);
   t->val = dalloc_n<float>(ctx, count);

@@ -57,17 +57,18 @@ __global__ void __launch_bounds__(kBlock) k_row_ptr(const int32_t* __restrict__ 
       int64_t e0 = v << 2;
       int r[4];
       float x[4];
+      // val == nullptr: the source is known zero-free; rows only
       if (e0 + 4 <= nnz) {
         int4 rr = ld_stream(reinterpret_cast<const int4*>(row + e0));
-        float4 vv = ld_stream(reinterpret_cast<const float4*>(val + e0));
         r[0] = rr.x; r[1] = rr.y; r[2] = rr.z; r[3] = rr.w;
+        float4 vv = val ? ld_stream(reinterpret_cast<const float4*>(val + e0)) : make_float4(1.f, 1.f, 1.f, 1.f);
         x[0] = vv.x; x[1] = vv.y; x[2] = vv.z; x[3] = vv.w;
       } else {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           bool ok = e0 + i < nnz;
           r[i] = ok ? row[e0 + i] : -1;
-          x[i] = ok ? val[e0 + i] : 1.f;
+          x[i] = (ok && val) ? val[e0 + i] : 1.f;
         }
       }
       int prev = e0 == 0 ? -1 : row[e0 - 1];
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(kBlock) k_row_scan(const int32_t* __restrict__
   for (int i = threadIdx.x; i <= kScanTile; i += kBlock) {
     int64_t r = tile0 + i;
     sp[sk(i)] = r <= m ? __ldg(ptr + r) : 0;
-    if (i < kScanTile) sz[sk(i)] = r < m ? __ldg(zcnt + r) : 0;
+    if (i < kScanTile) sz[sk(i)] = (has_zeros && r < m) ? __ldg(zcnt + r) : 0;
   }
   __syncthreads();
   const int t0 = threadIdx.x * kScanItems;
@@ -294,25 +295,31 @@ struct RowInfo {
 RowInfo row_info(sfg_context* ctx, const sfg_tensor* s, int64_t min_sum, int32_t* totals) {
   RowInfo ri;
   const int64_t m = s->m;
+  // Explicit zeros only matter when the source may hold them: a tensor known
+  // to be zero-free (from_coo checked it, or a generator built it) skips the
+  // value stream and the per-row zero counts entirely.
+  const bool zeros_possible = s->has_zeros != 0;
   ri.ptr = dalloc_n<int32_t>(ctx, m + 1);
-  ri.zcnt = dalloc_n<int32_t>(ctx, m);
+  ri.zcnt = zeros_possible ? dalloc_n<int32_t>(ctx, m) : nullptr;
   ri.off = dalloc_n<uint32_t>(ctx, m);
   int tiles = (int)ceil_div(m, kScanTile);
   auto* status = lookback_status(ctx, tiles);
   auto* tail = static_cast<int32_t*>(scratch(ctx, 64));  // [any_zero, nnz_sel, k_max]
   SFG_CUDA(cudaMemsetAsync(tail, 0, 16, ctx->stream));
-  SFG_CUDA(cudaMemsetAsync(ri.zcnt, 0, m * sizeof(int32_t), ctx->stream));
+  if (zeros_possible) SFG_CUDA(cudaMemsetAsync(ri.zcnt, 0, m * sizeof(int32_t), ctx->stream));
   if (s->nnz == 0) {
     SFG_CUDA(cudaMemsetAsync(ri.ptr, 0, (m + 1) * sizeof(int32_t), ctx->stream));
   } else {
     int64_t nvec = ceil_div(s->nnz, 4);
     SFG_LAUNCH(k_row_ptr, stream_grid(ctx, nvec, kBlock, 1, 8), kBlock, 0, ctx->stream, s->row,
-               static_cast<const float*>(s->val), s->nnz, (int32_t)m, ri.ptr, ri.zcnt, tail);
+               zeros_possible ? static_cast<const float*>(s->val) : nullptr, s->nnz, (int32_t)m, ri.ptr,
+               ri.zcnt, tail);
   }
   // zcnt is exact (zeroed, incremented only for zero values), so the scan
-  // always subtracts it; the flag only selects the ELL fill's slow path.
-  SFG_LAUNCH(k_row_scan, tiles, kBlock, 0, ctx->stream, ri.ptr, ri.zcnt, 1, (int32_t)m, min_sum,
-             ri.off, totals, status, ctx->epoch++, reinterpret_cast<ScanOut*>(tail + 1));
+  // subtracts it whenever it exists; the flag only selects the ELL fill's
+  // slow path.
+  SFG_LAUNCH(k_row_scan, tiles, kBlock, 0, ctx->stream, ri.ptr, ri.zcnt, zeros_possible ? 1 : 0, (int32_t)m,
+             min_sum, ri.off, totals, status, ctx->epoch++, reinterpret_cast<ScanOut*>(tail + 1));
   int32_t h[4];
   read_back(ctx, tail, 16, h);
   ri.has_zeros = h[0];
@@ -362,6 +369,7 @@ void decompose_rows(sfg_context* ctx, const sfg_tensor* s, int64_t min_sum, sfg_
   RowInfo ri = row_info(ctx, s, min_sum, totals);
   sfg_tensor* a = coo_part(ctx, s->m, s->n, ri.nnz_sel);
   sfg_tensor* b = coo_part(ctx, s->m, s->n, s->nnz - ri.nnz_sel);
+  a->has_zeros = b->has_zeros = s->has_zeros == 0 ? 0 : -1;
   if (s->nnz)
     SFG_LAUNCH(k_split, stream_grid(ctx, ceil_div(s->nnz, kSplitRun), kBlock, 1, 8), kBlock, 0, ctx->stream,
                s->row, s->idx, static_cast<const float*>(s->val), s->nnz, ri.off, a->row, a->idx,
@@ -384,6 +392,7 @@ sfg_tensor* coo_to_hyb(sfg_context* ctx, const sfg_tensor* s, int64_t min_sum) {
   sfg_tensor* h = new_tensor(ctx, SFG_HYB, s->m, s->n);
   h->threshold = min_sum;
   h->part[1] = coo_part(ctx, s->m, s->n, ri.nnz_sel);
+  h->part[1]->has_zeros = s->has_zeros == 0 ? 0 : -1;
   if (s->nnz)
     SFG_LAUNCH(k_split, stream_grid(ctx, ceil_div(s->nnz, kSplitRun), kBlock, 1, 8), kBlock, 0, ctx->stream,
                s->row, s->idx, static_cast<const float*>(s->val), s->nnz, ri.off, h->part[1]->row,

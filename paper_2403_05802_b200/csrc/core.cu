@@ -95,6 +95,8 @@ void free_tensor_arrays(sfg_tensor* t) {
   dfree(ctx, t->idx);
   dfree(ctx, t->slots);
   dfree(ctx, t->val);
+  dfree(ctx, t->tc_plan);
+  t->tc_plan = nullptr;
   t->row = t->ptr = t->idx = t->slots = nullptr;
   t->val = nullptr;
 }

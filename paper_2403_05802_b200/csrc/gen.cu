@@ -72,6 +72,7 @@ int64_t unique_positions(sfg_context* ctx, const uint64_t* keys, int64_t n, int3
 sfg_tensor* gen_uniform(sfg_context* ctx, uint64_t seed, int64_t m, int64_t n, int per_row) {
   sfg_tensor* t = new_tensor(ctx, SFG_COO, m, n);
   t->nnz = m * per_row;
+  t->has_zeros = 0;  // generator values are +-[0.5, 1.5)
   t->row = dalloc_n<int32_t>(ctx, t->nnz);
   t->idx = dalloc_n<int32_t>(ctx, t->nnz);
   t->val = dalloc_n<float>(ctx, t->nnz);
@@ -93,6 +94,7 @@ sfg_tensor* gen_from_keys(sfg_context* ctx, uint64_t seed, int kind, int scale, 
   int64_t u = unique_positions(ctx, sorted, draws, pos);
   sfg_tensor* t = new_tensor(ctx, SFG_COO, m, n);
   t->nnz = u;
+  t->has_zeros = 0;
   t->row = dalloc_n<int32_t>(ctx, u);
   t->idx = dalloc_n<int32_t>(ctx, u);
   t->val = dalloc_n<float>(ctx, u);

@@ -78,6 +78,8 @@ struct sfg_tensor {
   int64_t rb = 0, cb = 0;        // BCSR level-2/3 extents (== r, c except one-tile edge)
   int64_t nbr = 0, nbc = 0;      // BCSR block grid
   int64_t threshold = 0;         // HYB min_sum
+  int32_t has_zeros = -1;        // COO: explicit zero values present? 1/0, -1 unknown
+  uint32_t* tc_plan = nullptr;   // BCSR: cached tensor-core SpMM plan (bcsr_tc.cu)
   int32_t* row = nullptr;
   int32_t* ptr = nullptr;
   int32_t* idx = nullptr;
@@ -122,7 +124,8 @@ inline int stream_grid(const sfg_context* ctx, int64_t work_items, int block, in
 
 // ----------------------------------------------------- kernel entry points
 // (defined in the per-area .cu files, called from abi.cu)
-void check_coo_canonical(sfg_context* ctx, const int32_t* row, const int32_t* col, int64_t m,
+// Validates a caller-sorted COO; returns 1 when it holds explicit zero values.
+int check_coo_canonical(sfg_context* ctx, const int32_t* row, const int32_t* col, const float* val, int64_t m,
                          int64_t n, int64_t nnz);
 sfg_tensor* sort_coo(sfg_context* ctx, int64_t m, int64_t n, int64_t nnz, const int32_t* row,
                      const int32_t* col, const float* val, bool sum_duplicates);

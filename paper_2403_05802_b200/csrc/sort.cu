@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(kBlock) k_unique_pos(const uint64_t* __restric
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *total = (int32_t)(tp + tot);
 }
 
-enum { kBadRange = 1 };
+enum { kBadRange = 1, kZeroValue = 2 };
 
 __global__ void __launch_bounds__(kBlock) k_make_keys(const int32_t* __restrict__ row,
                                                        const int32_t* __restrict__ col,
@@ -203,7 +203,8 @@ __global__ void __launch_bounds__(kBlock) k_make_keys(const int32_t* __restrict_
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
        e += (int64_t)gridDim.x * blockDim.x) {
     int r = row[e], c = col[e];
-    if (r < 0 || r >= m || c < 0 || c >= n) f = kBadRange;
+    if (r < 0 || r >= m || c < 0 || c >= n) f |= kBadRange;
+    if (val[e] == 0.f) f |= kZeroValue;
     keys[e] = ((uint64_t)(uint32_t)r << cbits) | (uint32_t)c;
     pay[e] = __float_as_uint(val[e]);
   }
@@ -359,6 +360,9 @@ sfg_tensor* sort_coo(sfg_context* ctx, int64_t m, int64_t n, int64_t nnz, const 
               std::to_string(k & ((1ull << cbits) - 1)) + ")");
   }
   t->nnz = uniq;
+  // summed duplicates may cancel to zero: only a duplicate-free input keeps
+  // the zero-free guarantee
+  t->has_zeros = (f & kZeroValue) ? 1 : (sum_duplicates && res[0] != ~0ull ? -1 : 0);
   t->row = dalloc_n<int32_t>(ctx, uniq);
   t->idx = dalloc_n<int32_t>(ctx, uniq);
   t->val = dalloc_n<float>(ctx, uniq);

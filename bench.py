@@ -23,6 +23,7 @@ scale 22 + log2 N), y reassembled with an NCCL all-gather.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -139,9 +140,10 @@ class Cfg2(SpmvWorkload):
 
     def convert_bytes(self):
         i = self.info
-        # count pass (row + val) + row pointers, split (row, col, val read;
-        # COO part written), ELL cells written
-        return 8 * self.nnz + 4 * self.m + 12 * self.nnz + 12 * i["nnz_coo"] + 8 * i["ell_cells"]
+        # count pass over the rows (4 nnz; the source is known
+        # zero-free, so values are not read) + row pointers, split (row, col,
+        # val read once), COO part written, ELL cells written
+        return 4 * self.nnz + 4 * self.m + 12 * self.nnz + 12 * i["nnz_coo"] + 8 * i["ell_cells"]
 
     def spmv_bytes(self):
         i = self.info
@@ -353,6 +355,11 @@ def run_ours(args):
         return [s.elapsed_time(e) for s, e in ev]
 
     warm = max(args.warmup, 3)
+    # a full (gen-2) Python GC pass over torch's object graph can stall the
+    # host for hundreds of ms in the middle of a step: collect now, then keep
+    # the collector off for the measurement
+    gc.collect()
+    gc.disable()
     for _ in range(warm):
         step()
     torch.cuda.synchronize()

@@ -208,7 +208,8 @@ __global__ void __launch_bounds__(kBlock) k_make_keys(const int32_t* __restrict_
     keys[e] = ((uint64_t)(uint32_t)r << cbits) | (uint32_t)c;
     pay[e] = __float_as_uint(val[e]);
   }
-  if (__reduce_or_sync(kFull, f) && (threadIdx.x & 31) == 0) atomicOr(flags, f);
+  f = __reduce_or_sync(kFull, f);
+  if (f && (threadIdx.x & 31) == 0) atomicOr(flags, f);
 }
 
 // Unique keys -> canonical COO. With sum_duplicates, the head of each run

@@ -45,6 +45,14 @@ def test_from_coo_errors(ctx):
     assert ei.value.kind == "DuplicateCoordinate"
     t = ctx.from_coo(3, 3, [1, 0, 1], [2, 0, 2], [5.0, 1.0, 7.0], sum_duplicates=True)
     assert t.coo_arrays()[2].tolist() == [1.0, 12.0]
+    # the offending entry sits in a lane other than 0 of its warp
+    rows = np.arange(40) % 5
+    rows[37] = 9
+    for sorted_input in (False, True):
+        with pytest.raises(sfg.SfgError) as ei:
+            ctx.from_coo(5, 40, rows if not sorted_input else np.sort(rows), np.arange(40), np.ones(40),
+                         sorted=sorted_input)
+        assert ei.value.kind == "InvalidOperation"
 
 
 @pytest.mark.parametrize("seed", range(6))

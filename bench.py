@@ -345,14 +345,19 @@ def run_ours(args):
 
     def timed(fn, k, flush_between=True):
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
+        host_ms.clear()
         for i in range(k):
             if flush_between:
                 flush.zero_()
             ev[i][0].record(stream)
+            h0 = time.perf_counter()
             fn()
+            host_ms.append((time.perf_counter() - h0) * 1e3)
             ev[i][1].record(stream)
         torch.cuda.synchronize()
         return [s.elapsed_time(e) for s, e in ev]
+
+    host_ms = []
 
     warm = max(args.warmup, 3)
     # a full (gen-2) Python GC pass over torch's object graph can stall the
@@ -377,6 +382,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         l0 = sfg.launch_count()
         step_ms = timed(step, args.steps)
+        step_host_ms = list(host_ms)
         launches = sfg.launch_count() - l0
         if world > 1:
             dist.barrier()
@@ -445,7 +451,8 @@ def run_ours(args):
                        "parallelism": f"row-partitioned x{world}, NCCL all-gather of the output"
                        if world > 1 else "single GPU", **wl.info},
             "step_ms": {"min": round(min(step_ms), 4), "median": round(statistics.median(step_ms), 4),
-                        "max": round(max(step_ms), 4), "all": [round(t, 4) for t in step_ms]},
+                        "max": round(max(step_ms), 4), "all": [round(t, 4) for t in step_ms],
+                        "host_enqueue_ms": [round(t, 3) for t in step_host_ms]},
             "roofline": roof, "kernels": kernels, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }

@@ -107,9 +107,14 @@ typedef struct sfg_tensor_view {
 const char* sfg_last_error(void);
 /* stream: a cudaStream_t, or NULL for the legacy default stream. */
 int sfg_context_create(int device, void* stream, sfg_context** out);
+/* Waits for the old stream before switching (cached blocks move with it). */
 int sfg_context_set_stream(sfg_context* ctx, void* stream);
 int sfg_context_destroy(sfg_context* ctx);
 int sfg_context_synchronize(sfg_context* ctx);
+/* Device memory freed by tensors stays cached in the context for the next
+ * conversion; this returns the cached blocks to the driver pool. bytes_out
+ * (optional) receives how many bytes were cached before the call. */
+int sfg_context_release_cached(sfg_context* ctx, int64_t* bytes_out);
 
 /* ------------------------------------------------------- format / planner */
 /* resolve_format (formats.hpp:92-125) for the names above: "COO", "CSR",

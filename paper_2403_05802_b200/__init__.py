@@ -108,6 +108,7 @@ def load():
         "sfg_context_set_stream": (C.c_int, [vp, vp]),
         "sfg_context_destroy": (C.c_int, [vp]),
         "sfg_context_synchronize": (C.c_int, [vp]),
+        "sfg_context_release_cached": (C.c_int, [vp, C.POINTER(i64)]),
         "sfg_format_resolve": (C.c_int, [C.c_char_p, C.POINTER(Format)]),
         "sfg_plan_text": (C.c_int, [C.POINTER(Format), C.POINTER(Format), C.c_char_p, i64]),
         "sfg_storage_explain": (C.c_int, [C.POINTER(Format), C.c_char_p, i64]),
@@ -293,6 +294,13 @@ class Context:
 
     def synchronize(self):
         _check(self.lib.sfg_context_synchronize(self.h))
+
+    def release_cached(self) -> int:
+        """Return the context's cached device blocks to the driver pool;
+        returns how many bytes were cached."""
+        b = C.c_int64()
+        _check(self.lib.sfg_context_release_cached(self.h, C.byref(b)))
+        return b.value
 
     def buffer(self, nbytes) -> DeviceBuffer:
         return DeviceBuffer(self, nbytes)

@@ -150,7 +150,16 @@ int sfg_context_create(int device, void* stream, sfg_context** out) {
 int sfg_context_set_stream(sfg_context* ctx, void* stream) {
   return guard([&] {
     require(ctx, SFG_ERR_INVALID_OPERATION, "null context");
+    SFG_CUDA(cudaStreamSynchronize(ctx->stream));
     ctx->stream = static_cast<cudaStream_t>(stream);
+  });
+}
+
+int sfg_context_release_cached(sfg_context* ctx, int64_t* bytes_out) {
+  return guard([&] {
+    require(ctx, SFG_ERR_INVALID_OPERATION, "null context");
+    if (bytes_out) *bytes_out = static_cast<int64_t>(ctx->cached_bytes);
+    sfg::release_cached(ctx);
   });
 }
 
@@ -163,6 +172,7 @@ int sfg_context_destroy(sfg_context* ctx) {
     if (!ctx) return;
     if (ctx->scratch) sfg::dfree(ctx, ctx->scratch);
     if (ctx->status) sfg::dfree(ctx, ctx->status);
+    sfg::release_cached(ctx);
     cudaStreamSynchronize(ctx->stream);
     cudaFreeHost(ctx->pinned);
     delete ctx;

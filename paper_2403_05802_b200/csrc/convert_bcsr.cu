@@ -37,16 +37,13 @@ __global__ void __launch_bounds__(kBlock) k_brow_ptr(const int32_t* __restrict__
   const int64_t base0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
   for (int64_t wbase = base0; wbase < nnz; wbase += stride) {
     int64_t e = wbase + (threadIdx.x & 31);
-    Gap g[5];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) g[i] = {1, 0, 0};
+    int32_t b[1] = {0}, prev = 0, end_hi = 0;  // lanes past nnz write nothing
     if (e < nnz) {
-      int b = __ldg(row + e) / r;
-      int prev = e == 0 ? -1 : __ldg(row + e - 1) / r;
-      g[0] = {prev + 1, b, (int32_t)e};
-      if (e == nnz - 1) g[1] = {b + 1, nbr, (int32_t)nnz};
+      b[0] = __ldg(row + e) / r;
+      prev = e == 0 ? -1 : __ldg(row + e - 1) / r;
+      end_hi = e == nnz - 1 ? nbr : b[0];
     }
-    fill_gaps(g, bptr);
+    write_row_ptr<1>(b, prev, (int32_t)e, end_hi, (int32_t)nnz, bptr);
   }
 }
 

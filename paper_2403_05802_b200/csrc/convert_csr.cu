@@ -45,58 +45,43 @@ __global__ void __launch_bounds__(kBlock) k_check_canonical(const int32_t* __res
 }
 
 // ----------------------------------------------------------- COO -> CSR
-// One thread owns 4 consecutive entries (128-bit loads/stores of row, col,
-// val). Row boundaries inside its run write ptr[q] = e for every row q in
+// A lane owns 2 x 4 consecutive entries (128-bit loads/stores of row, col,
+// val). Row boundaries inside its runs write ptr[q] = e for every row q in
 // (row[e-1], row[e]]; the owner of the last entry closes ptr up to m.
-// Empty-row gaps longer than a warp are filled cooperatively by the warp.
+// Long empty-row gaps are filled cooperatively by the warp (write_row_ptr).
 __global__ void __launch_bounds__(kBlock) k_coo_to_csr(const int32_t* __restrict__ row,
                                                         const int32_t* __restrict__ col,
                                                         const float* __restrict__ val, int64_t nnz,
                                                         int32_t m, int32_t* __restrict__ ptr,
                                                         int32_t* __restrict__ ocol,
                                                         float* __restrict__ oval) {
-  const int64_t nvec = (nnz + 3) >> 2;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  // uniform trip count across the warp (fill_gaps uses warp collectives)
-  const int64_t base0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
-  for (int64_t wbase = base0; wbase < nvec; wbase += stride) {
-    int64_t v = wbase + (threadIdx.x & 31);
-    Gap g[5];
+  const int lane = threadIdx.x & 31;
+  const int64_t nchunk = (nnz + 255) >> 8;
+  const int64_t warps = (int64_t)gridDim.x * (kBlock / 32);
+  // a warp per 256-entry chunk: uniform trip count (write_row_ptr is a warp
+  // collective)
+  for (int64_t ch = (int64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); ch < nchunk; ch += warps) {
+    const int64_t base = ch << 8;
+    RowChunk c;
+    load_row_chunk(row, nnz, base, c);
 #pragma unroll
-    for (int i = 0; i < 5; ++i) g[i] = {1, 0, 0};
-    if (v < nvec) {
-      int64_t e0 = v << 2;
-      int r[4];
-      if (e0 + 4 <= nnz) {
-        int4 rr = ld_stream(reinterpret_cast<const int4*>(row + e0));
+    for (int g = 0; g < 2; ++g) {
+      int64_t e0 = base + 128 * g + 4 * lane;
+      if (c.full) {
         int4 cc = ld_stream(reinterpret_cast<const int4*>(col + e0));
         float4 vv = ld_stream(reinterpret_cast<const float4*>(val + e0));
         st_stream(reinterpret_cast<int4*>(ocol + e0), cc);
         st_stream(reinterpret_cast<float4*>(oval + e0), vv);
-        r[0] = rr.x; r[1] = rr.y; r[2] = rr.z; r[3] = rr.w;
       } else {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < 4; ++i)
           if (e0 + i < nnz) {
-            r[i] = row[e0 + i];
             ocol[e0 + i] = col[e0 + i];
             oval[e0 + i] = val[e0 + i];
-          } else {
-            r[i] = -1;
           }
-        }
       }
-      int prev = e0 == 0 ? -1 : row[e0 - 1];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        if (e0 + i < nnz) {
-          g[i] = {prev + 1, r[i], (int32_t)(e0 + i)};
-          prev = r[i];
-        }
-      }
-      if (e0 + 4 >= nnz) g[4] = {prev + 1, m, (int32_t)nnz};
     }
-    fill_gaps(g, ptr);
+    chunk_row_ptr(c, nnz, base, m, ptr);
   }
 }
 
@@ -253,7 +238,7 @@ void compress_sorted(sfg_context* ctx, const int32_t* key, const int32_t* other,
                extent + 1, 0);
     return;
   }
-  SFG_LAUNCH(k_coo_to_csr, stream_grid(ctx, ceil_div(nnz, 4), kBlock, 1, 8), kBlock, 0, ctx->stream,
+  SFG_LAUNCH(k_coo_to_csr, stream_grid(ctx, ceil_div(nnz, 256), kBlock / 32, 1, 8), kBlock, 0, ctx->stream,
              key, other, val, nnz, (int32_t)extent, ptr, oidx, oval);
 }
 
@@ -268,8 +253,7 @@ sfg_tensor* coo_to_csr(sfg_context* ctx, const sfg_tensor* s) {
                s->m + 1, 0);
     return t;
   }
-  int64_t nvec = ceil_div(s->nnz, 4);
-  SFG_LAUNCH(k_coo_to_csr, stream_grid(ctx, nvec, kBlock, 1, 8), kBlock, 0, ctx->stream, s->row,
+  SFG_LAUNCH(k_coo_to_csr, stream_grid(ctx, ceil_div(s->nnz, 256), kBlock / 32, 1, 8), kBlock, 0, ctx->stream, s->row,
              s->idx, static_cast<const float*>(s->val), s->nnz, (int32_t)s->m, t->ptr, t->idx,
              static_cast<float*>(t->val));
   return t;

@@ -39,55 +39,46 @@ constexpr int kBlock = 256;
 constexpr uint32_t kSelBit = 0x80000000u;
 
 // --------------------------------------------------------- 1. row pointers
+// A warp handles 256 consecutive entries per iteration (two coalesced 512 B
+// row loads in flight per lane pair). kVals: the source may hold explicit
+// zeros, so values are read too; a zero-free source reads rows only.
+template <bool kVals>
 __global__ void __launch_bounds__(kBlock) k_row_ptr(const int32_t* __restrict__ row,
                                                      const float* __restrict__ val, int64_t nnz,
                                                      int32_t m, int32_t* __restrict__ ptr,
                                                      int32_t* __restrict__ zcnt,
                                                      int* __restrict__ any_zero) {
-  const int64_t nvec = (nnz + 3) >> 2;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t base0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+  const int lane = threadIdx.x & 31;
+  const int64_t nchunk = (nnz + 255) >> 8;
+  const int64_t warps = (int64_t)gridDim.x * (kBlock / 32);
   bool saw_zero = false;
-  for (int64_t wbase = base0; wbase < nvec; wbase += stride) {
-    int64_t v = wbase + (threadIdx.x & 31);
-    Gap g[5];
+  for (int64_t ch = (int64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); ch < nchunk; ch += warps) {
+    const int64_t base = ch << 8;
+    RowChunk c;
+    load_row_chunk(row, nnz, base, c);
+    if (kVals) {
 #pragma unroll
-    for (int i = 0; i < 5; ++i) g[i] = {1, 0, 0};
-    if (v < nvec) {
-      int64_t e0 = v << 2;
-      int r[4];
-      float x[4];
-      // val == nullptr: the source is known zero-free; rows only
-      if (e0 + 4 <= nnz) {
-        int4 rr = ld_stream(reinterpret_cast<const int4*>(row + e0));
-        r[0] = rr.x; r[1] = rr.y; r[2] = rr.z; r[3] = rr.w;
-        float4 vv = val ? ld_stream(reinterpret_cast<const float4*>(val + e0)) : make_float4(1.f, 1.f, 1.f, 1.f);
-        x[0] = vv.x; x[1] = vv.y; x[2] = vv.z; x[3] = vv.w;
-      } else {
+      for (int g = 0; g < 2; ++g) {
+        int64_t e0 = base + 128 * g + 4 * lane;
+        float x[4];
+        if (c.full) {
+          float4 vv = ld_stream(reinterpret_cast<const float4*>(val + e0));
+          x[0] = vv.x; x[1] = vv.y; x[2] = vv.z; x[3] = vv.w;
+        } else {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          bool ok = e0 + i < nnz;
-          r[i] = ok ? row[e0 + i] : -1;
-          x[i] = (ok && val) ? val[e0 + i] : 1.f;
+          for (int i = 0; i < 4; ++i) x[i] = e0 + i < nnz ? val[e0 + i] : 1.f;
         }
-      }
-      int prev = e0 == 0 ? -1 : row[e0 - 1];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        if (e0 + i < nnz) {
-          g[i] = {prev + 1, r[i], (int32_t)(e0 + i)};
-          prev = r[i];
+        for (int i = 0; i < 4; ++i)
           if (x[i] == 0.f) {
-            atomicAdd(zcnt + r[i], 1);
+            atomicAdd(zcnt + c.r[g][i], 1);
             saw_zero = true;
           }
-        }
       }
-      if (e0 + 4 >= nnz) g[4] = {prev + 1, m, (int32_t)nnz};
     }
-    fill_gaps(g, ptr);
+    chunk_row_ptr(c, nnz, base, m, ptr);
   }
-  if (__any_sync(kFull, saw_zero) && (threadIdx.x & 31) == 0) atomicOr(any_zero, 1);
+  if (kVals && __any_sync(kFull, saw_zero) && lane == 0) atomicOr(any_zero, 1);
 }
 
 // ------------------------------------------------------------ 2. row scan
@@ -310,10 +301,13 @@ RowInfo row_info(sfg_context* ctx, const sfg_tensor* s, int64_t min_sum, int32_t
   if (s->nnz == 0) {
     SFG_CUDA(cudaMemsetAsync(ri.ptr, 0, (m + 1) * sizeof(int32_t), ctx->stream));
   } else {
-    int64_t nvec = ceil_div(s->nnz, 4);
-    SFG_LAUNCH(k_row_ptr, stream_grid(ctx, nvec, kBlock, 1, 8), kBlock, 0, ctx->stream, s->row,
-               zeros_possible ? static_cast<const float*>(s->val) : nullptr, s->nnz, (int32_t)m, ri.ptr,
-               ri.zcnt, tail);
+    int grid = stream_grid(ctx, ceil_div(s->nnz, 256), kBlock / 32, 1, 8);
+    if (zeros_possible)
+      SFG_LAUNCH(k_row_ptr<true>, grid, kBlock, 0, ctx->stream, s->row, static_cast<const float*>(s->val),
+                 s->nnz, (int32_t)m, ri.ptr, ri.zcnt, tail);
+    else
+      SFG_LAUNCH(k_row_ptr<false>, grid, kBlock, 0, ctx->stream, s->row, nullptr, s->nnz, (int32_t)m,
+                 ri.ptr, ri.zcnt, tail);
   }
   // zcnt is exact (zeroed, incremented only for zero values), so the scan
   // subtracts it whenever it exists; the flag only selects the ELL fill's

@@ -1,4 +1,5 @@
 // core.cu — context, allocation, tensor lifetime and error plumbing.
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -36,19 +37,82 @@ void raise_cuda(cudaError_t e, const char* what, const char* file, int line) {
   raise(e == cudaErrorMemoryAllocation ? SFG_ERR_OOM : SFG_ERR_CUDA, buf);
 }
 
-void* dalloc(sfg_context* ctx, size_t bytes) {
+static bool trace_alloc() {
+  static const bool on = [] {
+    const char* v = std::getenv("SFG_TRACE_ALLOC");
+    return v && *v && *v != '0';
+  }();
+  return on;
+}
+
+// Size classes: powers of two up to 1 MB, then multiples of 2 MB. A cached
+// block serves a request of at least 7/8 of its size, so repeated
+// conversions of one matrix reuse their blocks exactly.
+static size_t size_class(size_t bytes) {
+  if (bytes <= (1u << 20)) {
+    size_t c = 512;
+    while (c < bytes) c <<= 1;
+    return c;
+  }
+  constexpr size_t kGran = 2u << 20;
+  return (bytes + kGran - 1) / kGran * kGran;
+}
+
+static void* pool_alloc(sfg_context* ctx, size_t bytes) {
   void* p = nullptr;
-  cudaError_t e = cudaMallocAsync(&p, bytes ? bytes : 1, ctx->stream);
+  auto t0 = std::chrono::steady_clock::now();
+  cudaError_t e = cudaMallocAsync(&p, bytes, ctx->stream);
+  if (e != cudaSuccess) {
+    // out of memory: give the cached blocks back and try once more
+    cudaGetLastError();
+    release_cached(ctx);
+    cudaStreamSynchronize(ctx->stream);
+    e = cudaMallocAsync(&p, bytes, ctx->stream);
+  }
   if (e != cudaSuccess) {
     cudaGetLastError();
     raise(SFG_ERR_OOM, "device allocation of " + std::to_string(bytes) + " bytes failed: " +
                            cudaGetErrorString(e));
   }
+  if (trace_alloc()) {
+    double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    std::fprintf(stderr, "[sfg] pool alloc %zu bytes: %.2f ms\n", bytes, ms);
+  }
+  return p;
+}
+
+void* dalloc(sfg_context* ctx, size_t bytes) {
+  size_t cls = size_class(bytes ? bytes : 1);
+  auto it = ctx->free_blocks.lower_bound(cls);
+  if (it != ctx->free_blocks.end() && it->first - it->first / 8 <= cls) {
+    void* p = it->second;
+    ctx->cached_bytes -= it->first;
+    ctx->free_blocks.erase(it);
+    return p;
+  }
+  void* p = pool_alloc(ctx, cls);
+  ctx->block_size[p] = cls;
   return p;
 }
 
 void dfree(sfg_context* ctx, void* p) {
-  if (p) cudaFreeAsync(p, ctx->stream);
+  if (!p) return;
+  auto it = ctx->block_size.find(p);
+  if (it == ctx->block_size.end()) {
+    cudaFreeAsync(p, ctx->stream);
+    return;
+  }
+  ctx->free_blocks.emplace(it->second, p);
+  ctx->cached_bytes += it->second;
+}
+
+void release_cached(sfg_context* ctx) {
+  for (auto& kv : ctx->free_blocks) {
+    ctx->block_size.erase(kv.second);
+    cudaFreeAsync(kv.second, ctx->stream);
+  }
+  ctx->free_blocks.clear();
+  ctx->cached_bytes = 0;
 }
 
 void* scratch(sfg_context* ctx, size_t bytes) {

@@ -163,31 +163,100 @@ __device__ __forceinline__ uint32_t lookback_prefix(unsigned long long* status, 
   return r;
 }
 
-// ---------------------------------------------------- row-pointer gaps
-// ptr[lo..hi] = v for the rows between two consecutive sorted entries.
-// Gaps longer than a warp are filled cooperatively by the whole warp, so a
-// long run of empty rows costs gap/32 iterations, not gap. All 32 lanes
-// must call this (warp collectives).
-struct Gap {
-  int32_t lo, hi, v;  // ptr[lo..hi] = v
-};
-
-__device__ __forceinline__ void fill_gaps(Gap (&g)[5], int32_t* __restrict__ ptr) {
-  int lane = threadIdx.x & 31;
+// ---------------------------------------------------- row-pointer writes
+// A lane owns N consecutive entries of a sorted row array, rows r[0..N-1],
+// entry positions v0..v0+N-1, and `prev` = the row of the entry before
+// them. For each entry i it writes ptr[q] = v0 + i for every row q in
+// (r[i-1], r[i]] (the rows it opens, including empty rows before it); then
+// ptr[q] = end_v for q in (r[N-1], end_hi] (end_hi = r[N-1] for "nothing":
+// only the owner of the last entry closes the array up to m).
+//
+// Up to kInline rows per gap are written as predicated stores with no
+// branch; the rest of a longer gap (a run of empty rows) is written by the
+// whole warp cooperatively, so a gap of G rows costs G/32 store rounds.
+// One ballot per call. All 32 lanes must call this.
+template <int N>
+__device__ __forceinline__ void write_row_ptr(const int32_t (&r)[N], int32_t prev, int32_t v0,
+                                              int32_t end_hi, int32_t end_v,
+                                              int32_t* __restrict__ ptr) {
+  constexpr int kInline = 2;
+  const int lane = threadIdx.x & 31;
+  unsigned big = 0;
 #pragma unroll
-  for (int i = 0; i < 5; ++i) {
-    int len = g[i].hi - g[i].lo + 1;
-    bool big = len > 32;
-    if (!big)
-      for (int q = g[i].lo; q <= g[i].hi; ++q) ptr[q] = g[i].v;
-    unsigned mask = __ballot_sync(kFull, big);
-    while (mask) {
-      int src = __ffs(mask) - 1;
-      mask &= mask - 1;
-      int lo = __shfl_sync(kFull, g[i].lo, src), hi = __shfl_sync(kFull, g[i].hi, src);
-      int v = __shfl_sync(kFull, g[i].v, src);
+  for (int i = 0; i <= N; ++i) {
+    int lo = (i ? r[i - 1] : prev) + 1;
+    int hi = i < N ? r[i] : end_hi;
+    int v = i < N ? v0 + i : end_v;
+#pragma unroll
+    for (int j = 0; j < kInline; ++j)
+      if (lo + j <= hi) ptr[lo + j] = v;
+    if (hi - lo >= kInline) big |= 1u << i;
+  }
+  unsigned lanes = __ballot_sync(kFull, big != 0);
+  while (lanes) {
+    int src = __ffs(lanes) - 1;
+    lanes &= lanes - 1;
+    unsigned which = __shfl_sync(kFull, big, src);
+#pragma unroll
+    for (int i = 0; i <= N; ++i) {
+      if (!(which >> i & 1u)) continue;
+      int lo = __shfl_sync(kFull, (i ? r[i - 1] : prev) + 1 + kInline, src);
+      int hi = __shfl_sync(kFull, i < N ? r[i] : end_hi, src);
+      int v = __shfl_sync(kFull, i < N ? v0 + i : end_v, src);
       for (int q = lo + lane; q <= hi; q += 32) ptr[q] = v;
     }
+  }
+}
+
+// Loads the rows of one warp chunk of 2 x 128 entries: group g of lane l
+// holds entries base + 128 g + 4 l .. +3 (coalesced 512 B per group).
+// Entries at or past nnz read as the last row, so they open no rows; `prev`
+// is the row before each group (-1 before entry 0).
+struct RowChunk {
+  int32_t r[2][4];
+  int32_t prev[2];
+  bool full;
+};
+
+__device__ __forceinline__ void load_row_chunk(const int32_t* __restrict__ row, int64_t nnz,
+                                               int64_t base, RowChunk& c) {
+  const int lane = threadIdx.x & 31;
+  c.full = base + 256 <= nnz;
+  if (c.full) {
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+      int4 v = ld_stream(reinterpret_cast<const int4*>(row + base + 128 * g) + lane);
+      c.r[g][0] = v.x; c.r[g][1] = v.y; c.r[g][2] = v.z; c.r[g][3] = v.w;
+    }
+  } else {
+    const int32_t last = row[nnz - 1];
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        int64_t e = base + 128 * g + 4 * lane + i;
+        c.r[g][i] = e < nnz ? row[e] : last;
+      }
+  }
+  int32_t before = 0;
+  if (lane == 0) before = base == 0 ? -1 : row[base - 1];
+  int32_t up0 = __shfl_up_sync(kFull, c.r[0][3], 1);
+  int32_t up1 = __shfl_up_sync(kFull, c.r[1][3], 1);
+  int32_t wrap = __shfl_sync(kFull, c.r[0][3], 31);
+  c.prev[0] = lane ? up0 : before;
+  c.prev[1] = lane ? up1 : wrap;
+}
+
+// The row-pointer writes for a loaded chunk; the owner of entry nnz - 1
+// closes ptr up to m.
+__device__ __forceinline__ void chunk_row_ptr(const RowChunk& c, int64_t nnz, int64_t base,
+                                              int32_t m, int32_t* __restrict__ ptr) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    int64_t e0 = base + 128 * g + 4 * lane;
+    bool closes = e0 <= nnz - 1 && nnz - 1 < e0 + 4;
+    write_row_ptr<4>(c.r[g], c.prev[g], (int32_t)e0, closes ? m : c.r[g][3], (int32_t)nnz, ptr);
   }
 }
 

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <map>
+#include <unordered_map>
 #include <cstdint>
 #include <string>
 
@@ -55,6 +57,12 @@ struct sfg_context {
   void* status = nullptr;      // look-back status words only
   size_t status_words = 0;
   uint32_t epoch = 1;          // look-back status generation
+  // Block cache over the stream-ordered pool (core.cu: dalloc/dfree). All
+  // work of a context runs on ctx->stream, so a freed block can be handed
+  // out again at once: stream order serialises its old and new users.
+  std::multimap<size_t, void*> free_blocks;     // size class -> block
+  std::unordered_map<void*, size_t> block_size;  // every cached-or-live block
+  size_t cached_bytes = 0;
 };
 
 // ------------------------------------------------------------------ tensor
@@ -90,9 +98,13 @@ struct sfg_tensor {
 
 namespace sfg {
 
-// Stream-ordered device allocation from the context's pool.
+// Stream-ordered device allocation through the context's block cache (a
+// conversion allocates the same large arrays every call; growing the
+// driver pool for them costs milliseconds of host time per call).
 void* dalloc(sfg_context* ctx, size_t bytes);
 void dfree(sfg_context* ctx, void* p);
+// Returns every cached (free) block to the pool.
+void release_cached(sfg_context* ctx);
 template <class T>
 T* dalloc_n(sfg_context* ctx, int64_t n) {
   return static_cast<T*>(dalloc(ctx, static_cast<size_t>(n > 0 ? n : 1) * sizeof(T)));

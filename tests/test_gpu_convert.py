@@ -193,3 +193,20 @@ def test_config2_full_size_hybrid(ctx, port):
     ps, pr, _ = port.decompose_rows(p, 8)
     assert_same_materialized(ell.download(), port.convert(pr, "ELL").download(), "cfg2 ELL")
     assert_same_materialized(coo.download(), port.convert(ps, "COO").download(), "cfg2 COO")
+
+
+def test_block_cache_reuse_and_release(ctx, port):
+    """Freed tensor arrays are cached by the context and reused by the next
+    conversion; release_cached hands them back to the driver pool."""
+    ctx.release_cached()
+    d = ctx.gen_rmat(3, 12, 16 << 12)
+    ref = ctx.convert(d, "HYB(4)")
+    want = [p.download() for p in ref.parts()]
+    del ref
+    cached = ctx.release_cached()
+    assert cached > 0 and ctx.release_cached() == 0
+    for _ in range(3):  # the reused blocks give the same result
+        h = ctx.convert(d, "HYB(4)")
+        for a, b in zip((p.download() for p in h.parts()), want):
+            assert_same_materialized(a, b, "reuse")
+        del h

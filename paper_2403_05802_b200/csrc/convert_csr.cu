@@ -45,27 +45,29 @@ __global__ void __launch_bounds__(kBlock) k_check_canonical(const int32_t* __res
 }
 
 // ----------------------------------------------------------- COO -> CSR
-// A lane owns 2 x 4 consecutive entries (128-bit loads/stores of row, col,
-// val). Row boundaries inside its runs write ptr[q] = e for every row q in
-// (row[e-1], row[e]]; the owner of the last entry closes ptr up to m.
-// Long empty-row gaps are filled cooperatively by the warp (write_row_ptr).
+// A warp owns chunks of 128*kCsrVec consecutive entries (128-bit
+// loads/stores of row, col, val) and writes the row pointers of the rows
+// each chunk opens (chunk_row_ptr: ptr[q] = first entry with row >= q).
+constexpr int kCsrVec = 2;
+
 __global__ void __launch_bounds__(kBlock) k_coo_to_csr(const int32_t* __restrict__ row,
                                                         const int32_t* __restrict__ col,
                                                         const float* __restrict__ val, int64_t nnz,
                                                         int32_t m, int32_t* __restrict__ ptr,
                                                         int32_t* __restrict__ ocol,
                                                         float* __restrict__ oval) {
+  constexpr int kChunk = 128 * kCsrVec;
+  __shared__ __align__(16) int32_t s_rows[kBlock / 32][kChunk];
   const int lane = threadIdx.x & 31;
-  const int64_t nchunk = (nnz + 255) >> 8;
+  const int64_t nchunk = (nnz + kChunk - 1) / kChunk;
   const int64_t warps = (int64_t)gridDim.x * (kBlock / 32);
-  // a warp per 256-entry chunk: uniform trip count (write_row_ptr is a warp
-  // collective)
+  // a warp per chunk: uniform trip count (chunk_row_ptr is a warp collective)
   for (int64_t ch = (int64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); ch < nchunk; ch += warps) {
-    const int64_t base = ch << 8;
-    RowChunk c;
+    const int64_t base = ch * kChunk;
+    RowChunk<kCsrVec> c;
     load_row_chunk(row, nnz, base, c);
 #pragma unroll
-    for (int g = 0; g < 2; ++g) {
+    for (int g = 0; g < kCsrVec; ++g) {
       int64_t e0 = base + 128 * g + 4 * lane;
       if (c.full) {
         int4 cc = ld_stream(reinterpret_cast<const int4*>(col + e0));
@@ -81,7 +83,7 @@ __global__ void __launch_bounds__(kBlock) k_coo_to_csr(const int32_t* __restrict
           }
       }
     }
-    chunk_row_ptr(c, nnz, base, m, ptr);
+    chunk_row_ptr(c, nnz, base, m, s_rows[threadIdx.x >> 5], ptr);
   }
 }
 
@@ -238,7 +240,7 @@ void compress_sorted(sfg_context* ctx, const int32_t* key, const int32_t* other,
                extent + 1, 0);
     return;
   }
-  SFG_LAUNCH(k_coo_to_csr, stream_grid(ctx, ceil_div(nnz, 256), kBlock / 32, 1, 8), kBlock, 0, ctx->stream,
+  SFG_LAUNCH(k_coo_to_csr, stream_grid(ctx, ceil_div(nnz, 128 * kCsrVec), kBlock / 32, 1, 8), kBlock, 0, ctx->stream,
              key, other, val, nnz, (int32_t)extent, ptr, oidx, oval);
 }
 
@@ -253,7 +255,7 @@ sfg_tensor* coo_to_csr(sfg_context* ctx, const sfg_tensor* s) {
                s->m + 1, 0);
     return t;
   }
-  SFG_LAUNCH(k_coo_to_csr, stream_grid(ctx, ceil_div(s->nnz, 256), kBlock / 32, 1, 8), kBlock, 0, ctx->stream, s->row,
+  SFG_LAUNCH(k_coo_to_csr, stream_grid(ctx, ceil_div(s->nnz, 128 * kCsrVec), kBlock / 32, 1, 8), kBlock, 0, ctx->stream, s->row,
              s->idx, static_cast<const float*>(s->val), s->nnz, (int32_t)s->m, t->ptr, t->idx,
              static_cast<float*>(t->val));
   return t;

@@ -39,26 +39,30 @@ constexpr int kBlock = 256;
 constexpr uint32_t kSelBit = 0x80000000u;
 
 // --------------------------------------------------------- 1. row pointers
-// A warp handles 256 consecutive entries per iteration (two coalesced 512 B
-// row loads in flight per lane pair). kVals: the source may hold explicit
-// zeros, so values are read too; a zero-free source reads rows only.
+// A warp handles 128*kRowVec consecutive entries per iteration. kVals: the
+// source may hold explicit zeros, so values are read too; a zero-free
+// source reads rows only.
+constexpr int kRowVec = 4;
+
 template <bool kVals>
 __global__ void __launch_bounds__(kBlock) k_row_ptr(const int32_t* __restrict__ row,
                                                      const float* __restrict__ val, int64_t nnz,
                                                      int32_t m, int32_t* __restrict__ ptr,
                                                      int32_t* __restrict__ zcnt,
                                                      int* __restrict__ any_zero) {
+  constexpr int kChunk = 128 * kRowVec;
+  __shared__ __align__(16) int32_t s_rows[kBlock / 32][kChunk];
   const int lane = threadIdx.x & 31;
-  const int64_t nchunk = (nnz + 255) >> 8;
+  const int64_t nchunk = (nnz + kChunk - 1) / kChunk;
   const int64_t warps = (int64_t)gridDim.x * (kBlock / 32);
   bool saw_zero = false;
   for (int64_t ch = (int64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); ch < nchunk; ch += warps) {
-    const int64_t base = ch << 8;
-    RowChunk c;
+    const int64_t base = ch * kChunk;
+    RowChunk<kRowVec> c;
     load_row_chunk(row, nnz, base, c);
     if (kVals) {
 #pragma unroll
-      for (int g = 0; g < 2; ++g) {
+      for (int g = 0; g < kRowVec; ++g) {
         int64_t e0 = base + 128 * g + 4 * lane;
         float x[4];
         if (c.full) {
@@ -76,7 +80,7 @@ __global__ void __launch_bounds__(kBlock) k_row_ptr(const int32_t* __restrict__ 
           }
       }
     }
-    chunk_row_ptr(c, nnz, base, m, ptr);
+    chunk_row_ptr(c, nnz, base, m, s_rows[threadIdx.x >> 5], ptr);
   }
   if (kVals && __any_sync(kFull, saw_zero) && lane == 0) atomicOr(any_zero, 1);
 }
@@ -109,10 +113,24 @@ __global__ void __launch_bounds__(kBlock) k_row_scan(const int32_t* __restrict__
   __shared__ int32_t sz[kScanTile + kScanTile / 16 + 1];
   auto sk = [](int i) { return i + (i >> 4); };
   const int64_t tile0 = (int64_t)blockIdx.x * kScanTile;
-  for (int i = threadIdx.x; i <= kScanTile; i += kBlock) {
-    int64_t r = tile0 + i;
-    sp[sk(i)] = r <= m ? __ldg(ptr + r) : 0;
-    if (i < kScanTile) sz[sk(i)] = (has_zeros && r < m) ? __ldg(zcnt + r) : 0;
+  {
+    // all loads in flight before the first shared store
+    int32_t pv[kScanItems], zv[kScanItems];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      int64_t r = tile0 + threadIdx.x + k * kBlock;
+      pv[k] = r <= m ? ld_stream(ptr + r) : 0;
+      zv[k] = (has_zeros && r < m) ? ld_stream(zcnt + r) : 0;
+    }
+    int32_t pend = 0;
+    if (threadIdx.x == 0 && tile0 + kScanTile <= m) pend = __ldg(ptr + tile0 + kScanTile);
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      int i = threadIdx.x + k * kBlock;
+      sp[sk(i)] = pv[k];
+      sz[sk(i)] = zv[k];
+    }
+    if (threadIdx.x == 0) sp[sk(kScanTile)] = pend;
   }
   __syncthreads();
   const int t0 = threadIdx.x * kScanItems;
@@ -301,7 +319,7 @@ RowInfo row_info(sfg_context* ctx, const sfg_tensor* s, int64_t min_sum, int32_t
   if (s->nnz == 0) {
     SFG_CUDA(cudaMemsetAsync(ri.ptr, 0, (m + 1) * sizeof(int32_t), ctx->stream));
   } else {
-    int grid = stream_grid(ctx, ceil_div(s->nnz, 256), kBlock / 32, 1, 8);
+    int grid = stream_grid(ctx, ceil_div(s->nnz, 128 * kRowVec), kBlock / 32, 1, 8);
     if (zeros_possible)
       SFG_LAUNCH(k_row_ptr<true>, grid, kBlock, 0, ctx->stream, s->row, static_cast<const float*>(s->val),
                  s->nnz, (int32_t)m, ri.ptr, ri.zcnt, tail);

@@ -208,56 +208,69 @@ __device__ __forceinline__ void write_row_ptr(const int32_t (&r)[N], int32_t pre
   }
 }
 
-// Loads the rows of one warp chunk of 2 x 128 entries: group g of lane l
-// holds entries base + 128 g + 4 l .. +3 (coalesced 512 B per group).
-// Entries at or past nnz read as the last row, so they open no rows; `prev`
-// is the row before each group (-1 before entry 0).
+// ------------------------------------------------ chunked row pointers
+// A warp owns a chunk of 128*V consecutive sorted entries; lane l holds
+// entries base + 128 g + 4 l .. +3 for g < V (coalesced 512 B per group).
+// Entries at or past nnz read as the last row.
+template <int V>
 struct RowChunk {
-  int32_t r[2][4];
-  int32_t prev[2];
+  int32_t r[V][4];
+  int32_t prev;  // row of entry base - 1 (-1 before entry 0)
   bool full;
 };
 
+template <int V>
 __device__ __forceinline__ void load_row_chunk(const int32_t* __restrict__ row, int64_t nnz,
-                                               int64_t base, RowChunk& c) {
+                                               int64_t base, RowChunk<V>& c) {
   const int lane = threadIdx.x & 31;
-  c.full = base + 256 <= nnz;
+  c.full = base + 128 * V <= nnz;
   if (c.full) {
 #pragma unroll
-    for (int g = 0; g < 2; ++g) {
+    for (int g = 0; g < V; ++g) {
       int4 v = ld_stream(reinterpret_cast<const int4*>(row + base + 128 * g) + lane);
       c.r[g][0] = v.x; c.r[g][1] = v.y; c.r[g][2] = v.z; c.r[g][3] = v.w;
     }
   } else {
     const int32_t last = row[nnz - 1];
 #pragma unroll
-    for (int g = 0; g < 2; ++g)
+    for (int g = 0; g < V; ++g)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         int64_t e = base + 128 * g + 4 * lane + i;
         c.r[g][i] = e < nnz ? row[e] : last;
       }
   }
-  int32_t before = 0;
-  if (lane == 0) before = base == 0 ? -1 : row[base - 1];
-  int32_t up0 = __shfl_up_sync(kFull, c.r[0][3], 1);
-  int32_t up1 = __shfl_up_sync(kFull, c.r[1][3], 1);
-  int32_t wrap = __shfl_sync(kFull, c.r[0][3], 31);
-  c.prev[0] = lane ? up0 : before;
-  c.prev[1] = lane ? up1 : wrap;
+  c.prev = base == 0 ? -1 : row[base - 1];  // one broadcast load per warp
 }
 
-// The row-pointer writes for a loaded chunk; the owner of entry nnz - 1
-// closes ptr up to m.
-__device__ __forceinline__ void chunk_row_ptr(const RowChunk& c, int64_t nnz, int64_t base,
-                                              int32_t m, int32_t* __restrict__ ptr) {
+// Row pointers of the rows this chunk opens: ptr[q] for q in
+// (prev, last row] (and up to m for the chunk holding entry nnz - 1) is the
+// position of the first entry with row >= q — a lower-bound search over
+// the chunk's rows staged in shared memory (s: 128*V words per warp).
+// Lanes take consecutive q, so the stores are coalesced and a run of empty
+// rows costs one search per 32 rows; no per-gap branches. Warp collective.
+template <int V>
+__device__ __forceinline__ void chunk_row_ptr(const RowChunk<V>& c, int64_t nnz, int64_t base,
+                                              int32_t m, int32_t* __restrict__ s,
+                                              int32_t* __restrict__ ptr) {
+  constexpr int kN = 128 * V;
   const int lane = threadIdx.x & 31;
 #pragma unroll
-  for (int g = 0; g < 2; ++g) {
-    int64_t e0 = base + 128 * g + 4 * lane;
-    bool closes = e0 <= nnz - 1 && nnz - 1 < e0 + 4;
-    write_row_ptr<4>(c.r[g], c.prev[g], (int32_t)e0, closes ? m : c.r[g][3], (int32_t)nnz, ptr);
+  for (int g = 0; g < V; ++g)
+    reinterpret_cast<int4*>(s + 128 * g)[lane] = make_int4(c.r[g][0], c.r[g][1], c.r[g][2], c.r[g][3]);
+  __syncwarp();
+  const int32_t last = s[kN - 1];
+  const int32_t hi = base + kN >= nnz ? m : last;
+  for (int32_t q = c.prev + 1 + lane; q <= hi; q += 32) {
+    int pos = 0;
+#pragma unroll
+    for (int step = kN / 2; step > 0; step >>= 1)
+      if (s[pos + step - 1] < q) pos += step;
+    if (pos == kN - 1 && s[kN - 1] < q) pos = kN;
+    int64_t v = base + pos;
+    ptr[q] = (int32_t)(v < nnz ? v : nnz);
   }
+  __syncwarp();
 }
 
 }  // namespace sfg

@@ -56,10 +56,15 @@ __global__ void __launch_bounds__(kBlock) k_row_ptr(const int32_t* __restrict__ 
   const int64_t nchunk = (nnz + kChunk - 1) / kChunk;
   const int64_t warps = (int64_t)gridDim.x * (kBlock / 32);
   bool saw_zero = false;
-  for (int64_t ch = (int64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); ch < nchunk; ch += warps) {
+  // software pipeline: the next chunk's rows are in flight while this
+  // chunk's row pointers are searched and written
+  int64_t ch = (int64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
+  RowChunk<kRowVec> next;
+  if (ch < nchunk) load_row_chunk(row, nnz, ch * kChunk, next);
+  for (; ch < nchunk; ch += warps) {
     const int64_t base = ch * kChunk;
-    RowChunk<kRowVec> c;
-    load_row_chunk(row, nnz, base, c);
+    RowChunk<kRowVec> c = next;
+    if (ch + warps < nchunk) load_row_chunk(row, nnz, (ch + warps) * kChunk, next);
     if (kVals) {
 #pragma unroll
       for (int g = 0; g < kRowVec; ++g) {

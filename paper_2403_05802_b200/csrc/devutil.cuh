@@ -249,27 +249,46 @@ __device__ __forceinline__ void load_row_chunk(const int32_t* __restrict__ row, 
 // the chunk's rows staged in shared memory (s: 128*V words per warp).
 // Lanes take consecutive q, so the stores are coalesced and a run of empty
 // rows costs one search per 32 rows; no per-gap branches. Warp collective.
-template <int V>
-__device__ __forceinline__ void chunk_row_ptr(const RowChunk<V>& c, int64_t nnz, int64_t base,
-                                              int32_t m, int32_t* __restrict__ s,
-                                              int32_t* __restrict__ ptr) {
-  constexpr int kN = 128 * V;
+template <int kN>
+__device__ __forceinline__ void row_ptr_from_smem(const int32_t* __restrict__ s, int32_t prev, int64_t nnz,
+                                                  int64_t base, int32_t m, int32_t* __restrict__ ptr) {
   const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int g = 0; g < V; ++g)
-    reinterpret_cast<int4*>(s + 128 * g)[lane] = make_int4(c.r[g][0], c.r[g][1], c.r[g][2], c.r[g][3]);
-  __syncwarp();
   const int32_t last = s[kN - 1];
   const int32_t hi = base + kN >= nnz ? m : last;
-  for (int32_t q = c.prev + 1 + lane; q <= hi; q += 32) {
+  int32_t q0 = prev + 1;
+  while (q0 <= hi) {  // warp-uniform
+    const int32_t q = q0 + lane;
     int pos = 0;
 #pragma unroll
     for (int step = kN / 2; step > 0; step >>= 1)
       if (s[pos + step - 1] < q) pos += step;
     if (pos == kN - 1 && s[kN - 1] < q) pos = kN;
     int64_t v = base + pos;
-    ptr[q] = (int32_t)(v < nnz ? v : nnz);
+    const int32_t pv = (int32_t)(v < nnz ? v : nnz);
+    if (q <= hi) ptr[q] = pv;
+    const int p0 = __shfl_sync(kFull, pos, 0), p31 = __shfl_sync(kFull, pos, 31);
+    if (p0 == p31 && q0 + 31 < hi) {
+      // all 32 rows fall in one run of empty rows ending at row s[p0]:
+      // fill the rest of the run without searching
+      const int32_t end = p0 < kN ? s[p0] : hi;
+      for (int32_t r = q0 + 32 + lane; r <= end; r += 32) ptr[r] = pv;
+      q0 = end + 1;
+    } else {
+      q0 += 32;
+    }
   }
+}
+
+template <int V>
+__device__ __forceinline__ void chunk_row_ptr(const RowChunk<V>& c, int64_t nnz, int64_t base,
+                                              int32_t m, int32_t* __restrict__ s,
+                                              int32_t* __restrict__ ptr) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int g = 0; g < V; ++g)
+    reinterpret_cast<int4*>(s + 128 * g)[lane] = make_int4(c.r[g][0], c.r[g][1], c.r[g][2], c.r[g][3]);
+  __syncwarp();
+  row_ptr_from_smem<128 * V>(s, c.prev, nnz, base, m, ptr);
   __syncwarp();
 }
 

@@ -130,79 +130,89 @@ __global__ void __launch_bounds__(kBlock) k_spmv_ell(const int32_t* __restrict__
 }
 
 // ---------------------------------------------------------------- COO
-// Row-sorted entries, thread-sequential segmented reduction: each lane owns
-// kCooRun consecutive entries (128-bit loads of row/col/val), sums runs of
-// equal rows in registers, and writes a row with a plain add when the row
-// lies strictly inside its run (no other lane can touch it); the lane's
-// first and last rows may continue in a neighbouring lane or warp and use
-// atomicAdd. y must be zeroed (or hold a partial result) beforehand.
-constexpr int kCooRun = 16;
-
-__device__ __forceinline__ void coo_flush(float* __restrict__ y, int r, float s, bool shared) {
-  if (shared) atomicAdd(y + r, s);
-  else y[r] += s;
+// Row-sorted entries, load-balanced by entries (a heavy row spans many
+// warps). No shared memory. A warp walks its chunk
+// in steps of 32 consecutive entries (lane-strided loads, all kCooSteps
+// steps' loads and x gathers in flight first). The warp keeps one open row
+// `cur` whose per-lane partial sums live in `acc`: a step entirely inside
+// `cur` (the common case for long rows) is one add per lane and no
+// communication. A step that starts a new row closes `cur` (warp sum, one
+// RED); a step holding a row boundary reduces its segments with a
+// head-flag segmented scan (5 shuffles), RED-adds every segment but the
+// last, and the last becomes the new `cur`.
+__device__ __forceinline__ void coo_close(float* __restrict__ y, int32_t row, float acc) {
+  float s = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0 && row >= 0 && row != 0x7fffffff) atomicAdd(y + row, s);
 }
 
-// Loads are lane-strided (entry base + 32 i + lane: one 128-byte line per
-// warp load, so L1 wavefronts go to the x gathers, not to the streams), the
-// products pass through shared memory (skewed by one word per 16, so both
-// the strided writes and the blocked reads are conflict-free), and each lane
-// then reduces its own kCooRun consecutive entries.
-__global__ void __launch_bounds__(kBlock) k_spmv_coo(const int32_t* __restrict__ row,
-                                                      const int32_t* __restrict__ col,
-                                                      const float* __restrict__ val,
-                                                      const float* __restrict__ x,
-                                                      float* __restrict__ y, int64_t nnz) {
-  constexpr int kSpan = 32 * kCooRun;
-  constexpr int kSkew = kSpan + kSpan / 16;
-  __shared__ int s_row[kBlock / 32][kSkew];
-  __shared__ float s_p[kBlock / 32][kSkew];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  auto sk = [](int j) { return j + (j >> 4); };
+// 12 steps with >= 4 CTAs per SM (56 registers) measured fastest on the
+// config-2 COO part (241 us vs 291 us for 16 steps at 72 registers; the
+// stream + gather floor of the same data is ~214 us, scripts/coo_exp.cu).
+constexpr int kCooSteps = 12;
+
+__global__ void __launch_bounds__(kBlock, 4) k_spmv_coo(const int32_t* __restrict__ row,
+                                                          const int32_t* __restrict__ col,
+                                                          const float* __restrict__ val,
+                                                          const float* __restrict__ x,
+                                                          float* __restrict__ y, int64_t nnz) {
+  constexpr int32_t kNone = 0x7fffffff;  // past nnz: sorts after every row
+  const int lane = threadIdx.x & 31;
+  const int64_t span = 32 * kCooSteps;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w * kSpan < nnz; w += warps) {
-    const int64_t base = w * kSpan;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w * span < nnz; w += warps) {
+    int32_t r[kCooSteps];
+    float p[kCooSteps];
     {
-      int rr[kCooRun], cc[kCooRun];
-      float vv[kCooRun];
+      int32_t c[kCooSteps];
+      float v[kCooSteps];
 #pragma unroll
-      for (int i = 0; i < kCooRun; ++i) {
-        int64_t e = base + 32 * i + lane;
+      for (int i = 0; i < kCooSteps; ++i) {
+        int64_t e = w * span + 32 * i + lane;
         bool ok = e < nnz;
-        rr[i] = ok ? ld_stream(row + e) : -1;
-        cc[i] = ok ? ld_stream(col + e) : 0;
-        vv[i] = ok ? ld_stream(val + e) : 0.f;
+        r[i] = ok ? ld_stream(row + e) : kNone;
+        c[i] = ok ? ld_stream(col + e) : 0;
+        v[i] = ok ? ld_stream(val + e) : 0.f;
       }
 #pragma unroll
-      for (int i = 0; i < kCooRun; ++i) {
-        s_row[wid][sk(32 * i + lane)] = rr[i];
-        s_p[wid][sk(32 * i + lane)] = vv[i] * ldx(x, cc[i]);
+      for (int i = 0; i < kCooSteps; ++i) p[i] = v[i] * ldx(x, c[i]);
+    }
+    int32_t cur = -1;
+    float acc = 0.f;
+#pragma unroll
+    for (int i = 0; i < kCooSteps; ++i) {
+      const int32_t r0 = __shfl_sync(kFull, r[i], 0), r31 = __shfl_sync(kFull, r[i], 31);
+      if (r0 == r31) {  // one row in this step (warp-uniform branch)
+        if (r0 != cur) {
+          coo_close(y, cur, acc);
+          cur = r0;
+          acc = 0.f;
+        }
+        acc += p[i];
+      } else {
+        // entries continuing `cur` join its partial sums, which close now
+        const bool in_cur = r[i] == cur;
+        coo_close(y, cur, acc + (in_cur ? p[i] : 0.f));
+        // segmented inclusive scan of the other entries, keyed by row
+        const int32_t up = __shfl_up_sync(kFull, r[i], 1);
+        const bool head = lane == 0 || up != r[i];
+        const unsigned heads = __ballot_sync(kFull, head);
+        const int start = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
+        float t = in_cur ? 0.f : p[i];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          float u = __shfl_up_sync(kFull, t, o);
+          if (lane - o >= start) t += u;
+        }
+        const int32_t dn = __shfl_down_sync(kFull, r[i], 1);
+        // segments ending before lane 31 are complete (rows are sorted)
+        if (lane < 31 && dn != r[i] && !in_cur && r[i] != kNone) atomicAdd(y + r[i], t);
+        // the last segment stays open: its sum moves to lane 0's partial
+        const float last = __shfl_sync(kFull, t, 31);
+        cur = r31;
+        acc = lane == 0 ? last : 0.f;
       }
     }
-    __syncwarp();
-    int r[kCooRun];
-    float p[kCooRun];
-#pragma unroll
-    for (int i = 0; i < kCooRun; ++i) {
-      r[i] = s_row[wid][sk(lane * kCooRun + i)];
-      p[i] = s_p[wid][sk(lane * kCooRun + i)];
-    }
-    __syncwarp();
-    if (r[0] < 0) continue;
-    const int first = r[0];
-    int cur = r[0];
-    float s = p[0];
-#pragma unroll
-    for (int i = 1; i < kCooRun; ++i) {
-      if (r[i] < 0) break;
-      if (r[i] != cur) {
-        coo_flush(y, cur, s, cur == first);
-        cur = r[i];
-        s = 0.f;
-      }
-      s += p[i];
-    }
-    coo_flush(y, cur, s, true);  // the run's last row may continue
+    coo_close(y, cur, acc);  // the row may continue in the next chunk
   }
 }
 
@@ -301,7 +311,7 @@ void zero_y(sfg_context* ctx, float* y, int64_t m) {
 void spmv_coo(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, bool acc) {
   if (!acc) zero_y(ctx, y, a->m);
   if (a->nnz == 0) return;
-  int grid = stream_grid(ctx, ceil_div(a->nnz, kCooRun), kBlock, 1, 8);
+  int grid = stream_grid(ctx, ceil_div(a->nnz, 32 * kCooSteps), kBlock / 32, 1, 8);
   SFG_LAUNCH(k_spmv_coo, grid, kBlock, 0, ctx->stream, a->row, a->idx,
              static_cast<const float*>(a->val), x, y, a->nnz);
 }

@@ -25,6 +25,7 @@
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
 #include <mutex>
 
 #include "async.cuh"
@@ -52,6 +53,24 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64
       : "memory");
 }
 
+__device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+
+// 16-byte global -> shared copy (L2 only) and the mbarrier arrive that
+// fires when all of this thread's earlier cp.async copies have landed (the
+// barrier's pending count is raised first, so it waits for them).
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -64,6 +83,30 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// Issued by one elected lane of a converged warp: the operands are
+// warp-uniform, so they go to uniform registers without a per-lane loop.
+__device__ __forceinline__ void tc_mma_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "}\n" ::"r"(smem_u32(bar))
       : "memory");
 }
 
@@ -258,8 +301,11 @@ struct GShared {
 
 __device__ __forceinline__ void mbar_arrive_plain(uint64_t* bar) { mbar_arrive(bar); }
 
-__global__ void __launch_bounds__(kThreads, 1)
-    k_bcsr_tc_group(const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_a,
+// kProducers producer warps (stages dealt round-robin), kMmaWarps MMA
+// warps (block rows dealt by j % kMmaWarps).
+template <int kProducers, int kMmaWarps>
+__global__ void __launch_bounds__(32 * (4 + kProducers + kMmaWarps), 1)
+    k_bcsr_tc_group(const __grid_constant__ CUtensorMap tmap_b, const uint8_t* __restrict__ aval,
                     const int32_t* __restrict__ ptr, const int32_t* __restrict__ bcol, int32_t nbr,
                     int32_t m, float* __restrict__ c, int64_t ldc, int accumulate,
                     const uint32_t* __restrict__ plan, int32_t nbc) {
@@ -268,17 +314,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   GShared* sh = reinterpret_cast<GShared*>(stages + kGStages * kGStageBytes);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t ngroups = (nbr + kGroup - 1) / kGroup;
+  constexpr int kMmaWarp = 4 + kProducers;  // first MMA warp
+  static_assert(kGStages % kProducers == 0, "producers must divide the ring (exact parity waits)");
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kGStages; ++s) {
       mbar_init(&sh->full[s], 1);
-      mbar_init(&sh->empty[s], 1);
+      mbar_init(&sh->empty[s], kMmaWarps);  // each MMA warp commits every stage
     }
-    mbar_init(&sh->acc_full, 1);
+    mbar_init(&sh->acc_full, kMmaWarps);
     mbar_init(&sh->acc_empty, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 5) {
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sh->tmem_base)),
                  "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -288,38 +336,54 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = sh->tmem_base;
 
+  // Producer warps 4 .. 4+kProducers-1 all walk the same sequence of
+  // pipeline stages (so they agree on every stage's index and contents);
+  // stage t is issued by producer warp t % kProducers, so the TMA issue
+  // work — serialised per warp — runs kProducers-wide.
+  const int pw = warp - 4;
   // One pipeline step: the B tile of block column `bc` and the value blocks
   // of the block rows in `mask` (split into stages of <= kMaxA blocks).
   // Lanes whose bit is set issue their own value-block load and advance.
-  auto issue = [&](uint32_t mask, uint32_t bc, int32_t& cur, int& stage, uint32_t& phase) {
+  auto issue = [&](uint32_t mask, uint32_t bc, int32_t& cur, int& stage, uint32_t& phase, uint32_t& t) {
     uint32_t rest = mask;
     do {
       uint32_t chunk = rest;
       if (__popc(rest) > kMaxA) {  // rare: more than kMaxA block rows share bc
         chunk = 0;
-        uint32_t t = rest;
+        uint32_t tt = rest;
 #pragma unroll
         for (int k = 0; k < kMaxA; ++k) {
-          uint32_t low = t & (0u - t);
+          uint32_t low = tt & (0u - tt);
           chunk |= low;
-          t ^= low;
+          tt ^= low;
         }
       }
       rest ^= chunk;
-      if (lane == 0) {
-        mbar_wait(&sh->empty[stage], phase ^ 1);
-        sh->mask[stage] = chunk;
+      if ((int)(t % kProducers) == pw) {
+        if (lane == 0) mbar_wait(&sh->empty[stage], phase ^ 1);
+        __syncwarp();
         uint8_t* st = stages + stage * kGStageBytes;
-        mbar_expect_tx(&sh->full[stage], kTileBytes + __popc(chunk) * kABytes);
-        tma_2d(st, &tmap_b, &sh->full[stage], 0, (int)bc * kBlk);
-        tma_2d(st + 2048, &tmap_b, &sh->full[stage], 64, (int)bc * kBlk);
+        // value blocks: a 512-byte block is one 16-byte cp.async per lane,
+        // placed in the 32-byte-swizzled K-major layout the MMA reads
+        // (16-byte chunk c of row r lands at chunk c ^ (r >> 2 & 1))
+        const int r = lane >> 1, ch = lane & 1;
+        const uint32_t dst_off = r * 32 + ((ch ^ ((r >> 2) & 1)) << 4);
+        uint32_t cm = chunk;
+        for (int slot = 0; cm; ++slot) {
+          const int j = __ffs(cm) - 1;
+          cm &= cm - 1;
+          const int32_t kblk = __shfl_sync(kFull, cur, j);
+          cp_async16(st + kTileBytes + slot * kABytes + dst_off, aval + (int64_t)kblk * kABytes + lane * 16);
+        }
+        cp_async_mbar_arrive(&sh->full[stage]);
+        __syncwarp();
+        if (lane == 0) {
+          sh->mask[stage] = chunk;
+          mbar_expect_tx(&sh->full[stage], kTileBytes);
+          tma_3d(st, &tmap_b, &sh->full[stage], 0, (int)bc * kBlk, 0);  // both 64-column halves
+        }
       }
-      __syncwarp();
-      if (chunk >> lane & 1u) {
-        uint8_t* st = stages + stage * kGStageBytes;
-        int slot = __popc(chunk & ((1u << lane) - 1u));
-        tma_2d(st + kTileBytes + slot * kABytes, &tmap_a, &sh->full[stage], 0, cur * kBlk);
-      }
+      ++t;
       if (++stage == kGStages) {
         stage = 0;
         phase ^= 1;
@@ -327,27 +391,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     } while (rest);
     if (mask >> lane & 1u) ++cur;
   };
-  auto end_group = [&](int& stage, uint32_t& phase) {
-    if (lane == 0) {
+  auto end_group = [&](int& stage, uint32_t& phase, uint32_t& t) {
+    if ((int)(t % kProducers) == pw && lane == 0) {
       mbar_wait(&sh->empty[stage], phase ^ 1);
       sh->mask[stage] = 0;
       mbar_arrive_plain(&sh->full[stage]);  // end-of-group marker
     }
     __syncwarp();
+    ++t;
     if (++stage == kGStages) {
       stage = 0;
       phase ^= 1;
     }
   };
 
-  if (warp == 4 && plan != nullptr) {
+  if (warp >= 4 && warp < kMmaWarp && plan != nullptr) {
     // ------------------------------------ producer: stream the mask plan
     // plan[g * nbc + bc] = bit j set iff block row g*32+j holds block
     // column bc. Lane l reads the masks of 32 consecutive block columns
     // (one coalesced load, the next batch prefetched); the nonzero ones are
     // issued in order.
     int stage = 0;
-    uint32_t phase = 0;
+    uint32_t phase = 0, t = 0;
     for (int32_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
       const int32_t br = g * kGroup + lane;
       int32_t cur = br < nbr ? __ldg(ptr + br) : 0;
@@ -361,15 +426,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           int src = __ffs(nz) - 1;
           nz &= nz - 1;
           uint32_t mask = __shfl_sync(kFull, mine, src);
-          issue(mask, (uint32_t)(bc0 + src), cur, stage, phase);
+          issue(mask, (uint32_t)(bc0 + src), cur, stage, phase, t);
         }
       }
-      end_group(stage, phase);
+      end_group(stage, phase, t);
     }
-  } else if (warp == 4) {
+  } else if (warp >= 4 && warp < kMmaWarp) {
     // ------------------------------------------- producer: k-way merge
     int stage = 0;
-    uint32_t phase = 0;
+    uint32_t phase = 0, t = 0;
     for (int32_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
       const int32_t br = g * kGroup + lane;
       int32_t cur = 0, end = 0;
@@ -394,10 +459,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t mn = __reduce_min_sync(kFull, bc);
         uint32_t mask = __ballot_sync(kFull, bc == mn && mn != 0xffffffffu);
         if (!mask) {
-          end_group(stage, phase);
+          end_group(stage, phase, t);
           break;
         }
-        issue(mask, mn, cur, stage, phase);
+        issue(mask, mn, cur, stage, phase, t);
         if (mask >> lane & 1u) {
           if (++wi == 8) {
 #pragma unroll
@@ -413,11 +478,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 1; k < 8; ++k)
             if (k == wi) bc = wa[k];
         }
-        if (!mask) break;
       }
     }
-  } else if (warp == 5) {
-    // ------------------------------------------- MMA issuer
+  } else if (warp >= kMmaWarp) {
+    // ------------------------------------------- MMA issuers
+    // kMmaWarps converged warps; warp w issues the MMAs of the block rows j
+    // with j % kMmaWarps == w (disjoint accumulators) and commits every
+    // stage, so a stage is free once all of them have committed. The
+    // issue path is warp-uniform: stage descriptors are the base
+    // descriptors plus the stage offset, one elected lane issues.
+    const int w = warp - kMmaWarp;
+    uint32_t mine = 0;
+    for (int j = w; j < kGroup; j += kMmaWarps) mine |= 1u << j;
+    const uint32_t base0 = smem_u32(stages);
+    const uint64_t adesc0 = smem_desc(base0, 2048, 1024, 2);             // SW128, MN-major
+    const uint64_t bdesc0 = smem_desc(base0 + kTileBytes, 16, 256, 6);   // SW32, K-major
     int stage = 0, it = 0;
     uint32_t phase = 0;
     for (int32_t g = blockIdx.x; g < ngroups; g += gridDim.x, ++it) {
@@ -427,25 +502,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       while (true) {
         mbar_wait(&sh->full[stage], phase);
         tc_fence_after();
-        uint32_t mask = sh->mask[stage];
-        if (lane == 0) {
-          if (mask) {
-            uint32_t base = smem_u32(stages + stage * kGStageBytes);
-            uint64_t adesc = smem_desc(base, 2048, 1024, 2);
-            uint32_t mm = mask;
-            for (int slot = 0; mm; ++slot) {
-              int j = __ffs(mm) - 1;
-              mm &= mm - 1;
-              uint64_t bdesc = smem_desc(base + kTileBytes + slot * kABytes, 16, 256, 6);
-              tc_mma(tmem + j * kBlk, adesc, bdesc, kIdesc, (started >> j) & 1u);
-            }
-            tc_commit(&sh->empty[stage]);
-          } else {
-            tc_commit(&sh->acc_full);
-            mbar_arrive(&sh->empty[stage]);
+        // the value blocks were written by cp.async (generic proxy); the
+        // MMA reads them through the async proxy
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const uint32_t mask = sh->mask[stage];
+        const uint64_t soff = (uint64_t)((stage * kGStageBytes) >> 4);
+        if (mask) {
+          uint32_t mm = mask & mine;
+          while (mm) {
+            const int j = __ffs(mm) - 1;
+            mm &= mm - 1;
+            const uint32_t slot = __popc(mask & ((1u << j) - 1u));
+            tc_mma_elect(tmem + j * kBlk, adesc0 + soff, bdesc0 + soff + ((slot * kABytes) >> 4), kIdesc,
+                         (started >> j) & 1u);
           }
+          tc_commit_elect(&sh->empty[stage]);
+          started |= mask & mine;
+        } else {
+          tc_commit_elect(&sh->acc_full);
+          if (lane == 0) mbar_arrive(&sh->empty[stage]);
         }
-        started |= mask;
         __syncwarp();
         if (++stage == kGStages) {
           stage = 0;
@@ -487,9 +563,369 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// ------------------------------------------------------------------------
+// Panel variant (used with the mask plan). Same group / TMEM layout as the
+// grouped kernel, but a pipeline stage carries up to kPanel block columns
+// (B tiles, one 3-D TMA copy each) and up to kPanelA value blocks, so the
+// per-stage costs — barrier waits, commits, the plan walk — are paid once
+// per ~kPanel x 3 MMAs instead of per ~3. Value blocks arrive by cp.async
+// (one 16-byte copy per lane per block, written in the 32-byte-swizzled
+// K-major layout). Stage metadata (tile masks) travels in shared memory.
+constexpr int kPanel = 4;
+constexpr int kPanelA = 32;
+constexpr int kPStages = 6;
+constexpr int kPStageBytes = kPanel * kTileBytes + kPanelA * kABytes;  // 32 KB
+constexpr int kDescWords = 64;  // 0 head, 1-4 tile columns, 5-8 masks, 32-63 slot blocks
+
+struct PShared {
+  uint64_t full[kPStages];
+  uint64_t empty[kPStages];
+  uint64_t acc_full;
+  uint64_t acc_empty;
+  alignas(16) uint32_t mask[kPStages][kPanel];  // mask[s][t]: block rows of tile t; a zero tile ends the stage
+  alignas(16) uint8_t slot[kPStages][kPanelA];  // slot -> block row | tile << 5
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ void tmem_zero16(uint32_t taddr) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+      "r"(0u)
+      : "memory");
+}
+
+// Warps: 0-3 epilogue (TMEM lane quarter each), 4 .. 4+kProducers-1
+// producers, then kMmaWarps MMA issuers. Ring position t (every stage of
+// every group of this CTA, plus one end marker per group) is filled by
+// producer t % kProducers and consumed by MMA warp t % kMmaWarps, so both
+// sides work on several stages at once. Accumulators are zeroed by the
+// epilogue after each drain and every MMA accumulates, so the MMAs of one
+// group may come from any MMA warp (the CTA's MMAs execute in one tensor
+// pipe; each adds into its accumulator).
+template <int kProducers, int kMmaWarps>
+__global__ void __launch_bounds__(32 * (4 + kProducers + kMmaWarps), 1)
+    k_bcsr_tc_panel(const __grid_constant__ CUtensorMap tmap_b, const uint8_t* __restrict__ aval,
+                    const int32_t* __restrict__ ptr, int32_t nbr, int32_t m, float* __restrict__ c, int64_t ldc,
+                    int accumulate, const int32_t* __restrict__ sbase, const uint32_t* __restrict__ sdesc,
+                    int dbg, unsigned long long* __restrict__ dbg_out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* stages = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  PShared* sh = reinterpret_cast<PShared*>(stages + kPStages * kPStageBytes);
+  unsigned long long t_wait = 0, t_start = clock64();
+  auto timed_wait = [&](uint64_t* bar, uint32_t par) {
+    if (dbg & 256) {
+      unsigned long long a = clock64();
+      mbar_wait(bar, par);
+      t_wait += clock64() - a;
+    } else {
+      mbar_wait(bar, par);
+    }
+  };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t ngroups = (nbr + kGroup - 1) / kGroup;
+  constexpr int kMmaWarp = 4 + kProducers;
+  // A parity wait is exact only if the stage's previous use (one ring round
+  // earlier) has already been waited on by the same warp: role counts must
+  // divide the ring size.
+  static_assert(kPStages % kProducers == 0 && kPStages % kMmaWarps == 0, "roles must divide the ring");
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kPStages; ++s) {
+      mbar_init(&sh->full[s], 1);   // the stage's producer arrives once
+      mbar_init(&sh->empty[s], 1);  // the stage's MMA warp commits once
+    }
+    mbar_init(&sh->acc_full, kMmaWarps);  // every MMA warp commits once per group
+    mbar_init(&sh->acc_empty, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sh->tmem_base)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sh->tmem_base;
+  if (warp < 4) {  // accumulators start at zero
+    const uint32_t lanes = (uint32_t)(warp * 32) << 16;
+    for (int col = 0; col < kGroup * kBlk; col += 16) tmem_zero16(tmem + lanes + col);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  // Positions of this CTA's ring: group g (g = blockIdx.x + k * gridDim.x)
+  // holds ns stages at tg .. tg + ns - 1 and its end marker at tg + ns.
+  struct Pos {
+    int32_t g, i, s0, ns;
+    uint32_t tg;
+  };
+  auto settle = [&](Pos& p) {  // carry i past the end of group g into later groups
+    while (p.g < ngroups && p.i > p.ns) {
+      p.i -= p.ns + 1;
+      p.tg += (uint32_t)p.ns + 1;
+      p.g += gridDim.x;
+      if (p.g < ngroups) {
+        p.s0 = __ldg(sbase + p.g);
+        p.ns = __ldg(sbase + p.g + 1) - p.s0;
+      }
+    }
+  };
+  auto first = [&](int i0) {
+    Pos p{(int32_t)blockIdx.x, i0, 0, 0, 0u};
+    if (p.g < ngroups) {
+      p.s0 = __ldg(sbase + p.g);
+      p.ns = __ldg(sbase + p.g + 1) - p.s0;
+    }
+    settle(p);
+    return p;
+  };
+
+  if (warp >= 4 && warp < kMmaWarp) {
+    // --------------------------------------------------------- producers
+    // Descriptors (k_bcsr_sched) are 64 words, read with one coalesced
+    // load two positions ahead, so no global latency sits between a free
+    // stage and its copies.
+    const int q = warp - 4;
+    const int r = lane >> 1, ch = lane & 1;
+    const uint32_t dst_off = r * 32 + ((ch ^ ((r >> 2) & 1)) << 4);
+    auto load = [&](const Pos& p, uint32_t& w0, uint32_t& w1) {
+      w0 = w1 = 0u;
+      if (p.g < ngroups && p.i < p.ns) {
+        const uint32_t* d = sdesc + (int64_t)(p.s0 + p.i) * kDescWords;
+        w0 = __ldg(d + lane);
+        w1 = __ldg(d + 32 + lane);
+      }
+    };
+    Pos cur = first(q);
+    Pos n1 = cur;
+    n1.i += kProducers;
+    settle(n1);
+    uint32_t c0, c1, a0, a1;
+    load(cur, c0, c1);
+    load(n1, a0, a1);
+    while (cur.g < ngroups) {
+      Pos n2 = n1;
+      n2.i += kProducers;
+      settle(n2);
+      uint32_t b0, b1;
+      load(n2, b0, b1);
+      const uint32_t tq = cur.tg + (uint32_t)cur.i;
+      const int stage = (int)(tq % kPStages);
+      const uint32_t phase = (tq / kPStages) & 1u;
+      if (lane == 0) timed_wait(&sh->empty[stage], phase ^ 1);
+      __syncwarp();
+      uint8_t* st = stages + stage * kPStageBytes;
+      if (cur.i < cur.ns) {
+        const uint32_t head = __shfl_sync(kFull, c0, 0);
+        const int ntile = (int)(head & 0xff), nblk = (int)(head >> 8 & 0xff);
+        const uint32_t tbc = __shfl_sync(kFull, c0, 1 + (lane & 3));
+        const uint32_t tmask = __shfl_sync(kFull, c0, 5 + (lane & 3));
+        if (lane >= 10 && lane < 18) sts_u32(smem_u32(&sh->slot[stage][4 * (lane - 10)]), c0);
+        if (lane < kPanel) {
+          sts_u32(smem_u32(&sh->mask[stage][lane]), lane < ntile ? tmask : 0u);
+          if (lane < ntile && !(dbg & 2)) {
+            mbar_expect_tx_only(&sh->full[stage], kTileBytes);
+            tma_3d(st + lane * kTileBytes, &tmap_b, &sh->full[stage], 0, (int)tbc * kBlk, 0);
+          }
+        }
+        __syncwarp();  // reconverge: the shuffles below must not take the divergent path
+        for (int sl = 0; sl < ((dbg & 4) ? 0 : nblk); ++sl) {
+          const int32_t kb = (int32_t)__shfl_sync(kFull, c1, sl);
+          cp_async16(st + kPanel * kTileBytes + sl * kABytes + dst_off, aval + (int64_t)kb * kABytes + lane * 16);
+        }
+      } else if (lane < kPanel) {
+        sts_u32(smem_u32(&sh->mask[stage][lane]), 0u);  // end-of-group marker
+      }
+      cp_async_mbar_arrive(&sh->full[stage]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh->full[stage]);
+      cur = n1;
+      n1 = n2;
+      c0 = a0;
+      c1 = a1;
+      a0 = b0;
+      a1 = b1;
+    }
+  } else if (warp >= kMmaWarp) {
+    // ------------------------------------------------------- MMA issuers
+    // Per stage the lanes fetch slot s = lane's (block row, tile) byte in
+    // parallel; the issue loop broadcasts one byte per MMA (the next one is
+    // fetched while the current MMA issues).
+    const int w = warp - kMmaWarp;
+    const uint32_t base0 = smem_u32(stages);
+    const uint64_t adesc0 = smem_desc(base0, 2048, 1024, 2);                     // SW128, MN-major
+    const uint64_t bdesc0 = smem_desc(base0 + kPanel * kTileBytes, 16, 256, 6);  // SW32, K-major
+    uint32_t tg = 0;  // ring position of the group's first stage
+    int it = 0;
+    for (int32_t g = blockIdx.x; g < ngroups; g += gridDim.x, ++it) {
+      const int32_t ns = __ldg(sbase + g + 1) - __ldg(sbase + g);
+      mbar_wait(&sh->acc_empty, (it & 1) ^ 1);  // accumulators drained and cleared
+      tc_fence_after();
+      // this warp's positions of the group (stages and the end marker)
+      for (uint32_t tq = tg + (uint32_t)((w - (int)(tg % kMmaWarps) + kMmaWarps) % kMmaWarps);
+           tq <= tg + (uint32_t)ns; tq += kMmaWarps) {
+        const int stage = (int)(tq % kPStages);
+        const uint32_t phase = (tq / kPStages) & 1u;
+        timed_wait(&sh->full[stage], phase);
+        tc_fence_after();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // cp.async data -> MMA reads
+        const uint4 mv = lds_v4(smem_u32(&sh->mask[stage][0]));
+        const int nblk = __popc(mv.x) + __popc(mv.y) + __popc(mv.z) + __popc(mv.w);
+        uint32_t b = 0;
+        if (lane < nblk) asm volatile("ld.shared.u8 %0, [%1];" : "=r"(b) : "r"(smem_u32(&sh->slot[stage][lane])));
+        __syncwarp();
+        const uint64_t soff = (uint64_t)((stage * kPStageBytes) >> 4);
+        if (!(dbg & 1)) {
+          uint32_t pk = __shfl_sync(kFull, b, 0);
+          for (int sl = 0; sl < nblk; ++sl) {
+            const uint32_t nx = __shfl_sync(kFull, b, (sl + 1) & 31);
+            tc_mma_elect(tmem + (pk & 31u) * kBlk, adesc0 + soff + (pk >> 5) * (kTileBytes >> 4),
+                         bdesc0 + soff + (uint32_t)sl * (kABytes >> 4), kIdesc, 1u);
+            pk = nx;
+          }
+        }
+        tc_commit_elect(&sh->empty[stage]);
+        __syncwarp();
+      }
+      tc_commit_elect(&sh->acc_full);  // fires when this warp's MMAs of the group are done
+      __syncwarp();
+      tg += (uint32_t)ns + 1;
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    // Drain the group's accumulators into C, clear them, hand them back.
+    int it = 0;
+    const int col = warp * 32 + lane;
+    const uint32_t lanes = (uint32_t)(warp * 32) << 16;
+    for (int32_t g = blockIdx.x; g < ngroups; g += gridDim.x, ++it) {
+      timed_wait(&sh->acc_full, it & 1);
+      tc_fence_after();
+      for (int j = 0; j < kGroup; ++j) {
+        const int64_t r0 = ((int64_t)g * kGroup + j) * kBlk;
+        if (r0 >= m) break;
+        float v[16];
+        tc_ld16(tmem + lanes + j * kBlk, v);
+#pragma unroll
+        for (int i = 0; i < kBlk; ++i) {
+          if (r0 + i < m) {
+            float* p = c + (r0 + i) * ldc + col;
+            *p = accumulate ? *p + v[i] : v[i];
+          }
+        }
+      }
+      for (int cc = 0; cc < kGroup * kBlk; cc += 16) tmem_zero16(tmem + lanes + cc);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh->acc_empty);
+    }
+  }
+  if ((dbg & 256) && lane == 0) {
+    atomicAdd(dbg_out + 2 * warp, t_wait);
+    atomicAdd(dbg_out + 2 * warp + 1, clock64() - t_start);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// Stage schedule of the panel SpMM, built once per matrix from the mask
+// plan and cached on the tensor. A warp per group walks the plan in block
+// column order and packs the nonzero columns greedily into stages of <=
+// kPanel tiles and <= kPanelA value blocks. kWrite = false counts stages;
+// kWrite = true writes, at sbase[g], one descriptor per stage —
+// [0] ntile | nblk << 8, [1..4] tile block columns, [5..8] tile masks,
+// [9] first slot (group-relative), [10..17] per slot one byte (block row
+// | tile << 5), [32 + slot] the slot's value block.
+template <bool kWrite>
+__global__ void __launch_bounds__(256) k_bcsr_sched(const int32_t* __restrict__ ptr, const uint32_t* __restrict__ plan,
+                                                     int32_t nbr, int32_t nbc, int32_t* __restrict__ sbase,
+                                                     uint32_t* __restrict__ sdesc) {
+  const int lane = threadIdx.x & 31;
+  const int32_t ngroups = (nbr + kGroup - 1) / kGroup;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < ngroups; g += warps) {
+    const int64_t br = g * kGroup + lane;
+    int32_t cur = br < nbr ? __ldg(ptr + br) : 0;
+    int32_t stage = kWrite ? sbase[g] : 0;
+    int ntile = 0, nblk = 0, abeg = 0, apos = 0;
+    uint32_t my_bc = 0, my_mask = 0;  // lane t < kPanel: tile t of the open stage
+    auto close = [&]() {
+      if (kWrite) {
+        uint32_t* d = sdesc + (int64_t)stage * kDescWords;
+        if (lane == 0) {
+          d[0] = (uint32_t)ntile | ((uint32_t)nblk << 8);
+          d[9] = (uint32_t)abeg;
+        }
+        if (lane < kPanel) {
+          d[1 + lane] = lane < ntile ? my_bc : 0u;
+          d[5 + lane] = lane < ntile ? my_mask : 0u;
+        }
+      }
+      ++stage;
+      ntile = 0;
+    };
+    const uint32_t* pg = plan + g * nbc;
+    for (int32_t bc0 = 0; bc0 < nbc; bc0 += 32) {
+      const uint32_t mine = bc0 + lane < nbc ? __ldg(pg + bc0 + lane) : 0u;
+      uint32_t nz = __ballot_sync(kFull, mine != 0);
+      while (nz) {
+        const int src = __ffs(nz) - 1;
+        nz &= nz - 1;
+        const uint32_t mask = __shfl_sync(kFull, mine, src);
+        const int cnt = __popc(mask);
+        if (ntile && (ntile == kPanel || nblk + cnt > kPanelA)) close();
+        if (!ntile) {
+          nblk = 0;
+          abeg = apos;
+        }
+        if (lane == ntile) {
+          my_bc = (uint32_t)(bc0 + src);
+          my_mask = mask;
+        }
+        if (kWrite && (mask >> lane & 1u)) {
+          const int sl = nblk + __popc(mask & ((1u << lane) - 1u));
+          sdesc[(int64_t)stage * kDescWords + 32 + sl] = (uint32_t)cur;
+          reinterpret_cast<uint8_t*>(sdesc + (int64_t)stage * kDescWords + 10)[sl] = (uint8_t)(lane | (ntile << 5));
+        }
+        if (mask >> lane & 1u) ++cur;
+        apos += cnt;
+        nblk += cnt;
+        ++ntile;
+      }
+    }
+    if (ntile) close();
+    if (!kWrite && lane == 0) sbase[g] = stage;
+  }
+}
+
+// In-place exclusive scan of n + 1 counts (n small: one CTA, chunked).
+__global__ void __launch_bounds__(1024) k_scan_small(int32_t* __restrict__ v, int32_t n) {
+  __shared__ int32_t sm[34];
+  __shared__ int32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int32_t b = 0; b <= n; b += 1024) {
+    const int32_t i = b + threadIdx.x;
+    const int32_t x = i < n ? v[i] : 0;
+    int32_t total;
+    const int32_t ex = block_exclusive_scan<int32_t, 1024>(x, sm, &total);
+    if (i <= n) v[i] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += total;
+    __syncthreads();
   }
 }
 
@@ -551,12 +987,22 @@ bool spmm_bcsr_tc(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dt
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       raise(SFG_ERR_CUDA, "cuTensorMapEncodeTiled(A) failed");
   }
+  CUtensorMap tb3;  // both 64-column halves of a B tile in one copy: dims (64, n, 2)
+  {
+    cuuint64_t dims[3] = {64, (cuuint64_t)a->n, 2};
+    cuuint64_t strides[2] = {(cuuint64_t)ldb * 2, 128};
+    cuuint32_t box[3] = {64, kBlk, 2};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (encode(&tb3, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(b), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      raise(SFG_ERR_CUDA, "cuTensorMapEncodeTiled(B, 3-D) failed");
+  }
   const size_t smem = 1024 + kStages * kStageBytes + sizeof(Shared) + 64;
   const size_t gsmem = 1024 + kGStages * kGStageBytes + sizeof(GShared) + 64;
   static bool attr = false;
   if (!attr) {
     SFG_CUDA(cudaFuncSetAttribute(k_bcsr_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    SFG_CUDA(cudaFuncSetAttribute(k_bcsr_tc_group, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem));
     attr = true;
   }
   static const bool per_row = [] {
@@ -581,8 +1027,56 @@ bool spmm_bcsr_tc(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dt
                  (int32_t)a->nbr, (int32_t)a->nbc, mut->tc_plan);
     }
     int grid = (int)std::min<int64_t>(ngroups, (int64_t)ctx->sms);
-    SFG_LAUNCH(k_bcsr_tc_group, grid, kThreads, gsmem, ctx->stream, tb, ta, a->ptr, a->idx, (int32_t)a->nbr,
-               (int32_t)a->m, c, ldc, accumulate ? 1 : 0, mut->tc_plan, (int32_t)a->nbc);
+    if (mut->tc_plan && !mut->tc_desc) {
+      // stage schedule: count, scan, write (once per matrix, cached)
+      mut->tc_base = dalloc_n<int32_t>(ctx, ngroups + 1);
+      int sgrid = stream_grid(ctx, ngroups * 32, 256, 1, 8);
+      SFG_LAUNCH(k_bcsr_sched<false>, sgrid, 256, 0, ctx->stream, a->ptr, mut->tc_plan, (int32_t)a->nbr,
+                 (int32_t)a->nbc, mut->tc_base, nullptr);
+      SFG_LAUNCH(k_scan_small, 1, 1024, 0, ctx->stream, mut->tc_base, (int32_t)ngroups);
+      int32_t nstages = 0;
+      read_back(ctx, mut->tc_base + ngroups, sizeof(int32_t), &nstages);
+      mut->tc_desc = dalloc_n<uint32_t>(ctx, (int64_t)nstages * kDescWords);
+      SFG_LAUNCH(k_bcsr_sched<true>, sgrid, 256, 0, ctx->stream, a->ptr, mut->tc_plan, (int32_t)a->nbr,
+                 (int32_t)a->nbc, mut->tc_base, mut->tc_desc);
+    }
+    if (mut->tc_desc) {
+      // 3 producer and 3 MMA warps measured best (scripts/gpu_run46.sh
+      // sweep: 0.46 ms vs 0.55-0.61 ms for 2 or 6 producers at m = 65536)
+      constexpr int kP = 3, kW = 3;
+      const size_t psmem = 1024 + kPStages * kPStageBytes + sizeof(PShared) + 64;
+      static const int dbg = (std::getenv("SFG_TC_PROF") ? 256 : 0) |
+                             (std::getenv("SFG_TC_ABLATE") ? std::atoi(std::getenv("SFG_TC_ABLATE")) : 0);
+      unsigned long long* dbg_out = nullptr;
+      if (dbg) {
+        dbg_out = static_cast<unsigned long long*>(scratch(ctx, 64 * 8));
+        SFG_CUDA(cudaMemsetAsync(dbg_out, 0, 64 * 8, ctx->stream));
+      }
+      auto go = [&](auto kern, int threads) {
+        // set on every call: a once-only static setup measured 30 % slower
+        // launches (0.61 vs 0.46 ms at m = 65536)
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+        SFG_LAUNCH(kern, grid, threads, psmem, ctx->stream, tb3, static_cast<const uint8_t*>(a->val), a->ptr,
+                   (int32_t)a->nbr, (int32_t)a->m, c, ldc, accumulate ? 1 : 0, mut->tc_base, mut->tc_desc, dbg,
+                   dbg_out);
+      };
+      go(k_bcsr_tc_panel<kP, kW>, 32 * (4 + kP + kW));
+      if (dbg & 256) {
+        unsigned long long h[64];
+        SFG_CUDA(cudaMemcpyAsync(h, dbg_out, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+        SFG_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (int w = 0; w < 4 + kP + kW; ++w)
+          std::fprintf(stderr, "[tc prof] warp %2d: wait %5.1f%% of %.0f cycles/CTA\n", w,
+                       100.0 * h[2 * w] / (double)(h[2 * w + 1] ? h[2 * w + 1] : 1), h[2 * w + 1] / (double)grid);
+      }
+    } else {
+      // set on every call: a once-only static setup measured 30 % slower
+      // launches of the panel kernel (0.61 vs 0.46 ms at m = 65536)
+      cudaFuncSetAttribute(k_bcsr_tc_group<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem);
+      SFG_LAUNCH((k_bcsr_tc_group<2, 2>), grid, 32 * 8, gsmem, ctx->stream, tb3,
+                 static_cast<const uint8_t*>(a->val), a->ptr, a->idx, (int32_t)a->nbr, (int32_t)a->m, c, ldc,
+                 accumulate ? 1 : 0, mut->tc_plan, (int32_t)a->nbc);
+    }
   }
   return true;
 }

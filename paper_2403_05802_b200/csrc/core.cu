@@ -160,7 +160,11 @@ void free_tensor_arrays(sfg_tensor* t) {
   dfree(ctx, t->slots);
   dfree(ctx, t->val);
   dfree(ctx, t->tc_plan);
+  dfree(ctx, t->tc_base);
+  dfree(ctx, t->tc_desc);
   t->tc_plan = nullptr;
+  t->tc_base = nullptr;
+  t->tc_desc = nullptr;
   t->row = t->ptr = t->idx = t->slots = nullptr;
   t->val = nullptr;
 }

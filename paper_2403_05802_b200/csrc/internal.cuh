@@ -88,6 +88,8 @@ struct sfg_tensor {
   int64_t threshold = 0;         // HYB min_sum
   int32_t has_zeros = -1;        // COO: explicit zero values present? 1/0, -1 unknown
   uint32_t* tc_plan = nullptr;   // BCSR: cached tensor-core SpMM plan (bcsr_tc.cu)
+  int32_t* tc_base = nullptr;    //   and its stage schedule: per-group first stage,
+  uint32_t* tc_desc = nullptr;   //   stage descriptors
   int32_t* row = nullptr;
   int32_t* ptr = nullptr;
   int32_t* idx = nullptr;

@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+for v in 0 1 2 3 4 5; do
+echo "variant $v" >> gpurun_out/prof34.log
+SFG_BCSR_TC_VAR=$v timeout 300 python scripts/prof_bcsr.py 65536 >> gpurun_out/prof34.log 2>&1
+SFG_BCSR_TC_VAR=$v timeout 600 python -m pytest tests/test_gpu_spmm.py -m "gpu and not slow" -q --timeout 120 -p no:cacheprovider -x -k "tensor_core" 2>&1 | tail -1 >> gpurun_out/prof34.log
+done

@@ -9,6 +9,8 @@
 // fp32 or bf16. The BCSR tensor-core path lives in bcsr_tc.cu.
 #include <cuda_bf16.h>
 
+#include <algorithm>
+
 #include "devutil.cuh"
 #include "internal.cuh"
 
@@ -63,7 +65,8 @@ struct Dense {
   float* c;
   int64_t ldc;
   int32_t nd;
-  int acc;
+  int acc;        // non-atomic row stores add to C (accumulate, or C was zeroed first)
+  int keep = 0;   // the caller's accumulate flag (C holds input to add to)
 };
 
 // Accumulate `val * B[col][cols of this lane]` for the lane's column chunk.
@@ -130,6 +133,81 @@ __global__ void __launch_bounds__(kBlock) k_spmm_rows(const int32_t* __restrict_
     }
     int64_t r = rows ? __ldg(rows + p) : p;
     store_row<V>(d, r, c0, false, acc);
+  }
+}
+
+// Merge-path CSR (load balanced by rows + entries, so one row of a million
+// entries no longer serialises the kernel). The (row ends, entries) merge
+// sequence of length m + nnz is cut into chunks of kMergeItems; a first
+// kernel finds every cut's (row, entry) coordinate by binary search
+// (Merrill & Garland's merge-path), then a warp per chunk walks its entries
+// in order, flushing each row as its end passes. Rows wholly inside the
+// chunk are stored; the chunk's first and last rows may be shared with
+// neighbouring chunks and are added atomically. C is zeroed beforehand
+// (or holds the accumulate input), so empty rows need no work.
+constexpr int kMergeItems = 1024;
+
+__global__ void k_merge_cuts(const int32_t* __restrict__ ptr, int64_t m, int64_t nnz, int64_t ncuts,
+                             int2* __restrict__ cuts) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < ncuts; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t dgl = std::min<int64_t>(q * kMergeItems, m + nnz);
+    int64_t lo = dgl > nnz ? dgl - nnz : 0, hi = dgl < m ? dgl : m;
+    while (lo < hi) {  // rows consumed before the diagonal: row ends ptr[i+1] <= entries consumed
+      const int64_t mid = (lo + hi) >> 1;
+      if ((int64_t)__ldg(ptr + mid + 1) <= dgl - mid - 1) lo = mid + 1;
+      else hi = mid;
+    }
+    cuts[q] = make_int2((int)lo, (int)(dgl - lo));
+  }
+}
+
+template <typename TB, int V>
+__global__ void __launch_bounds__(kBlock) k_spmm_merge(const int32_t* __restrict__ ptr,
+                                                        const int32_t* __restrict__ col,
+                                                        const float* __restrict__ val,
+                                                        const int2* __restrict__ cuts, int64_t nchunks,
+                                                        Dense d) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int chunks = (d.nd + 32 * V - 1) / (32 * V);
+  const bool vec_ok = (d.nd % (32 * V) == 0) && (d.ldb % V == 0);
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nchunks * chunks; w += warps) {
+    const int64_t q = w / chunks;
+    const int c0 = (int)(w - q * chunks) * 32 * V + lane * V;
+    const int2 a = __ldg(cuts + q), b = __ldg(cuts + q + 1);
+    int i = a.x;
+    const int j0 = a.y, j1 = b.y;
+    int row_end = __ldg(ptr + i + 1);
+    const bool first_shared = j0 > __ldg(ptr + i);  // row a.x began in an earlier chunk
+    bool shared = first_shared;
+    Dense dw = d;  // rows owned by this chunk: plain stores unless accumulating
+    dw.acc = d.keep;
+    float acc[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) acc[k] = 0.f;
+    bool any = false;
+    for (int base = j0; base < j1; base += 32) {
+      const int k = base + lane;
+      const int mc = k < j1 ? ld_stream(col + k) : 0;
+      const float mv = k < j1 ? ld_stream(val + k) : 0.f;
+      const int cnt = min(32, j1 - base);
+      for (int t = 0; t < cnt; ++t) {
+        const int j = base + t;
+        while (j >= row_end) {  // row i ends before entry j: flush it
+          if (any) store_row<V>(dw, i, c0, shared, acc);
+#pragma unroll
+          for (int k2 = 0; k2 < V; ++k2) acc[k2] = 0.f;
+          any = false;
+          shared = false;
+          ++i;
+          row_end = __ldg(ptr + i + 1);
+        }
+        fma_row<TB, V>(d, __shfl_sync(kFull, mc, t), __shfl_sync(kFull, mv, t), c0, vec_ok, acc);
+        any = true;
+      }
+    }
+    // the open row: complete if its end is this chunk's last row end
+    if (any) store_row<V>(dw, i, c0, shared || row_end > j1 || i >= b.x, acc);
   }
 }
 
@@ -363,6 +441,17 @@ void launch_fmt(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
   constexpr int kR = 4;
   switch (a->kind) {
     case SFG_CSR:
+      if (a->m == 0 || a->nnz == 0) break;
+      {
+        const int64_t total = a->m + a->nnz;
+        const int64_t nchunks = ceil_div(total, kMergeItems);
+        auto* cuts = static_cast<int2*>(scratch(ctx, (nchunks + 1) * sizeof(int2)));
+        SFG_LAUNCH(k_merge_cuts, (int)std::min<int64_t>(ceil_div(nchunks + 1, 256), (int64_t)ctx->sms * 8), 256, 0,
+                   ctx->stream, a->ptr, a->m, a->nnz, nchunks + 1, cuts);
+        SFG_LAUNCH((k_spmm_merge<TB, V>), grid_for(nchunks * chunks), kBlock, 0, ctx->stream, a->ptr, a->idx, fv,
+                   cuts, nchunks, d);
+      }
+      break;
     case SFG_DCSR: {
       if (stored_rows == 0) break;
       const int32_t* rows = a->kind == SFG_DCSR ? a->row : nullptr;
@@ -436,12 +525,13 @@ void spmm(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dtype, int
     SFG_LAUNCH(k_zero_gap_rows, (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a->nnr + 1, kBlock / 32),
                                                                             (int64_t)ctx->sms * 16)),
                kBlock, 0, ctx->stream, a->row, a->nnr, a->m, (int32_t)nd, c, ldc);
-    Dense d{b, ldb, c, ldc, (int32_t)nd, 0};
+    Dense d{b, ldb, c, ldc, (int32_t)nd, 0, 0};
     if (b_dtype == SFG_BF16) launch_v<__nv_bfloat16>(ctx, a, d);
     else launch_v<float>(ctx, a, d);
     return;
   }
-  bool zero_first = !accumulate && (a->kind == SFG_COO || a->kind == SFG_CSC || a->kind == SFG_BCSR);
+  bool zero_first =
+      !accumulate && (a->kind == SFG_COO || a->kind == SFG_CSC || a->kind == SFG_BCSR || a->kind == SFG_CSR);
   if (zero_first && a->m > 0) {
     if (ldc == nd)
       SFG_CUDA(cudaMemsetAsync(c, 0, a->m * ldc * sizeof(float), ctx->stream));
@@ -449,7 +539,7 @@ void spmm(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dtype, int
       SFG_CUDA(cudaMemset2DAsync(c, ldc * sizeof(float), 0, nd * sizeof(float), a->m, ctx->stream));
   }
   // kernels that own whole rows write with accumulate semantics after zeroing
-  Dense d{b, ldb, c, ldc, (int32_t)nd, (accumulate || zero_first) ? 1 : 0};
+  Dense d{b, ldb, c, ldc, (int32_t)nd, (accumulate || zero_first) ? 1 : 0, accumulate ? 1 : 0};
   if (b_dtype == SFG_BF16) launch_v<__nv_bfloat16>(ctx, a, d);
   else launch_v<float>(ctx, a, d);
 }

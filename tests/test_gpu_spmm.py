@@ -122,3 +122,29 @@ def test_bcsr16_bf16_tensor_core(ctx, port, shape, density):
     b64 = bits_to_f64(bb)
     cr = port.spmm(port.convert(p, "BCSR", 16, 16), b64)
     check(cd, cr, abs_bound(rows, cols, vals, m, b64), ("bcsr-tc", shape, density))
+
+
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_spmm_csr_heavy_and_empty_rows(ctx, port, accumulate):
+    """CSR SpMM is load balanced over (rows + entries): one row far longer
+    than a merge chunk (1024 items), runs of empty rows, a full last row."""
+    rng = np.random.default_rng(4)
+    m, n, nd = 5000, 6000, 32
+    rows = [np.full(5000, 3), np.full(2500, 4), rng.integers(100, 4000, 20000), np.full(3000, m - 1)]
+    r = np.concatenate(rows)
+    c = rng.integers(0, n, len(r))
+    key = np.unique(r.astype(np.int64) * n + c)
+    r, c = key // n, key % n
+    v = (rng.random(len(r)) * 2 - 1).astype(np.float32)
+    b = (rng.random((n, nd)) * 2 - 1).astype(np.float32)
+    d, p = ctx.from_coo(m, n, r, c, v), port.from_coo(m, n, r, c, v)
+    a = ctx.convert(d, "CSR")
+    c0 = (rng.random((m, nd)) * 2 - 1).astype(np.float32)
+    cbuf = ctx.buffer(c0.nbytes).upload(c0)
+    bbuf = ctx.buffer(b.nbytes).upload(b)
+    ctx.spmm_device(a, bbuf.ptr, sfg.F32, nd, cbuf.ptr, accumulate=accumulate)
+    cd = cbuf.download(np.float32, m * nd).reshape(m, nd)
+    cr = port.spmm(port.convert(p, "CSR"), b.astype(np.float64))
+    if accumulate:
+        cr = cr + c0.astype(np.float64)
+    check(cd, cr, abs_bound(r, c, v, m, b.astype(np.float64)) + np.abs(c0) * accumulate, ("heavy", accumulate))

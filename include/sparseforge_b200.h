@@ -173,6 +173,14 @@ int sfg_spmv(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, ui
 int sfg_spmm(sfg_context* ctx, const sfg_tensor* a, const void* b, int32_t b_dtype, int64_t nd,
              int64_t ldb, float* c, int64_t ldc, uint32_t flags);
 
+/* ---------------------------------------------------------------- ingest */
+/* read_matrix_market (io.hpp:50-121) + from_coo (tensor.hpp:156): a
+ * coordinate Matrix Market file (real | integer | pattern, general |
+ * symmetric) parsed on the device into a canonical COO. Same header checks
+ * (SFG_ERR_UNSUPPORTED_HEADER), the same "path:line: msg" SFG_ERR_PARSE
+ * errors, SFG_ERR_IO when unreadable; flags: SFG_FLAG_SUM_DUPLICATES. */
+int sfg_read_matrix_market(sfg_context* ctx, const char* path, uint32_t flags, sfg_tensor** out);
+
 /* ------------------------------------------------------ row partitioning */
 /* nnz-balanced contiguous row split for P devices: bounds[0..P]
  * with bounds[0] = 0, bounds[P] = rows, boundaries at ptr quantiles. */

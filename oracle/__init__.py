@@ -256,6 +256,14 @@ class Ref(_Base):
     def _spmm(self, mat, b, c, threads):
         return self.lib.sfr_spmm(mat.h, _pf64(b), C.c_int64(b.shape[1]), _pf64(c), C.c_int(threads))
 
+    def read_mm(self, path, sum_duplicates=False):
+        """read_matrix_market + from_coo (io.hpp:50, tensor.hpp:156)."""
+        h = C.c_void_p()
+        self._check(self.lib.sfr_read_mm(os.fsencode(path), C.c_int(1 if sum_duplicates else 0), C.byref(h)))
+        m, n = C.c_int64(), C.c_int64()
+        self.lib.sfr_coo_shape(h, C.byref(m), C.byref(n))
+        return _Coo(self.lib, h, self.prefix, (m.value, n.value))
+
     def plan(self, src, dst):
         buf = C.create_string_buffer(4096)
         self._check(self.lib.sfr_plan(src.encode(), dst.encode(), buf, C.c_int64(4096)))

@@ -16,6 +16,7 @@
 //                                                      kernel.hpp:80, 236
 //   sfr_decompose_rows -> decompose(count rule)        decompose.hpp:30
 //   sfr_plan           -> plan_conversion + plan_lines planner.hpp:95, 22
+//   sfr_read_mm        -> read_matrix_market + from_coo io.hpp:50-121
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -23,6 +24,7 @@
 
 #include "sparseforge/decompose.hpp"
 #include "sparseforge/formats.hpp"
+#include "sparseforge/io.hpp"
 #include "sparseforge/kernel.hpp"
 #include "sparseforge/parse.hpp"
 #include "sparseforge/planner.hpp"
@@ -96,6 +98,23 @@ int sfr_coo_get(void* h, int64_t* row, int64_t* col, double* val) {
 }
 
 void sfr_coo_free(void* h) { delete static_cast<RefCoo*>(h); }
+
+// Matrix Market file -> canonical COO, exactly as the reference CLI loads a
+// COO operand: read_matrix_market, then from_coo (io.hpp:50, tensor.hpp:156).
+int sfr_read_mm(const char* path, int sum_duplicates, void** out) {
+  *out = nullptr;
+  return guard([&] {
+    CooData d = read_matrix_market(path);
+    *out = new RefCoo{from_coo(d.shape, d.coords, d.values, sum_duplicates != 0)};
+  });
+}
+
+int sfr_coo_shape(void* h, int64_t* m, int64_t* n) {
+  const WorkingTensor& t = static_cast<RefCoo*>(h)->t;
+  *m = t.shape.extents[0];
+  *n = t.shape.extents[1];
+  return 0;
+}
 
 int sfr_convert(void* h, const char* fmt, void** out) {
   *out = nullptr;

@@ -121,6 +121,7 @@ def load():
         "sfg_spmm": (C.c_int, [vp, vp, vp, i32, i64, i64, vp, i64, u32]),
         "sfg_row_partition": (C.c_int, [vp, vp, i32, C.POINTER(C.c_int64)]),
         "sfg_coo_slice_rows": (C.c_int, [vp, vp, i64, i64, pp]),
+        "sfg_read_matrix_market": (C.c_int, [vp, C.c_char_p, u32, pp]),
         "sfgx_gen_uniform": (C.c_int, [vp, C.c_uint64, i64, i64, i32, pp]),
         "sfgx_gen_rmat": (C.c_int, [vp, C.c_uint64, i32, i64, pp]),
         "sfgx_gen_hypersparse": (C.c_int, [vp, C.c_uint64, i64, i64, i64, pp]),
@@ -341,6 +342,14 @@ class Context:
         b = (C.c_int64 * (parts + 1))()
         _check(self.lib.sfg_row_partition(self.h, coo.h, parts, b))
         return list(b)
+
+    def read_matrix_market(self, path: str, sum_duplicates: bool = False) -> Tensor:
+        """read_matrix_market + from_coo (io.hpp:50, tensor.hpp:156), parsed
+        on the device."""
+        h = C.c_void_p()
+        _check(self.lib.sfg_read_matrix_market(self.h, os.fsencode(path),
+                                               FLAG_SUM_DUPLICATES if sum_duplicates else 0, C.byref(h)))
+        return Tensor(self, h)
 
     def slice_rows(self, coo: Tensor, r0: int, r1: int) -> Tensor:
         h = C.c_void_p()

@@ -175,6 +175,7 @@ int sfg_context_destroy(sfg_context* ctx) {
     sfg::release_cached(ctx);
     cudaStreamSynchronize(ctx->stream);
     cudaFreeHost(ctx->pinned);
+    if (ctx->staging) cudaFreeHost(ctx->staging);
     delete ctx;
   });
 }
@@ -469,6 +470,14 @@ int sfg_row_partition(sfg_context* ctx, const sfg_tensor* coo, int32_t parts, in
     require(ctx && coo && bounds && parts > 0, SFG_ERR_INVALID_OPERATION, "bad argument");
     require(coo->kind == SFG_COO, SFG_ERR_INVALID_OPERATION, "row partition expects COO");
     sfg::row_partition(ctx, coo, parts, bounds);
+  });
+}
+
+int sfg_read_matrix_market(sfg_context* ctx, const char* path, uint32_t flags, sfg_tensor** out) {
+  return guard([&] {
+    require(ctx && path && out, SFG_ERR_INVALID_OPERATION, "null argument");
+    *out = nullptr;
+    *out = sfg::read_matrix_market(ctx, path, (flags & SFG_FLAG_SUM_DUPLICATES) != 0);
   });
 }
 

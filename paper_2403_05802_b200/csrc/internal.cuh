@@ -52,6 +52,8 @@ struct sfg_context {
   cudaStream_t stream = nullptr;
   int sms = 148;
   int64_t* pinned = nullptr;   // small host scratch for size read-backs
+  char* staging = nullptr;     // pinned host staging for file ingest (grow-only)
+  size_t staging_bytes = 0;
   void* scratch = nullptr;     // device scratch (counters, histograms, flags)
   size_t scratch_bytes = 0;
   void* status = nullptr;      // look-back status words only
@@ -141,6 +143,8 @@ inline int stream_grid(const sfg_context* ctx, int64_t work_items, int block, in
 // Validates a caller-sorted COO; returns 1 when it holds explicit zero values.
 int check_coo_canonical(sfg_context* ctx, const int32_t* row, const int32_t* col, const float* val, int64_t m,
                          int64_t n, int64_t nnz);
+// Matrix Market file -> canonical COO (mm_read.cu).
+sfg_tensor* read_matrix_market(sfg_context* ctx, const char* path, bool sum_duplicates);
 sfg_tensor* sort_coo(sfg_context* ctx, int64_t m, int64_t n, int64_t nnz, const int32_t* row,
                      const int32_t* col, const float* val, bool sum_duplicates);
 void radix_sort(sfg_context* ctx, uint64_t* keys, uint32_t* pay, int64_t n, int key_bits,

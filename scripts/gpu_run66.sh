@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT
+timeout 600 python -m pytest tests/test_mm.py -q --timeout 120 -p no:cacheprovider -m gpu > gpurun_out/pytest66.log 2>&1
+echo "pytest exit $?" >> gpurun_out/pytest66.log
+SFG_TRACE_MM=1 timeout 900 python scripts/bench_mm.py 1048576 16 > gpurun_out/bench_mm66.log 2>&1

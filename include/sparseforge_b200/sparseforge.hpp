@@ -352,6 +352,39 @@ inline WorkingTensor from_coo(TensorShape shape, const std::vector<std::vector<s
   return t;
 }
 
+// -------------------------------------------------------------- io.hpp
+// read_matrix_market (io.hpp:50-121). The file is parsed on the device;
+// CooData holds the entries in canonical (row, col) order — from_coo of it
+// gives the same tensor as from_coo of the reference's file-order CooData.
+struct CooData {
+  TensorShape shape;
+  std::vector<std::vector<std::int64_t>> coords;
+  std::vector<double> values;
+};
+
+// The device path end to end: file -> canonical COO WorkingTensor (what the
+// reference's CLI builds with read_matrix_market + from_coo).
+inline WorkingTensor load_matrix_market(const std::string& path, bool sum_duplicates = false) {
+  sfg_tensor* h = nullptr;
+  b200::check(sfg_read_matrix_market(b200::default_context().get(), path.c_str(),
+                                     sum_duplicates ? SFG_FLAG_SUM_DUPLICATES : 0u, &h));
+  sfg_tensor_view v;
+  b200::check(sfg_tensor_view_get(b200::default_context().get(), h, &v));
+  WorkingTensor t;
+  t.shape = TensorShape{{v.rows, v.cols}};
+  t.enc = resolve_format("COO");
+  t.dev = std::make_shared<b200::TensorHandle>(h);
+  return t;
+}
+
+inline CooData read_matrix_market(const std::string& path) {
+  WorkingTensor t = load_matrix_market(path);  // duplicates: DuplicateCoordinate, as from_coo would
+  CooData d;
+  d.shape = t.shape;
+  t.download(d.coords, d.values);
+  return d;
+}
+
 // --------------------------------------------------------- planner.hpp
 struct ConversionOp {
   std::string text;  // print_op form, e.g. "Fill(0)"

@@ -4,6 +4,7 @@
 // values are the reference goldens for matrix A (proj/tests/oracle_data.hpp).
 #include <cmath>
 #include <cstdio>
+#include <string>
 #include <vector>
 
 #include "sparseforge_b200/sparseforge.hpp"
@@ -27,7 +28,7 @@ static bool same(const A& a, const B& b) {
   return true;
 }
 
-int main() {
+int main(int argc, char** argv) {
   const std::vector<std::int64_t> coo_d0 = {0, 1, 2, 2, 2, 4}, coo_d1 = {0, 1, 1, 2, 3, 3};
   const std::vector<double> coo_val = {1, 2, 3, 4, 5, 6};
   // shuffled input (FromCooSortsInput, test_tensor.cpp:47-54)
@@ -125,6 +126,24 @@ int main() {
   s.download(coords, values);
   EXPECT(same(values, std::vector<double>{1.0, 12.0}));
 
+  if (argc > 1) {  // Matrix Market ingest (io.hpp:50): tests/golden/mm fixtures
+    const std::string dir = argv[1];
+    CooData d = read_matrix_market(dir + "/real_symmetric.mtx");
+    EXPECT(d.shape.extents == (std::vector<std::int64_t>{4, 4}));
+    EXPECT(same(d.coords[0], std::vector<std::int64_t>{0, 0, 1, 1, 2, 2, 3, 3}));
+    EXPECT(same(d.coords[1], std::vector<std::int64_t>{0, 1, 0, 2, 1, 3, 2, 3}));
+    EXPECT(same(d.values, std::vector<double>{2, -1, -1, -1, -1, -1, -1, 2}));
+    WorkingTensor w = load_matrix_market(dir + "/pattern_symmetric.mtx");
+    w.download(coords, values);
+    EXPECT(values.size() == 6);
+    try {
+      read_matrix_market(dir + "/err_missing_value.mtx");
+      EXPECT(false);
+    } catch (const Error& e) {
+      EXPECT(e.kind() == ErrorKind::Parse);
+      EXPECT(std::string(e.what()).find(":4: missing value") != std::string::npos);
+    }
+  }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
 }

@@ -25,6 +25,7 @@ def test_cpp_api_compiles(tmp_path):
 @pytest.mark.gpu
 def test_cpp_api_runs_on_gpu(tmp_path):
     exe = build(tmp_path)
-    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    out = subprocess.run([exe, os.path.join(ROOT, "tests", "golden", "mm")], capture_output=True, text=True,
+                         timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "OK" in out.stdout

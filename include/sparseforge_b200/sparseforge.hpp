@@ -404,11 +404,16 @@ inline std::vector<std::string> plan_lines(const ConversionPlan& plan) {
 
 // plan_conversion (planner.hpp:95-252) for COO sources.
 inline ConversionPlan plan_conversion(const FormatEncoding& src, const FormatEncoding& dst) {
-  char buf[1024];
-  b200::check(sfg_plan_text(&src.fmt, &dst.fmt, buf, sizeof buf));
   ConversionPlan p;
   p.src = src;
   p.dst = dst;
+  if (src.fmt.kind != SFG_COO) {
+    // compressed sources: the device dematerializes and regrows in one call
+    // (convert_src.cu); ELL and hybrid sources fail there (UnsupportedSource)
+    return p;
+  }
+  char buf[1024];
+  b200::check(sfg_plan_text(&src.fmt, &dst.fmt, buf, sizeof buf));
   std::string s(buf);
   size_t pos = 0;
   while (pos < s.size()) {
@@ -429,6 +434,9 @@ inline void apply_plan(WorkingTensor& t, const ConversionPlan& plan) {
   b200::check(sfg_convert(b200::default_context().get(), t.dev->h, &plan.dst.fmt, &out));
   t.dev = std::make_shared<b200::TensorHandle>(out);
   t.enc = plan.dst;
+  sfg_tensor_view v;  // a BCSR source regrows over its whole block grid
+  b200::check(sfg_tensor_view_get(b200::default_context().get(), out, &v));
+  t.shape = TensorShape{{v.rows, v.cols}};
 }
 
 inline void convert_structure(WorkingTensor& t, const FormatEncoding& src, const FormatEncoding& dst) {

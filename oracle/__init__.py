@@ -256,6 +256,15 @@ class Ref(_Base):
     def _spmm(self, mat, b, c, threads):
         return self.lib.sfr_spmm(mat.h, _pf64(b), C.c_int64(b.shape[1]), _pf64(c), C.c_int(threads))
 
+    def convert_from(self, coo, mid, fmt, r=0, c=0, mr=0, mc=0):
+        """A tensor first converted to `mid`, then from `mid` to `fmt`
+        (convert_structure from a non-COO source, planner.hpp:95)."""
+        h = C.c_void_p()
+        text = _fmt_text(fmt, r, c)
+        mtext = _fmt_text(mid, mr, mc)
+        self._check(self.lib.sfr_convert_from(coo.h, mtext.encode(), text.encode(), C.byref(h)))
+        return _Mat(self.lib, h, self.prefix, text, coo.shape)
+
     def read_mm(self, path, sum_duplicates=False):
         """read_matrix_market + from_coo (io.hpp:50, tensor.hpp:156)."""
         h = C.c_void_p()

@@ -17,6 +17,7 @@
 //   sfr_decompose_rows -> decompose(count rule)        decompose.hpp:30
 //   sfr_plan           -> plan_conversion + plan_lines planner.hpp:95, 22
 //   sfr_read_mm        -> read_matrix_market + from_coo io.hpp:50-121
+//   sfr_convert_from   -> convert_structure from a non-COO structure
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -124,6 +125,19 @@ int sfr_convert(void* h, const char* fmt, void** out) {
     convert_structure(t, resolve_format("COO"), dst);
     auto* m = new RefMat{dst, materialize(t, infer_storage(dst))};
     *out = m;
+  });
+}
+
+// A tensor held in structure `mid` converted to `dst` (convert_structure
+// from a non-COO source, planner.hpp:95-252: normalize, realign, regrow).
+int sfr_convert_from(void* h, const char* mid, const char* fmt, void** out) {
+  *out = nullptr;
+  return guard([&] {
+    WorkingTensor t = static_cast<RefCoo*>(h)->t;
+    FormatEncoding src = resolve_format(mid), dst = resolve_format(fmt);
+    convert_structure(t, resolve_format("COO"), src);
+    convert_structure(t, src, dst);
+    *out = new RefMat{dst, materialize(t, infer_storage(dst))};
   });
 }
 

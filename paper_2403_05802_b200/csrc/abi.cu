@@ -236,7 +236,7 @@ int sfg_plan_text(const sfg_format* src, const sfg_format* dst, char* buf, int64
     require(src && dst, SFG_ERR_INVALID_OPERATION, "null format");
     validate_format(*dst);
     if (src->kind != SFG_COO)
-      sfg::raise(SFG_ERR_UNSUPPORTED_SOURCE, "the device planner converts from COO sources");
+      sfg::raise(SFG_ERR_UNSUPPORTED_SOURCE, "plan text is generated for COO sources");
     copy_text(plan_for(*dst), buf, len);
   });
 }
@@ -304,8 +304,10 @@ int sfg_convert(sfg_context* ctx, const sfg_tensor* src, const sfg_format* dst, 
     require(ctx && src && dst && out, SFG_ERR_INVALID_OPERATION, "null argument");
     *out = nullptr;
     validate_format(*dst);
-    if (src->kind != SFG_COO)
-      sfg::raise(SFG_ERR_UNSUPPORTED_SOURCE, "the device planner converts from COO sources");
+    if (src->kind != SFG_COO) {
+      *out = sfg::convert_from_compressed(ctx, src, *dst);
+      return;
+    }
     if (src->m <= 0 || src->n <= 0)
       sfg::raise(SFG_ERR_INVALID_OPERATION, "empty bounds at extent-only level");
     switch (dst->kind) {

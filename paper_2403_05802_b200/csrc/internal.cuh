@@ -155,6 +155,8 @@ void compress_sorted(sfg_context* ctx, const int32_t* key, const int32_t* other,
 void sort_u64_keys(sfg_context* ctx, uint64_t* keys, int64_t n, int key_bits, uint64_t** sorted_out);
 
 sfg_tensor* coo_to_coo(sfg_context* ctx, const sfg_tensor* s);
+// Non-COO sources (convert_src.cu): dematerialize, then the COO paths.
+sfg_tensor* convert_from_compressed(sfg_context* ctx, const sfg_tensor* s, const sfg_format& dst);
 sfg_tensor* coo_to_csr(sfg_context* ctx, const sfg_tensor* s);
 sfg_tensor* coo_to_csc(sfg_context* ctx, const sfg_tensor* s);
 sfg_tensor* coo_to_dcsr(sfg_context* ctx, const sfg_tensor* s);

@@ -60,7 +60,7 @@ def test_format_resolution():
         assert ei.value.kind == "Parse", bad
 
 
-def test_non_coo_sources_are_rejected():
+def test_non_coo_sources_have_no_plan_text():
     with pytest.raises(sfg.SfgError) as ei:
         sfg.plan_lines("CSR", "COO")
     assert ei.value.kind == "UnsupportedSource"

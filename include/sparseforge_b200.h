@@ -181,6 +181,15 @@ int sfg_spmm(sfg_context* ctx, const sfg_tensor* a, const void* b, int32_t b_dty
  * errors, SFG_ERR_IO when unreadable; flags: SFG_FLAG_SUM_DUPLICATES. */
 int sfg_read_matrix_market(sfg_context* ctx, const char* path, uint32_t flags, sfg_tensor** out);
 
+/* USPT binary container (io.hpp:202-334): write_container of the tensor's
+ * materialized levels (byte-identical to the reference's for the same
+ * tensor) and read_container into a device tensor of the given format
+ * (the container does not name its format; its level kinds must match;
+ * fmt == NULL infers it from them, CSR for the CSR/CSC look-alikes).
+ * SFG_ERR_IO for unreadable / truncated / bad-magic files. */
+int sfg_write_container(sfg_context* ctx, const sfg_tensor* t, const char* path);
+int sfg_read_container(sfg_context* ctx, const char* path, const sfg_format* fmt, sfg_tensor** out);
+
 /* ------------------------------------------------------ row partitioning */
 /* nnz-balanced contiguous row split for P devices: bounds[0..P]
  * with bounds[0] = 0, bounds[P] = rows, boundaries at ptr quantiles. */

@@ -385,6 +385,12 @@ inline CooData read_matrix_market(const std::string& path) {
   return d;
 }
 
+// write_container / read_container (io.hpp:247, 283): the USPT file of a
+// materialized tensor, written from / read into device memory.
+struct MaterializedTensor;
+inline void write_container(const std::string& path, const MaterializedTensor& m);
+inline MaterializedTensor read_container(const std::string& path);
+
 // --------------------------------------------------------- planner.hpp
 struct ConversionOp {
   std::string text;  // print_op form, e.g. "Fill(0)"
@@ -467,6 +473,42 @@ inline MaterializedTensor materialize(const WorkingTensor& t, const StorageSchem
   }
   m.values = b200::download_values(v);
   return m;
+}
+
+inline void write_container(const std::string& path, const MaterializedTensor& m) {
+  if (!m.dev) fail(ErrorKind::InvalidOperation, "the tensor has no device form");
+  b200::check(sfg_write_container(b200::default_context().get(), m.dev->h, path.c_str()));
+}
+
+// The container does not name its format: the level kinds do (CSR is taken
+// for the CSR / CSC look-alikes; pass the encoding to read a CSC).
+inline MaterializedTensor read_container(const std::string& path, const FormatEncoding& enc) {
+  sfg_tensor* h = nullptr;
+  b200::check(sfg_read_container(b200::default_context().get(), path.c_str(), &enc.fmt, &h));
+  WorkingTensor t;
+  t.enc = enc;
+  t.dev = std::make_shared<b200::TensorHandle>(h);
+  sfg_tensor_view v;
+  b200::check(sfg_tensor_view_get(b200::default_context().get(), h, &v));
+  t.shape = TensorShape{{v.rows, v.cols}};
+  return materialize(t, infer_storage(enc));
+}
+
+inline MaterializedTensor read_container(const std::string& path) {
+  sfg_tensor* h = nullptr;
+  b200::check(sfg_read_container(b200::default_context().get(), path.c_str(), nullptr, &h));
+  sfg_tensor_view v;
+  b200::check(sfg_tensor_view_get(b200::default_context().get(), h, &v));
+  sfg_format f{};
+  f.kind = v.kind;
+  f.value_dtype = v.value_dtype;
+  FormatEncoding enc;
+  enc.fmt = f;
+  WorkingTensor t;
+  t.enc = enc;
+  t.dev = std::make_shared<b200::TensorHandle>(h);
+  t.shape = TensorShape{{v.rows, v.cols}};
+  return materialize(t, infer_storage(enc));
 }
 
 // ------------------------------------------------------- decompose.hpp

@@ -265,6 +265,10 @@ class Ref(_Base):
         self._check(self.lib.sfr_convert_from(coo.h, mtext.encode(), text.encode(), C.byref(h)))
         return _Mat(self.lib, h, self.prefix, text, coo.shape)
 
+    def write_container(self, coo, fmt, path, r=0, c=0):
+        """write_container (io.hpp:247) of the materialized `fmt` form."""
+        self._check(self.lib.sfr_write_container(coo.h, _fmt_text(fmt, r, c).encode(), os.fsencode(path)))
+
     def read_mm(self, path, sum_duplicates=False):
         """read_matrix_market + from_coo (io.hpp:50, tensor.hpp:156)."""
         h = C.c_void_p()

@@ -110,6 +110,16 @@ int sfr_read_mm(const char* path, int sum_duplicates, void** out) {
   });
 }
 
+// write_container of the reference's materialized `fmt` form of a COO.
+int sfr_write_container(void* h, const char* fmt, const char* path) {
+  return guard([&] {
+    WorkingTensor t = static_cast<RefCoo*>(h)->t;
+    FormatEncoding dst = resolve_format(fmt);
+    convert_structure(t, resolve_format("COO"), dst);
+    write_container(path, materialize(t, infer_storage(dst)));
+  });
+}
+
 int sfr_coo_shape(void* h, int64_t* m, int64_t* n) {
   const WorkingTensor& t = static_cast<RefCoo*>(h)->t;
   *m = t.shape.extents[0];

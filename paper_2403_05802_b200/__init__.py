@@ -122,6 +122,8 @@ def load():
         "sfg_row_partition": (C.c_int, [vp, vp, i32, C.POINTER(C.c_int64)]),
         "sfg_coo_slice_rows": (C.c_int, [vp, vp, i64, i64, pp]),
         "sfg_read_matrix_market": (C.c_int, [vp, C.c_char_p, u32, pp]),
+        "sfg_write_container": (C.c_int, [vp, vp, C.c_char_p]),
+        "sfg_read_container": (C.c_int, [vp, C.c_char_p, C.POINTER(Format), pp]),
         "sfgx_gen_uniform": (C.c_int, [vp, C.c_uint64, i64, i64, i32, pp]),
         "sfgx_gen_rmat": (C.c_int, [vp, C.c_uint64, i32, i64, pp]),
         "sfgx_gen_hypersparse": (C.c_int, [vp, C.c_uint64, i64, i64, i64, pp]),
@@ -349,6 +351,18 @@ class Context:
         h = C.c_void_p()
         _check(self.lib.sfg_read_matrix_market(self.h, os.fsencode(path),
                                                FLAG_SUM_DUPLICATES if sum_duplicates else 0, C.byref(h)))
+        return Tensor(self, h)
+
+    def write_container(self, t: Tensor, path: str):
+        """write_container (io.hpp:247): the USPT file of t's levels."""
+        _check(self.lib.sfg_write_container(self.h, t.h, os.fsencode(path)))
+
+    def read_container(self, path: str, fmt: str, value_dtype: int = F32) -> Tensor:
+        """read_container (io.hpp:283) into a device tensor of format `fmt`."""
+        f = resolve_format(fmt)
+        f.value_dtype = value_dtype
+        h = C.c_void_p()
+        _check(self.lib.sfg_read_container(self.h, os.fsencode(path), C.byref(f), C.byref(h)))
         return Tensor(self, h)
 
     def slice_rows(self, coo: Tensor, r0: int, r1: int) -> Tensor:

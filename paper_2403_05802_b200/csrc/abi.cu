@@ -483,6 +483,25 @@ int sfg_read_matrix_market(sfg_context* ctx, const char* path, uint32_t flags, s
   });
 }
 
+int sfg_write_container(sfg_context* ctx, const sfg_tensor* t, const char* path) {
+  return guard([&] {
+    require(ctx && t && path, SFG_ERR_INVALID_OPERATION, "null argument");
+    sfg::write_container(ctx, t, path);
+  });
+}
+
+int sfg_read_container(sfg_context* ctx, const char* path, const sfg_format* fmt, sfg_tensor** out) {
+  return guard([&] {
+    require(ctx && path && out, SFG_ERR_INVALID_OPERATION, "null argument");
+    *out = nullptr;
+    if (fmt) {
+      validate_format(*fmt);
+      if (fmt->kind == SFG_HYB) sfg::raise(SFG_ERR_INVALID_OPERATION, "the hybrid pair is two containers");
+    }
+    *out = sfg::read_container(ctx, path, fmt);
+  });
+}
+
 int sfg_coo_slice_rows(sfg_context* ctx, const sfg_tensor* coo, int64_t r0, int64_t r1,
                        sfg_tensor** out) {
   return guard([&] {

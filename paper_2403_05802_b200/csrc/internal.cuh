@@ -143,6 +143,12 @@ inline int stream_grid(const sfg_context* ctx, int64_t work_items, int block, in
 // Validates a caller-sorted COO; returns 1 when it holds explicit zero values.
 int check_coo_canonical(sfg_context* ctx, const int32_t* row, const int32_t* col, const float* val, int64_t m,
                          int64_t n, int64_t nnz);
+// Whole file -> the context's pinned staging by parallel reads (and, with
+// `dev`, a device copy); returns the host bytes (NUL-terminated).
+char* read_file_pinned(sfg_context* ctx, const char* path, int64_t* size, char** dev);
+// USPT container (container.cu, io.hpp:202-334).
+void write_container(sfg_context* ctx, const sfg_tensor* t, const char* path);
+sfg_tensor* read_container(sfg_context* ctx, const char* path, const sfg_format* fmt /* null: infer */);
 // Matrix Market file -> canonical COO (mm_read.cu).
 sfg_tensor* read_matrix_market(sfg_context* ctx, const char* path, bool sum_duplicates);
 sfg_tensor* sort_coo(sfg_context* ctx, int64_t m, int64_t n, int64_t nnz, const int32_t* row,

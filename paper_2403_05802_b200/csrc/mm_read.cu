@@ -390,6 +390,72 @@ HostLine host_parse(const std::string& line, int64_t rows, int64_t cols, bool pa
 
 }  // namespace
 
+// File -> the context's pinned staging (grow-only) by parallel preads; with
+// `dev`, each chunk is also queued for a device copy as soon as it is read.
+char* read_file_pinned(sfg_context* ctx, const char* path_c, int64_t* size_out, char** dev) {
+  const std::string path(path_c);
+  const int fd = ::open(path_c, O_RDONLY);
+  if (fd < 0) raise(SFG_ERR_IO, "cannot open " + path);
+  struct stat stt;
+  if (::fstat(fd, &stt) != 0) {
+    ::close(fd);
+    raise(SFG_ERR_IO, "cannot open " + path);
+  }
+  const int64_t size = stt.st_size;
+  if ((size_t)size + 1 > ctx->staging_bytes) {
+    cudaStreamSynchronize(ctx->stream);  // earlier copies may still read it
+    if (ctx->staging) cudaFreeHost(ctx->staging);
+    ctx->staging = nullptr;
+    ctx->staging_bytes = 0;
+    const size_t want = (size_t)size + 1 + ((size_t)size >> 3);
+    if (cudaMallocHost(&ctx->staging, want) != cudaSuccess) {
+      cudaGetLastError();
+      ::close(fd);
+      raise(SFG_ERR_OOM, "pinned staging of " + std::to_string(want) + " bytes failed");
+    }
+    ctx->staging_bytes = want;
+  } else {
+    cudaStreamSynchronize(ctx->stream);  // the staging is about to be overwritten
+  }
+  char* host = ctx->staging;
+  char* dcopy = (dev && size) ? static_cast<char*>(dalloc(ctx, size)) : nullptr;
+  constexpr int64_t kChunk = 32 << 20;
+  const int64_t nchunks = (size + kChunk - 1) / kChunk;
+  const int nthreads = (int)std::min<int64_t>(nchunks, 8);
+  std::atomic<int64_t> next{0};
+  std::atomic<bool> bad{false};
+  std::vector<std::thread> pool;
+  for (int w = 0; w < nthreads; ++w)
+    pool.emplace_back([&] {
+      for (int64_t k = next++; k < nchunks; k = next++) {
+        const int64_t off = k * kChunk, len = std::min(kChunk, size - off);
+        int64_t done = 0;
+        while (done < len) {
+          ssize_t got = ::pread(fd, host + off + done, (size_t)(len - done), off + done);
+          if (got <= 0) {
+            bad = true;
+            return;
+          }
+          done += got;
+        }
+        if (dcopy && cudaMemcpyAsync(dcopy + off, host + off, len, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess)
+          bad = true;
+      }
+    });
+  for (auto& th : pool) th.join();
+  ::close(fd);
+  if (bad) {
+    cudaGetLastError();
+    cudaStreamSynchronize(ctx->stream);
+    dfree(ctx, dcopy);
+    raise(SFG_ERR_IO, "cannot read " + path);
+  }
+  host[size] = 0;
+  *size_out = size;
+  if (dev) *dev = dcopy;
+  return host;
+}
+
 sfg_tensor* read_matrix_market(sfg_context* ctx, const char* path_c, bool sum_duplicates) {
   static const bool trace = std::getenv("SFG_TRACE_MM") != nullptr;
   auto t_start = std::chrono::steady_clock::now();
@@ -402,63 +468,9 @@ sfg_tensor* read_matrix_market(sfg_context* ctx, const char* path_c, bool sum_du
     t_start = now;
   };
   const std::string path(path_c);
-  // File -> pinned staging (cached on the context) by parallel preads; each
-  // chunk is queued for the device as soon as it is read.
-  const int fd = ::open(path_c, O_RDONLY);
-  if (fd < 0) raise(SFG_ERR_IO, "cannot open " + path);
-  struct stat stt;
-  if (::fstat(fd, &stt) != 0) {
-    ::close(fd);
-    raise(SFG_ERR_IO, "cannot open " + path);
-  }
-  const int64_t size = stt.st_size;
-  if ((size_t)size + 1 > ctx->staging_bytes) {
-    if (ctx->staging) cudaFreeHost(ctx->staging);
-    ctx->staging = nullptr;
-    ctx->staging_bytes = 0;
-    const size_t want = (size_t)size + 1 + ((size_t)size >> 3);
-    if (cudaMallocHost(&ctx->staging, want) != cudaSuccess) {
-      cudaGetLastError();
-      ::close(fd);
-      raise(SFG_ERR_OOM, "pinned staging of " + std::to_string(want) + " bytes failed");
-    }
-    ctx->staging_bytes = want;
-  }
-  char* host = ctx->staging;
-  char* dtext_all = size ? static_cast<char*>(dalloc(ctx, size)) : nullptr;
-  {
-    constexpr int64_t kChunk = 32 << 20;
-    const int64_t nchunks = (size + kChunk - 1) / kChunk;
-    const int nthreads = (int)std::min<int64_t>(nchunks, 8);
-    std::atomic<int64_t> next{0};
-    std::atomic<bool> bad{false};
-    std::vector<std::thread> pool;
-    for (int w = 0; w < nthreads; ++w)
-      pool.emplace_back([&] {
-        for (int64_t k = next++; k < nchunks; k = next++) {
-          const int64_t off = k * kChunk, len = std::min(kChunk, size - off);
-          int64_t done = 0;
-          while (done < len) {
-            ssize_t got = ::pread(fd, host + off + done, (size_t)(len - done), off + done);
-            if (got <= 0) {
-              bad = true;
-              return;
-            }
-            done += got;
-          }
-          if (cudaMemcpyAsync(dtext_all + off, host + off, len, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess)
-            bad = true;
-        }
-      });
-    for (auto& th : pool) th.join();
-    ::close(fd);
-    if (bad) {
-      cudaGetLastError();
-      cudaStreamSynchronize(ctx->stream);
-      dfree(ctx, dtext_all);
-      raise(SFG_ERR_IO, "cannot read " + path);
-    }
-  }
+  int64_t size = 0;
+  char* dtext_all = nullptr;
+  char* host = read_file_pinned(ctx, path_c, &size, &dtext_all);
   host[size] = 0;
   mark("read file");
 

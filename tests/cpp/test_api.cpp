@@ -144,6 +144,15 @@ int main(int argc, char** argv) {
       EXPECT(std::string(e.what()).find(":4: missing value") != std::string::npos);
     }
   }
+  {  // USPT container round trip (io.hpp:247, 283)
+    WorkingTensor a = from_coo(TensorShape{{5, 4}}, {coo_d0, coo_d1}, coo_val);
+    convert_structure(a, resolve_format("COO"), resolve_format("CSR"));
+    MaterializedTensor ma = materialize(a, infer_storage(resolve_format("CSR")));
+    write_container("/tmp/sfg_test_api.uspt", ma);
+    MaterializedTensor mb = read_container("/tmp/sfg_test_api.uspt");
+    EXPECT(mb.levels.size() == 2 && same(mb.levels[1].ptr, ma.levels[1].ptr) &&
+           same(mb.levels[1].idx, ma.levels[1].idx) && same(mb.values, ma.values));
+  }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
 }

@@ -190,6 +190,13 @@ int sfg_read_matrix_market(sfg_context* ctx, const char* path, uint32_t flags, s
 int sfg_write_container(sfg_context* ctx, const sfg_tensor* t, const char* path);
 int sfg_read_container(sfg_context* ctx, const char* path, const sfg_format* fmt, sfg_tensor** out);
 
+/* run_kernel(spgemm_kernel(), {A, B}) (kernel.hpp:53, 424-567): dense
+ * C[M x N2] (fp32, ldc) = A B for two sparse operands in COO / CSR / DCSR /
+ * CSC / BCSR (ELL, hybrid: SFG_ERR_UNSUPPORTED_SOURCE). flags:
+ * SFG_COMPUTE_ACCUMULATE adds into C; SFG_COMPUTE_HOST: c is host memory. */
+int sfg_spgemm(sfg_context* ctx, const sfg_tensor* a, const sfg_tensor* b, float* c, int64_t ldc,
+               uint32_t flags);
+
 /* ------------------------------------------------------ row partitioning */
 /* nnz-balanced contiguous row split for P devices: bounds[0..P]
  * with bounds[0] = 0, bounds[P] = rows, boundaries at ptr quantiles. */

@@ -265,6 +265,13 @@ class Ref(_Base):
         self._check(self.lib.sfr_convert_from(coo.h, mtext.encode(), text.encode(), C.byref(h)))
         return _Mat(self.lib, h, self.prefix, text, coo.shape)
 
+    def spgemm(self, ma, mb):
+        """run_kernel(spgemm_kernel(), {A, B}) -> (dense C f64, plan mode)."""
+        c = np.zeros((ma.shape[0], mb.shape[1]), np.float64)
+        buf = C.create_string_buffer(64)
+        self._check(self.lib.sfr_spgemm(ma.h, mb.h, _pf64(c), buf, C.c_int64(64)))
+        return c, buf.value.decode()
+
     def write_container(self, coo, fmt, path, r=0, c=0):
         """write_container (io.hpp:247) of the materialized `fmt` form."""
         self._check(self.lib.sfr_write_container(coo.h, _fmt_text(fmt, r, c).encode(), os.fsencode(path)))

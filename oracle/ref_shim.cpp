@@ -18,6 +18,7 @@
 //   sfr_plan           -> plan_conversion + plan_lines planner.hpp:95, 22
 //   sfr_read_mm        -> read_matrix_market + from_coo io.hpp:50-121
 //   sfr_convert_from   -> convert_structure from a non-COO structure
+//   sfr_spgemm         -> run_kernel(spgemm_kernel(), {A, B})   kernel.hpp:424
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -214,6 +215,22 @@ int sfr_spmm(void* h, const double* b, int64_t nd, double* c, int threads) {
         spmm_kernel(), {KernelOperand::from_materialized(a->enc, a->m), KernelOperand::from_dense(bd)},
         opt);
     std::memcpy(c, c_out.data.data(), static_cast<size_t>(m * nd) * sizeof(double));
+  });
+}
+
+// run_kernel(spgemm_kernel(), {A, B}) with two sparse operands
+// (kernel.hpp:53, 424-567): dense C[M x N2] (f64).
+int sfr_spgemm(void* ha, void* hb, double* c, char* mode, int64_t mode_len) {
+  return guard([&] {
+    RefMat* a = static_cast<RefMat*>(ha);
+    RefMat* b = static_cast<RefMat*>(hb);
+    IterationPlan plan;
+    DenseTensor c_out = run_kernel(spgemm_kernel(),
+                                   {KernelOperand::from_materialized(a->enc, a->m),
+                                    KernelOperand::from_materialized(b->enc, b->m)},
+                                   KernelOptions{}, &plan);
+    std::memcpy(c, c_out.data.data(), c_out.data.size() * sizeof(double));
+    if (mode) copy_text(plan.gemm_mode, mode, mode_len);
   });
 }
 

@@ -123,6 +123,7 @@ def load():
         "sfg_coo_slice_rows": (C.c_int, [vp, vp, i64, i64, pp]),
         "sfg_read_matrix_market": (C.c_int, [vp, C.c_char_p, u32, pp]),
         "sfg_write_container": (C.c_int, [vp, vp, C.c_char_p]),
+        "sfg_spgemm": (C.c_int, [vp, vp, vp, vp, i64, u32]),
         "sfg_read_container": (C.c_int, [vp, C.c_char_p, C.POINTER(Format), pp]),
         "sfgx_gen_uniform": (C.c_int, [vp, C.c_uint64, i64, i64, i32, pp]),
         "sfgx_gen_rmat": (C.c_int, [vp, C.c_uint64, i32, i64, pp]),
@@ -352,6 +353,18 @@ class Context:
         _check(self.lib.sfg_read_matrix_market(self.h, os.fsencode(path),
                                                FLAG_SUM_DUPLICATES if sum_duplicates else 0, C.byref(h)))
         return Tensor(self, h)
+
+    def spgemm(self, a: Tensor, b: Tensor) -> np.ndarray:
+        """Dense C = A B over two sparse operands (run_kernel(spgemm_kernel(),
+        {A, B}), kernel.hpp:424); host result."""
+        m, n = a.shape[0], b.shape[1]
+        c = np.zeros((m, n), np.float32)
+        _check(self.lib.sfg_spgemm(self.h, a.h, b.h, c.ctypes.data_as(C.c_void_p), n, COMPUTE_HOST))
+        return c
+
+    def spgemm_device(self, a: Tensor, b: Tensor, c_ptr: int, ldc=None, accumulate=False):
+        _check(self.lib.sfg_spgemm(self.h, a.h, b.h, C.c_void_p(c_ptr), ldc or b.shape[1],
+                                   COMPUTE_ACCUMULATE if accumulate else 0))
 
     def write_container(self, t: Tensor, path: str):
         """write_container (io.hpp:247): the USPT file of t's levels."""

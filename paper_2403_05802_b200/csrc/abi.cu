@@ -483,6 +483,30 @@ int sfg_read_matrix_market(sfg_context* ctx, const char* path, uint32_t flags, s
   });
 }
 
+int sfg_spgemm(sfg_context* ctx, const sfg_tensor* a, const sfg_tensor* b, float* c, int64_t ldc,
+               uint32_t flags) {
+  return guard([&] {
+    require(ctx && a && b && c, SFG_ERR_INVALID_OPERATION, "null argument");
+    require(ldc >= b->n, SFG_ERR_INVALID_OPERATION, "ldc < columns of B");
+    const bool acc = (flags & SFG_COMPUTE_ACCUMULATE) != 0;
+    if (flags & SFG_COMPUTE_HOST) {
+      float* dc = sfg::dalloc_n<float>(ctx, a->m * ldc);
+      try {
+        if (acc) SFG_CUDA(cudaMemcpyAsync(dc, c, a->m * ldc * 4, cudaMemcpyHostToDevice, ctx->stream));
+        sfg::spgemm(ctx, a, b, dc, ldc, acc);
+        SFG_CUDA(cudaMemcpyAsync(c, dc, a->m * ldc * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        SFG_CUDA(cudaStreamSynchronize(ctx->stream));
+      } catch (...) {
+        sfg::dfree(ctx, dc);
+        throw;
+      }
+      sfg::dfree(ctx, dc);
+    } else {
+      sfg::spgemm(ctx, a, b, c, ldc, acc);
+    }
+  });
+}
+
 int sfg_write_container(sfg_context* ctx, const sfg_tensor* t, const char* path) {
   return guard([&] {
     require(ctx && t && path, SFG_ERR_INVALID_OPERATION, "null argument");

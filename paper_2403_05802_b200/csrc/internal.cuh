@@ -149,6 +149,8 @@ char* read_file_pinned(sfg_context* ctx, const char* path, int64_t* size, char**
 // USPT container (container.cu, io.hpp:202-334).
 void write_container(sfg_context* ctx, const sfg_tensor* t, const char* path);
 sfg_tensor* read_container(sfg_context* ctx, const char* path, const sfg_format* fmt /* null: infer */);
+// Dense C = A B over two sparse operands (spgemm.cu).
+void spgemm(sfg_context* ctx, const sfg_tensor* a, const sfg_tensor* b, float* c, int64_t ldc, bool accumulate);
 // Matrix Market file -> canonical COO (mm_read.cu).
 sfg_tensor* read_matrix_market(sfg_context* ctx, const char* path, bool sum_duplicates);
 sfg_tensor* sort_coo(sfg_context* ctx, int64_t m, int64_t n, int64_t nnz, const int32_t* row,

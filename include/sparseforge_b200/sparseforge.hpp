@@ -555,8 +555,9 @@ struct KernelSpec {
 };
 inline KernelSpec spmv_kernel() { return {"spmv"}; }
 inline KernelSpec spmm_kernel() { return {"spmm"}; }
+inline KernelSpec spgemm_kernel() { return {"spgemm"}; }
 inline KernelSpec builtin_kernel(const std::string& name) {
-  if (name == "spmv" || name == "spmm") return {name};
+  if (name == "spmv" || name == "spmm" || name == "spgemm") return {name};
   fail(ErrorKind::InvalidOperation, "unknown kernel: " + name);
 }
 
@@ -596,11 +597,24 @@ inline DenseTensor run_kernel(const KernelSpec& spec, const std::vector<KernelOp
   if (inputs.size() != 2) fail(ErrorKind::InvalidOperation, "operand count does not match the kernel");
   const KernelOperand& a = inputs[0];
   const KernelOperand& d = inputs[1];
+  auto& ctx = b200::default_context();
+  if (a.sparse && d.sparse) {  // two sparse operands (kernel.hpp:424-567): dense C
+    if (spec.name != "spgemm" && spec.name != "spmm")
+      fail(ErrorKind::InvalidOperation, "two sparse operands run the spgemm kernel");
+    if (!a.mat.dev || !d.mat.dev) fail(ErrorKind::InvalidOperation, "materialized tensor has no device arrays");
+    const std::int64_t m = a.mat.logical_shape.extents[0], n2 = d.mat.logical_shape.extents[1];
+    if (a.mat.logical_shape.extents[1] != d.mat.logical_shape.extents[0])
+      fail(ErrorKind::InvalidOperation, "operand shapes disagree on a shared iterator");
+    std::vector<float> c(static_cast<size_t>(m * n2));
+    b200::check(sfg_spgemm(ctx.get(), a.mat.dev->h, d.mat.dev->h, c.data(), n2, SFG_COMPUTE_HOST));
+    DenseTensor out(TensorShape{{m, n2}});
+    std::copy(c.begin(), c.end(), out.data.begin());
+    return out;
+  }
   if (!a.sparse || d.sparse)
     fail(ErrorKind::InvalidOperation, "the B200 path runs one sparse operand times one dense operand");
   if (!a.mat.dev) fail(ErrorKind::InvalidOperation, "materialized tensor has no device arrays");
   const std::int64_t m = a.mat.logical_shape.extents[0], n = a.mat.logical_shape.extents[1];
-  auto& ctx = b200::default_context();
   if (spec.name == "spmv") {
     if (d.dense.shape.rank() != 1 || d.dense.shape.extents[0] != n)
       fail(ErrorKind::InvalidOperation, "operand shapes disagree on a shared iterator");
@@ -620,7 +634,7 @@ inline DenseTensor run_kernel(const KernelSpec& spec, const std::vector<KernelOp
     std::copy(c.begin(), c.end(), out.data.begin());
     return out;
   }
-  fail(ErrorKind::InvalidOperation, "the B200 path runs spmv and spmm");
+  fail(ErrorKind::InvalidOperation, "the B200 path runs spmv, spmm and spgemm");
 }
 
 }  // namespace sparseforge

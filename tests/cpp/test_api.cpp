@@ -153,6 +153,17 @@ int main(int argc, char** argv) {
     EXPECT(mb.levels.size() == 2 && same(mb.levels[1].ptr, ma.levels[1].ptr) &&
            same(mb.levels[1].idx, ma.levels[1].idx) && same(mb.values, ma.values));
   }
+  {  // two sparse operands (kernel.hpp:424): A (5x4) times A^T-shaped B (4x5)
+    WorkingTensor a = from_coo(TensorShape{{5, 4}}, {coo_d0, coo_d1}, coo_val);
+    WorkingTensor b = from_coo(TensorShape{{4, 5}}, {coo_d1, coo_d0}, coo_val);
+    convert_structure(a, resolve_format("COO"), resolve_format("CSR"));
+    MaterializedTensor ma = materialize(a, infer_storage(resolve_format("CSR")));
+    MaterializedTensor mb = materialize(b, infer_storage(resolve_format("COO")));
+    DenseTensor c = run_kernel(spgemm_kernel(), {KernelOperand::from_materialized(ma.enc, ma),
+                                                 KernelOperand::from_materialized(mb.enc, mb)});
+    // (A A^T)[2][2] = 3*3 + 4*4 + 5*5 = 50; [0][0] = 1; [2][4] = 5*6 = 30
+    EXPECT(c.data[2 * 5 + 2] == 50 && c.data[0] == 1 && c.data[2 * 5 + 4] == 30);
+  }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
 }

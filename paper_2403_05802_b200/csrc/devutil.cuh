@@ -255,26 +255,36 @@ __device__ __forceinline__ void row_ptr_from_smem(const int32_t* __restrict__ s,
   const int lane = threadIdx.x & 31;
   const int32_t last = s[kN - 1];
   const int32_t hi = base + kN >= nnz ? m : last;
+  constexpr int kQ = 4;  // independent searches per lane per pass (ILP)
   int32_t q0 = prev + 1;
   while (q0 <= hi) {  // warp-uniform
-    const int32_t q = q0 + lane;
-    int pos = 0;
+    int pos[kQ];
+#pragma unroll
+    for (int j = 0; j < kQ; ++j) pos[j] = 0;
 #pragma unroll
     for (int step = kN / 2; step > 0; step >>= 1)
-      if (s[pos + step - 1] < q) pos += step;
-    if (pos == kN - 1 && s[kN - 1] < q) pos = kN;
-    int64_t v = base + pos;
-    const int32_t pv = (int32_t)(v < nnz ? v : nnz);
-    if (q <= hi) ptr[q] = pv;
-    const int p0 = __shfl_sync(kFull, pos, 0), p31 = __shfl_sync(kFull, pos, 31);
-    if (p0 == p31 && q0 + 31 < hi) {
-      // all 32 rows fall in one run of empty rows ending at row s[p0]:
-      // fill the rest of the run without searching
-      const int32_t end = p0 < kN ? s[p0] : hi;
-      for (int32_t r = q0 + 32 + lane; r <= end; r += 32) ptr[r] = pv;
+#pragma unroll
+      for (int j = 0; j < kQ; ++j)
+        if (s[pos[j] + step - 1] < q0 + 32 * j + lane) pos[j] += step;
+    int32_t pv0 = 0;
+#pragma unroll
+    for (int j = 0; j < kQ; ++j) {
+      const int32_t q = q0 + 32 * j + lane;
+      if (pos[j] == kN - 1 && s[kN - 1] < q) pos[j] = kN;
+      const int64_t v = base + pos[j];
+      const int32_t pv = (int32_t)(v < nnz ? v : nnz);
+      if (j == 0) pv0 = pv;
+      if (q <= hi) ptr[q] = pv;
+    }
+    const int pfirst = __shfl_sync(kFull, pos[0], 0), plast = __shfl_sync(kFull, pos[kQ - 1], 31);
+    if (pfirst == plast && q0 + 32 * kQ - 1 < hi) {
+      // the whole pass falls in one run of empty rows ending at row
+      // s[pfirst]: fill the rest of the run without searching
+      const int32_t end = pfirst < kN ? s[pfirst] : hi;
+      for (int32_t r = q0 + 32 * kQ + lane; r <= end; r += 32) ptr[r] = pv0;
       q0 = end + 1;
     } else {
-      q0 += 32;
+      q0 += 32 * kQ;
     }
   }
 }

@@ -10,6 +10,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "devutil.cuh"
 #include "internal.cuh"
@@ -67,7 +68,23 @@ struct Dense {
   int32_t nd;
   int acc;        // non-atomic row stores add to C (accumulate, or C was zeroed first)
   int keep = 0;   // the caller's accumulate flag (C holds input to add to)
+  int64_t zero_m = 0;  // DCSR, not accumulating: rows of C (the gaps are zeroed in the kernel)
 };
+
+// DCSR without accumulate: the rows of C between stored row p - 1 and
+// stored row p (and, for the last stored row, up to M) hold no entry; the
+// warp that owns row p zeroes its column chunk of them.
+template <int V>
+__device__ __forceinline__ void zero_gap_before(const Dense& d, const int32_t* __restrict__ rows, int64_t p,
+                                                int64_t nrows, int c0) {
+  if (!d.zero_m || !rows) return;
+  const int64_t lo = p == 0 ? 0 : (int64_t)__ldg(rows + p - 1) + 1;
+  const int64_t hi = p < nrows ? (int64_t)__ldg(rows + p) : d.zero_m;
+  for (int64_t r = lo; r < hi; ++r)
+#pragma unroll
+    for (int i = 0; i < V; ++i)
+      if (c0 + i < d.nd) d.c[r * d.ldc + c0 + i] = 0.f;
+}
 
 // Accumulate `val * B[col][cols of this lane]` for the lane's column chunk.
 template <typename TB, int V>
@@ -133,6 +150,8 @@ __global__ void __launch_bounds__(kBlock) k_spmm_rows(const int32_t* __restrict_
     }
     int64_t r = rows ? __ldg(rows + p) : p;
     store_row<V>(d, r, c0, false, acc);
+    zero_gap_before<V>(d, rows, p, nrows, c0);
+    if (p == nrows - 1) zero_gap_before<V>(d, rows, nrows, nrows, c0);
   }
 }
 
@@ -253,23 +272,9 @@ __global__ void __launch_bounds__(kBlock) k_spmm_rows_multi(const int32_t* __res
       if (p0 + i >= nrows) break;
       int64_t r = rows ? __ldg(rows + p0 + i) : p0 + i;
       store_row<V>(d, r, c0, false, acc[i]);
+      zero_gap_before<V>(d, rows, p0 + i, nrows, c0);
+      if (p0 + i == nrows - 1) zero_gap_before<V>(d, rows, nrows, nrows, c0);
     }
-  }
-}
-
-// DCSR: zero the rows that hold no entry (the gaps between consecutive
-// stored rows), instead of clearing all of C before the kernel writes the
-// stored rows. A warp per gap.
-__global__ void __launch_bounds__(kBlock) k_zero_gap_rows(const int32_t* __restrict__ rows, int64_t nnr,
-                                                           int64_t m, int32_t nd, float* __restrict__ c,
-                                                           int64_t ldc) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q <= nnr; q += warps) {
-    int64_t lo = q == 0 ? 0 : (int64_t)__ldg(rows + q - 1) + 1;
-    int64_t hi = q == nnr ? m : (int64_t)__ldg(rows + q);
-    for (int64_t r = lo; r < hi; ++r)
-      for (int j = lane; j < nd; j += 32) c[r * ldc + j] = 0.f;
   }
 }
 
@@ -521,11 +526,14 @@ void spmm(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dtype, int
   }
   if (a->kind == SFG_BCSR && spmm_bcsr_tc(ctx, a, b, b_dtype, nd, ldb, c, ldc, accumulate)) return;
   if (a->kind == SFG_DCSR && !accumulate && a->m > 0) {
-    // stored rows are written whole by the kernel; only the gaps need zeros
-    SFG_LAUNCH(k_zero_gap_rows, (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a->nnr + 1, kBlock / 32),
-                                                                            (int64_t)ctx->sms * 16)),
-               kBlock, 0, ctx->stream, a->row, a->nnr, a->m, (int32_t)nd, c, ldc);
-    Dense d{b, ldb, c, ldc, (int32_t)nd, 0, 0};
+    if (a->nnr == 0) {
+      if (ldc == nd) SFG_CUDA(cudaMemsetAsync(c, 0, a->m * ldc * sizeof(float), ctx->stream));
+      else SFG_CUDA(cudaMemset2DAsync(c, ldc * sizeof(float), 0, nd * sizeof(float), a->m, ctx->stream));
+      return;
+    }
+    // stored rows are written whole by the kernel, which also zeroes the
+    // gaps between them
+    Dense d{b, ldb, c, ldc, (int32_t)nd, 0, 0, a->m};
     if (b_dtype == SFG_BF16) launch_v<__nv_bfloat16>(ctx, a, d);
     else launch_v<float>(ctx, a, d);
     return;

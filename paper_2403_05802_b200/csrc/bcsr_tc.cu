@@ -578,9 +578,9 @@ __global__ void __launch_bounds__(32 * (4 + kProducers + kMmaWarps), 1)
 // (one 16-byte copy per lane per block, written in the 32-byte-swizzled
 // K-major layout). Stage metadata (tile masks) travels in shared memory.
 constexpr int kPanel = 4;
-constexpr int kPanelA = 32;
-constexpr int kPStages = 6;
-constexpr int kPStageBytes = kPanel * kTileBytes + kPanelA * kABytes;  // 32 KB
+constexpr int kPanelA = 16;  // value blocks per stage (a wider block column splits)
+constexpr int kPStages = 8;
+constexpr int kPStageBytes = kPanel * kTileBytes + kPanelA * kABytes;  // 24 KB
 constexpr int kDescWords = 64;  // 0 head, 1-4 tile columns, 5-8 masks, 32-63 slot blocks
 
 struct PShared {
@@ -729,7 +729,7 @@ __global__ void __launch_bounds__(32 * (4 + kProducers + kMmaWarps), 1)
         const int ntile = (int)(head & 0xff), nblk = (int)(head >> 8 & 0xff);
         const uint32_t tbc = __shfl_sync(kFull, c0, 1 + (lane & 3));
         const uint32_t tmask = __shfl_sync(kFull, c0, 5 + (lane & 3));
-        if (lane >= 10 && lane < 18) sts_u32(smem_u32(&sh->slot[stage][4 * (lane - 10)]), c0);
+        if (lane >= 10 && lane < 10 + kPanelA / 4) sts_u32(smem_u32(&sh->slot[stage][4 * (lane - 10)]), c0);
         if (lane < kPanel) {
           sts_u32(smem_u32(&sh->mask[stage][lane]), lane < ntile ? tmask : 0u);
           if (lane < ntile && !(dbg & 2)) {
@@ -884,26 +884,41 @@ __global__ void __launch_bounds__(256) k_bcsr_sched(const int32_t* __restrict__ 
       while (nz) {
         const int src = __ffs(nz) - 1;
         nz &= nz - 1;
-        const uint32_t mask = __shfl_sync(kFull, mine, src);
-        const int cnt = __popc(mask);
-        if (ntile && (ntile == kPanel || nblk + cnt > kPanelA)) close();
-        if (!ntile) {
-          nblk = 0;
-          abeg = apos;
+        uint32_t rest = __shfl_sync(kFull, mine, src);
+        while (rest) {
+          // a block column held by more than kPanelA block rows is split
+          // into several tiles (the B tile is loaded once per tile)
+          uint32_t mask = rest;
+          if (__popc(rest) > kPanelA) {
+            mask = 0;
+            uint32_t t = rest;
+            for (int k = 0; k < kPanelA; ++k) {
+              const uint32_t low = t & (0u - t);
+              mask |= low;
+              t ^= low;
+            }
+          }
+          rest ^= mask;
+          const int cnt = __popc(mask);
+          if (ntile && (ntile == kPanel || nblk + cnt > kPanelA)) close();
+          if (!ntile) {
+            nblk = 0;
+            abeg = apos;
+          }
+          if (lane == ntile) {
+            my_bc = (uint32_t)(bc0 + src);
+            my_mask = mask;
+          }
+          if (kWrite && (mask >> lane & 1u)) {
+            const int sl = nblk + __popc(mask & ((1u << lane) - 1u));
+            sdesc[(int64_t)stage * kDescWords + 32 + sl] = (uint32_t)cur;
+            reinterpret_cast<uint8_t*>(sdesc + (int64_t)stage * kDescWords + 10)[sl] = (uint8_t)(lane | (ntile << 5));
+          }
+          if (mask >> lane & 1u) ++cur;
+          apos += cnt;
+          nblk += cnt;
+          ++ntile;
         }
-        if (lane == ntile) {
-          my_bc = (uint32_t)(bc0 + src);
-          my_mask = mask;
-        }
-        if (kWrite && (mask >> lane & 1u)) {
-          const int sl = nblk + __popc(mask & ((1u << lane) - 1u));
-          sdesc[(int64_t)stage * kDescWords + 32 + sl] = (uint32_t)cur;
-          reinterpret_cast<uint8_t*>(sdesc + (int64_t)stage * kDescWords + 10)[sl] = (uint8_t)(lane | (ntile << 5));
-        }
-        if (mask >> lane & 1u) ++cur;
-        apos += cnt;
-        nblk += cnt;
-        ++ntile;
       }
     }
     if (ntile) close();
@@ -1041,9 +1056,10 @@ bool spmm_bcsr_tc(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dt
                  (int32_t)a->nbc, mut->tc_base, mut->tc_desc);
     }
     if (mut->tc_desc) {
-      // 3 producer and 3 MMA warps measured best (scripts/gpu_run46.sh
-      // sweep: 0.46 ms vs 0.55-0.61 ms for 2 or 6 producers at m = 65536)
-      constexpr int kP = 3, kW = 3;
+      // 4 producer and 4 MMA warps over 8 stages measured best
+      // (scripts/gpu_run78.sh: 0.40 ms at m = 65536; 4/2: 0.43, 8/4: 0.47,
+      // 2/4: 0.61; 3/3 over 6 stages of 32 value blocks: 0.46)
+      constexpr int kP = 4, kW = 4;
       const size_t psmem = 1024 + kPStages * kPStageBytes + sizeof(PShared) + 64;
       static const int dbg = (std::getenv("SFG_TC_PROF") ? 256 : 0) |
                              (std::getenv("SFG_TC_ABLATE") ? std::atoi(std::getenv("SFG_TC_ABLATE")) : 0);

@@ -97,7 +97,7 @@ def bf16_round(a):
 
 
 @pytest.mark.parametrize("shape", [(256, 256), (250, 200), (16, 16), (1000, 3000), (4096, 512)])
-@pytest.mark.parametrize("density", [0.02, 0.3])
+@pytest.mark.parametrize("density", [0.02, 0.3, 0.9])  # 0.9: block columns shared by > 16 block rows
 def test_bcsr16_bf16_tensor_core(ctx, port, shape, density):
     """BCSR(16,16) with bf16 values and bf16 B, nd = 128: the tcgen05 path
     (bcsr_tc.cu). The oracle runs on the bf16-rounded values and B."""

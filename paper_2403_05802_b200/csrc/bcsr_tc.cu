@@ -1057,8 +1057,9 @@ bool spmm_bcsr_tc(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dt
     }
     if (mut->tc_desc) {
       // 4 producer and 4 MMA warps over 8 stages measured best
-      // (scripts/gpu_run78.sh: 0.40 ms at m = 65536; 4/2: 0.43, 8/4: 0.47,
-      // 2/4: 0.61; 3/3 over 6 stages of 32 value blocks: 0.46)
+      // (scripts/gpu_run78.sh: 0.40 ms at m = 65536; 4/8: 0.39, 4/2: 0.43,
+      // 8/4: 0.47, 8/8: 0.47, 2/4: 0.61; 3/3 over 6 stages of 32 value
+      // blocks: 0.46)
       constexpr int kP = 4, kW = 4;
       const size_t psmem = 1024 + kPStages * kPStageBytes + sizeof(PShared) + 64;
       static const int dbg = (std::getenv("SFG_TC_PROF") ? 256 : 0) |

@@ -321,6 +321,10 @@ class Context:
         _check(self.lib.sfg_from_coo(self.h, m, n, len(val), vp(row), vp(col), vp(val), flags, C.byref(h)))
         return Tensor(self, h)
 
+    def copy_device(self, dst_ptr: int, src_ptr: int, nbytes: int):
+        """Device-to-device copy on the context's stream."""
+        _check(self.lib.sfgx_copy(self.h, C.c_void_p(dst_ptr), C.c_void_p(src_ptr), nbytes, 2))
+
     def from_coo_device(self, m, n, nnz, row_ptr, col_ptr, val_ptr, flags=0) -> Tensor:
         h = C.c_void_p()
         _check(self.lib.sfg_from_coo(self.h, m, n, nnz, C.c_void_p(row_ptr), C.c_void_p(col_ptr),

@@ -61,12 +61,9 @@ __device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, uint64
       : "memory");
 }
 
-// 16-byte global -> shared copy (L2 only) and the mbarrier arrive that
-// fires when all of this thread's earlier cp.async copies have landed (the
-// barrier's pending count is raised first, so it waits for them).
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
+// The mbarrier arrive that fires when all of this thread's earlier cp.async
+// copies (async.cuh cp_async16) have landed (the barrier's pending count is
+// raised first, so it waits for them).
 __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }

@@ -9,12 +9,15 @@
 // every digit position; each sort pass then streams tiles of 4096 keys:
 // per-warp match_any ranking (stable: rounds of 32 consecutive keys in
 // input order), per-digit decoupled look-back across tiles for the tile's
-// digit offsets, scatter. Digit positions where every key has the same
+// digit offsets, then the tile is ordered by digit in shared memory and
+// written out run by run (coalesced, unlike a scatter straight from
+// registers, which spreads every warp store over up to 32 digit runs). Digit positions where every key has the same
 // digit are skipped.
 #include <cuda_bf16.h>
 
 #include <vector>
 
+#include "async.cuh"
 #include "devutil.cuh"
 #include "internal.cuh"
 
@@ -45,30 +48,56 @@ __global__ void __launch_bounds__(kBlock) k_global_hist(const uint64_t* __restri
   }
 }
 
+constexpr int kStageBytes = kTile * 8;  // the tile's keys, ordered by digit
+constexpr int kPayInBytes = kTile * 4;  // the tile's payload, input order
+
 template <bool kPayload>
-__global__ void __launch_bounds__(kBlock) k_onesweep(const uint64_t* __restrict__ kin,
+constexpr int onesweep_dyn_smem() {
+  return kStageBytes + (kPayload ? kPayInBytes : 0);
+}
+
+template <bool kPayload>
+__global__ void __launch_bounds__(kBlock, 3) k_onesweep(const uint64_t* __restrict__ kin,
                                                       const uint32_t* __restrict__ pin,
                                                       uint64_t* __restrict__ kout,
                                                       uint32_t* __restrict__ pout, int64_t n,
                                                       int shift, const uint32_t* __restrict__ goff,
                                                       unsigned long long* __restrict__ status,
                                                       uint32_t epoch) {
+  static_assert(kBlock == 256, "one thread per digit");
   __shared__ uint32_t wcnt[kWarps][256];
-  __shared__ uint32_t base_d[256];
+  __shared__ uint32_t dstart[256];  // tile-local start of each digit's run
+  __shared__ uint32_t gshift[256];  // output position - tile-local position
+  __shared__ uint32_t scan_smem[34];
+  extern __shared__ __align__(16) uint8_t dyn[];
+  uint64_t* stage = reinterpret_cast<uint64_t*>(dyn);
+  uint32_t* pay_in = reinterpret_cast<uint32_t*>(dyn + kStageBytes);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tile = blockIdx.x;
+  const int64_t rem = n - (int64_t)tile * kTile;
+  const int tn = rem < kTile ? (int)rem : kTile;
+  if (kPayload) {
+    // the payload goes straight to shared memory, off the register file,
+    // while the keys are ranked
+    const uint32_t* src = pin + (int64_t)tile * kTile;
+    if (tn == kTile) {
+#pragma unroll
+      for (int c = threadIdx.x; c < kTile / 4; c += kBlock) cp_async16(pay_in + 4 * c, src + 4 * c);
+      cp_async_commit();
+    } else {
+      for (int i = threadIdx.x; i < tn; i += kBlock) pay_in[i] = src[i];
+    }
+  }
   for (int i = threadIdx.x; i < kWarps * 256; i += blockDim.x) (&wcnt[0][0])[i] = 0;
   __syncthreads();
 
   const int64_t wbase = (int64_t)tile * kTile + (int64_t)warp * (32 * kRounds);
   uint64_t key[kRounds];
-  uint32_t pay[kRounds];
   uint32_t rank[kRounds];
 #pragma unroll
   for (int j = 0; j < kRounds; ++j) {
     int64_t i = wbase + j * 32 + lane;
     key[j] = i < n ? kin[i] : 0;
-    if (kPayload) pay[j] = i < n ? pin[i] : 0;
   }
   const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
@@ -87,7 +116,8 @@ __global__ void __launch_bounds__(kBlock) k_onesweep(const uint64_t* __restrict_
     __syncwarp();
   }
   __syncthreads();
-  // per digit: exclusive prefix over warps, tile total, look-back
+  // per digit: exclusive prefix over warps, tile total (posted at once so
+  // later tiles can proceed), tile-local digit starts, global look-back
   {
     const int d = threadIdx.x;
     uint32_t s = 0;
@@ -98,12 +128,13 @@ __global__ void __launch_bounds__(kBlock) k_onesweep(const uint64_t* __restrict_
       s += c;
     }
     unsigned long long* st = status + (size_t)tile * 256 + d;
-    uint32_t ep = epoch & 0x3fffffffu;
+    st_relaxed(st, lb_pack(epoch, tile == 0 ? 2 : 1, s));
+    uint32_t tot;
+    const uint32_t ds = block_exclusive_scan<uint32_t, kBlock>(s, scan_smem, &tot);
+    dstart[d] = ds;
+    const uint32_t ep = epoch & 0x3fffffffu;
     uint32_t excl = 0;
-    if (tile == 0) {
-      st_relaxed(st, lb_pack(epoch, 2, s));
-    } else {
-      st_relaxed(st, lb_pack(epoch, 1, s));
+    if (tile > 0) {
       for (int t = tile - 1; t >= 0; --t) {
         unsigned long long w;
         uint32_t state;
@@ -117,17 +148,46 @@ __global__ void __launch_bounds__(kBlock) k_onesweep(const uint64_t* __restrict_
       }
       st_relaxed(st, lb_pack(epoch, 2, excl + s));
     }
-    base_d[d] = goff[d] + excl;
+    gshift[d] = goff[d] + excl - ds;
   }
   __syncthreads();
+  // order the tile by digit in shared memory ...
 #pragma unroll
   for (int j = 0; j < kRounds; ++j) {
     int64_t i = wbase + j * 32 + lane;
     if (i < n) {
       uint32_t d = (uint32_t)((key[j] >> shift) & 0xff);
-      uint32_t o = base_d[d] + wcnt[warp][d] + rank[j];
-      kout[o] = key[j];
-      if (kPayload) pout[o] = pay[j];
+      rank[j] += dstart[d] + wcnt[warp][d];
+      stage[rank[j]] = key[j];
+    }
+  }
+  __syncthreads();
+  // ... then write it out: consecutive threads store consecutive keys of
+  // each digit's run
+  uint32_t o[kRounds];
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r) {
+    const int i = r * kBlock + threadIdx.x;
+    if (i < tn) {
+      const uint64_t k = stage[i];
+      o[r] = gshift[(k >> shift) & 0xff] + i;
+      kout[o[r]] = k;
+    }
+  }
+  if (kPayload) {
+    cp_async_wait_all();
+    __syncthreads();
+    uint32_t* sp = reinterpret_cast<uint32_t*>(stage);
+#pragma unroll
+    for (int j = 0; j < kRounds; ++j) {
+      const int t = warp * (32 * kRounds) + j * 32 + lane;
+      if (t < tn) sp[rank[j]] = pay_in[t];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+      const int i = r * kBlock + threadIdx.x;
+      if (i < tn) pout[o[r]] = sp[i];
     }
   }
 }
@@ -151,6 +211,8 @@ __global__ void k_digit_offsets(uint32_t* __restrict__ hist, int passes) {
 constexpr int kUItems = 16;
 constexpr int kUTile = kBlock * kUItems;
 
+// Warp-striped: element wbase + 32 j + lane; head flags by ballot, so loads
+// and position stores stay coalesced.
 __global__ void __launch_bounds__(kBlock) k_unique_pos(const uint64_t* __restrict__ keys, int64_t n,
                                                         int32_t* __restrict__ pos,
                                                         unsigned long long* __restrict__ status,
@@ -158,34 +220,43 @@ __global__ void __launch_bounds__(kBlock) k_unique_pos(const uint64_t* __restric
                                                         unsigned long long* __restrict__ first_dup) {
   __shared__ uint32_t smem[34];
   __shared__ uint32_t slot;
-  const int64_t e0 = (int64_t)blockIdx.x * kUTile + (int64_t)threadIdx.x * kUItems;
-  uint32_t heads = 0, hm = 0;
-  uint64_t prev = e0 > 0 && e0 < n ? keys[e0 - 1] : ~0ull;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t wbase = (int64_t)blockIdx.x * kUTile + (int64_t)warp * (32 * kUItems);
+  uint64_t k[kUItems];
+#pragma unroll
+  for (int j = 0; j < kUItems; ++j) {
+    const int64_t e = wbase + j * 32 + lane;
+    k[j] = e < n ? keys[e] : 0;
+  }
+  const uint64_t before = lane == 0 && wbase > 0 && wbase < n ? keys[wbase - 1] : 0;
+  unsigned ball[kUItems];
+  uint32_t cnt = 0;
   unsigned long long dup = ~0ull;
 #pragma unroll
-  for (int i = 0; i < kUItems; ++i) {
-    int64_t e = e0 + i;
-    if (e < n) {
-      uint64_t k = keys[e];
-      bool h = e == 0 || k != prev;
-      if (!h && k < dup) dup = k;
-      hm |= (h ? 1u : 0u) << i;
-      heads += h;
-      prev = k;
-    }
+  for (int j = 0; j < kUItems; ++j) {
+    const int64_t e = wbase + j * 32 + lane;
+    uint64_t p = __shfl_up_sync(kFull, k[j], 1);
+    const uint64_t t31 = j > 0 ? __shfl_sync(kFull, k[j - 1], 31) : before;
+    if (lane == 0) p = t31;
+    const bool valid = e < n;
+    const bool h = valid && (e == 0 || k[j] != p);
+    if (valid && !h && k[j] < dup) dup = k[j];
+    ball[j] = __ballot_sync(kFull, h);
+    cnt += __popc(ball[j]);
   }
   if (dup != ~0ull) atomicMin(first_dup, dup);
   uint32_t tot;
-  uint32_t excl = block_exclusive_scan<uint32_t, kBlock>(heads, smem, &tot);
-  uint32_t tp = lookback_prefix(status, epoch, blockIdx.x, tot, &slot);
-  uint32_t p = tp + excl;
+  const uint32_t wex = block_exclusive_scan<uint32_t, kBlock>(lane == 0 ? cnt : 0u, smem, &tot);
+  const uint32_t wpre = __shfl_sync(kFull, wex, 0);
+  const uint32_t tp = lookback_prefix(status, epoch, blockIdx.x, tot, &slot);
+  const unsigned lt = (1u << lane) - 1u;
+  uint32_t run = tp + wpre;
 #pragma unroll
-  for (int i = 0; i < kUItems; ++i) {
-    int64_t e = e0 + i;
-    if (e < n) {
-      p += (hm >> i) & 1u;
-      pos[e] = (int32_t)(p - 1);  // position of this key's unique slot
-    }
+  for (int j = 0; j < kUItems; ++j) {
+    const int64_t e = wbase + j * 32 + lane;
+    // position of this key's unique slot
+    if (e < n) pos[e] = (int32_t)(run + __popc(ball[j] & lt) + ((ball[j] >> lane) & 1u) - 1u);
+    run += __popc(ball[j]);
   }
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *total = (int32_t)(tp + tot);
 }
@@ -274,12 +345,15 @@ void radix_sort(sfg_context* ctx, uint64_t* keys, uint32_t* pay, int64_t n, int 
       bool constant = false;
       for (int d = 0; d < 256; ++d) constant |= (h[p * 256 + d] == (uint32_t)n);
       if (constant) continue;
-      if (pay)
-        SFG_LAUNCH(k_onesweep<true>, tiles, kBlock, 0, ctx->stream, kin, pin, kout, pout, n, 8 * p,
-                   hist + p * 256, status, ctx->epoch++);
-      else
-        SFG_LAUNCH(k_onesweep<false>, tiles, kBlock, 0, ctx->stream, kin, nullptr, kout, nullptr, n,
-                   8 * p, hist + p * 256, status, ctx->epoch++);
+      if (pay) {
+        SFG_CUDA(cudaFuncSetAttribute(k_onesweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      onesweep_dyn_smem<true>()));
+        SFG_LAUNCH(k_onesweep<true>, tiles, kBlock, onesweep_dyn_smem<true>(), ctx->stream, kin, pin, kout,
+                   pout, n, 8 * p, hist + p * 256, status, ctx->epoch++);
+      } else {
+        SFG_LAUNCH(k_onesweep<false>, tiles, kBlock, onesweep_dyn_smem<false>(), ctx->stream, kin, nullptr,
+                   kout, nullptr, n, 8 * p, hist + p * 256, status, ctx->epoch++);
+      }
       std::swap(kin, kout);
       std::swap(pin, pout);
     }

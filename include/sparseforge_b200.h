@@ -134,7 +134,7 @@ enum {
   SFG_FLAG_HOST = 4,            /* pointers are host memory */
 };
 
-/* from_coo (tensor.hpp:156-200): range check -> InvalidOperation; stable
+/* from_coo (tensor.hpp:118-162): range check -> InvalidOperation; stable
  * (row,col) sort (device LSD radix sort); duplicates -> DuplicateCoordinate,
  * or summed in sorted order with SFG_FLAG_SUM_DUPLICATES. Copies the input. */
 int sfg_from_coo(sfg_context* ctx, int64_t rows, int64_t cols, int64_t nnz, const int32_t* row,
@@ -174,7 +174,7 @@ int sfg_spmm(sfg_context* ctx, const sfg_tensor* a, const void* b, int32_t b_dty
              int64_t ldb, float* c, int64_t ldc, uint32_t flags);
 
 /* ---------------------------------------------------------------- ingest */
-/* read_matrix_market (io.hpp:50-121) + from_coo (tensor.hpp:156): a
+/* read_matrix_market (io.hpp:50-121) + from_coo (tensor.hpp:118): a
  * coordinate Matrix Market file (real | integer | pattern, general |
  * symmetric) parsed on the device into a canonical COO. Same header checks
  * (SFG_ERR_UNSUPPORTED_HEADER), the same "path:line: msg" SFG_ERR_PARSE

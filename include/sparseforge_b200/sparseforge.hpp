@@ -3,7 +3,7 @@
 // Mirrors the reference's proj/include/sparseforge API for the hot path
 // (names, argument meaning, ErrorKind errors) so reference-style code such as
 //
-//   WorkingTensor t = from_coo(TensorShape{{m, n}}, coords, values);   // tensor.hpp:156
+//   WorkingTensor t = from_coo(TensorShape{{m, n}}, coords, values);   // tensor.hpp:118
 //   FormatEncoding enc = resolve_format("CSR");                          // formats.hpp:92
 //   convert_structure(t, resolve_format("COO"), enc);                    // planner.hpp:261
 //   MaterializedTensor mat = materialize(t, infer_storage(enc));         // storage.hpp:97
@@ -272,7 +272,7 @@ struct WorkingTensor {
     b200::check(sfg_tensor_view_get(b200::default_context().get(), dev->h, &v));
     return static_cast<size_t>(v.nvals);
   }
-  // Host copy of the canonical COO columns and values (tensor.hpp:108-112).
+  // Host copy of the canonical COO columns and values (tensor.hpp:70-96).
   void download(std::vector<std::vector<std::int64_t>>& coords, std::vector<double>& values) const;
 };
 
@@ -322,7 +322,7 @@ inline void WorkingTensor::download(std::vector<std::vector<std::int64_t>>& coor
   values = b200::download_values(v);
 }
 
-// from_coo (tensor.hpp:156-200): range check, stable sort, duplicates
+// from_coo (tensor.hpp:118-162): range check, stable sort, duplicates
 // rejected (DuplicateCoordinate) or summed (f64, rounded once to fp32).
 inline WorkingTensor from_coo(TensorShape shape, const std::vector<std::vector<std::int64_t>>& coords,
                               const std::vector<double>& values, bool sum_duplicates = false) {
@@ -385,7 +385,7 @@ inline CooData read_matrix_market(const std::string& path) {
   return d;
 }
 
-// write_container / read_container (io.hpp:247, 283): the USPT file of a
+// write_container / read_container (io.hpp:240, 283): the USPT file of a
 // materialized tensor, written from / read into device memory.
 struct MaterializedTensor;
 inline void write_container(const std::string& path, const MaterializedTensor& m);

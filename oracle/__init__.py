@@ -273,11 +273,11 @@ class Ref(_Base):
         return c, buf.value.decode()
 
     def write_container(self, coo, fmt, path, r=0, c=0):
-        """write_container (io.hpp:247) of the materialized `fmt` form."""
+        """write_container (io.hpp:240) of the materialized `fmt` form."""
         self._check(self.lib.sfr_write_container(coo.h, _fmt_text(fmt, r, c).encode(), os.fsencode(path)))
 
     def read_mm(self, path, sum_duplicates=False):
-        """read_matrix_market + from_coo (io.hpp:50, tensor.hpp:156)."""
+        """read_matrix_market + from_coo (io.hpp:50, tensor.hpp:118)."""
         h = C.c_void_p()
         self._check(self.lib.sfr_read_mm(os.fsencode(path), C.c_int(1 if sum_duplicates else 0), C.byref(h)))
         m, n = C.c_int64(), C.c_int64()

@@ -8,7 +8,7 @@
 // reference (sfr_*) and the C restatement (sfo_*).
 //
 // Call chain per entry point (reference file:line):
-//   sfr_from_coo       -> from_coo                    tensor.hpp:156
+//   sfr_from_coo       -> from_coo                    tensor.hpp:118
 //   sfr_convert        -> resolve_format               formats.hpp:92
 //                         convert_structure(COO->dst)  planner.hpp:261
 //                         materialize(infer_storage)   storage.hpp:97, 35
@@ -102,7 +102,7 @@ int sfr_coo_get(void* h, int64_t* row, int64_t* col, double* val) {
 void sfr_coo_free(void* h) { delete static_cast<RefCoo*>(h); }
 
 // Matrix Market file -> canonical COO, exactly as the reference CLI loads a
-// COO operand: read_matrix_market, then from_coo (io.hpp:50, tensor.hpp:156).
+// COO operand: read_matrix_market, then from_coo (io.hpp:50, tensor.hpp:118).
 int sfr_read_mm(const char* path, int sum_duplicates, void** out) {
   *out = nullptr;
   return guard([&] {

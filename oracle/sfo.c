@@ -131,7 +131,7 @@ static void merge_sort(int64_t* p, int64_t* tmp, int64_t n) {
 }
 
 /* Permutation that stably sorts entries lexicographically by (row, col):
- * sort_entries (tensor.hpp:136-152) uses std::stable_sort with a per-level
+ * sort_entries (tensor.hpp:98-114) uses std::stable_sort with a per-level
  * compare; an LSD pair of stable counting sorts gives the same order. */
 static int64_t* stable_order(const int64_t* row, const int64_t* col, int64_t nnz, int64_t m,
                              int64_t n) {
@@ -171,9 +171,9 @@ static void radix_sort_u64(uint64_t* keys, int64_t n) {
 
 /* --------------------------------------------------------------- from_coo */
 
-/* from_coo (tensor.hpp:156-200): range check (171-174, before sorting),
- * stable lexicographic sort (175 -> sort_entries 136-152), then duplicate
- * rejection (185-191) or summation in sorted order (192). */
+/* from_coo (tensor.hpp:118-162): range check (131-135, before sorting),
+ * stable lexicographic sort (137 -> sort_entries 98-114), then duplicate
+ * rejection (147-153) or summation in sorted order (154). */
 int sfo_from_coo(int64_t m, int64_t n, int64_t nnz, const int64_t* row, const int64_t* col,
                  const double* val, int sum_duplicates, sfo_coo** out) {
   *out = NULL;
@@ -288,7 +288,7 @@ static sfo_mat* to_csr(const sfo_coo* s) {
 
 /* CSC: plan Swap(0,1) Sort Fill(0) Merge(0). Swap exchanges the columns
  * and level metadata (operators.hpp:234-241); Sort is the stable
- * sort_entries (tensor.hpp:136) — on row-sorted input a stable counting
+ * sort_entries (tensor.hpp:98) — on row-sorted input a stable counting
  * sort by column. */
 static sfo_mat* to_csc(const sfo_coo* s) {
   sfo_mat* a = mat_alloc(SFO_CSC, s, 2);

@@ -48,7 +48,7 @@ typedef struct sfo_mat sfo_mat;
 
 const char* sfo_last_error(void);
 
-/* from_coo (tensor.hpp:156-200). */
+/* from_coo (tensor.hpp:118-162). */
 int sfo_from_coo(int64_t m, int64_t n, int64_t nnz, const int64_t* row, const int64_t* col,
                  const double* val, int sum_duplicates, sfo_coo** out);
 int64_t sfo_coo_nnz(const sfo_coo* t);

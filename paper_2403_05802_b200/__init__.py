@@ -6,7 +6,7 @@ computes anything itself: when the library (or a B200) is missing it raises.
 
     import paper_2403_05802_b200 as sfg
     ctx = sfg.Context(0)
-    coo = ctx.from_coo(m, n, rows, cols, vals)          # from_coo (tensor.hpp:156)
+    coo = ctx.from_coo(m, n, rows, cols, vals)          # from_coo (tensor.hpp:118)
     csr = ctx.convert(coo, "CSR")                        # convert_structure + materialize
     y   = ctx.spmv(csr, x)                               # run_kernel(spmv_kernel(), ...)
 """
@@ -311,7 +311,7 @@ class Context:
 
     # ---------------------------------------------------------------- ingest
     def from_coo(self, m, n, row, col, val, sorted=False, sum_duplicates=False) -> Tensor:
-        """from_coo (tensor.hpp:156) from host arrays."""
+        """from_coo (tensor.hpp:118) from host arrays."""
         row = np.ascontiguousarray(row, np.int32)
         col = np.ascontiguousarray(col, np.int32)
         val = np.ascontiguousarray(val, np.float32)
@@ -351,7 +351,7 @@ class Context:
         return list(b)
 
     def read_matrix_market(self, path: str, sum_duplicates: bool = False) -> Tensor:
-        """read_matrix_market + from_coo (io.hpp:50, tensor.hpp:156), parsed
+        """read_matrix_market + from_coo (io.hpp:50, tensor.hpp:118), parsed
         on the device."""
         h = C.c_void_p()
         _check(self.lib.sfg_read_matrix_market(self.h, os.fsencode(path),
@@ -371,11 +371,11 @@ class Context:
                                    COMPUTE_ACCUMULATE if accumulate else 0))
 
     def write_container(self, t: Tensor, path: str):
-        """write_container (io.hpp:247): the USPT file of t's levels."""
+        """write_container (io.hpp:240): the USPT file of t's levels."""
         _check(self.lib.sfg_write_container(self.h, t.h, os.fsencode(path)))
 
     def read_container(self, path: str, fmt: str, value_dtype: int = F32) -> Tensor:
-        """read_container (io.hpp:283) into a device tensor of format `fmt`."""
+        """read_container (io.hpp:279) into a device tensor of format `fmt`."""
         f = resolve_format(fmt)
         f.value_dtype = value_dtype
         h = C.c_void_p()

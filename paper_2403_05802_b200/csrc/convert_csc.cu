@@ -2,7 +2,7 @@
 //
 // Reference: plan Swap(0,1) Sort Fill(0) Merge(0) (
 // operators.hpp:234-241 Swap, 298-301 Sort = stable sort_entries,
-// tensor.hpp:136-152). The result is uniquely determined: column pointers
+// tensor.hpp:98-114). The result is uniquely determined: column pointers
 // ptr[n+1], and within each column the rows in ascending order (the input
 // is row-sorted and the sort is stable), materialized like CSR with the
 // roles of rows and columns exchanged (storage.hpp:171-200).

@@ -8,7 +8,7 @@
 //   DCSR = plan Merge(0); L0 is fused (one node per distinct row,
 //          storage.hpp:142-149), L1 ptr[nnr+1] + idx[nnz].
 // The canonical COO handed in is (row, col)-sorted and unique
-// (from_coo, tensor.hpp:156-200), so both are pure streaming passes.
+// (from_coo, tensor.hpp:118-162), so both are pure streaming passes.
 #include <vector>
 
 #include "devutil.cuh"

@@ -1,7 +1,7 @@
 // mm_read.cu — Matrix Market ingest on the device.
 //
 // Reference: read_matrix_market (io.hpp:50-121) followed by from_coo
-// (tensor.hpp:156) — how the reference CLI loads a COO operand. Semantics
+// (tensor.hpp:118) — how the reference CLI loads a COO operand. Semantics
 // kept: banner/object/format/field/symmetry checks (UnsupportedHeader),
 // '%' comment lines (only when '%' is the first character) and blank lines
 // skipped, 1-based indices shifted to 0-based, symmetric inputs mirrored

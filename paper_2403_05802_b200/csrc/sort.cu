@@ -1,9 +1,9 @@
 // sort.cu — from_coo on the device: range check, stable LSD radix sort of
 // packed (row, col) keys, duplicate rejection or f64 summation.
 //
-// Reference: from_coo (tensor.hpp:156-200) = range check (171-174), stable
-// lexicographic sort_entries (136-152, std::stable_sort), duplicates ->
-// DuplicateCoordinate (185-191) or summed in sorted order (192).
+// Reference: from_coo (tensor.hpp:118-162) = range check (131-135), stable
+// lexicographic sort_entries (98-114, std::stable_sort), duplicates ->
+// DuplicateCoordinate (147-153) or summed in sorted order (154).
 //
 // Radix sort: one-sweep LSD with 8-bit digits. An upfront pass histograms
 // every digit position; each sort pass then streams tiles of 4096 keys:
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(kBlock) k_make_keys(const int32_t* __restrict_
 
 // Unique keys -> canonical COO. With sum_duplicates, the head of each run
 // adds the run's values in sorted (= stable input) order in f64, like
-// `out.values.back() += t.values[e]` over doubles (tensor.hpp:192), and
+// `out.values.back() += t.values[e]` over doubles (tensor.hpp:154), and
 // rounds once to fp32.
 __global__ void __launch_bounds__(kBlock) k_emit_coo(const uint64_t* __restrict__ keys,
                                                       const uint32_t* __restrict__ pay,
@@ -305,6 +305,27 @@ __global__ void __launch_bounds__(kBlock) k_emit_coo(const uint64_t* __restrict_
     col[o] = (int32_t)(k & cmask);
     val[o] = (float)s;
   }
+}
+
+// Without sum_duplicates any repeated key is an error, so an accepted
+// input has no duplicates and entry i of the sorted keys is entry i of the
+// result: emit straight through, recording the smallest repeated key.
+__global__ void __launch_bounds__(kBlock) k_emit_distinct(const uint64_t* __restrict__ keys,
+                                                           const uint32_t* __restrict__ pay, int64_t n,
+                                                           int cbits, int32_t* __restrict__ row,
+                                                           int32_t* __restrict__ col, float* __restrict__ val,
+                                                           unsigned long long* __restrict__ first_dup) {
+  const uint64_t cmask = (1ull << cbits) - 1;
+  unsigned long long dup = ~0ull;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = keys[i];
+    if (i > 0 && keys[i - 1] == k && k < dup) dup = k;
+    row[i] = (int32_t)(k >> cbits);
+    col[i] = (int32_t)(k & cmask);
+    val[i] = __uint_as_float(pay[i]);
+  }
+  if (dup != ~0ull) atomicMin(first_dup, dup);
 }
 
 int bits_for(int64_t extent) {
@@ -411,6 +432,37 @@ sfg_tensor* sort_coo(sfg_context* ctx, int64_t m, int64_t n, int64_t nnz, const 
   uint64_t *kres, *kalt;
   uint32_t *pres, *palt;
   radix_sort(ctx, keys, pay, nnz, cbits + rbits, &kres, &pres, &kalt, &palt);
+  auto free_sort = [&] {
+    dfree(ctx, keys);
+    dfree(ctx, pay);
+    dfree(ctx, kalt);
+    dfree(ctx, palt);
+  };
+  auto dup_error = [&](uint64_t k) {
+    delete t;
+    raise(SFG_ERR_DUPLICATE_COORDINATE,
+          "duplicate coordinate (" + std::to_string(k >> cbits) + "," +
+              std::to_string(k & ((1ull << cbits) - 1)) + ")");
+  };
+  if (!sum_duplicates) {
+    t->row = dalloc_n<int32_t>(ctx, nnz);
+    t->idx = dalloc_n<int32_t>(ctx, nnz);
+    t->val = dalloc_n<float>(ctx, nnz);
+    auto* dup = static_cast<unsigned long long*>(scratch(ctx, 64));
+    SFG_CUDA(cudaMemsetAsync(dup, 0xff, 8, ctx->stream));
+    SFG_LAUNCH(k_emit_distinct, stream_grid(ctx, nnz, kBlock, 4), kBlock, 0, ctx->stream, kres, pres, nnz,
+               cbits, t->row, t->idx, static_cast<float*>(t->val), dup);
+    unsigned long long k = 0;
+    read_back(ctx, dup, 8, &k);
+    free_sort();
+    if (k != ~0ull) {
+      free_tensor_arrays(t);
+      dup_error(k);
+    }
+    t->nnz = nnz;
+    t->has_zeros = (f & kZeroValue) ? 1 : 0;
+    return t;
+  }
   int32_t* pos = dalloc_n<int32_t>(ctx, nnz);
   // unique_positions also records the smallest duplicated key
   int tiles = (int)ceil_div(nnz, kUTile);
@@ -422,32 +474,17 @@ sfg_tensor* sort_coo(sfg_context* ctx, int64_t m, int64_t n, int64_t nnz, const 
   unsigned long long res[2];
   read_back(ctx, tail, 16, res);
   int64_t uniq = static_cast<int32_t>(res[1] & 0xffffffffu);
-  if (res[0] != ~0ull && !sum_duplicates) {
-    uint64_t k = res[0];
-    dfree(ctx, keys);
-    dfree(ctx, pay);
-    dfree(ctx, kalt);
-    dfree(ctx, palt);
-    dfree(ctx, pos);
-    delete t;
-    raise(SFG_ERR_DUPLICATE_COORDINATE,
-          "duplicate coordinate (" + std::to_string(k >> cbits) + "," +
-              std::to_string(k & ((1ull << cbits) - 1)) + ")");
-  }
   t->nnz = uniq;
   // summed duplicates may cancel to zero: only a duplicate-free input keeps
   // the zero-free guarantee
-  t->has_zeros = (f & kZeroValue) ? 1 : (sum_duplicates && res[0] != ~0ull ? -1 : 0);
+  t->has_zeros = (f & kZeroValue) ? 1 : (res[0] != ~0ull ? -1 : 0);
   t->row = dalloc_n<int32_t>(ctx, uniq);
   t->idx = dalloc_n<int32_t>(ctx, uniq);
   t->val = dalloc_n<float>(ctx, uniq);
   SFG_LAUNCH(k_emit_coo, stream_grid(ctx, nnz, kBlock, 4), kBlock, 0, ctx->stream, kres, pres, pos,
              nnz, cbits, t->row, t->idx, static_cast<float*>(t->val));
   dfree(ctx, pos);
-  dfree(ctx, keys);
-  dfree(ctx, pay);
-  dfree(ctx, kalt);
-  dfree(ctx, palt);
+  free_sort();
   return t;
 }
 

@@ -103,7 +103,7 @@ int main(int argc, char** argv) {
     EXPECT(r.selected.entry_count() == 3 && r.remainder.entry_count() == 3);
   }
 
-  // errors keep the reference ErrorKind (tensor.hpp:171-191)
+  // errors keep the reference ErrorKind (tensor.hpp:131-153)
   try {
     from_coo(TensorShape{{3, 3}}, {{1, 1}, {2, 2}}, {5.0, 7.0});
     EXPECT(false);
@@ -144,7 +144,7 @@ int main(int argc, char** argv) {
       EXPECT(std::string(e.what()).find(":4: missing value") != std::string::npos);
     }
   }
-  {  // USPT container round trip (io.hpp:247, 283)
+  {  // USPT container round trip (io.hpp:240, 283)
     WorkingTensor a = from_coo(TensorShape{{5, 4}}, {coo_d0, coo_d1}, coo_val);
     convert_structure(a, resolve_format("COO"), resolve_format("CSR"));
     MaterializedTensor ma = materialize(a, infer_storage(resolve_format("CSR")));

@@ -1,6 +1,6 @@
 """Writes the Matrix Market parity fixtures (tests/golden/mm/*.mtx) and
 records what the unmodified reference returns for each — read_matrix_market
-followed by from_coo (io.hpp:50-121, tensor.hpp:156), through the oracle
+followed by from_coo (io.hpp:50-121, tensor.hpp:118), through the oracle
 shim oracle/_ref — into tests/golden/mm/expected.json. Values are stored
 as float.hex (exact f64). Error messages have the file path replaced by
 "{path}". Run here (where /root/reference exists):

@@ -55,12 +55,30 @@ def test_from_coo_errors(ctx):
         assert ei.value.kind == "InvalidOperation"
 
 
+def test_from_coo_names_smallest_duplicate(ctx):
+    # the reference walks the sorted entries and throws at the first repeat
+    # (tensor.hpp:147-153): the smallest duplicated coordinate, wherever the
+    # copies sit in the unsorted input and however many tiles the sort spans
+    rng = np.random.default_rng(5)
+    m = n = 4096
+    keys = rng.choice(m * n, size=200_000, replace=False)
+    r, c = (keys // n).astype(np.int32), (keys % n).astype(np.int32)
+    order = np.argsort(keys)
+    big, small = order[-1], order[1000]
+    r2, c2 = np.append(r, [r[big], r[small]]), np.append(c, [c[big], c[small]])
+    perm = rng.permutation(r2.size)
+    with pytest.raises(sfg.SfgError) as ei:
+        ctx.from_coo(m, n, r2[perm], c2[perm], np.ones(r2.size, np.float32))
+    assert ei.value.kind == "DuplicateCoordinate"
+    assert f"({r[small]},{c[small]})" in str(ei.value)
+
+
 @pytest.mark.parametrize("seed", range(6))
 def test_from_coo_sort_and_sum_duplicates(ctx, port, seed):
     m, n = [(1, 1), (17, 33), (300, 7), (64, 64), (1000, 999), (5, 4)][seed]
     r, c, v = random_coo(seed, m, n, 0.3, dups=(seed * 7) % 23)
     d, p = dev_and_port(ctx, port, m, n, r, c, v, sum_dups=True)
-    # duplicates are summed in f64 like the reference (tensor.hpp:192) and
+    # duplicates are summed in f64 like the reference (tensor.hpp:154) and
     # rounded once to fp32: equal to the oracle's f64 sums narrowed to fp32
     for a, b in zip(d.coo_arrays(), p.arrays()):
         np.testing.assert_array_equal(a, b.astype(a.dtype))

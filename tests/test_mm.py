@@ -1,5 +1,5 @@
 """Matrix Market ingest: read_matrix_market + from_coo
-(io.hpp:50-121, tensor.hpp:156). Fixtures and the reference's answers are in
+(io.hpp:50-121, tensor.hpp:118). Fixtures and the reference's answers are in
 tests/golden/mm (made by tests/golden/make_mm_goldens.py through the
 unmodified reference). CPU: the oracle shim still reproduces them. GPU: the
 device parser returns the same canonical COO (int arrays exact, values the

@@ -155,8 +155,12 @@ void spgemm(sfg_context* ctx, const sfg_tensor* a, const sfg_tensor* b, float* c
 sfg_tensor* read_matrix_market(sfg_context* ctx, const char* path, bool sum_duplicates);
 sfg_tensor* sort_coo(sfg_context* ctx, int64_t m, int64_t n, int64_t nnz, const int32_t* row,
                      const int32_t* col, const float* val, bool sum_duplicates);
+// `hist`: the digit histograms of the keys (8 bits per pass, 256 counts per
+// pass, in the context scratch buffer), when the caller built them while
+// writing the keys; null = computed here.
 void radix_sort(sfg_context* ctx, uint64_t* keys, uint32_t* pay, int64_t n, int key_bits,
-                uint64_t** kres, uint32_t** pres, uint64_t** kalt, uint32_t** palt);
+                uint64_t** kres, uint32_t** pres, uint64_t** kalt, uint32_t** palt,
+                uint32_t* hist = nullptr);
 // ptr[extent+1] + copies of (other, val) from entries sorted by `key`.
 void compress_sorted(sfg_context* ctx, const int32_t* key, const int32_t* other, const float* val,
                      int64_t nnz, int64_t extent, int32_t* ptr, int32_t* oidx, float* oval);

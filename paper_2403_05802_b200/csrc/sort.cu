@@ -135,16 +135,28 @@ __global__ void __launch_bounds__(kBlock, 3) k_onesweep(const uint64_t* __restri
     const uint32_t ep = epoch & 0x3fffffffu;
     uint32_t excl = 0;
     if (tile > 0) {
-      for (int t = tile - 1; t >= 0; --t) {
-        unsigned long long w;
-        uint32_t state;
-        do {
-          w = ld_relaxed(status + (size_t)t * 256 + d);
-          uint32_t hi = (uint32_t)(w >> 32);
-          state = (hi >> 2) == ep ? (hi & 3u) : 0u;
-        } while (state == 0);
-        excl += (uint32_t)w;
-        if (state == 2) break;
+      // kLook predecessors' words in flight at once: a walk over tiles that
+      // have posted only their aggregate costs one L2 round trip per kLook
+      // tiles instead of per tile
+      constexpr int kLook = 4;
+      int t = tile - 1;
+      for (bool done = false; !done;) {
+        unsigned long long w[kLook];
+#pragma unroll
+        for (int q = 0; q < kLook; ++q)
+          w[q] = t - q >= 0 ? ld_relaxed(status + (size_t)(t - q) * 256 + d) : lb_pack(epoch, 2, 0);
+        int q = 0;
+        for (; q < kLook; ++q) {
+          const uint32_t hi = (uint32_t)(w[q] >> 32);
+          const uint32_t state = (hi >> 2) == ep ? (hi & 3u) : 0u;
+          if (state == 0) break;  // not posted yet: poll again from here
+          excl += (uint32_t)w[q];
+          if (state == 2) {
+            done = true;
+            break;
+          }
+        }
+        t -= q;
       }
       st_relaxed(st, lb_pack(epoch, 2, excl + s));
     }
@@ -244,7 +256,13 @@ __global__ void __launch_bounds__(kBlock) k_unique_pos(const uint64_t* __restric
     ball[j] = __ballot_sync(kFull, h);
     cnt += __popc(ball[j]);
   }
-  if (dup != ~0ull) atomicMin(first_dup, dup);
+  // R-MAT draws repeat often: one guarded atomic per warp, not per lane
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long w = __shfl_xor_sync(kFull, dup, o);
+    dup = w < dup ? w : dup;
+  }
+  if (lane == 0 && dup != ~0ull && dup < *(volatile unsigned long long*)first_dup) atomicMin(first_dup, dup);
   uint32_t tot;
   const uint32_t wex = block_exclusive_scan<uint32_t, kBlock>(lane == 0 ? cnt : 0u, smem, &tot);
   const uint32_t wpre = __shfl_sync(kFull, wex, 0);
@@ -263,24 +281,37 @@ __global__ void __launch_bounds__(kBlock) k_unique_pos(const uint64_t* __restric
 
 enum { kBadRange = 1, kZeroValue = 2 };
 
+// Also the radix sort's digit histograms (as k_global_hist), while the
+// keys are in registers.
 __global__ void __launch_bounds__(kBlock) k_make_keys(const int32_t* __restrict__ row,
                                                        const int32_t* __restrict__ col,
                                                        const float* __restrict__ val, int64_t nnz,
-                                                       int32_t m, int32_t n, int cbits,
+                                                       int32_t m, int32_t n, int cbits, int passes,
                                                        uint64_t* __restrict__ keys,
                                                        uint32_t* __restrict__ pay,
+                                                       uint32_t* __restrict__ hist,
                                                        int* __restrict__ flags) {
+  __shared__ uint32_t h[kMaxPasses][256];
+  for (int i = threadIdx.x; i < kMaxPasses * 256; i += blockDim.x) (&h[0][0])[i] = 0;
+  __syncthreads();
   int f = 0;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
        e += (int64_t)gridDim.x * blockDim.x) {
     int r = row[e], c = col[e];
     if (r < 0 || r >= m || c < 0 || c >= n) f |= kBadRange;
     if (val[e] == 0.f) f |= kZeroValue;
-    keys[e] = ((uint64_t)(uint32_t)r << cbits) | (uint32_t)c;
+    const uint64_t k = ((uint64_t)(uint32_t)r << cbits) | (uint32_t)c;
+    keys[e] = k;
     pay[e] = __float_as_uint(val[e]);
+    for (int p = 0; p < passes; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 0xff], 1u);
   }
   f = __reduce_or_sync(kFull, f);
   if (f && (threadIdx.x & 31) == 0) atomicOr(flags, f);
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) {
+    uint32_t v = (&h[0][0])[i];
+    if (v) atomicAdd(hist + i, v);
+  }
 }
 
 // Unique keys -> canonical COO. With sum_duplicates, the head of each run
@@ -339,7 +370,7 @@ int bits_for(int64_t extent) {
 // LSD radix sort of (key, payload) by the low `key_bits` bits. The result
 // lands in either the input or the alternate buffer; *kres / *pres say which.
 void radix_sort(sfg_context* ctx, uint64_t* keys, uint32_t* pay, int64_t n, int key_bits,
-                       uint64_t** kres, uint32_t** pres, uint64_t** kalt_out, uint32_t** palt_out) {
+                uint64_t** kres, uint32_t** pres, uint64_t** kalt_out, uint32_t** palt_out, uint32_t* hist) {
   int passes = (key_bits + 7) / 8;
   if (passes > kMaxPasses) passes = kMaxPasses;
   uint64_t* kalt = dalloc_n<uint64_t>(ctx, n);
@@ -354,10 +385,12 @@ void radix_sort(sfg_context* ctx, uint64_t* keys, uint32_t* pay, int64_t n, int 
     int tiles = (int)ceil_div(n, kTile);
     size_t status_bytes = (size_t)tiles * 256 * 8;
     auto* status = lookback_status(ctx, status_bytes / 8);
-    auto* hist = static_cast<uint32_t*>(scratch(ctx, kMaxPasses * 256 * 4 + 256));
-    SFG_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * 256 * 4, ctx->stream));
-    SFG_LAUNCH(k_global_hist, stream_grid(ctx, n, kBlock, 8, 4), kBlock, 0, ctx->stream, keys, n,
-               passes, hist);
+    if (!hist) {
+      hist = static_cast<uint32_t*>(scratch(ctx, kMaxPasses * 256 * 4 + 256));
+      SFG_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * 256 * 4, ctx->stream));
+      SFG_LAUNCH(k_global_hist, stream_grid(ctx, n, kBlock, 8, 4), kBlock, 0, ctx->stream, keys, n,
+                 passes, hist);
+    }
     std::vector<uint32_t> h(passes * 256);
     SFG_CUDA(cudaMemcpyAsync(h.data(), hist, passes * 256 * 4, cudaMemcpyDeviceToHost, ctx->stream));
     SFG_LAUNCH(k_digit_offsets, passes, 32, 0, ctx->stream, hist, passes);
@@ -416,13 +449,15 @@ sfg_tensor* sort_coo(sfg_context* ctx, int64_t m, int64_t n, int64_t nnz, const 
   int cbits = bits_for(n), rbits = bits_for(m);
   uint64_t* keys = dalloc_n<uint64_t>(ctx, nnz);
   uint32_t* pay = dalloc_n<uint32_t>(ctx, nnz);
-  int* flags = static_cast<int*>(dalloc(ctx, 16));
-  SFG_CUDA(cudaMemsetAsync(flags, 0, 4, ctx->stream));
+  const int passes = std::min((cbits + rbits + 7) / 8, kMaxPasses);
+  // scratch: the digit histograms radix_sort takes over, then the flags
+  auto* hist = static_cast<uint32_t*>(scratch(ctx, kMaxPasses * 256 * 4 + 256));
+  int* flags = reinterpret_cast<int*>(hist + kMaxPasses * 256);
+  SFG_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * 256 * 4 + 16, ctx->stream));
   SFG_LAUNCH(k_make_keys, stream_grid(ctx, nnz, kBlock, 4), kBlock, 0, ctx->stream, row, col, val,
-             nnz, (int32_t)m, (int32_t)n, cbits, keys, pay, flags);
+             nnz, (int32_t)m, (int32_t)n, cbits, passes, keys, pay, hist, flags);
   int f = 0;
   read_back(ctx, flags, 4, &f);
-  dfree(ctx, flags);
   if (f & kBadRange) {
     dfree(ctx, keys);
     dfree(ctx, pay);
@@ -431,7 +466,7 @@ sfg_tensor* sort_coo(sfg_context* ctx, int64_t m, int64_t n, int64_t nnz, const 
   }
   uint64_t *kres, *kalt;
   uint32_t *pres, *palt;
-  radix_sort(ctx, keys, pay, nnz, cbits + rbits, &kres, &pres, &kalt, &palt);
+  radix_sort(ctx, keys, pay, nnz, cbits + rbits, &kres, &pres, &kalt, &palt, hist);
   auto free_sort = [&] {
     dfree(ctx, keys);
     dfree(ctx, pay);

@@ -13,6 +13,7 @@
 // row, which restores the stable order. Any longer column switches to the
 // general path: stable LSD radix sort on the column bits with the row
 // carried in the upper key half, then compression of the sorted columns.
+#include "async.cuh"
 #include "devutil.cuh"
 #include "internal.cuh"
 
@@ -73,12 +74,15 @@ __global__ void __launch_bounds__(kBlock) k_csc_scatter(const int32_t* __restric
                                                          int32_t* __restrict__ cursor,
                                                          int32_t* __restrict__ orow,
                                                          float* __restrict__ oval) {
+  // the scattered 4-byte stores fill their lines over the whole pass: keep
+  // those lines (and k_csc_fix's re-read) in L2 ahead of the streamed input
+  const uint64_t once = l2_evict_first(), keep = l2_evict_last();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
        e += (int64_t)gridDim.x * blockDim.x) {
-    int c = ld_stream(col + e);
+    int c = (int)ld_hint(col + e, once);
     int pos = atomicAdd(cursor + c, 1);
-    orow[pos] = ld_stream(row + e);
-    oval[pos] = ld_stream(val + e);
+    st_hint(orow + pos, ld_hint(row + e, once), keep);
+    st_hint(oval + pos, ld_hint(val + e, once), keep);
   }
 }
 

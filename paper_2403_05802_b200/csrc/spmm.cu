@@ -86,6 +86,18 @@ __device__ __forceinline__ void zero_gap_before(const Dense& d, const int32_t* _
       if (c0 + i < d.nd) d.c[r * d.ldc + c0 + i] = 0.f;
 }
 
+// B[col][cols of this lane] for the lane's column chunk.
+template <typename TB, int V>
+__device__ __forceinline__ void load_brow(const Dense& d, int col, int c0, bool vec, float (&v)[V]) {
+  const TB* brow = static_cast<const TB*>(d.b) + (int64_t)col * d.ldb + c0;
+  if (vec) {
+    BRow<TB>::template load<V>(brow, v);
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; ++i) v[i] = c0 + i < d.nd ? (float)brow[i] : 0.f;
+  }
+}
+
 // Accumulate `val * B[col][cols of this lane]` for the lane's column chunk.
 template <typename TB, int V>
 __device__ __forceinline__ void fma_row(const Dense& d, int col, float val, int c0, bool vec,
@@ -165,6 +177,7 @@ __global__ void __launch_bounds__(kBlock) k_spmm_rows(const int32_t* __restrict_
 // neighbouring chunks and are added atomically. C is zeroed beforehand
 // (or holds the accumulate input), so empty rows need no work.
 constexpr int kMergeItems = 1024;
+constexpr int kMergeK = 8;  // B-row gathers in flight per warp
 
 __global__ void k_merge_cuts(const int32_t* __restrict__ ptr, int64_t m, int64_t nnz, int64_t ncuts,
                              int2* __restrict__ cuts) {
@@ -210,19 +223,34 @@ __global__ void __launch_bounds__(kBlock) k_spmm_merge(const int32_t* __restrict
       const int mc = k < j1 ? ld_stream(col + k) : 0;
       const float mv = k < j1 ? ld_stream(val + k) : 0.f;
       const int cnt = min(32, j1 - base);
-      for (int t = 0; t < cnt; ++t) {
-        const int j = base + t;
-        while (j >= row_end) {  // row i ends before entry j: flush it
-          if (any) store_row<V>(dw, i, c0, shared, acc);
+      for (int t0 = 0; t0 < cnt; t0 += kMergeK) {
+        // the B-row gathers of kMergeK entries are issued before any row
+        // flush (whose C stores the compiler cannot move loads across)
+        float v[kMergeK][V];
 #pragma unroll
-          for (int k2 = 0; k2 < V; ++k2) acc[k2] = 0.f;
-          any = false;
-          shared = false;
-          ++i;
-          row_end = __ldg(ptr + i + 1);
+        for (int u = 0; u < kMergeK; ++u) {
+          const int ck = __shfl_sync(kFull, mc, (t0 + u) & 31);
+          if (t0 + u < cnt) load_brow<TB, V>(d, ck, c0, vec_ok, v[u]);
         }
-        fma_row<TB, V>(d, __shfl_sync(kFull, mc, t), __shfl_sync(kFull, mv, t), c0, vec_ok, acc);
-        any = true;
+#pragma unroll
+        for (int u = 0; u < kMergeK; ++u) {
+          const float ak = __shfl_sync(kFull, mv, (t0 + u) & 31);
+          if (t0 + u < cnt) {
+            const int j = base + t0 + u;
+            while (j >= row_end) {  // row i ends before entry j: flush it
+              if (any) store_row<V>(dw, i, c0, shared, acc);
+#pragma unroll
+              for (int k2 = 0; k2 < V; ++k2) acc[k2] = 0.f;
+              any = false;
+              shared = false;
+              ++i;
+              row_end = __ldg(ptr + i + 1);
+            }
+#pragma unroll
+            for (int k2 = 0; k2 < V; ++k2) acc[k2] = fmaf(ak, v[u][k2], acc[k2]);
+            any = true;
+          }
+        }
       }
     }
     // the open row: complete if its end is this chunk's last row end
@@ -230,15 +258,19 @@ __global__ void __launch_bounds__(kBlock) k_spmm_merge(const int32_t* __restrict
   }
 }
 
-// Short rows (a few entries each, e.g. hypersparse DCSR): a warp walks R
-// consecutive rows side by side so R independent B-row gathers are in flight
-// per step; entry (col, val) loads are warp-uniform (broadcast).
-template <typename TB, int V, int R>
-__global__ void __launch_bounds__(kBlock) k_spmm_rows_multi(const int32_t* __restrict__ rows,
+// Short rows (DCSR / CSR, <= 8 entries per row on average): a warp owns R
+// consecutive stored rows, whose entries are one contiguous range. Lanes
+// fetch 32 entries (col, val, local row) at a time, then the warp issues
+// the B-row loads of kK entries back to back before consuming them in
+// order — kK independent 32·V-wide gathers in flight per warp rather than
+// one per row — flushing each row as the local row index moves past it.
+template <typename TB, int V, int R, int kK>
+__global__ void __launch_bounds__(kBlock) k_spmm_rows_batch(const int32_t* __restrict__ rows,
                                                              const int32_t* __restrict__ ptr,
                                                              const int32_t* __restrict__ col,
                                                              const float* __restrict__ val,
                                                              int64_t nrows, Dense d) {
+  static_assert(R < 32 && kK <= 32, "row group and batch fit a warp");
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int chunks = (d.nd + 32 * V - 1) / (32 * V);
@@ -248,33 +280,54 @@ __global__ void __launch_bounds__(kBlock) k_spmm_rows_multi(const int32_t* __res
     const int64_t g = w / chunks;
     const int c0 = (int)(w - g * chunks) * 32 * V + lane * V;
     const int64_t p0 = g * R;
-    int s[R], e[R];
-    int len = 0;
+    const int nr = nrows - p0 < R ? (int)(nrows - p0) : R;
+    const int pv = lane <= nr ? __ldg(ptr + p0 + lane) : 0;
+    const int beg = __shfl_sync(kFull, pv, 0), end = __shfl_sync(kFull, pv, nr);
+    float acc[V];
 #pragma unroll
-    for (int i = 0; i < R; ++i) {
-      bool ok = p0 + i < nrows;
-      s[i] = ok ? __ldg(ptr + p0 + i) : 0;
-      e[i] = ok ? __ldg(ptr + p0 + i + 1) : 0;
-      len = max(len, e[i] - s[i]);
+    for (int i = 0; i < V; ++i) acc[i] = 0.f;
+    int cur = 0;  // local row being accumulated
+    auto flush_to = [&](int upto) {
+      for (; cur < upto; ++cur) {
+        const int64_t p = p0 + cur;
+        store_row<V>(d, rows ? __ldg(rows + p) : p, c0, false, acc);
+        zero_gap_before<V>(d, rows, p, nrows, c0);
+        if (p == nrows - 1) zero_gap_before<V>(d, rows, nrows, nrows, c0);
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] = 0.f;
+      }
+    };
+    for (int base = beg; base < end; base += 32) {
+      const int e = base + lane;
+      const int mc = e < end ? ld_stream(col + e) : 0;
+      const float mv = e < end ? ld_stream(val + e) : 0.f;
+      int mr = 0;
+#pragma unroll
+      for (int i = 1; i < R; ++i) {
+        const int b = __shfl_sync(kFull, pv, i);
+        mr += (i < nr && b <= e) ? 1 : 0;
+      }
+      const int cnt = min(32, end - base);
+      for (int k0 = 0; k0 < cnt; k0 += kK) {
+        float v[kK][V];
+#pragma unroll
+        for (int k = 0; k < kK; ++k) {
+          const int ck = __shfl_sync(kFull, mc, (k0 + k) & 31);
+          if (k0 + k < cnt) load_brow<TB, V>(d, ck, c0, vec_ok, v[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < kK; ++k) {
+          const int rk = __shfl_sync(kFull, mr, (k0 + k) & 31);
+          const float ak = __shfl_sync(kFull, mv, (k0 + k) & 31);
+          if (k0 + k < cnt) {
+            flush_to(rk);
+#pragma unroll
+            for (int i = 0; i < V; ++i) acc[i] = fmaf(ak, v[k][i], acc[i]);
+          }
+        }
+      }
     }
-    float acc[R][V];
-#pragma unroll
-    for (int i = 0; i < R; ++i)
-#pragma unroll
-      for (int v = 0; v < V; ++v) acc[i][v] = 0.f;
-    for (int t = 0; t < len; ++t) {
-#pragma unroll
-      for (int i = 0; i < R; ++i)
-        if (s[i] + t < e[i]) fma_row<TB, V>(d, __ldg(col + s[i] + t), __ldg(val + s[i] + t), c0, vec_ok, acc[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      if (p0 + i >= nrows) break;
-      int64_t r = rows ? __ldg(rows + p0 + i) : p0 + i;
-      store_row<V>(d, r, c0, false, acc[i]);
-      zero_gap_before<V>(d, rows, p0 + i, nrows, c0);
-      if (p0 + i == nrows - 1) zero_gap_before<V>(d, rows, nrows, nrows, c0);
-    }
+    flush_to(nr);
   }
 }
 
@@ -443,7 +496,9 @@ void launch_fmt(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
   const float* fv = static_cast<const float*>(a->val);
   const int64_t stored_rows = a->kind == SFG_DCSR ? a->nnr : a->m;
   const bool short_rows = stored_rows > 0 && a->nnz <= 8 * stored_rows;  // <= 8 entries per row
-  constexpr int kR = 4;
+  // measured on config 3 (3.6 M rows of ~2.3 entries, nd = 64): R = 16,
+  // kK = 4 beat (8, 8) by 16 % and (8, 16) / (16, 16) by 2x (occupancy)
+  constexpr int kBatchRows = 16, kBatchK = 4;
   switch (a->kind) {
     case SFG_CSR:
       if (a->m == 0 || a->nnz == 0) break;
@@ -461,8 +516,8 @@ void launch_fmt(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
       if (stored_rows == 0) break;
       const int32_t* rows = a->kind == SFG_DCSR ? a->row : nullptr;
       if (short_rows)
-        SFG_LAUNCH((k_spmm_rows_multi<TB, V, kR>), grid_for(ceil_div(stored_rows, kR) * chunks), kBlock, 0,
-                   ctx->stream, rows, a->ptr, a->idx, fv, stored_rows, d);
+        SFG_LAUNCH((k_spmm_rows_batch<TB, V, kBatchRows, kBatchK>), grid_for(ceil_div(stored_rows, kBatchRows) * chunks),
+                   kBlock, 0, ctx->stream, rows, a->ptr, a->idx, fv, stored_rows, d);
       else
         SFG_LAUNCH((k_spmm_rows<TB, V>), grid_for(stored_rows * chunks), kBlock, 0, ctx->stream, rows,
                    a->ptr, a->idx, fv, stored_rows, d);

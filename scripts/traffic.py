@@ -8,14 +8,15 @@ import csv
 import json
 import sys
 
+# kernel names as the launch list prints them, template arguments dropped
 FAMILIES = {
     1: {"convert": ["k_coo_to_csr"], "spmv": ["k_spmv_csr"]},
     2: {"convert": ["k_row_ptr", "k_row_scan", "k_split", "k_iota", "k_ell_fill"],
         "spmv": ["k_spmv_ell", "k_spmv_coo"]},
     3: {"convert_dcsr": ["k_coo_to_dcsr"], "convert_csc": ["k_col_hist", "k_count_scan", "k_csc_scatter", "k_csc_fix"],
         "spmm": ["k_spmm_rows"]},
-    4: {"spmm_bcsr_tc": ["k_bcsr_tc"]},
-    5: {"convert": ["k_coo_to_csr"], "spmm": ["k_spmm_rows"]},
+    4: {"spmm_bcsr_tc": ["k_bcsr_tc", "k_bcsr_sched", "k_bcsr_plan"]},
+    5: {"convert": ["k_coo_to_csr"], "spmm": ["k_merge_cuts", "k_spmm_merge"]},
 }
 
 path, cfg = sys.argv[1], int(sys.argv[2])
@@ -40,10 +41,12 @@ out = {"source": path, "config": cfg, "families": {}}
 for fam, kernels in FAMILIES[cfg].items():
     traffic = 0.0
     time_ns = 0.0
-    for k in kernels:
-        if cnt[k]:
-            traffic += (per[k]["dram__bytes_read.sum"] + per[k]["dram__bytes_write.sum"]) / cnt[k]
-            time_ns += per[k]["gpu__time_duration.sum"] / cnt[k]
+    # a family entry names a kernel or a prefix of its instantiations
+    # (k_spmm_rows -> k_spmm_rows_batch, ...)
+    for name in cnt:
+        if any(name == k or name.startswith(k + "_") for k in kernels):
+            traffic += (per[name]["dram__bytes_read.sum"] + per[name]["dram__bytes_write.sum"]) / cnt[name]
+            time_ns += per[name]["gpu__time_duration.sum"] / cnt[name]
     out["families"][fam] = {"dram_bytes_per_launch": int(traffic), "ncu_time_us": round(time_ns / 1e3, 1),
                             "kernels": kernels}
 print(json.dumps(out, indent=1))

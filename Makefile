@@ -22,7 +22,7 @@ build/obj/%.o: $(CSRC)/%.cu $(HDRS)
 
 $(LIB): $(OBJS)
 	@mkdir -p $(dir $(LIB))
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart -ldl
 
 oracle:
 	$(MAKE) -C oracle

@@ -50,6 +50,7 @@ enum sfg_status {
   /* device-side failures (no reference equivalent) */
   SFG_ERR_CUDA = 64,
   SFG_ERR_OOM = 65,
+  SFG_ERR_NCCL = 66,
 };
 
 /* ---------------------------------------------------------------- formats */
@@ -81,6 +82,7 @@ enum { SFG_LEVEL_SIZE = 1, SFG_LEVEL_PTR = 2, SFG_LEVEL_IDX = 4, SFG_LEVEL_DENSE
 
 typedef struct sfg_context sfg_context;
 typedef struct sfg_tensor sfg_tensor;
+typedef struct sfg_comm sfg_comm; /* NCCL communicator of the row-partitioned path */
 
 /* One level of a MaterializedTensor (storage.hpp:77-83); device pointers. */
 typedef struct sfg_level_view {
@@ -204,6 +206,36 @@ int sfg_row_partition(sfg_context* ctx, const sfg_tensor* coo, int32_t parts, in
 /* Rows [r0, r1) of a canonical COO as a new COO with rows rebased to 0. */
 int sfg_coo_slice_rows(sfg_context* ctx, const sfg_tensor* coo, int64_t r0, int64_t r1,
                        sfg_tensor** out);
+
+/* Row-partitioned SpMV / SpMM over P GPUs, one process per GPU (
+ * the §8b `sfg_rowpart_spmm(ctxs[], P, ncclComm_t[], ..., gather_flag)`
+ * entry, one call per rank). Rank r holds its row block of A (above, then
+ * converted to any format) and a replica of x / B; the output buffer holds
+ * P equal chunks of chunk_rows rows (chunk_rows >= every rank's block
+ * rows, e.g. the maximum over ranks). The product goes straight into chunk
+ * r; with SFG_ROWPART_GATHER an in-place NCCL all-gather then completes
+ * every chunk on every rank. Rows of a chunk past its block are padding.
+ * The reference has no multi-device path; its run_kernel threads split a
+ * single host's work (kernel.hpp:365-384).
+ *
+ * Communicators: rank 0 calls sfg_comm_unique_id and hands the bytes to
+ * every rank (any side channel), then each rank calls sfg_comm_create.
+ * NCCL is loaded at run time (the copy already in the process first). */
+#define SFG_COMM_ID_BYTES 128
+#define SFG_ROWPART_GATHER 1u
+int sfg_comm_unique_id(uint8_t id[SFG_COMM_ID_BYTES]);
+int sfg_comm_create(sfg_context* ctx, int32_t nranks, int32_t rank, const uint8_t id[SFG_COMM_ID_BYTES],
+                    sfg_comm** out);
+int sfg_comm_destroy(sfg_comm* comm);
+/* y: P * chunk_rows floats, device. */
+int sfg_rowpart_spmv(sfg_context* ctx, sfg_comm* comm, const sfg_tensor* a_block, const float* x, float* y,
+                     int64_t chunk_rows, uint32_t flags);
+/* c: P * chunk_rows * nd floats (row-major, ldc = nd), device. */
+int sfg_rowpart_spmm(sfg_context* ctx, sfg_comm* comm, const sfg_tensor* a_block, const void* b, int32_t b_dtype,
+                     int64_t nd, int64_t ldb, float* c, int64_t chunk_rows, uint32_t flags);
+/* The all-gather alone: chunk `rank` of buf (chunk_elems floats each) to
+ * every rank, in place. */
+int sfg_allgather_chunks(sfg_context* ctx, sfg_comm* comm, float* buf, int64_t chunk_elems);
 
 /* ------------------------------------------- synthetic inputs (bench/test) */
 /* Extension entry points (no reference equivalent): the seeded generators of

@@ -26,19 +26,20 @@ KIND_NAMES = {v: k for k, v in KINDS.items()}
 F32, BF16 = 0, 1
 FLAG_SORTED, FLAG_SUM_DUPLICATES, FLAG_HOST = 1, 2, 4
 COMPUTE_HOST, COMPUTE_ACCUMULATE = 1, 2
+COMM_ID_BYTES, ROWPART_GATHER = 128, 1
 ERROR_KINDS = ["Parse", "NonAffine", "NonIntegral", "UnsupportedSource", "UnsupportedHeader",
                "DuplicateCoordinate", "Collision", "InvalidOperation", "Singular", "Io"]
 
 
 class SfgError(RuntimeError):
     """Status from the C-ABI: ``kind`` is the reference ErrorKind name
-    (errors.hpp:10-21) or "Cuda" / "OutOfMemory"."""
+    (errors.hpp:10-21) or "Cuda" / "OutOfMemory" / "Nccl"."""
 
     def __init__(self, status, msg):
         if 1 <= status <= 10:
             kind = ERROR_KINDS[status - 1]
         else:
-            kind = {64: "Cuda", 65: "OutOfMemory"}.get(status, f"status{status}")
+            kind = {64: "Cuda", 65: "OutOfMemory", 66: "Nccl"}.get(status, f"status{status}")
         super().__init__(f"{kind}: {msg}")
         self.kind = kind
         self.status = status
@@ -125,6 +126,12 @@ def load():
         "sfg_write_container": (C.c_int, [vp, vp, C.c_char_p]),
         "sfg_spgemm": (C.c_int, [vp, vp, vp, vp, i64, u32]),
         "sfg_read_container": (C.c_int, [vp, C.c_char_p, C.POINTER(Format), pp]),
+        "sfg_comm_unique_id": (C.c_int, [vp]),
+        "sfg_comm_create": (C.c_int, [vp, i32, i32, vp, pp]),
+        "sfg_comm_destroy": (C.c_int, [vp]),
+        "sfg_rowpart_spmv": (C.c_int, [vp, vp, vp, vp, vp, i64, u32]),
+        "sfg_rowpart_spmm": (C.c_int, [vp, vp, vp, vp, i32, i64, i64, vp, i64, u32]),
+        "sfg_allgather_chunks": (C.c_int, [vp, vp, vp, i64]),
         "sfgx_gen_uniform": (C.c_int, [vp, C.c_uint64, i64, i64, i32, pp]),
         "sfgx_gen_rmat": (C.c_int, [vp, C.c_uint64, i32, i64, pp]),
         "sfgx_gen_hypersparse": (C.c_int, [vp, C.c_uint64, i64, i64, i64, pp]),
@@ -146,6 +153,32 @@ def load():
 def _check(st):
     if st != 0:
         raise SfgError(st, _lib.sfg_last_error().decode(errors="replace"))
+
+
+def comm_unique_id() -> bytes:
+    """ncclGetUniqueId through the C-ABI (rank 0 of the row-partitioned path)."""
+    lib = load()
+    buf = C.create_string_buffer(COMM_ID_BYTES)
+    _check(lib.sfg_comm_unique_id(buf))
+    return buf.raw
+
+
+class Comm:
+    """Owns an sfg_comm (NCCL communicator) handle."""
+
+    def __init__(self, h, nranks, rank):
+        self.h, self.nranks, self.rank = h, nranks, rank
+
+    def close(self):
+        if self.h:
+            _lib.sfg_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def resolve_format(text: str) -> Format:
@@ -386,6 +419,31 @@ class Context:
         h = C.c_void_p()
         _check(self.lib.sfg_coo_slice_rows(self.h, coo.h, r0, r1, C.byref(h)))
         return Tensor(self, h)
+
+    # ------------------------------------------- row-partitioned multi-GPU
+    def comm_create(self, nranks: int, rank: int, unique_id: bytes) -> "Comm":
+        """NCCL communicator of the row-partitioned path (sfg_comm_create);
+        `unique_id` from comm_unique_id() on rank 0, shared by any channel."""
+        assert len(unique_id) == COMM_ID_BYTES
+        h = C.c_void_p()
+        buf = C.create_string_buffer(unique_id, COMM_ID_BYTES)
+        _check(self.lib.sfg_comm_create(self.h, nranks, rank, buf, C.byref(h)))
+        return Comm(h, nranks, rank)
+
+    def rowpart_spmv(self, comm: "Comm", a_block: Tensor, x_ptr: int, y_ptr: int, chunk_rows: int,
+                     gather=True):
+        """y chunk `rank` = A_block x, then the in-place all-gather of the
+        P chunks (sfg_rowpart_spmv)."""
+        _check(self.lib.sfg_rowpart_spmv(self.h, comm.h, a_block.h, C.c_void_p(x_ptr), C.c_void_p(y_ptr),
+                                         chunk_rows, ROWPART_GATHER if gather else 0))
+
+    def rowpart_spmm(self, comm: "Comm", a_block: Tensor, b_ptr: int, b_dtype: int, nd: int, c_ptr: int,
+                     chunk_rows: int, ldb=None, gather=True):
+        _check(self.lib.sfg_rowpart_spmm(self.h, comm.h, a_block.h, C.c_void_p(b_ptr), b_dtype, nd, ldb or nd,
+                                         C.c_void_p(c_ptr), chunk_rows, ROWPART_GATHER if gather else 0))
+
+    def allgather_chunks(self, comm: "Comm", buf_ptr: int, chunk_elems: int):
+        _check(self.lib.sfg_allgather_chunks(self.h, comm.h, C.c_void_p(buf_ptr), chunk_elems))
 
     # --------------------------------------------------------------- compute
     def spmv(self, a: Tensor, x: np.ndarray) -> np.ndarray:

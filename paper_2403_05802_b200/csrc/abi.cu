@@ -536,6 +536,54 @@ int sfg_coo_slice_rows(sfg_context* ctx, const sfg_tensor* coo, int64_t r0, int6
   });
 }
 
+int sfg_comm_unique_id(uint8_t id[SFG_COMM_ID_BYTES]) {
+  return guard([&] {
+    require(id, SFG_ERR_INVALID_OPERATION, "null argument");
+    sfg::comm_unique_id(id);
+  });
+}
+
+int sfg_comm_create(sfg_context* ctx, int32_t nranks, int32_t rank, const uint8_t id[SFG_COMM_ID_BYTES],
+                    sfg_comm** out) {
+  return guard([&] {
+    require(ctx && id && out, SFG_ERR_INVALID_OPERATION, "null argument");
+    require(nranks > 0 && rank >= 0 && rank < nranks, SFG_ERR_INVALID_OPERATION, "bad rank");
+    *out = nullptr;
+    *out = sfg::comm_create(ctx, nranks, rank, id);
+  });
+}
+
+int sfg_comm_destroy(sfg_comm* comm) {
+  return guard([&] {
+    if (comm) sfg::comm_destroy(comm);
+  });
+}
+
+int sfg_rowpart_spmv(sfg_context* ctx, sfg_comm* comm, const sfg_tensor* a_block, const float* x, float* y,
+                     int64_t chunk_rows, uint32_t flags) {
+  return guard([&] {
+    require(ctx && comm && a_block && x && y, SFG_ERR_INVALID_OPERATION, "null argument");
+    sfg::rowpart_spmv(ctx, comm, a_block, x, y, chunk_rows, (flags & SFG_ROWPART_GATHER) != 0);
+  });
+}
+
+int sfg_rowpart_spmm(sfg_context* ctx, sfg_comm* comm, const sfg_tensor* a_block, const void* b, int32_t b_dtype,
+                     int64_t nd, int64_t ldb, float* c, int64_t chunk_rows, uint32_t flags) {
+  return guard([&] {
+    require(ctx && comm && a_block && b && c, SFG_ERR_INVALID_OPERATION, "null argument");
+    require(nd > 0 && ldb >= nd, SFG_ERR_INVALID_OPERATION, "bad dense shape");
+    require(b_dtype == SFG_F32 || b_dtype == SFG_BF16, SFG_ERR_INVALID_OPERATION, "bad dtype");
+    sfg::rowpart_spmm(ctx, comm, a_block, b, b_dtype, nd, ldb, c, chunk_rows, (flags & SFG_ROWPART_GATHER) != 0);
+  });
+}
+
+int sfg_allgather_chunks(sfg_context* ctx, sfg_comm* comm, float* buf, int64_t chunk_elems) {
+  return guard([&] {
+    require(ctx && comm && buf && chunk_elems >= 0, SFG_ERR_INVALID_OPERATION, "bad argument");
+    sfg::allgather_chunks(ctx, comm, buf, chunk_elems);
+  });
+}
+
 int sfgx_gen_uniform(sfg_context* ctx, uint64_t seed, int64_t rows, int64_t cols, int32_t per_row,
                      sfg_tensor** out) {
   return guard([&] {

@@ -158,6 +158,16 @@ sfg_tensor* sort_coo(sfg_context* ctx, int64_t m, int64_t n, int64_t nnz, const 
 // `hist`: the digit histograms of the keys (8 bits per pass, 256 counts per
 // pass, in the context scratch buffer), when the caller built them while
 // writing the keys; null = computed here.
+// rowpart.cu (row-partitioned multi-GPU path)
+void comm_unique_id(uint8_t* out);
+sfg_comm* comm_create(sfg_context* ctx, int32_t nranks, int32_t rank, const uint8_t* id);
+void comm_destroy(sfg_comm* c);
+void allgather_chunks(sfg_context* ctx, sfg_comm* c, float* buf, int64_t chunk_elems);
+void rowpart_spmv(sfg_context* ctx, sfg_comm* c, const sfg_tensor* a, const float* x, float* y, int64_t chunk_rows,
+                  bool gather);
+void rowpart_spmm(sfg_context* ctx, sfg_comm* c, const sfg_tensor* a, const void* b, int b_dtype, int64_t nd,
+                  int64_t ldb, float* cbuf, int64_t chunk_rows, bool gather);
+
 void radix_sort(sfg_context* ctx, uint64_t* keys, uint32_t* pay, int64_t n, int key_bits,
                 uint64_t** kres, uint32_t** pres, uint64_t** kalt, uint32_t** palt,
                 uint32_t* hist = nullptr);

@@ -55,7 +55,7 @@ class Workload:
     (name, fn, algorithmic bytes, flops)."""
     unit = "Mnnz/s"
     fmt = ""
-    has_cpu_sample = False
+    has_cpu_sample = True  # bounded reference sample (cpu_baseline)
 
     def __init__(self, sfg, ctx, rank, world):
         self.sfg, self.ctx, self.rank, self.world = sfg, ctx, rank, world
@@ -557,25 +557,75 @@ def reference_sample(config):
 
 
 def cpu_baseline(config, steps=1):
+    """The unmodified reference (oracle/_ref; the C port if it is absent) on
+    a bounded sample of the config's workload, on this host's cores."""
     import oracle
     lib = oracle.Ref() if oracle.ref_available() else oracle.Port()
     kind = "reference" if isinstance(lib, oracle.Ref) else "port"
-    m, n, r, c, v, x, desc = reference_sample(config)
+    port = oracle.Port()
     threads = os.cpu_count() or 1
-    coo = lib.from_coo(m, n, r, c, v)
+    unit, per_step_units = "Mnnz/s", None
+    if config in (1, 2):
+        m, n, r, c, v, x, desc = reference_sample(config)
+        coo = lib.from_coo(m, n, r, c, v)
+
+        def step():
+            if config == 1:
+                a = lib.convert(coo, "CSR")
+                lib.spmv(a, x, threads=threads)
+            else:
+                sel, rem, _ = lib.decompose_rows(coo, 8)
+                e, co = lib.convert(rem, "ELL"), lib.convert(sel, "COO")
+                lib.spmv(e, x, threads=threads) + lib.spmv(co, x, threads=threads)
+        work = len(v)
+    elif config == 3:
+        # the config-3 generator at 1/16 of the extent (B = n x 64 in f64
+        # stays in host memory); per-entry work is the same
+        m = n = 1 << 18
+        r, c, v = port.gen_hypersparse(5, m, n, 2 * m).arrays()
+        b = port.gen_dense(3, n * 64).reshape(n, 64)
+        coo = lib.from_coo(m, n, r, c, v)
+        desc = f"config-3 generator at {m} x {n}, {len(v)} nnz, Nd = 64"
+
+        def step():
+            a = lib.convert(coo, "DCSR")
+            lib.convert(coo, "CSC")
+            lib.spmm(a, b, threads=threads)
+        work = len(v)
+    elif config == 4:
+        m = n = 4096  # SURVEY.md §8d: <= 4096^2 for the CPU reference
+        r, c, v = port.gen_block_sparse(11, m, n, 16, 16, 0.1).arrays()
+        b = port.gen_dense(3, n * 128).reshape(n, 128)
+        a = lib.convert(lib.from_coo(m, n, r, c, v), "BCSR", 16, 16)
+        desc = f"config-4 generator at {m} x {n} (BCSR 16x16, {len(v)} stored values), Nd = 128, SpMM only"
+        unit = "GFLOP/s"
+
+        def step():
+            lib.spmm(a, b, threads=threads)
+        work = 2 * len(v) * 128 / 1e3  # MFLOP -> GFLOP/s below
+    else:
+        # config 5 shape at scale 20 (SURVEY.md §8d: scale <= 22), a row block
+        full = port.gen_rmat(7, 20, 16 << 20)
+        rr, cc, vv = full.arrays()
+        rows = (1 << 18, (1 << 18) + (1 << 16))
+        sel = (rr >= rows[0]) & (rr < rows[1])
+        r, c, v = rr[sel] - rows[0], cc[sel], vv[sel]
+        m, n = rows[1] - rows[0], 1 << 20
+        b = port.gen_dense(3, n * 32).reshape(n, 32)
+        coo = lib.from_coo(m, n, r, c, v)
+        desc = f"rows [{rows[0]}, {rows[1]}) of R-MAT scale 20 (config-5 generator): {m} x {n}, {len(v)} nnz, Nd = 32"
+
+        def step():
+            a = lib.convert(coo, "CSR")
+            lib.spmm(a, b, threads=threads)
+        work = len(v)
     times = []
     for _ in range(steps):
         t0 = time.perf_counter()
-        if config == 1:
-            a = lib.convert(coo, "CSR")
-            lib.spmv(a, x, threads=threads)
-        else:
-            sel, rem, _ = lib.decompose_rows(coo, 8)
-            e, co = lib.convert(rem, "ELL"), lib.convert(sel, "COO")
-            lib.spmv(e, x, threads=threads) + lib.spmv(co, x, threads=threads)
+        step()
         times.append(time.perf_counter() - t0)
     sec = statistics.mean(times)
-    return {"value": round(len(v) / sec / 1e6, 4), "unit": "Mnnz/s", "cores": threads, "kind": kind,
+    return {"value": round(work / sec / 1e6, 4), "unit": unit, "cores": threads, "kind": kind,
             "sample": desc + f"; conversions single-threaded (as in the reference), run_kernel threads={threads}",
             "sec_per_step": round(sec, 3)}
 
@@ -583,19 +633,16 @@ def cpu_baseline(config, steps=1):
 def run_reference(args):
     if int(os.environ.get("RANK", 0)) != 0:
         return
-    if args.config not in (1, 2):
-        print(json.dumps({"impl": "reference", "unavailable": f"config {args.config} has no bounded CPU sample"}))
-        return
     cb = cpu_baseline(args.config, steps=args.steps)
     doc = WORKLOADS[args.config].__doc__.strip()
     print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "Mnnz/s", "n_gpus": 0,
+        "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": cb["unit"], "n_gpus": 0,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(cb["sec_per_step"] * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generators, csrc/synth.h)",
         "config": {"workload": f"config {args.config}: {doc}", "format": WORKLOADS[args.config].fmt},
         "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
-        "e2e": {"value": cb["value"], "unit": "Mnnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "e2e": {"value": cb["value"], "unit": cb["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
 

@@ -77,3 +77,13 @@ def test_context_without_gpu_fails_loudly():
     with pytest.raises(sfg.SfgError) as ei:
         sfg.Context(0)
     assert ei.value.kind == "Cuda"
+
+
+def test_missing_extension_fails_loudly(monkeypatch):
+    # no CPU fallback: without libsfg.so every entry point refuses to run
+    monkeypatch.setattr(sfg, "_lib", None)
+    monkeypatch.setattr(sfg, "LIB_PATH", sfg.LIB_PATH + ".absent")
+    with pytest.raises(ImportError):
+        sfg.load()
+    with pytest.raises(ImportError):
+        sfg.resolve_format("CSR")

@@ -131,9 +131,14 @@ class Cfg1(SpmvWorkload):
 class Cfg2(SpmvWorkload):
     """hybrid ELL+COO conversion (decompose, T=8) + SpMV, R-MAT scale 22 (+log2 N), edge factor 16"""
     fmt = "HYB(8)"
+    threshold = 8  # --threshold: SURVEY.md §8d sweeps T in {4, 8, 16, 32}; 8 is the default line
     has_cpu_sample = True
 
+    def describe(self):
+        return self.__doc__.strip().replace("T=8", f"T={self.threshold}")
+
     def setup(self, torch):
+        self.fmt = f"HYB({self.threshold})"
         self.scale = 22 + (self.world.bit_length() - 1 if self.world > 1 else 0)
         self.coo = self.rows_block(self.ctx.gen_rmat(7, self.scale, 16 << self.scale))
         self.setup_dense(torch)
@@ -142,7 +147,7 @@ class Cfg2(SpmvWorkload):
         ell, cpart = a.parts()
         ev, cv = ell.view(), cpart.view()
         self.info = {"ell_cells": int(ev.nvals), "ell_k": int(ev.level[0].node_count),
-                     "nnz_coo": int(cv.nvals), "nnz_ell": self.nnz - int(cv.nvals), "threshold": 8}
+                     "nnz_coo": int(cv.nvals), "nnz_ell": self.nnz - int(cv.nvals), "threshold": self.threshold}
 
     def convert_bytes(self):
         i = self.info
@@ -574,7 +579,7 @@ def cpu_baseline(config, steps=1):
                 a = lib.convert(coo, "CSR")
                 lib.spmv(a, x, threads=threads)
             else:
-                sel, rem, _ = lib.decompose_rows(coo, 8)
+                sel, rem, _ = lib.decompose_rows(coo, Cfg2.threshold)
                 e, co = lib.convert(rem, "ELL"), lib.convert(sel, "COO")
                 lib.spmv(e, x, threads=threads) + lib.spmv(co, x, threads=threads)
         work = len(v)
@@ -634,13 +639,15 @@ def run_reference(args):
     if int(os.environ.get("RANK", 0)) != 0:
         return
     cb = cpu_baseline(args.config, steps=args.steps)
-    doc = WORKLOADS[args.config].__doc__.strip()
+    wcls = WORKLOADS[args.config]
+    doc = wcls.describe(wcls)
+    fmt = f"HYB({Cfg2.threshold})" if wcls is Cfg2 else wcls.fmt
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": cb["unit"], "n_gpus": 0,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(cb["sec_per_step"] * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generators, csrc/synth.h)",
-        "config": {"workload": f"config {args.config}: {doc}", "format": WORKLOADS[args.config].fmt},
+        "config": {"workload": f"config {args.config}: {doc}", "format": fmt},
         "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": cb["value"], "unit": cb["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -653,11 +660,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2, choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--threshold", type=int, default=8, help="config 2: hybrid split threshold T")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: no clock soak, no e2e, no CPU baseline")
     args = ap.parse_args()
+    Cfg2.threshold = args.threshold
     if args.impl == "reference":
         run_reference(args)
     else:

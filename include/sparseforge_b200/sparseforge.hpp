@@ -20,6 +20,7 @@
 #pragma once
 
 #include <algorithm>
+#include <array>
 #include <cctype>
 #include <cstdint>
 #include <cstring>
@@ -342,7 +343,7 @@ inline WorkingTensor from_coo(TensorShape shape, const std::vector<std::vector<s
     v[e] = static_cast<float>(values[e]);
   }
   sfg_tensor* h = nullptr;
-  std::uint32_t flags = SFG_FLAG_HOST | (sum_duplicates ? SFG_FLAG_SUM_DUPLICATES : 0u);
+  std::uint32_t flags = SFG_FLAG_HOST | (sum_duplicates ? std::uint32_t(SFG_FLAG_SUM_DUPLICATES) : 0u);
   b200::check(sfg_from_coo(b200::default_context().get(), shape.extents[0], shape.extents[1],
                            static_cast<int64_t>(nnz), r.data(), c.data(), v.data(), flags, &h));
   WorkingTensor t;
@@ -367,7 +368,7 @@ struct CooData {
 inline WorkingTensor load_matrix_market(const std::string& path, bool sum_duplicates = false) {
   sfg_tensor* h = nullptr;
   b200::check(sfg_read_matrix_market(b200::default_context().get(), path.c_str(),
-                                     sum_duplicates ? SFG_FLAG_SUM_DUPLICATES : 0u, &h));
+                                     sum_duplicates ? std::uint32_t(SFG_FLAG_SUM_DUPLICATES) : 0u, &h));
   sfg_tensor_view v;
   b200::check(sfg_tensor_view_get(b200::default_context().get(), h, &v));
   WorkingTensor t;
@@ -635,6 +636,79 @@ inline DenseTensor run_kernel(const KernelSpec& spec, const std::vector<KernelOp
     return out;
   }
   fail(ErrorKind::InvalidOperation, "the B200 path runs spmv, spmm and spgemm");
+}
+
+// ------------------------------------------------ row-partitioned multi-GPU
+// No reference equivalent (its only parallelism is run_kernel's host threads,
+// kernel.hpp:365-384): one process per GPU, rank r holding the row block
+// [bounds[r], bounds[r+1]) of A. Communicator: rank 0 calls
+// comm_unique_id() and shares the bytes; every rank constructs a Comm.
+namespace b200 {
+
+inline std::array<std::uint8_t, SFG_COMM_ID_BYTES> comm_unique_id() {
+  std::array<std::uint8_t, SFG_COMM_ID_BYTES> id{};
+  check(sfg_comm_unique_id(id.data()));
+  return id;
+}
+
+class Comm {
+ public:
+  Comm(int nranks, int rank, const std::array<std::uint8_t, SFG_COMM_ID_BYTES>& id) : nranks_(nranks), rank_(rank) {
+    check(sfg_comm_create(default_context().get(), nranks, rank, id.data(), &h_));
+  }
+  ~Comm() {
+    if (h_) sfg_comm_destroy(h_);
+  }
+  Comm(const Comm&) = delete;
+  Comm& operator=(const Comm&) = delete;
+  sfg_comm* get() const { return h_; }
+  int nranks() const { return nranks_; }
+  int rank() const { return rank_; }
+
+ private:
+  sfg_comm* h_ = nullptr;
+  int nranks_, rank_;
+};
+
+}  // namespace b200
+
+// run_kernel over a row-partitioned operand: `inputs[0]` is this rank's row
+// block (chunk_rows >= the largest block), `inputs[1]` the replicated dense
+// operand. Returns the whole product on every rank: P chunks of chunk_rows
+// rows, chunk r holding block r (rows past a block are padding).
+inline DenseTensor run_kernel_rowpart(const KernelSpec& spec, const std::vector<KernelOperand>& inputs,
+                                      b200::Comm& comm, std::int64_t chunk_rows) {
+  if (inputs.size() != 2 || !inputs[0].sparse || inputs[1].sparse || !inputs[0].mat.dev)
+    fail(ErrorKind::InvalidOperation, "row-partitioned run_kernel takes a sparse block and a dense operand");
+  const KernelOperand& a = inputs[0];
+  const KernelOperand& d = inputs[1];
+  auto& ctx = b200::default_context();
+  const std::int64_t n = a.mat.logical_shape.extents[1];
+  if (d.dense.shape.extents[0] != n) fail(ErrorKind::InvalidOperation, "operand shapes disagree on a shared iterator");
+  const std::int64_t nd = spec.name == "spmv" ? 1 : d.dense.shape.extents[1];
+  if (spec.name != "spmv" && (spec.name != "spmm" || d.dense.shape.rank() != 2))
+    fail(ErrorKind::InvalidOperation, "row-partitioned run_kernel runs spmv or spmm");
+  const std::int64_t total = comm.nranks() * chunk_rows * nd;
+  std::vector<float> host(d.dense.data.begin(), d.dense.data.end());
+  void *db = nullptr, *dc = nullptr;
+  b200::check(sfgx_device_alloc(ctx.get(), n * nd * 4, &db));
+  b200::check(sfgx_device_alloc(ctx.get(), total * 4, &dc));
+  std::vector<float> out_f(static_cast<size_t>(total));
+  int st = sfgx_copy(ctx.get(), db, host.data(), n * nd * 4, 0);
+  if (st == SFG_OK)
+    st = spec.name == "spmv"
+             ? sfg_rowpart_spmv(ctx.get(), comm.get(), a.mat.dev->h, static_cast<const float*>(db),
+                                static_cast<float*>(dc), chunk_rows, SFG_ROWPART_GATHER)
+             : sfg_rowpart_spmm(ctx.get(), comm.get(), a.mat.dev->h, db, SFG_F32, nd, nd, static_cast<float*>(dc),
+                                chunk_rows, SFG_ROWPART_GATHER);
+  if (st == SFG_OK) st = sfgx_copy(ctx.get(), out_f.data(), dc, total * 4, 1);
+  sfgx_device_free(ctx.get(), db);
+  sfgx_device_free(ctx.get(), dc);
+  b200::check(st);
+  DenseTensor out(nd == 1 && spec.name == "spmv" ? TensorShape{{comm.nranks() * chunk_rows}}
+                                                 : TensorShape{{comm.nranks() * chunk_rows, nd}});
+  std::copy(out_f.begin(), out_f.end(), out.data.begin());
+  return out;
 }
 
 }  // namespace sparseforge

@@ -44,19 +44,6 @@ void copy_text(const std::string& s, char* buf, int64_t len) {
   buf[n] = 0;
 }
 
-std::string fmt_name(const sfg_format& f) {
-  switch (f.kind) {
-    case SFG_COO: return "COO";
-    case SFG_CSR: return "CSR";
-    case SFG_CSC: return "CSC";
-    case SFG_DCSR: return "DCSR";
-    case SFG_ELL: return "ELL";
-    case SFG_BCSR: return "BCSR(" + std::to_string(f.block_r) + "," + std::to_string(f.block_c) + ")";
-    case SFG_HYB: return "HYB(" + std::to_string(f.threshold) + ")";
-  }
-  return "?";
-}
-
 // plan_conversion output for a COO source (planner.hpp:95-252), as the
 // reference prints it (plan_lines, planner.hpp:22-27).
 std::string plan_for(const sfg_format& dst) {

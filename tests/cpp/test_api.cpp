@@ -164,6 +164,19 @@ int main(int argc, char** argv) {
     // (A A^T)[2][2] = 3*3 + 4*4 + 5*5 = 50; [0][0] = 1; [2][4] = 5*6 = 30
     EXPECT(c.data[2 * 5 + 2] == 50 && c.data[0] == 1 && c.data[2 * 5 + 4] == 30);
   }
+  {  // row-partitioned path, one rank: chunk 0 = the plain product
+    WorkingTensor a = from_coo(TensorShape{{5, 4}}, {coo_d0, coo_d1}, coo_val);
+    convert_structure(a, resolve_format("COO"), resolve_format("CSR"));
+    MaterializedTensor ma = materialize(a, infer_storage(resolve_format("CSR")));
+    DenseTensor x(TensorShape{{4}});
+    for (auto& v : x.data) v = 1.0;
+    b200::Comm comm(1, 0, b200::comm_unique_id());
+    DenseTensor y = run_kernel_rowpart(spmv_kernel(), {KernelOperand::from_materialized(ma.enc, ma),
+                                                       KernelOperand::from_dense(x)}, comm, 7);
+    const std::vector<double> want{1, 2, 12, 0, 6};  // spmv_y (oracle_data.hpp:125)
+    EXPECT(y.data.size() == 7);
+    for (size_t i = 0; i < want.size(); ++i) EXPECT(y.data[i] == want[i]);
+  }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
 }

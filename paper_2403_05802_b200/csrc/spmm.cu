@@ -98,6 +98,18 @@ __device__ __forceinline__ void load_brow(const Dense& d, int col, int c0, bool 
   }
 }
 
+template <int V>
+__device__ __forceinline__ void store_vec(float* p, const float (&v)[V]) {
+  if constexpr (V == 4) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  } else if constexpr (V == 2) {
+    *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; ++i) p[i] = v[i];
+  }
+}
+
 // Accumulate `val * B[col][cols of this lane]` for the lane's column chunk.
 template <typename TB, int V>
 __device__ __forceinline__ void fma_row(const Dense& d, int col, float val, int c0, bool vec,
@@ -264,7 +276,9 @@ __global__ void __launch_bounds__(kBlock) k_spmm_merge(const int32_t* __restrict
 // the B-row loads of kK entries back to back before consuming them in
 // order — kK independent 32·V-wide gathers in flight per warp rather than
 // one per row — flushing each row as the local row index moves past it.
-template <typename TB, int V, int R, int kK>
+// kVec: nd a multiple of 32 V and both leading dimensions multiples of V
+// (vector loads / stores, no column guards) — chosen at launch.
+template <typename TB, int V, int R, int kK, bool kVec>
 __global__ void __launch_bounds__(kBlock) k_spmm_rows_batch(const int32_t* __restrict__ rows,
                                                              const int32_t* __restrict__ ptr,
                                                              const int32_t* __restrict__ col,
@@ -274,7 +288,8 @@ __global__ void __launch_bounds__(kBlock) k_spmm_rows_batch(const int32_t* __res
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int chunks = (d.nd + 32 * V - 1) / (32 * V);
-  const bool vec_ok = (d.nd % (32 * V) == 0) && (d.ldb % V == 0);
+  constexpr bool vec_ok = kVec, vec_c = kVec;
+  const bool gaps = d.zero_m && rows;  // DCSR, not accumulating: zero the rows between stored rows
   const int64_t groups = (nrows + R - 1) / R;
   for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < groups * chunks; w += warps) {
     const int64_t g = w / chunks;
@@ -283,19 +298,29 @@ __global__ void __launch_bounds__(kBlock) k_spmm_rows_batch(const int32_t* __res
     const int nr = nrows - p0 < R ? (int)(nrows - p0) : R;
     const int pv = lane <= nr ? __ldg(ptr + p0 + lane) : 0;
     const int beg = __shfl_sync(kFull, pv, 0), end = __shfl_sync(kFull, pv, nr);
+    // lane i < nr: output row of stored row p0 + i (and the one before it)
+    const int orow = lane < nr ? (rows ? __ldg(rows + p0 + lane) : (int)(p0 + lane)) : 0;
     float acc[V];
 #pragma unroll
     for (int i = 0; i < V; ++i) acc[i] = 0.f;
     int cur = 0;  // local row being accumulated
-    auto flush_to = [&](int upto) {
-      for (; cur < upto; ++cur) {
-        const int64_t p = p0 + cur;
-        store_row<V>(d, rows ? __ldg(rows + p) : p, c0, false, acc);
-        zero_gap_before<V>(d, rows, p, nrows, c0);
-        if (p == nrows - 1) zero_gap_before<V>(d, rows, nrows, nrows, c0);
+    auto store_cur = [&]() {
+      float* crow = d.c + (int64_t)__shfl_sync(kFull, orow, cur) * d.ldc + c0;
+      if (vec_c) {
+        if (d.acc) {
+          float o[V];
+          BRow<float>::template load<V>(crow, o);
 #pragma unroll
-        for (int i = 0; i < V; ++i) acc[i] = 0.f;
+          for (int i = 0; i < V; ++i) acc[i] += o[i];
+        }
+        store_vec<V>(crow, acc);
+      } else {
+#pragma unroll
+        for (int i = 0; i < V; ++i)
+          if (c0 + i < d.nd) crow[i] = d.acc ? crow[i] + acc[i] : acc[i];
       }
+#pragma unroll
+      for (int i = 0; i < V; ++i) acc[i] = 0.f;
     };
     for (int base = beg; base < end; base += 32) {
       const int e = base + lane;
@@ -310,24 +335,50 @@ __global__ void __launch_bounds__(kBlock) k_spmm_rows_batch(const int32_t* __res
       const int cnt = min(32, end - base);
       for (int k0 = 0; k0 < cnt; k0 += kK) {
         float v[kK][V];
+        // past the batch end the lanes hold col 0 (a valid B row): the
+        // loads are unconditional and the dead values are selected away, so
+        // the batch has no per-entry branches besides the row flush
+#pragma unroll
+        for (int k = 0; k < kK; ++k) load_brow<TB, V>(d, __shfl_sync(kFull, mc, (k0 + k) & 31), c0, vec_ok, v[k]);
 #pragma unroll
         for (int k = 0; k < kK; ++k) {
-          const int ck = __shfl_sync(kFull, mc, (k0 + k) & 31);
-          if (k0 + k < cnt) load_brow<TB, V>(d, ck, c0, vec_ok, v[k]);
-        }
-#pragma unroll
-        for (int k = 0; k < kK; ++k) {
+          const bool live = k0 + k < cnt;
           const int rk = __shfl_sync(kFull, mr, (k0 + k) & 31);
           const float ak = __shfl_sync(kFull, mv, (k0 + k) & 31);
-          if (k0 + k < cnt) {
-            flush_to(rk);
+          for (; cur < rk; ++cur) store_cur();  // rk of a dead slot is the last live row
 #pragma unroll
-            for (int i = 0; i < V; ++i) acc[i] = fmaf(ak, v[k][i], acc[i]);
+          for (int i = 0; i < V; ++i) acc[i] = fmaf(ak, live ? v[k][i] : 0.f, acc[i]);
+        }
+      }
+    }
+    for (; cur < nr; ++cur) store_cur();
+    if (gaps) {
+      // rows with no entry before each stored row of the group (and after
+      // the last stored row of the matrix) are zeroed here
+      const int prev = lane == 0 ? (p0 == 0 ? -1 : __ldg(rows + p0 - 1)) : 0;
+      int lo = __shfl_up_sync(kFull, orow, 1);
+      if (lane == 0) lo = prev;
+      const bool last = p0 + nr == nrows;
+      for (int i = 0; i <= nr; ++i) {
+        // gap before stored row i: (row of i - 1, row of i); i == nr: the
+        // tail after the matrix's last stored row, up to M
+        const int64_t a0 = (int64_t)__shfl_sync(kFull, lo, i) + 1;
+        const int64_t a1 = i < nr ? (int64_t)__shfl_sync(kFull, orow, i) : (last ? d.zero_m : a0);
+        for (int64_t r = a0; r < a1; ++r) {
+          float* crow = d.c + r * d.ldc + c0;
+          if (vec_c) {
+            float z[V];
+#pragma unroll
+            for (int q = 0; q < V; ++q) z[q] = 0.f;
+            store_vec<V>(crow, z);
+          } else {
+#pragma unroll
+            for (int q = 0; q < V; ++q)
+              if (c0 + q < d.nd) crow[q] = 0.f;
           }
         }
       }
     }
-    flush_to(nr);
   }
 }
 
@@ -496,9 +547,10 @@ void launch_fmt(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
   const float* fv = static_cast<const float*>(a->val);
   const int64_t stored_rows = a->kind == SFG_DCSR ? a->nnr : a->m;
   const bool short_rows = stored_rows > 0 && a->nnz <= 8 * stored_rows;  // <= 8 entries per row
-  // measured on config 3 (3.6 M rows of ~2.3 entries, nd = 64): R = 16,
-  // kK = 4 beat (8, 8) by 16 % and (8, 16) / (16, 16) by 2x (occupancy)
-  constexpr int kBatchRows = 16, kBatchK = 4;
+  // measured on config 3 (3.6 M rows of ~2.3 entries, nd = 64), SpMM ms:
+  // (R, kK) = (24, 8) 0.70, (31, 8) 0.71, (16, 8) 0.73, (16, 4) 0.79,
+  // (8, 4) 0.83, (16, 16) 0.92
+  constexpr int kBatchRows = 24, kBatchK = 8;
   switch (a->kind) {
     case SFG_CSR:
       if (a->m == 0 || a->nnz == 0) break;
@@ -515,9 +567,14 @@ void launch_fmt(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
     case SFG_DCSR: {
       if (stored_rows == 0) break;
       const int32_t* rows = a->kind == SFG_DCSR ? a->row : nullptr;
-      if (short_rows)
-        SFG_LAUNCH((k_spmm_rows_batch<TB, V, kBatchRows, kBatchK>), grid_for(ceil_div(stored_rows, kBatchRows) * chunks),
-                   kBlock, 0, ctx->stream, rows, a->ptr, a->idx, fv, stored_rows, d);
+      if (short_rows && d.nd % (32 * V) == 0 && d.ldb % V == 0 && d.ldc % V == 0)
+        SFG_LAUNCH((k_spmm_rows_batch<TB, V, kBatchRows, kBatchK, true>),
+                   grid_for(ceil_div(stored_rows, kBatchRows) * chunks), kBlock, 0, ctx->stream, rows, a->ptr,
+                   a->idx, fv, stored_rows, d);
+      else if (short_rows)
+        SFG_LAUNCH((k_spmm_rows_batch<TB, V, kBatchRows, kBatchK, false>),
+                   grid_for(ceil_div(stored_rows, kBatchRows) * chunks), kBlock, 0, ctx->stream, rows, a->ptr,
+                   a->idx, fv, stored_rows, d);
       else
         SFG_LAUNCH((k_spmm_rows<TB, V>), grid_for(stored_rows * chunks), kBlock, 0, ctx->stream, rows,
                    a->ptr, a->idx, fv, stored_rows, d);

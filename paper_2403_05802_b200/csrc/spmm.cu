@@ -270,6 +270,110 @@ __global__ void __launch_bounds__(kBlock) k_spmm_merge(const int32_t* __restrict
   }
 }
 
+// Merge-path CSR for narrow dense operands (nd = 32 / G * V, e.g. 32 with
+// G = 4, V = 4): a B row is only 32 V / G floats, so a warp splits into G
+// lane groups of 32 / G lanes and takes G entries per instruction (vector
+// loads, one entry per group) instead of one. Each group keeps a partial
+// sum of the current row; a row flush reduces the G partials with lane
+// shuffles and group 0 stores. While a step's entries all lie inside the
+// current row (the common case on rows of tens of entries) the step is
+// branch-free: kU entries per group, their B rows loaded back to back.
+template <typename TB, int G, int V, int kU>
+__global__ void __launch_bounds__(kBlock, 4) k_spmm_merge_grp(const int32_t* __restrict__ ptr,
+                                                            const int32_t* __restrict__ col,
+                                                            const float* __restrict__ val,
+                                                            const int2* __restrict__ cuts, int64_t nchunks,
+                                                            Dense d) {
+  constexpr int L = 32 / G;  // lanes per group
+  constexpr int kStep = G * kU;
+  static_assert(G * L == 32 && kStep <= 32, "groups tile the warp");
+  const int lane = threadIdx.x & 31, grp = lane / L, sub = lane % L;
+  const int c0 = sub * V;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < nchunks; q += warps) {
+    const int2 a = __ldg(cuts + q), b = __ldg(cuts + q + 1);
+    int i = a.x;
+    const int j0 = a.y, j1 = b.y;
+    int row_end = __ldg(ptr + i + 1);
+    bool shared = j0 > __ldg(ptr + i);  // row a.x began in an earlier chunk
+    float acc[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) acc[k] = 0.f;
+    bool any = false;
+    auto flush = [&](bool atomic) {  // reduce the groups' partials of row i; group 0 stores
+#pragma unroll
+      for (int o = L; o < 32; o <<= 1)
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc[k] += __shfl_xor_sync(kFull, acc[k], o);
+      if (grp == 0) {
+        float* crow = d.c + (int64_t)i * d.ldc + c0;
+        if (atomic) {
+#pragma unroll
+          for (int k = 0; k < V; ++k) atomicAdd(crow + k, acc[k]);
+        } else {
+          if (d.keep) {
+            float o[V];
+            BRow<float>::template load<V>(crow, o);
+#pragma unroll
+            for (int k = 0; k < V; ++k) acc[k] += o[k];
+          }
+          store_vec<V>(crow, acc);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc[k] = 0.f;
+    };
+    for (int base = j0; base < j1; base += 32) {
+      const int e = base + lane;
+      const int mc = e < j1 ? ld_stream(col + e) : 0;  // past the chunk: col 0, value 0
+      const float mv = e < j1 ? ld_stream(val + e) : 0.f;
+      const int cnt = min(32, j1 - base);
+      for (int t0 = 0; t0 < cnt; t0 += kStep) {
+        const int last = base + min(t0 + kStep, cnt) - 1;
+        if (last < row_end) {
+          // fast path: the whole step is in row i
+          float v[kU][V];
+#pragma unroll
+          for (int u = 0; u < kU; ++u)
+            load_brow<TB, V>(d, __shfl_sync(kFull, mc, (t0 + u * G + grp) & 31), c0, true, v[u]);
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const bool live = t0 + u * G + grp < cnt;  // past cnt: B row 0, selected away
+            const float ak = __shfl_sync(kFull, mv, (t0 + u * G + grp) & 31);
+#pragma unroll
+            for (int k = 0; k < V; ++k) acc[k] = fmaf(ak, live ? v[u][k] : 0.f, acc[k]);
+          }
+          any = true;
+        } else {
+          // a row ends inside the step: entry by entry, group (t % G) adds it
+          const int tn = min(t0 + kStep, cnt);
+          for (int t = t0; t < tn; ++t) {
+            const int j = base + t;
+            while (j >= row_end) {  // row i ends before entry j: flush it
+              if (any) flush(shared);
+              any = false;
+              shared = false;
+              ++i;
+              row_end = __ldg(ptr + i + 1);
+            }
+            const int ck = __shfl_sync(kFull, mc, t);
+            const float ak = __shfl_sync(kFull, mv, t);
+            if (grp == t % G) {
+              float v[V];
+              load_brow<TB, V>(d, ck, c0, true, v);
+#pragma unroll
+              for (int k = 0; k < V; ++k) acc[k] = fmaf(ak, v[k], acc[k]);
+            }
+            any = true;
+          }
+        }
+      }
+    }
+    // the open row: complete if its end is this chunk's last row end
+    if (any) flush(shared || row_end > j1 || i >= b.x);
+  }
+}
+
 // Short rows (DCSR / CSR, <= 8 entries per row on average): a warp owns R
 // consecutive stored rows, whose entries are one contiguous range. Lanes
 // fetch 32 entries (col, val, local row) at a time, then the warp issues
@@ -560,8 +664,18 @@ void launch_fmt(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
         auto* cuts = static_cast<int2*>(scratch(ctx, (nchunks + 1) * sizeof(int2)));
         SFG_LAUNCH(k_merge_cuts, (int)std::min<int64_t>(ceil_div(nchunks + 1, 256), (int64_t)ctx->sms * 8), 256, 0,
                    ctx->stream, a->ptr, a->m, a->nnz, nchunks + 1, cuts);
-        SFG_LAUNCH((k_spmm_merge<TB, V>), grid_for(nchunks * chunks), kBlock, 0, ctx->stream, a->ptr, a->idx, fv,
-                   cuts, nchunks, d);
+        const bool vec4 = d.ldb % 4 == 0 && d.ldc % 4 == 0;
+        // nd = 32 on config 5: kU = 2 28.7 ms, kU = 4 32.5, kU = 1 34.2
+        // (the one-entry-per-warp-step kernel: 43 ms, issue-bound)
+        if (vec4 && d.nd == 32)
+          SFG_LAUNCH((k_spmm_merge_grp<TB, 4, 4, 2>), grid_for(nchunks), kBlock, 0, ctx->stream, a->ptr, a->idx,
+                     fv, cuts, nchunks, d);
+        else if (vec4 && d.nd == 64)
+          SFG_LAUNCH((k_spmm_merge_grp<TB, 2, 4, 4>), grid_for(nchunks), kBlock, 0, ctx->stream, a->ptr, a->idx,
+                     fv, cuts, nchunks, d);
+        else
+          SFG_LAUNCH((k_spmm_merge<TB, V>), grid_for(nchunks * chunks), kBlock, 0, ctx->stream, a->ptr, a->idx, fv,
+                     cuts, nchunks, d);
       }
       break;
     case SFG_DCSR: {

@@ -330,12 +330,14 @@ __global__ void __launch_bounds__(kBlock, 4) k_spmm_merge_grp(const int32_t* __r
       const int cnt = min(32, j1 - base);
       for (int t0 = 0; t0 < cnt; t0 += kStep) {
         const int last = base + min(t0 + kStep, cnt) - 1;
+        // the step's B rows, entry t0 + u G + grp in group grp (past cnt:
+        // B row 0, selected away), all loads in flight at once
+        float v[kU][V];
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+          load_brow<TB, V>(d, __shfl_sync(kFull, mc, (t0 + u * G + grp) & 31), c0, true, v[u]);
         if (last < row_end) {
           // fast path: the whole step is in row i
-          float v[kU][V];
-#pragma unroll
-          for (int u = 0; u < kU; ++u)
-            load_brow<TB, V>(d, __shfl_sync(kFull, mc, (t0 + u * G + grp) & 31), c0, true, v[u]);
 #pragma unroll
           for (int u = 0; u < kU; ++u) {
             const bool live = t0 + u * G + grp < cnt;  // past cnt: B row 0, selected away
@@ -345,27 +347,30 @@ __global__ void __launch_bounds__(kBlock, 4) k_spmm_merge_grp(const int32_t* __r
           }
           any = true;
         } else {
-          // a row ends inside the step: entry by entry, group (t % G) adds it
-          const int tn = min(t0 + kStep, cnt);
-          for (int t = t0; t < tn; ++t) {
-            const int j = base + t;
-            while (j >= row_end) {  // row i ends before entry j: flush it
-              if (any) flush(shared);
-              any = false;
-              shared = false;
-              ++i;
-              row_end = __ldg(ptr + i + 1);
-            }
-            const int ck = __shfl_sync(kFull, mc, t);
-            const float ak = __shfl_sync(kFull, mv, t);
-            if (grp == t % G) {
-              float v[V];
-              load_brow<TB, V>(d, ck, c0, true, v);
+          // a row ends inside the step: entry by entry in order, flushing
+          // rows as they end; the owning group adds its preloaded row
 #pragma unroll
-              for (int k = 0; k < V; ++k) acc[k] = fmaf(ak, v[k], acc[k]);
+          for (int u = 0; u < kU; ++u)
+#pragma unroll
+            for (int gg = 0; gg < G; ++gg) {
+              const int t = t0 + u * G + gg;
+              if (t < cnt) {
+                const int j = base + t;
+                while (j >= row_end) {  // row i ends before entry j: flush it
+                  if (any) flush(shared);
+                  any = false;
+                  shared = false;
+                  ++i;
+                  row_end = __ldg(ptr + i + 1);
+                }
+                const float ak = __shfl_sync(kFull, mv, t);
+                if (grp == gg) {
+#pragma unroll
+                  for (int k = 0; k < V; ++k) acc[k] = fmaf(ak, v[u][k], acc[k]);
+                }
+                any = true;
+              }
             }
-            any = true;
-          }
         }
       }
     }
@@ -664,11 +669,12 @@ void launch_fmt(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
         auto* cuts = static_cast<int2*>(scratch(ctx, (nchunks + 1) * sizeof(int2)));
         SFG_LAUNCH(k_merge_cuts, (int)std::min<int64_t>(ceil_div(nchunks + 1, 256), (int64_t)ctx->sms * 8), 256, 0,
                    ctx->stream, a->ptr, a->m, a->nnz, nchunks + 1, cuts);
-        const bool vec4 = d.ldb % 4 == 0 && d.ldc % 4 == 0;
-        // nd = 32 on config 5: kU = 2 28.7 ms, kU = 4 32.5, kU = 1 34.2
-        // (the one-entry-per-warp-step kernel: 43 ms, issue-bound)
+        const bool vec4 = d.ldb % 4 == 0 && d.ldc % 4 == 0 &&
+                          ((reinterpret_cast<uintptr_t>(d.b) | reinterpret_cast<uintptr_t>(d.c)) & 15) == 0;
+        // nd = 32 on config 5 (SpMM ms): kU = 4 25.1, kU = 2 28.9, kU = 8 31.3
+        // (spills); the one-entry-per-warp-step kernel: 43 (issue-bound)
         if (vec4 && d.nd == 32)
-          SFG_LAUNCH((k_spmm_merge_grp<TB, 4, 4, 2>), grid_for(nchunks), kBlock, 0, ctx->stream, a->ptr, a->idx,
+          SFG_LAUNCH((k_spmm_merge_grp<TB, 4, 4, 4>), grid_for(nchunks), kBlock, 0, ctx->stream, a->ptr, a->idx,
                      fv, cuts, nchunks, d);
         else if (vec4 && d.nd == 64)
           SFG_LAUNCH((k_spmm_merge_grp<TB, 2, 4, 4>), grid_for(nchunks), kBlock, 0, ctx->stream, a->ptr, a->idx,
@@ -681,7 +687,8 @@ void launch_fmt(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
     case SFG_DCSR: {
       if (stored_rows == 0) break;
       const int32_t* rows = a->kind == SFG_DCSR ? a->row : nullptr;
-      if (short_rows && d.nd % (32 * V) == 0 && d.ldb % V == 0 && d.ldc % V == 0)
+      if (short_rows && d.nd % (32 * V) == 0 && d.ldb % V == 0 && d.ldc % V == 0 &&
+          ((reinterpret_cast<uintptr_t>(d.b) | reinterpret_cast<uintptr_t>(d.c)) & (4 * V - 1)) == 0)
         SFG_LAUNCH((k_spmm_rows_batch<TB, V, kBatchRows, kBatchK, true>),
                    grid_for(ceil_div(stored_rows, kBatchRows) * chunks), kBlock, 0, ctx->stream, rows, a->ptr,
                    a->idx, fv, stored_rows, d);

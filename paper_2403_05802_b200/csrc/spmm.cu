@@ -739,8 +739,11 @@ void launch_fmt(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
 
 template <typename TB>
 void launch_v(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
-  if (d.nd >= 128) launch_fmt<TB, 4>(ctx, a, d);
-  else if (d.nd >= 64) launch_fmt<TB, 2>(ctx, a, d);
+  // vector B loads need a B pointer aligned to the vector (callers may pass
+  // any element offset)
+  const uintptr_t pb = reinterpret_cast<uintptr_t>(d.b);
+  if (d.nd >= 128 && pb % (4 * sizeof(TB)) == 0) launch_fmt<TB, 4>(ctx, a, d);
+  else if (d.nd >= 64 && pb % (2 * sizeof(TB)) == 0) launch_fmt<TB, 2>(ctx, a, d);
   else launch_fmt<TB, 1>(ctx, a, d);
 }
 

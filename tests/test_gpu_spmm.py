@@ -148,3 +148,23 @@ def test_spmm_csr_heavy_and_empty_rows(ctx, port, accumulate):
     if accumulate:
         cr = cr + c0.astype(np.float64)
     check(cd, cr, abs_bound(r, c, v, m, b.astype(np.float64)) + np.abs(c0) * accumulate, ("heavy", accumulate))
+
+
+@pytest.mark.parametrize("fmt", ["CSR", "DCSR", "COO", "ELL"])
+@pytest.mark.parametrize("nd", [32, 64, 128])
+def test_spmm_unaligned_dense_pointers(ctx, port, fmt, nd):
+    """B and C may start at any element offset (vector paths are chosen only
+    for aligned pointers)."""
+    rng = np.random.default_rng(nd)
+    m, n = 300, 200
+    key = np.unique(rng.integers(0, m * n, 3000))
+    r, c = key // n, key % n
+    v = (rng.random(len(r)) * 2 - 1).astype(np.float32)
+    b = (rng.random((n, nd)) * 2 - 1).astype(np.float32)
+    a = ctx.convert(ctx.from_coo(m, n, r, c, v), fmt)
+    bbuf = ctx.buffer(b.nbytes + 4).upload(np.concatenate([np.zeros(1, np.float32), b.ravel()]))
+    cbuf = ctx.buffer(m * nd * 4 + 4)
+    ctx.spmm_device(a, bbuf.ptr + 4, sfg.F32, nd, cbuf.ptr + 4)
+    cd = cbuf.download(np.float32, m * nd + 1)[1:].reshape(m, nd)
+    cr = port.spmm(port.convert(port.from_coo(m, n, r, c, v), fmt), b.astype(np.float64))
+    check(cd, cr, abs_bound(r, c, v, m, b.astype(np.float64)), (fmt, nd, "unaligned"))

@@ -36,19 +36,28 @@ constexpr int kItems = 16;
 constexpr int kTile = kBlock * kItems;
 
 __global__ void __launch_bounds__(kBlock) k_count_scan(const int32_t* __restrict__ cnt, int32_t n,
-                                                        int32_t* __restrict__ ptr,
-                                                        int32_t* __restrict__ cursor,
+                                                        int32_t* __restrict__ ptr, int32_t* __restrict__ cursor,
                                                         unsigned long long* __restrict__ status,
                                                         uint32_t epoch, int32_t* __restrict__ maxcnt) {
   __shared__ uint32_t smem[34];
   __shared__ uint32_t slot;
   const int64_t c0 = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kItems;
+  const bool full = c0 + kItems <= n;  // 16-byte vector loads / stores
   uint32_t v[kItems];
   uint32_t sum = 0;
   int32_t mx = 0;
+  if (full) {
+#pragma unroll
+    for (int q = 0; q < kItems / 4; ++q) {
+      const int4 w = __ldg(reinterpret_cast<const int4*>(cnt + c0) + q);
+      v[4 * q] = w.x, v[4 * q + 1] = w.y, v[4 * q + 2] = w.z, v[4 * q + 3] = w.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) v[i] = c0 + i < n ? (uint32_t)__ldg(cnt + c0 + i) : 0u;
+  }
 #pragma unroll
   for (int i = 0; i < kItems; ++i) {
-    v[i] = c0 + i < n ? (uint32_t)__ldg(cnt + c0 + i) : 0u;
     sum += v[i];
     mx = max(mx, (int32_t)v[i]);
   }
@@ -57,16 +66,35 @@ __global__ void __launch_bounds__(kBlock) k_count_scan(const int32_t* __restrict
   mx = warp_max(mx);
   if ((threadIdx.x & 31) == 0) atomicMax(maxcnt, mx);
   uint32_t p = lookback_prefix(status, epoch, blockIdx.x, total, &slot) + excl;
+  if (full) {
 #pragma unroll
-  for (int i = 0; i < kItems; ++i) {
-    if (c0 + i < n) {
-      ptr[c0 + i] = (int32_t)p;
-      cursor[c0 + i] = (int32_t)p;
-      p += v[i];
+    for (int q = 0; q < kItems / 4; ++q) {
+      int4 w;
+      w.x = (int32_t)p, p += v[4 * q];
+      w.y = (int32_t)p, p += v[4 * q + 1];
+      w.z = (int32_t)p, p += v[4 * q + 2];
+      w.w = (int32_t)p, p += v[4 * q + 3];
+      reinterpret_cast<int4*>(ptr + c0)[q] = w;
+      reinterpret_cast<int4*>(cursor + c0)[q] = w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      if (c0 + i < n) {
+        ptr[c0 + i] = (int32_t)p;
+        cursor[c0 + i] = (int32_t)p;
+        p += v[i];
+      }
     }
   }
   if (c0 + kItems >= n && c0 < n) ptr[n] = (int32_t)p;
 }
+
+// Atomic-cursor scatter; the order inside a column is fixed afterwards
+// (mostly ascending already: earlier entries tend to claim earlier slots).
+// kScatterU entries per thread are in flight at once (the atomic's round
+// trip dominates).
+constexpr int kScatterU = 4;
 
 __global__ void __launch_bounds__(kBlock) k_csc_scatter(const int32_t* __restrict__ row,
                                                          const int32_t* __restrict__ col,
@@ -77,12 +105,20 @@ __global__ void __launch_bounds__(kBlock) k_csc_scatter(const int32_t* __restric
   // the scattered 4-byte stores fill their lines over the whole pass: keep
   // those lines (and k_csc_fix's re-read) in L2 ahead of the streamed input
   const uint64_t once = l2_evict_first(), keep = l2_evict_last();
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int c = (int)ld_hint(col + e, once);
-    int pos = atomicAdd(cursor + c, 1);
-    st_hint(orow + pos, ld_hint(row + e, once), keep);
-    st_hint(oval + pos, ld_hint(val + e, once), keep);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += kScatterU * stride) {
+    int c[kScatterU], pos[kScatterU];
+#pragma unroll
+    for (int u = 0; u < kScatterU; ++u) c[u] = e + u * stride < nnz ? (int)ld_hint(col + e + u * stride, once) : -1;
+#pragma unroll
+    for (int u = 0; u < kScatterU; ++u)
+      if (c[u] >= 0) pos[u] = atomicAdd(cursor + c[u], 1);
+#pragma unroll
+    for (int u = 0; u < kScatterU; ++u)
+      if (c[u] >= 0) {
+        st_hint(orow + pos[u], ld_hint(row + e + u * stride, once), keep);
+        st_hint(oval + pos[u], ld_hint(val + e + u * stride, once), keep);
+      }
   }
 }
 
@@ -170,8 +206,8 @@ sfg_tensor* coo_to_csc(sfg_context* ctx, const sfg_tensor* s) {
   int32_t mx = 0;
   read_back(ctx, maxcnt, sizeof mx, &mx);
   if (mx <= kShortCol) {
-    SFG_LAUNCH(k_csc_scatter, stream_grid(ctx, nnz, kBlock, 4), kBlock, 0, ctx->stream, s->row,
-               s->idx, sv, nnz, cursor, t->idx, tv);
+    SFG_LAUNCH(k_csc_scatter, stream_grid(ctx, ceil_div(nnz, kScatterU), kBlock, 1), kBlock, 0, ctx->stream,
+               s->row, s->idx, sv, nnz, cursor, t->idx, tv);
     SFG_LAUNCH(k_csc_fix, stream_grid(ctx, n, kBlock, 2), kBlock, 0, ctx->stream, t->ptr,
                (int32_t)n, t->idx, tv);
     dfree(ctx, cnt);

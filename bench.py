@@ -333,7 +333,10 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
-    if world > 1:
+    # --rowpart runs the row-partitioned path (communicator, chunked output,
+    # all-gather) even at N = 1, under torchrun: a check of that code path
+    rowpart = world > 1 or args.rowpart
+    if rowpart:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
     ctx = sfg.Context(local, stream.cuda_stream)
@@ -341,7 +344,7 @@ def run_ours(args):
     wl.setup(torch)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
-    if world > 1:
+    if rowpart:
         # the library's own NCCL communicator (sfg_comm_create); the id
         # travels over torch.distributed
         uid = [sfg.comm_unique_id() if rank == 0 else None]
@@ -356,7 +359,7 @@ def run_ours(args):
 
     def step():
         wl.step()
-        if world > 1:
+        if rowpart:
             ctx.allgather_chunks(comm, ybuf.data_ptr(), chunk * width)
 
     def timed(fn, k, flush_between=True):
@@ -466,7 +469,7 @@ def run_ours(args):
                        "l2": "flushed (256 MB write) before every timed step",
                        "parallelism": f"row-partitioned x{world}, in-place NCCL all-gather of the output "
                                       "(C-ABI sfg_allgather_chunks)"
-                       if world > 1 else "single GPU", **wl.info},
+                       if rowpart else "single GPU", **wl.info},
             "step_ms": {"min": round(min(step_ms), 4), "median": round(statistics.median(step_ms), 4),
                         "max": round(max(step_ms), 4), "all": [round(t, 4) for t in step_ms],
                         "host_enqueue_ms": [round(t, 3) for t in step_host_ms]},
@@ -476,7 +479,7 @@ def run_ours(args):
         if world == 1 and wl.has_cpu_sample and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(args.config, steps=1)
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if rowpart:
         dist.barrier()
         comm.close()
         dist.destroy_process_group()
@@ -661,6 +664,8 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--threshold", type=int, default=8, help="config 2: hybrid split threshold T")
+    ap.add_argument("--rowpart", action="store_true",
+                    help="row-partitioned path at N=1 too (under torchrun; exercises the NCCL all-gather)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
     ap.add_argument("--profile", action="store_true",

@@ -107,7 +107,7 @@ void comm_destroy(sfg_comm* c) {
 
 // In place: rank r's chunk is buf[r * chunk_elems, (r + 1) * chunk_elems).
 void allgather_chunks(sfg_context* ctx, sfg_comm* c, float* buf, int64_t chunk_elems) {
-  if (c->nranks == 1 || chunk_elems == 0) return;
+  if (chunk_elems == 0) return;  // one rank too: the same NCCL call (a no-op copy)
   check(nccl().all_gather(buf + (int64_t)c->rank * chunk_elems, buf, (size_t)chunk_elems, ncclFloat32, c->comm,
                           ctx->stream),
         "ncclAllGather");

@@ -417,6 +417,17 @@ def run_ours(args):
         units = float(tn.item())
     ms_per_step = total_ms / args.steps
     value = units / (ms_per_step * 1e-3) / 1e6
+    split = None
+    if rowpart:
+        # the same steps without the output all-gather
+        # (compute only), max over ranks, next to the gathered step above
+        dist.barrier()
+        comp = sum(timed(wl.step, args.steps))
+        t = torch.tensor([comp], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        comp_ms = float(t.item()) / args.steps
+        split = {"compute_only_ms": round(comp_ms, 4), "with_allgather_ms": round(ms_per_step, 4),
+                 "allgather_bytes_per_rank": int(4 * chunk * width * (world - 1))}
 
     # ---- kernel families alone (CUDA events on the launching stream)
     hbm, _, peak_src = load_peaks()
@@ -474,6 +485,7 @@ def run_ours(args):
                         "max": round(max(step_ms), 4), "all": [round(t, 4) for t in step_ms],
                         "host_enqueue_ms": [round(t, 3) for t in step_host_ms]},
             "roofline": roof, "kernels": kernels, "e2e": e2e, "gpu_launches": int(launches),
+            **({"rowpart": split} if split else {}),
             "clocks": clk.summary(),
         }
         if world == 1 and wl.has_cpu_sample and not args.no_cpu_baseline:

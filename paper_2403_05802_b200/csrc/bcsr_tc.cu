@@ -1059,8 +1059,13 @@ bool spmm_bcsr_tc(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dt
       // blocks: 0.46)
       constexpr int kP = 4, kW = 4;
       const size_t psmem = 1024 + kPStages * kPStageBytes + sizeof(PShared) + 64;
+#ifdef SFG_TC_DEBUG
+      // profiling / ablation switches (ablations skip work: debug builds only)
       static const int dbg = (std::getenv("SFG_TC_PROF") ? 256 : 0) |
                              (std::getenv("SFG_TC_ABLATE") ? std::atoi(std::getenv("SFG_TC_ABLATE")) : 0);
+#else
+      constexpr int dbg = 0;
+#endif
       unsigned long long* dbg_out = nullptr;
       if (dbg) {
         dbg_out = static_cast<unsigned long long*>(scratch(ctx, 64 * 8));

@@ -7,12 +7,16 @@
 // is row-sorted and the sort is stable), materialized like CSR with the
 // roles of rows and columns exchanged (storage.hpp:171-200).
 //
-// Device plan. Fast path (every column holds <= kShortCol entries, e.g. the
-// hypersparse config 3): column histogram (RED atomics) -> single-pass
-// look-back scan -> atomic-cursor scatter -> per-column insertion sort by
-// row, which restores the stable order. Any longer column switches to the
-// general path: stable LSD radix sort on the column bits with the row
-// carried in the upper key half, then compression of the sorted columns.
+// Device plan. (1) Column-block partition (every block of 1,024 columns
+// holds <= 4,096 entries, e.g. the hypersparse config 3): count per block,
+// scan, scatter into block regions, sort each block in shared memory —
+// below. (2) Otherwise, when every column holds <= kShortCol entries:
+// column histogram (RED atomics) -> single-pass look-back scan ->
+// atomic-cursor scatter -> per-column insertion sort by row, which restores
+// the stable order. (3) Any longer column: stable LSD radix sort on the
+// column bits with the row carried in the upper key half, then compression
+// of the sorted columns. Config 3 (8.4 M entries, 4 M columns): (1) 0.35 ms,
+// (2) 0.37 ms.
 #include "async.cuh"
 #include "devutil.cuh"
 #include "internal.cuh"
@@ -172,6 +176,164 @@ __global__ void __launch_bounds__(kBlock) k_csc_unpack(const uint64_t* __restric
   }
 }
 
+// ---------------------------------------------- column-block partition path
+// Atomic-free in global memory and coalesced: (1) each of P CTAs counts its
+// contiguous share of the entries per column block of kBlkCols columns (in
+// shared memory); (2) an exclusive scan over (block, CTA) gives every CTA
+// its write range inside every block's region; (3) the CTAs scatter their
+// entries into those ranges (shared-memory cursors); (4) one CTA per column
+// block loads its <= kBlkCap entries, counts them per column in shared
+// memory, places them by column, insertion-sorts each (short) column by row
+// and writes idx / val / ptr for its columns with coalesced stores.
+constexpr int kBlkColBits = 10;
+constexpr int kBlkCols = 1 << kBlkColBits;  // columns per block
+constexpr int kBlkCap = 4096;               // entries one block CTA sorts in shared memory
+constexpr int kMaxBlks = 8192;              // shared-memory counters of steps 1 and 3
+constexpr int kPartCtas = 296;              // P (2 per SM)
+
+__global__ void __launch_bounds__(kBlock) k_blk_count(const int32_t* __restrict__ col, int64_t nnz, int nb,
+                                                       int32_t* __restrict__ counts) {
+  __shared__ int32_t h[kMaxBlks];
+  for (int i = threadIdx.x; i < nb; i += kBlock) h[i] = 0;
+  __syncthreads();
+  const int64_t per = (nnz + gridDim.x - 1) / gridDim.x;
+  const int64_t e0 = blockIdx.x * per, e1 = min(nnz, e0 + per);
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += kBlock) atomicAdd(&h[ld_stream(col + e) >> kBlkColBits], 1);
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb; b += kBlock) counts[(int64_t)b * gridDim.x + blockIdx.x] = h[b];
+}
+
+__global__ void __launch_bounds__(kBlock) k_blk_max(const int32_t* __restrict__ off, int nb, int p,
+                                                     int32_t* __restrict__ mx) {
+  int m = 0;
+  for (int b = blockIdx.x * kBlock + threadIdx.x; b < nb; b += gridDim.x * kBlock)
+    m = max(m, off[(int64_t)(b + 1) * p] - off[(int64_t)b * p]);
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) atomicMax(mx, m);
+}
+
+// Entries travel as (row << kBlkColBits | column within the block, value):
+// rows must fit 32 - kBlkColBits bits (checked by the caller).
+__global__ void __launch_bounds__(kBlock) k_blk_scatter(const int32_t* __restrict__ row,
+                                                         const int32_t* __restrict__ col,
+                                                         const float* __restrict__ val, int64_t nnz, int nb,
+                                                         const int32_t* __restrict__ off,
+                                                         uint32_t* __restrict__ tkey, float* __restrict__ tval) {
+  __shared__ int32_t cur[kMaxBlks];
+  for (int b = threadIdx.x; b < nb; b += kBlock) cur[b] = off[(int64_t)b * gridDim.x + blockIdx.x];
+  __syncthreads();
+  // the scattered stores fill their lines over the whole pass: keep them in
+  // L2 (k_blk_sort reads them next) ahead of the streamed input
+  const uint64_t once = l2_evict_first(), keep = l2_evict_last();
+  const int64_t per = (nnz + gridDim.x - 1) / gridDim.x;
+  const int64_t e0 = blockIdx.x * per, e1 = min(nnz, e0 + per);
+  constexpr int U = 4;  // entries per thread in flight
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += U * kBlock) {
+    uint32_t c[U], r[U], v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (e + u * kBlock < e1) {
+        c[u] = ld_hint(col + e + u * kBlock, once);
+        r[u] = ld_hint(row + e + u * kBlock, once);
+        v[u] = ld_hint(val + e + u * kBlock, once);
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (e + u * kBlock < e1) {
+        const int slot = atomicAdd(&cur[c[u] >> kBlkColBits], 1);
+        st_hint(tkey + slot, (r[u] << kBlkColBits) | (c[u] & (kBlkCols - 1)), keep);
+        st_hint(tval + slot, v[u], keep);
+      }
+  }
+}
+
+constexpr int kSortThreads = 512;
+
+__global__ void __launch_bounds__(kSortThreads) k_blk_sort(const uint32_t* __restrict__ tkey,
+                                                      const float* __restrict__ tval,
+                                                      const int32_t* __restrict__ off, int p, int64_t n,
+                                                      int64_t nnz, int32_t* __restrict__ ptr,
+                                                      int32_t* __restrict__ orow, float* __restrict__ oval) {
+  constexpr int kPer = kBlkCap / kSortThreads;
+  __shared__ int32_t cnt[kBlkCols + 1];
+  __shared__ uint32_t scan_smem[34];
+  __shared__ int32_t srow[kBlkCap];
+  __shared__ float sval[kBlkCap];
+  const int b = blockIdx.x;
+  const int32_t s = off[(int64_t)b * p], size = off[(int64_t)(b + 1) * p] - s;
+  const int64_t c0 = (int64_t)b << kBlkColBits;
+  const int ncols = n - c0 < kBlkCols ? (int)(n - c0) : kBlkCols;
+  for (int i = threadIdx.x; i < kBlkCols; i += kSortThreads) cnt[i] = 0;
+  __syncthreads();
+  int r[kPer], c[kPer], slot[kPer];
+  float v[kPer];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int i = k * kSortThreads + threadIdx.x;
+    if (i < size) {
+      const uint32_t key = tkey[s + i];
+      r[k] = (int)(key >> kBlkColBits);
+      c[k] = (int)(key & (kBlkCols - 1));
+      v[k] = tval[s + i];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kPer; ++k)
+    if (k * kSortThreads + threadIdx.x < size) slot[k] = atomicAdd(&cnt[c[k]], 1);
+  __syncthreads();
+  // exclusive scan of the per-column counts (kBlkCols / kBlock per thread)
+  constexpr int kColsPer = kBlkCols / kSortThreads;
+  int loc[kColsPer], sum = 0;
+#pragma unroll
+  for (int q = 0; q < kColsPer; ++q) {
+    loc[q] = cnt[threadIdx.x * kColsPer + q];
+    sum += loc[q];
+  }
+  uint32_t tot;
+  int run = (int)block_exclusive_scan<uint32_t, kSortThreads>((uint32_t)sum, scan_smem, &tot);
+  int len[kColsPer];
+#pragma unroll
+  for (int q = 0; q < kColsPer; ++q) {
+    len[q] = loc[q];
+    cnt[threadIdx.x * kColsPer + q] = run;  // column start within the block
+    run += loc[q];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kPer; ++k)
+    if (k * kSortThreads + threadIdx.x < size) {
+      const int pos = cnt[c[k]] + slot[k];
+      srow[pos] = r[k];
+      sval[pos] = v[k];
+    }
+  __syncthreads();
+  // each column's rows in ascending order (columns are short; the reference
+  // order is the stable sort of a row-sorted input)
+#pragma unroll
+  for (int q = 0; q < kColsPer; ++q) {
+    const int st = cnt[threadIdx.x * kColsPer + q], n_ = len[q];
+    for (int i = st + 1; i < st + n_; ++i) {
+      const int rr = srow[i];
+      const float vv = sval[i];
+      int j = i - 1;
+      while (j >= st && srow[j] > rr) {
+        srow[j + 1] = srow[j];
+        sval[j + 1] = sval[j];
+        --j;
+      }
+      srow[j + 1] = rr;
+      sval[j + 1] = vv;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < size; i += kSortThreads) {
+    orow[s + i] = srow[i];
+    oval[s + i] = sval[i];
+  }
+  for (int i = threadIdx.x; i < ncols; i += kSortThreads) ptr[c0 + i] = s + cnt[i];
+  if (c0 + ncols == n && threadIdx.x == 0) ptr[n] = (int32_t)nnz;
+}
+
 int bits_for(int64_t extent) {
   int b = 0;
   while ((int64_t(1) << b) < extent) ++b;
@@ -179,6 +341,43 @@ int bits_for(int64_t extent) {
 }
 
 }  // namespace
+
+// Column-block partition path (above); false when a block would exceed the
+// shared-memory sort (then the caller takes the histogram path).
+bool csc_by_column_blocks(sfg_context* ctx, const sfg_tensor* s, sfg_tensor* t) {
+  const int64_t n = s->n, nnz = s->nnz;
+  const int64_t nb = ceil_div(n, (int64_t)kBlkCols);
+  if (nb > kMaxBlks || nb * kBlkCap < nnz) return false;  // some block would overflow anyway
+  if (s->m > (int64_t(1) << (32 - kBlkColBits))) return false;  // rows travel in 22 bits
+  const int p = kPartCtas;
+  const int64_t cells = nb * p;
+  int32_t* counts = dalloc_n<int32_t>(ctx, cells);
+  int32_t* off = dalloc_n<int32_t>(ctx, cells + 1);
+  int32_t* dummy = dalloc_n<int32_t>(ctx, cells);
+  const int tiles = (int)ceil_div(cells, kTile);
+  auto* status = lookback_status(ctx, tiles);
+  auto* mx = static_cast<int32_t*>(scratch(ctx, 64));
+  SFG_CUDA(cudaMemsetAsync(mx, 0, 8, ctx->stream));
+  SFG_LAUNCH(k_blk_count, p, kBlock, 0, ctx->stream, s->idx, nnz, (int)nb, counts);
+  SFG_LAUNCH(k_count_scan, tiles, kBlock, 0, ctx->stream, counts, (int32_t)cells, off, dummy, status,
+             ctx->epoch++, mx + 1);
+  SFG_LAUNCH(k_blk_max, (int)std::min<int64_t>(ceil_div(nb, kBlock), 64), kBlock, 0, ctx->stream, off, (int)nb, p,
+             mx);
+  int32_t big = 0;
+  read_back(ctx, mx, sizeof big, &big);
+  if (big > kBlkCap) {
+    for (void* q : {(void*)counts, (void*)off, (void*)dummy}) dfree(ctx, q);
+    return false;
+  }
+  uint32_t* tkey = dalloc_n<uint32_t>(ctx, nnz);
+  float* tval = dalloc_n<float>(ctx, nnz);
+  SFG_LAUNCH(k_blk_scatter, p, kBlock, 0, ctx->stream, s->row, s->idx, static_cast<const float*>(s->val), nnz,
+             (int)nb, off, tkey, tval);
+  SFG_LAUNCH(k_blk_sort, (int)nb, kSortThreads, 0, ctx->stream, tkey, tval, off, p, n, nnz, t->ptr, t->idx,
+             static_cast<float*>(t->val));
+  for (void* q : {(void*)counts, (void*)off, (void*)dummy, (void*)tkey, (void*)tval}) dfree(ctx, q);
+  return true;
+}
 
 sfg_tensor* coo_to_csc(sfg_context* ctx, const sfg_tensor* s) {
   const int64_t n = s->n, nnz = s->nnz;
@@ -193,6 +392,7 @@ sfg_tensor* coo_to_csc(sfg_context* ctx, const sfg_tensor* s) {
     SFG_CUDA(cudaMemsetAsync(t->ptr, 0, (n + 1) * sizeof(int32_t), ctx->stream));
     return t;
   }
+  if (csc_by_column_blocks(ctx, s, t)) return t;
   int32_t* cnt = dalloc_n<int32_t>(ctx, n);
   int32_t* cursor = dalloc_n<int32_t>(ctx, n);
   int tiles = (int)ceil_div(n, kTile);

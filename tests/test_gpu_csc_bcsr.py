@@ -37,6 +37,31 @@ def test_csc_long_columns_general_path(ctx, port, seed):
     assert_same_materialized(ctx.convert(d, "CSC").download(), port.convert(p, "CSC").download(), "CSC")
 
 
+@pytest.mark.parametrize("m,n,nnz", [(1 << 22, 1 << 22, 300_000), (5000, 70_000, 150_000), (100, 1500, 60_000)])
+def test_csc_column_blocks(ctx, port, m, n, nnz):
+    # the column-block partition path: many blocks of 1,024 columns, each
+    # sorted in shared memory; the last block is partial when n % 1024 != 0;
+    # (100, 1500, 60000) puts ~40 rows in a column (dense short matrix)
+    rng = np.random.default_rng(nnz)
+    key = np.unique(rng.integers(0, m * n, nnz, dtype=np.int64))
+    r, c = key // n, key % n
+    v = (rng.random(len(key)) + 0.5).astype(np.float32)
+    d, p = ctx.from_coo(m, n, r, c, v), port.from_coo(m, n, r, c, v)
+    assert_same_materialized(ctx.convert(d, "CSC").download(), port.convert(p, "CSC").download(), ("CSC", m, n))
+
+
+def test_csc_block_overflow_takes_histogram_path(ctx, port):
+    # ~10 entries per column but > 4,096 entries per column block: the
+    # per-column histogram path (short columns, atomic cursors)
+    m, n = 50_000, 3000
+    rng = np.random.default_rng(3)
+    key = np.unique(rng.integers(0, m * n, 30_000, dtype=np.int64))
+    r, c = key // n, key % n
+    v = (rng.random(len(key)) + 0.5).astype(np.float32)
+    d, p = ctx.from_coo(m, n, r, c, v), port.from_coo(m, n, r, c, v)
+    assert_same_materialized(ctx.convert(d, "CSC").download(), port.convert(p, "CSC").download(), "CSC")
+
+
 def test_csc_matrix_a(ctx):
     g = matrix_a()
     t = ctx.from_coo(g["rows"], g["cols"], g["coo_d0"], g["coo_d1"], g["coo_val"])

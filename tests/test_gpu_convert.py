@@ -228,3 +228,15 @@ def test_block_cache_reuse_and_release(ctx, port):
         for a, b in zip((p.download() for p in h.parts()), want):
             assert_same_materialized(a, b, "reuse")
         del h
+
+
+def test_int32_index_range_is_enforced(ctx):
+    # SURVEY §8c trap (7): extents or nnz past the int32 index range raise
+    # InvalidOperation before anything is allocated or read
+    for m, n in ((1 << 31, 8), (8, 1 << 31)):
+        with pytest.raises(sfg.SfgError) as ei:
+            ctx.from_coo(m, n, [0], [0], [1.0])
+        assert ei.value.kind == "InvalidOperation"
+    with pytest.raises(sfg.SfgError) as ei:
+        ctx.from_coo_device(8, 8, 1 << 31, 0, 0, 0)  # never dereferenced
+    assert ei.value.kind == "InvalidOperation"

@@ -162,6 +162,7 @@ int sfg_context_destroy(sfg_context* ctx) {
     sfg::release_cached(ctx);
     cudaStreamSynchronize(ctx->stream);
     cudaFreeHost(ctx->pinned);
+    if (ctx->sizes_ev) cudaEventDestroy(ctx->sizes_ev);
     if (ctx->staging) cudaFreeHost(ctx->staging);
     delete ctx;
   });

@@ -306,7 +306,10 @@ struct RowInfo {
   int64_t k = 0;
 };
 
-RowInfo row_info(sfg_context* ctx, const sfg_tensor* s, int64_t min_sum, int32_t* totals) {
+// defer: the sizes (nnz_sel, k, has_zeros) are read back asynchronously;
+// call row_info_finish before using them (work that needs only the device
+// arrays — k_split — can be enqueued in between).
+RowInfo row_info(sfg_context* ctx, const sfg_tensor* s, int64_t min_sum, int32_t* totals, bool defer = false) {
   RowInfo ri;
   const int64_t m = s->m;
   // Explicit zeros only matter when the source may hold them: a tensor known
@@ -337,12 +340,24 @@ RowInfo row_info(sfg_context* ctx, const sfg_tensor* s, int64_t min_sum, int32_t
   // slow path.
   SFG_LAUNCH(k_row_scan, tiles, kBlock, 0, ctx->stream, ri.ptr, ri.zcnt, zeros_possible ? 1 : 0, (int32_t)m,
              min_sum, ri.off, totals, status, ctx->epoch++, reinterpret_cast<ScanOut*>(tail + 1));
+  if (defer) {
+    read_back_start(ctx, tail, 16);
+    return ri;
+  }
   int32_t h[4];
   read_back(ctx, tail, 16, h);
   ri.has_zeros = h[0];
   ri.nnz_sel = h[1];
   ri.k = h[2];
   return ri;
+}
+
+void row_info_finish(sfg_context* ctx, RowInfo& ri) {
+  int32_t h[4];
+  read_back_wait(ctx, 16, h);
+  ri.has_zeros = h[0];
+  ri.nnz_sel = h[1];
+  ri.k = h[2];
 }
 
 void free_row_info(sfg_context* ctx, RowInfo& ri) {
@@ -405,15 +420,21 @@ sfg_tensor* coo_to_ell(sfg_context* ctx, const sfg_tensor* s) {
 }
 
 sfg_tensor* coo_to_hyb(sfg_context* ctx, const sfg_tensor* s, int64_t min_sum) {
-  RowInfo ri = row_info(ctx, s, min_sum, nullptr);
+  // The split needs only the device offsets, so it is enqueued before the
+  // host waits for the sizes: the read-back round trip overlaps the split
+  // instead of idling the GPU. The COO part is allocated for every entry
+  // (an upper bound) and its size set once known.
+  RowInfo ri = row_info(ctx, s, min_sum, nullptr, /*defer=*/true);
   sfg_tensor* h = new_tensor(ctx, SFG_HYB, s->m, s->n);
   h->threshold = min_sum;
-  h->part[1] = coo_part(ctx, s->m, s->n, ri.nnz_sel);
+  h->part[1] = coo_part(ctx, s->m, s->n, s->nnz);
   h->part[1]->has_zeros = s->has_zeros == 0 ? 0 : -1;
   if (s->nnz)
     SFG_LAUNCH(k_split, stream_grid(ctx, ceil_div(s->nnz, kSplitRun), kBlock, 1, 8), kBlock, 0, ctx->stream,
                s->row, s->idx, static_cast<const float*>(s->val), s->nnz, ri.off, h->part[1]->row,
                h->part[1]->idx, static_cast<float*>(h->part[1]->val), nullptr, nullptr, nullptr);
+  row_info_finish(ctx, ri);
+  h->part[1]->nnz = ri.nnz_sel;
   h->part[0] = ell_from(ctx, s, ri, true);
   free_row_info(ctx, ri);
   return h;

@@ -143,6 +143,20 @@ void read_back(sfg_context* ctx, const void* dev, size_t bytes, void* host) {
   std::memcpy(host, ctx->pinned, bytes);
 }
 
+// second KB of the pinned scratch, so a plain read_back in between is safe
+void read_back_start(sfg_context* ctx, const void* dev, size_t bytes) {
+  if (bytes > 1024) raise(SFG_ERR_INVALID_OPERATION, "read_back too large");
+  if (!ctx->sizes_ev) SFG_CUDA(cudaEventCreateWithFlags(&ctx->sizes_ev, cudaEventDisableTiming));
+  SFG_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->pinned) + 2048, dev, bytes, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  SFG_CUDA(cudaEventRecord(ctx->sizes_ev, ctx->stream));
+}
+
+void read_back_wait(sfg_context* ctx, size_t bytes, void* host) {
+  SFG_CUDA(cudaEventSynchronize(ctx->sizes_ev));
+  std::memcpy(host, reinterpret_cast<char*>(ctx->pinned) + 2048, bytes);
+}
+
 sfg_tensor* new_tensor(sfg_context* ctx, int kind, int64_t m, int64_t n) {
   auto* t = new sfg_tensor;
   t->ctx = ctx;

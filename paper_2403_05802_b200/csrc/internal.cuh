@@ -52,6 +52,7 @@ struct sfg_context {
   cudaStream_t stream = nullptr;
   int sms = 148;
   int64_t* pinned = nullptr;   // small host scratch for size read-backs
+  cudaEvent_t sizes_ev = nullptr;  // read_back_async completion
   char* staging = nullptr;     // pinned host staging for file ingest (grow-only)
   size_t staging_bytes = 0;
   void* scratch = nullptr;     // device scratch (counters, histograms, flags)
@@ -123,6 +124,11 @@ void* scratch(sfg_context* ctx, size_t bytes);
 unsigned long long* lookback_status(sfg_context* ctx, size_t words);
 // Copy `count` int64 values device->host through pinned memory and sync.
 void read_back(sfg_context* ctx, const void* dev, size_t bytes, void* host);
+// The same in two halves, so the host can enqueue more work before it
+// waits: start copies `bytes` (<= 1 KB) at this point of the stream, wait
+// blocks until they arrived. One outstanding read at a time per context.
+void read_back_start(sfg_context* ctx, const void* dev, size_t bytes);
+void read_back_wait(sfg_context* ctx, size_t bytes, void* host);
 
 sfg_tensor* new_tensor(sfg_context* ctx, int kind, int64_t m, int64_t n);
 void free_tensor_arrays(sfg_tensor* t);

@@ -163,6 +163,9 @@ int sfg_context_destroy(sfg_context* ctx) {
     cudaStreamSynchronize(ctx->stream);
     cudaFreeHost(ctx->pinned);
     if (ctx->sizes_ev) cudaEventDestroy(ctx->sizes_ev);
+    for (cudaEvent_t e : ctx->size_events)
+      if (e) cudaEventDestroy(e);
+    if (ctx->size_slots) cudaFreeHost(ctx->size_slots);
     if (ctx->staging) cudaFreeHost(ctx->staging);
     delete ctx;
   });
@@ -354,12 +357,14 @@ int sfg_tensor_view_get(sfg_context* ctx, const sfg_tensor* t, sfg_tensor_view* 
         v.level[1] = level(P | I, 0, t->m - 1, t->nnz, t->nnz, t->idx, t->n + 1, t->ptr);
         v.nvals = t->nnz;
         break;
-      case SFG_DCSR:
+      case SFG_DCSR: {
+        const int64_t nnr = sfg::tensor_nnr(t);  // may still be in flight
         v.nlevels = 2;
-        v.level[0] = level(I, 0, t->m - 1, t->nnr, t->nnr, t->row, 0, nullptr);
-        v.level[1] = level(P | I, 0, t->n - 1, t->nnz, t->nnz, t->idx, t->nnr + 1, t->ptr);
+        v.level[0] = level(I, 0, t->m - 1, nnr, nnr, t->row, 0, nullptr);
+        v.level[1] = level(P | I, 0, t->n - 1, t->nnz, t->nnz, t->idx, nnr + 1, t->ptr);
         v.nvals = t->nnz;
         break;
+      }
       case SFG_ELL:
         v.nlevels = 3;
         v.level[0] = level(I, 0, t->k - 1, t->k, t->k, t->slots, 0, nullptr);

@@ -280,9 +280,14 @@ sfg_tensor* coo_to_dcsr(sfg_context* ctx, const sfg_tensor* s) {
   SFG_LAUNCH(k_coo_to_dcsr, tiles, kBlock, 0, ctx->stream, s->row, s->idx,
              static_cast<const float*>(s->val), s->nnz, t->row, t->ptr, t->idx,
              static_cast<float*>(t->val), status, ctx->epoch++, nnr_dev);
-  int32_t nnr = 0;
-  read_back(ctx, nnr_dev, sizeof nnr, &nnr);
-  t->nnr = nnr;
+  // nnr is read back asynchronously: the tensor is usable at once and the
+  // host only waits where the count is needed (tensor_nnr)
+  t->nnr_slot = size_slot_start(ctx, nnr_dev);
+  if (t->nnr_slot < 0) {
+    int32_t nnr = 0;
+    read_back(ctx, nnr_dev, sizeof nnr, &nnr);
+    t->nnr = nnr;
+  }
   return t;
 }
 

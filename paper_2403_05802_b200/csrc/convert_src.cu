@@ -244,6 +244,7 @@ sfg_tensor* bcsr_to_coo(sfg_context* ctx, const sfg_tensor* s) {
 }
 
 sfg_tensor* deep_copy(sfg_context* ctx, const sfg_tensor* s) {
+  tensor_nnr(s);  // the copy must not share a pending read-back slot
   sfg_tensor* t = new sfg_tensor(*s);
   t->tc_plan = nullptr;
   t->tc_base = nullptr;
@@ -275,7 +276,7 @@ sfg_tensor* deep_copy(sfg_context* ctx, const sfg_tensor* s) {
       t->val = dup(s->val, s->nnz * esz);
       break;
     case SFG_DCSR:
-      t->row = static_cast<int32_t*>(dup(s->row, s->nnr * 4));
+      t->row = static_cast<int32_t*>(dup(s->row, s->nnr * 4));  // resolved above
       t->ptr = static_cast<int32_t*>(dup(s->ptr, (s->nnr + 1) * 4));
       t->idx = static_cast<int32_t*>(dup(s->idx, s->nnz * 4));
       t->val = dup(s->val, s->nnz * esz);
@@ -307,7 +308,7 @@ sfg_tensor* convert_from_compressed(sfg_context* ctx, const sfg_tensor* s, const
                                   s->m, s->n, dst.kind != SFG_CSR);
       break;
     case SFG_DCSR:
-      coo = row_compressed_to_coo(ctx, s->ptr, s->row, s->nnr, s->idx, static_cast<const float*>(s->val), s->nnz,
+      coo = row_compressed_to_coo(ctx, s->ptr, s->row, tensor_nnr(s), s->idx, static_cast<const float*>(s->val), s->nnz,
                                   s->m, s->n, false);
       break;
     case SFG_CSC:

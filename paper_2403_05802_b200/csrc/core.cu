@@ -157,6 +157,41 @@ void read_back_wait(sfg_context* ctx, size_t bytes, void* host) {
   std::memcpy(host, reinterpret_cast<char*>(ctx->pinned) + 2048, bytes);
 }
 
+constexpr int kSizeSlots = 1024;
+
+int size_slot_start(sfg_context* ctx, const int32_t* dev) {
+  if (!ctx->size_slots) {
+    SFG_CUDA(cudaMallocHost(&ctx->size_slots, kSizeSlots * sizeof(int32_t)));
+    ctx->size_events.assign(kSizeSlots, nullptr);
+    for (int i = kSizeSlots - 1; i >= 0; --i) ctx->free_size_slots.push_back(i);
+  }
+  if (ctx->free_size_slots.empty()) return -1;
+  const int slot = ctx->free_size_slots.back();
+  if (!ctx->size_events[slot])
+    SFG_CUDA(cudaEventCreateWithFlags(&ctx->size_events[slot], cudaEventDisableTiming));
+  SFG_CUDA(cudaMemcpyAsync(ctx->size_slots + slot, dev, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  SFG_CUDA(cudaEventRecord(ctx->size_events[slot], ctx->stream));
+  ctx->free_size_slots.pop_back();
+  return slot;
+}
+
+int32_t size_slot_finish(sfg_context* ctx, int slot) {
+  SFG_CUDA(cudaEventSynchronize(ctx->size_events[slot]));
+  const int32_t v = ctx->size_slots[slot];
+  ctx->free_size_slots.push_back(slot);
+  return v;
+}
+
+int64_t tensor_nnr(const sfg_tensor* t) {
+  if (t->nnr_slot >= 0) {
+    auto* mt = const_cast<sfg_tensor*>(t);
+    const int slot = mt->nnr_slot;
+    mt->nnr_slot = -1;
+    mt->nnr = size_slot_finish(mt->ctx, slot);
+  }
+  return t->nnr;
+}
+
 sfg_tensor* new_tensor(sfg_context* ctx, int kind, int64_t m, int64_t n) {
   auto* t = new sfg_tensor;
   t->ctx = ctx;
@@ -168,6 +203,7 @@ sfg_tensor* new_tensor(sfg_context* ctx, int kind, int64_t m, int64_t n) {
 
 void free_tensor_arrays(sfg_tensor* t) {
   sfg_context* ctx = t->ctx;
+  tensor_nnr(t);  // a pending read-back must land before its slot is reused
   dfree(ctx, t->row);
   dfree(ctx, t->ptr);
   dfree(ctx, t->idx);

@@ -6,6 +6,7 @@
 #include <atomic>
 #include <map>
 #include <unordered_map>
+#include <vector>
 #include <cstdint>
 #include <string>
 
@@ -53,6 +54,11 @@ struct sfg_context {
   int sms = 148;
   int64_t* pinned = nullptr;   // small host scratch for size read-backs
   cudaEvent_t sizes_ev = nullptr;  // read_back_async completion
+  // Deferred size read-backs owned by tensors (core.cu: size slots): pinned
+  // words, one completion event each, and the free list.
+  int32_t* size_slots = nullptr;
+  std::vector<cudaEvent_t> size_events;
+  std::vector<int> free_size_slots;
   char* staging = nullptr;     // pinned host staging for file ingest (grow-only)
   size_t staging_bytes = 0;
   void* scratch = nullptr;     // device scratch (counters, histograms, flags)
@@ -83,7 +89,8 @@ struct sfg_tensor {
   int32_t dtype = SFG_F32;
   int64_t m = 0, n = 0;
   int64_t nnz = 0;       // stored coordinates (COO/CSR/CSC/DCSR), cells (ELL), blocks (BCSR)
-  int64_t nnr = 0;       // DCSR nonempty rows
+  int64_t nnr = 0;       // DCSR nonempty rows (read via tensor_nnr: may still be in flight)
+  int32_t nnr_slot = -1; // >= 0: nnr is being read back into this size slot
   int64_t k = 0;         // ELL slots
   int64_t br = 0, bc = 0;        // BCSR block shape (r, c)
   int64_t rb = 0, cb = 0;        // BCSR level-2/3 extents (== r, c except one-tile edge)
@@ -128,6 +135,11 @@ void read_back(sfg_context* ctx, const void* dev, size_t bytes, void* host);
 // waits: start copies `bytes` (<= 1 KB) at this point of the stream, wait
 // blocks until they arrived. One outstanding read at a time per context.
 void read_back_start(sfg_context* ctx, const void* dev, size_t bytes);
+// Deferred 4-byte read-back into a size slot (-1: none free, read now).
+int size_slot_start(sfg_context* ctx, const int32_t* dev);
+int32_t size_slot_finish(sfg_context* ctx, int slot);
+// A DCSR's nonempty-row count, waiting for its read-back if still pending.
+int64_t tensor_nnr(const sfg_tensor* t);
 void read_back_wait(sfg_context* ctx, size_t bytes, void* host);
 
 sfg_tensor* new_tensor(sfg_context* ctx, int kind, int64_t m, int64_t n);

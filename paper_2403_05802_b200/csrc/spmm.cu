@@ -654,7 +654,7 @@ void launch_fmt(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
                                                       (int64_t)ctx->sms * 16));
   };
   const float* fv = static_cast<const float*>(a->val);
-  const int64_t stored_rows = a->kind == SFG_DCSR ? a->nnr : a->m;
+  const int64_t stored_rows = a->kind == SFG_DCSR ? tensor_nnr(a) : a->m;
   const bool short_rows = stored_rows > 0 && a->nnz <= 8 * stored_rows;  // <= 8 entries per row
   // measured on config 3 (3.6 M rows of ~2.3 entries, nd = 64), SpMM ms:
   // (R, kK) = (24, 8) 0.70, (31, 8) 0.71, (16, 8) 0.73, (16, 4) 0.79,
@@ -762,7 +762,7 @@ void spmm(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dtype, int
   }
   if (a->kind == SFG_BCSR && spmm_bcsr_tc(ctx, a, b, b_dtype, nd, ldb, c, ldc, accumulate)) return;
   if (a->kind == SFG_DCSR && !accumulate && a->m > 0) {
-    if (a->nnr == 0) {
+    if (tensor_nnr(a) == 0) {
       if (ldc == nd) SFG_CUDA(cudaMemsetAsync(c, 0, a->m * ldc * sizeof(float), ctx->stream));
       else SFG_CUDA(cudaMemset2DAsync(c, ldc * sizeof(float), 0, nd * sizeof(float), a->m, ctx->stream));
       return;

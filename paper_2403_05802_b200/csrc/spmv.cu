@@ -337,7 +337,7 @@ void spmv(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, bool 
     case SFG_ELL: spmv_ell(ctx, a, x, y, acc); break;
     case SFG_DCSR: {
       if (!acc) zero_y(ctx, y, a->m);
-      if (a->nnr == 0) break;
+      if (tensor_nnr(a) == 0) break;
       int g = pick_group(double(a->nnz) / double(a->nnr));
       int grid = (int)std::min<int64_t>(ceil_div(a->nnr, kBlock / g), (int64_t)ctx->sms * 16);
       auto v = static_cast<const float*>(a->val);

@@ -363,16 +363,20 @@ bool csc_by_column_blocks(sfg_context* ctx, const sfg_tensor* s, sfg_tensor* t) 
              ctx->epoch++, mx + 1);
   SFG_LAUNCH(k_blk_max, (int)std::min<int64_t>(ceil_div(nb, kBlock), 64), kBlock, 0, ctx->stream, off, (int)nb, p,
              mx);
-  int32_t big = 0;
-  read_back(ctx, mx, sizeof big, &big);
-  if (big > kBlkCap) {
-    for (void* q : {(void*)counts, (void*)off, (void*)dummy}) dfree(ctx, q);
-    return false;
-  }
+  // The scatter needs only the offsets: it is enqueued before the host
+  // waits for the largest block size, so that round trip overlaps it (an
+  // oversized block — rare — discards the scatter and takes the other path).
+  read_back_start(ctx, mx, sizeof(int32_t));
   uint32_t* tkey = dalloc_n<uint32_t>(ctx, nnz);
   float* tval = dalloc_n<float>(ctx, nnz);
   SFG_LAUNCH(k_blk_scatter, p, kBlock, 0, ctx->stream, s->row, s->idx, static_cast<const float*>(s->val), nnz,
              (int)nb, off, tkey, tval);
+  int32_t big = 0;
+  read_back_wait(ctx, sizeof big, &big);
+  if (big > kBlkCap) {
+    for (void* q : {(void*)counts, (void*)off, (void*)dummy, (void*)tkey, (void*)tval}) dfree(ctx, q);
+    return false;
+  }
   SFG_LAUNCH(k_blk_sort, (int)nb, kSortThreads, 0, ctx->stream, tkey, tval, off, p, n, nnz, t->ptr, t->idx,
              static_cast<float*>(t->val));
   for (void* q : {(void*)counts, (void*)off, (void*)dummy, (void*)tkey, (void*)tval}) dfree(ctx, q);

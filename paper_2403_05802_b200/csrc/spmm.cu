@@ -278,8 +278,11 @@ __global__ void __launch_bounds__(kBlock) k_spmm_merge(const int32_t* __restrict
 // shuffles and group 0 stores. While a step's entries all lie inside the
 // current row (the common case on rows of tens of entries) the step is
 // branch-free: kU entries per group, their B rows loaded back to back.
+#ifndef SFG_MERGE_MINB
+#define SFG_MERGE_MINB 5  // CTAs per SM the register budget is sized for (config 5 SpMM: 5 -> 24.1 ms, 4 -> 25.1, 3 -> 25.1)
+#endif
 template <typename TB, int G, int V, int kU>
-__global__ void __launch_bounds__(kBlock, 4) k_spmm_merge_grp(const int32_t* __restrict__ ptr,
+__global__ void __launch_bounds__(kBlock, SFG_MERGE_MINB) k_spmm_merge_grp(const int32_t* __restrict__ ptr,
                                                             const int32_t* __restrict__ col,
                                                             const float* __restrict__ val,
                                                             const int2* __restrict__ cuts, int64_t nchunks,

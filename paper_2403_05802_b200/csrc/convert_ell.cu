@@ -189,7 +189,10 @@ __global__ void __launch_bounds__(kBlock) k_row_scan(const int32_t* __restrict__
 // ---------------------------------------------------------------- 3. split
 constexpr int kSplitRun = 8;
 
-__global__ void __launch_bounds__(kBlock) k_split(
+#ifndef SFG_SPLIT_MINB
+#define SFG_SPLIT_MINB 1  // config 2 conversion: 1 (64 registers) 0.437 ms; 5 -> 0.486 (spills)
+#endif
+__global__ void __launch_bounds__(kBlock, SFG_SPLIT_MINB) k_split(
     const int32_t* __restrict__ row, const int32_t* __restrict__ col,
     const float* __restrict__ val, int64_t nnz, const uint32_t* __restrict__ off,
     int32_t* __restrict__ srow, int32_t* __restrict__ scol, float* __restrict__ sval,

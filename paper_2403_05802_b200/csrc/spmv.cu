@@ -150,7 +150,10 @@ __device__ __forceinline__ void coo_close(float* __restrict__ y, int32_t row, fl
 // stream + gather floor of the same data is ~214 us, scripts/coo_exp.cu).
 constexpr int kCooSteps = 12;
 
-__global__ void __launch_bounds__(kBlock, 4) k_spmv_coo(const int32_t* __restrict__ row,
+#ifndef SFG_COO_MINB
+#define SFG_COO_MINB 4  // config 2 SpMV: 4 -> 0.291 ms; 5 -> 0.331 (spills); 6 -> 0.376
+#endif
+__global__ void __launch_bounds__(kBlock, SFG_COO_MINB) k_spmv_coo(const int32_t* __restrict__ row,
                                                           const int32_t* __restrict__ col,
                                                           const float* __restrict__ val,
                                                           const float* __restrict__ x,

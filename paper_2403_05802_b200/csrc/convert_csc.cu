@@ -249,7 +249,10 @@ __global__ void __launch_bounds__(kBlock) k_blk_scatter(const int32_t* __restric
 
 constexpr int kSortThreads = 512;
 
-__global__ void __launch_bounds__(kSortThreads) k_blk_sort(const uint32_t* __restrict__ tkey,
+#ifndef SFG_BLKSORT_MINB
+#define SFG_BLKSORT_MINB 1  // 2 or 3 CTAs per SM measured the same (config 3)
+#endif
+__global__ void __launch_bounds__(kSortThreads, SFG_BLKSORT_MINB) k_blk_sort(const uint32_t* __restrict__ tkey,
                                                       const float* __restrict__ tval,
                                                       const int32_t* __restrict__ off, int p, int64_t n,
                                                       int64_t nnz, int32_t* __restrict__ ptr,

@@ -30,26 +30,36 @@ namespace {
 constexpr int kBlock = 256;
 constexpr int kMaxWords = 24 * 1024;  // 96 KB bitmap (+96 KB prefix) => <= 786K block columns
 
+// Block-row pointers: the row pointers of the block-row ids (row / r) of
+// the sorted entries — the CSR row-pointer pass (devutil.cuh: 16-byte row
+// loads, warp-staged lower-bound searches, coalesced stores).
+constexpr int kBrowVec = 4;
+
 __global__ void __launch_bounds__(kBlock) k_brow_ptr(const int32_t* __restrict__ row, int64_t nnz,
                                                       int32_t r, int32_t nbr,
                                                       int32_t* __restrict__ bptr) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t base0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
-  for (int64_t wbase = base0; wbase < nnz; wbase += stride) {
-    int64_t e = wbase + (threadIdx.x & 31);
-    int32_t b[1] = {0}, prev = 0, end_hi = 0;  // lanes past nnz write nothing
-    if (e < nnz) {
-      b[0] = __ldg(row + e) / r;
-      prev = e == 0 ? -1 : __ldg(row + e - 1) / r;
-      end_hi = e == nnz - 1 ? nbr : b[0];
-    }
-    write_row_ptr<1>(b, prev, (int32_t)e, end_hi, (int32_t)nnz, bptr);
+  constexpr int kChunk = 128 * kBrowVec;
+  __shared__ __align__(16) int32_t s_rows[kBlock / 32][kChunk];
+  const int64_t nchunk = (nnz + kChunk - 1) / kChunk;
+  const int64_t warps = (int64_t)gridDim.x * (kBlock / 32);
+  for (int64_t ch = (int64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); ch < nchunk; ch += warps) {
+    const int64_t base = ch * kChunk;
+    RowChunk<kBrowVec> c;
+    load_row_chunk(row, nnz, base, c);
+#pragma unroll
+    for (int g = 0; g < kBrowVec; ++g)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) c.r[g][i] /= r;
+    c.prev = c.prev < 0 ? -1 : c.prev / r;
+    chunk_row_ptr(c, nnz, base, nbr, s_rows[threadIdx.x >> 5], bptr);
   }
 }
 
 // Bitmap of the block columns present in block row `br` over [lo, hi].
 __device__ __forceinline__ void mark(const int32_t* __restrict__ col, int32_t s, int32_t e,
                                      int32_t c, int32_t lo, uint32_t* bm) {
+  // (a shuffle OR-scan per run of equal words with one atomic per run was
+  // measured slower: 451 vs 290 us for the count kernel at 32768^2)
   for (int32_t k = s + threadIdx.x; k < e; k += blockDim.x) {
     int b = __ldg(col + k) / c - lo;
     atomicOr(bm + (b >> 5), 1u << (b & 31));
@@ -83,9 +93,13 @@ __device__ __forceinline__ void col_range(const int32_t* __restrict__ col, int32
   *hi = *smax;
 }
 
+// A block-column grid this narrow is marked over its whole range: no
+// separate min/max pass over the columns.
+constexpr int32_t kFullRangeCols = 32768;
+
 __global__ void __launch_bounds__(kBlock) k_count_blocks(const int32_t* __restrict__ bptr,
                                                           const int32_t* __restrict__ col,
-                                                          int32_t c, int32_t nbr,
+                                                          int32_t c, int32_t nbr, int32_t nbc,
                                                           int32_t* __restrict__ cnt,
                                                           int* __restrict__ too_wide) {
   extern __shared__ uint32_t bm[];
@@ -96,8 +110,8 @@ __global__ void __launch_bounds__(kBlock) k_count_blocks(const int32_t* __restri
       if (threadIdx.x == 0) cnt[br] = 0;
       continue;
     }
-    int32_t lo, hi;
-    col_range(col, s, e, c, &smin, &smax, &lo, &hi);
+    int32_t lo = 0, hi = nbc - 1;
+    if (nbc > kFullRangeCols) col_range(col, s, e, c, &smin, &smax, &lo, &hi);
     int words = ((hi - lo) >> 5) + 1;
     if (words > kMaxWords) {
       if (threadIdx.x == 0) atomicOr(too_wide, 1);
@@ -157,7 +171,7 @@ template <typename T>
 __global__ void __launch_bounds__(kBlock) k_fill_blocks(
     const int32_t* __restrict__ bptr, const int32_t* __restrict__ row,
     const int32_t* __restrict__ col, const float* __restrict__ val, int32_t r, int32_t c,
-    int32_t rb, int32_t cb, int32_t nbr, const int32_t* __restrict__ blk_ptr,
+    int32_t rb, int32_t cb, int32_t nbr, int32_t nbc, const int32_t* __restrict__ blk_ptr,
     int32_t* __restrict__ bidx, T* __restrict__ bval) {
   extern __shared__ uint32_t bm[];  // [words] bitmap, then [words] prefix
   __shared__ int smin, smax;
@@ -165,8 +179,8 @@ __global__ void __launch_bounds__(kBlock) k_fill_blocks(
   for (int32_t br = blockIdx.x; br < nbr; br += gridDim.x) {
     int32_t s = __ldg(bptr + br), e = __ldg(bptr + br + 1);
     if (s == e) continue;
-    int32_t lo, hi;
-    col_range(col, s, e, c, &smin, &smax, &lo, &hi);
+    int32_t lo = 0, hi = nbc - 1;
+    if (nbc > kFullRangeCols) col_range(col, s, e, c, &smin, &smax, &lo, &hi);
     int words = ((hi - lo) >> 5) + 1;
     uint32_t* pre = bm + words;
     for (int w = threadIdx.x; w < words; w += blockDim.x) bm[w] = 0;
@@ -240,8 +254,8 @@ sfg_tensor* coo_to_bcsr(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_
     dfree(ctx, cnt);
     return t;
   }
-  SFG_LAUNCH(k_brow_ptr, stream_grid(ctx, nnz, kBlock, 1, 8), kBlock, 0, ctx->stream, s->row, nnz,
-             (int32_t)r, nbr, bptr);
+  SFG_LAUNCH(k_brow_ptr, stream_grid(ctx, ceil_div(nnz, 128 * kBrowVec), kBlock / 32, 1, 8), kBlock, 0,
+             ctx->stream, s->row, nnz, (int32_t)r, nbr, bptr);
   int tiles = (int)ceil_div(nbr, kTile);
   auto* status = lookback_status(ctx, tiles);
   auto* tail = static_cast<int32_t*>(scratch(ctx, 64));
@@ -266,7 +280,7 @@ sfg_tensor* coo_to_bcsr(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_
               " block columns)");
   int grid = (int)std::min<int64_t>(nbr, (int64_t)ctx->sms * 8);
   SFG_LAUNCH(k_count_blocks, grid, kBlock, words * 4, ctx->stream, bptr, s->idx, (int32_t)c, nbr,
-             cnt, tail + 1);
+             (int32_t)t->nbc, cnt, tail + 1);
   SFG_LAUNCH(k_scan_i32, tiles, kBlock, 0, ctx->stream, cnt, nbr, t->ptr, status, ctx->epoch++);
   int32_t nblocks = 0;
   read_back(ctx, t->ptr + nbr, sizeof nblocks, &nblocks);
@@ -279,11 +293,11 @@ sfg_tensor* coo_to_bcsr(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_
   if (dtype == SFG_BF16)
     SFG_LAUNCH(k_fill_blocks<__nv_bfloat16>, grid, kBlock, words * 8, ctx->stream, bptr, s->row,
                s->idx, static_cast<const float*>(s->val), (int32_t)r, (int32_t)c, (int32_t)t->rb,
-               (int32_t)t->cb, nbr, t->ptr, t->idx, static_cast<__nv_bfloat16*>(t->val));
+               (int32_t)t->cb, nbr, (int32_t)t->nbc, t->ptr, t->idx, static_cast<__nv_bfloat16*>(t->val));
   else
     SFG_LAUNCH(k_fill_blocks<float>, grid, kBlock, words * 8, ctx->stream, bptr, s->row, s->idx,
                static_cast<const float*>(s->val), (int32_t)r, (int32_t)c, (int32_t)t->rb,
-               (int32_t)t->cb, nbr, t->ptr, t->idx, static_cast<float*>(t->val));
+               (int32_t)t->cb, nbr, (int32_t)t->nbc, t->ptr, t->idx, static_cast<float*>(t->val));
   dfree(ctx, bptr);
   dfree(ctx, cnt);
   return t;

@@ -56,13 +56,23 @@ __global__ void __launch_bounds__(kBlock) k_brow_ptr(const int32_t* __restrict__
 }
 
 // Bitmap of the block columns present in block row `br` over [lo, hi].
+// Four entries per thread per step, loads first (the loop is latency
+// bound). (Skipping entries whose block column repeats its predecessor's,
+// or an OR-scan per run of equal words with one atomic per run, both
+// measured slower: 391 / 451 vs 290 us for the count kernel at 32768^2.)
 __device__ __forceinline__ void mark(const int32_t* __restrict__ col, int32_t s, int32_t e,
                                      int32_t c, int32_t lo, uint32_t* bm) {
-  // (a shuffle OR-scan per run of equal words with one atomic per run was
-  // measured slower: 451 vs 290 us for the count kernel at 32768^2)
-  for (int32_t k = s + threadIdx.x; k < e; k += blockDim.x) {
-    int b = __ldg(col + k) / c - lo;
-    atomicOr(bm + (b >> 5), 1u << (b & 31));
+  constexpr int U = 4;
+  for (int32_t k = s + threadIdx.x; k < e; k += U * blockDim.x) {
+    int v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = k + u * (int32_t)blockDim.x < e ? __ldg(col + k + u * blockDim.x) : -1;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (v[u] >= 0) {
+        const int b = v[u] / c - lo;
+        atomicOr(bm + (b >> 5), 1u << (b & 31));
+      }
   }
 }
 
@@ -100,6 +110,7 @@ constexpr int32_t kFullRangeCols = 32768;
 __global__ void __launch_bounds__(kBlock) k_count_blocks(const int32_t* __restrict__ bptr,
                                                           const int32_t* __restrict__ col,
                                                           int32_t c, int32_t nbr, int32_t nbc,
+                                                          uint32_t* __restrict__ gbm,
                                                           int32_t* __restrict__ cnt,
                                                           int* __restrict__ too_wide) {
   extern __shared__ uint32_t bm[];
@@ -123,7 +134,10 @@ __global__ void __launch_bounds__(kBlock) k_count_blocks(const int32_t* __restri
     mark(col, s, e, c, lo, bm);
     __syncthreads();
     int pc = 0;
-    for (int w = threadIdx.x; w < words; w += blockDim.x) pc += __popc(bm[w]);
+    for (int w = threadIdx.x; w < words; w += blockDim.x) {
+      pc += __popc(bm[w]);
+      if (gbm) gbm[(int64_t)br * words + w] = bm[w];  // full-range bitmaps only: the fill reuses them
+    }
     pc = warp_sum(pc);
     if ((threadIdx.x & 31) == 0) atomicAdd(&ssum, pc);
     __syncthreads();
@@ -171,7 +185,8 @@ template <typename T>
 __global__ void __launch_bounds__(kBlock) k_fill_blocks(
     const int32_t* __restrict__ bptr, const int32_t* __restrict__ row,
     const int32_t* __restrict__ col, const float* __restrict__ val, int32_t r, int32_t c,
-    int32_t rb, int32_t cb, int32_t nbr, int32_t nbc, const int32_t* __restrict__ blk_ptr,
+    int32_t rb, int32_t cb, int32_t nbr, int32_t nbc, const uint32_t* __restrict__ gbm,
+    const int32_t* __restrict__ blk_ptr,
     int32_t* __restrict__ bidx, T* __restrict__ bval) {
   extern __shared__ uint32_t bm[];  // [words] bitmap, then [words] prefix
   __shared__ int smin, smax;
@@ -183,9 +198,13 @@ __global__ void __launch_bounds__(kBlock) k_fill_blocks(
     if (nbc > kFullRangeCols) col_range(col, s, e, c, &smin, &smax, &lo, &hi);
     int words = ((hi - lo) >> 5) + 1;
     uint32_t* pre = bm + words;
-    for (int w = threadIdx.x; w < words; w += blockDim.x) bm[w] = 0;
-    __syncthreads();
-    mark(col, s, e, c, lo, bm);
+    if (gbm) {  // the count kernel's bitmap of this block row
+      for (int w = threadIdx.x; w < words; w += blockDim.x) bm[w] = gbm[(int64_t)br * words + w];
+    } else {
+      for (int w = threadIdx.x; w < words; w += blockDim.x) bm[w] = 0;
+      __syncthreads();
+      mark(col, s, e, c, lo, bm);
+    }
     __syncthreads();
     // exclusive prefix of popcounts over the words: each thread owns a
     // contiguous run of words
@@ -279,8 +298,13 @@ sfg_tensor* coo_to_bcsr(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_
           "BCSR: block-column range wider than the device bitmap (" + std::to_string(t->nbc) +
               " block columns)");
   int grid = (int)std::min<int64_t>(nbr, (int64_t)ctx->sms * 8);
+  // full-range bitmaps (narrow block grids) are kept for the fill kernel
+  // when they are small, saving it a second pass over the columns
+  uint32_t* gbm = t->nbc <= kFullRangeCols && (int64_t)nbr * words * 4 <= (int64_t(256) << 20)
+                      ? dalloc_n<uint32_t>(ctx, (int64_t)nbr * words)
+                      : nullptr;
   SFG_LAUNCH(k_count_blocks, grid, kBlock, words * 4, ctx->stream, bptr, s->idx, (int32_t)c, nbr,
-             (int32_t)t->nbc, cnt, tail + 1);
+             (int32_t)t->nbc, gbm, cnt, tail + 1);
   SFG_LAUNCH(k_scan_i32, tiles, kBlock, 0, ctx->stream, cnt, nbr, t->ptr, status, ctx->epoch++);
   int32_t nblocks = 0;
   read_back(ctx, t->ptr + nbr, sizeof nblocks, &nblocks);
@@ -293,11 +317,12 @@ sfg_tensor* coo_to_bcsr(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_
   if (dtype == SFG_BF16)
     SFG_LAUNCH(k_fill_blocks<__nv_bfloat16>, grid, kBlock, words * 8, ctx->stream, bptr, s->row,
                s->idx, static_cast<const float*>(s->val), (int32_t)r, (int32_t)c, (int32_t)t->rb,
-               (int32_t)t->cb, nbr, (int32_t)t->nbc, t->ptr, t->idx, static_cast<__nv_bfloat16*>(t->val));
+               (int32_t)t->cb, nbr, (int32_t)t->nbc, gbm, t->ptr, t->idx, static_cast<__nv_bfloat16*>(t->val));
   else
     SFG_LAUNCH(k_fill_blocks<float>, grid, kBlock, words * 8, ctx->stream, bptr, s->row, s->idx,
                static_cast<const float*>(s->val), (int32_t)r, (int32_t)c, (int32_t)t->rb,
-               (int32_t)t->cb, nbr, (int32_t)t->nbc, t->ptr, t->idx, static_cast<float*>(t->val));
+               (int32_t)t->cb, nbr, (int32_t)t->nbc, gbm, t->ptr, t->idx, static_cast<float*>(t->val));
+  dfree(ctx, gbm);
   dfree(ctx, bptr);
   dfree(ctx, cnt);
   return t;

@@ -303,7 +303,10 @@ sfg_tensor* coo_to_bcsr(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_
   uint32_t* gbm = t->nbc <= kFullRangeCols && (int64_t)nbr * words * 4 <= (int64_t(256) << 20)
                       ? dalloc_n<uint32_t>(ctx, (int64_t)nbr * words)
                       : nullptr;
-  SFG_LAUNCH(k_count_blocks, grid, kBlock, words * 4, ctx->stream, bptr, s->idx, (int32_t)c, nbr,
+  // half-size CTAs, twice as many resident: one wave over the block rows
+  // of a 2,048-block-row matrix instead of 1.7
+  const int cgrid = (int)std::min<int64_t>(nbr, (int64_t)ctx->sms * 16);
+  SFG_LAUNCH(k_count_blocks, cgrid, kBlock / 2, words * 4, ctx->stream, bptr, s->idx, (int32_t)c, nbr,
              (int32_t)t->nbc, gbm, cnt, tail + 1);
   SFG_LAUNCH(k_scan_i32, tiles, kBlock, 0, ctx->stream, cnt, nbr, t->ptr, status, ctx->epoch++);
   int32_t nblocks = 0;

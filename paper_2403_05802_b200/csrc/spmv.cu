@@ -297,7 +297,9 @@ void spmv_csr(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, b
   if (a->m == 0) return;
   int g = pick_group(a->m ? double(a->nnz) / double(a->m) : 0);
   const int R = 4;
-  int grid = (int)std::min<int64_t>(ceil_div(a->m, (int64_t)(kBlock / g) * R), (int64_t)ctx->sms * 16);
+  // up to 32 CTAs per SM worth of row groups: config 1 SpMV 0.094 -> 0.088 ms
+  // against a cap of 16 (64: 0.090)
+  int grid = (int)std::min<int64_t>(ceil_div(a->m, (int64_t)(kBlock / g) * R), (int64_t)ctx->sms * 32);
   if (grid < 1) grid = 1;
   auto v = static_cast<const float*>(a->val);
   switch (g) {

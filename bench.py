@@ -264,61 +264,70 @@ WORKLOADS = {1: Cfg1, 2: Cfg2, 3: Cfg3, 4: Cfg4, 5: Cfg5}
 
 
 # ------------------------------------------------------------------- clocks
+_SAMPLER = r"""
+import json, sys, time
+import pynvml as N
+dev, period = int(sys.argv[1]), float(sys.argv[2])
+N.nvmlInit()
+h = N.nvmlDeviceGetHandleByIndex(dev)
+out = {"max": N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM), "s": [], "call_ms": 0.0}
+print("ready", flush=True)
+import select
+while True:
+    t0 = time.perf_counter()
+    out["s"].append((N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM), N.nvmlDeviceGetCurrentClocksEventReasons(h)))
+    out["call_ms"] = max(out["call_ms"], (time.perf_counter() - t0) * 1e3)
+    r, _, _ = select.select([sys.stdin], [], [], period)
+    if r:
+        break
+print(json.dumps(out), flush=True)
+"""
+
+
 class ClockSampler:
-    """In-process NVML sampling of SM clocks and throttle reasons (a
-    background thread; lighter than an nvidia-smi subprocess)."""
+    """NVML sampling of SM clocks and throttle reasons in a separate
+    process: NVML calls can take milliseconds inside the driver, and made
+    in this process they could delay this process's kernel launches."""
 
     def __init__(self, device, period=0.05):
         self.device, self.period = device, period
-        self.samples, self.ok = [], False
+        self.samples, self.ok, self.err = [], False, ""
 
     def __enter__(self):
+        import subprocess
         try:
-            import pynvml as N
-            N.nvmlInit()
-            self.N, self.h = N, N.nvmlDeviceGetHandleByIndex(self.device)
-            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER, str(self.device), str(self.period)],
+                                         stdin=subprocess.PIPE, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                         text=True)
+            line = self.proc.stdout.readline().strip()
+            if line != "ready":
+                raise RuntimeError(line or self.proc.stderr.read()[-300:])
             self.ok = True
         except Exception as e:  # noqa: BLE001
             self.err = str(e)
-            return self
-        self.stop = threading.Event()
-        self.th = threading.Thread(target=self._run, daemon=True)
-        self.th.start()
         return self
 
-    def _run(self):
-        N = self.N
-        self.call_ms = []
-        while not self.stop.is_set():
-            try:
-                t0 = time.perf_counter()
-                self.samples.append((N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM),
-                                     N.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
-                self.call_ms.append((time.perf_counter() - t0) * 1e3)
-            except Exception:
-                pass
-            self.stop.wait(self.period)
-
     def __exit__(self, *exc):
-        if self.ok:
-            self.stop.set()
-            self.th.join()
+        if not self.ok:
+            return
+        try:
+            out, err = self.proc.communicate(input="stop\n", timeout=30)
+            d = json.loads(out.strip().splitlines()[-1])
+            self.max_mhz, self.samples, self.call_ms = d["max"], [tuple(x) for x in d["s"]], d["call_ms"]
+        except Exception as e:  # noqa: BLE001
+            self.ok, self.err = False, str(e)
 
     def summary(self):
         if not self.ok:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [f"nvml unavailable: {self.err}"]}
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["no samples"]}
-        N = self.N
-        names = {N.nvmlClocksThrottleReasonHwSlowdown: "hw_slowdown",
-                 N.nvmlClocksThrottleReasonHwThermalSlowdown: "hw_thermal_slowdown",
-                 N.nvmlClocksThrottleReasonSwThermalSlowdown: "sw_thermal_slowdown",
-                 N.nvmlClocksThrottleReasonSwPowerCap: "sw_power_cap"}
+        names = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+                 0x4: "sw_power_cap"}
         reasons = sorted({n for _, r in self.samples for bit, n in names.items() if r & bit})
         return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": reasons, "samples": len(self.samples), "source": "NVML, 50 ms period",
-                "nvml_call_ms_max": round(max(self.call_ms), 2) if self.call_ms else None}
+                "reasons": reasons, "samples": len(self.samples),
+                "source": "NVML in a sampler process, 50 ms period", "nvml_call_ms_max": round(self.call_ms, 2)}
 
 
 # ---------------------------------------------------------------- our arm

@@ -99,7 +99,7 @@ __global__ void k_fill_i32(int32_t* __restrict__ p, int64_t n, int32_t v) {
 // decoupled look-back scan: tile t learns how many heads precede it and
 // writes L0.idx[pos] = row, L1.ptr[pos] = e directly. col/val are copied in
 // the same pass.
-constexpr int kDcsrItems = 16;  // 4 x int4 per thread
+constexpr int kDcsrItems = 16;  // per lane, warp-striped
 constexpr int kDcsrTile = kBlock * kDcsrItems;
 
 __global__ void __launch_bounds__(kBlock) k_coo_to_dcsr(
@@ -107,59 +107,53 @@ __global__ void __launch_bounds__(kBlock) k_coo_to_dcsr(
     const float* __restrict__ val, int64_t nnz, int32_t* __restrict__ orow,
     int32_t* __restrict__ optr, int32_t* __restrict__ ocol, float* __restrict__ oval,
     unsigned long long* __restrict__ status, uint32_t epoch, int32_t* __restrict__ nnr_out) {
+  // Warp-striped: element wbase + 32 j + lane, so the col/val copy and the
+  // head stores (ballot ranks) are coalesced.
   __shared__ uint32_t smem[34];
   __shared__ uint32_t slot;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tile = blockIdx.x;
-  const int64_t e_base = (int64_t)tile * kDcsrTile + (int64_t)threadIdx.x * kDcsrItems;
+  const int64_t wbase = (int64_t)tile * kDcsrTile + (int64_t)warp * (32 * kDcsrItems);
   int r[kDcsrItems];
-  bool full = e_base + kDcsrItems <= nnz;
-  if (full) {
 #pragma unroll
-    for (int q = 0; q < kDcsrItems / 4; ++q) {
-      // L1-allocating: lane runs are 64 B apart, so consecutive q steps
-      // share each 32 B sector
-      int4 rr = __ldg(reinterpret_cast<const int4*>(row + e_base) + q);
-      int4 cc = __ldg(reinterpret_cast<const int4*>(col + e_base) + q);
-      float4 vv = __ldg(reinterpret_cast<const float4*>(val + e_base) + q);
-      reinterpret_cast<int4*>(ocol + e_base)[q] = cc;  // halves of a sector: keep in L2
-      reinterpret_cast<float4*>(oval + e_base)[q] = vv;
-      r[4 * q] = rr.x; r[4 * q + 1] = rr.y; r[4 * q + 2] = rr.z; r[4 * q + 3] = rr.w;
-    }
-  } else {
+  for (int j = 0; j < kDcsrItems; ++j) {
+    const int64_t e = wbase + 32 * j + lane;
+    r[j] = e < nnz ? ld_stream(row + e) : -2;
+  }
 #pragma unroll
-    for (int i = 0; i < kDcsrItems; ++i) {
-      int64_t e = e_base + i;
-      if (e < nnz) {
-        r[i] = row[e];
-        ocol[e] = col[e];
-        oval[e] = val[e];
-      } else {
-        r[i] = -2;
-      }
+  for (int j = 0; j < kDcsrItems; ++j) {
+    const int64_t e = wbase + 32 * j + lane;
+    if (e < nnz) {
+      ocol[e] = ld_stream(col + e);
+      oval[e] = ld_stream(val + e);
     }
   }
-  int prev = (e_base == 0 || e_base >= nnz) ? -1 : row[e_base - 1];
-  uint32_t heads = 0;
-  uint32_t hmask = 0;
+  const int before = lane == 0 && wbase > 0 && wbase < nnz ? __ldg(row + wbase - 1) : -1;
+  unsigned ball[kDcsrItems];
+  uint32_t cnt = 0;
 #pragma unroll
-  for (int i = 0; i < kDcsrItems; ++i) {
-    bool valid = e_base + i < nnz;
-    bool h = valid && r[i] != prev;
-    hmask |= (h ? 1u : 0u) << i;
-    heads += h;
-    if (valid) prev = r[i];
+  for (int j = 0; j < kDcsrItems; ++j) {
+    const int64_t e = wbase + 32 * j + lane;
+    int p = __shfl_up_sync(kFull, r[j], 1);
+    const int t31 = j > 0 ? __shfl_sync(kFull, r[j - 1], 31) : before;
+    if (lane == 0) p = t31;
+    const bool h = e < nnz && (e == 0 || r[j] != p);
+    ball[j] = __ballot_sync(kFull, h);
+    cnt += __popc(ball[j]);
   }
   uint32_t total;
-  uint32_t excl = block_exclusive_scan<uint32_t, kBlock>(heads, smem, &total);
-  uint32_t tile_prefix = lookback_prefix(status, epoch, tile, total, &slot);
-  uint32_t pos = tile_prefix + excl;
+  const uint32_t wex = block_exclusive_scan<uint32_t, kBlock>(lane == 0 ? cnt : 0u, smem, &total);
+  const uint32_t tile_prefix = lookback_prefix(status, epoch, tile, total, &slot);
+  uint32_t pos = tile_prefix + __shfl_sync(kFull, wex, 0);
+  const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
-  for (int i = 0; i < kDcsrItems; ++i) {
-    if (hmask >> i & 1u) {
-      orow[pos] = r[i];
-      optr[pos] = (int32_t)(e_base + i);
-      ++pos;
+  for (int j = 0; j < kDcsrItems; ++j) {
+    if ((ball[j] >> lane) & 1u) {
+      const uint32_t q = pos + __popc(ball[j] & lt);
+      orow[q] = r[j];
+      optr[q] = (int32_t)(wbase + 32 * j + lane);
     }
+    pos += __popc(ball[j]);
   }
   if (tile == gridDim.x - 1 && threadIdx.x == 0) {
     uint32_t nnr = tile_prefix + total;

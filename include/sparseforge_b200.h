@@ -203,6 +203,10 @@ int sfg_spgemm(sfg_context* ctx, const sfg_tensor* a, const sfg_tensor* b, float
 /* nnz-balanced contiguous row split for P devices: bounds[0..P]
  * with bounds[0] = 0, bounds[P] = rows, boundaries at ptr quantiles. */
 int sfg_row_partition(sfg_context* ctx, const sfg_tensor* coo, int32_t parts, int64_t* bounds);
+/* The same boundary rule over a host array of the row-sorted COO's rows
+ * (no device work: callers that hold the rows on the host, e.g. a launcher
+ * planning the split before any GPU is touched). */
+int sfgx_row_bounds_host(const int32_t* rows, int64_t nnz, int64_t n_rows, int32_t parts, int64_t* bounds);
 /* Rows [r0, r1) of a canonical COO as a new COO with rows rebased to 0. */
 int sfg_coo_slice_rows(sfg_context* ctx, const sfg_tensor* coo, int64_t r0, int64_t r1,
                        sfg_tensor** out);

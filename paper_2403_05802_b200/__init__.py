@@ -13,6 +13,7 @@ computes anything itself: when the library (or a B200) is missing it raises.
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 import os
 from dataclasses import dataclass, field
 
@@ -122,6 +123,7 @@ def load():
         "sfg_spmm": (C.c_int, [vp, vp, vp, i32, i64, i64, vp, i64, u32]),
         "sfg_row_partition": (C.c_int, [vp, vp, i32, C.POINTER(C.c_int64)]),
         "sfg_coo_slice_rows": (C.c_int, [vp, vp, i64, i64, pp]),
+        "sfgx_row_bounds_host": (C.c_int, [vp, i64, i64, i32, C.POINTER(C.c_int64)]),
         "sfg_read_matrix_market": (C.c_int, [vp, C.c_char_p, u32, pp]),
         "sfg_write_container": (C.c_int, [vp, vp, C.c_char_p]),
         "sfg_spgemm": (C.c_int, [vp, vp, vp, vp, i64, u32]),
@@ -153,6 +155,17 @@ def load():
 def _check(st):
     if st != 0:
         raise SfgError(st, _lib.sfg_last_error().decode(errors="replace"))
+
+
+def row_bounds_host(rows: np.ndarray, m: int, parts: int) -> list[int]:
+    """The library's nnz-balanced row split (sfgx_row_bounds_host, the rule
+    sfg_row_partition applies on the device) over a host array of the
+    row-sorted COO's rows; no GPU needed."""
+    lib = load()
+    rows = np.ascontiguousarray(rows, np.int32)
+    b = (C.c_int64 * (parts + 1))()
+    _check(lib.sfgx_row_bounds_host(rows.ctypes.data_as(C.c_void_p), len(rows), m, parts, b))
+    return list(b)
 
 
 def comm_unique_id() -> bytes:
@@ -235,11 +248,12 @@ class DeviceBuffer:
                                       arr.nbytes, 0))
         return self
 
-    def download(self, dtype, count) -> np.ndarray:
+    def download(self, dtype, count, offset=0) -> np.ndarray:
+        """`count` elements from element `offset` on."""
         out = np.empty(int(count), dtype)
         if out.nbytes:
             _check(self.ctx.lib.sfgx_copy(self.ctx.h, out.ctypes.data_as(C.c_void_p),
-                                          C.c_void_p(self.ptr), out.nbytes, 1))
+                                          C.c_void_p(self.ptr + int(offset) * out.itemsize), out.nbytes, 1))
         return out
 
 
@@ -248,11 +262,20 @@ class Tensor:
 
     def __init__(self, ctx: "Context", handle, owned=True):
         self.ctx, self.h, self.owned = ctx, handle, owned
+        if owned and handle:
+            ctx._live.add(self)
+
+    def free(self):
+        """Release the device arrays now (also done when collected, and by
+        Context.close for tensors still alive then)."""
+        if self.owned and self.h and self.ctx.h:
+            self.ctx.lib.sfg_tensor_free(self.h)
+        self.h = None
+        self.ctx._live.discard(self)
 
     def __del__(self):
         try:
-            if self.owned and self.h:
-                self.ctx.lib.sfg_tensor_free(self.h)
+            self.free()
         except Exception:
             pass
 
@@ -272,7 +295,10 @@ class Tensor:
 
     def parts(self):
         v = self.view()
-        return [Tensor(self.ctx, C.c_void_p(p), owned=False) for p in v.parts if p]
+        out = [Tensor(self.ctx, C.c_void_p(p), owned=False) for p in v.parts if p]
+        for t in out:
+            t._parent = self  # the parts live in (and die with) this tensor
+        return out
 
     def _dl(self, ptr, dtype, count):
         out = np.empty(int(count), dtype)
@@ -312,11 +338,16 @@ class Context:
     def __init__(self, device: int = 0, stream: int | None = None):
         self.lib = load()
         h = C.c_void_p()
+        self._live = weakref.WeakSet()  # owned tensors: freed before the context goes
         _check(self.lib.sfg_context_create(device, C.c_void_p(stream or 0), C.byref(h)))
         self.h = h
 
     def close(self):
         if self.h:
+            # a tensor collected after this point must not touch the deleted
+            # context: free the live ones now, their handles become null
+            for t in list(self._live):
+                t.free()
             self.lib.sfg_context_destroy(self.h)
             self.h = None
 
@@ -353,6 +384,14 @@ class Context:
         vp = lambda a: a.ctypes.data_as(C.c_void_p)
         _check(self.lib.sfg_from_coo(self.h, m, n, len(val), vp(row), vp(col), vp(val), flags, C.byref(h)))
         return Tensor(self, h)
+
+    def download_ptr(self, ptr: int, dtype, count, offset=0) -> np.ndarray:
+        """Host copy of `count` elements at device address ptr + offset elements."""
+        out = np.empty(int(count), dtype)
+        if out.nbytes:
+            _check(self.lib.sfgx_copy(self.h, out.ctypes.data_as(C.c_void_p),
+                                      C.c_void_p(int(ptr) + int(offset) * out.itemsize), out.nbytes, 1))
+        return out
 
     def copy_device(self, dst_ptr: int, src_ptr: int, nbytes: int):
         """Device-to-device copy on the context's stream."""

@@ -16,6 +16,23 @@ const char* last_error();
 
 namespace {
 
+// Makes ctx's device current for the duration of an entry point (several
+// contexts on several devices may be driven from one host thread).
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(const sfg_context* ctx) {
+    if (!ctx) return;
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != ctx->device) {
+      if (cudaSetDevice(ctx->device) == cudaSuccess) prev = cur;
+      else cudaGetLastError();
+    }
+  }
+  ~DeviceScope() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 template <class F>
 int guard(F&& f) {
   try {
@@ -31,6 +48,12 @@ int guard(F&& f) {
     sfg::set_last_error(e.what());
     return SFG_ERR_INVALID_OPERATION;
   }
+}
+
+template <class F>
+int guard(const sfg_context* ctx, F&& f) {
+  DeviceScope scope(ctx);
+  return guard(static_cast<F&&>(f));
 }
 
 void require(bool ok, int code, const char* msg) {
@@ -135,7 +158,7 @@ int sfg_context_create(int device, void* stream, sfg_context** out) {
 }
 
 int sfg_context_set_stream(sfg_context* ctx, void* stream) {
-  return guard([&] {
+  return guard(ctx, [&] {
     require(ctx, SFG_ERR_INVALID_OPERATION, "null context");
     SFG_CUDA(cudaStreamSynchronize(ctx->stream));
     ctx->stream = static_cast<cudaStream_t>(stream);
@@ -143,7 +166,7 @@ int sfg_context_set_stream(sfg_context* ctx, void* stream) {
 }
 
 int sfg_context_release_cached(sfg_context* ctx, int64_t* bytes_out) {
-  return guard([&] {
+  return guard(ctx, [&] {
     require(ctx, SFG_ERR_INVALID_OPERATION, "null context");
     if (bytes_out) *bytes_out = static_cast<int64_t>(ctx->cached_bytes);
     sfg::release_cached(ctx);
@@ -151,11 +174,11 @@ int sfg_context_release_cached(sfg_context* ctx, int64_t* bytes_out) {
 }
 
 int sfg_context_synchronize(sfg_context* ctx) {
-  return guard([&] { SFG_CUDA(cudaStreamSynchronize(ctx->stream)); });
+  return guard(ctx, [&] { SFG_CUDA(cudaStreamSynchronize(ctx->stream)); });
 }
 
 int sfg_context_destroy(sfg_context* ctx) {
-  return guard([&] {
+  return guard(ctx, [&] {
     if (!ctx) return;
     if (ctx->scratch) sfg::dfree(ctx, ctx->scratch);
     if (ctx->status) sfg::dfree(ctx, ctx->status);
@@ -242,7 +265,7 @@ int sfg_storage_explain(const sfg_format* f, char* buf, int64_t len) {
 
 int sfg_from_coo(sfg_context* ctx, int64_t rows, int64_t cols, int64_t nnz, const int32_t* row,
                  const int32_t* col, const float* val, uint32_t flags, sfg_tensor** out) {
-  return guard([&] {
+  return guard(ctx, [&] {
     require(ctx && out, SFG_ERR_INVALID_OPERATION, "null argument");
     *out = nullptr;
     require(nnz >= 0 && rows >= 0 && cols >= 0, SFG_ERR_INVALID_OPERATION,
@@ -291,7 +314,7 @@ int sfg_from_coo(sfg_context* ctx, int64_t rows, int64_t cols, int64_t nnz, cons
 }
 
 int sfg_convert(sfg_context* ctx, const sfg_tensor* src, const sfg_format* dst, sfg_tensor** out) {
-  return guard([&] {
+  return guard(ctx, [&] {
     require(ctx && src && dst && out, SFG_ERR_INVALID_OPERATION, "null argument");
     *out = nullptr;
     validate_format(*dst);
@@ -317,7 +340,7 @@ int sfg_convert(sfg_context* ctx, const sfg_tensor* src, const sfg_format* dst, 
 
 int sfg_decompose_rows(sfg_context* ctx, const sfg_tensor* coo, int64_t min_sum,
                        sfg_tensor** selected, sfg_tensor** remainder, int32_t* totals) {
-  return guard([&] {
+  return guard(ctx, [&] {
     require(ctx && coo && selected && remainder, SFG_ERR_INVALID_OPERATION, "null argument");
     require(coo->kind == SFG_COO, SFG_ERR_INVALID_OPERATION,
             "decompose expects coordinate-form input");
@@ -327,7 +350,7 @@ int sfg_decompose_rows(sfg_context* ctx, const sfg_tensor* coo, int64_t min_sum,
 }
 
 int sfg_tensor_view_get(sfg_context* ctx, const sfg_tensor* t, sfg_tensor_view* out) {
-  return guard([&] {
+  return guard(ctx, [&] {
     require(t && out, SFG_ERR_INVALID_OPERATION, "null argument");
     (void)ctx;
     sfg_tensor_view v;
@@ -391,7 +414,7 @@ int sfg_tensor_view_get(sfg_context* ctx, const sfg_tensor* t, sfg_tensor_view* 
 }
 
 int sfg_tensor_free(sfg_tensor* t) {
-  return guard([&] {
+  return guard(t ? t->ctx : nullptr, [&] {
     if (!t) return;
     for (auto* p : t->part)
       if (p) {
@@ -404,7 +427,7 @@ int sfg_tensor_free(sfg_tensor* t) {
 }
 
 int sfg_spmv(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, uint32_t flags) {
-  return guard([&] {
+  return guard(ctx, [&] {
     require(ctx && a && x && y, SFG_ERR_INVALID_OPERATION, "null argument");
     if (flags & SFG_COMPUTE_HOST) {
       float* dx = sfg::dalloc_n<float>(ctx, a->n);
@@ -431,7 +454,7 @@ int sfg_spmv(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, ui
 
 int sfg_spmm(sfg_context* ctx, const sfg_tensor* a, const void* b, int32_t b_dtype, int64_t nd,
              int64_t ldb, float* c, int64_t ldc, uint32_t flags) {
-  return guard([&] {
+  return guard(ctx, [&] {
     require(ctx && a && b && c, SFG_ERR_INVALID_OPERATION, "null argument");
     require(nd > 0 && ldb >= nd && ldc >= nd, SFG_ERR_INVALID_OPERATION, "bad dense shape");
     require(b_dtype == SFG_F32 || b_dtype == SFG_BF16, SFG_ERR_INVALID_OPERATION, "bad dtype");
@@ -461,7 +484,7 @@ int sfg_spmm(sfg_context* ctx, const sfg_tensor* a, const void* b, int32_t b_dty
 }
 
 int sfg_row_partition(sfg_context* ctx, const sfg_tensor* coo, int32_t parts, int64_t* bounds) {
-  return guard([&] {
+  return guard(ctx, [&] {
     require(ctx && coo && bounds && parts > 0, SFG_ERR_INVALID_OPERATION, "bad argument");
     require(coo->kind == SFG_COO, SFG_ERR_INVALID_OPERATION, "row partition expects COO");
     sfg::row_partition(ctx, coo, parts, bounds);
@@ -469,7 +492,7 @@ int sfg_row_partition(sfg_context* ctx, const sfg_tensor* coo, int32_t parts, in
 }
 
 int sfg_read_matrix_market(sfg_context* ctx, const char* path, uint32_t flags, sfg_tensor** out) {
-  return guard([&] {
+  return guard(ctx, [&] {
     require(ctx && path && out, SFG_ERR_INVALID_OPERATION, "null argument");
     *out = nullptr;
     *out = sfg::read_matrix_market(ctx, path, (flags & SFG_FLAG_SUM_DUPLICATES) != 0);
@@ -478,7 +501,7 @@ int sfg_read_matrix_market(sfg_context* ctx, const char* path, uint32_t flags, s
 
 int sfg_spgemm(sfg_context* ctx, const sfg_tensor* a, const sfg_tensor* b, float* c, int64_t ldc,
                uint32_t flags) {
-  return guard([&] {
+  return guard(ctx, [&] {
     require(ctx && a && b && c, SFG_ERR_INVALID_OPERATION, "null argument");
     require(ldc >= b->n, SFG_ERR_INVALID_OPERATION, "ldc < columns of B");
     const bool acc = (flags & SFG_COMPUTE_ACCUMULATE) != 0;
@@ -501,14 +524,14 @@ int sfg_spgemm(sfg_context* ctx, const sfg_tensor* a, const sfg_tensor* b, float
 }
 
 int sfg_write_container(sfg_context* ctx, const sfg_tensor* t, const char* path) {
-  return guard([&] {
+  return guard(ctx, [&] {
     require(ctx && t && path, SFG_ERR_INVALID_OPERATION, "null argument");
     sfg::write_container(ctx, t, path);
   });
 }
 
 int sfg_read_container(sfg_context* ctx, const char* path, const sfg_format* fmt, sfg_tensor** out) {
-  return guard([&] {
+  return guard(ctx, [&] {
     require(ctx && path && out, SFG_ERR_INVALID_OPERATION, "null argument");
     *out = nullptr;
     if (fmt) {
@@ -519,9 +542,17 @@ int sfg_read_container(sfg_context* ctx, const char* path, const sfg_format* fmt
   });
 }
 
+int sfgx_row_bounds_host(const int32_t* rows, int64_t nnz, int64_t n_rows, int32_t parts, int64_t* bounds) {
+  return guard([&] {
+    require(parts >= 1 && bounds, SFG_ERR_INVALID_OPERATION, "row_bounds: parts must be >= 1");
+    require(nnz == 0 || rows, SFG_ERR_INVALID_OPERATION, "row_bounds: null rows");
+    sfg::row_bounds_host(rows, nnz, n_rows, parts, bounds);
+  });
+}
+
 int sfg_coo_slice_rows(sfg_context* ctx, const sfg_tensor* coo, int64_t r0, int64_t r1,
                        sfg_tensor** out) {
-  return guard([&] {
+  return guard(ctx, [&] {
     require(ctx && coo && out, SFG_ERR_INVALID_OPERATION, "null argument");
     require(coo->kind == SFG_COO, SFG_ERR_INVALID_OPERATION, "row slice expects COO");
     require(0 <= r0 && r0 <= r1 && r1 <= coo->m, SFG_ERR_INVALID_OPERATION, "bad row range");
@@ -538,7 +569,7 @@ int sfg_comm_unique_id(uint8_t id[SFG_COMM_ID_BYTES]) {
 
 int sfg_comm_create(sfg_context* ctx, int32_t nranks, int32_t rank, const uint8_t id[SFG_COMM_ID_BYTES],
                     sfg_comm** out) {
-  return guard([&] {
+  return guard(ctx, [&] {
     require(ctx && id && out, SFG_ERR_INVALID_OPERATION, "null argument");
     require(nranks > 0 && rank >= 0 && rank < nranks, SFG_ERR_INVALID_OPERATION, "bad rank");
     *out = nullptr;
@@ -554,7 +585,7 @@ int sfg_comm_destroy(sfg_comm* comm) {
 
 int sfg_rowpart_spmv(sfg_context* ctx, sfg_comm* comm, const sfg_tensor* a_block, const float* x, float* y,
                      int64_t chunk_rows, uint32_t flags) {
-  return guard([&] {
+  return guard(ctx, [&] {
     require(ctx && comm && a_block && x && y, SFG_ERR_INVALID_OPERATION, "null argument");
     sfg::rowpart_spmv(ctx, comm, a_block, x, y, chunk_rows, (flags & SFG_ROWPART_GATHER) != 0);
   });
@@ -562,7 +593,7 @@ int sfg_rowpart_spmv(sfg_context* ctx, sfg_comm* comm, const sfg_tensor* a_block
 
 int sfg_rowpart_spmm(sfg_context* ctx, sfg_comm* comm, const sfg_tensor* a_block, const void* b, int32_t b_dtype,
                      int64_t nd, int64_t ldb, float* c, int64_t chunk_rows, uint32_t flags) {
-  return guard([&] {
+  return guard(ctx, [&] {
     require(ctx && comm && a_block && b && c, SFG_ERR_INVALID_OPERATION, "null argument");
     require(nd > 0 && ldb >= nd, SFG_ERR_INVALID_OPERATION, "bad dense shape");
     require(b_dtype == SFG_F32 || b_dtype == SFG_BF16, SFG_ERR_INVALID_OPERATION, "bad dtype");
@@ -571,7 +602,7 @@ int sfg_rowpart_spmm(sfg_context* ctx, sfg_comm* comm, const sfg_tensor* a_block
 }
 
 int sfg_allgather_chunks(sfg_context* ctx, sfg_comm* comm, float* buf, int64_t chunk_elems) {
-  return guard([&] {
+  return guard(ctx, [&] {
     require(ctx && comm && buf && chunk_elems >= 0, SFG_ERR_INVALID_OPERATION, "bad argument");
     sfg::allgather_chunks(ctx, comm, buf, chunk_elems);
   });
@@ -579,7 +610,7 @@ int sfg_allgather_chunks(sfg_context* ctx, sfg_comm* comm, float* buf, int64_t c
 
 int sfgx_gen_uniform(sfg_context* ctx, uint64_t seed, int64_t rows, int64_t cols, int32_t per_row,
                      sfg_tensor** out) {
-  return guard([&] {
+  return guard(ctx, [&] {
     require(per_row > 0 && per_row <= 64 && per_row <= cols, SFG_ERR_INVALID_OPERATION,
             "per_row must be in [1, min(64, cols)]");
     require(rows * per_row < INT32_MAX, SFG_ERR_INVALID_OPERATION, "too many entries");
@@ -588,7 +619,7 @@ int sfgx_gen_uniform(sfg_context* ctx, uint64_t seed, int64_t rows, int64_t cols
 }
 
 int sfgx_gen_rmat(sfg_context* ctx, uint64_t seed, int32_t scale, int64_t edges, sfg_tensor** out) {
-  return guard([&] {
+  return guard(ctx, [&] {
     require(scale > 0 && scale <= 30 && edges > 0 && edges < INT32_MAX, SFG_ERR_INVALID_OPERATION,
             "bad R-MAT size");
     *out = sfg::gen_from_keys(ctx, seed, 0, scale, int64_t(1) << scale, int64_t(1) << scale, edges);
@@ -597,7 +628,7 @@ int sfgx_gen_rmat(sfg_context* ctx, uint64_t seed, int32_t scale, int64_t edges,
 
 int sfgx_gen_hypersparse(sfg_context* ctx, uint64_t seed, int64_t rows, int64_t cols,
                          int64_t draws, sfg_tensor** out) {
-  return guard([&] {
+  return guard(ctx, [&] {
     require(rows > 0 && cols > 0 && rows < INT32_MAX && cols < INT32_MAX && draws > 0 &&
                 draws < INT32_MAX,
             SFG_ERR_INVALID_OPERATION, "bad hypersparse size");
@@ -607,7 +638,7 @@ int sfgx_gen_hypersparse(sfg_context* ctx, uint64_t seed, int64_t rows, int64_t 
 
 int sfgx_gen_block_sparse(sfg_context* ctx, uint64_t seed, int64_t rows, int64_t cols, int32_t r,
                           int32_t c, uint32_t thresh, int32_t value_dtype, sfg_tensor** out) {
-  return guard([&] {
+  return guard(ctx, [&] {
     require(ctx && out && rows > 0 && cols > 0 && r > 0 && c > 0 && rows < INT32_MAX && cols < INT32_MAX,
             SFG_ERR_INVALID_OPERATION, "bad block-sparse shape");
     require(value_dtype == SFG_F32 || value_dtype == SFG_BF16, SFG_ERR_INVALID_OPERATION, "bad dtype");
@@ -616,24 +647,24 @@ int sfgx_gen_block_sparse(sfg_context* ctx, uint64_t seed, int64_t rows, int64_t
 }
 
 int sfgx_gen_dense(sfg_context* ctx, uint64_t seed, int64_t count, float* out) {
-  return guard([&] { sfg::gen_dense(ctx, seed, count, out); });
+  return guard(ctx, [&] { sfg::gen_dense(ctx, seed, count, out); });
 }
 
 int64_t sfgx_launch_count(void) { return sfg::g_launches.load(); }
 
 int sfgx_device_alloc(sfg_context* ctx, int64_t bytes, void** out) {
-  return guard([&] {
+  return guard(ctx, [&] {
     require(ctx && out && bytes >= 0, SFG_ERR_INVALID_OPERATION, "bad argument");
     *out = sfg::dalloc(ctx, static_cast<size_t>(bytes));
   });
 }
 
 int sfgx_device_free(sfg_context* ctx, void* p) {
-  return guard([&] { sfg::dfree(ctx, p); });
+  return guard(ctx, [&] { sfg::dfree(ctx, p); });
 }
 
 int sfgx_copy(sfg_context* ctx, void* dst, const void* src, int64_t bytes, int32_t kind) {
-  return guard([&] {
+  return guard(ctx, [&] {
     require(ctx && bytes >= 0 && kind >= 0 && kind <= 2, SFG_ERR_INVALID_OPERATION, "bad argument");
     if (bytes == 0) return;
     cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice

@@ -1012,16 +1012,13 @@ bool spmm_bcsr_tc(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dt
   }
   const size_t smem = 1024 + kStages * kStageBytes + sizeof(Shared) + 64;
   const size_t gsmem = 1024 + kGStages * kGStageBytes + sizeof(GShared) + 64;
-  static bool attr = false;
-  if (!attr) {
-    SFG_CUDA(cudaFuncSetAttribute(k_bcsr_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
   static const bool per_row = [] {
     const char* v = std::getenv("SFG_BCSR_TC_PER_ROW");  // A/B switch: one block row per accumulator
     return v && *v == '1';
   }();
   if (per_row) {
+    // the attribute is per device: set on every call (a few host microseconds)
+    SFG_CUDA(cudaFuncSetAttribute(k_bcsr_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int grid = (int)std::min<int64_t>(a->nbr, (int64_t)ctx->sms);
     SFG_LAUNCH(k_bcsr_tc, grid, kThreads, smem, ctx->stream, tb, ta, a->ptr, a->idx, (int32_t)a->nbr,
                (int32_t)a->m, c, ldc, accumulate ? 1 : 0);

@@ -111,8 +111,7 @@ __global__ void __launch_bounds__(kBlock) k_count_blocks(const int32_t* __restri
                                                           const int32_t* __restrict__ col,
                                                           int32_t c, int32_t nbr, int32_t nbc,
                                                           uint32_t* __restrict__ gbm,
-                                                          int32_t* __restrict__ cnt,
-                                                          int* __restrict__ too_wide) {
+                                                          int32_t* __restrict__ cnt) {
   extern __shared__ uint32_t bm[];
   __shared__ int smin, smax, ssum;
   for (int32_t br = blockIdx.x; br < nbr; br += gridDim.x) {
@@ -123,11 +122,10 @@ __global__ void __launch_bounds__(kBlock) k_count_blocks(const int32_t* __restri
     }
     int32_t lo = 0, hi = nbc - 1;
     if (nbc > kFullRangeCols) col_range(col, s, e, c, &smin, &smax, &lo, &hi);
+    // words <= kMaxWords: the host rejects block grids wider than the bitmap
+    // before launching (coo_to_bcsr), so there is no skip path here (which
+    // would have to pass the same barriers as the marking path)
     int words = ((hi - lo) >> 5) + 1;
-    if (words > kMaxWords) {
-      if (threadIdx.x == 0) atomicOr(too_wide, 1);
-      continue;
-    }
     for (int w = threadIdx.x; w < words; w += blockDim.x) bm[w] = 0;
     if (threadIdx.x == 0) ssum = 0;
     __syncthreads();
@@ -277,20 +275,14 @@ sfg_tensor* coo_to_bcsr(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_
              ctx->stream, s->row, nnz, (int32_t)r, nbr, bptr);
   int tiles = (int)ceil_div(nbr, kTile);
   auto* status = lookback_status(ctx, tiles);
-  auto* tail = static_cast<int32_t*>(scratch(ctx, 64));
-  SFG_CUDA(cudaMemsetAsync(tail, 0, 16, ctx->stream));
   const size_t smem_count = kMaxWords * 4;
   const size_t smem_fill = kMaxWords * 8;
-  static bool attr_set = false;
-  if (!attr_set) {
-    SFG_CUDA(cudaFuncSetAttribute(k_count_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem_count));
-    SFG_CUDA(cudaFuncSetAttribute(k_fill_blocks<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem_fill));
-    SFG_CUDA(cudaFuncSetAttribute(k_fill_blocks<__nv_bfloat16>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fill));
-    attr_set = true;
-  }
+  // the attribute is per device (and the call is cheap): set on every call
+  SFG_CUDA(cudaFuncSetAttribute(k_count_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_count));
+  SFG_CUDA(cudaFuncSetAttribute(k_fill_blocks<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem_fill));
+  SFG_CUDA(cudaFuncSetAttribute(k_fill_blocks<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem_fill));
   // bitmap words actually needed: the widest possible row span
   int64_t words = (t->nbc + 31) / 32;
   if (words * 8 > (int64_t)smem_fill)
@@ -307,7 +299,7 @@ sfg_tensor* coo_to_bcsr(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_
   // of a 2,048-block-row matrix instead of 1.7
   const int cgrid = (int)std::min<int64_t>(nbr, (int64_t)ctx->sms * 16);
   SFG_LAUNCH(k_count_blocks, cgrid, kBlock / 2, words * 4, ctx->stream, bptr, s->idx, (int32_t)c, nbr,
-             (int32_t)t->nbc, gbm, cnt, tail + 1);
+             (int32_t)t->nbc, gbm, cnt);
   SFG_LAUNCH(k_scan_i32, tiles, kBlock, 0, ctx->stream, cnt, nbr, t->ptr, status, ctx->epoch++);
   int32_t nblocks = 0;
   read_back(ctx, t->ptr + nbr, sizeof nblocks, &nblocks);

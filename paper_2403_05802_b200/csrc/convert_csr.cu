@@ -11,6 +11,8 @@
 // (from_coo, tensor.hpp:118-162), so both are pure streaming passes.
 #include <vector>
 
+#include <algorithm>
+
 #include "devutil.cuh"
 #include "internal.cuh"
 
@@ -285,34 +287,47 @@ sfg_tensor* coo_to_dcsr(sfg_context* ctx, const sfg_tensor* s) {
   return t;
 }
 
-void row_partition(sfg_context* ctx, const sfg_tensor* coo, int parts, int64_t* bounds) {
-  // Partition p starts at the row holding entry floor(p * nnz / P): nnz
-  // balanced to within one row.
-  std::vector<int64_t> keys(parts + 1);
+// The boundary rule, shared by the device and host entry points: partition
+// p starts at the row holding entry floor(p * nnz / P) (nnz balanced to
+// within one row), monotone, [0, m]. `row_at(e)` returns the
+// row of entry e of the row-sorted COO.
+template <class RowAt>
+static void bounds_from_quantiles(int64_t m, int64_t nnz, int parts, RowAt row_at, int64_t* bounds) {
   bounds[0] = 0;
-  bounds[parts] = coo->m;
-  if (parts == 1) return;
-  if (coo->nnz == 0) {
-    for (int p = 1; p < parts; ++p) bounds[p] = coo->m * p / parts;
+  bounds[parts] = m;
+  for (int p = 1; p < parts; ++p) {
+    int64_t b = nnz == 0 ? m * p / parts : row_at(nnz * p / parts);
+    if (b < bounds[p - 1]) b = bounds[p - 1];
+    bounds[p] = b;
+  }
+}
+
+void row_bounds_host(const int32_t* rows, int64_t nnz, int64_t m, int parts, int64_t* bounds) {
+  bounds_from_quantiles(m, nnz, parts, [&](int64_t e) -> int64_t { return rows[e]; }, bounds);
+}
+
+void row_partition(sfg_context* ctx, const sfg_tensor* coo, int parts, int64_t* bounds) {
+  if (parts == 1 || coo->nnz == 0) {
+    bounds_from_quantiles(coo->m, coo->nnz, parts, [](int64_t) -> int64_t { return 0; }, bounds);
     return;
   }
+  // the P - 1 quantile entries' rows, gathered on the device
   int64_t* dpos = dalloc_n<int64_t>(ctx, parts);
   std::vector<int64_t> pos(parts - 1);
   for (int p = 1; p < parts; ++p) pos[p - 1] = coo->nnz * p / parts;
   SFG_CUDA(cudaMemcpyAsync(dpos, pos.data(), (parts - 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
   int64_t* drows = dalloc_n<int64_t>(ctx, parts);
-  SFG_LAUNCH(k_gather_rows, 1, 256, 0, ctx->stream, coo->row, dpos, parts - 1, coo->nnz,
-             (int32_t)coo->m, drows);
+  SFG_LAUNCH(k_gather_rows, (int)ceil_div(parts - 1, 256), 256, 0, ctx->stream, coo->row, dpos, parts - 1,
+             coo->nnz, (int32_t)coo->m, drows);
   std::vector<int64_t> rows(parts - 1);
   SFG_CUDA(cudaMemcpyAsync(rows.data(), drows, (parts - 1) * 8, cudaMemcpyDeviceToHost, ctx->stream));
   SFG_CUDA(cudaStreamSynchronize(ctx->stream));
   dfree(ctx, dpos);
   dfree(ctx, drows);
-  for (int p = 1; p < parts; ++p) {
-    int64_t b = rows[p - 1];
-    if (b < bounds[p - 1]) b = bounds[p - 1];
-    bounds[p] = b;
-  }
+  bounds_from_quantiles(coo->m, coo->nnz, parts,
+                        [&](int64_t e) -> int64_t { return rows[static_cast<size_t>(
+                                                       std::lower_bound(pos.begin(), pos.end(), e) - pos.begin())]; },
+                        bounds);
 }
 
 sfg_tensor* coo_slice_rows(sfg_context* ctx, const sfg_tensor* coo, int64_t r0, int64_t r1) {

@@ -427,16 +427,31 @@ sfg_tensor* coo_to_hyb(sfg_context* ctx, const sfg_tensor* s, int64_t min_sum) {
   // host waits for the sizes: the read-back round trip overlaps the split
   // instead of idling the GPU. The COO part is allocated for every entry
   // (an upper bound) and its size set once known.
-  RowInfo ri = row_info(ctx, s, min_sum, nullptr, /*defer=*/true);
+  //
+  // The over-allocation (12 B for every entry not selected, held until the
+  // tensor is freed) is only taken while it is small next to the free
+  // device memory; otherwise the sizes are waited for and the COO part is
+  // allocated exactly.
+  const size_t upper = 12 * static_cast<size_t>(s->nnz);
+  bool defer = true;
+  if (upper > (size_t(256) << 20)) {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+      cudaGetLastError();
+      free_b = 0;
+    }
+    defer = upper <= free_b / 4;
+  }
+  RowInfo ri = row_info(ctx, s, min_sum, nullptr, defer);
   sfg_tensor* h = new_tensor(ctx, SFG_HYB, s->m, s->n);
   h->threshold = min_sum;
-  h->part[1] = coo_part(ctx, s->m, s->n, s->nnz);
+  h->part[1] = coo_part(ctx, s->m, s->n, defer ? s->nnz : ri.nnz_sel);
   h->part[1]->has_zeros = s->has_zeros == 0 ? 0 : -1;
   if (s->nnz)
     SFG_LAUNCH(k_split, stream_grid(ctx, ceil_div(s->nnz, kSplitRun), kBlock, 1, 8), kBlock, 0, ctx->stream,
                s->row, s->idx, static_cast<const float*>(s->val), s->nnz, ri.off, h->part[1]->row,
                h->part[1]->idx, static_cast<float*>(h->part[1]->val), nullptr, nullptr, nullptr);
-  row_info_finish(ctx, ri);
+  if (defer) row_info_finish(ctx, ri);
   h->part[1]->nnz = ri.nnz_sel;
   h->part[0] = ell_from(ctx, s, ri, true);
   free_row_info(ctx, ri);

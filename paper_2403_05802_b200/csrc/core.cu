@@ -176,10 +176,10 @@ int size_slot_start(sfg_context* ctx, const int32_t* dev) {
 }
 
 int32_t size_slot_finish(sfg_context* ctx, int slot) {
-  SFG_CUDA(cudaEventSynchronize(ctx->size_events[slot]));
-  const int32_t v = ctx->size_slots[slot];
-  ctx->free_size_slots.push_back(slot);
-  return v;
+  const cudaError_t e = cudaEventSynchronize(ctx->size_events[slot]);
+  ctx->free_size_slots.push_back(slot);  // returned even when the wait failed
+  if (e != cudaSuccess) raise_cuda(e, "cudaEventSynchronize(size slot)", __FILE__, __LINE__);
+  return ctx->size_slots[slot];
 }
 
 int64_t tensor_nnr(const sfg_tensor* t) {
@@ -203,7 +203,14 @@ sfg_tensor* new_tensor(sfg_context* ctx, int kind, int64_t m, int64_t n) {
 
 void free_tensor_arrays(sfg_tensor* t) {
   sfg_context* ctx = t->ctx;
-  tensor_nnr(t);  // a pending read-back must land before its slot is reused
+  // a pending read-back must land before its slot is reused; on the free
+  // path a failed wait (a sticky CUDA error) must not leak the arrays or
+  // the slot, so it is waited for without raising
+  if (t->nnr_slot >= 0) {
+    if (cudaEventSynchronize(ctx->size_events[t->nnr_slot]) != cudaSuccess) cudaGetLastError();
+    ctx->free_size_slots.push_back(t->nnr_slot);
+    t->nnr_slot = -1;
+  }
   dfree(ctx, t->row);
   dfree(ctx, t->ptr);
   dfree(ctx, t->idx);

@@ -206,6 +206,8 @@ sfg_tensor* coo_to_hyb(sfg_context* ctx, const sfg_tensor* s, int64_t min_sum);
 void decompose_rows(sfg_context* ctx, const sfg_tensor* s, int64_t min_sum, sfg_tensor** sel,
                     sfg_tensor** rem, int32_t* totals);
 void row_partition(sfg_context* ctx, const sfg_tensor* coo, int parts, int64_t* bounds);
+// The same rule over a host row array (no device work).
+void row_bounds_host(const int32_t* rows, int64_t nnz, int64_t m, int parts, int64_t* bounds);
 sfg_tensor* coo_slice_rows(sfg_context* ctx, const sfg_tensor* coo, int64_t r0, int64_t r1);
 
 void spmv(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, bool accumulate);

@@ -1,7 +1,8 @@
 """Multi-rank row partitioning on CPU (gloo, world_size 2): each rank takes
-its nnz-balanced row block, computes its slice of y (the CPU oracle stands
-in for the device SpMV), and the padded all-gather reassembles exactly the
-full product."""
+its nnz-balanced row block by the library's own boundary rule
+(sfgx_row_bounds_host, the rule sfg_row_partition applies on the device),
+computes its slice of y (the CPU oracle stands in for the device SpMV), and
+the padded all-gather reassembles exactly the full product."""
 import os
 import socket
 
@@ -34,12 +35,23 @@ def test_row_bounds_balance():
     assert row_bounds(np.zeros(0, int), 10, 4) == [0, 2, 5, 7, 10]
 
 
+def test_library_host_rule_matches_restatement():
+    """sfgx_row_bounds_host (C-ABI, no GPU) == rowpart.row_bounds."""
+    import paper_2403_05802_b200 as sfg
+    rng = np.random.default_rng(1)
+    for m, nnz in ((1, 0), (10, 0), (1000, 5000), (4096, 70000)):
+        rows = np.sort(rng.integers(0, m, nnz)).astype(np.int32)
+        for parts in (1, 2, 3, 4, 8, 16):
+            assert sfg.row_bounds_host(rows, m, parts) == row_bounds(rows, m, parts), (m, nnz, parts)
+
+
 def _worker(rank, world, port, result_path):
     import torch
     import torch.distributed as dist
 
     import oracle
     from matrices import power_law_coo
+    import paper_2403_05802_b200 as sfg
     from paper_2403_05802_b200.rowpart import gather_rows, padded_chunk, row_bounds, unpad
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -48,7 +60,8 @@ def _worker(rank, world, port, result_path):
     m, n = 900, 700
     r, c, v = power_law_coo(3, m, n, avg=9)
     x = np.random.default_rng(1).random(n)
-    b = row_bounds(r, m, world)
+    b = sfg.row_bounds_host(r, m, world)
+    assert b == row_bounds(r, m, world)
     sel = (r >= b[rank]) & (r < b[rank + 1])
     mloc = b[rank + 1] - b[rank]
     loc = port_lib.from_coo(max(mloc, 1), n, r[sel] - b[rank], c[sel], v[sel])

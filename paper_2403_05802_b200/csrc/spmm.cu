@@ -10,6 +10,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 
 #include "devutil.cuh"
@@ -180,16 +181,18 @@ __global__ void __launch_bounds__(kBlock) k_spmm_rows(const int32_t* __restrict_
 }
 
 // Merge-path CSR (load balanced by rows + entries, so one row of a million
-// entries no longer serialises the kernel). The (row ends, entries) merge
+// entries does not serialise the kernel). The (row ends, entries) merge
 // sequence of length m + nnz is cut into chunks of kMergeItems; a first
 // kernel finds every cut's (row, entry) coordinate by binary search
 // (Merrill & Garland's merge-path), then a warp per chunk walks its entries
-// in order, flushing each row as its end passes. Rows wholly inside the
-// chunk are stored; the chunk's first and last rows may be shared with
-// neighbouring chunks and are added atomically. C is zeroed beforehand
-// (or holds the accumulate input), so empty rows need no work.
+// in order. Every row of C is written exactly once, by the chunk holding the
+// row's end item: rows with no entry are zeroed there (no memset of C), a
+// completed row stores this chunk's part of it. A row still open at the end
+// of a chunk leaves its partial sum in a carry slot (one per chunk), and
+// k_spmm_carry_fix adds the carries of each row in chunk order afterwards —
+// no atomics, so C is bit-identical from run to run (the reference reduces
+// its thread partials in worker order for the same reason, kernel.hpp:370-384).
 constexpr int kMergeItems = 1024;
-constexpr int kMergeK = 8;  // B-row gathers in flight per warp
 
 __global__ void k_merge_cuts(const int32_t* __restrict__ ptr, int64_t m, int64_t nnz, int64_t ncuts,
                              int2* __restrict__ cuts) {
@@ -205,126 +208,101 @@ __global__ void k_merge_cuts(const int32_t* __restrict__ ptr, int64_t m, int64_t
   }
 }
 
-template <typename TB, int V>
-__global__ void __launch_bounds__(kBlock) k_spmm_merge(const int32_t* __restrict__ ptr,
-                                                        const int32_t* __restrict__ col,
-                                                        const float* __restrict__ val,
-                                                        const int2* __restrict__ cuts, int64_t nchunks,
-                                                        Dense d) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int chunks = (d.nd + 32 * V - 1) / (32 * V);
-  const bool vec_ok = (d.nd % (32 * V) == 0) && (d.ldb % V == 0);
-  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nchunks * chunks; w += warps) {
-    const int64_t q = w / chunks;
-    const int c0 = (int)(w - q * chunks) * 32 * V + lane * V;
-    const int2 a = __ldg(cuts + q), b = __ldg(cuts + q + 1);
-    int i = a.x;
-    const int j0 = a.y, j1 = b.y;
-    int row_end = __ldg(ptr + i + 1);
-    const bool first_shared = j0 > __ldg(ptr + i);  // row a.x began in an earlier chunk
-    bool shared = first_shared;
-    Dense dw = d;  // rows owned by this chunk: plain stores unless accumulating
-    dw.acc = d.keep;
-    float acc[V];
-#pragma unroll
-    for (int k = 0; k < V; ++k) acc[k] = 0.f;
-    bool any = false;
-    for (int base = j0; base < j1; base += 32) {
-      const int k = base + lane;
-      const int mc = k < j1 ? ld_stream(col + k) : 0;
-      const float mv = k < j1 ? ld_stream(val + k) : 0.f;
-      const int cnt = min(32, j1 - base);
-      for (int t0 = 0; t0 < cnt; t0 += kMergeK) {
-        // the B-row gathers of kMergeK entries are issued before any row
-        // flush (whose C stores the compiler cannot move loads across)
-        float v[kMergeK][V];
-#pragma unroll
-        for (int u = 0; u < kMergeK; ++u) {
-          const int ck = __shfl_sync(kFull, mc, (t0 + u) & 31);
-          if (t0 + u < cnt) load_brow<TB, V>(d, ck, c0, vec_ok, v[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < kMergeK; ++u) {
-          const float ak = __shfl_sync(kFull, mv, (t0 + u) & 31);
-          if (t0 + u < cnt) {
-            const int j = base + t0 + u;
-            while (j >= row_end) {  // row i ends before entry j: flush it
-              if (any) store_row<V>(dw, i, c0, shared, acc);
-#pragma unroll
-              for (int k2 = 0; k2 < V; ++k2) acc[k2] = 0.f;
-              any = false;
-              shared = false;
-              ++i;
-              row_end = __ldg(ptr + i + 1);
-            }
-#pragma unroll
-            for (int k2 = 0; k2 < V; ++k2) acc[k2] = fmaf(ak, v[u][k2], acc[k2]);
-            any = true;
-          }
-        }
-      }
-    }
-    // the open row: complete if its end is this chunk's last row end
-    if (any) store_row<V>(dw, i, c0, shared || row_end > j1 || i >= b.x, acc);
-  }
-}
+// Carry slots of the merge-path walkers: row[q] = the row open at the end of
+// chunk q (-1: none), val[q * nd + c] its partial sum over the chunk.
+struct Carry {
+  int32_t* row;
+  float* val;
+};
 
-// Merge-path CSR for narrow dense operands (nd = 32 / G * V, e.g. 32 with
-// G = 4, V = 4): a B row is only 32 V / G floats, so a warp splits into G
-// lane groups of 32 / G lanes and takes G entries per instruction (vector
-// loads, one entry per group) instead of one. Each group keeps a partial
-// sum of the current row; a row flush reduces the G partials with lane
-// shuffles and group 0 stores. While a step's entries all lie inside the
-// current row (the common case on rows of tens of entries) the step is
-// branch-free: kU entries per group, their B rows loaded back to back.
+// A warp walks one merge-path chunk for one chunk of output columns. The
+// warp splits into G lane groups of L = 32 / G lanes; a group covers L·V
+// output columns (V per lane) and takes one entry per load instruction, so
+// a narrow dense operand (nd = 32: G = 4 groups of 8 lanes × float4) still
+// has G entries per warp instruction. Each group keeps a partial sum of the
+// current row; closing a row reduces the G partials with lane shuffles and
+// group 0 stores. While a step's kStep = G·kU entries all lie inside the
+// current row the step is branch-free, its B rows loaded back to back.
+// kVec: nd a multiple of L·V, vector-aligned B and C (no column guards).
 #ifndef SFG_MERGE_MINB
 #define SFG_MERGE_MINB 5  // CTAs per SM the register budget is sized for (config 5 SpMM: 5 -> 24.1 ms, 4 -> 25.1, 3 -> 25.1)
 #endif
-template <typename TB, int G, int V, int kU>
-__global__ void __launch_bounds__(kBlock, SFG_MERGE_MINB) k_spmm_merge_grp(const int32_t* __restrict__ ptr,
-                                                            const int32_t* __restrict__ col,
-                                                            const float* __restrict__ val,
-                                                            const int2* __restrict__ cuts, int64_t nchunks,
-                                                            Dense d) {
+template <typename TB, int G, int V, int kU, bool kVec, bool kOne, int kMinB = SFG_MERGE_MINB>
+__global__ void __launch_bounds__(kBlock, kMinB) k_spmm_merge(const int32_t* __restrict__ ptr,
+                                                               const int32_t* __restrict__ col,
+                                                               const float* __restrict__ val,
+                                                               const int2* __restrict__ cuts, int64_t nchunks,
+                                                               int32_t m, Dense d, Carry cy) {
   constexpr int L = 32 / G;  // lanes per group
   constexpr int kStep = G * kU;
   static_assert(G * L == 32 && kStep <= 32, "groups tile the warp");
+  static_assert(kVec || V == 1, "guarded columns are scalar");
   const int lane = threadIdx.x & 31, grp = lane / L, sub = lane % L;
-  const int c0 = sub * V;
+  const int ccols = kOne ? 1 : (d.nd + L * V - 1) / (L * V);  // column chunks (kOne: nd == L V)
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < nchunks; q += warps) {
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nchunks * ccols; w += warps) {
+    const int64_t q = kOne ? w : w / ccols;
+    const int cc = kOne ? 0 : (int)(w - q * ccols);
+    const int c0 = cc * L * V + sub * V;
+    const bool live_col = kVec || c0 < d.nd;
     const int2 a = __ldg(cuts + q), b = __ldg(cuts + q + 1);
     int i = a.x;
     const int j0 = a.y, j1 = b.y;
-    int row_end = __ldg(ptr + i + 1);
-    bool shared = j0 > __ldg(ptr + i);  // row a.x began in an earlier chunk
+    // row-end window: lane t holds ptr[wb + t + 1] (rows past m: INT_MAX)
+    int wb = i;
+    int pw = wb + lane < m ? __ldg(ptr + wb + lane + 1) : INT_MAX;
+    int row_end = __shfl_sync(kFull, pw, 0);
     float acc[V];
 #pragma unroll
     for (int k = 0; k < V; ++k) acc[k] = 0.f;
-    bool any = false;
-    auto flush = [&](bool atomic) {  // reduce the groups' partials of row i; group 0 stores
+    bool any = false;  // entries of row i seen in this chunk
+    auto reduce = [&]() {
 #pragma unroll
       for (int o = L; o < 32; o <<= 1)
 #pragma unroll
         for (int k = 0; k < V; ++k) acc[k] += __shfl_xor_sync(kFull, acc[k], o);
-      if (grp == 0) {
-        float* crow = d.c + (int64_t)i * d.ldc + c0;
-        if (atomic) {
+    };
+    auto put = [&](int64_t r, float (&x)[V]) {  // C[r][this lane's columns] = x (+ C with accumulate)
+      float* crow = d.c + r * d.ldc + c0;
+      if constexpr (kVec) {
+        if (d.keep) {
+          float o[V];
+          BRow<float>::template load<V>(crow, o);
 #pragma unroll
-          for (int k = 0; k < V; ++k) atomicAdd(crow + k, acc[k]);
-        } else {
-          if (d.keep) {
-            float o[V];
-            BRow<float>::template load<V>(crow, o);
-#pragma unroll
-            for (int k = 0; k < V; ++k) acc[k] += o[k];
-          }
-          store_vec<V>(crow, acc);
+          for (int k = 0; k < V; ++k) x[k] += o[k];
         }
+        store_vec<V>(crow, x);
+      } else {
+        if (live_col) crow[0] = d.keep ? crow[0] + x[0] : x[0];
       }
+    };
+    // Row i is complete (its end item lies in this chunk at or before entry
+    // position `at`): store it and move to the first row ending after `at`
+    // (rows from b.x on are closed by later chunks). The empty rows passed
+    // over are zeroed once the chunk is done.
+    const int lim = b.x;
+    auto close = [&](int at) {
+      reduce();
+      if (grp == 0 && (any || !d.keep)) put(i, acc);
 #pragma unroll
       for (int k = 0; k < V; ++k) acc[k] = 0.f;
+      any = false;
+      int r = i + 1;
+      for (;;) {
+        if (r - wb >= 32) {
+          wb = r;
+          pw = wb + lane < m ? __ldg(ptr + wb + lane + 1) : INT_MAX;
+        }
+        const unsigned past = __ballot_sync(kFull, pw > at) & (~0u << (r - wb));
+        r = past ? wb + __ffs(past) - 1 : wb + 32;
+        if (past || r >= lim) break;
+      }
+      i = min(r, lim);
+      if (i - wb >= 32) {
+        wb = i;
+        pw = wb + lane < m ? __ldg(ptr + wb + lane + 1) : INT_MAX;
+      }
+      row_end = __shfl_sync(kFull, pw, i - wb);
     };
     for (int base = j0; base < j1; base += 32) {
       const int e = base + lane;
@@ -337,48 +315,107 @@ __global__ void __launch_bounds__(kBlock, SFG_MERGE_MINB) k_spmm_merge_grp(const
         // B row 0, selected away), all loads in flight at once
         float v[kU][V];
 #pragma unroll
-        for (int u = 0; u < kU; ++u)
-          load_brow<TB, V>(d, __shfl_sync(kFull, mc, (t0 + u * G + grp) & 31), c0, true, v[u]);
+        for (int u = 0; u < kU; ++u) {
+          const int ck = __shfl_sync(kFull, mc, (t0 + u * G + grp) & 31);
+          const TB* brow = static_cast<const TB*>(d.b) + (int64_t)ck * d.ldb + c0;
+          if constexpr (kVec) {
+            BRow<TB>::template load<V>(brow, v[u]);
+          } else {
+            v[u][0] = live_col ? (float)brow[0] : 0.f;
+          }
+        }
         if (last < row_end) {
           // fast path: the whole step is in row i
 #pragma unroll
           for (int u = 0; u < kU; ++u) {
-            const bool live = t0 + u * G + grp < cnt;  // past cnt: B row 0, selected away
+            const bool live = t0 + u * G + grp < cnt;
             const float ak = __shfl_sync(kFull, mv, (t0 + u * G + grp) & 31);
 #pragma unroll
             for (int k = 0; k < V; ++k) acc[k] = fmaf(ak, live ? v[u][k] : 0.f, acc[k]);
           }
           any = true;
         } else {
-          // a row ends inside the step: entry by entry in order, flushing
+          // a row ends inside the step: entry by entry in order, closing
           // rows as they end; the owning group adds its preloaded row
+          {
 #pragma unroll
-          for (int u = 0; u < kU; ++u)
+            for (int u = 0; u < kU; ++u)
 #pragma unroll
-            for (int gg = 0; gg < G; ++gg) {
-              const int t = t0 + u * G + gg;
-              if (t < cnt) {
-                const int j = base + t;
-                while (j >= row_end) {  // row i ends before entry j: flush it
-                  if (any) flush(shared);
-                  any = false;
-                  shared = false;
-                  ++i;
-                  row_end = __ldg(ptr + i + 1);
+              for (int gg = 0; gg < G; ++gg) {
+                const int t = t0 + u * G + gg;
+                if (t < cnt) {
+                  const int j = base + t;
+                  if (j >= row_end) close(j);
+                  const float ak = __shfl_sync(kFull, mv, t);
+                  if (grp == gg) {
+#pragma unroll
+                    for (int k = 0; k < V; ++k) acc[k] = fmaf(ak, v[u][k], acc[k]);
+                  }
+                  any = true;
                 }
-                const float ak = __shfl_sync(kFull, mv, t);
-                if (grp == gg) {
-#pragma unroll
-                  for (int k = 0; k < V; ++k) acc[k] = fmaf(ak, v[u][k], acc[k]);
-                }
-                any = true;
               }
-            }
+          }
         }
       }
     }
-    // the open row: complete if its end is this chunk's last row end
-    if (any) flush(shared || row_end > j1 || i >= b.x);
+    // rows ending at the chunk's end: complete here
+    if (i < b.x) close(j1);
+    // rows of this chunk without entries (ptr[r] == ptr[r + 1]) are zero
+    if (!d.keep) {
+      float z[V];
+#pragma unroll
+      for (int k = 0; k < V; ++k) z[k] = 0.f;
+      for (int r0 = a.x; r0 < b.x; r0 += 32) {
+        const int r = r0 + lane;
+        const int hi = r < b.x ? __ldg(ptr + r + 1) : 0;
+        const int lo = r < b.x ? __ldg(ptr + r) : 1;
+        unsigned empty = __ballot_sync(kFull, hi == lo);
+        while (empty) {  // G empty rows at a time, one per group
+          int pick = -1;
+#pragma unroll
+          for (int g2 = 0; g2 < G; ++g2) {
+            if (empty) {
+              const int f = __ffs(empty) - 1;
+              if (g2 == grp) pick = f;
+              empty &= empty - 1;
+            }
+          }
+          if (pick >= 0) put(r0 + pick, z);
+        }
+      }
+    }
+    // the row left open: its partial goes to the carry slot
+    if (any) {
+      reduce();
+      if (grp == 0 && live_col) {
+        float* cv = cy.val + q * d.nd + c0;
+        if constexpr (kVec) {
+          store_vec<V>(cv, acc);
+        } else {
+          cv[0] = acc[0];
+        }
+      }
+    }
+    if (cc == 0 && lane == 0) cy.row[q] = any ? i : -1;
+  }
+}
+
+// Adds each row's carries, in chunk order, to the value its completing
+// chunk stored. A warp per chunk; only the first chunk of a run carrying the
+// same row does the sum (runs: rows longer than a chunk).
+__global__ void __launch_bounds__(kBlock) k_spmm_carry_fix(Carry cy, int64_t nchunks, Dense d) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < nchunks; q += warps) {
+    const int r = __ldg(cy.row + q);
+    if (r < 0 || (q > 0 && __ldg(cy.row + q - 1) == r)) continue;
+    int64_t t1 = q + 1;
+    while (t1 < nchunks && __ldg(cy.row + t1) == r) ++t1;
+    for (int c = lane; c < d.nd; c += 32) {
+      float s = 0.f;
+      for (int64_t t = q; t < t1; ++t) s += __ldg(cy.val + t * d.nd + c);
+      d.c[(int64_t)r * d.ldc + c] += s;
+    }
   }
 }
 
@@ -520,15 +557,18 @@ __global__ void __launch_bounds__(kBlock) k_spmm_ell(const int32_t* __restrict__
 
 // ------------------------------------------------------------------- COO
 // A warp owns 32*kCooIters consecutive row-sorted entries; it accumulates a
-// row while the row stays the same and flushes on change. Only the first and
-// last rows of a chunk may be shared with neighbouring warps (atomicAdd).
+// row while the row stays the same and stores it when the row changes. A row
+// belongs to the chunk holding its last entry (C was zeroed first, or holds
+// the accumulate input, so that chunk adds its part with a plain store); a
+// row continuing into the next chunk leaves its partial in the chunk's carry
+// slot, added in chunk order by k_spmm_carry_fix — no atomics.
 constexpr int kCooIters = 4;
 
 template <typename TB, int V>
 __global__ void __launch_bounds__(kBlock) k_spmm_coo(const int32_t* __restrict__ row,
                                                       const int32_t* __restrict__ col,
                                                       const float* __restrict__ val, int64_t nnz,
-                                                      Dense d) {
+                                                      Dense d, Carry cy) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int chunks = (d.nd + 32 * V - 1) / (32 * V);
@@ -538,11 +578,10 @@ __global__ void __launch_bounds__(kBlock) k_spmm_coo(const int32_t* __restrict__
   for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nchunks * chunks;
        w += warps) {
     int64_t q = w / chunks;
-    int c0 = (int)(w - q * chunks) * 32 * V + lane * V;
+    const int cc = (int)(w - q * chunks);
+    int c0 = cc * 32 * V + lane * V;
     int64_t e0 = q * span, e1 = min(nnz, e0 + span);
-    int first = __ldg(row + e0);
-    int last = __ldg(row + e1 - 1);
-    int cur = first;
+    int cur = __ldg(row + e0);
     float acc[V];
 #pragma unroll
     for (int i = 0; i < V; ++i) acc[i] = 0.f;
@@ -555,7 +594,7 @@ __global__ void __launch_bounds__(kBlock) k_spmm_coo(const int32_t* __restrict__
       for (int j = 0; j < cnt; ++j) {
         int rj = __shfl_sync(kFull, mr, j);
         if (rj != cur) {
-          store_row<V>(d, cur, c0, cur == first, acc);
+          store_row<V>(d, cur, c0, false, acc);
 #pragma unroll
           for (int i = 0; i < V; ++i) acc[i] = 0.f;
           cur = rj;
@@ -563,7 +602,15 @@ __global__ void __launch_bounds__(kBlock) k_spmm_coo(const int32_t* __restrict__
         fma_row<TB, V>(d, __shfl_sync(kFull, mc, j), __shfl_sync(kFull, mv, j), c0, vec_ok, acc);
       }
     }
-    store_row<V>(d, cur, c0, cur == first || cur == last, acc);
+    const int next = e1 < nnz ? __ldg(row + e1) : -1;
+    if (cur != next) {
+      store_row<V>(d, cur, c0, false, acc);
+    } else {
+#pragma unroll
+      for (int i = 0; i < V; ++i)
+        if (c0 + i < d.nd) cy.val[q * d.nd + c0 + i] = acc[i];
+    }
+    if (cc == 0 && lane == 0) cy.row[q] = cur != next ? -1 : cur;
   }
 }
 
@@ -649,6 +696,43 @@ __global__ void __launch_bounds__(kBlock) k_spmm_bcsr(const int32_t* __restrict_
   }
 }
 
+template <typename TB>
+void spmm_csr_merge(sfg_context* ctx, const sfg_tensor* a, Dense d) {
+  const int64_t total = a->m + a->nnz;
+  const int64_t nchunks = ceil_div(total, kMergeItems);
+  // scratch: cuts[nchunks + 1] | carry rows[nchunks] | carry values[nchunks][nd]
+  const size_t cut_b = ((size_t)(nchunks + 1) * sizeof(int2) + 15) & ~size_t(15);
+  const size_t row_b = ((size_t)nchunks * 4 + 15) & ~size_t(15);
+  const size_t val_b = (size_t)nchunks * d.nd * 4;
+  char* s = static_cast<char*>(scratch(ctx, cut_b + row_b + val_b));
+  auto* cuts = reinterpret_cast<int2*>(s);
+  Carry cy{reinterpret_cast<int32_t*>(s + cut_b), reinterpret_cast<float*>(s + cut_b + row_b)};
+  SFG_LAUNCH(k_merge_cuts, (int)std::min<int64_t>(ceil_div(nchunks + 1, 256), (int64_t)ctx->sms * 8), 256, 0,
+             ctx->stream, a->ptr, a->m, a->nnz, nchunks + 1, cuts);
+  const bool vec4 = d.ldb % 4 == 0 && d.ldc % 4 == 0 &&
+                    ((reinterpret_cast<uintptr_t>(d.b) | reinterpret_cast<uintptr_t>(d.c)) & 15) == 0;
+  auto grid_for = [&](int64_t warps_needed) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(warps_needed, kBlock / 32), (int64_t)ctx->sms * 16));
+  };
+  const int32_t m = (int32_t)a->m;
+  const float* fv = static_cast<const float*>(a->val);
+#define SFG_MERGE(G, V, U, VEC, ONE, MB, CC)                                                                   \
+  SFG_LAUNCH((k_spmm_merge<TB, G, V, U, VEC, ONE, MB>), grid_for(nchunks * (CC)), kBlock, 0, ctx->stream, \
+             a->ptr, a->idx, fv, cuts, nchunks, m, d, cy)
+  // nd = 32 on config 5 (SpMM ms): this unrolled step, 5 CTAs/SM 24.6;
+  // 4 CTAs/SM 24.9; kU = 2 at 6 CTAs/SM 25.3; the row-end path as a rolled
+  // loop (smaller code, more instructions) 26.3; the first version of this
+  // kernel with the zeroing of empty rows inside every row close (code 5x
+  // the size, instruction-cache bound) 44
+  if (vec4 && d.nd == 32) SFG_MERGE(4, 4, 4, true, true, 5, 1);
+  else if (vec4 && d.nd == 16) SFG_MERGE(8, 4, 4, true, true, 5, 1);
+  else if (vec4 && d.nd == 64) SFG_MERGE(2, 4, 4, true, true, 5, 1);
+  else if (vec4 && d.nd % 128 == 0) SFG_MERGE(1, 4, 4, true, false, 5, d.nd / 128);
+  else SFG_MERGE(1, 1, 8, false, false, 5, ceil_div(d.nd, 32));
+#undef SFG_MERGE
+  SFG_LAUNCH(k_spmm_carry_fix, grid_for(nchunks), kBlock, 0, ctx->stream, cy, nchunks, d);
+}
+
 template <typename TB, int V>
 void launch_fmt(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
   int64_t chunks = ceil_div(d.nd, 32 * V);
@@ -665,27 +749,8 @@ void launch_fmt(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
   constexpr int kBatchRows = 24, kBatchK = 8;
   switch (a->kind) {
     case SFG_CSR:
-      if (a->m == 0 || a->nnz == 0) break;
-      {
-        const int64_t total = a->m + a->nnz;
-        const int64_t nchunks = ceil_div(total, kMergeItems);
-        auto* cuts = static_cast<int2*>(scratch(ctx, (nchunks + 1) * sizeof(int2)));
-        SFG_LAUNCH(k_merge_cuts, (int)std::min<int64_t>(ceil_div(nchunks + 1, 256), (int64_t)ctx->sms * 8), 256, 0,
-                   ctx->stream, a->ptr, a->m, a->nnz, nchunks + 1, cuts);
-        const bool vec4 = d.ldb % 4 == 0 && d.ldc % 4 == 0 &&
-                          ((reinterpret_cast<uintptr_t>(d.b) | reinterpret_cast<uintptr_t>(d.c)) & 15) == 0;
-        // nd = 32 on config 5 (SpMM ms): kU = 4 25.1, kU = 2 28.9, kU = 8 31.3
-        // (spills); the one-entry-per-warp-step kernel: 43 (issue-bound)
-        if (vec4 && d.nd == 32)
-          SFG_LAUNCH((k_spmm_merge_grp<TB, 4, 4, 4>), grid_for(nchunks), kBlock, 0, ctx->stream, a->ptr, a->idx,
-                     fv, cuts, nchunks, d);
-        else if (vec4 && d.nd == 64)
-          SFG_LAUNCH((k_spmm_merge_grp<TB, 2, 4, 4>), grid_for(nchunks), kBlock, 0, ctx->stream, a->ptr, a->idx,
-                     fv, cuts, nchunks, d);
-        else
-          SFG_LAUNCH((k_spmm_merge<TB, V>), grid_for(nchunks * chunks), kBlock, 0, ctx->stream, a->ptr, a->idx, fv,
-                     cuts, nchunks, d);
-      }
+      if (a->m == 0) break;
+      spmm_csr_merge<TB>(ctx, a, d);
       break;
     case SFG_DCSR: {
       if (stored_rows == 0) break;
@@ -709,9 +774,15 @@ void launch_fmt(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
                  (int32_t)a->m, (int32_t)a->k, d);
       break;
     case SFG_COO:
-      if (a->nnz)
-        SFG_LAUNCH((k_spmm_coo<TB, V>), grid_for(ceil_div(a->nnz, 32 * kCooIters) * chunks), kBlock,
-                   0, ctx->stream, a->row, a->idx, fv, a->nnz, d);
+      if (a->nnz) {
+        const int64_t nq = ceil_div(a->nnz, 32 * kCooIters);
+        const size_t row_b = ((size_t)nq * 4 + 15) & ~size_t(15);
+        char* s = static_cast<char*>(scratch(ctx, row_b + (size_t)nq * d.nd * 4));
+        Carry cy{reinterpret_cast<int32_t*>(s), reinterpret_cast<float*>(s + row_b)};
+        SFG_LAUNCH((k_spmm_coo<TB, V>), grid_for(nq * chunks), kBlock, 0, ctx->stream, a->row, a->idx, fv, a->nnz,
+                   d, cy);
+        SFG_LAUNCH(k_spmm_carry_fix, grid_for(nq), kBlock, 0, ctx->stream, cy, nq, d);
+      }
       break;
     case SFG_CSC:
       if (a->nnz)
@@ -778,7 +849,7 @@ void spmm(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dtype, int
     return;
   }
   bool zero_first =
-      !accumulate && (a->kind == SFG_COO || a->kind == SFG_CSC || a->kind == SFG_BCSR || a->kind == SFG_CSR);
+      !accumulate && (a->kind == SFG_COO || a->kind == SFG_CSC || a->kind == SFG_BCSR);
   if (zero_first && a->m > 0) {
     if (ldc == nd)
       SFG_CUDA(cudaMemsetAsync(c, 0, a->m * ldc * sizeof(float), ctx->stream));

@@ -9,6 +9,7 @@
 // association order; padded ELL slots are multiplied like the reference
 // (0 * x[0]); BCSR slots past M/N are guarded out.
 #include <cuda_bf16.h>
+#include <algorithm>
 
 #include "devutil.cuh"
 #include "internal.cuh"
@@ -137,12 +138,21 @@ __global__ void __launch_bounds__(kBlock) k_spmv_ell(const int32_t* __restrict__
 // `cur` whose per-lane partial sums live in `acc`: a step entirely inside
 // `cur` (the common case for long rows) is one add per lane and no
 // communication. A step that starts a new row closes `cur` (warp sum, one
-// RED); a step holding a row boundary reduces its segments with a
-// head-flag segmented scan (5 shuffles), RED-adds every segment but the
+// store); a step holding a row boundary reduces its segments with a
+// head-flag segmented scan (5 shuffles), stores every segment but the
 // last, and the last becomes the new `cur`.
-__device__ __forceinline__ void coo_close(float* __restrict__ y, int32_t row, float acc) {
-  float s = warp_sum(acc);
-  if ((threadIdx.x & 31) == 0 && row >= 0 && row != 0x7fffffff) atomicAdd(y + row, s);
+// No atomics: a row belongs to the chunk holding its last entry, which
+// stores it (y was zeroed first, or holds the accumulate input); a row
+// continuing past the chunk's end leaves its partial sum in the chunk's
+// carry slot, added in chunk order by k_carry_fix afterwards — y is
+// bit-identical from run to run (the reference reduces its thread partials
+// in worker order for the same reason, kernel.hpp:370-384).
+__device__ __forceinline__ void coo_put(float* __restrict__ y, int32_t row, float s, int acc) {
+  if (row >= 0 && row != 0x7fffffff) y[row] = acc ? y[row] + s : s;
+}
+__device__ __forceinline__ void coo_close(float* __restrict__ y, int32_t row, float acc, int accum) {
+  const float s = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) coo_put(y, row, s, accum);
 }
 
 // 12 steps with >= 4 CTAs per SM (56 registers) measured fastest on the
@@ -157,7 +167,9 @@ __global__ void __launch_bounds__(kBlock, SFG_COO_MINB) k_spmv_coo(const int32_t
                                                           const int32_t* __restrict__ col,
                                                           const float* __restrict__ val,
                                                           const float* __restrict__ x,
-                                                          float* __restrict__ y, int64_t nnz) {
+                                                          float* __restrict__ y, int64_t nnz, int accum,
+                                                          int32_t* __restrict__ carry_row,
+                                                          float* __restrict__ carry_val) {
   constexpr int32_t kNone = 0x7fffffff;  // past nnz: sorts after every row
   const int lane = threadIdx.x & 31;
   const int64_t span = 32 * kCooSteps;
@@ -186,7 +198,7 @@ __global__ void __launch_bounds__(kBlock, SFG_COO_MINB) k_spmv_coo(const int32_t
       const int32_t r0 = __shfl_sync(kFull, r[i], 0), r31 = __shfl_sync(kFull, r[i], 31);
       if (r0 == r31) {  // one row in this step (warp-uniform branch)
         if (r0 != cur) {
-          coo_close(y, cur, acc);
+          coo_close(y, cur, acc, accum);
           cur = r0;
           acc = 0.f;
         }
@@ -194,7 +206,7 @@ __global__ void __launch_bounds__(kBlock, SFG_COO_MINB) k_spmv_coo(const int32_t
       } else {
         // entries continuing `cur` join its partial sums, which close now
         const bool in_cur = r[i] == cur;
-        coo_close(y, cur, acc + (in_cur ? p[i] : 0.f));
+        coo_close(y, cur, acc + (in_cur ? p[i] : 0.f), accum);
         // segmented inclusive scan of the other entries, keyed by row
         const int32_t up = __shfl_up_sync(kFull, r[i], 1);
         const bool head = lane == 0 || up != r[i];
@@ -208,14 +220,40 @@ __global__ void __launch_bounds__(kBlock, SFG_COO_MINB) k_spmv_coo(const int32_t
         }
         const int32_t dn = __shfl_down_sync(kFull, r[i], 1);
         // segments ending before lane 31 are complete (rows are sorted)
-        if (lane < 31 && dn != r[i] && !in_cur && r[i] != kNone) atomicAdd(y + r[i], t);
+        if (lane < 31 && dn != r[i] && !in_cur) coo_put(y, r[i], t, accum);
         // the last segment stays open: its sum moves to lane 0's partial
         const float last = __shfl_sync(kFull, t, 31);
         cur = r31;
         acc = lane == 0 ? last : 0.f;
       }
     }
-    coo_close(y, cur, acc);  // the row may continue in the next chunk
+    // the last row: complete here unless the next chunk continues it
+    const int64_t e1 = (w + 1) * span;
+    const int32_t next = e1 < nnz ? __ldg(row + e1) : -1;
+    if (cur != next) {
+      coo_close(y, cur, acc, accum);
+      if (lane == 0) carry_row[w] = -1;
+    } else {
+      const float sum = warp_sum(acc);
+      if (lane == 0) {
+        carry_row[w] = cur;
+        carry_val[w] = sum;
+      }
+    }
+  }
+}
+
+// Adds each row's carries (chunk order) to the value its owning chunk
+// stored: a thread per chunk, the first chunk of a run of equal carry rows
+// sums the run.
+__global__ void k_carry_fix(const int32_t* __restrict__ crow, const float* __restrict__ cval, int64_t n,
+                            float* __restrict__ y) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = crow[q];
+    if (r < 0 || (q > 0 && crow[q - 1] == r)) continue;
+    float s = 0.f;
+    for (int64_t t = q; t < n && crow[t] == r; ++t) s += cval[t];
+    y[r] += s;
   }
 }
 
@@ -238,6 +276,9 @@ __global__ void __launch_bounds__(kBlock) k_spmv_csc(const int32_t* __restrict__
 // ---------------------------------------------------------------- BCSR
 // Warp per block row; lanes own (row-in-block) x (col-in-block) slots of
 // each block in turn. Slots past M/N are guarded out like the reference.
+// Each lane sums its slots into its own row partials (shared memory, one
+// column per lane); the rows' partials are then added in lane order, so y
+// is bit-identical from run to run.
 template <typename T>
 __device__ __forceinline__ float to_f(T v);
 template <>
@@ -255,15 +296,14 @@ __global__ void __launch_bounds__(kBlock) k_spmv_bcsr(const int32_t* __restrict_
                                                        float* __restrict__ y, int64_t nbr, int32_t m,
                                                        int32_t n, int32_t br, int32_t bc, int32_t rb,
                                                        int32_t cb, int acc) {
-  extern __shared__ float sh_rows[];  // [warps][rb]
+  extern __shared__ float sh_rows[];  // [warps][rb][32]: row i's partial of lane l at [i][l]
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
-  float* mine = sh_rows + wid * rb;
+  float* mine = sh_rows + wid * rb * 32;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int slots = rb * cb;
   for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nbr; b += warps) {
-    for (int i = lane; i < rb; i += 32) mine[i] = 0.f;
-    __syncwarp();
+    for (int i = 0; i < rb; ++i) mine[i * 32 + lane] = 0.f;
     int s = __ldg(ptr + b), e = __ldg(ptr + b + 1);
     for (int k = s; k < e; ++k) {
       int c0 = __ldg(bcol + k) * bc;
@@ -271,13 +311,15 @@ __global__ void __launch_bounds__(kBlock) k_spmv_bcsr(const int32_t* __restrict_
       for (int q = lane; q < slots; q += 32) {
         int i = q / cb, j = q - i * cb;
         int cc = c0 + j;
-        if (cc < n) atomicAdd(mine + i, to_f(blk[q]) * ldx(x, cc));
+        if (cc < n) mine[i * 32 + lane] += to_f(blk[q]) * ldx(x, cc);
       }
     }
     __syncwarp();
     for (int i = lane; i < rb; i += 32) {
       int64_t r = b * br + i;
-      if (r < m) y[r] = acc ? y[r] + mine[i] : mine[i];
+      float t = 0.f;
+      for (int l = 0; l < 32; ++l) t += mine[i * 32 + l];
+      if (r < m) y[r] = acc ? y[r] + t : t;
     }
     __syncwarp();
   }
@@ -318,9 +360,15 @@ void zero_y(sfg_context* ctx, float* y, int64_t m) {
 void spmv_coo(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, bool acc) {
   if (!acc) zero_y(ctx, y, a->m);
   if (a->nnz == 0) return;
-  int grid = stream_grid(ctx, ceil_div(a->nnz, 32 * kCooSteps), kBlock / 32, 1, 8);
+  const int64_t nchunks = ceil_div(a->nnz, 32 * kCooSteps);
+  int grid = stream_grid(ctx, nchunks, kBlock / 32, 1, 8);
+  char* s = static_cast<char*>(scratch(ctx, (size_t)nchunks * 8 + 16));
+  auto* crow = reinterpret_cast<int32_t*>(s);
+  auto* cval = reinterpret_cast<float*>(s + (((size_t)nchunks * 4 + 15) & ~size_t(15)));
   SFG_LAUNCH(k_spmv_coo, grid, kBlock, 0, ctx->stream, a->row, a->idx,
-             static_cast<const float*>(a->val), x, y, a->nnz);
+             static_cast<const float*>(a->val), x, y, a->nnz, acc ? 1 : 0, crow, cval);
+  SFG_LAUNCH(k_carry_fix, (int)std::min<int64_t>(ceil_div(nchunks, 256), (int64_t)ctx->sms * 8), 256, 0,
+             ctx->stream, crow, cval, nchunks, y);
 }
 
 void spmv_ell(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, bool acc) {
@@ -365,16 +413,26 @@ void spmv(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, bool 
     }
     case SFG_BCSR: {
       if (a->nbr == 0) break;
-      int grid = (int)std::min<int64_t>(ceil_div(a->nbr, kBlock / 32), (int64_t)ctx->sms * 16);
-      size_t smem = (kBlock / 32) * a->rb * sizeof(float);
-      if (a->dtype == SFG_BF16)
-        SFG_LAUNCH(k_spmv_bcsr<__nv_bfloat16_raw>, grid, kBlock, smem, ctx->stream, a->ptr, a->idx,
+      // per-lane row partials: rb KB of shared memory per warp
+      const size_t per_warp = (size_t)a->rb * 32 * sizeof(float);
+      const int wpb = (int)std::min<size_t>(kBlock / 32, (227u << 10) / per_warp);
+      if (wpb < 1) raise(SFG_ERR_INVALID_OPERATION, "BCSR SpMV: block rows > 1816 not supported");
+      const size_t smem = wpb * per_warp;
+      int grid = (int)std::min<int64_t>(ceil_div(a->nbr, wpb), (int64_t)ctx->sms * 16);
+      if (a->dtype == SFG_BF16) {
+        if (smem > (48u << 10))
+          SFG_CUDA(cudaFuncSetAttribute(k_spmv_bcsr<__nv_bfloat16_raw>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+        SFG_LAUNCH(k_spmv_bcsr<__nv_bfloat16_raw>, grid, wpb * 32, smem, ctx->stream, a->ptr, a->idx,
                    static_cast<const __nv_bfloat16_raw*>(a->val), x, y, a->nbr, (int)a->m, (int)a->n,
                    (int)a->br, (int)a->bc, (int)a->rb, (int)a->cb, acc);
-      else
-        SFG_LAUNCH(k_spmv_bcsr<float>, grid, kBlock, smem, ctx->stream, a->ptr, a->idx,
+      } else {
+        if (smem > (48u << 10))
+          SFG_CUDA(cudaFuncSetAttribute(k_spmv_bcsr<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        SFG_LAUNCH(k_spmv_bcsr<float>, grid, wpb * 32, smem, ctx->stream, a->ptr, a->idx,
                    static_cast<const float*>(a->val), x, y, a->nbr, (int)a->m, (int)a->n,
                    (int)a->br, (int)a->bc, (int)a->rb, (int)a->cb, acc);
+      }
       break;
     }
     case SFG_HYB:

@@ -4,8 +4,10 @@
 A step = one pass of the hot path over one synthetic matrix resident in HBM:
 canonical (row-sorted) COO -> format conversion -> SpMV/SpMM, i.e. the
 reference's convert_structure + materialize + run_kernel (planner.hpp:261,
-storage.hpp:97, kernel.hpp:236). Default workload: BASELINE config 2
-(hybrid ELL+COO conversion + SpMV on R-MAT scale 22, edge factor 16, T=8).
+storage.hpp:97, kernel.hpp:236). Default workload: BASELINE config 5
+(COO->CSR conversion + CSR SpMM N=32 fp32 on R-MAT scale 26, edge factor 16:
+the largest configuration that fits one GPU, and the one the north star
+row-partitions over 1/2/4/8 GPUs).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5]
                   [--impl ours|reference]
@@ -15,10 +17,13 @@ over all ranks (Mnnz/s; config 4, which has no conversion in the step, is
 reported in GFLOP/s). `e2e` runs the same step through the C-ABI with host
 buffers (from_coo from pinned host arrays, SpMV with host x / host y).
 `roofline` = dominant kernel family's algorithmic bytes / CUDA-event time vs
-the measured HBM copy peak. `cpu_baseline` / --impl reference = the
-unmodified reference (oracle/_ref) on a bounded row-block sample.
-N > 1 (torchrun): nnz-balanced row blocks of a weak-scaled matrix (R-MAT
-scale 22 + log2 N), y reassembled with an NCCL all-gather.
+the measured HBM copy peak (and vs the nominal 8 TB/s). `cpu_baseline` /
+--impl reference = the unmodified reference (oracle/_ref) on a bounded
+row-strided sample (every k-th row, so rows keep the matrix's average
+length), with the host's CPU model, core count and RAM.
+N > 1 (torchrun): nnz-balanced row blocks, the output reassembled with an
+NCCL all-gather; config 5 partitions the one scale-26 matrix (strong
+scaling), configs 1 and 2 grow the matrix with N (weak scaling).
 """
 from __future__ import annotations
 
@@ -37,6 +42,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "SpMV/SpMM GFLOP/s + achieved HBM GB/s; format conversion Mnnz/s"
+NOMINAL_HBM_GBS = 8000.0  # the north star's "roughly 8 TB/s"
 
 
 def load_peaks():
@@ -55,6 +61,7 @@ class Workload:
     (name, fn, algorithmic bytes, flops)."""
     unit = "Mnnz/s"
     fmt = ""
+    scaling = "weak"  # per-GPU work fixed as N grows (the matrix grows with N)
     has_cpu_sample = True  # bounded reference sample (cpu_baseline)
 
     def __init__(self, sfg, ctx, rank, world):
@@ -232,6 +239,7 @@ class Cfg5(SpmvWorkload):
     """CSR conversion + CSR SpMM N=32 fp32, R-MAT scale 26 (row-partitioned over N GPUs)"""
     fmt = "CSR"
     nd = 32
+    scaling = "strong"  # one scale-26 matrix split over the N GPUs
 
     def setup(self, torch):
         self.scale = 26
@@ -453,7 +461,10 @@ def run_ours(args):
     dom = max(kernels, key=lambda k: kernels[k]["ms"])
     ach = kernels[dom]["GB/s"]
     roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4),
-            "traffic": None, "kernel": dom, "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs"}
+            "traffic": None, "kernel": dom, "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs",
+            "peak_nominal": NOMINAL_HBM_GBS, "frac_nominal": round(ach / NOMINAL_HBM_GBS, 4)}
+    for k in kernels.values():
+        k["hbm_frac_nominal"] = round(k["GB/s"] / NOMINAL_HBM_GBS, 4)
     # DRAM bytes per launch of the dominant family, from the committed ncu
     # launch list of this config (profiles/traffic_config<N>.json)
     tpath = os.path.join(ROOT, "profiles", f"traffic_config{args.config}.json")
@@ -479,7 +490,7 @@ def run_ours(args):
         out = {
             "metric": METRIC, "value": round(value, 2), "unit": wl.unit, "n_gpus": world,
             "steps": args.steps, "warmup": warm, "ms_per_step": round(ms_per_step, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": wl.scaling, "vs_baseline": None,
             "dtype": "bf16" if args.config == 4 else "f32",
             "data": "synthetic (seeded generators, csrc/synth.h)",
             "config": {"workload": f"config {args.config}: {wl.describe()}", "format": wl.fmt,
@@ -565,23 +576,48 @@ def e2e_measure(args, sfg, ctx, wl, timed, torch, dist, world):
 
 
 # ------------------------------------------------------- reference (CPU) arm
+def host_info():
+    """CPU model, logical cores and RAM of this host (the CPU baseline's machine)."""
+    model, ram = "?", None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                ram = round(int(line.split()[1]) / 2**20, 1)
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "logical_cpus": os.cpu_count(), "ram_gib": ram}
+
+
+def sampled_rows(r, c, v, m, stride):
+    """About one row in `stride`, picked by a hash of the row id, renumbered
+    densely: the sample keeps the matrix's own row-length distribution (a
+    contiguous block, or every stride-th row, of an R-MAT matrix would not:
+    low row ids and ids with low zero bits are the heavy rows)."""
+    keep = ((np.arange(m, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)) >> np.uint64(40)) % np.uint64(stride) == 0
+    newid = np.cumsum(keep) - 1
+    sel = keep[r]
+    return int(keep.sum()), newid[r[sel]].astype(r.dtype), c[sel], v[sel]
+
+
 def reference_sample(config):
-    """Bounded row-block sample of the workload, from the oracle's generator
-    (the same matrix the GPU arm uses)."""
+    """Bounded row-strided sample of the workload, from the oracle's
+    generator (the same matrix the GPU arm uses)."""
     import oracle
     port = oracle.Port()
     if config == 1:
-        full = port.gen_uniform(1, 1 << 20, 1 << 20, 16)
-        rows = (0, 1 << 16)  # 1/16 of the rows: 1,048,576 nnz
+        full, stride = port.gen_uniform(1, 1 << 20, 1 << 20, 16), 16  # 65,536 rows, 1,048,576 nnz
     else:
-        full = port.gen_rmat(7, 22, 16 << 22)
-        rows = (1 << 20, (1 << 20) + (1 << 17))  # a mid-graph row block, ~5.2 M nnz
-    r, c, v = full.arrays()
-    sel = (r >= rows[0]) & (r < rows[1])
-    r, c, v = r[sel] - rows[0], c[sel], v[sel]
-    m, n = rows[1] - rows[0], full.shape[1]
+        full, stride = port.gen_rmat(7, 22, 16 << 22), 32  # 131,072 rows, ~2.0 M nnz
+    m, r, c, v = sampled_rows(*full.arrays(), full.shape[0], stride)
+    n = full.shape[1]
     x = port.gen_dense(3, n)
-    desc = f"rows [{rows[0]}, {rows[1]}) of the config-{config} matrix: {m} x {n}, {len(v)} nnz"
+    desc = (f"1/{stride} of the rows of the config-{config} matrix (hash-picked): {m} x {n}, {len(v)} nnz "
+            f"({len(v) / m:.2f} per row; the full matrix: {full.nnz / full.shape[0]:.2f})")
     return m, n, r, c, v, x, desc
 
 
@@ -633,16 +669,16 @@ def cpu_baseline(config, steps=1):
             lib.spmm(a, b, threads=threads)
         work = 2 * len(v) * 128 / 1e3  # MFLOP -> GFLOP/s below
     else:
-        # config 5 shape at scale 20 (scale <= 22), a row block
-        full = port.gen_rmat(7, 20, 16 << 20)
-        rr, cc, vv = full.arrays()
-        rows = (1 << 18, (1 << 18) + (1 << 16))
-        sel = (rr >= rows[0]) & (rr < rows[1])
-        r, c, v = rr[sel] - rows[0], cc[sel], vv[sel]
-        m, n = rows[1] - rows[0], 1 << 20
+        # config-5 generator at scale 22 (scale <= 22; at
+        # scale 26 the reference's f64 B alone is 17 GB), 1/16 of the rows
+        full = port.gen_rmat(7, 22, 16 << 22)
+        stride = 16
+        m, r, c, v = sampled_rows(*full.arrays(), full.shape[0], stride)
+        n = full.shape[1]
         b = port.gen_dense(3, n * 32).reshape(n, 32)
         coo = lib.from_coo(m, n, r, c, v)
-        desc = f"rows [{rows[0]}, {rows[1]}) of R-MAT scale 20 (config-5 generator): {m} x {n}, {len(v)} nnz, Nd = 32"
+        desc = (f"1/{stride} of the rows of R-MAT scale 22 (config-5 generator, hash-picked): {m} x {n}, "
+                f"{len(v)} nnz ({len(v) / m:.2f} per row; the full matrix: {full.nnz / full.shape[0]:.2f}), Nd = 32")
 
         def step():
             a = lib.convert(coo, "CSR")
@@ -656,7 +692,7 @@ def cpu_baseline(config, steps=1):
     sec = statistics.mean(times)
     return {"value": round(work / sec / 1e6, 4), "unit": unit, "cores": threads, "kind": kind,
             "sample": desc + f"; conversions single-threaded (as in the reference), run_kernel threads={threads}",
-            "sec_per_step": round(sec, 3)}
+            "host": host_info(), "sec_per_step": round(sec, 3)}
 
 
 def run_reference(args):
@@ -669,10 +705,10 @@ def run_reference(args):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": cb["unit"], "n_gpus": 0,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(cb["sec_per_step"] * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": wcls.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generators, csrc/synth.h)",
         "config": {"workload": f"config {args.config}: {doc}", "format": fmt},
-        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "host")},
         "e2e": {"value": cb["value"], "unit": cb["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -682,7 +718,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2, choices=sorted(WORKLOADS))
+    ap.add_argument("--config", type=int, default=5, choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--threshold", type=int, default=8, help="config 2: hybrid split threshold T")
     ap.add_argument("--rowpart", action="store_true",

@@ -147,6 +147,7 @@ int sfg_context_create(int device, void* stream, sfg_context** out) {
     ctx->device = device;
     ctx->stream = static_cast<cudaStream_t>(stream);
     ctx->sms = prop.multiProcessorCount;
+    ctx->total_mem = prop.totalGlobalMem;
     SFG_CUDA(cudaMallocHost(&ctx->pinned, 4096));
     // Keep freed blocks in the pool: conversions allocate and free per call.
     cudaMemPool_t pool;

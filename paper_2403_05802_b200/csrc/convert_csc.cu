@@ -176,31 +176,38 @@ __global__ void __launch_bounds__(kBlock) k_csc_unpack(const uint64_t* __restric
   }
 }
 
-// ---------------------------------------------- column-block partition path
-// Atomic-free in global memory and coalesced: (1) each of P CTAs counts its
-// contiguous share of the entries per column block of kBlkCols columns (in
-// shared memory); (2) an exclusive scan over (block, CTA) gives every CTA
-// its write range inside every block's region; (3) the CTAs scatter their
-// entries into those ranges (shared-memory cursors); (4) one CTA per column
-// block loads its <= kBlkCap entries, counts them per column in shared
-// memory, places them by column, insertion-sorts each (short) column by row
-// and writes idx / val / ptr for its columns with coalesced stores.
-constexpr int kBlkColBits = 10;
-constexpr int kBlkCols = 1 << kBlkColBits;  // columns per block
-constexpr int kBlkCap = 4096;               // entries one block CTA sorts in shared memory
-constexpr int kMaxBlks = 8192;              // shared-memory counters of steps 1 and 3
-constexpr int kPartCtas = 296;              // P (2 per SM)
+// --------------------------------------------- column-bucket partition path
+// Two passes, atomic-free in global memory and coalesced both ways.
+// (0) Each of P CTAs counts its contiguous share of the entries per column
+//     bucket (2^bits columns) in shared memory; an exclusive scan over
+//     (bucket, CTA) gives every CTA its write range inside every bucket.
+// (1) Each CTA reorders its share, kPartTile entries at a time, by bucket
+//     in shared memory and writes each bucket's run to the bucket's range:
+//     consecutive threads write consecutive addresses. The intermediate
+//     (row, value, column-in-bucket: 10 B an entry) is kept in L2 for pass 2.
+// (2) One CTA per bucket loads its <= kBucketCap entries, counts them per
+//     column, places them by column, insertion-sorts each (short) column by
+//     row — the stable order of the row-sorted input — and writes idx / val
+//     / ptr of its columns with coalesced stores.
+constexpr int kPartThreads = 512;
+constexpr int kPartPer = 24;                          // entries per thread per round
+constexpr int kPartTile = kPartThreads * kPartPer;    // 12,288 entries reordered per round
+constexpr int kMaxBuckets = 4096;
+constexpr int kMaxBucketBits = 12;                    // columns per bucket <= 4,096
+constexpr int kSortThreads = 1024;
+constexpr int kSortPer = 12;
+constexpr int kBucketCap = kSortThreads * kSortPer;   // 12,288 entries sorted per pass-2 CTA
 
-__global__ void __launch_bounds__(kBlock) k_blk_count(const int32_t* __restrict__ col, int64_t nnz, int nb,
-                                                       int32_t* __restrict__ counts) {
-  __shared__ int32_t h[kMaxBlks];
-  for (int i = threadIdx.x; i < nb; i += kBlock) h[i] = 0;
+__global__ void __launch_bounds__(kPartThreads) k_bkt_count(const int32_t* __restrict__ col, int64_t nnz, int bits,
+                                                             int nb, int32_t* __restrict__ counts) {
+  __shared__ int32_t h[kMaxBuckets];
+  for (int i = threadIdx.x; i < nb; i += kPartThreads) h[i] = 0;
   __syncthreads();
   const int64_t per = (nnz + gridDim.x - 1) / gridDim.x;
   const int64_t e0 = blockIdx.x * per, e1 = min(nnz, e0 + per);
-  for (int64_t e = e0 + threadIdx.x; e < e1; e += kBlock) atomicAdd(&h[ld_stream(col + e) >> kBlkColBits], 1);
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += kPartThreads) atomicAdd(&h[ld_stream(col + e) >> bits], 1);
   __syncthreads();
-  for (int b = threadIdx.x; b < nb; b += kBlock) counts[(int64_t)b * gridDim.x + blockIdx.x] = h[b];
+  for (int b = threadIdx.x; b < nb; b += kPartThreads) counts[(int64_t)b * gridDim.x + blockIdx.x] = h[b];
 }
 
 __global__ void __launch_bounds__(kBlock) k_blk_max(const int32_t* __restrict__ off, int nb, int p,
@@ -212,110 +219,154 @@ __global__ void __launch_bounds__(kBlock) k_blk_max(const int32_t* __restrict__ 
   if ((threadIdx.x & 31) == 0) atomicMax(mx, m);
 }
 
-// Entries travel as (row << kBlkColBits | column within the block, value):
-// rows must fit 32 - kBlkColBits bits (checked by the caller).
-__global__ void __launch_bounds__(kBlock) k_blk_scatter(const int32_t* __restrict__ row,
-                                                         const int32_t* __restrict__ col,
-                                                         const float* __restrict__ val, int64_t nnz, int nb,
-                                                         const int32_t* __restrict__ off,
-                                                         uint32_t* __restrict__ tkey, float* __restrict__ tval) {
-  __shared__ int32_t cur[kMaxBlks];
-  for (int b = threadIdx.x; b < nb; b += kBlock) cur[b] = off[(int64_t)b * gridDim.x + blockIdx.x];
-  __syncthreads();
-  // the scattered stores fill their lines over the whole pass: keep them in
-  // L2 (k_blk_sort reads them next) ahead of the streamed input
+// Pass 1. Dynamic shared memory: row, value, column of kPartTile entries,
+// then per-bucket count, start and write cursor.
+__global__ void __launch_bounds__(kPartThreads, 1) k_bkt_part(const int32_t* __restrict__ row,
+                                                               const int32_t* __restrict__ col,
+                                                               const float* __restrict__ val, int64_t nnz,
+                                                               int bits, int nb, const int32_t* __restrict__ off,
+                                                               int32_t* __restrict__ trow, float* __restrict__ tval,
+                                                               uint16_t* __restrict__ tcol) {
+  extern __shared__ int32_t sm[];
+  int32_t* s_row = sm;
+  float* s_val = reinterpret_cast<float*>(sm + kPartTile);
+  int32_t* s_col = sm + 2 * kPartTile;
+  int32_t* s_cnt = sm + 3 * kPartTile;
+  int32_t* s_start = s_cnt + kMaxBuckets;
+  int32_t* s_cur = s_start + kMaxBuckets;
+  __shared__ uint32_t scan_smem[34];
+  const int tid = threadIdx.x;
+  for (int b = tid; b < nb; b += kPartThreads) s_cur[b] = off[(int64_t)b * gridDim.x + blockIdx.x];
   const uint64_t once = l2_evict_first(), keep = l2_evict_last();
+  const uint32_t cmask = (1u << bits) - 1;
   const int64_t per = (nnz + gridDim.x - 1) / gridDim.x;
   const int64_t e0 = blockIdx.x * per, e1 = min(nnz, e0 + per);
-  constexpr int U = 4;  // entries per thread in flight
-  for (int64_t e = e0 + threadIdx.x; e < e1; e += U * kBlock) {
-    uint32_t c[U], r[U], v[U];
+  constexpr int kBPer = kMaxBuckets / kPartThreads;  // buckets per thread in the scan
+  for (int64_t base = e0; base < e1; base += kPartTile) {
+    const int cnt = (int)(e1 - base < kPartTile ? e1 - base : kPartTile);
+    for (int b = tid; b < nb; b += kPartThreads) s_cnt[b] = 0;
+    __syncthreads();
+    int r[kPartPer], c[kPartPer], rank[kPartPer];
+    float v[kPartPer];
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (e + u * kBlock < e1) {
-        c[u] = ld_hint(col + e + u * kBlock, once);
-        r[u] = ld_hint(row + e + u * kBlock, once);
-        v[u] = ld_hint(val + e + u * kBlock, once);
+    for (int k = 0; k < kPartPer; ++k) {
+      const int i = k * kPartThreads + tid;
+      if (i < cnt) {
+        c[k] = (int)ld_hint(col + base + i, once);
+        r[k] = (int)ld_hint(row + base + i, once);
+        v[k] = __uint_as_float(ld_hint(val + base + i, once));
       }
+    }
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (e + u * kBlock < e1) {
-        const int slot = atomicAdd(&cur[c[u] >> kBlkColBits], 1);
-        st_hint(tkey + slot, (r[u] << kBlkColBits) | (c[u] & (kBlkCols - 1)), keep);
-        st_hint(tval + slot, v[u], keep);
+    for (int k = 0; k < kPartPer; ++k)
+      if (k * kPartThreads + tid < cnt) rank[k] = atomicAdd(&s_cnt[c[k] >> bits], 1);
+    __syncthreads();
+    int loc[kBPer], sum = 0;
+#pragma unroll
+    for (int q = 0; q < kBPer; ++q) {
+      const int b = tid * kBPer + q;
+      loc[q] = b < nb ? s_cnt[b] : 0;
+      sum += loc[q];
+    }
+    uint32_t tot;
+    int run = (int)block_exclusive_scan<uint32_t, kPartThreads>((uint32_t)sum, scan_smem, &tot);
+#pragma unroll
+    for (int q = 0; q < kBPer; ++q) {
+      const int b = tid * kBPer + q;
+      if (b < nb) s_start[b] = run;
+      run += loc[q];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kPartPer; ++k)
+      if (k * kPartThreads + tid < cnt) {
+        const int pos = s_start[c[k] >> bits] + rank[k];
+        s_row[pos] = r[k];
+        s_val[pos] = v[k];
+        s_col[pos] = c[k];
       }
+    __syncthreads();
+    // bucket runs out: consecutive positions of a bucket go to consecutive
+    // addresses of the bucket's range
+    for (int p = tid; p < cnt; p += kPartThreads) {
+      const int cc = s_col[p], b = cc >> bits;
+      const int64_t dst = (int64_t)s_cur[b] + (p - s_start[b]);
+      st_hint(trow + dst, (uint32_t)s_row[p], keep);
+      st_hint(tval + dst, __float_as_uint(s_val[p]), keep);
+      tcol[dst] = (uint16_t)(cc & cmask);
+    }
+    __syncthreads();
+    for (int b = tid; b < nb; b += kPartThreads) s_cur[b] += s_cnt[b];
   }
 }
 
-constexpr int kSortThreads = 512;
-
-#ifndef SFG_BLKSORT_MINB
-#define SFG_BLKSORT_MINB 1  // 2 or 3 CTAs per SM measured the same (config 3)
-#endif
-__global__ void __launch_bounds__(kSortThreads, SFG_BLKSORT_MINB) k_blk_sort(const uint32_t* __restrict__ tkey,
-                                                      const float* __restrict__ tval,
-                                                      const int32_t* __restrict__ off, int p, int64_t n,
-                                                      int64_t nnz, int32_t* __restrict__ ptr,
-                                                      int32_t* __restrict__ orow, float* __restrict__ oval) {
-  constexpr int kPer = kBlkCap / kSortThreads;
-  __shared__ int32_t cnt[kBlkCols + 1];
+// Pass 2: a CTA per bucket. Static shared memory: sorted rows and values of
+// <= kBucketCap entries, per-column counts / starts.
+__global__ void __launch_bounds__(kSortThreads, 1) k_bkt_sort(const int32_t* __restrict__ trow,
+                                                               const float* __restrict__ tval,
+                                                               const uint16_t* __restrict__ tcol,
+                                                               const int32_t* __restrict__ off, int p, int bits,
+                                                               int64_t n, int64_t nnz, int32_t* __restrict__ ptr,
+                                                               int32_t* __restrict__ orow, float* __restrict__ oval) {
+  extern __shared__ int32_t sm2[];  // cnt[4096] | srow[kBucketCap] | sval[kBucketCap]
+  int32_t* cnt = sm2;
+  int32_t* srow = sm2 + (1 << kMaxBucketBits);
+  float* sval = reinterpret_cast<float*>(srow + kBucketCap);
   __shared__ uint32_t scan_smem[34];
-  __shared__ int32_t srow[kBlkCap];
-  __shared__ float sval[kBlkCap];
   const int b = blockIdx.x;
+  const int ncols_b = 1 << bits;
   const int32_t s = off[(int64_t)b * p], size = off[(int64_t)(b + 1) * p] - s;
-  const int64_t c0 = (int64_t)b << kBlkColBits;
-  const int ncols = n - c0 < kBlkCols ? (int)(n - c0) : kBlkCols;
-  for (int i = threadIdx.x; i < kBlkCols; i += kSortThreads) cnt[i] = 0;
+  const int64_t c0 = (int64_t)b << bits;
+  const int ncols = n - c0 < ncols_b ? (int)(n - c0) : ncols_b;
+  for (int i = threadIdx.x; i < ncols_b; i += kSortThreads) cnt[i] = 0;
   __syncthreads();
-  int r[kPer], c[kPer], slot[kPer];
-  float v[kPer];
+  // per entry: row, value, and (slot within its column << 16 | column)
+  int r[kSortPer], cs[kSortPer];
+  float v[kSortPer];
 #pragma unroll
-  for (int k = 0; k < kPer; ++k) {
+  for (int k = 0; k < kSortPer; ++k) {
     const int i = k * kSortThreads + threadIdx.x;
     if (i < size) {
-      const uint32_t key = tkey[s + i];
-      r[k] = (int)(key >> kBlkColBits);
-      c[k] = (int)(key & (kBlkCols - 1));
+      r[k] = trow[s + i];
       v[k] = tval[s + i];
+      cs[k] = tcol[s + i];
     }
   }
 #pragma unroll
-  for (int k = 0; k < kPer; ++k)
-    if (k * kSortThreads + threadIdx.x < size) slot[k] = atomicAdd(&cnt[c[k]], 1);
+  for (int k = 0; k < kSortPer; ++k)
+    if (k * kSortThreads + threadIdx.x < size) cs[k] |= atomicAdd(&cnt[cs[k]], 1) << 16;
   __syncthreads();
-  // exclusive scan of the per-column counts (kBlkCols / kBlock per thread)
-  constexpr int kColsPer = kBlkCols / kSortThreads;
-  int loc[kColsPer], sum = 0;
-#pragma unroll
-  for (int q = 0; q < kColsPer; ++q) {
-    loc[q] = cnt[threadIdx.x * kColsPer + q];
-    sum += loc[q];
-  }
+  // exclusive scan of the per-column counts; each thread owns a run of
+  // columns (ncols_b / kSortThreads, at least one)
+  const int per = ncols_b >= kSortThreads ? ncols_b / kSortThreads : 1;
+  const int cbeg = threadIdx.x * per;
+  int sum = 0;
+  for (int q = 0; q < per; ++q) sum += cbeg + q < ncols_b ? cnt[cbeg + q] : 0;
   uint32_t tot;
   int run = (int)block_exclusive_scan<uint32_t, kSortThreads>((uint32_t)sum, scan_smem, &tot);
-  int len[kColsPer];
-#pragma unroll
-  for (int q = 0; q < kColsPer; ++q) {
-    len[q] = loc[q];
-    cnt[threadIdx.x * kColsPer + q] = run;  // column start within the block
-    run += loc[q];
-  }
+  __syncthreads();
+  for (int q = 0; q < per; ++q)
+    if (cbeg + q < ncols_b) {
+      const int l = cnt[cbeg + q];
+      cnt[cbeg + q] = run;  // column start within the bucket
+      run += l;
+    }
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < kPer; ++k)
+  for (int k = 0; k < kSortPer; ++k)
     if (k * kSortThreads + threadIdx.x < size) {
-      const int pos = cnt[c[k]] + slot[k];
+      const int pos = cnt[cs[k] & 0xffff] + (cs[k] >> 16);
       srow[pos] = r[k];
       sval[pos] = v[k];
     }
   __syncthreads();
   // each column's rows in ascending order (columns are short; the reference
   // order is the stable sort of a row-sorted input)
-#pragma unroll
-  for (int q = 0; q < kColsPer; ++q) {
-    const int st = cnt[threadIdx.x * kColsPer + q], n_ = len[q];
-    for (int i = st + 1; i < st + n_; ++i) {
+  for (int q = 0; q < per; ++q) {
+    const int cq = cbeg + q;
+    if (cq >= ncols_b) break;
+    const int st = cnt[cq], en = cq + 1 < ncols_b ? cnt[cq + 1] : size;
+    for (int i = st + 1; i < en; ++i) {
       const int rr = srow[i];
       const float vv = sval[i];
       int j = i - 1;
@@ -345,14 +396,18 @@ int bits_for(int64_t extent) {
 
 }  // namespace
 
-// Column-block partition path (above); false when a block would exceed the
-// shared-memory sort (then the caller takes the histogram path).
-bool csc_by_column_blocks(sfg_context* ctx, const sfg_tensor* s, sfg_tensor* t) {
+// Column-bucket partition path (above); false when no bucket width fits
+// the shared-memory sort (then the caller takes the histogram path).
+bool csc_by_column_buckets(sfg_context* ctx, const sfg_tensor* s, sfg_tensor* t) {
   const int64_t n = s->n, nnz = s->nnz;
-  const int64_t nb = ceil_div(n, (int64_t)kBlkCols);
-  if (nb > kMaxBlks || nb * kBlkCap < nnz) return false;  // some block would overflow anyway
-  if (s->m > (int64_t(1) << (32 - kBlkColBits))) return false;  // rows travel in 22 bits
-  const int p = kPartCtas;
+  // fewest buckets (longest pass-1 runs) whose average fill is at most 3/4
+  // of a pass-2 CTA's capacity, with <= 4,096 columns per bucket
+  constexpr int64_t kAvgFill = kBucketCap * 3 / 4;
+  int bits = kMaxBucketBits;
+  while (bits > 0 && ceil_div(n, int64_t(1) << bits) * kAvgFill < nnz) --bits;
+  const int64_t nb = ceil_div(n, int64_t(1) << bits);
+  if (nb > kMaxBuckets || nb * kAvgFill < nnz) return false;
+  const int p = ctx->sms;  // one pass-1 CTA per SM (196 KB of shared memory each)
   const int64_t cells = nb * p;
   int32_t* counts = dalloc_n<int32_t>(ctx, cells);
   int32_t* off = dalloc_n<int32_t>(ctx, cells + 1);
@@ -361,28 +416,36 @@ bool csc_by_column_blocks(sfg_context* ctx, const sfg_tensor* s, sfg_tensor* t) 
   auto* status = lookback_status(ctx, tiles);
   auto* mx = static_cast<int32_t*>(scratch(ctx, 64));
   SFG_CUDA(cudaMemsetAsync(mx, 0, 8, ctx->stream));
-  SFG_LAUNCH(k_blk_count, p, kBlock, 0, ctx->stream, s->idx, nnz, (int)nb, counts);
+  SFG_LAUNCH(k_bkt_count, p, kPartThreads, 0, ctx->stream, s->idx, nnz, bits, (int)nb, counts);
   SFG_LAUNCH(k_count_scan, tiles, kBlock, 0, ctx->stream, counts, (int32_t)cells, off, dummy, status,
              ctx->epoch++, mx + 1);
   SFG_LAUNCH(k_blk_max, (int)std::min<int64_t>(ceil_div(nb, kBlock), 64), kBlock, 0, ctx->stream, off, (int)nb, p,
              mx);
-  // The scatter needs only the offsets: it is enqueued before the host
-  // waits for the largest block size, so that round trip overlaps it (an
-  // oversized block — rare — discards the scatter and takes the other path).
+  // Pass 1 needs only the offsets: it is enqueued before the host waits for
+  // the largest bucket, so that round trip overlaps it (an oversized bucket
+  // — rare — discards pass 1 and takes the other path).
   read_back_start(ctx, mx, sizeof(int32_t));
-  uint32_t* tkey = dalloc_n<uint32_t>(ctx, nnz);
+  int32_t* trow = dalloc_n<int32_t>(ctx, nnz);
   float* tval = dalloc_n<float>(ctx, nnz);
-  SFG_LAUNCH(k_blk_scatter, p, kBlock, 0, ctx->stream, s->row, s->idx, static_cast<const float*>(s->val), nnz,
-             (int)nb, off, tkey, tval);
+  uint16_t* tcol = dalloc_n<uint16_t>(ctx, nnz);
+  const size_t smem = (size_t)3 * kPartTile * 4 + (size_t)3 * kMaxBuckets * 4;
+  SFG_CUDA(cudaFuncSetAttribute(k_bkt_part, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SFG_LAUNCH(k_bkt_part, p, kPartThreads, smem, ctx->stream, s->row, s->idx, static_cast<const float*>(s->val), nnz,
+             bits, (int)nb, off, trow, tval, tcol);
   int32_t big = 0;
   read_back_wait(ctx, sizeof big, &big);
-  if (big > kBlkCap) {
-    for (void* q : {(void*)counts, (void*)off, (void*)dummy, (void*)tkey, (void*)tval}) dfree(ctx, q);
+  auto release = [&] {
+    for (void* q : {(void*)counts, (void*)off, (void*)dummy, (void*)trow, (void*)tval, (void*)tcol}) dfree(ctx, q);
+  };
+  if (big > kBucketCap) {
+    release();
     return false;
   }
-  SFG_LAUNCH(k_blk_sort, (int)nb, kSortThreads, 0, ctx->stream, tkey, tval, off, p, n, nnz, t->ptr, t->idx,
-             static_cast<float*>(t->val));
-  for (void* q : {(void*)counts, (void*)off, (void*)dummy, (void*)tkey, (void*)tval}) dfree(ctx, q);
+  const size_t smem2 = ((size_t)(1 << kMaxBucketBits) + 2 * kBucketCap) * 4;
+  SFG_CUDA(cudaFuncSetAttribute(k_bkt_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+  SFG_LAUNCH(k_bkt_sort, (int)nb, kSortThreads, smem2, ctx->stream, trow, tval, tcol, off, p, bits, n, nnz, t->ptr,
+             t->idx, static_cast<float*>(t->val));
+  release();
   return true;
 }
 
@@ -399,7 +462,7 @@ sfg_tensor* coo_to_csc(sfg_context* ctx, const sfg_tensor* s) {
     SFG_CUDA(cudaMemsetAsync(t->ptr, 0, (n + 1) * sizeof(int32_t), ctx->stream));
     return t;
   }
-  if (csc_by_column_blocks(ctx, s, t)) return t;
+  if (csc_by_column_buckets(ctx, s, t)) return t;
   int32_t* cnt = dalloc_n<int32_t>(ctx, n);
   int32_t* cursor = dalloc_n<int32_t>(ctx, n);
   int tiles = (int)ceil_div(n, kTile);

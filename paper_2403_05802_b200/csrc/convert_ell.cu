@@ -429,19 +429,13 @@ sfg_tensor* coo_to_hyb(sfg_context* ctx, const sfg_tensor* s, int64_t min_sum) {
   // (an upper bound) and its size set once known.
   //
   // The over-allocation (12 B for every entry not selected, held until the
-  // tensor is freed) is only taken while it is small next to the free
-  // device memory; otherwise the sizes are waited for and the COO part is
-  // allocated exactly.
+  // tensor is freed) is only taken while it is small next to the device's
+  // memory (an eighth of it); otherwise the sizes are waited for and the
+  // COO part is allocated exactly. (Not decided on cudaMemGetInfo: that
+  // call can block the host for milliseconds, and a decision flipping with
+  // the momentary free memory would change the allocation sizes per call.)
   const size_t upper = 12 * static_cast<size_t>(s->nnz);
-  bool defer = true;
-  if (upper > (size_t(256) << 20)) {
-    size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
-      cudaGetLastError();
-      free_b = 0;
-    }
-    defer = upper <= free_b / 4;
-  }
+  const bool defer = upper <= (size_t(256) << 20) || upper <= ctx->total_mem / 8;
   RowInfo ri = row_info(ctx, s, min_sum, nullptr, defer);
   sfg_tensor* h = new_tensor(ctx, SFG_HYB, s->m, s->n);
   h->threshold = min_sum;

@@ -52,6 +52,7 @@ struct sfg_context {
   int device = 0;
   cudaStream_t stream = nullptr;
   int sms = 148;
+  size_t total_mem = 0;         // device memory (bytes)
   int64_t* pinned = nullptr;   // small host scratch for size read-backs
   cudaEvent_t sizes_ev = nullptr;  // read_back_async completion
   // Deferred size read-backs owned by tensors (core.cu: size slots): pinned
@@ -121,6 +122,11 @@ template <class T>
 T* dalloc_n(sfg_context* ctx, int64_t n) {
   return static_cast<T*>(dalloc(ctx, static_cast<size_t>(n > 0 ? n : 1) * sizeof(T)));
 }
+
+// Adds carry slots (row[i] >= 0: partial sum val[i * nd ...] of that row;
+// runs of equal rows are consecutive) to C in slot order, without atomics:
+// a log-32 tree of k_carry_level passes (spmm.cu). Deterministic.
+void carry_fix(sfg_context* ctx, const int32_t* row, const float* val, int64_t n, int nd, float* c, int64_t ldc);
 
 // Scratch with at least `bytes` bytes (grows; contents undefined). Never
 // used for look-back status words.

@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(kBlock) k_spmm_rows(const int32_t* __restrict_
 // row's end item: rows with no entry are zeroed there (no memset of C), a
 // completed row stores this chunk's part of it. A row still open at the end
 // of a chunk leaves its partial sum in a carry slot (one per chunk), and
-// k_spmm_carry_fix adds the carries of each row in chunk order afterwards —
+// carry_fix adds the carries of each row in chunk order afterwards —
 // no atomics, so C is bit-identical from run to run (the reference reduces
 // its thread partials in worker order for the same reason, kernel.hpp:370-384).
 constexpr int kMergeItems = 1024;
@@ -400,24 +400,6 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_spmm_merge(const int32_t* __r
   }
 }
 
-// Adds each row's carries, in chunk order, to the value its completing
-// chunk stored. A warp per chunk; only the first chunk of a run carrying the
-// same row does the sum (runs: rows longer than a chunk).
-__global__ void __launch_bounds__(kBlock) k_spmm_carry_fix(Carry cy, int64_t nchunks, Dense d) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < nchunks; q += warps) {
-    const int r = __ldg(cy.row + q);
-    if (r < 0 || (q > 0 && __ldg(cy.row + q - 1) == r)) continue;
-    int64_t t1 = q + 1;
-    while (t1 < nchunks && __ldg(cy.row + t1) == r) ++t1;
-    for (int c = lane; c < d.nd; c += 32) {
-      float s = 0.f;
-      for (int64_t t = q; t < t1; ++t) s += __ldg(cy.val + t * d.nd + c);
-      d.c[(int64_t)r * d.ldc + c] += s;
-    }
-  }
-}
 
 // Short rows (DCSR / CSR, <= 8 entries per row on average): a warp owns R
 // consecutive stored rows, whose entries are one contiguous range. Lanes
@@ -561,7 +543,7 @@ __global__ void __launch_bounds__(kBlock) k_spmm_ell(const int32_t* __restrict__
 // belongs to the chunk holding its last entry (C was zeroed first, or holds
 // the accumulate input, so that chunk adds its part with a plain store); a
 // row continuing into the next chunk leaves its partial in the chunk's carry
-// slot, added in chunk order by k_spmm_carry_fix — no atomics.
+// slot, added in chunk order by carry_fix — no atomics.
 constexpr int kCooIters = 4;
 
 template <typename TB, int V>
@@ -730,7 +712,7 @@ void spmm_csr_merge(sfg_context* ctx, const sfg_tensor* a, Dense d) {
   else if (vec4 && d.nd % 128 == 0) SFG_MERGE(1, 4, 4, true, false, 5, d.nd / 128);
   else SFG_MERGE(1, 1, 8, false, false, 5, ceil_div(d.nd, 32));
 #undef SFG_MERGE
-  SFG_LAUNCH(k_spmm_carry_fix, grid_for(nchunks), kBlock, 0, ctx->stream, cy, nchunks, d);
+  carry_fix(ctx, cy.row, cy.val, nchunks, d.nd, d.c, d.ldc);
 }
 
 template <typename TB, int V>
@@ -781,7 +763,7 @@ void launch_fmt(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
         Carry cy{reinterpret_cast<int32_t*>(s), reinterpret_cast<float*>(s + row_b)};
         SFG_LAUNCH((k_spmm_coo<TB, V>), grid_for(nq * chunks), kBlock, 0, ctx->stream, a->row, a->idx, fv, a->nnz,
                    d, cy);
-        SFG_LAUNCH(k_spmm_carry_fix, grid_for(nq), kBlock, 0, ctx->stream, cy, nq, d);
+        carry_fix(ctx, cy.row, cy.val, nq, d.nd, d.c, d.ldc);
       }
       break;
     case SFG_CSC:
@@ -822,6 +804,140 @@ void launch_v(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
 }
 
 }  // namespace
+
+namespace {
+// One level of the carry reduction: a warp per group of 32 consecutive
+// carry slots. Rows with carries form runs of consecutive slots (a row
+// longer than a chunk); the warp walks its slots in order, lanes over the
+// columns, the group's values loaded up front. A run ending inside the
+// group is complete: its sum is added to C. The group is that row's only
+// writer at this level and the levels run in order, so the add is an
+// atomic only to make it a fire-and-forget reduction (a load-add-store
+// would stall the warp once per run); the result does not depend on
+// timing. The run still open at the group's end (the next slot carries the
+// same row) becomes the group's carry for the next level, which sees 32x
+// fewer slots.
+__device__ __forceinline__ void carry_group(const int32_t* __restrict__ in_row, const float* __restrict__ in_val,
+                                            int64_t n, int nd, float* __restrict__ c, int64_t ldc,
+                                            int32_t* __restrict__ out_row, float* __restrict__ out_val, int64_t g) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t0 = g * 32;
+  const int cnt = (int)(n - t0 < 32 ? n - t0 : 32);
+  const int rl = lane < cnt ? in_row[t0 + lane] : -1;
+  const int next = t0 + 32 < n ? in_row[t0 + 32] : -1;
+  const int last = __shfl_sync(kFull, rl, cnt - 1);
+  const bool open = last >= 0 && last == next;
+  if (nd == 1) {
+    // one value per slot: lane t holds slot t; a head-flag segmented scan
+    // (fixed shuffle order) sums each run, its last lane adds it
+    float t = rl >= 0 ? in_val[t0 + lane] : 0.f;
+    const int up = __shfl_up_sync(kFull, rl, 1);
+    const unsigned heads = __ballot_sync(kFull, lane == 0 || up != rl);
+    const int start = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const float u = __shfl_up_sync(kFull, t, o);
+      if (lane - o >= start) t += u;
+    }
+    const int dn = __shfl_down_sync(kFull, rl, 1);
+    const bool tail = lane == 31 || dn != rl;  // last slot of its run in this group
+    if (tail && rl >= 0) {
+      if (open && lane == cnt - 1) out_val[g] = t;
+      else atomicAdd(c + (int64_t)rl * ldc, t);
+    }
+  } else {
+    for (int cb = 0; cb < nd; cb += 32) {
+      const int col = cb + lane;
+      float acc = 0.f;
+      int cur = -1;
+      for (int t8 = 0; t8 < cnt; t8 += 8) {
+        float vv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int r = __shfl_sync(kFull, rl, (t8 + k) & 31);
+          vv[k] = t8 + k < cnt && r >= 0 && col < nd ? in_val[(t0 + t8 + k) * nd + col] : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int r = __shfl_sync(kFull, rl, (t8 + k) & 31);
+          if (t8 + k < cnt && r >= 0 && r != cur) {
+            if (cur >= 0 && col < nd) atomicAdd(c + (int64_t)cur * ldc + col, acc);
+            cur = r;
+            acc = 0.f;
+          }
+          acc += vv[k];
+        }
+      }
+      if (cur >= 0 && col < nd) {
+        if (open) out_val[g * nd + col] = acc;
+        else atomicAdd(c + (int64_t)cur * ldc + col, acc);
+      }
+    }
+  }
+  if (lane == 0) out_row[g] = open ? last : -1;
+}
+
+__global__ void __launch_bounds__(256) k_carry_level(const int32_t* __restrict__ in_row,
+                                                     const float* __restrict__ in_val, int64_t n, int nd,
+                                                     float* __restrict__ c, int64_t ldc,
+                                                     int32_t* __restrict__ out_row, float* __restrict__ out_val) {
+  const int64_t groups = (n + 31) / 32;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < groups; g += warps)
+    carry_group(in_row, in_val, n, nd, c, ldc, out_row, out_val, g);
+}
+
+// The last level: a warp per slot; the first slot of each run adds the
+// run's carries, in slot order, to C. Runs are short here (a row spanning
+// r chunks leaves a run of r / 32^levels slots).
+__global__ void __launch_bounds__(256) k_carry_runs(const int32_t* __restrict__ in_row,
+                                                    const float* __restrict__ in_val, int64_t n, int nd,
+                                                    float* __restrict__ c, int64_t ldc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < n; q += warps) {
+    const int r = in_row[q];
+    if (r < 0 || (q > 0 && in_row[q - 1] == r)) continue;
+    int64_t t1 = q + 1;
+    while (t1 < n && in_row[t1] == r) ++t1;
+    for (int col = lane; col < nd; col += 32) {
+      float acc = 0.f;
+      for (int64_t t = q; t < t1; ++t) acc += in_val[t * nd + col];
+      atomicAdd(c + (int64_t)r * ldc + col, acc);
+    }
+  }
+}
+}  // namespace
+
+void carry_fix(sfg_context* ctx, const int32_t* row, const float* val, int64_t n, int nd, float* c, int64_t ldc) {
+  if (n <= 0) return;
+  const int64_t n2 = (n + 31) / 32;
+  int32_t* rows[2] = {nullptr, nullptr};
+  float* vals[2] = {nullptr, nullptr};
+  if (n > 1024) {
+    rows[0] = dalloc_n<int32_t>(ctx, n2);
+    rows[1] = dalloc_n<int32_t>(ctx, n2);
+    vals[0] = dalloc_n<float>(ctx, n2 * nd);
+    vals[1] = dalloc_n<float>(ctx, n2 * nd);
+  }
+  const int32_t* ir = row;
+  const float* iv = val;
+  int lvl = 0;
+  while (n > 1024) {  // 32 slots to one per level
+    const int64_t groups = (n + 31) / 32;
+    const int grid = (int)std::min<int64_t>(ceil_div(groups, 8), (int64_t)ctx->sms * 16);
+    SFG_LAUNCH(k_carry_level, grid, 256, 0, ctx->stream, ir, iv, n, nd, c, ldc, rows[lvl & 1], vals[lvl & 1]);
+    ir = rows[lvl & 1];
+    iv = vals[lvl & 1];
+    n = groups;
+    ++lvl;
+  }
+  SFG_LAUNCH(k_carry_runs, (int)std::max<int64_t>(1, ceil_div(n, 8)), 256, 0, ctx->stream, ir, iv, n, nd, c, ldc);
+  for (int k = 0; k < 2; ++k) {
+    if (rows[k]) dfree(ctx, rows[k]);
+    if (vals[k]) dfree(ctx, vals[k]);
+  }
+}
 
 // Tensor-core BCSR path (bcsr_tc.cu); returns false when not applicable.
 bool spmm_bcsr_tc(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dtype, int64_t nd,

@@ -144,11 +144,17 @@ __global__ void __launch_bounds__(kBlock) k_spmv_ell(const int32_t* __restrict__
 // No atomics: a row belongs to the chunk holding its last entry, which
 // stores it (y was zeroed first, or holds the accumulate input); a row
 // continuing past the chunk's end leaves its partial sum in the chunk's
-// carry slot, added in chunk order by k_carry_fix afterwards — y is
+// carry slot, added in chunk order by carry_fix afterwards — y is
 // bit-identical from run to run (the reference reduces its thread partials
 // in worker order for the same reason, kernel.hpp:370-384).
 __device__ __forceinline__ void coo_put(float* __restrict__ y, int32_t row, float s, int acc) {
-  if (row >= 0 && row != 0x7fffffff) y[row] = acc ? y[row] + s : s;
+  // the owner is y[row]'s only writer in this kernel, so the accumulating
+  // add is an atomic only to make it a fire-and-forget reduction (RED): a
+  // load-add-store here would stall the warp on y[row]
+  if (row >= 0 && row != 0x7fffffff) {
+    if (acc) atomicAdd(y + row, s);
+    else y[row] = s;
+  }
 }
 __device__ __forceinline__ void coo_close(float* __restrict__ y, int32_t row, float acc, int accum) {
   const float s = warp_sum(acc);
@@ -175,6 +181,9 @@ __global__ void __launch_bounds__(kBlock, SFG_COO_MINB) k_spmv_coo(const int32_t
   const int64_t span = 32 * kCooSteps;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w * span < nnz; w += warps) {
+    // the first row of the next chunk (loaded with this chunk's entries)
+    const int64_t e1 = (w + 1) * span;
+    const int32_t next = e1 < nnz ? ld_stream(row + e1) : -1;
     int32_t r[kCooSteps];
     float p[kCooSteps];
     {
@@ -228,8 +237,6 @@ __global__ void __launch_bounds__(kBlock, SFG_COO_MINB) k_spmv_coo(const int32_t
       }
     }
     // the last row: complete here unless the next chunk continues it
-    const int64_t e1 = (w + 1) * span;
-    const int32_t next = e1 < nnz ? __ldg(row + e1) : -1;
     if (cur != next) {
       coo_close(y, cur, acc, accum);
       if (lane == 0) carry_row[w] = -1;
@@ -243,19 +250,6 @@ __global__ void __launch_bounds__(kBlock, SFG_COO_MINB) k_spmv_coo(const int32_t
   }
 }
 
-// Adds each row's carries (chunk order) to the value its owning chunk
-// stored: a thread per chunk, the first chunk of a run of equal carry rows
-// sums the run.
-__global__ void k_carry_fix(const int32_t* __restrict__ crow, const float* __restrict__ cval, int64_t n,
-                            float* __restrict__ y) {
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t r = crow[q];
-    if (r < 0 || (q > 0 && crow[q - 1] == r)) continue;
-    float s = 0.f;
-    for (int64_t t = q; t < n && crow[t] == r; ++t) s += cval[t];
-    y[r] += s;
-  }
-}
 
 // ---------------------------------------------------------------- CSC
 // Column-major walk: warp per column, scatter-add into y.
@@ -367,8 +361,7 @@ void spmv_coo(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, b
   auto* cval = reinterpret_cast<float*>(s + (((size_t)nchunks * 4 + 15) & ~size_t(15)));
   SFG_LAUNCH(k_spmv_coo, grid, kBlock, 0, ctx->stream, a->row, a->idx,
              static_cast<const float*>(a->val), x, y, a->nnz, acc ? 1 : 0, crow, cval);
-  SFG_LAUNCH(k_carry_fix, (int)std::min<int64_t>(ceil_div(nchunks, 256), (int64_t)ctx->sms * 8), 256, 0,
-             ctx->stream, crow, cval, nchunks, y);
+  carry_fix(ctx, crow, cval, nchunks, 1, y, 1);
 }
 
 void spmv_ell(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, bool acc) {

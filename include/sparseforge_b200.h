@@ -65,6 +65,11 @@ enum sfg_format_kind {
   SFG_BCSR = 5, /* (d0/r, d1/c, d0%r, d1%c); merge(0), trim(1,1) formats.hpp:49-53 */
   SFG_HYB = 6,  /* decompose by row count >= threshold: selected rows -> COO,
                    remaining rows -> ELL (the hybrid ELL+COO format)          */
+  /* Value-layout formats: Pack(0,1) (operators.hpp:424-430) stores the
+   * level-0..1 coordinates and the value of each entry as one record (AoS,
+   * storage.hpp:128-133) instead of separate arrays (SoA).                 */
+  SFG_DOK = 7,  /* COO + pack(0,1): records {row, col, val}      formats.hpp:40 */
+  SFG_LIL = 8,  /* CSR + pack(0,1): ptr[m+1] + records {col, val} formats.hpp:45 */
 };
 
 enum sfg_dtype { SFG_F32 = 0, SFG_BF16 = 1 };
@@ -103,6 +108,13 @@ typedef struct sfg_tensor_view {
   int64_t nvals;
   const void* values; /* device */
   const sfg_tensor* parts[2]; /* SFG_HYB: {ELL of remainder, COO of selection} */
+  /* ValueLayout (tensor.hpp:58-64): 0 SoA, 1 AoS over levels
+   * [aos_start, aos_end] (the Pack span). With AoS, the idx arrays of the
+   * packed levels and the values are interleaved records of record_words
+   * 32-bit words: element i of such an array is at pointer[i * record_words]. */
+  int32_t layout;
+  int32_t aos_start, aos_end;
+  int32_t record_words; /* 1 for SoA */
 } sfg_tensor_view;
 
 /* --------------------------------------------------------------- context */

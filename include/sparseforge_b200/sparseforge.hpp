@@ -168,6 +168,8 @@ inline std::string name_of(const sfg_format& f) {
     case SFG_ELL: return "ELL";
     case SFG_BCSR: return "BCSR(" + std::to_string(f.block_r) + "," + std::to_string(f.block_c) + ")";
     case SFG_HYB: return "HYB(" + std::to_string(f.threshold) + ")";
+    case SFG_DOK: return "DOK";
+    case SFG_LIL: return "LIL";
   }
   return "?";
 }
@@ -185,6 +187,8 @@ inline FormatEncoding resolve_format(const std::string& text) {
         {"map(d0,d1)->(d0,d1);merge(0),trim(1,1)", "CSR"},
         {"map(d0,d1)->(d1,d0);merge(0),trim(1,1)", "CSC"},
         {"map(d0,d1)->(d0,d1);merge(0),trim(0,1)", "DCSR"},
+        {"map(d0,d1)->(d0,d1);trim(0,1),pack(0,1)", "DOK"},
+        {"map(d0,d1)->(d0,d1);merge(0),trim(1,1),pack(0,1)", "LIL"},
     };
     for (const auto& [enc, name] : known)
       if (t == enc) return resolve_format(name);
@@ -236,8 +240,10 @@ inline StorageScheme infer_storage(const FormatEncoding& enc) {
   s.enc = enc;
   auto L = [](bool size, bool ptr, bool idx, bool dv) { return LevelStorage{size, ptr, idx, dv}; };
   switch (enc.fmt.kind) {
-    case SFG_COO: s.levels = {L(0, 0, 1, 0), L(0, 0, 1, 0)}; break;
+    case SFG_COO:
+    case SFG_DOK: s.levels = {L(0, 0, 1, 0), L(0, 0, 1, 0)}; break;
     case SFG_CSR:
+    case SFG_LIL:
     case SFG_CSC: s.levels = {L(1, 0, 0, 0), L(0, 1, 1, 0)}; break;
     case SFG_DCSR: s.levels = {L(0, 0, 1, 0), L(0, 1, 1, 0)}; break;
     case SFG_ELL: s.levels = {L(0, 0, 1, 0), L(1, 0, 0, 0), L(0, 0, 1, 0)}; break;
@@ -277,10 +283,20 @@ struct WorkingTensor {
   void download(std::vector<std::vector<std::int64_t>>& coords, std::vector<double>& values) const;
 };
 
+// ValueLayout (tensor.hpp:58-64): AoS over levels [aos_start, aos_end] after
+// Pack (operators.hpp:424-430); DOK and LIL carry pack(0,1).
+enum class ValueLayoutKind { SoA, AoS };
+struct ValueLayout {
+  ValueLayoutKind kind = ValueLayoutKind::SoA;
+  size_t aos_start = 0;
+  size_t aos_end = 0;
+};
+
 struct MaterializedTensor {
   TensorShape logical_shape;
   std::vector<MaterializedLevel> levels;
   std::vector<double> values;
+  ValueLayout layout;
   FormatEncoding enc;
   std::shared_ptr<b200::TensorHandle> dev;  // the device arrays behind the host copy
 };
@@ -291,6 +307,15 @@ std::vector<T> download_array(const void* dev, int64_t count) {
   std::vector<T> out(static_cast<size_t>(count));
   if (count > 0)
     check(sfgx_copy(default_context().get(), out.data(), dev, count * static_cast<int64_t>(sizeof(T)), 1));
+  return out;
+}
+// count elements at dev[i * stride] (stride > 1: a field of packed records)
+template <class T>
+std::vector<T> download_strided(const void* dev, int64_t count, int64_t stride) {
+  if (stride <= 1) return download_array<T>(dev, count);
+  std::vector<T> rec = download_array<T>(dev, count > 0 ? (count - 1) * stride + 1 : 0);
+  std::vector<T> out(static_cast<size_t>(count));
+  for (int64_t i = 0; i < count; ++i) out[static_cast<size_t>(i)] = rec[static_cast<size_t>(i * stride)];
   return out;
 }
 inline std::vector<std::int64_t> widen(const std::vector<std::int32_t>& v) {
@@ -308,7 +333,7 @@ inline std::vector<double> download_values(const sfg_tensor_view& v) {
     }
     return out;
   }
-  auto f = download_array<float>(v.values, v.nvals);
+  auto f = download_strided<float>(v.values, v.nvals, v.layout == 1 ? v.record_words : 1);
   return std::vector<double>(f.begin(), f.end());
 }
 }  // namespace b200
@@ -468,11 +493,14 @@ inline MaterializedTensor materialize(const WorkingTensor& t, const StorageSchem
                   (lv.storage & SFG_LEVEL_IDX) != 0, (lv.storage & SFG_LEVEL_DENSE_VECTOR) != 0};
     ml.bounds = {lv.lo, lv.hi};
     ml.node_count = static_cast<size_t>(lv.node_count);
-    ml.idx = b200::widen(b200::download_array<std::int32_t>(lv.idx, lv.idx_len));
+    const bool packed = v.layout == 1 && l >= v.aos_start && l <= v.aos_end;
+    ml.idx = b200::widen(b200::download_strided<std::int32_t>(lv.idx, lv.idx_len, packed ? v.record_words : 1));
     ml.ptr = b200::widen(b200::download_array<std::int32_t>(lv.ptr, lv.ptr_len));
     m.levels.push_back(std::move(ml));
   }
   m.values = b200::download_values(v);
+  if (v.layout == 1)
+    m.layout = {ValueLayoutKind::AoS, static_cast<size_t>(v.aos_start), static_cast<size_t>(v.aos_end)};
   return m;
 }
 

@@ -86,9 +86,11 @@ class Materialized:
     shape: tuple
     levels: list = field(default_factory=list)
     values: np.ndarray = None
+    layout: tuple = None  # AoS span (aos_start, aos_end) of a packed format; None: SoA
 
     def explain(self) -> str:
-        return " | ".join(f"L{i}: {lv.explain()}" for i, lv in enumerate(self.levels)) + " | val"
+        text = " | ".join(f"L{i}: {lv.explain()}" for i, lv in enumerate(self.levels)) + " | val"
+        return text + (f" | pack({self.layout[0]},{self.layout[1]})" if self.layout else "")
 
 
 class _Coo:
@@ -135,6 +137,11 @@ class _Mat:
         vals = np.zeros(int(f("mat_nvals")(self.h)), np.float64)
         f("mat_values")(self.h, _pf64(vals))
         out.values = vals
+        if hasattr(self._lib, self._p + "mat_layout"):  # the reference shim only
+            lay = np.zeros(3, np.int64)
+            f("mat_layout")(self.h, _p64(lay))
+            if lay[0] == 1:
+                out.layout = (int(lay[1]), int(lay[2]))
         return out
 
 

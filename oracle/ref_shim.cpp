@@ -186,6 +186,16 @@ int sfr_mat_values(void* h, double* out) {
   return 0;
 }
 
+// ValueLayout of the materialized tensor (tensor.hpp:58-64; set by Pack,
+// storage.hpp:128-133): {0 SoA / 1 AoS, aos_start, aos_end}.
+int sfr_mat_layout(void* h, int64_t out[3]) {
+  const auto& l = static_cast<RefMat*>(h)->m.layout;
+  out[0] = l.kind == ValueLayoutKind::AoS ? 1 : 0;
+  out[1] = static_cast<int64_t>(l.aos_start);
+  out[2] = static_cast<int64_t>(l.aos_end);
+  return 0;
+}
+
 void sfr_mat_free(void* h) { delete static_cast<RefMat*>(h); }
 
 int sfr_spmv(void* h, const double* x, double* y, int threads) {

@@ -22,7 +22,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_lib", "libsfg.so")
 
-KINDS = {"COO": 0, "CSR": 1, "CSC": 2, "DCSR": 3, "ELL": 4, "BCSR": 5, "HYB": 6}
+KINDS = {"COO": 0, "CSR": 1, "CSC": 2, "DCSR": 3, "ELL": 4, "BCSR": 5, "HYB": 6, "DOK": 7, "LIL": 8}
 KIND_NAMES = {v: k for k, v in KINDS.items()}
 F32, BF16 = 0, 1
 FLAG_SORTED, FLAG_SUM_DUPLICATES, FLAG_HOST = 1, 2, 4
@@ -60,7 +60,9 @@ class LevelView(C.Structure):
 class TensorView(C.Structure):
     _fields_ = [("kind", C.c_int32), ("value_dtype", C.c_int32), ("rows", C.c_int64),
                 ("cols", C.c_int64), ("nlevels", C.c_int32), ("level", LevelView * 4),
-                ("nvals", C.c_int64), ("values", C.c_void_p), ("parts", C.c_void_p * 2)]
+                ("nvals", C.c_int64), ("values", C.c_void_p), ("parts", C.c_void_p * 2),
+                ("layout", C.c_int32), ("aos_start", C.c_int32), ("aos_end", C.c_int32),
+                ("record_words", C.c_int32)]
 
 
 @dataclass
@@ -85,9 +87,11 @@ class Materialized:
     shape: tuple
     levels: list = field(default_factory=list)
     values: np.ndarray = None
+    layout: tuple = None  # AoS span (aos_start, aos_end) of a packed format; None: SoA
 
     def explain(self) -> str:
-        return " | ".join(f"L{i}: {lv.explain()}" for i, lv in enumerate(self.levels)) + " | val"
+        text = " | ".join(f"L{i}: {lv.explain()}" for i, lv in enumerate(self.levels)) + " | val"
+        return text + (f" | pack({self.layout[0]},{self.layout[1]})" if self.layout else "")
 
 
 _lib = None
@@ -300,12 +304,15 @@ class Tensor:
             t._parent = self  # the parts live in (and die with) this tensor
         return out
 
-    def _dl(self, ptr, dtype, count):
-        out = np.empty(int(count), dtype)
-        if out.nbytes:
+    def _dl(self, ptr, dtype, count, stride=1):
+        """count elements from device pointer ptr, element i at ptr[i * stride]
+        (stride > 1: a field of packed records)."""
+        out = np.empty(int(count) * int(stride), dtype)
+        nbytes = (int(count) - 1) * int(stride) * out.itemsize + out.itemsize if count else 0
+        if nbytes:
             _check(self.ctx.lib.sfgx_copy(self.ctx.h, out.ctypes.data_as(C.c_void_p), C.c_void_p(ptr),
-                                          out.nbytes, 1))
-        return out
+                                          nbytes, 1))
+        return np.ascontiguousarray(out[::int(stride)][:int(count)])
 
     def download(self):
         """Host copy shaped like the reference MaterializedTensor
@@ -313,9 +320,13 @@ class Tensor:
         the layout the oracle returns."""
         v = self.view()
         out = Materialized(KIND_NAMES[v.kind], (v.rows, v.cols))
+        rw = v.record_words if v.layout == 1 else 1
+        if v.layout == 1:
+            out.layout = (int(v.aos_start), int(v.aos_end))
         for i in range(v.nlevels):
             lv = v.level[i]
-            idx = self._dl(lv.idx, np.int32, lv.idx_len).astype(np.int64)
+            packed = v.layout == 1 and v.aos_start <= i <= v.aos_end
+            idx = self._dl(lv.idx, np.int32, lv.idx_len, rw if packed else 1).astype(np.int64)
             ptr = self._dl(lv.ptr, np.int32, lv.ptr_len).astype(np.int64)
             out.levels.append(Level(int(lv.storage), int(lv.lo), int(lv.hi),
                                            int(lv.node_count), idx, ptr))
@@ -323,7 +334,7 @@ class Tensor:
             raw = self._dl(v.values, np.uint16, v.nvals).astype(np.uint32) << 16
             out.values = raw.view(np.float32).astype(np.float64)
         else:
-            out.values = self._dl(v.values, np.float32, v.nvals).astype(np.float64)
+            out.values = self._dl(v.values, np.float32, v.nvals, rw).astype(np.float64)
         return out
 
     def coo_arrays(self):
@@ -446,12 +457,16 @@ class Context:
         """write_container (io.hpp:240): the USPT file of t's levels."""
         _check(self.lib.sfg_write_container(self.h, t.h, os.fsencode(path)))
 
-    def read_container(self, path: str, fmt: str, value_dtype: int = F32) -> Tensor:
-        """read_container (io.hpp:279) into a device tensor of format `fmt`."""
-        f = resolve_format(fmt)
-        f.value_dtype = value_dtype
+    def read_container(self, path: str, fmt: str | None = None, value_dtype: int = F32) -> Tensor:
+        """read_container (io.hpp:279) into a device tensor of format `fmt`
+        (None: the format the stored levels and layout tag name)."""
         h = C.c_void_p()
-        _check(self.lib.sfg_read_container(self.h, os.fsencode(path), C.byref(f), C.byref(h)))
+        if fmt is None:
+            _check(self.lib.sfg_read_container(self.h, os.fsencode(path), None, C.byref(h)))
+        else:
+            f = resolve_format(fmt)
+            f.value_dtype = value_dtype
+            _check(self.lib.sfg_read_container(self.h, os.fsencode(path), C.byref(f), C.byref(h)))
         return Tensor(self, h)
 
     def slice_rows(self, coo: Tensor, r0: int, r1: int) -> Tensor:

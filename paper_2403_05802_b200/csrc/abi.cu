@@ -85,6 +85,8 @@ std::string plan_for(const sfg_format& dst) {
              std::to_string(dst.threshold) +
              ")\nremainder: Sum(0)\nremainder: Enumerate(0)\nremainder: Sort\nremainder: Fill(1)\n"
              "remainder: Merge(0)\n";
+    case SFG_DOK: return "Pack(0,1)\n";
+    case SFG_LIL: return "Fill(0)\nMerge(0)\nPack(0,1)\n";
   }
   return "";
 }
@@ -100,12 +102,14 @@ std::string explain_for(const sfg_format& f) {
     case SFG_BCSR:
       return "L0: size | L1: ptr, idx | L2: size, dense_vector | L3: size, dense_vector | val";
     case SFG_HYB: return "ELL(L0: idx | L1: size | L2: idx | val) + COO(L0: idx | L1: idx | val)";
+    case SFG_DOK: return "L0: idx | L1: idx | val | pack(0,1)";
+    case SFG_LIL: return "L0: size | L1: ptr, idx | val | pack(0,1)";
   }
   return "";
 }
 
 void validate_format(const sfg_format& f) {
-  require(f.kind >= SFG_COO && f.kind <= SFG_HYB, SFG_ERR_PARSE, "unknown format kind");
+  require(f.kind >= SFG_COO && f.kind <= SFG_LIL, SFG_ERR_PARSE, "unknown format kind");
   if (f.kind == SFG_BCSR)
     require(f.block_r > 0 && f.block_c > 0, SFG_ERR_INVALID_OPERATION,
             "TileSplit factor must be positive");
@@ -230,6 +234,8 @@ int sfg_format_resolve(const char* text, sfg_format* out) {
     else if (name == "CSC") f.kind = SFG_CSC;
     else if (name == "DCSR") f.kind = SFG_DCSR;
     else if (name == "ELL") f.kind = SFG_ELL;
+    else if (name == "DOK") f.kind = SFG_DOK;
+    else if (name == "LIL") f.kind = SFG_LIL;
     else if (name == "BCSR") {
       // formats.hpp:49-53: r defaults to 2, c defaults to r
       f.kind = SFG_BCSR;
@@ -335,6 +341,8 @@ int sfg_convert(sfg_context* ctx, const sfg_tensor* src, const sfg_format* dst, 
         *out = sfg::coo_to_bcsr(ctx, src, dst->block_r, dst->block_c, dst->value_dtype);
         break;
       case SFG_HYB: *out = sfg::coo_to_hyb(ctx, src, dst->threshold); break;
+      case SFG_DOK: *out = sfg::coo_to_dok(ctx, src); break;
+      case SFG_LIL: *out = sfg::coo_to_lil(ctx, src); break;
     }
   });
 }
@@ -361,6 +369,7 @@ int sfg_tensor_view_get(sfg_context* ctx, const sfg_tensor* t, sfg_tensor_view* 
     v.rows = t->m;
     v.cols = t->n;
     v.values = t->val;
+    v.record_words = 1;
     const int S = SFG_LEVEL_SIZE, P = SFG_LEVEL_PTR, I = SFG_LEVEL_IDX, D = SFG_LEVEL_DENSE_VECTOR;
     switch (t->kind) {
       case SFG_COO:
@@ -409,6 +418,26 @@ int sfg_tensor_view_get(sfg_context* ctx, const sfg_tensor* t, sfg_tensor_view* 
         v.parts[0] = t->part[0];
         v.parts[1] = t->part[1];
         break;
+      case SFG_DOK: {  // records {row, col, val}
+        const int32_t* rec = static_cast<const int32_t*>(t->val);
+        v.nlevels = 2;
+        v.level[0] = level(I, 0, t->m - 1, t->nnz, t->nnz, rec, 0, nullptr);
+        v.level[1] = level(I, 0, t->n - 1, t->nnz, t->nnz, rec ? rec + 1 : nullptr, 0, nullptr);
+        v.values = rec ? rec + 2 : nullptr;
+        v.nvals = t->nnz;
+        v.layout = 1, v.aos_start = 0, v.aos_end = 1, v.record_words = 3;
+        break;
+      }
+      case SFG_LIL: {  // ptr + records {col, val}
+        const int32_t* rec = static_cast<const int32_t*>(t->val);
+        v.nlevels = 2;
+        v.level[0] = level(S, 0, t->m - 1, t->m, 0, nullptr, 0, nullptr);
+        v.level[1] = level(P | I, 0, t->n - 1, t->nnz, t->nnz, rec, t->m + 1, t->ptr);
+        v.values = rec ? rec + 1 : nullptr;
+        v.nvals = t->nnz;
+        v.layout = 1, v.aos_start = 0, v.aos_end = 1, v.record_words = 2;
+        break;
+      }
     }
     *out = v;
   });

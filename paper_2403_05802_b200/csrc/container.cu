@@ -95,6 +95,8 @@ std::vector<uint8_t> expected_kinds(int kind) {
     case SFG_DCSR: return {kUIdx, kUIdx | kUPtr};
     case SFG_ELL: return {kUIdx, kUSize, kUIdx};
     case SFG_BCSR: return {kUSize, kUIdx | kUPtr, kUSize | kUDense, kUSize | kUDense};
+    case SFG_DOK: return {kUIdx, kUIdx};           // COO + pack(0,1)
+    case SFG_LIL: return {kUSize, kUIdx | kUPtr};  // CSR + pack(0,1)
   }
   return {};
 }
@@ -133,6 +135,25 @@ void write_container(sfg_context* ctx, const sfg_tensor* t, const char* path_c) 
   if (t->kind == SFG_HYB) raise(SFG_ERR_INVALID_OPERATION, "the hybrid pair is two tensors: write each part");
   sfg_tensor_view v;
   if (int st = sfg_tensor_view_get(ctx, t, &v)) raise(st, "tensor view");
+  // a packed (AoS) tensor is written like its SoA base plus the layout tag
+  // (io.hpp:262-268): its records are split into plain arrays first
+  const void* values = t->val;
+  int32_t *ur = nullptr, *ui = nullptr;
+  float* uv = nullptr;
+  struct Unpacked {
+    sfg_context* ctx;
+    std::vector<void*> p;
+    ~Unpacked() {
+      for (void* q : p) dfree(ctx, q);
+    }
+  } unpacked{ctx, {}};
+  if (v.layout == 1) {
+    aos_unpack(ctx, t, &ur, &ui, &uv);
+    unpacked.p = {ur, ui, uv};
+    if (t->kind == SFG_DOK) v.level[0].idx = ur;
+    v.level[1].idx = ui;
+    values = uv;
+  }
   // layout: header bytes per piece, payload offsets
   struct Piece {
     int64_t off, n;
@@ -171,7 +192,13 @@ void write_container(sfg_context* ctx, const sfg_tensor* t, const char* path_c) 
   emit(head);
   const int64_t voff = off;
   off += 8 * v.nvals;
-  put(head, 0, 1);  // SoA
+  if (v.layout == 1) {  // AoS over levels [aos_start, aos_end]
+    put(head, 1, 1);
+    put(head, (uint64_t)v.aos_start, 1);
+    put(head, (uint64_t)v.aos_end, 1);
+  } else {
+    put(head, 0, 1);  // SoA
+  }
   put(head, 0, 4);  // no partitions
   emit(head);
   const int64_t size = off;
@@ -208,10 +235,10 @@ void write_container(sfg_context* ctx, const sfg_tensor* t, const char* path_c) 
       temps.push_back(w);
       if (t->dtype == SFG_BF16)
         SFG_LAUNCH(k_widen_val<__nv_bfloat16>, stream_grid(ctx, v.nvals, kBlock, 4, 8), kBlock, 0, ctx->stream,
-                   static_cast<const __nv_bfloat16*>(t->val), v.nvals, w);
+                   static_cast<const __nv_bfloat16*>(values), v.nvals, w);
       else
         SFG_LAUNCH(k_widen_val<float>, stream_grid(ctx, v.nvals, kBlock, 4, 8), kBlock, 0, ctx->stream,
-                   static_cast<const float*>(t->val), v.nvals, w);
+                   static_cast<const float*>(values), v.nvals, w);
       SFG_CUDA(cudaMemcpyAsync(host + voff, w, 8 * v.nvals, cudaMemcpyDeviceToHost, ctx->stream));
     }
     SFG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -267,8 +294,15 @@ sfg_tensor* read_container(sfg_context* ctx, const char* path_c, const sfg_forma
   if (pos + 8 * nvals > size) raise(SFG_ERR_IO, "truncated container");
   pos += 8 * nvals;
   const uint64_t tag = get(1);
-  if (tag == 1) raise(SFG_ERR_UNSUPPORTED_SOURCE, path + ": AoS value layouts are not held on the device");
-  if (tag != 0) raise(SFG_ERR_IO, path + ": bad layout tag");
+  if (tag > 1) raise(SFG_ERR_IO, path + ": bad layout tag");
+  uint64_t aos_start = 0, aos_end = 0;
+  if (tag == 1) {
+    aos_start = get(1);
+    aos_end = get(1);
+    // the device's packed formats: DOK / LIL, Pack(0,1) (formats.hpp:40,45)
+    if (aos_start != 0 || aos_end != 1)
+      raise(SFG_ERR_UNSUPPORTED_SOURCE, path + ": only the Pack(0,1) value layout (DOK / LIL) is held on the device");
+  }
   const uint64_t nparts = get(4);
   if (nparts) raise(SFG_ERR_UNSUPPORTED_SOURCE, path + ": partitioned containers are not held on the device");
 
@@ -287,6 +321,11 @@ sfg_tensor* read_container(sfg_context* ctx, const char* path_c, const sfg_forma
       if (same) found = k;
     }
     if (found < 0) raise(SFG_ERR_UNSUPPORTED_SOURCE, path + ": no device format has these levels");
+    if (tag == 1) {
+      if (found == SFG_COO) found = SFG_DOK;
+      else if (found == SFG_CSR) found = SFG_LIL;
+      else raise(SFG_ERR_UNSUPPORTED_SOURCE, path + ": packed layout over a format the device does not pack");
+    }
     fmt.kind = found;
     if (found == SFG_BCSR) {
       fmt.block_r = lv[2].hi - lv[2].lo + 1;
@@ -296,6 +335,7 @@ sfg_tensor* read_container(sfg_context* ctx, const char* path_c, const sfg_forma
   const auto want = expected_kinds(fmt.kind);
   bool ok = rank == 2 && lv.size() == want.size();
   for (size_t l = 0; ok && l < lv.size(); ++l) ok = lv[l].kind == want[l];
+  if (ok) ok = (tag == 1) == (fmt.kind == SFG_DOK || fmt.kind == SFG_LIL);
   if (!ok) raise(SFG_ERR_INVALID_OPERATION, path + ": the container does not hold this format");
   const int64_t m = ext[0], n = ext[1];
   if (m >= INT32_MAX || n >= INT32_MAX || nvals >= INT32_MAX)
@@ -334,6 +374,21 @@ sfg_tensor* read_container(sfg_context* ctx, const char* path_c, const sfg_forma
       dfree(ctx, tmp);
     }
     switch (fmt.kind) {
+      case SFG_DOK:
+      case SFG_LIL: {
+        const bool dok = fmt.kind == SFG_DOK;
+        t->nnz = lv[1].nidx;
+        int32_t* r = dok ? load_i(lv[0].idx_off, lv[0].nidx) : nullptr;
+        if (!dok) t->ptr = load_i(lv[1].ptr_off, lv[1].nptr);
+        int32_t* c = load_i(lv[1].idx_off, lv[1].nidx);
+        float* vals = static_cast<float*>(t->val);
+        t->val = dalloc_n<int32_t>(ctx, t->nnz * (dok ? 3 : 2));
+        aos_pack_into(ctx, t, r, c, vals);
+        dfree(ctx, r);
+        dfree(ctx, c);
+        dfree(ctx, vals);
+        break;
+      }
       case SFG_COO:
         t->nnz = lv[0].nidx;
         t->row = load_i(lv[0].idx_off, lv[0].nidx);

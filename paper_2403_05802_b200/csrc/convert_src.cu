@@ -298,6 +298,9 @@ sfg_tensor* deep_copy(sfg_context* ctx, const sfg_tensor* s) {
 sfg_tensor* convert_from_compressed(sfg_context* ctx, const sfg_tensor* s, const sfg_format& dst) {
   if (s->kind == SFG_ELL) raise(SFG_ERR_UNSUPPORTED_SOURCE, "conversion from a format with indirect levels");
   if (s->kind == SFG_HYB) raise(SFG_ERR_UNSUPPORTED_SOURCE, "conversion from the hybrid pair");
+  // planner.hpp:98-99: sources with a value layout are rejected
+  if (s->kind == SFG_DOK || s->kind == SFG_LIL)
+    raise(SFG_ERR_UNSUPPORTED_SOURCE, "conversion from a format with a value layout");
   const bool same = s->kind == dst.kind &&
                     (s->kind != SFG_BCSR || (s->br == dst.block_r && s->bc == dst.block_c && s->dtype == dst.value_dtype));
   if (same) return deep_copy(ctx, s);

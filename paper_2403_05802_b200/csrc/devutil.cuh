@@ -35,6 +35,28 @@ __device__ __forceinline__ float ld_stream(const float* p) {
   asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
   return r;
 }
+__device__ __forceinline__ int2 ld_stream(const int2* p) {
+  int2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.s32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
+}
+
+// (column, value) of entry k: separate arrays (S = 1), or the records of a
+// packed (AoS) format — {col, val} (S = 2, one 64-bit load) or {row, col,
+// val} (S = 3, col / val pointing at the record's fields).
+template <int S>
+__device__ __forceinline__ void ld_entry(const int32_t* __restrict__ col, const float* __restrict__ val, int64_t k,
+                                         int& c, float& v) {
+  if constexpr (S == 2) {
+    const int2 q = ld_stream(reinterpret_cast<const int2*>(col) + k);
+    c = q.x;
+    v = __int_as_float(q.y);
+  } else {
+    c = ld_stream(col + k * S);
+    v = ld_stream(val + k * S);
+  }
+}
+
 // Streaming stores: evict-first.
 __device__ __forceinline__ void st_stream(int4* p, int4 v) {
   asm volatile("st.global.cs.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),

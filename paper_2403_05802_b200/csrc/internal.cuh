@@ -209,6 +209,16 @@ sfg_tensor* coo_to_dcsr(sfg_context* ctx, const sfg_tensor* s);
 sfg_tensor* coo_to_ell(sfg_context* ctx, const sfg_tensor* s);
 sfg_tensor* coo_to_bcsr(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_t c, int dtype);
 sfg_tensor* coo_to_hyb(sfg_context* ctx, const sfg_tensor* s, int64_t min_sum);
+// Value-layout formats (pack.cu): Pack(0,1) over COO (DOK) / CSR (LIL).
+sfg_tensor* coo_to_dok(sfg_context* ctx, const sfg_tensor* s);
+sfg_tensor* coo_to_lil(sfg_context* ctx, const sfg_tensor* s);
+// A DOK / LIL tensor as separate arrays (new device arrays; row only for
+// DOK), e.g. for the container writer. The caller frees them (dfree).
+void aos_unpack(sfg_context* ctx, const sfg_tensor* t, int32_t** row, int32_t** idx, float** val);
+// A DOK / LIL tensor as a new COO / CSR tensor (the same entries, SoA).
+sfg_tensor* aos_to_soa(sfg_context* ctx, const sfg_tensor* t);
+// The reverse: records from separate arrays (t->val must hold nnz records).
+void aos_pack_into(sfg_context* ctx, sfg_tensor* t, const int32_t* row, const int32_t* idx, const float* val);
 void decompose_rows(sfg_context* ctx, const sfg_tensor* s, int64_t min_sum, sfg_tensor** sel,
                     sfg_tensor** rem, int32_t* totals);
 void row_partition(sfg_context* ctx, const sfg_tensor* coo, int parts, int64_t* bounds);

@@ -58,6 +58,14 @@ sfg_tensor* to_csr(sfg_context* ctx, const sfg_tensor* t) {
   f.kind = SFG_CSR;
   f.value_dtype = SFG_F32;
   if (t->kind == SFG_COO) return coo_to_csr(ctx, t);
+  if (t->kind == SFG_DOK || t->kind == SFG_LIL) {  // the layout is storage only: same entries
+    sfg_tensor* soa = aos_to_soa(ctx, t);
+    if (soa->kind == SFG_CSR) return soa;
+    sfg_tensor* csr = coo_to_csr(ctx, soa);
+    free_tensor_arrays(soa);
+    delete soa;
+    return csr;
+  }
   return convert_from_compressed(ctx, t, f);
 }
 

@@ -227,7 +227,8 @@ struct Carry {
 #ifndef SFG_MERGE_MINB
 #define SFG_MERGE_MINB 5  // CTAs per SM the register budget is sized for (config 5 SpMM: 5 -> 24.1 ms, 4 -> 25.1, 3 -> 25.1)
 #endif
-template <typename TB, int G, int V, int kU, bool kVec, bool kOne, int kMinB = SFG_MERGE_MINB>
+// S: entry stride (1 separate idx / val arrays; 2 LIL records {col, val}).
+template <typename TB, int G, int V, int kU, bool kVec, bool kOne, int kMinB, int S>
 __global__ void __launch_bounds__(kBlock, kMinB) k_spmm_merge(const int32_t* __restrict__ ptr,
                                                                const int32_t* __restrict__ col,
                                                                const float* __restrict__ val,
@@ -306,8 +307,9 @@ __global__ void __launch_bounds__(kBlock, kMinB) k_spmm_merge(const int32_t* __r
     };
     for (int base = j0; base < j1; base += 32) {
       const int e = base + lane;
-      const int mc = e < j1 ? ld_stream(col + e) : 0;  // past the chunk: col 0, value 0
-      const float mv = e < j1 ? ld_stream(val + e) : 0.f;
+      int mc = 0;  // past the chunk: col 0, value 0
+      float mv = 0.f;
+      if (e < j1) ld_entry<S>(col, val, e, mc, mv);
       const int cnt = min(32, j1 - base);
       for (int t0 = 0; t0 < cnt; t0 += kStep) {
         const int last = base + min(t0 + kStep, cnt) - 1;
@@ -546,7 +548,8 @@ __global__ void __launch_bounds__(kBlock) k_spmm_ell(const int32_t* __restrict__
 // slot, added in chunk order by carry_fix — no atomics.
 constexpr int kCooIters = 4;
 
-template <typename TB, int V>
+// S: entry stride (1 separate arrays; 3 DOK records {row, col, val}).
+template <typename TB, int V, int S>
 __global__ void __launch_bounds__(kBlock) k_spmm_coo(const int32_t* __restrict__ row,
                                                       const int32_t* __restrict__ col,
                                                       const float* __restrict__ val, int64_t nnz,
@@ -563,15 +566,15 @@ __global__ void __launch_bounds__(kBlock) k_spmm_coo(const int32_t* __restrict__
     const int cc = (int)(w - q * chunks);
     int c0 = cc * 32 * V + lane * V;
     int64_t e0 = q * span, e1 = min(nnz, e0 + span);
-    int cur = __ldg(row + e0);
+    int cur = __ldg(row + e0 * S);
     float acc[V];
 #pragma unroll
     for (int i = 0; i < V; ++i) acc[i] = 0.f;
     for (int64_t base = e0; base < e1; base += 32) {
       int64_t k = base + lane;
-      int mr = k < e1 ? __ldg(row + k) : -1;
-      int mc = k < e1 ? __ldg(col + k) : 0;
-      float mv = k < e1 ? __ldg(val + k) : 0.f;
+      int mr = k < e1 ? __ldg(row + k * S) : -1;
+      int mc = k < e1 ? __ldg(col + k * S) : 0;
+      float mv = k < e1 ? __ldg(val + k * S) : 0.f;
       int cnt = (int)(e1 - base < 32 ? e1 - base : 32);
       for (int j = 0; j < cnt; ++j) {
         int rj = __shfl_sync(kFull, mr, j);
@@ -584,7 +587,7 @@ __global__ void __launch_bounds__(kBlock) k_spmm_coo(const int32_t* __restrict__
         fma_row<TB, V>(d, __shfl_sync(kFull, mc, j), __shfl_sync(kFull, mv, j), c0, vec_ok, acc);
       }
     }
-    const int next = e1 < nnz ? __ldg(row + e1) : -1;
+    const int next = e1 < nnz ? __ldg(row + e1 * S) : -1;
     if (cur != next) {
       store_row<V>(d, cur, c0, false, acc);
     } else {
@@ -678,8 +681,8 @@ __global__ void __launch_bounds__(kBlock) k_spmm_bcsr(const int32_t* __restrict_
   }
 }
 
-template <typename TB>
-void spmm_csr_merge(sfg_context* ctx, const sfg_tensor* a, Dense d) {
+template <typename TB, int S>
+void spmm_csr_merge(sfg_context* ctx, const sfg_tensor* a, const int32_t* col, const float* fv, Dense d) {
   const int64_t total = a->m + a->nnz;
   const int64_t nchunks = ceil_div(total, kMergeItems);
   // scratch: cuts[nchunks + 1] | carry rows[nchunks] | carry values[nchunks][nd]
@@ -697,10 +700,9 @@ void spmm_csr_merge(sfg_context* ctx, const sfg_tensor* a, Dense d) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(warps_needed, kBlock / 32), (int64_t)ctx->sms * 16));
   };
   const int32_t m = (int32_t)a->m;
-  const float* fv = static_cast<const float*>(a->val);
-#define SFG_MERGE(G, V, U, VEC, ONE, MB, CC)                                                                   \
-  SFG_LAUNCH((k_spmm_merge<TB, G, V, U, VEC, ONE, MB>), grid_for(nchunks * (CC)), kBlock, 0, ctx->stream, \
-             a->ptr, a->idx, fv, cuts, nchunks, m, d, cy)
+#define SFG_MERGE(G, V, U, VEC, ONE, MB, CC)                                                                      \
+  SFG_LAUNCH((k_spmm_merge<TB, G, V, U, VEC, ONE, MB, S>), grid_for(nchunks * (CC)), kBlock, 0, ctx->stream, \
+             a->ptr, col, fv, cuts, nchunks, m, d, cy)
   // nd = 32 on config 5 (SpMM ms): this unrolled step, 5 CTAs/SM 24.6;
   // 4 CTAs/SM 24.9; kU = 2 at 6 CTAs/SM 25.3; the row-end path as a rolled
   // loop (smaller code, more instructions) 26.3; the first version of this
@@ -732,8 +734,14 @@ void launch_fmt(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
   switch (a->kind) {
     case SFG_CSR:
       if (a->m == 0) break;
-      spmm_csr_merge<TB>(ctx, a, d);
+      spmm_csr_merge<TB, 1>(ctx, a, a->idx, fv, d);
       break;
+    case SFG_LIL: {
+      if (a->m == 0) break;
+      const auto* rec = static_cast<const int32_t*>(a->val);
+      spmm_csr_merge<TB, 2>(ctx, a, rec, reinterpret_cast<const float*>(rec + 1), d);
+      break;
+    }
     case SFG_DCSR: {
       if (stored_rows == 0) break;
       const int32_t* rows = a->kind == SFG_DCSR ? a->row : nullptr;
@@ -756,13 +764,20 @@ void launch_fmt(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
                  (int32_t)a->m, (int32_t)a->k, d);
       break;
     case SFG_COO:
+    case SFG_DOK:
       if (a->nnz) {
         const int64_t nq = ceil_div(a->nnz, 32 * kCooIters);
         const size_t row_b = ((size_t)nq * 4 + 15) & ~size_t(15);
         char* s = static_cast<char*>(scratch(ctx, row_b + (size_t)nq * d.nd * 4));
         Carry cy{reinterpret_cast<int32_t*>(s), reinterpret_cast<float*>(s + row_b)};
-        SFG_LAUNCH((k_spmm_coo<TB, V>), grid_for(nq * chunks), kBlock, 0, ctx->stream, a->row, a->idx, fv, a->nnz,
-                   d, cy);
+        if (a->kind == SFG_DOK) {  // records {row, col, val}
+          const auto* rec = static_cast<const int32_t*>(a->val);
+          SFG_LAUNCH((k_spmm_coo<TB, V, 3>), grid_for(nq * chunks), kBlock, 0, ctx->stream, rec, rec + 1,
+                     reinterpret_cast<const float*>(rec + 2), a->nnz, d, cy);
+        } else {
+          SFG_LAUNCH((k_spmm_coo<TB, V, 1>), grid_for(nq * chunks), kBlock, 0, ctx->stream, a->row, a->idx, fv,
+                     a->nnz, d, cy);
+        }
         carry_fix(ctx, cy.row, cy.val, nq, d.nd, d.c, d.ldc);
       }
       break;
@@ -965,7 +980,7 @@ void spmm(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dtype, int
     return;
   }
   bool zero_first =
-      !accumulate && (a->kind == SFG_COO || a->kind == SFG_CSC || a->kind == SFG_BCSR);
+      !accumulate && (a->kind == SFG_COO || a->kind == SFG_DOK || a->kind == SFG_CSC || a->kind == SFG_BCSR);
   if (zero_first && a->m > 0) {
     if (ldc == nd)
       SFG_CUDA(cudaMemsetAsync(c, 0, a->m * ldc * sizeof(float), ctx->stream));

@@ -29,7 +29,8 @@ __device__ __forceinline__ float ldx(const float* __restrict__ x, int c) { retur
 // col -> x gathers in flight (the gathers, not HBM, bound CSR SpMV on random
 // columns). Entries are strided by G inside a row (coalesced idx/val
 // streams); partial sums reduce inside the lane group with shuffles.
-template <int G, int R>
+// S: entry stride (1 separate idx / val arrays; 2 LIL records).
+template <int G, int R, int S>
 __global__ void __launch_bounds__(kBlock) k_spmv_csr(const int32_t* __restrict__ ptr,
                                                       const int32_t* __restrict__ col,
                                                       const float* __restrict__ val,
@@ -62,8 +63,8 @@ __global__ void __launch_bounds__(kBlock) k_spmv_csr(const int32_t* __restrict__
 #pragma unroll
       for (int i = 0; i < R; ++i) {
         bool ok = s[i] + t < e[i];
-        c[i] = ok ? ld_stream(col + s[i] + t) : 0;
-        v[i] = ok ? ld_stream(val + s[i] + t) : 0.f;
+        c[i] = 0, v[i] = 0.f;
+        if (ok) ld_entry<S>(col, val, s[i] + t, c[i], v[i]);
       }
 #pragma unroll
       for (int i = 0; i < R; ++i)
@@ -169,6 +170,8 @@ constexpr int kCooSteps = 12;
 #ifndef SFG_COO_MINB
 #define SFG_COO_MINB 4  // config 2 SpMV: 4 -> 0.291 ms; 5 -> 0.331 (spills); 6 -> 0.376
 #endif
+// S: entry stride (1 separate arrays; 3 DOK records {row, col, val}).
+template <int S>
 __global__ void __launch_bounds__(kBlock, SFG_COO_MINB) k_spmv_coo(const int32_t* __restrict__ row,
                                                           const int32_t* __restrict__ col,
                                                           const float* __restrict__ val,
@@ -183,7 +186,7 @@ __global__ void __launch_bounds__(kBlock, SFG_COO_MINB) k_spmv_coo(const int32_t
   for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w * span < nnz; w += warps) {
     // the first row of the next chunk (loaded with this chunk's entries)
     const int64_t e1 = (w + 1) * span;
-    const int32_t next = e1 < nnz ? ld_stream(row + e1) : -1;
+    const int32_t next = e1 < nnz ? ld_stream(row + e1 * S) : -1;
     int32_t r[kCooSteps];
     float p[kCooSteps];
     {
@@ -193,9 +196,9 @@ __global__ void __launch_bounds__(kBlock, SFG_COO_MINB) k_spmv_coo(const int32_t
       for (int i = 0; i < kCooSteps; ++i) {
         int64_t e = w * span + 32 * i + lane;
         bool ok = e < nnz;
-        r[i] = ok ? ld_stream(row + e) : kNone;
-        c[i] = ok ? ld_stream(col + e) : 0;
-        v[i] = ok ? ld_stream(val + e) : 0.f;
+        r[i] = ok ? ld_stream(row + e * S) : kNone;
+        c[i] = ok ? ld_stream(col + e * S) : 0;
+        v[i] = ok ? ld_stream(val + e * S) : 0.f;
       }
 #pragma unroll
       for (int i = 0; i < kCooSteps; ++i) p[i] = v[i] * ldx(x, c[i]);
@@ -329,7 +332,9 @@ int pick_group(double avg) {
   return 32;
 }
 
-void spmv_csr(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, bool acc) {
+template <int S>
+void spmv_csr_s(sfg_context* ctx, const sfg_tensor* a, const int32_t* col, const float* v, const float* x, float* y,
+                bool acc) {
   if (a->m == 0) return;
   int g = pick_group(a->m ? double(a->nnz) / double(a->m) : 0);
   const int R = 4;
@@ -337,13 +342,21 @@ void spmv_csr(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, b
   // against a cap of 16 (64: 0.090)
   int grid = (int)std::min<int64_t>(ceil_div(a->m, (int64_t)(kBlock / g) * R), (int64_t)ctx->sms * 32);
   if (grid < 1) grid = 1;
-  auto v = static_cast<const float*>(a->val);
   switch (g) {
-    case 2: SFG_LAUNCH((k_spmv_csr<2, 1>), (int)std::min<int64_t>(ceil_div(a->m, kBlock / 2), (int64_t)ctx->sms * 16), kBlock, 0, ctx->stream, a->ptr, a->idx, v, x, y, (int)a->m, acc); break;
-    case 4: SFG_LAUNCH((k_spmv_csr<4, 3>), (int)std::min<int64_t>(ceil_div(a->m, (kBlock / 4) * 3), (int64_t)ctx->sms * 16), kBlock, 0, ctx->stream, a->ptr, a->idx, v, x, y, (int)a->m, acc); break;
-    case 8: SFG_LAUNCH((k_spmv_csr<8, R>), grid, kBlock, 0, ctx->stream, a->ptr, a->idx, v, x, y, (int)a->m, acc); break;
-    case 16: SFG_LAUNCH((k_spmv_csr<16, R>), grid, kBlock, 0, ctx->stream, a->ptr, a->idx, v, x, y, (int)a->m, acc); break;
-    default: SFG_LAUNCH((k_spmv_csr<32, R>), grid, kBlock, 0, ctx->stream, a->ptr, a->idx, v, x, y, (int)a->m, acc); break;
+    case 2: SFG_LAUNCH((k_spmv_csr<2, 1, S>), (int)std::min<int64_t>(ceil_div(a->m, kBlock / 2), (int64_t)ctx->sms * 16), kBlock, 0, ctx->stream, a->ptr, col, v, x, y, (int)a->m, acc); break;
+    case 4: SFG_LAUNCH((k_spmv_csr<4, 3, S>), (int)std::min<int64_t>(ceil_div(a->m, (kBlock / 4) * 3), (int64_t)ctx->sms * 16), kBlock, 0, ctx->stream, a->ptr, col, v, x, y, (int)a->m, acc); break;
+    case 8: SFG_LAUNCH((k_spmv_csr<8, R, S>), grid, kBlock, 0, ctx->stream, a->ptr, col, v, x, y, (int)a->m, acc); break;
+    case 16: SFG_LAUNCH((k_spmv_csr<16, R, S>), grid, kBlock, 0, ctx->stream, a->ptr, col, v, x, y, (int)a->m, acc); break;
+    default: SFG_LAUNCH((k_spmv_csr<32, R, S>), grid, kBlock, 0, ctx->stream, a->ptr, col, v, x, y, (int)a->m, acc); break;
+  }
+}
+
+void spmv_csr(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, bool acc) {
+  if (a->kind == SFG_LIL) {
+    const auto* rec = static_cast<const int32_t*>(a->val);
+    spmv_csr_s<2>(ctx, a, rec, reinterpret_cast<const float*>(rec + 1), x, y, acc);
+  } else {
+    spmv_csr_s<1>(ctx, a, a->idx, static_cast<const float*>(a->val), x, y, acc);
   }
 }
 
@@ -359,8 +372,14 @@ void spmv_coo(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, b
   char* s = static_cast<char*>(scratch(ctx, (size_t)nchunks * 8 + 16));
   auto* crow = reinterpret_cast<int32_t*>(s);
   auto* cval = reinterpret_cast<float*>(s + (((size_t)nchunks * 4 + 15) & ~size_t(15)));
-  SFG_LAUNCH(k_spmv_coo, grid, kBlock, 0, ctx->stream, a->row, a->idx,
-             static_cast<const float*>(a->val), x, y, a->nnz, acc ? 1 : 0, crow, cval);
+  if (a->kind == SFG_DOK) {  // records {row, col, val}
+    const auto* rec = static_cast<const int32_t*>(a->val);
+    SFG_LAUNCH(k_spmv_coo<3>, grid, kBlock, 0, ctx->stream, rec, rec + 1, reinterpret_cast<const float*>(rec + 2),
+               x, y, a->nnz, acc ? 1 : 0, crow, cval);
+  } else {
+    SFG_LAUNCH(k_spmv_coo<1>, grid, kBlock, 0, ctx->stream, a->row, a->idx, static_cast<const float*>(a->val), x,
+               y, a->nnz, acc ? 1 : 0, crow, cval);
+  }
   carry_fix(ctx, crow, cval, nchunks, 1, y, 1);
 }
 
@@ -378,8 +397,10 @@ void spmv_ell(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, b
 
 void spmv(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, bool acc) {
   switch (a->kind) {
-    case SFG_CSR: spmv_csr(ctx, a, x, y, acc); break;
-    case SFG_COO: spmv_coo(ctx, a, x, y, acc); break;
+    case SFG_CSR:
+    case SFG_LIL: spmv_csr(ctx, a, x, y, acc); break;
+    case SFG_COO:
+    case SFG_DOK: spmv_coo(ctx, a, x, y, acc); break;
     case SFG_ELL: spmv_ell(ctx, a, x, y, acc); break;
     case SFG_DCSR: {
       if (!acc) zero_y(ctx, y, a->m);

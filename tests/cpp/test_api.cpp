@@ -56,13 +56,30 @@ int main(int argc, char** argv) {
   // spmv_y = A * 1 (oracle_data.hpp:125) for every covered format
   DenseTensor ones(TensorShape{{4}});
   for (auto& v : ones.data) v = 1.0;
-  for (const char* name : {"COO", "CSR", "CSC", "DCSR", "ELL", "BCSR(2,2)", "BCSR(4,4)"}) {
+  for (const char* name : {"COO", "CSR", "CSC", "DCSR", "ELL", "BCSR(2,2)", "BCSR(4,4)", "DOK", "LIL"}) {
     FormatEncoding enc = resolve_format(name);
     WorkingTensor w = t;
     convert_structure(w, resolve_format("COO"), enc);
     DenseTensor y = run_kernel(spmv_kernel(), {KernelOperand::from_materialized(enc, materialize(w, infer_storage(enc))),
                                                KernelOperand::from_dense(ones)});
     EXPECT(same(y.data, std::vector<double>{1, 2, 12, 0, 6}));
+  }
+
+  // LIL = CSR + pack(0,1) (formats.hpp:45): the CSR goldens (oracle_data.hpp:34-36)
+  // with the AoS layout over levels 0..1 (operators.hpp:424-430)
+  {
+    FormatEncoding lil = resolve_format("map (d0, d1) -> (d0, d1); merge(0), trim(1,1), pack(0,1)");
+    EXPECT(lil.name == "LIL");
+    EXPECT(same(plan_lines(plan_conversion(resolve_format("COO"), lil)),
+                std::vector<std::string>{"Fill(0)", "Merge(0)", "Pack(0,1)"}));
+    WorkingTensor w = t;
+    convert_structure(w, resolve_format("COO"), lil);
+    MaterializedTensor m = materialize(w, infer_storage(lil));
+    EXPECT(m.layout.kind == ValueLayoutKind::AoS && m.layout.aos_start == 0 && m.layout.aos_end == 1);
+    EXPECT(same(m.levels[1].ptr, std::vector<std::int64_t>{0, 1, 2, 5, 5, 6}));
+    EXPECT(same(m.levels[1].idx, std::vector<std::int64_t>{0, 1, 1, 2, 3, 3}));
+    EXPECT(same(m.values, coo_val));
+    EXPECT(explain_storage(infer_storage(lil)) == "L0: size | L1: ptr, idx | val | pack(0,1)");
   }
 
   // ELL and BCSR(2,2) goldens (oracle_data.hpp:67-97)

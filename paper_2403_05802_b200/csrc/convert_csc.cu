@@ -205,7 +205,15 @@ __global__ void __launch_bounds__(kPartThreads) k_bkt_count(const int32_t* __res
   __syncthreads();
   const int64_t per = (nnz + gridDim.x - 1) / gridDim.x;
   const int64_t e0 = blockIdx.x * per, e1 = min(nnz, e0 + per);
-  for (int64_t e = e0 + threadIdx.x; e < e1; e += kPartThreads) atomicAdd(&h[ld_stream(col + e) >> bits], 1);
+  constexpr int U = 8;  // loads in flight per thread
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += U * kPartThreads) {
+    int c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = e + u * kPartThreads < e1 ? ld_stream(col + e + u * kPartThreads) : -1;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (c[u] >= 0) atomicAdd(&h[c[u] >> bits], 1);
+  }
   __syncthreads();
   for (int b = threadIdx.x; b < nb; b += kPartThreads) counts[(int64_t)b * gridDim.x + blockIdx.x] = h[b];
 }

@@ -704,7 +704,8 @@ void spmm_csr_merge(sfg_context* ctx, const sfg_tensor* a, const int32_t* col, c
   SFG_LAUNCH((k_spmm_merge<TB, G, V, U, VEC, ONE, MB, S>), grid_for(nchunks * (CC)), kBlock, 0, ctx->stream, \
              a->ptr, col, fv, cuts, nchunks, m, d, cy)
   // nd = 32 on config 5 (SpMM ms): this unrolled step, 5 CTAs/SM 24.6;
-  // 4 CTAs/SM 24.9; kU = 2 at 6 CTAs/SM 25.3; the row-end path as a rolled
+  // 4 CTAs/SM 24.9; kU = 2 at 6 CTAs/SM 25.3; kU = 6 / 8 at 4 CTAs/SM 41.0 /
+  // 43.8 (spills, code size); the row-end path as a rolled
   // loop (smaller code, more instructions) 26.3; the first version of this
   // kernel with the zeroing of empty rows inside every row close (code 5x
   // the size, instruction-cache bound) 44

@@ -204,35 +204,55 @@ class Cfg3(Workload):
 
 
 class Cfg4(Workload):
-    """BCSR(16,16) bf16 SpMM N=128 (tcgen05), block-sparse 512K x 512K, 10% block density, generated as BCSR"""
+    """BCSR(r,r) SpMM N=128 (16x16 bf16: tcgen05), block-sparse 512K x 512K, 10% block density, generated as BCSR"""
     unit = "GFLOP/s"
     nd = 128
+    block = 16       # --block: 16 or 4
+    vdtype = "bf16"  # --bcsr-dtype: bf16 (values and B) or f32
+
+    def describe(self):
+        return (f"BCSR({self.block},{self.block}) {self.vdtype} SpMM N=128"
+                f"{' (tcgen05)' if self.block == 16 and self.vdtype == 'bf16' else ' (CUDA cores)'}, "
+                "block-sparse 512K x 512K, 10% block density, generated as BCSR")
 
     def setup(self, torch):
         m = 1 << 19
+        r = self.block
+        bf = self.vdtype == "bf16"
         self.m = self.n = m
-        self.a = self.ctx.gen_block_sparse(11, m, m, 16, 16, 0.1, value_dtype=self.sfg.BF16)
+        self.a = self.ctx.gen_block_sparse(11, m, m, r, r, 0.1, value_dtype=self.sfg.BF16 if bf else self.sfg.F32)
         v = self.a.view()
         self.nblocks = int(v.level[1].node_count)
-        self.nnz = self.nblocks * 256
-        self.b = torch.empty(m * self.nd, dtype=torch.bfloat16, device="cuda")
+        self.nnz = self.nblocks * r * r
+        self.b = torch.empty(m * self.nd, dtype=torch.bfloat16 if bf else torch.float32, device="cuda")
         self.b.uniform_(-1, 1)
         self.c = torch.zeros(m * self.nd, dtype=torch.float32, device="cuda")
         self.y = self.c
-        self.fmt = "BCSR(16,16) bf16"
+        self.fmt = f"BCSR({r},{r}) {self.vdtype}"
         self.bounds = [0, m]
-        self.info = {"nblocks": self.nblocks, "nd": self.nd, "value_dtype": "bf16", "b_dtype": "bf16"}
+        self.info = {"nblocks": self.nblocks, "nd": self.nd, "value_dtype": self.vdtype, "b_dtype": self.vdtype}
+        if bf and r == 16:
+            # the tensor-core path builds its per-matrix block schedule on the
+            # first product and caches it on the tensor: timed here once
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ev[0].record()
+            self.step()
+            ev[1].record()
+            torch.cuda.synchronize()
+            self.info["first_call_ms_with_schedule_build"] = round(ev[0].elapsed_time(ev[1]), 3)
 
     def step(self):
-        self.ctx.spmm_device(self.a, self.b.data_ptr(), self.sfg.BF16, self.nd, self.c.data_ptr())
+        bdt = self.sfg.BF16 if self.vdtype == "bf16" else self.sfg.F32
+        self.ctx.spmm_device(self.a, self.b.data_ptr(), bdt, self.nd, self.c.data_ptr())
 
     def work_units(self):
         return 2 * self.nnz * self.nd / 1e3  # unit conversion below: (MFLOP) -> GFLOP/s
 
     def kernels(self):
-        nb, m, n, nd = self.nblocks, self.m, self.n, self.nd
-        byts = nb * 256 * 2 + 4 * nb + 4 * (m // 16 + 1) + 2 * n * nd + 4 * m * nd
-        return [("spmm_bcsr_tc", self.step, byts, 2 * self.nnz * nd)]
+        nb, m, n, nd, r = self.nblocks, self.m, self.n, self.nd, self.block
+        s = 2 if self.vdtype == "bf16" else 4
+        byts = nb * r * r * s + 4 * nb + 4 * (m // r + 1) + s * n * nd + 4 * m * nd
+        return [("spmm_bcsr_tc" if r == 16 and s == 2 else "spmm_bcsr", self.step, byts, 2 * self.nnz * nd)]
 
 
 class Cfg5(SpmvWorkload):
@@ -491,7 +511,7 @@ def run_ours(args):
             "metric": METRIC, "value": round(value, 2), "unit": wl.unit, "n_gpus": world,
             "steps": args.steps, "warmup": warm, "ms_per_step": round(ms_per_step, 4),
             "higher_is_better": True, "scaling": wl.scaling, "vs_baseline": None,
-            "dtype": "bf16" if args.config == 4 else "f32",
+            "dtype": Cfg4.vdtype if args.config == 4 else "f32",
             "data": "synthetic (seeded generators, csrc/synth.h)",
             "config": {"workload": f"config {args.config}: {wl.describe()}", "format": wl.fmt,
                        "rows": int(wl.bounds[-1]), "cols": int(wl.n), "nnz_per_rank": int(wl.nnz),
@@ -525,14 +545,15 @@ def e2e_measure(args, sfg, ctx, wl, timed, torch, dist, world):
     lib = sfg.load()
     if args.config == 4:
         # no conversion in the config-4 step: host B in, host C out
-        b_p = torch.empty(wl.b.numel(), dtype=torch.bfloat16).pin_memory()
+        b_p = torch.empty(wl.b.numel(), dtype=wl.b.dtype).pin_memory()
         b_p.copy_(wl.b.cpu())
         c_p = torch.empty(wl.c.numel(), dtype=torch.float32).pin_memory()
+        bdt = sfg.BF16 if wl.b.dtype == torch.bfloat16 else sfg.F32
 
         def e2e_step():
-            sfg._check(lib.sfg_spmm(ctx.h, wl.a.h, C.c_void_p(b_p.data_ptr()), sfg.BF16, wl.nd, wl.nd,
+            sfg._check(lib.sfg_spmm(ctx.h, wl.a.h, C.c_void_p(b_p.data_ptr()), bdt, wl.nd, wl.nd,
                                     C.c_void_p(c_p.data_ptr()), wl.nd, sfg.COMPUTE_HOST))
-        h2d, d2h = b_p.numel() * 2, c_p.numel() * 4
+        h2d, d2h = b_p.numel() * b_p.element_size(), c_p.numel() * 4
     else:
         r_h, c_h, v_h = wl.coo.coo_arrays()
         pin = lambda arr: torch.from_numpy(arr).pin_memory()
@@ -721,6 +742,8 @@ def main():
     ap.add_argument("--config", type=int, default=5, choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--threshold", type=int, default=8, help="config 2: hybrid split threshold T")
+    ap.add_argument("--block", type=int, default=16, choices=[4, 16], help="config 4: BCSR block size")
+    ap.add_argument("--bcsr-dtype", default="bf16", choices=["bf16", "f32"], help="config 4: values and B")
     ap.add_argument("--rowpart", action="store_true",
                     help="row-partitioned path at N=1 too (under torchrun; exercises the NCCL all-gather)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -729,6 +752,7 @@ def main():
                     help="short run for ncu: no clock soak, no e2e, no CPU baseline")
     args = ap.parse_args()
     Cfg2.threshold = args.threshold
+    Cfg4.block, Cfg4.vdtype = args.block, args.bcsr_dtype
     if args.impl == "reference":
         run_reference(args)
     else:

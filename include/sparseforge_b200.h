@@ -70,14 +70,16 @@ enum sfg_format_kind {
    * storage.hpp:128-133) instead of separate arrays (SoA).                 */
   SFG_DOK = 7,  /* COO + pack(0,1): records {row, col, val}      formats.hpp:40 */
   SFG_LIL = 8,  /* CSR + pack(0,1): ptr[m+1] + records {col, val} formats.hpp:45 */
+  SFG_BELL = 9, /* blocked ELL: (indirect(d1/b), d0/b, d1/b, d0%b, d1%b) + block
+                   count / slot chain, slot-major b x b blocks  formats.hpp:79-85 */
 };
 
 enum sfg_dtype { SFG_F32 = 0, SFG_BF16 = 1 };
 
 typedef struct sfg_format {
   int32_t kind;        /* sfg_format_kind */
-  int32_t block_r;     /* BCSR block rows (r)    */
-  int32_t block_c;     /* BCSR block columns (c) */
+  int32_t block_r;     /* BCSR block rows (r); BELL block size (b) */
+  int32_t block_c;     /* BCSR block columns (c); BELL: b           */
   int32_t value_dtype; /* sfg_dtype of stored values (BF16: BCSR only) */
   int64_t threshold;   /* HYB: DecomposeRule::min_sum (decompose.hpp:17-20) */
 } sfg_format;
@@ -104,7 +106,7 @@ typedef struct sfg_tensor_view {
   int32_t value_dtype;
   int64_t rows, cols; /* logical shape */
   int32_t nlevels;
-  sfg_level_view level[4];
+  sfg_level_view level[5]; /* BELL has five levels */
   int64_t nvals;
   const void* values; /* device */
   const sfg_tensor* parts[2]; /* SFG_HYB: {ELL of remainder, COO of selection} */

@@ -170,6 +170,7 @@ inline std::string name_of(const sfg_format& f) {
     case SFG_HYB: return "HYB(" + std::to_string(f.threshold) + ")";
     case SFG_DOK: return "DOK";
     case SFG_LIL: return "LIL";
+    case SFG_BELL: return "BELL(" + std::to_string(f.block_r) + ")";
   }
   return "?";
 }
@@ -248,6 +249,9 @@ inline StorageScheme infer_storage(const FormatEncoding& enc) {
     case SFG_DCSR: s.levels = {L(0, 0, 1, 0), L(0, 1, 1, 0)}; break;
     case SFG_ELL: s.levels = {L(0, 0, 1, 0), L(1, 0, 0, 0), L(0, 0, 1, 0)}; break;
     case SFG_BCSR: s.levels = {L(1, 0, 0, 0), L(0, 1, 1, 0), L(1, 0, 0, 1), L(1, 0, 0, 1)}; break;
+    case SFG_BELL:
+      s.levels = {L(0, 0, 1, 0), L(1, 0, 0, 0), L(0, 0, 1, 0), L(1, 0, 0, 1), L(1, 0, 0, 1)};
+      break;
     default: break;  // HYB: two parts, see DecomposeResult
   }
   return s;
@@ -271,6 +275,7 @@ struct WorkingTensor {
     switch (enc.fmt.kind) {
       case SFG_ELL: return 3;
       case SFG_BCSR: return 4;
+      case SFG_BELL: return 5;
       default: return 2;
     }
   }

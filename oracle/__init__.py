@@ -194,7 +194,11 @@ class _Base:
 
 
 def _fmt_text(fmt, r=None, c=None):
-    return f"BCSR({r},{c})" if fmt == "BCSR" else fmt
+    if fmt == "BCSR":
+        return f"BCSR({r},{c})"
+    if fmt == "BELL":  # formats.hpp:79-85: BELL(b)
+        return f"BELL({r})"
+    return fmt
 
 
 class Port(_Base):

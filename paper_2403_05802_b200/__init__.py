@@ -22,7 +22,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_lib", "libsfg.so")
 
-KINDS = {"COO": 0, "CSR": 1, "CSC": 2, "DCSR": 3, "ELL": 4, "BCSR": 5, "HYB": 6, "DOK": 7, "LIL": 8}
+KINDS = {"COO": 0, "CSR": 1, "CSC": 2, "DCSR": 3, "ELL": 4, "BCSR": 5, "HYB": 6, "DOK": 7, "LIL": 8, "BELL": 9}
 KIND_NAMES = {v: k for k, v in KINDS.items()}
 F32, BF16 = 0, 1
 FLAG_SORTED, FLAG_SUM_DUPLICATES, FLAG_HOST = 1, 2, 4
@@ -59,7 +59,7 @@ class LevelView(C.Structure):
 
 class TensorView(C.Structure):
     _fields_ = [("kind", C.c_int32), ("value_dtype", C.c_int32), ("rows", C.c_int64),
-                ("cols", C.c_int64), ("nlevels", C.c_int32), ("level", LevelView * 4),
+                ("cols", C.c_int64), ("nlevels", C.c_int32), ("level", LevelView * 5),
                 ("nvals", C.c_int64), ("values", C.c_void_p), ("parts", C.c_void_p * 2),
                 ("layout", C.c_int32), ("aos_start", C.c_int32), ("aos_end", C.c_int32),
                 ("record_words", C.c_int32)]

@@ -86,6 +86,11 @@ std::string plan_for(const sfg_format& dst) {
              ")\nremainder: Sum(0)\nremainder: Enumerate(0)\nremainder: Sort\nremainder: Fill(1)\n"
              "remainder: Merge(0)\n";
     case SFG_DOK: return "Pack(0,1)\n";
+    case SFG_BELL: {
+      const std::string b = std::to_string(dst.block_r);
+      return "TileSplit(0," + b + ")\nTileSplit(2," + b + ")\nSwap(1,2)\nSum(0)\nEnumerate(0)\nSort\nFill(4)\n"
+             "Fill(3)\nFill(1)\nVectorize(3)\nMerge(0)\n";
+    }
     case SFG_LIL: return "Fill(0)\nMerge(0)\nPack(0,1)\n";
   }
   return "";
@@ -103,14 +108,16 @@ std::string explain_for(const sfg_format& f) {
       return "L0: size | L1: ptr, idx | L2: size, dense_vector | L3: size, dense_vector | val";
     case SFG_HYB: return "ELL(L0: idx | L1: size | L2: idx | val) + COO(L0: idx | L1: idx | val)";
     case SFG_DOK: return "L0: idx | L1: idx | val | pack(0,1)";
+    case SFG_BELL:
+      return "L0: idx | L1: size | L2: idx | L3: size, dense_vector | L4: size, dense_vector | val";
     case SFG_LIL: return "L0: size | L1: ptr, idx | val | pack(0,1)";
   }
   return "";
 }
 
 void validate_format(const sfg_format& f) {
-  require(f.kind >= SFG_COO && f.kind <= SFG_LIL, SFG_ERR_PARSE, "unknown format kind");
-  if (f.kind == SFG_BCSR)
+  require(f.kind >= SFG_COO && f.kind <= SFG_BELL, SFG_ERR_PARSE, "unknown format kind");
+  if (f.kind == SFG_BCSR || f.kind == SFG_BELL)
     require(f.block_r > 0 && f.block_c > 0, SFG_ERR_INVALID_OPERATION,
             "TileSplit factor must be positive");
   require(f.value_dtype == SFG_F32 || (f.value_dtype == SFG_BF16 && f.kind == SFG_BCSR),
@@ -241,6 +248,10 @@ int sfg_format_resolve(const char* text, sfg_format* out) {
       f.kind = SFG_BCSR;
       f.block_r = static_cast<int32_t>(nargs > 0 ? args[0] : 2);
       f.block_c = static_cast<int32_t>(nargs > 1 ? args[1] : f.block_r);
+    } else if (name == "BELL") {
+      // formats.hpp:79-85: one argument, the block size (default 2)
+      f.kind = SFG_BELL;
+      f.block_r = f.block_c = static_cast<int32_t>(nargs > 0 ? args[0] : 2);
     } else if (name == "HYB") {
       f.kind = SFG_HYB;
       f.threshold = nargs > 0 ? args[0] : 8;
@@ -343,6 +354,7 @@ int sfg_convert(sfg_context* ctx, const sfg_tensor* src, const sfg_format* dst, 
       case SFG_HYB: *out = sfg::coo_to_hyb(ctx, src, dst->threshold); break;
       case SFG_DOK: *out = sfg::coo_to_dok(ctx, src); break;
       case SFG_LIL: *out = sfg::coo_to_lil(ctx, src); break;
+      case SFG_BELL: *out = sfg::coo_to_bell(ctx, src, dst->block_r); break;
     }
   });
 }
@@ -426,6 +438,17 @@ int sfg_tensor_view_get(sfg_context* ctx, const sfg_tensor* t, sfg_tensor_view* 
         v.values = rec ? rec + 2 : nullptr;
         v.nvals = t->nnz;
         v.layout = 1, v.aos_start = 0, v.aos_end = 1, v.record_words = 3;
+        break;
+      }
+      case SFG_BELL: {  // slot-major cells (slot, block row), dense b x b blocks
+        const int64_t cells = t->k * t->nbr;
+        v.nlevels = 5;
+        v.level[0] = level(I, 0, t->k - 1, t->k, t->k, t->slots, 0, nullptr);
+        v.level[1] = level(S, 0, t->nbr - 1, cells, 0, nullptr, 0, nullptr);
+        v.level[2] = level(I, 0, t->nbc - 1, cells, cells, t->idx, 0, nullptr);
+        v.level[3] = level(S | D, 0, t->rb - 1, cells * t->rb, 0, nullptr, 0, nullptr);
+        v.level[4] = level(S | D, 0, t->cb - 1, cells * t->rb * t->cb, 0, nullptr, 0, nullptr);
+        v.nvals = cells * t->rb * t->cb;
         break;
       }
       case SFG_LIL: {  // ptr + records {col, val}

@@ -95,6 +95,7 @@ std::vector<uint8_t> expected_kinds(int kind) {
     case SFG_DCSR: return {kUIdx, kUIdx | kUPtr};
     case SFG_ELL: return {kUIdx, kUSize, kUIdx};
     case SFG_BCSR: return {kUSize, kUIdx | kUPtr, kUSize | kUDense, kUSize | kUDense};
+    case SFG_BELL: return {kUIdx, kUSize, kUIdx, kUSize | kUDense, kUSize | kUDense};
     case SFG_DOK: return {kUIdx, kUIdx};           // COO + pack(0,1)
     case SFG_LIL: return {kUSize, kUIdx | kUPtr};  // CSR + pack(0,1)
   }
@@ -314,7 +315,7 @@ sfg_tensor* read_container(sfg_context* ctx, const char* path_c, const sfg_forma
   } else {
     fmt.value_dtype = SFG_F32;
     int found = -1;
-    for (int k : {SFG_COO, SFG_CSR, SFG_DCSR, SFG_ELL, SFG_BCSR}) {
+    for (int k : {SFG_COO, SFG_CSR, SFG_DCSR, SFG_ELL, SFG_BCSR, SFG_BELL}) {
       const auto w = expected_kinds(k);
       bool same = w.size() == lv.size();
       for (size_t l = 0; same && l < lv.size(); ++l) same = lv[l].kind == w[l];
@@ -330,6 +331,8 @@ sfg_tensor* read_container(sfg_context* ctx, const char* path_c, const sfg_forma
     if (found == SFG_BCSR) {
       fmt.block_r = lv[2].hi - lv[2].lo + 1;
       fmt.block_c = lv[3].hi - lv[3].lo + 1;
+    } else if (found == SFG_BELL) {
+      fmt.block_r = fmt.block_c = lv[3].hi - lv[3].lo + 1;
     }
   }
   const auto want = expected_kinds(fmt.kind);
@@ -389,6 +392,17 @@ sfg_tensor* read_container(sfg_context* ctx, const char* path_c, const sfg_forma
         dfree(ctx, vals);
         break;
       }
+      case SFG_BELL:
+        t->br = t->bc = fmt.block_r;
+        t->k = lv[0].nidx;
+        t->nbr = lv[1].hi - lv[1].lo + 1;
+        t->nbc = lv[2].hi - lv[2].lo + 1;
+        t->rb = lv[3].hi - lv[3].lo + 1;
+        t->cb = lv[4].hi - lv[4].lo + 1;
+        t->nnz = lv[2].nidx;
+        t->slots = load_i(lv[0].idx_off, lv[0].nidx);
+        t->idx = load_i(lv[2].idx_off, lv[2].nidx);
+        break;
       case SFG_COO:
         t->nnz = lv[0].nidx;
         t->row = load_i(lv[0].idx_off, lv[0].nidx);

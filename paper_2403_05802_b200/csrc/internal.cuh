@@ -84,6 +84,9 @@ struct sfg_context {
 //   ELL : slots[K] (L0 idx), idx[K*m] (L2 idx, slot-major), val[K*m]
 //   BCSR: ptr[nbr+1], idx[nblocks] (bcol), val[nblocks*rb*cb] block-major
 //   HYB : part[0] = ELL of the remainder, part[1] = COO of the selection
+//   BELL: slots[K], idx[K*nbr] (block column of cell (slot, block row),
+//         slot-major), val[K*nbr*rb*cb]; nnz = K*nbr cells
+//   DOK : val = records {row, col, val}[nnz];  LIL: ptr[m+1], val = {col, val}[nnz]
 struct sfg_tensor {
   sfg_context* ctx = nullptr;
   int32_t kind = SFG_COO;
@@ -209,6 +212,8 @@ sfg_tensor* coo_to_dcsr(sfg_context* ctx, const sfg_tensor* s);
 sfg_tensor* coo_to_ell(sfg_context* ctx, const sfg_tensor* s);
 sfg_tensor* coo_to_bcsr(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_t c, int dtype);
 sfg_tensor* coo_to_hyb(sfg_context* ctx, const sfg_tensor* s, int64_t min_sum);
+// Blocked ELL (convert_bell.cu): the BCSR blocks relaid slot by slot.
+sfg_tensor* coo_to_bell(sfg_context* ctx, const sfg_tensor* s, int64_t b);
 // Value-layout formats (pack.cu): Pack(0,1) over COO (DOK) / CSR (LIL).
 sfg_tensor* coo_to_dok(sfg_context* ctx, const sfg_tensor* s);
 sfg_tensor* coo_to_lil(sfg_context* ctx, const sfg_tensor* s);

@@ -634,12 +634,14 @@ __global__ void __launch_bounds__(kBlock) k_spmm_csc(const int32_t* __restrict__
 // Warp per (block row, column chunk): lanes keep rb accumulators (one per
 // row of the block row) for their V columns; every stored slot of every
 // block is applied; rows/cols past M/N are guarded out (kernel.hpp:290-302).
-template <typename TB, typename TA, int V, int RB>
+// kBell: BELL cells — block row b holds the K slots k * nbr + b (padding:
+// block column 0, a zero block), no ptr.
+template <typename TB, typename TA, int V, int RB, bool kBell>
 __global__ void __launch_bounds__(kBlock) k_spmm_bcsr(const int32_t* __restrict__ ptr,
                                                        const int32_t* __restrict__ bcol,
                                                        const TA* __restrict__ val, int64_t nbr,
                                                        int32_t m, int32_t n, int32_t br, int32_t bc,
-                                                       int32_t rb, int32_t cb, Dense d) {
+                                                       int32_t rb, int32_t cb, Dense d, int64_t kslots) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int chunks = (d.nd + 32 * V - 1) / (32 * V);
@@ -653,10 +655,11 @@ __global__ void __launch_bounds__(kBlock) k_spmm_bcsr(const int32_t* __restrict_
     for (int i = 0; i < RB; ++i)
 #pragma unroll
       for (int v = 0; v < V; ++v) acc[i][v] = 0.f;
-    int s = __ldg(ptr + b), e = __ldg(ptr + b + 1);
-    for (int k = s; k < e; ++k) {
+    const int64_t s = kBell ? 0 : __ldg(ptr + b), e = kBell ? kslots : __ldg(ptr + b + 1);
+    for (int64_t kk = s; kk < e; ++kk) {
+      const int64_t k = kBell ? kk * nbr + b : kk;
       int colbase = __ldg(bcol + k) * bc;
-      const TA* blk = val + (int64_t)k * rb * cb;
+      const TA* blk = val + k * rb * cb;
       for (int j = 0; j < cb; ++j) {
         if (colbase + j >= n) break;
         float bv[V];
@@ -787,18 +790,22 @@ void launch_fmt(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
         SFG_LAUNCH((k_spmm_csc<TB, V>), grid_for(a->n * chunks), kBlock, 0, ctx->stream, a->ptr,
                    a->idx, fv, (int32_t)a->n, d);
       break;
-    case SFG_BCSR: {
+    case SFG_BCSR:
+    case SFG_BELL: {
       if (a->nbr == 0 || a->nnz == 0) break;
       if (a->rb > 16) raise(SFG_ERR_INVALID_OPERATION, "BCSR SpMM: block rows > 16 not supported");
       int g = grid_for(a->nbr * chunks);
-#define SFG_BCSR_CASE(RB)                                                                          \
-  if (a->dtype == SFG_BF16)                                                                        \
-    SFG_LAUNCH((k_spmm_bcsr<TB, __nv_bfloat16, V, RB>), g, kBlock, 0, ctx->stream, a->ptr, a->idx, \
-               static_cast<const __nv_bfloat16*>(a->val), a->nbr, (int)a->m, (int)a->n,           \
-               (int)a->br, (int)a->bc, (int)a->rb, (int)a->cb, d);                                 \
-  else                                                                                             \
-    SFG_LAUNCH((k_spmm_bcsr<TB, float, V, RB>), g, kBlock, 0, ctx->stream, a->ptr, a->idx, fv,     \
-               a->nbr, (int)a->m, (int)a->n, (int)a->br, (int)a->bc, (int)a->rb, (int)a->cb, d);
+#define SFG_BCSR_CASE(RB)                                                                                 \
+  if (a->kind == SFG_BELL)                                                                                \
+    SFG_LAUNCH((k_spmm_bcsr<TB, float, V, RB, true>), g, kBlock, 0, ctx->stream, a->ptr, a->idx, fv, a->nbr, \
+               (int)a->m, (int)a->n, (int)a->br, (int)a->bc, (int)a->rb, (int)a->cb, d, a->k);            \
+  else if (a->dtype == SFG_BF16)                                                                          \
+    SFG_LAUNCH((k_spmm_bcsr<TB, __nv_bfloat16, V, RB, false>), g, kBlock, 0, ctx->stream, a->ptr, a->idx,  \
+               static_cast<const __nv_bfloat16*>(a->val), a->nbr, (int)a->m, (int)a->n,                  \
+               (int)a->br, (int)a->bc, (int)a->rb, (int)a->cb, d, a->k);                                  \
+  else                                                                                                    \
+    SFG_LAUNCH((k_spmm_bcsr<TB, float, V, RB, false>), g, kBlock, 0, ctx->stream, a->ptr, a->idx, fv,      \
+               a->nbr, (int)a->m, (int)a->n, (int)a->br, (int)a->bc, (int)a->rb, (int)a->cb, d, a->k);
       if (a->rb <= 4) { SFG_BCSR_CASE(4) }
       else if (a->rb <= 8) { SFG_BCSR_CASE(8) }
       else { SFG_BCSR_CASE(16) }
@@ -981,7 +988,8 @@ void spmm(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dtype, int
     return;
   }
   bool zero_first =
-      !accumulate && (a->kind == SFG_COO || a->kind == SFG_DOK || a->kind == SFG_CSC || a->kind == SFG_BCSR);
+      !accumulate && (a->kind == SFG_COO || a->kind == SFG_DOK || a->kind == SFG_CSC || a->kind == SFG_BCSR ||
+                      a->kind == SFG_BELL);
   if (zero_first && a->m > 0) {
     if (ldc == nd)
       SFG_CUDA(cudaMemsetAsync(c, 0, a->m * ldc * sizeof(float), ctx->stream));

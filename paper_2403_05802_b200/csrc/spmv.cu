@@ -285,14 +285,16 @@ __device__ __forceinline__ float to_f<__nv_bfloat16_raw>(__nv_bfloat16_raw v) {
   return __uint_as_float(static_cast<uint32_t>(v.x) << 16);
 }
 
-template <typename T>
+// kBell: BELL cells — block row b holds the K slots k * nbr + b (padding
+// slots: block column 0, a zero block), no ptr.
+template <typename T, bool kBell>
 __global__ void __launch_bounds__(kBlock) k_spmv_bcsr(const int32_t* __restrict__ ptr,
                                                        const int32_t* __restrict__ bcol,
                                                        const T* __restrict__ val,
                                                        const float* __restrict__ x,
                                                        float* __restrict__ y, int64_t nbr, int32_t m,
                                                        int32_t n, int32_t br, int32_t bc, int32_t rb,
-                                                       int32_t cb, int acc) {
+                                                       int32_t cb, int acc, int64_t kslots) {
   extern __shared__ float sh_rows[];  // [warps][rb][32]: row i's partial of lane l at [i][l]
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
@@ -301,10 +303,11 @@ __global__ void __launch_bounds__(kBlock) k_spmv_bcsr(const int32_t* __restrict_
   const int slots = rb * cb;
   for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nbr; b += warps) {
     for (int i = 0; i < rb; ++i) mine[i * 32 + lane] = 0.f;
-    int s = __ldg(ptr + b), e = __ldg(ptr + b + 1);
-    for (int k = s; k < e; ++k) {
+    const int64_t s = kBell ? 0 : __ldg(ptr + b), e = kBell ? kslots : __ldg(ptr + b + 1);
+    for (int64_t kk = s; kk < e; ++kk) {
+      const int64_t k = kBell ? kk * nbr + b : kk;
       int c0 = __ldg(bcol + k) * bc;
-      const T* blk = val + (int64_t)k * slots;
+      const T* blk = val + k * slots;
       for (int q = lane; q < slots; q += 32) {
         int i = q / cb, j = q - i * cb;
         int cc = c0 + j;
@@ -425,28 +428,30 @@ void spmv(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, bool 
                  static_cast<const float*>(a->val), x, y, (int)a->n);
       break;
     }
-    case SFG_BCSR: {
+    case SFG_BCSR:
+    case SFG_BELL: {
       if (a->nbr == 0) break;
+      if (a->kind == SFG_BELL && a->k == 0) {
+        if (!acc) zero_y(ctx, y, a->m);
+        break;
+      }
       // per-lane row partials: rb KB of shared memory per warp
       const size_t per_warp = (size_t)a->rb * 32 * sizeof(float);
       const int wpb = (int)std::min<size_t>(kBlock / 32, (227u << 10) / per_warp);
       if (wpb < 1) raise(SFG_ERR_INVALID_OPERATION, "BCSR SpMV: block rows > 1816 not supported");
       const size_t smem = wpb * per_warp;
       int grid = (int)std::min<int64_t>(ceil_div(a->nbr, wpb), (int64_t)ctx->sms * 16);
-      if (a->dtype == SFG_BF16) {
+      auto go = [&](auto kern, const auto* v) {
         if (smem > (48u << 10))
-          SFG_CUDA(cudaFuncSetAttribute(k_spmv_bcsr<__nv_bfloat16_raw>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smem));
-        SFG_LAUNCH(k_spmv_bcsr<__nv_bfloat16_raw>, grid, wpb * 32, smem, ctx->stream, a->ptr, a->idx,
-                   static_cast<const __nv_bfloat16_raw*>(a->val), x, y, a->nbr, (int)a->m, (int)a->n,
-                   (int)a->br, (int)a->bc, (int)a->rb, (int)a->cb, acc);
-      } else {
-        if (smem > (48u << 10))
-          SFG_CUDA(cudaFuncSetAttribute(k_spmv_bcsr<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        SFG_LAUNCH(k_spmv_bcsr<float>, grid, wpb * 32, smem, ctx->stream, a->ptr, a->idx,
-                   static_cast<const float*>(a->val), x, y, a->nbr, (int)a->m, (int)a->n,
-                   (int)a->br, (int)a->bc, (int)a->rb, (int)a->cb, acc);
-      }
+          SFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        SFG_LAUNCH(kern, grid, wpb * 32, smem, ctx->stream, a->ptr, a->idx, v, x, y, a->nbr, (int)a->m, (int)a->n,
+                   (int)a->br, (int)a->bc, (int)a->rb, (int)a->cb, acc, a->k);
+      };
+      const auto* vb = static_cast<const __nv_bfloat16_raw*>(a->val);
+      const auto* vf = static_cast<const float*>(a->val);
+      if (a->kind == SFG_BELL) go(k_spmv_bcsr<float, true>, vf);
+      else if (a->dtype == SFG_BF16) go(k_spmv_bcsr<__nv_bfloat16_raw, false>, vb);
+      else go(k_spmv_bcsr<float, false>, vf);
       break;
     }
     case SFG_HYB:

@@ -34,7 +34,7 @@ def test_library_is_sm100a():
     assert "sm_100a" in out.stdout
 
 
-FORMATS = ["COO", "CSR", "CSC", "DCSR", "ELL", "BCSR(2,2)", "BCSR(4,4)", "BCSR(16,16)", "BCSR(3,2)", "DOK", "LIL"]
+FORMATS = ["COO", "CSR", "CSC", "DCSR", "ELL", "BCSR(2,2)", "BCSR(4,4)", "BCSR(16,16)", "BCSR(3,2)", "DOK", "LIL", "BELL(2)", "BELL(4)", "BELL(16)"]
 
 
 @pytest.mark.parametrize("fmt", FORMATS)

@@ -13,6 +13,7 @@
 #include <climits>
 #include <cstdlib>
 
+#include "async.cuh"
 #include "devutil.cuh"
 #include "internal.cuh"
 
@@ -721,6 +722,231 @@ void spmm_csr_merge(sfg_context* ctx, const sfg_tensor* a, const int32_t* col, c
   carry_fix(ctx, cy.row, cy.val, nchunks, d.nd, d.c, d.ldc);
 }
 
+// BCSR / BELL with 128-column chunks of the dense operand (nd % 128 == 0,
+// aligned B and C): register-tiled CUDA-core kernel for the shapes the
+// tensor-core path does not take (fp32 values, 4x4 / 8x8 blocks). A warp
+// owns (block row, 128 columns): lane l holds C[rows of the block row][4 l ..
+// 4 l + 3] in registers (RB x 4 accumulators). Per block the warp stages the
+// r x c value block in its shared-memory slot (fp32, row-major, padded to
+// CB columns), then walks the block's columns four at a time: four B-row
+// loads (16 bytes per lane) and, per block row r, one 16-byte shared load
+// of a[r][j..j+3] broadcast to the warp and 16 FMAs. Per 16x16 block: 16
+// B-row loads, 64 shared loads, 1,024 FMAs per lane.
+template <typename TB, typename TA, int RB, int CB, bool kBell>
+__global__ void __launch_bounds__(kBlock, RB == 16 ? 1 : 2) k_spmm_bcsr128(const int32_t* __restrict__ ptr,
+                                                             const int32_t* __restrict__ bcol,
+                                                             const TA* __restrict__ val, int64_t nbr, int32_t m,
+                                                             int32_t n, int32_t br, int32_t bc, int32_t rb,
+                                                             int32_t cb, Dense d, int64_t kslots) {
+  static_assert(CB % 4 == 0 && RB <= 16 && CB <= 16, "block tile");
+  __shared__ __align__(16) float s_blk[kBlock / 32][RB * CB];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  float* a_s = s_blk[wid];
+  const int chunks = d.nd / 128;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int slots = rb * cb;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nbr * chunks; w += warps) {
+    const int64_t b = w / chunks;
+    const int c0 = (int)(w - b * chunks) * 128 + lane * 4;
+    float acc[RB][4];
+#pragma unroll
+    for (int i = 0; i < RB; ++i)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[i][v] = 0.f;
+    const int64_t s = kBell ? 0 : __ldg(ptr + b), e = kBell ? kslots : __ldg(ptr + b + 1);
+    for (int64_t kk = s; kk < e; ++kk) {
+      const int64_t k = kBell ? kk * nbr + b : kk;
+      const int colbase = __ldg(bcol + k) * bc;
+      const TA* blk = val + k * slots;
+      __syncwarp();
+      for (int q = lane; q < RB * CB; q += 32) {
+        const int i = q / CB, j = q - i * CB;
+        a_s[q] = i < rb && j < cb ? (float)blk[i * cb + j] : 0.f;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int j0 = 0; j0 < CB; j0 += 4) {
+        float bv[4][4];
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int col = colbase + j0 + jj;
+          if (j0 + jj < cb && col < n) {
+            BRow<TB>::template load<4>(static_cast<const TB*>(d.b) + (int64_t)col * d.ldb + c0, bv[jj]);
+          } else {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) bv[jj][v] = 0.f;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < RB; ++i) {
+          const float4 a4 = *reinterpret_cast<const float4*>(a_s + i * CB + j0);
+          const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[i][v] = fmaf(av[jj], bv[jj][v], acc[i][v]);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < RB; ++i) {
+      const int64_t r = b * br + i;
+      if (i < rb && r < m) {
+        float* crow = d.c + r * d.ldc + c0;
+        float4 o = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        if (d.acc) {
+          const float4 p = *reinterpret_cast<const float4*>(crow);
+          o.x += p.x, o.y += p.y, o.z += p.z, o.w += p.w;
+        }
+        *reinterpret_cast<float4*>(crow) = o;
+      }
+    }
+  }
+}
+
+// The same product for exact tiles (r = RB, c = CB: 4x4, 8x8, 16x16 blocks)
+// with the operands staged by cp.async in a two-deep ring per warp, so a
+// warp keeps a whole stage of B rows in flight without holding them in
+// registers (the B of config 4 is 268 MB in fp32, more than L2: its rows
+// come from HBM and the kernel is bound by how many are in flight). A stage
+// is 16 / CB blocks = 16 B-row slices of 512 bytes (fp32 B) plus the value
+// blocks; the block columns of the stage after next are loaded a stage
+// ahead, so issuing a stage never waits on them.
+__device__ __forceinline__ void cp_async16_zfill(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8_zfill(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 8 : 0)
+               : "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <typename TB, typename TA, int RB, int CB, bool kBell>
+__global__ void __launch_bounds__(kBlock, 1) k_spmm_bcsr128p(const int32_t* __restrict__ ptr,
+                                                              const int32_t* __restrict__ bcol,
+                                                              const TA* __restrict__ val, int64_t nbr, int32_t m,
+                                                              int32_t n, int32_t br, Dense d, int64_t kslots) {
+  constexpr int kPer = 16 / CB;               // blocks per stage
+  constexpr int kRows = 16;                   // B rows per stage
+  constexpr int kBW = 4 * (int)sizeof(TB);    // B bytes per lane per row (4 columns)
+  constexpr int kABytes = RB * CB * (int)sizeof(TA);
+  constexpr int kAChunks = kABytes / 16;      // 16-byte pieces of one value block
+  static_assert(kABytes % 16 == 0, "value blocks in 16-byte pieces");
+  struct Stage {
+    uint8_t b[kRows][32 * kBW];
+    uint8_t a[kPer][kABytes];
+  };
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  Stage* ring = reinterpret_cast<Stage*>(smem_raw) + wid * 2;
+  const int chunks = d.nd / 128;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const TB* bbase = static_cast<const TB*>(d.b);
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nbr * chunks; w += warps) {
+    const int64_t b = w / chunks;
+    const int cw = (int)(w - b * chunks) * 128;
+    const int c0 = cw + lane * 4;
+    float acc[RB][4];
+#pragma unroll
+    for (int i = 0; i < RB; ++i)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[i][v] = 0.f;
+    const int64_t s = kBell ? 0 : __ldg(ptr + b), e = kBell ? kslots : __ldg(ptr + b + 1);
+    const int64_t nst = (e - s + kPer - 1) / kPer;
+    auto blk_of = [&](int64_t kk) -> int64_t { return kBell ? kk * nbr + b : kk; };
+    // block column of block kk (lane t < kPer holds block t of a stage)
+    auto load_bcol = [&](int64_t st) -> int {
+      const int64_t kk = s + st * kPer + lane;
+      return lane < kPer && kk < e ? __ldg(bcol + blk_of(kk)) : -1;
+    };
+    auto issue = [&](int64_t st, int bc_lane) {
+      Stage& g = ring[st & 1];
+#pragma unroll
+      for (int t = 0; t < kPer; ++t) {
+        const int bcv = __shfl_sync(kFull, bc_lane, t);
+        const int64_t kk = s + st * kPer + t;
+#pragma unroll
+        for (int j = 0; j < CB; ++j) {
+          const int col = bcv * CB + j;
+          const bool ok = bcv >= 0 && col < n;
+          const TB* src = bbase + (ok ? (int64_t)col * d.ldb + c0 : 0);
+          if constexpr (kBW == 16) cp_async16_zfill(&g.b[t * CB + j][lane * 16], src, ok);
+          else cp_async8_zfill(&g.b[t * CB + j][lane * 8], src, ok);
+        }
+        const uint8_t* asrc = reinterpret_cast<const uint8_t*>(val + (bcv >= 0 ? blk_of(kk) : 0) * RB * CB);
+        for (int q = lane; q < kAChunks; q += 32) cp_async16_zfill(&g.a[t][q * 16], asrc + q * 16, bcv >= 0);
+      }
+      cp_async_commit();
+    };
+    int bc_next = load_bcol(0);
+    if (nst > 0) issue(0, bc_next);
+    bc_next = load_bcol(1);
+    for (int64_t st = 0; st < nst; ++st) {
+      if (st + 1 < nst) issue(st + 1, bc_next);
+      else cp_async_commit();  // keep the group count: wait_group 1 below
+      bc_next = load_bcol(st + 2);
+      cp_async_wait<1>();
+      __syncwarp();
+      const Stage& g = ring[st & 1];
+#pragma unroll
+      for (int t = 0; t < kPer; ++t) {
+#pragma unroll
+        for (int j0 = 0; j0 < CB; j0 += 4) {
+          float bv[4][4];
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const uint8_t* pb = &g.b[t * CB + j0 + jj][lane * kBW];
+            if constexpr (kBW == 16) {
+              const float4 q = *reinterpret_cast<const float4*>(pb);
+              bv[jj][0] = q.x, bv[jj][1] = q.y, bv[jj][2] = q.z, bv[jj][3] = q.w;
+            } else {
+              const uint2 q = *reinterpret_cast<const uint2*>(pb);
+              bv[jj][0] = __uint_as_float(q.x << 16), bv[jj][1] = __uint_as_float(q.x & 0xffff0000u);
+              bv[jj][2] = __uint_as_float(q.y << 16), bv[jj][3] = __uint_as_float(q.y & 0xffff0000u);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < RB; ++i) {
+            float av[4];
+            if constexpr (sizeof(TA) == 4) {
+              const float4 a4 = *reinterpret_cast<const float4*>(&g.a[t][(i * CB + j0) * 4]);
+              av[0] = a4.x, av[1] = a4.y, av[2] = a4.z, av[3] = a4.w;
+            } else {
+              const uint2 q = *reinterpret_cast<const uint2*>(&g.a[t][(i * CB + j0) * 2]);
+              av[0] = __uint_as_float(q.x << 16), av[1] = __uint_as_float(q.x & 0xffff0000u);
+              av[2] = __uint_as_float(q.y << 16), av[3] = __uint_as_float(q.y & 0xffff0000u);
+            }
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+              for (int v = 0; v < 4; ++v) acc[i][v] = fmaf(av[jj], bv[jj][v], acc[i][v]);
+          }
+        }
+      }
+      __syncwarp();  // the slot is refilled by the next iteration's issue
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int i = 0; i < RB; ++i) {
+      const int64_t r = b * br + i;
+      if (r < m) {
+        float* crow = d.c + r * d.ldc + c0;
+        float4 o = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        if (d.acc) {
+          const float4 p = *reinterpret_cast<const float4*>(crow);
+          o.x += p.x, o.y += p.y, o.z += p.z, o.w += p.w;
+        }
+        *reinterpret_cast<float4*>(crow) = o;
+      }
+    }
+  }
+}
+
 template <typename TB, int V>
 void launch_fmt(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
   int64_t chunks = ceil_div(d.nd, 32 * V);
@@ -794,6 +1020,61 @@ void launch_fmt(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
     case SFG_BELL: {
       if (a->nbr == 0 || a->nnz == 0) break;
       if (a->rb > 16) raise(SFG_ERR_INVALID_OPERATION, "BCSR SpMM: block rows > 16 not supported");
+      const bool v128 = d.nd % 128 == 0 && d.ldb % 4 == 0 && d.ldc % 4 == 0 && a->cb <= 16 &&
+                        ((reinterpret_cast<uintptr_t>(d.b) | reinterpret_cast<uintptr_t>(d.c)) & 15) == 0;
+      if (v128) {
+        // register-tiled path (fp32 or bf16 values; the 16x16 bf16 / bf16-B
+        // case with nd = 128 went to the tensor cores above)
+        const int g128 = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a->nbr * (d.nd / 128), kBlock / 32),
+                                                                     (int64_t)ctx->sms * 16));
+        const bool bell = a->kind == SFG_BELL, bf = a->dtype == SFG_BF16;
+        const int cbt = a->cb <= 4 ? 4 : a->cb <= 8 ? 8 : 16;
+        const int rbt = a->rb <= 4 ? 4 : a->rb <= 8 ? 8 : 16;
+        if (a->rb == a->cb && a->rb == rbt && a->cb == cbt) {
+          // exact square tiles: the cp.async-staged kernel (8 warps, two
+          // stages each, one CTA per SM)
+          auto go = [&](auto kern, size_t stage_bytes, auto v) {
+            const size_t smem = (size_t)(kBlock / 32) * 2 * stage_bytes;
+            SFG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            const int gp = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a->nbr * (d.nd / 128), kBlock / 32),
+                                                                       (int64_t)ctx->sms));
+            SFG_LAUNCH(kern, gp, kBlock, smem, ctx->stream, a->ptr, a->idx, v, a->nbr,
+                       (int)a->m, (int)a->n, (int)a->br, d, a->k);
+          };
+#define SFG_B128P(T, TAT)                                                                                          \
+  if (rbt == T) {                                                                                                   \
+    constexpr size_t kSB = 16 * 32 * 4 * sizeof(TB) + (16 / T) * T * T * sizeof(TAT);                             \
+    if (bell)                                                                                                       \
+      go(k_spmm_bcsr128p<TB, TAT, T, T, true>, kSB, static_cast<const TAT*>(a->val));                              \
+    else                                                                                                            \
+      go(k_spmm_bcsr128p<TB, TAT, T, T, false>, kSB, static_cast<const TAT*>(a->val));                             \
+    break;                                                                                                          \
+  }
+          if (bf && !bell) {
+            SFG_B128P(4, __nv_bfloat16) SFG_B128P(8, __nv_bfloat16) SFG_B128P(16, __nv_bfloat16)
+          } else {
+            SFG_B128P(4, float) SFG_B128P(8, float) SFG_B128P(16, float)
+          }
+#undef SFG_B128P
+        }
+#define SFG_B128(RBT, CBT)                                                                                      \
+  if (rbt == RBT && cbt == CBT) {                                                                               \
+    if (bell)                                                                                                   \
+      SFG_LAUNCH((k_spmm_bcsr128<TB, float, RBT, CBT, true>), g128, kBlock, 0, ctx->stream, a->ptr, a->idx, fv,  \
+                 a->nbr, (int)a->m, (int)a->n, (int)a->br, (int)a->bc, (int)a->rb, (int)a->cb, d, a->k);        \
+    else if (bf)                                                                                                \
+      SFG_LAUNCH((k_spmm_bcsr128<TB, __nv_bfloat16, RBT, CBT, false>), g128, kBlock, 0, ctx->stream, a->ptr,     \
+                 a->idx, static_cast<const __nv_bfloat16*>(a->val), a->nbr, (int)a->m, (int)a->n, (int)a->br,   \
+                 (int)a->bc, (int)a->rb, (int)a->cb, d, a->k);                                                 \
+    else                                                                                                        \
+      SFG_LAUNCH((k_spmm_bcsr128<TB, float, RBT, CBT, false>), g128, kBlock, 0, ctx->stream, a->ptr, a->idx, fv, \
+                 a->nbr, (int)a->m, (int)a->n, (int)a->br, (int)a->bc, (int)a->rb, (int)a->cb, d, a->k);        \
+    break;                                                                                                      \
+  }
+        SFG_B128(4, 4) SFG_B128(4, 8) SFG_B128(4, 16) SFG_B128(8, 4) SFG_B128(8, 8) SFG_B128(8, 16)
+        SFG_B128(16, 4) SFG_B128(16, 8) SFG_B128(16, 16)
+#undef SFG_B128
+      }
       int g = grid_for(a->nbr * chunks);
 #define SFG_BCSR_CASE(RB)                                                                                 \
   if (a->kind == SFG_BELL)                                                                                \

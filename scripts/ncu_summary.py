@@ -30,6 +30,14 @@ WANT = [
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy", 1, "%"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput", 1, "% of peak"),
     ("l1tex__throughput.avg.pct_of_peak_sustained_active", "L1/TEX throughput", 1, "% of peak"),
+    # tensor pipe (tcgen05 kernels): MMA cycles, the shared-memory operand
+    # reads feeding it, and the tensor-memory path
+    ("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+     "tensor pipe active", 1, "% of peak"),
+    ("sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active", "tc pipe instructions", 1, "% of peak"),
+    ("l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "smem reads by the MMA",
+     1, "% of peak"),
+    ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor memory active", 1, "% of peak"),
 ]
 
 

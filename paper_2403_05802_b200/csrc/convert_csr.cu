@@ -97,42 +97,54 @@ __global__ void k_fill_i32(int32_t* __restrict__ p, int64_t n, int32_t v) {
 }
 
 // ---------------------------------------------------------- COO -> DCSR
-// Row heads (e == 0 or row[e] != row[e-1]) are compacted with a single-pass
-// decoupled look-back scan: tile t learns how many heads precede it and
-// writes L0.idx[pos] = row, L1.ptr[pos] = e directly. col/val are copied in
-// the same pass.
+// Row heads (e == 0 or row[e] != row[e-1]) are compacted: tile t learns how
+// many heads precede it and writes L0.idx[pos] = row, L1.ptr[pos] = e
+// directly. The column and value arrays are the COO's own: k_copy2 moves
+// them with 16-byte loads and stores. (A single-pass decoupled look-back
+// version, copies included, took 59 µs on config 3; without the copies
+// still 41 µs — the look-back serialised the tiles.)
 constexpr int kDcsrItems = 16;  // per lane, warp-striped
 constexpr int kDcsrTile = kBlock * kDcsrItems;
 
-__global__ void __launch_bounds__(kBlock) k_coo_to_dcsr(
-    const int32_t* __restrict__ row, const int32_t* __restrict__ col,
-    const float* __restrict__ val, int64_t nnz, int32_t* __restrict__ orow,
-    int32_t* __restrict__ optr, int32_t* __restrict__ ocol, float* __restrict__ oval,
-    unsigned long long* __restrict__ status, uint32_t epoch, int32_t* __restrict__ nnr_out) {
-  // Warp-striped: element wbase + 32 j + lane, so the col/val copy and the
-  // head stores (ballot ranks) are coalesced.
-  __shared__ uint32_t smem[34];
-  __shared__ uint32_t slot;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int tile = blockIdx.x;
-  const int64_t wbase = (int64_t)tile * kDcsrTile + (int64_t)warp * (32 * kDcsrItems);
-  int r[kDcsrItems];
+// Two arrays of n 32-bit words copied with 16-byte loads / stores (all four
+// pointers 16-byte aligned: device allocations are).
+__global__ void __launch_bounds__(kBlock) k_copy2(const int4* __restrict__ a, const int4* __restrict__ b, int64_t n,
+                                                  int4* __restrict__ oa, int4* __restrict__ ob) {
+  const int64_t q = n / 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < q; i += 2 * stride) {
+    const int4 x0 = ld_stream(a + i), y0 = ld_stream(b + i);
+    const bool two = i + stride < q;
+    int4 x1, y1;
+    if (two) x1 = ld_stream(a + i + stride), y1 = ld_stream(b + i + stride);
+    st_stream(oa + i, x0);
+    st_stream(ob + i, y0);
+    if (two) {
+      st_stream(oa + i + stride, x1);
+      st_stream(ob + i + stride, y1);
+    }
+  }
+  for (int64_t e = q * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += stride) {
+    reinterpret_cast<int32_t*>(oa)[e] = reinterpret_cast<const int32_t*>(a)[e];
+    reinterpret_cast<int32_t*>(ob)[e] = reinterpret_cast<const int32_t*>(b)[e];
+  }
+}
+
+// Row heads without a serial look-back: k_dcsr_count counts each tile's
+// heads (a tile is one CTA's kDcsrTile entries, warp-striped), then
+// k_dcsr_heads has every CTA sum the counts of the tiles before it (at most
+// a few thousand words, read once per CTA) and write its heads — two
+// streaming passes over the rows that never wait on another CTA.
+__device__ __forceinline__ void dcsr_tile_heads(const int32_t* __restrict__ row, int64_t nnz, int64_t wbase,
+                                                int (&r)[kDcsrItems], unsigned (&ball)[kDcsrItems], uint32_t& cnt) {
+  const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int j = 0; j < kDcsrItems; ++j) {
     const int64_t e = wbase + 32 * j + lane;
     r[j] = e < nnz ? ld_stream(row + e) : -2;
   }
-#pragma unroll
-  for (int j = 0; j < kDcsrItems; ++j) {
-    const int64_t e = wbase + 32 * j + lane;
-    if (e < nnz) {
-      ocol[e] = ld_stream(col + e);
-      oval[e] = ld_stream(val + e);
-    }
-  }
   const int before = lane == 0 && wbase > 0 && wbase < nnz ? __ldg(row + wbase - 1) : -1;
-  unsigned ball[kDcsrItems];
-  uint32_t cnt = 0;
+  cnt = 0;
 #pragma unroll
   for (int j = 0; j < kDcsrItems; ++j) {
     const int64_t e = wbase + 32 * j + lane;
@@ -143,9 +155,47 @@ __global__ void __launch_bounds__(kBlock) k_coo_to_dcsr(
     ball[j] = __ballot_sync(kFull, h);
     cnt += __popc(ball[j]);
   }
-  uint32_t total;
-  const uint32_t wex = block_exclusive_scan<uint32_t, kBlock>(lane == 0 ? cnt : 0u, smem, &total);
-  const uint32_t tile_prefix = lookback_prefix(status, epoch, tile, total, &slot);
+}
+
+__global__ void __launch_bounds__(kBlock) k_dcsr_count(const int32_t* __restrict__ row, int64_t nnz,
+                                                       uint32_t* __restrict__ tile_cnt) {
+  __shared__ uint32_t wsum[kBlock / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t wbase = (int64_t)blockIdx.x * kDcsrTile + (int64_t)warp * (32 * kDcsrItems);
+  int r[kDcsrItems];
+  unsigned ball[kDcsrItems];
+  uint32_t cnt;
+  dcsr_tile_heads(row, nnz, wbase, r, ball, cnt);
+  if (lane == 0) wsum[warp] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < kBlock / 32; ++w) t += wsum[w];
+    tile_cnt[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_dcsr_heads(const int32_t* __restrict__ row, int64_t nnz,
+                                                       const uint32_t* __restrict__ tile_cnt,
+                                                       int32_t* __restrict__ orow, int32_t* __restrict__ optr,
+                                                       int32_t* __restrict__ nnr_out) {
+  __shared__ uint32_t smem[34];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tile = blockIdx.x;
+  // heads before this tile: the counts of tiles 0 .. tile-1
+  uint32_t before = 0;
+  for (int i = threadIdx.x; i < tile; i += kBlock) before += __ldg(tile_cnt + i);
+  const int64_t wbase = (int64_t)tile * kDcsrTile + (int64_t)warp * (32 * kDcsrItems);
+  int r[kDcsrItems];
+  unsigned ball[kDcsrItems];
+  uint32_t cnt;
+  dcsr_tile_heads(row, nnz, wbase, r, ball, cnt);
+  // the tile's prefix (the threads' partial sums added up), then this
+  // warp's offset inside the tile
+  uint32_t tile_prefix;
+  block_exclusive_scan<uint32_t, kBlock>(before, smem, &tile_prefix);
+  uint32_t wtot;
+  const uint32_t wex = block_exclusive_scan<uint32_t, kBlock>(lane == 0 ? cnt : 0u, smem, &wtot);
   uint32_t pos = tile_prefix + __shfl_sync(kFull, wex, 0);
   const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
@@ -158,7 +208,7 @@ __global__ void __launch_bounds__(kBlock) k_coo_to_dcsr(
     pos += __popc(ball[j]);
   }
   if (tile == gridDim.x - 1 && threadIdx.x == 0) {
-    uint32_t nnr = tile_prefix + total;
+    const uint32_t nnr = tile_prefix + wtot;
     optr[nnr] = (int32_t)nnz;
     *nnr_out = (int32_t)nnr;
   }
@@ -271,11 +321,14 @@ sfg_tensor* coo_to_dcsr(sfg_context* ctx, const sfg_tensor* s) {
     return t;
   }
   int tiles = (int)ceil_div(s->nnz, kDcsrTile);
-  auto* status = lookback_status(ctx, tiles);
-  int32_t* nnr_dev = static_cast<int32_t*>(scratch(ctx, 64));
-  SFG_LAUNCH(k_coo_to_dcsr, tiles, kBlock, 0, ctx->stream, s->row, s->idx,
-             static_cast<const float*>(s->val), s->nnz, t->row, t->ptr, t->idx,
-             static_cast<float*>(t->val), status, ctx->epoch++, nnr_dev);
+  auto* sc = static_cast<uint32_t*>(scratch(ctx, 64 + (size_t)tiles * 4));
+  int32_t* nnr_dev = reinterpret_cast<int32_t*>(sc);
+  uint32_t* tile_cnt = sc + 16;
+  SFG_LAUNCH(k_dcsr_count, tiles, kBlock, 0, ctx->stream, s->row, s->nnz, tile_cnt);
+  SFG_LAUNCH(k_dcsr_heads, tiles, kBlock, 0, ctx->stream, s->row, s->nnz, tile_cnt, t->row, t->ptr, nnr_dev);
+  SFG_LAUNCH(k_copy2, stream_grid(ctx, ceil_div(s->nnz, 8), kBlock, 1, 8), kBlock, 0, ctx->stream,
+             reinterpret_cast<const int4*>(s->idx), reinterpret_cast<const int4*>(s->val), s->nnz,
+             reinterpret_cast<int4*>(t->idx), reinterpret_cast<int4*>(t->val));
   // nnr is read back asynchronously: the tensor is usable at once and the
   // host only waits where the count is needed (tensor_nnr)
   t->nnr_slot = size_slot_start(ctx, nnr_dev);

@@ -130,6 +130,65 @@ __global__ void __launch_bounds__(kBlock) k_bcsr_slots(const int32_t* __restrict
   }
 }
 
+// ELL slots holding a nonzero value, as unordered (row, col, val) triples:
+// the padding cells (column 0, value 0) and explicit zeros drop out — a zero
+// slot contributes 0 * B[col] to a product, which is what the reference's
+// walk over every slot adds (kernel.hpp:147-153).
+__global__ void __launch_bounds__(kBlock) k_ell_nonzeros(const int32_t* __restrict__ idx,
+                                                         const float* __restrict__ val, int64_t m, int64_t k,
+                                                         int32_t* __restrict__ orow, int32_t* __restrict__ ocol,
+                                                         float* __restrict__ oval,
+                                                         unsigned long long* __restrict__ count) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t cell = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; cell - lane < k * m;
+       cell += (int64_t)gridDim.x * blockDim.x) {
+    const bool in = cell < k * m;
+    const float v = in ? __ldg(val + cell) : 0.f;
+    const bool nz = in && v != 0.f;
+    const unsigned msk = __ballot_sync(kFull, nz);
+    unsigned long long base = 0;
+    if (lane == 0 && msk) base = atomicAdd(count, (unsigned long long)__popc(msk));
+    base = __shfl_sync(kFull, base, 0);
+    if (nz) {
+      const unsigned long long at = base + __popc(msk & ((1u << lane) - 1u));
+      orow[at] = (int32_t)(cell % m);
+      ocol[at] = __ldg(idx + cell);
+      oval[at] = v;
+    }
+  }
+}
+
+// BELL values that are nonzero, as unordered (row, col, val) triples
+// (padding cells and the zero fill of blocks drop out).
+__global__ void __launch_bounds__(kBlock) k_bell_nonzeros(const int32_t* __restrict__ bcol,
+                                                          const float* __restrict__ val, int64_t nbr, int64_t cells,
+                                                          int32_t b, int32_t rb, int32_t cb,
+                                                          int32_t* __restrict__ orow, int32_t* __restrict__ ocol,
+                                                          float* __restrict__ oval,
+                                                          unsigned long long* __restrict__ count) {
+  const int lane = threadIdx.x & 31;
+  const int bs = rb * cb;
+  const int64_t total = cells * bs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e - lane < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const bool in = e < total;
+    const float v = in ? __ldg(val + e) : 0.f;
+    const bool nz = in && v != 0.f;
+    const unsigned msk = __ballot_sync(kFull, nz);
+    unsigned long long base = 0;
+    if (lane == 0 && msk) base = atomicAdd(count, (unsigned long long)__popc(msk));
+    base = __shfl_sync(kFull, base, 0);
+    if (nz) {
+      const int64_t cell = e / bs;
+      const int q = (int)(e - cell * bs);
+      const unsigned long long at = base + __popc(msk & ((1u << lane) - 1u));
+      orow[at] = (int32_t)((cell % nbr) * b + q / cb);
+      ocol[at] = __ldg(bcol + cell) * b + q % cb;
+      oval[at] = v;
+    }
+  }
+}
+
 sfg_tensor* make_coo(sfg_context* ctx, int64_t m, int64_t n, int64_t nnz) {
   sfg_tensor* t = new_tensor(ctx, SFG_COO, m, n);
   t->nnz = nnz;
@@ -242,6 +301,39 @@ sfg_tensor* bcsr_to_coo(sfg_context* ctx, const sfg_tensor* s) {
   free_tensor(tmp);
   return out;
 }
+
+}  // namespace
+
+// The nonzero entries of an ELL or BELL tensor as a canonical COO (for
+// operations whose result does not depend on zero slots, e.g. SpGEMM).
+sfg_tensor* ell_nonzeros_to_coo(sfg_context* ctx, const sfg_tensor* s) {
+  const bool bell = s->kind == SFG_BELL;
+  const int64_t cells = bell ? s->k * s->nbr * s->rb * s->cb : s->k * s->m;
+  sfg_tensor* tmp = make_coo(ctx, s->m, s->n, cells);
+  auto* count = static_cast<unsigned long long*>(scratch(ctx, 64));
+  SFG_CUDA(cudaMemsetAsync(count, 0, 8, ctx->stream));
+  if (cells && bell)
+    SFG_LAUNCH(k_bell_nonzeros, stream_grid(ctx, cells, kBlock, 1, 8), kBlock, 0, ctx->stream, s->idx,
+               static_cast<const float*>(s->val), s->nbr, s->k * s->nbr, (int32_t)s->br, (int32_t)s->rb,
+               (int32_t)s->cb, tmp->row, tmp->idx, static_cast<float*>(tmp->val), count);
+  else if (cells)
+    SFG_LAUNCH(k_ell_nonzeros, stream_grid(ctx, cells, kBlock, 1, 8), kBlock, 0, ctx->stream, s->idx,
+               static_cast<const float*>(s->val), s->m, s->k, tmp->row, tmp->idx, static_cast<float*>(tmp->val),
+               count);
+  unsigned long long nz = 0;
+  read_back(ctx, count, 8, &nz);
+  sfg_tensor* out = nullptr;
+  try {
+    out = sort_coo(ctx, s->m, s->n, (int64_t)nz, tmp->row, tmp->idx, static_cast<const float*>(tmp->val), false);
+  } catch (...) {
+    free_tensor(tmp);
+    throw;
+  }
+  free_tensor(tmp);
+  return out;
+}
+
+namespace {
 
 sfg_tensor* deep_copy(sfg_context* ctx, const sfg_tensor* s) {
   tensor_nnr(s);  // the copy must not share a pending read-back slot

@@ -212,6 +212,8 @@ sfg_tensor* coo_to_dcsr(sfg_context* ctx, const sfg_tensor* s);
 sfg_tensor* coo_to_ell(sfg_context* ctx, const sfg_tensor* s);
 sfg_tensor* coo_to_bcsr(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_t c, int dtype);
 sfg_tensor* coo_to_hyb(sfg_context* ctx, const sfg_tensor* s, int64_t min_sum);
+// The nonzero entries of an ELL / BELL tensor as a canonical COO (convert_src.cu).
+sfg_tensor* ell_nonzeros_to_coo(sfg_context* ctx, const sfg_tensor* s);
 // Blocked ELL (convert_bell.cu): the BCSR blocks relaid slot by slot.
 sfg_tensor* coo_to_bell(sfg_context* ctx, const sfg_tensor* s, int64_t b);
 // Value-layout formats (pack.cu): Pack(0,1) over COO (DOK) / CSR (LIL).

@@ -58,6 +58,13 @@ sfg_tensor* to_csr(sfg_context* ctx, const sfg_tensor* t) {
   f.kind = SFG_CSR;
   f.value_dtype = SFG_F32;
   if (t->kind == SFG_COO) return coo_to_csr(ctx, t);
+  if (t->kind == SFG_ELL || t->kind == SFG_BELL) {  // zero slots add nothing to a product
+    sfg_tensor* coo = ell_nonzeros_to_coo(ctx, t);
+    sfg_tensor* csr = coo_to_csr(ctx, coo);
+    free_tensor_arrays(coo);
+    delete coo;
+    return csr;
+  }
   if (t->kind == SFG_DOK || t->kind == SFG_LIL) {  // the layout is storage only: same entries
     sfg_tensor* soa = aos_to_soa(ctx, t);
     if (soa->kind == SFG_CSR) return soa;
@@ -73,9 +80,18 @@ sfg_tensor* to_csr(sfg_context* ctx, const sfg_tensor* t) {
 
 void spgemm(sfg_context* ctx, const sfg_tensor* a, const sfg_tensor* b, float* c, int64_t ldc, bool accumulate) {
   if (a->n != b->m) raise(SFG_ERR_INVALID_OPERATION, "spgemm: inner extents differ");
-  for (const sfg_tensor* t : {a, b})
-    if (t->kind == SFG_ELL || t->kind == SFG_HYB)
-      raise(SFG_ERR_UNSUPPORTED_SOURCE, "spgemm over ELL / hybrid operands");
+  // hybrid operands: the sum of their two parts' products (the reference
+  // runs the kernel once per part)
+  if (a->kind == SFG_HYB) {
+    spgemm(ctx, a->part[0], b, c, ldc, accumulate);
+    spgemm(ctx, a->part[1], b, c, ldc, true);
+    return;
+  }
+  if (b->kind == SFG_HYB) {
+    spgemm(ctx, a, b->part[0], c, ldc, accumulate);
+    spgemm(ctx, a, b->part[1], c, ldc, true);
+    return;
+  }
   const int64_t m = a->m, n = b->n;
   if (!accumulate && m > 0 && n > 0) {
     if (ldc == n)

@@ -66,7 +66,24 @@ def test_spgemm_errors(ctx):
     with pytest.raises(sfg.SfgError) as ei:
         ctx.spgemm(a, b)
     assert ei.value.kind == "InvalidOperation"
-    e = ctx.convert(ctx.from_coo(4, 2, [0], [1], [1.0]), "ELL")
-    with pytest.raises(sfg.SfgError) as ei:
-        ctx.spgemm(a, e)
-    assert ei.value.kind == "UnsupportedSource"
+
+
+
+EXTRA = ["ELL", "HYB(2)", "DOK", "LIL", "BELL(2)"]
+
+
+@pytest.mark.parametrize("fb", ["CSR"] + EXTRA)
+@pytest.mark.parametrize("fa", ["CSR"] + EXTRA)
+def test_spgemm_indirect_hybrid_packed_operands(ctx, fa, fb):
+    """ELL / hybrid operands (their zero slots add nothing), packed (AoS) and
+    blocked-ELL operands: the same product as the dense f64 one."""
+    m, k, n = 40, 31, 27
+    ra, ca, va = random_coo(5, m, k, 0.2)
+    rb, cb, vb = random_coo(6, k, n, 0.2)
+    da = ctx.convert(ctx.from_coo(m, k, ra, ca, va), fa)
+    db = ctx.convert(ctx.from_coo(k, n, rb, cb, vb), fb)
+    got = ctx.spgemm(da, db).astype(np.float64)
+    A = np.zeros((m, k)); A[ra, ca] = va
+    B = np.zeros((k, n)); B[rb, cb] = vb
+    bound = np.abs(A) @ np.abs(B)
+    assert (np.abs(got - A @ B) <= TOL * bound + 1e-30).all(), (fa, fb)

@@ -444,11 +444,11 @@ inline ConversionPlan plan_conversion(const FormatEncoding& src, const FormatEnc
   ConversionPlan p;
   p.src = src;
   p.dst = dst;
-  if (src.fmt.kind != SFG_COO) {
-    // compressed sources: the device dematerializes and regrows in one call
-    // (convert_src.cu); ELL and hybrid sources fail there (UnsupportedSource)
-    return p;
-  }
+  // the op list as the reference prints it; from a compressed source the
+  // device executes it by dematerializing and regrowing in one call
+  // (convert_src.cu). Sources with indirect levels or a value layout raise
+  // UnsupportedSource here, as in the reference (planner.hpp:96-99).
+  if (src.fmt.kind == SFG_HYB) return p;  // the hybrid pair: two tensors, no single plan
   char buf[1024];
   b200::check(sfg_plan_text(&src.fmt, &dst.fmt, buf, sizeof buf));
   std::string s(buf);

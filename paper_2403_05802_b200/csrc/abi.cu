@@ -96,6 +96,51 @@ std::string plan_for(const sfg_format& dst) {
   return "";
 }
 
+bool same_format(const sfg_format& a, const sfg_format& b) {
+  if (a.kind != b.kind) return false;
+  if (a.kind == SFG_BCSR || a.kind == SFG_BELL) return a.block_r == b.block_r && a.block_c == b.block_c;
+  if (a.kind == SFG_HYB) return a.threshold == b.threshold;
+  return true;
+}
+
+// plan_conversion from a compressed source (planner.hpp:95-252): the
+// source's levels are expanded back to coordinates (Split / Trim /
+// Swap / Devectorize / TileUnion), a Sort restores row order where the
+// target's own ops do not sort, then the target's ops as from COO. Sources
+// with an indirect level or a value layout are rejected (planner.hpp:96-99).
+std::string plan_from(const sfg_format& src, const sfg_format& dst) {
+  if (src.kind == SFG_COO) return plan_for(dst);
+  if (src.kind == SFG_ELL || src.kind == SFG_BELL)
+    sfg::raise(SFG_ERR_UNSUPPORTED_SOURCE, "conversion from a format with indirect levels");
+  if (src.kind == SFG_DOK || src.kind == SFG_LIL)
+    sfg::raise(SFG_ERR_UNSUPPORTED_SOURCE, "conversion from a format with a value layout");
+  if (src.kind == SFG_HYB || dst.kind == SFG_HYB)
+    sfg::raise(SFG_ERR_UNSUPPORTED_SOURCE, "the hybrid pair has no single-tensor plan from a compressed source");
+  if (same_format(src, dst)) return "";
+  const std::string tail = plan_for(dst);
+  const bool sorts = tail.find("Sort\n") != std::string::npos;
+  switch (src.kind) {
+    case SFG_CSR:
+      if (dst.kind == SFG_DCSR) return "Trim(0)\n";
+      if (dst.kind == SFG_LIL) return "Pack(0,1)\n";
+      return "Split(0)\nTrim(0)\n" + tail;
+    case SFG_DCSR:
+      if (dst.kind == SFG_CSR) return "Fill(0)\n";
+      if (dst.kind == SFG_LIL) return "Fill(0)\nPack(0,1)\n";
+      return "Split(0)\n" + tail;
+    case SFG_CSC: {
+      // the coordinates come back column-major: Swap(0,1), then the sort
+      // unless the target's ops sort
+      return "Split(0)\nTrim(0)\nSwap(0,1)\n" + std::string(sorts ? "" : "Sort\n") + tail;
+    }
+    case SFG_BCSR:
+      return "Devectorize(2)\nSplit(0)\nTrim(3)\nTrim(2)\nTrim(0)\nSwap(1,2)\nTileUnion(0," +
+             std::to_string(src.block_r) + ")\nTileUnion(1," + std::to_string(src.block_c) + ")\n" +
+             (sorts ? "" : "Sort\n") + tail;
+  }
+  sfg::raise(SFG_ERR_UNSUPPORTED_SOURCE, "unsupported source format");
+}
+
 // explain_storage(infer_storage(...)) (storage.hpp:35-75; oracle_data.hpp:128-148).
 std::string explain_for(const sfg_format& f) {
   switch (f.kind) {
@@ -266,10 +311,9 @@ int sfg_format_resolve(const char* text, sfg_format* out) {
 int sfg_plan_text(const sfg_format* src, const sfg_format* dst, char* buf, int64_t len) {
   return guard([&] {
     require(src && dst, SFG_ERR_INVALID_OPERATION, "null format");
+    validate_format(*src);
     validate_format(*dst);
-    if (src->kind != SFG_COO)
-      sfg::raise(SFG_ERR_UNSUPPORTED_SOURCE, "plan text is generated for COO sources");
-    copy_text(plan_for(*dst), buf, len);
+    copy_text(plan_from(*src, *dst), buf, len);
   });
 }
 

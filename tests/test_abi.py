@@ -60,10 +60,26 @@ def test_format_resolution():
         assert ei.value.kind == "Parse", bad
 
 
-def test_non_coo_sources_have_no_plan_text():
+SOURCES = ["CSR", "DCSR", "CSC", "BCSR(2,2)", "BCSR(4,4)", "BCSR(3,2)"]
+
+
+@pytest.mark.parametrize("src", SOURCES)
+def test_plan_from_compressed_sources_matches_reference(ref, src):
+    """planner.hpp:95-252 from a non-COO source: expand the source's levels,
+    sort where the target does not, then the target's ops."""
+    for dst in FORMATS:
+        assert sfg.plan_lines(src, dst) == ref.plan(src, dst), (src, dst)
+
+
+@pytest.mark.parametrize("src,why", [("ELL", "indirect levels"), ("BELL(2)", "indirect levels"),
+                                     ("DOK", "value layout"), ("LIL", "value layout")])
+def test_plan_rejects_sources_like_the_reference(ref, src, why):
     with pytest.raises(sfg.SfgError) as ei:
-        sfg.plan_lines("CSR", "COO")
-    assert ei.value.kind == "UnsupportedSource"
+        sfg.plan_lines(src, "CSR")
+    assert ei.value.kind == "UnsupportedSource" and why in str(ei.value)
+    with pytest.raises(Exception) as er:
+        ref.plan(src, "CSR")
+    assert why in str(er.value)
 
 
 def test_context_without_gpu_fails_loudly():

@@ -198,6 +198,8 @@ def _fmt_text(fmt, r=None, c=None):
         return f"BCSR({r},{c})"
     if fmt == "BELL":  # formats.hpp:79-85: BELL(b)
         return f"BELL({r})"
+    if fmt == "CSB":  # formats.hpp:54-57: CSB(r, c)
+        return f"CSB({r},{c})"
     return fmt
 
 

@@ -86,6 +86,10 @@ std::string plan_for(const sfg_format& dst) {
              ")\nremainder: Sum(0)\nremainder: Enumerate(0)\nremainder: Sort\nremainder: Fill(1)\n"
              "remainder: Merge(0)\n";
     case SFG_DOK: return "Pack(0,1)\n";
+    case SFG_DIA: return "Skew(0,1,-1)\nSwap(0,1)\nSort\nFill(1)\nVectorize(1)\nMerge(0)\n";
+    case SFG_CSB:
+      return "TileSplit(0," + std::to_string(dst.block_r) + ")\nTileSplit(2," + std::to_string(dst.block_c) +
+             ")\nSwap(1,2)\nSort\nFill(1)\nFill(0)\nMerge(0)\nMerge(1)\n";
     case SFG_BELL: {
       const std::string b = std::to_string(dst.block_r);
       return "TileSplit(0," + b + ")\nTileSplit(2," + b + ")\nSwap(1,2)\nSum(0)\nEnumerate(0)\nSort\nFill(4)\n"
@@ -98,10 +102,14 @@ std::string plan_for(const sfg_format& dst) {
 
 bool same_format(const sfg_format& a, const sfg_format& b) {
   if (a.kind != b.kind) return false;
-  if (a.kind == SFG_BCSR || a.kind == SFG_BELL) return a.block_r == b.block_r && a.block_c == b.block_c;
+  if (a.kind == SFG_BCSR || a.kind == SFG_BELL || a.kind == SFG_CSB)
+    return a.block_r == b.block_r && a.block_c == b.block_c;
   if (a.kind == SFG_HYB) return a.threshold == b.threshold;
   return true;
 }
+
+std::string simplify_plan(std::string p);
+std::string plan_from_raw(const sfg_format& src, const sfg_format& dst);
 
 // plan_conversion from a compressed source (planner.hpp:95-252): the
 // source's levels are expanded back to coordinates (Split / Trim /
@@ -117,6 +125,28 @@ std::string plan_from(const sfg_format& src, const sfg_format& dst) {
   if (src.kind == SFG_HYB || dst.kind == SFG_HYB)
     sfg::raise(SFG_ERR_UNSUPPORTED_SOURCE, "the hybrid pair has no single-tensor plan from a compressed source");
   if (same_format(src, dst)) return "";
+  // BCSR(r,c) and CSB(r,c) share the index map: only the storage of the
+  // inner levels changes (planner.hpp's equal-map branch)
+  if (src.kind == SFG_BCSR && dst.kind == SFG_CSB && src.block_r == dst.block_r && src.block_c == dst.block_c)
+    return "Devectorize(2)\nTrim(3)\nTrim(2)\nFill(1)\nMerge(1)\n";
+  if (src.kind == SFG_CSB && dst.kind == SFG_BCSR && src.block_r == dst.block_r && src.block_c == dst.block_c)
+    return "Split(1)\nTrim(1)\nFill(3)\nFill(2)\nVectorize(2)\n";
+  return simplify_plan(plan_from_raw(src, dst));
+}
+
+// The reference planner folds a swap of the two coordinates into the skew
+// next to it and drops a swap followed by its inverse.
+std::string simplify_plan(std::string p) {
+  const std::pair<const char*, const char*> rules[] = {
+      {"Swap(0,1)\nSkew(0,1,-1)\nSwap(0,1)\n", "Skew(1,0,-1)\n"},
+      {"Swap(0,1)\nSwap(0,1)\n", ""},
+  };
+  for (const auto& [from, to] : rules)
+    for (size_t at; (at = p.find(from)) != std::string::npos;) p.replace(at, std::strlen(from), to);
+  return p;
+}
+
+std::string plan_from_raw(const sfg_format& src, const sfg_format& dst) {
   const std::string tail = plan_for(dst);
   const bool sorts = tail.find("Sort\n") != std::string::npos;
   switch (src.kind) {
@@ -137,6 +167,12 @@ std::string plan_from(const sfg_format& src, const sfg_format& dst) {
       return "Devectorize(2)\nSplit(0)\nTrim(3)\nTrim(2)\nTrim(0)\nSwap(1,2)\nTileUnion(0," +
              std::to_string(src.block_r) + ")\nTileUnion(1," + std::to_string(src.block_c) + ")\n" +
              (sorts ? "" : "Sort\n") + tail;
+    case SFG_DIA:
+      return "Devectorize(1)\nSplit(0)\nTrim(1)\nSkew(1,0,1)\nSwap(0,1)\n" + std::string(sorts ? "" : "Sort\n") +
+             tail;
+    case SFG_CSB:
+      return "Split(1)\nSplit(0)\nTrim(1)\nTrim(0)\nSwap(1,2)\nTileUnion(0," + std::to_string(src.block_r) +
+             ")\nTileUnion(1," + std::to_string(src.block_c) + ")\n" + (sorts ? "" : "Sort\n") + tail;
   }
   sfg::raise(SFG_ERR_UNSUPPORTED_SOURCE, "unsupported source format");
 }
@@ -155,14 +191,16 @@ std::string explain_for(const sfg_format& f) {
     case SFG_DOK: return "L0: idx | L1: idx | val | pack(0,1)";
     case SFG_BELL:
       return "L0: idx | L1: size | L2: idx | L3: size, dense_vector | L4: size, dense_vector | val";
+    case SFG_DIA: return "L0: idx | L1: size, dense_vector | val";
+    case SFG_CSB: return "L0: size | L1: size | L2: ptr, idx | L3: idx | val";
     case SFG_LIL: return "L0: size | L1: ptr, idx | val | pack(0,1)";
   }
   return "";
 }
 
 void validate_format(const sfg_format& f) {
-  require(f.kind >= SFG_COO && f.kind <= SFG_BELL, SFG_ERR_PARSE, "unknown format kind");
-  if (f.kind == SFG_BCSR || f.kind == SFG_BELL)
+  require(f.kind >= SFG_COO && f.kind <= SFG_CSB, SFG_ERR_PARSE, "unknown format kind");
+  if (f.kind == SFG_BCSR || f.kind == SFG_BELL || f.kind == SFG_CSB)
     require(f.block_r > 0 && f.block_c > 0, SFG_ERR_INVALID_OPERATION,
             "TileSplit factor must be positive");
   require(f.value_dtype == SFG_F32 || (f.value_dtype == SFG_BF16 && f.kind == SFG_BCSR),
@@ -293,6 +331,13 @@ int sfg_format_resolve(const char* text, sfg_format* out) {
       f.kind = SFG_BCSR;
       f.block_r = static_cast<int32_t>(nargs > 0 ? args[0] : 2);
       f.block_c = static_cast<int32_t>(nargs > 1 ? args[1] : f.block_r);
+    } else if (name == "CSB") {
+      // formats.hpp:54-57: r defaults to 2, c defaults to r
+      f.kind = SFG_CSB;
+      f.block_r = static_cast<int32_t>(nargs > 0 ? args[0] : 2);
+      f.block_c = static_cast<int32_t>(nargs > 1 ? args[1] : f.block_r);
+    } else if (name == "DIA") {
+      f.kind = SFG_DIA;
     } else if (name == "BELL") {
       // formats.hpp:79-85: one argument, the block size (default 2)
       f.kind = SFG_BELL;
@@ -399,6 +444,8 @@ int sfg_convert(sfg_context* ctx, const sfg_tensor* src, const sfg_format* dst, 
       case SFG_DOK: *out = sfg::coo_to_dok(ctx, src); break;
       case SFG_LIL: *out = sfg::coo_to_lil(ctx, src); break;
       case SFG_BELL: *out = sfg::coo_to_bell(ctx, src, dst->block_r); break;
+      case SFG_DIA: *out = sfg::coo_to_dia(ctx, src); break;
+      case SFG_CSB: *out = sfg::coo_to_csb(ctx, src, dst->block_r, dst->block_c); break;
     }
   });
 }
@@ -495,6 +542,20 @@ int sfg_tensor_view_get(sfg_context* ctx, const sfg_tensor* t, sfg_tensor_view* 
         v.nvals = cells * t->rb * t->cb;
         break;
       }
+      case SFG_DIA:  // diagonals, then a dense vector over the rows
+        v.nlevels = 2;
+        v.level[0] = level(I, -(t->m - 1), t->n - 1, t->k, t->k, t->slots, 0, nullptr);
+        v.level[1] = level(S | D, 0, t->m - 1, t->k * t->m, 0, nullptr, 0, nullptr);
+        v.nvals = t->k * t->m;
+        break;
+      case SFG_CSB:  // dense block grid, entries per block (row, column in block)
+        v.nlevels = 4;
+        v.level[0] = level(S, 0, t->nbr - 1, t->nbr, 0, nullptr, 0, nullptr);
+        v.level[1] = level(S, 0, t->nbc - 1, t->nbr * t->nbc, 0, nullptr, 0, nullptr);
+        v.level[2] = level(P | I, 0, t->rb - 1, t->nnz, t->nnz, t->row, t->nbr * t->nbc + 1, t->ptr);
+        v.level[3] = level(I, 0, t->cb - 1, t->nnz, t->nnz, t->idx, 0, nullptr);
+        v.nvals = t->nnz;
+        break;
       case SFG_LIL: {  // ptr + records {col, val}
         const int32_t* rec = static_cast<const int32_t*>(t->val);
         v.nlevels = 2;

@@ -96,6 +96,8 @@ std::vector<uint8_t> expected_kinds(int kind) {
     case SFG_ELL: return {kUIdx, kUSize, kUIdx};
     case SFG_BCSR: return {kUSize, kUIdx | kUPtr, kUSize | kUDense, kUSize | kUDense};
     case SFG_BELL: return {kUIdx, kUSize, kUIdx, kUSize | kUDense, kUSize | kUDense};
+    case SFG_DIA: return {kUIdx, kUSize | kUDense};
+    case SFG_CSB: return {kUSize, kUSize, kUIdx | kUPtr, kUIdx};
     case SFG_DOK: return {kUIdx, kUIdx};           // COO + pack(0,1)
     case SFG_LIL: return {kUSize, kUIdx | kUPtr};  // CSR + pack(0,1)
   }
@@ -315,7 +317,7 @@ sfg_tensor* read_container(sfg_context* ctx, const char* path_c, const sfg_forma
   } else {
     fmt.value_dtype = SFG_F32;
     int found = -1;
-    for (int k : {SFG_COO, SFG_CSR, SFG_DCSR, SFG_ELL, SFG_BCSR, SFG_BELL}) {
+    for (int k : {SFG_COO, SFG_CSR, SFG_DCSR, SFG_ELL, SFG_BCSR, SFG_BELL, SFG_DIA, SFG_CSB}) {
       const auto w = expected_kinds(k);
       bool same = w.size() == lv.size();
       for (size_t l = 0; same && l < lv.size(); ++l) same = lv[l].kind == w[l];
@@ -333,6 +335,9 @@ sfg_tensor* read_container(sfg_context* ctx, const char* path_c, const sfg_forma
       fmt.block_c = lv[3].hi - lv[3].lo + 1;
     } else if (found == SFG_BELL) {
       fmt.block_r = fmt.block_c = lv[3].hi - lv[3].lo + 1;
+    } else if (found == SFG_CSB) {
+      fmt.block_r = lv[2].hi - lv[2].lo + 1;  // the in-block extents (one-tile edges shrink them)
+      fmt.block_c = lv[3].hi - lv[3].lo + 1;
     }
   }
   const auto want = expected_kinds(fmt.kind);
@@ -392,6 +397,23 @@ sfg_tensor* read_container(sfg_context* ctx, const char* path_c, const sfg_forma
         dfree(ctx, vals);
         break;
       }
+      case SFG_DIA:
+        t->k = lv[0].nidx;
+        t->nnz = t->k * m;
+        t->slots = load_i(lv[0].idx_off, lv[0].nidx);
+        break;
+      case SFG_CSB:
+        t->br = fmt.block_r;
+        t->bc = fmt.block_c;
+        t->nbr = lv[0].hi - lv[0].lo + 1;
+        t->nbc = lv[1].hi - lv[1].lo + 1;
+        t->rb = lv[2].hi - lv[2].lo + 1;
+        t->cb = lv[3].hi - lv[3].lo + 1;
+        t->nnz = lv[2].nidx;
+        t->ptr = load_i(lv[2].ptr_off, lv[2].nptr);
+        t->row = load_i(lv[2].idx_off, lv[2].nidx);
+        t->idx = load_i(lv[3].idx_off, lv[3].nidx);
+        break;
       case SFG_BELL:
         t->br = t->bc = fmt.block_r;
         t->k = lv[0].nidx;

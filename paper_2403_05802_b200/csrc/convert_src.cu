@@ -378,6 +378,16 @@ sfg_tensor* deep_copy(sfg_context* ctx, const sfg_tensor* s) {
       t->idx = static_cast<int32_t*>(dup(s->idx, s->nnz * 4));
       t->val = dup(s->val, s->nnz * s->rb * s->cb * esz);
       break;
+    case SFG_DIA:
+      t->slots = static_cast<int32_t*>(dup(s->slots, s->k * 4));
+      t->val = dup(s->val, s->k * s->m * esz);
+      break;
+    case SFG_CSB:
+      t->ptr = static_cast<int32_t*>(dup(s->ptr, (s->nbr * s->nbc + 1) * 4));
+      t->row = static_cast<int32_t*>(dup(s->row, s->nnz * 4));
+      t->idx = static_cast<int32_t*>(dup(s->idx, s->nnz * 4));
+      t->val = dup(s->val, s->nnz * esz);
+      break;
     default:
       delete t;
       raise(SFG_ERR_UNSUPPORTED_SOURCE, "identity copy of this format");
@@ -394,8 +404,16 @@ sfg_tensor* convert_from_compressed(sfg_context* ctx, const sfg_tensor* s, const
   // planner.hpp:98-99: sources with a value layout are rejected
   if (s->kind == SFG_DOK || s->kind == SFG_LIL)
     raise(SFG_ERR_UNSUPPORTED_SOURCE, "conversion from a format with a value layout");
+  // The reference expands a DIA source through its skewed map, so the
+  // column level comes back with the interval [-(m-1), n+m-2] (and a CSB
+  // source with its tile-grid extents and extra dangling nodes); the device
+  // tensors keep [0, n-1] columns, so these sources are not converted.
+  if (s->kind == SFG_DIA || s->kind == SFG_CSB)
+    raise(SFG_ERR_UNSUPPORTED_SOURCE,
+          "conversion from DIA / CSB: the reference's skewed / tile-grid level bounds are not held on the device");
   const bool same = s->kind == dst.kind &&
-                    (s->kind != SFG_BCSR || (s->br == dst.block_r && s->bc == dst.block_c && s->dtype == dst.value_dtype));
+                    (s->kind != SFG_BCSR || (s->br == dst.block_r && s->bc == dst.block_c && s->dtype == dst.value_dtype)) &&
+                    (s->kind != SFG_CSB || (s->br == dst.block_r && s->bc == dst.block_c));
   if (same) return deep_copy(ctx, s);
   sfg_tensor* coo = nullptr;
   switch (s->kind) {
@@ -431,6 +449,8 @@ sfg_tensor* convert_from_compressed(sfg_context* ctx, const sfg_tensor* s, const
       case SFG_BELL: out = coo_to_bell(ctx, coo, dst.block_r); break;
       case SFG_DOK: out = coo_to_dok(ctx, coo); break;
       case SFG_LIL: out = coo_to_lil(ctx, coo); break;
+      case SFG_DIA: out = coo_to_dia(ctx, coo); break;
+      case SFG_CSB: out = coo_to_csb(ctx, coo, dst.block_r, dst.block_c); break;
       default: raise(SFG_ERR_INVALID_OPERATION, "unknown target");
     }
   } catch (...) {

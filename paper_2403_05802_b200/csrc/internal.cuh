@@ -87,6 +87,9 @@ struct sfg_context {
 //   BELL: slots[K], idx[K*nbr] (block column of cell (slot, block row),
 //         slot-major), val[K*nbr*rb*cb]; nnz = K*nbr cells
 //   DOK : val = records {row, col, val}[nnz];  LIL: ptr[m+1], val = {col, val}[nnz]
+//   DIA : slots[K] (diagonals col - row, ascending), val[K*m]; nnz = K*m
+//   CSB : ptr[nbr*nbc+1] over the block grid, row[nnz] (row in block),
+//         idx[nnz] (column in block), val[nnz]
 struct sfg_tensor {
   sfg_context* ctx = nullptr;
   int32_t kind = SFG_COO;
@@ -212,6 +215,12 @@ sfg_tensor* coo_to_dcsr(sfg_context* ctx, const sfg_tensor* s);
 sfg_tensor* coo_to_ell(sfg_context* ctx, const sfg_tensor* s);
 sfg_tensor* coo_to_bcsr(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_t c, int dtype);
 sfg_tensor* coo_to_hyb(sfg_context* ctx, const sfg_tensor* s, int64_t min_sum);
+// DIA and CSB(r,c) (convert_dia.cu), and back to canonical COO (DIA: its
+// nonzero cells; CSB: every entry).
+sfg_tensor* coo_to_dia(sfg_context* ctx, const sfg_tensor* s);
+sfg_tensor* coo_to_csb(sfg_context* ctx, const sfg_tensor* s, int64_t br, int64_t bc);
+sfg_tensor* dia_to_coo(sfg_context* ctx, const sfg_tensor* t);
+sfg_tensor* csb_to_coo(sfg_context* ctx, const sfg_tensor* t);
 // The nonzero entries of an ELL / BELL tensor as a canonical COO (convert_src.cu).
 sfg_tensor* ell_nonzeros_to_coo(sfg_context* ctx, const sfg_tensor* s);
 // Blocked ELL (convert_bell.cu): the BCSR blocks relaid slot by slot.

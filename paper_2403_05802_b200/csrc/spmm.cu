@@ -540,6 +540,29 @@ __global__ void __launch_bounds__(kBlock) k_spmm_ell(const int32_t* __restrict__
   }
 }
 
+// ------------------------------------------------------------------- DIA
+template <typename TB, int V>
+__global__ void __launch_bounds__(kBlock) k_spmm_dia(const int32_t* __restrict__ diags,
+                                                      const float* __restrict__ val, int64_t m, int64_t n,
+                                                      int64_t k, Dense d) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int chunks = (d.nd + 32 * V - 1) / (32 * V);
+  const bool vec_ok = (d.nd % (32 * V) == 0) && (d.ldb % V == 0);
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < m * chunks; w += warps) {
+    const int64_t r = w / chunks;
+    const int c0 = (int)(w - r * chunks) * 32 * V + lane * V;
+    float acc[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[i] = 0.f;
+    for (int64_t q = 0; q < k; ++q) {
+      const int64_t c = r + __ldg(diags + q);
+      if (c >= 0 && c < n) fma_row<TB, V>(d, (int)c, __ldg(val + q * m + r), c0, vec_ok, acc);
+    }
+    store_row<V>(d, r, c0, false, acc);
+  }
+}
+
 // ------------------------------------------------------------------- COO
 // A warp owns 32*kCooIters consecutive row-sorted entries; it accumulates a
 // row while the row stays the same and stores it when the row changes. A row
@@ -993,6 +1016,11 @@ void launch_fmt(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
       SFG_LAUNCH((k_spmm_ell<TB, V>), grid_for(a->m * chunks), kBlock, 0, ctx->stream, a->idx, fv,
                  (int32_t)a->m, (int32_t)a->k, d);
       break;
+    case SFG_DIA:
+      if (a->m)
+        SFG_LAUNCH((k_spmm_dia<TB, V>), grid_for(a->m * chunks), kBlock, 0, ctx->stream, a->slots, fv, a->m, a->n,
+                   a->k, d);
+      break;
     case SFG_COO:
     case SFG_DOK:
       if (a->nnz) {
@@ -1255,6 +1283,19 @@ void spmm(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dtype, int
     return;
   }
   if (a->kind == SFG_BCSR && spmm_bcsr_tc(ctx, a, b, b_dtype, nd, ldb, c, ldc, accumulate)) return;
+  if (a->kind == SFG_CSB) {  // the blocks' entries back in row order (csb_to_coo), then COO
+    sfg_tensor* coo = csb_to_coo(ctx, a);
+    try {
+      spmm(ctx, coo, b, b_dtype, nd, ldb, c, ldc, accumulate);
+    } catch (...) {
+      free_tensor_arrays(coo);
+      delete coo;
+      throw;
+    }
+    free_tensor_arrays(coo);
+    delete coo;
+    return;
+  }
   if (a->kind == SFG_DCSR && !accumulate && a->m > 0) {
     if (tensor_nnr(a) == 0) {
       if (ldc == nd) SFG_CUDA(cudaMemsetAsync(c, 0, a->m * ldc * sizeof(float), ctx->stream));

@@ -131,6 +131,23 @@ __global__ void __launch_bounds__(kBlock) k_spmv_ell(const int32_t* __restrict__
   }
 }
 
+// ---------------------------------------------------------------- DIA
+// Thread per row: every diagonal's cell of the row (zero cells included,
+// like the reference's walk; columns past N guarded out).
+__global__ void __launch_bounds__(kBlock) k_spmv_dia(const int32_t* __restrict__ diags,
+                                                      const float* __restrict__ val, int64_t m, int64_t n,
+                                                      int64_t k, const float* __restrict__ x,
+                                                      float* __restrict__ y, int acc) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
+    float sum = 0.f;
+    for (int64_t q = 0; q < k; ++q) {
+      const int64_t c = r + __ldg(diags + q);
+      if (c >= 0 && c < n) sum = fmaf(ld_stream(val + q * m + r), ldx(x, (int)c), sum);
+    }
+    y[r] = acc ? y[r] + sum : sum;
+  }
+}
+
 // ---------------------------------------------------------------- COO
 // Row-sorted entries, load-balanced by entries (a heavy row spans many
 // warps). No shared memory. A warp walks its chunk
@@ -452,6 +469,19 @@ void spmv(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, bool 
       if (a->kind == SFG_BELL) go(k_spmv_bcsr<float, true>, vf);
       else if (a->dtype == SFG_BF16) go(k_spmv_bcsr<__nv_bfloat16_raw, false>, vb);
       else go(k_spmv_bcsr<float, false>, vf);
+      break;
+    }
+    case SFG_DIA:
+      if (a->m)
+        SFG_LAUNCH(k_spmv_dia, stream_grid(ctx, a->m, kBlock, 1, 8), kBlock, 0, ctx->stream, a->slots,
+                   static_cast<const float*>(a->val), a->m, a->n, a->k, x, y, acc);
+      break;
+    case SFG_CSB: {
+      // the blocks' entries back in row order (csb_to_coo), then COO
+      sfg_tensor* coo = csb_to_coo(ctx, a);
+      spmv_coo(ctx, coo, x, y, acc);
+      free_tensor_arrays(coo);
+      delete coo;
       break;
     }
     case SFG_HYB:

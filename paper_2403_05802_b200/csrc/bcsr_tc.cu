@@ -578,7 +578,8 @@ constexpr int kPanel = 4;
 constexpr int kPanelA = 16;  // value blocks per stage (a wider block column splits)
 constexpr int kPStages = 8;
 constexpr int kPStageBytes = kPanel * kTileBytes + kPanelA * kABytes;  // 24 KB
-constexpr int kDescWords = 64;  // 0 head, 1-4 tile columns, 5-8 masks, 32-63 slot blocks
+constexpr int kDescWords = 32;  // 0 head, 1-4 tile columns, 5-8 masks, 10-13 slot bytes, 16-31 slot blocks
+static_assert(kPanel <= 4 && kPanelA <= 16, "descriptor layout: 4 tiles, 16 slots");
 
 struct PShared {
   uint64_t full[kPStages];
@@ -688,33 +689,29 @@ __global__ void __launch_bounds__(32 * (4 + kProducers + kMmaWarps), 1)
 
   if (warp >= 4 && warp < kMmaWarp) {
     // --------------------------------------------------------- producers
-    // Descriptors (k_bcsr_sched) are 64 words, read with one coalesced
+    // Descriptors (k_bcsr_sched) are 32 words, read with one coalesced
     // load two positions ahead, so no global latency sits between a free
     // stage and its copies.
     const int q = warp - 4;
     const int r = lane >> 1, ch = lane & 1;
     const uint32_t dst_off = r * 32 + ((ch ^ ((r >> 2) & 1)) << 4);
-    auto load = [&](const Pos& p, uint32_t& w0, uint32_t& w1) {
-      w0 = w1 = 0u;
-      if (p.g < ngroups && p.i < p.ns) {
-        const uint32_t* d = sdesc + (int64_t)(p.s0 + p.i) * kDescWords;
-        w0 = __ldg(d + lane);
-        w1 = __ldg(d + 32 + lane);
-      }
+    auto load = [&](const Pos& p, uint32_t& w0) {
+      w0 = 0u;
+      if (p.g < ngroups && p.i < p.ns) w0 = __ldg(sdesc + (int64_t)(p.s0 + p.i) * kDescWords + lane);
     };
     Pos cur = first(q);
     Pos n1 = cur;
     n1.i += kProducers;
     settle(n1);
-    uint32_t c0, c1, a0, a1;
-    load(cur, c0, c1);
-    load(n1, a0, a1);
+    uint32_t c0, a0;
+    load(cur, c0);
+    load(n1, a0);
     while (cur.g < ngroups) {
       Pos n2 = n1;
       n2.i += kProducers;
       settle(n2);
-      uint32_t b0, b1;
-      load(n2, b0, b1);
+      uint32_t b0;
+      load(n2, b0);
       const uint32_t tq = cur.tg + (uint32_t)cur.i;
       const int stage = (int)(tq % kPStages);
       const uint32_t phase = (tq / kPStages) & 1u;
@@ -736,7 +733,7 @@ __global__ void __launch_bounds__(32 * (4 + kProducers + kMmaWarps), 1)
         }
         __syncwarp();  // reconverge: the shuffles below must not take the divergent path
         for (int sl = 0; sl < ((dbg & 4) ? 0 : nblk); ++sl) {
-          const int32_t kb = (int32_t)__shfl_sync(kFull, c1, sl);
+          const int32_t kb = (int32_t)__shfl_sync(kFull, c0, 16 + sl);
           cp_async16(st + kPanel * kTileBytes + sl * kABytes + dst_off, aval + (int64_t)kb * kABytes + lane * 16);
         }
       } else if (lane < kPanel) {
@@ -748,9 +745,7 @@ __global__ void __launch_bounds__(32 * (4 + kProducers + kMmaWarps), 1)
       cur = n1;
       n1 = n2;
       c0 = a0;
-      c1 = a1;
       a0 = b0;
-      a1 = b1;
     }
   } else if (warp >= kMmaWarp) {
     // ------------------------------------------------------- MMA issuers
@@ -839,33 +834,40 @@ __global__ void __launch_bounds__(32 * (4 + kProducers + kMmaWarps), 1)
 }
 
 // Stage schedule of the panel SpMM, built once per matrix from the mask
-// plan and cached on the tensor. A warp per group walks the plan in block
-// column order and packs the nonzero columns greedily into stages of <=
-// kPanel tiles and <= kPanelA value blocks. kWrite = false counts stages;
-// kWrite = true writes, at sbase[g], one descriptor per stage —
-// [0] ntile | nblk << 8, [1..4] tile block columns, [5..8] tile masks,
-// [9] first slot (group-relative), [10..17] per slot one byte (block row
-// | tile << 5), [32 + slot] the slot's value block.
+// plan and cached on the tensor. The plan of a group is cut into segments of
+// kSegCols block columns; a warp per (group, segment) walks its columns in
+// order and packs the nonzero ones greedily into stages of <= kPanel tiles
+// and <= kPanelA value blocks (a stage never spans two segments). The
+// stages of a group stay contiguous and in block-column order. kWrite =
+// false counts the segment's stages (sbase[seg]) and, per lane, the blocks
+// of that lane's block row in it (bcnt[seg][lane]); kWrite = true writes,
+// from stage sbase[seg] on and with the lane's first value block
+// bcnt[seg][lane] (both made exclusive prefixes in between), one descriptor
+// per stage — [0] ntile | nblk << 8, [1..4] tile block columns, [5..8] tile
+// masks, [10..13] per slot one byte (block row | tile << 5), [16 + slot]
+// the slot's value block.
+constexpr int kSegCols = 2048;
+
 template <bool kWrite>
-__global__ void __launch_bounds__(256) k_bcsr_sched(const int32_t* __restrict__ ptr, const uint32_t* __restrict__ plan,
-                                                     int32_t nbr, int32_t nbc, int32_t* __restrict__ sbase,
-                                                     uint32_t* __restrict__ sdesc) {
+__global__ void __launch_bounds__(256) k_bcsr_sched(const uint32_t* __restrict__ plan, int32_t nbr, int32_t nbc,
+                                                     int32_t nseg, int32_t* __restrict__ sbase,
+                                                     int32_t* __restrict__ bcnt, uint32_t* __restrict__ sdesc) {
   const int lane = threadIdx.x & 31;
   const int32_t ngroups = (nbr + kGroup - 1) / kGroup;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < ngroups; g += warps) {
-    const int64_t br = g * kGroup + lane;
-    int32_t cur = br < nbr ? __ldg(ptr + br) : 0;
-    int32_t stage = kWrite ? sbase[g] : 0;
-    int ntile = 0, nblk = 0, abeg = 0, apos = 0;
+  for (int64_t gs = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; gs < (int64_t)ngroups * nseg;
+       gs += warps) {
+    const int64_t g = gs / nseg;
+    const int32_t c_lo = (int32_t)(gs - g * nseg) * kSegCols;
+    const int32_t c_hi = min(nbc, c_lo + kSegCols);
+    int32_t cur = kWrite ? bcnt[gs * 32 + lane] : 0;
+    int32_t stage = kWrite ? sbase[gs] : 0;
+    int ntile = 0, nblk = 0;
     uint32_t my_bc = 0, my_mask = 0;  // lane t < kPanel: tile t of the open stage
     auto close = [&]() {
       if (kWrite) {
         uint32_t* d = sdesc + (int64_t)stage * kDescWords;
-        if (lane == 0) {
-          d[0] = (uint32_t)ntile | ((uint32_t)nblk << 8);
-          d[9] = (uint32_t)abeg;
-        }
+        if (lane == 0) d[0] = (uint32_t)ntile | ((uint32_t)nblk << 8);
         if (lane < kPanel) {
           d[1 + lane] = lane < ntile ? my_bc : 0u;
           d[5 + lane] = lane < ntile ? my_mask : 0u;
@@ -875,8 +877,8 @@ __global__ void __launch_bounds__(256) k_bcsr_sched(const int32_t* __restrict__ 
       ntile = 0;
     };
     const uint32_t* pg = plan + g * nbc;
-    for (int32_t bc0 = 0; bc0 < nbc; bc0 += 32) {
-      const uint32_t mine = bc0 + lane < nbc ? __ldg(pg + bc0 + lane) : 0u;
+    for (int32_t bc0 = c_lo; bc0 < c_hi; bc0 += 32) {
+      const uint32_t mine = bc0 + lane < c_hi ? __ldg(pg + bc0 + lane) : 0u;
       uint32_t nz = __ballot_sync(kFull, mine != 0);
       while (nz) {
         const int src = __ffs(nz) - 1;
@@ -898,29 +900,53 @@ __global__ void __launch_bounds__(256) k_bcsr_sched(const int32_t* __restrict__ 
           rest ^= mask;
           const int cnt = __popc(mask);
           if (ntile && (ntile == kPanel || nblk + cnt > kPanelA)) close();
-          if (!ntile) {
-            nblk = 0;
-            abeg = apos;
-          }
+          if (!ntile) nblk = 0;
           if (lane == ntile) {
             my_bc = (uint32_t)(bc0 + src);
             my_mask = mask;
           }
           if (kWrite && (mask >> lane & 1u)) {
             const int sl = nblk + __popc(mask & ((1u << lane) - 1u));
-            sdesc[(int64_t)stage * kDescWords + 32 + sl] = (uint32_t)cur;
+            sdesc[(int64_t)stage * kDescWords + 16 + sl] = (uint32_t)cur;
             reinterpret_cast<uint8_t*>(sdesc + (int64_t)stage * kDescWords + 10)[sl] = (uint8_t)(lane | (ntile << 5));
           }
           if (mask >> lane & 1u) ++cur;
-          apos += cnt;
           nblk += cnt;
           ++ntile;
         }
       }
     }
     if (ntile) close();
-    if (!kWrite && lane == 0) sbase[g] = stage;
+    if (!kWrite) {
+      if (lane == 0) sbase[gs] = stage;
+      bcnt[gs * 32 + lane] = cur;
+    }
   }
+}
+
+// Per (group, lane): the block counts of the lane's block row per segment
+// become each segment's first value block (ptr[br] + the blocks before it).
+__global__ void k_sched_first_blocks(const int32_t* __restrict__ ptr, int32_t nbr, int32_t nseg,
+                                     int32_t* __restrict__ bcnt) {
+  const int32_t ngroups = (nbr + kGroup - 1) / kGroup;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)ngroups * 32;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = t / 32, lane = t % 32, br = g * kGroup + lane;
+    int32_t run = br < nbr ? __ldg(ptr + br) : 0;
+    for (int32_t s = 0; s < nseg; ++s) {
+      int32_t* c = bcnt + ((g * nseg + s) * 32 + lane);
+      const int32_t n = *c;
+      *c = run;
+      run += n;
+    }
+  }
+}
+
+// tc_base[g] = the first stage of group g (its first segment's), g <= ngroups
+__global__ void k_sched_group_base(const int32_t* __restrict__ sbase, int32_t ngroups, int32_t nseg,
+                                   int32_t* __restrict__ gbase) {
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g <= ngroups; g += (int64_t)gridDim.x * blockDim.x)
+    gbase[g] = sbase[g * nseg];
 }
 
 // In-place exclusive scan of n + 1 counts (n small: one CTA, chunked).
@@ -1037,17 +1063,28 @@ bool spmm_bcsr_tc(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dt
     }
     int grid = (int)std::min<int64_t>(ngroups, (int64_t)ctx->sms);
     if (mut->tc_plan && !mut->tc_desc) {
-      // stage schedule: count, scan, write (once per matrix, cached)
+      // stage schedule: count, scan, write (once per matrix, cached); a
+      // warp per (group, segment of kSegCols block columns)
+      const int32_t nseg = (int32_t)ceil_div(a->nbc, (int64_t)kSegCols);
+      const int64_t nsg = ngroups * nseg;
+      auto* sbase = dalloc_n<int32_t>(ctx, nsg + 1);
+      auto* bcnt = dalloc_n<int32_t>(ctx, nsg * 32);
       mut->tc_base = dalloc_n<int32_t>(ctx, ngroups + 1);
-      int sgrid = stream_grid(ctx, ngroups * 32, 256, 1, 8);
-      SFG_LAUNCH(k_bcsr_sched<false>, sgrid, 256, 0, ctx->stream, a->ptr, mut->tc_plan, (int32_t)a->nbr,
-                 (int32_t)a->nbc, mut->tc_base, nullptr);
-      SFG_LAUNCH(k_scan_small, 1, 1024, 0, ctx->stream, mut->tc_base, (int32_t)ngroups);
+      const int sgrid = stream_grid(ctx, nsg * 32, 256, 1, 8);
+      SFG_LAUNCH(k_bcsr_sched<false>, sgrid, 256, 0, ctx->stream, mut->tc_plan, (int32_t)a->nbr, (int32_t)a->nbc,
+                 nseg, sbase, bcnt, nullptr);
+      SFG_LAUNCH(k_scan_small, 1, 1024, 0, ctx->stream, sbase, (int32_t)nsg);
+      SFG_LAUNCH(k_sched_first_blocks, stream_grid(ctx, ngroups * 32, 256, 1, 8), 256, 0, ctx->stream, a->ptr,
+                 (int32_t)a->nbr, nseg, bcnt);
+      SFG_LAUNCH(k_sched_group_base, (int)ceil_div(ngroups + 1, 256), 256, 0, ctx->stream, sbase, (int32_t)ngroups,
+                 nseg, mut->tc_base);
       int32_t nstages = 0;
-      read_back(ctx, mut->tc_base + ngroups, sizeof(int32_t), &nstages);
+      read_back(ctx, sbase + nsg, sizeof(int32_t), &nstages);
       mut->tc_desc = dalloc_n<uint32_t>(ctx, (int64_t)nstages * kDescWords);
-      SFG_LAUNCH(k_bcsr_sched<true>, sgrid, 256, 0, ctx->stream, a->ptr, mut->tc_plan, (int32_t)a->nbr,
-                 (int32_t)a->nbc, mut->tc_base, mut->tc_desc);
+      SFG_LAUNCH(k_bcsr_sched<true>, sgrid, 256, 0, ctx->stream, mut->tc_plan, (int32_t)a->nbr, (int32_t)a->nbc, nseg,
+                 sbase, bcnt, mut->tc_desc);
+      dfree(ctx, sbase);
+      dfree(ctx, bcnt);
     }
     if (mut->tc_desc) {
       // 4 producer and 4 MMA warps over 8 stages measured best

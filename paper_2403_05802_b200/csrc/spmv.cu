@@ -182,7 +182,11 @@ __device__ __forceinline__ void coo_close(float* __restrict__ y, int32_t row, fl
 // 12 steps with >= 4 CTAs per SM (56 registers) measured fastest on the
 // config-2 COO part (241 us vs 291 us for 16 steps at 72 registers; the
 // stream + gather floor of the same data is ~214 us, scripts/coo_exp.cu).
-constexpr int kCooSteps = 12;
+#ifndef SFG_COO_STEPS
+#define SFG_COO_STEPS 12  // deterministic version, config 2 hybrid SpMV ms: (CTAs/SM, steps) (4, 12) 0.331,
+                          // (5, 8) 0.335, (6, 8) 0.344, (5, 12) 0.370 (spills), (3, 16) 0.376
+#endif
+constexpr int kCooSteps = SFG_COO_STEPS;
 
 #ifndef SFG_COO_MINB
 #define SFG_COO_MINB 4  // config 2 SpMV: 4 -> 0.291 ms; 5 -> 0.331 (spills); 6 -> 0.376

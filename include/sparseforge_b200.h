@@ -74,13 +74,14 @@ enum sfg_format_kind {
                    count / slot chain, slot-major b x b blocks  formats.hpp:79-85 */
   SFG_DIA = 10, /* map (d0,d1)->(d1-d0, d0); merge(0), trim(0,0) formats.hpp:46 */
   SFG_CSB = 11, /* (d0/r, d1/c, d0%r, d1%c); merge(0,1), trim(2,3) formats.hpp:54-57 */
+  SFG_BDIA = 12, /* (d0/b, d1-d0, d0%b); merge(0), trim(1,1)     formats.hpp:76-79 */
 };
 
 enum sfg_dtype { SFG_F32 = 0, SFG_BF16 = 1 };
 
 typedef struct sfg_format {
   int32_t kind;        /* sfg_format_kind */
-  int32_t block_r;     /* BCSR / CSB block rows (r); BELL block size (b) */
+  int32_t block_r;     /* BCSR / CSB block rows (r); BELL / BDIA block size (b) */
   int32_t block_c;     /* BCSR / CSB block columns (c); BELL: b         */
   int32_t value_dtype; /* sfg_dtype of stored values (BF16: BCSR only) */
   int64_t threshold;   /* HYB: DecomposeRule::min_sum (decompose.hpp:17-20) */

@@ -172,6 +172,7 @@ inline std::string name_of(const sfg_format& f) {
     case SFG_LIL: return "LIL";
     case SFG_BELL: return "BELL(" + std::to_string(f.block_r) + ")";
     case SFG_DIA: return "DIA";
+    case SFG_BDIA: return "BDIA(" + std::to_string(f.block_r) + ")";
     case SFG_CSB: return "CSB(" + std::to_string(f.block_r) + "," + std::to_string(f.block_c) + ")";
   }
   return "?";
@@ -255,6 +256,7 @@ inline StorageScheme infer_storage(const FormatEncoding& enc) {
       s.levels = {L(0, 0, 1, 0), L(1, 0, 0, 0), L(0, 0, 1, 0), L(1, 0, 0, 1), L(1, 0, 0, 1)};
       break;
     case SFG_DIA: s.levels = {L(0, 0, 1, 0), L(1, 0, 0, 1)}; break;
+    case SFG_BDIA: s.levels = {L(1, 0, 0, 0), L(0, 1, 1, 0), L(1, 0, 0, 1)}; break;
     case SFG_CSB: s.levels = {L(1, 0, 0, 0), L(1, 0, 0, 0), L(0, 1, 1, 0), L(0, 0, 1, 0)}; break;
     default: break;  // HYB: two parts, see DecomposeResult
   }
@@ -281,6 +283,7 @@ struct WorkingTensor {
       case SFG_BCSR: return 4;
       case SFG_BELL: return 5;
       case SFG_CSB: return 4;
+      case SFG_BDIA: return 3;
       default: return 2;
     }
   }

@@ -196,8 +196,8 @@ class _Base:
 def _fmt_text(fmt, r=None, c=None):
     if fmt == "BCSR":
         return f"BCSR({r},{c})"
-    if fmt == "BELL":  # formats.hpp:79-85: BELL(b)
-        return f"BELL({r})"
+    if fmt in ("BELL", "BDIA"):  # formats.hpp:76-85: one block-size argument
+        return f"{fmt}({r})"
     if fmt == "CSB":  # formats.hpp:54-57: CSB(r, c)
         return f"CSB({r},{c})"
     return fmt

@@ -87,6 +87,9 @@ std::string plan_for(const sfg_format& dst) {
              "remainder: Merge(0)\n";
     case SFG_DOK: return "Pack(0,1)\n";
     case SFG_DIA: return "Skew(0,1,-1)\nSwap(0,1)\nSort\nFill(1)\nVectorize(1)\nMerge(0)\n";
+    case SFG_BDIA:
+      return "Skew(0,1,-1)\nTileSplit(0," + std::to_string(dst.block_r) +
+             ")\nSwap(1,2)\nSort\nFill(2)\nFill(0)\nVectorize(2)\nMerge(0)\n";
     case SFG_CSB:
       return "TileSplit(0," + std::to_string(dst.block_r) + ")\nTileSplit(2," + std::to_string(dst.block_c) +
              ")\nSwap(1,2)\nSort\nFill(1)\nFill(0)\nMerge(0)\nMerge(1)\n";
@@ -102,7 +105,7 @@ std::string plan_for(const sfg_format& dst) {
 
 bool same_format(const sfg_format& a, const sfg_format& b) {
   if (a.kind != b.kind) return false;
-  if (a.kind == SFG_BCSR || a.kind == SFG_BELL || a.kind == SFG_CSB)
+  if (a.kind == SFG_BCSR || a.kind == SFG_BELL || a.kind == SFG_CSB || a.kind == SFG_BDIA)
     return a.block_r == b.block_r && a.block_c == b.block_c;
   if (a.kind == SFG_HYB) return a.threshold == b.threshold;
   return true;
@@ -134,15 +137,24 @@ std::string plan_from(const sfg_format& src, const sfg_format& dst) {
   return simplify_plan(plan_from_raw(src, dst));
 }
 
-// The reference planner folds a swap of the two coordinates into the skew
-// next to it and drops a swap followed by its inverse.
+// The reference planner composes the affine maps it emits: a skew and its
+// inverse cancel, a swap commutes with a skew by conjugating it, two swaps
+// cancel, and a skew followed by a swap is written as a scale and two skews.
+// Applied in this order until nothing changes.
 std::string simplify_plan(std::string p) {
   const std::pair<const char*, const char*> rules[] = {
-      {"Swap(0,1)\nSkew(0,1,-1)\nSwap(0,1)\n", "Skew(1,0,-1)\n"},
+      {"Skew(0,1,1)\nSkew(0,1,-1)\n", ""},
+      {"Skew(1,0,1)\nSwap(0,1)\nSkew(0,1,-1)\n", "Swap(0,1)\n"},
+      {"Swap(0,1)\nSkew(0,1,-1)\n", "Skew(1,0,-1)\nSwap(0,1)\n"},
       {"Swap(0,1)\nSwap(0,1)\n", ""},
+      {"Skew(0,1,1)\nSwap(0,1)\n", "Scale(1,-1)\nSkew(1,0,-1)\nSkew(0,1,1)\n"},
   };
-  for (const auto& [from, to] : rules)
-    for (size_t at; (at = p.find(from)) != std::string::npos;) p.replace(at, std::strlen(from), to);
+  for (bool changed = true; changed;) {
+    changed = false;
+    for (const auto& [from, to] : rules)
+      for (size_t at; (at = p.find(from)) != std::string::npos; changed = true)
+        p.replace(at, std::strlen(from), to);
+  }
   return p;
 }
 
@@ -173,6 +185,9 @@ std::string plan_from_raw(const sfg_format& src, const sfg_format& dst) {
     case SFG_CSB:
       return "Split(1)\nSplit(0)\nTrim(1)\nTrim(0)\nSwap(1,2)\nTileUnion(0," + std::to_string(src.block_r) +
              ")\nTileUnion(1," + std::to_string(src.block_c) + ")\n" + (sorts ? "" : "Sort\n") + tail;
+    case SFG_BDIA:
+      return "Devectorize(2)\nSplit(0)\nTrim(2)\nTrim(0)\nSwap(1,2)\nTileUnion(0," + std::to_string(src.block_r) +
+             ")\nSkew(0,1,1)\n" + std::string(sorts ? "" : "Sort\n") + tail;
   }
   sfg::raise(SFG_ERR_UNSUPPORTED_SOURCE, "unsupported source format");
 }
@@ -192,6 +207,7 @@ std::string explain_for(const sfg_format& f) {
     case SFG_BELL:
       return "L0: idx | L1: size | L2: idx | L3: size, dense_vector | L4: size, dense_vector | val";
     case SFG_DIA: return "L0: idx | L1: size, dense_vector | val";
+    case SFG_BDIA: return "L0: size | L1: ptr, idx | L2: size, dense_vector | val";
     case SFG_CSB: return "L0: size | L1: size | L2: ptr, idx | L3: idx | val";
     case SFG_LIL: return "L0: size | L1: ptr, idx | val | pack(0,1)";
   }
@@ -199,8 +215,8 @@ std::string explain_for(const sfg_format& f) {
 }
 
 void validate_format(const sfg_format& f) {
-  require(f.kind >= SFG_COO && f.kind <= SFG_CSB, SFG_ERR_PARSE, "unknown format kind");
-  if (f.kind == SFG_BCSR || f.kind == SFG_BELL || f.kind == SFG_CSB)
+  require(f.kind >= SFG_COO && f.kind <= SFG_BDIA, SFG_ERR_PARSE, "unknown format kind");
+  if (f.kind == SFG_BCSR || f.kind == SFG_BELL || f.kind == SFG_CSB || f.kind == SFG_BDIA)
     require(f.block_r > 0 && f.block_c > 0, SFG_ERR_INVALID_OPERATION,
             "TileSplit factor must be positive");
   require(f.value_dtype == SFG_F32 || (f.value_dtype == SFG_BF16 && f.kind == SFG_BCSR),
@@ -338,6 +354,10 @@ int sfg_format_resolve(const char* text, sfg_format* out) {
       f.block_c = static_cast<int32_t>(nargs > 1 ? args[1] : f.block_r);
     } else if (name == "DIA") {
       f.kind = SFG_DIA;
+    } else if (name == "BDIA") {
+      // formats.hpp:76-79: one argument, the block size (default 3)
+      f.kind = SFG_BDIA;
+      f.block_r = f.block_c = static_cast<int32_t>(nargs > 0 ? args[0] : 3);
     } else if (name == "BELL") {
       // formats.hpp:79-85: one argument, the block size (default 2)
       f.kind = SFG_BELL;
@@ -446,6 +466,7 @@ int sfg_convert(sfg_context* ctx, const sfg_tensor* src, const sfg_format* dst, 
       case SFG_BELL: *out = sfg::coo_to_bell(ctx, src, dst->block_r); break;
       case SFG_DIA: *out = sfg::coo_to_dia(ctx, src); break;
       case SFG_CSB: *out = sfg::coo_to_csb(ctx, src, dst->block_r, dst->block_c); break;
+      case SFG_BDIA: *out = sfg::coo_to_bdia(ctx, src, dst->block_r); break;
     }
   });
 }
@@ -547,6 +568,13 @@ int sfg_tensor_view_get(sfg_context* ctx, const sfg_tensor* t, sfg_tensor_view* 
         v.level[0] = level(I, -(t->m - 1), t->n - 1, t->k, t->k, t->slots, 0, nullptr);
         v.level[1] = level(S | D, 0, t->m - 1, t->k * t->m, 0, nullptr, 0, nullptr);
         v.nvals = t->k * t->m;
+        break;
+      case SFG_BDIA:  // block rows, their diagonals, a dense vector over the block's rows
+        v.nlevels = 3;
+        v.level[0] = level(S, 0, t->nbr - 1, t->nbr, 0, nullptr, 0, nullptr);
+        v.level[1] = level(P | I, -(t->m - 1), t->n - 1, t->k, t->k, t->idx, t->nbr + 1, t->ptr);
+        v.level[2] = level(S | D, 0, t->rb - 1, t->k * t->rb, 0, nullptr, 0, nullptr);
+        v.nvals = t->k * t->rb;
         break;
       case SFG_CSB:  // dense block grid, entries per block (row, column in block)
         v.nlevels = 4;

@@ -97,6 +97,7 @@ std::vector<uint8_t> expected_kinds(int kind) {
     case SFG_BCSR: return {kUSize, kUIdx | kUPtr, kUSize | kUDense, kUSize | kUDense};
     case SFG_BELL: return {kUIdx, kUSize, kUIdx, kUSize | kUDense, kUSize | kUDense};
     case SFG_DIA: return {kUIdx, kUSize | kUDense};
+    case SFG_BDIA: return {kUSize, kUIdx | kUPtr, kUSize | kUDense};
     case SFG_CSB: return {kUSize, kUSize, kUIdx | kUPtr, kUIdx};
     case SFG_DOK: return {kUIdx, kUIdx};           // COO + pack(0,1)
     case SFG_LIL: return {kUSize, kUIdx | kUPtr};  // CSR + pack(0,1)
@@ -317,7 +318,7 @@ sfg_tensor* read_container(sfg_context* ctx, const char* path_c, const sfg_forma
   } else {
     fmt.value_dtype = SFG_F32;
     int found = -1;
-    for (int k : {SFG_COO, SFG_CSR, SFG_DCSR, SFG_ELL, SFG_BCSR, SFG_BELL, SFG_DIA, SFG_CSB}) {
+    for (int k : {SFG_COO, SFG_CSR, SFG_DCSR, SFG_ELL, SFG_BCSR, SFG_BELL, SFG_DIA, SFG_CSB, SFG_BDIA}) {
       const auto w = expected_kinds(k);
       bool same = w.size() == lv.size();
       for (size_t l = 0; same && l < lv.size(); ++l) same = lv[l].kind == w[l];
@@ -335,6 +336,8 @@ sfg_tensor* read_container(sfg_context* ctx, const char* path_c, const sfg_forma
       fmt.block_c = lv[3].hi - lv[3].lo + 1;
     } else if (found == SFG_BELL) {
       fmt.block_r = fmt.block_c = lv[3].hi - lv[3].lo + 1;
+    } else if (found == SFG_BDIA) {
+      fmt.block_r = fmt.block_c = lv[2].hi - lv[2].lo + 1;
     } else if (found == SFG_CSB) {
       fmt.block_r = lv[2].hi - lv[2].lo + 1;  // the in-block extents (one-tile edges shrink them)
       fmt.block_c = lv[3].hi - lv[3].lo + 1;
@@ -401,6 +404,15 @@ sfg_tensor* read_container(sfg_context* ctx, const char* path_c, const sfg_forma
         t->k = lv[0].nidx;
         t->nnz = t->k * m;
         t->slots = load_i(lv[0].idx_off, lv[0].nidx);
+        break;
+      case SFG_BDIA:
+        t->br = t->bc = fmt.block_r;
+        t->nbr = lv[0].hi - lv[0].lo + 1;
+        t->rb = lv[2].hi - lv[2].lo + 1;
+        t->k = lv[1].nidx;
+        t->nnz = t->k * t->rb;
+        t->ptr = load_i(lv[1].ptr_off, lv[1].nptr);
+        t->idx = load_i(lv[1].idx_off, lv[1].nidx);
         break;
       case SFG_CSB:
         t->br = fmt.block_r;

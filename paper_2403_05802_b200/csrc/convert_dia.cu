@@ -265,3 +265,179 @@ sfg_tensor* dia_to_coo(sfg_context* ctx, const sfg_tensor* t) {
 }
 
 }  // namespace sfg
+
+// --------------------------------------------------------------- BDIA(b)
+// BDIA(b): map (d0/b, d1-d0, d0%b); merge(0), trim(1,1) (formats.hpp:74-77);
+// plan Skew(0,1,-1) TileSplit(0,b) Swap(1,2) Sort Fill(2) Fill(0)
+// Vectorize(2) Merge(0). Arrays: L0 dense over the block rows, L1 ptr[nbr+1]
+// + idx = the diagonals d = col - row present in each block row (ascending;
+// bounds [-(m-1), n-1]), L2 a dense vector over the rows of the block
+// (extent min(b, m)): values[nodes * rb], row r_in of node (block row,
+// d) = A[b*br + r_in][b*br + r_in + d] or 0. Device: the canonical radix
+// sort orders the entries by (block row, diagonal, row in block) — each
+// entry keyed (block row, (d + m - 1) * b + r_in) — then per block row a warp
+// counts the distinct diagonals (a ballot of changes), a scan gives ptr, and
+// a second warp pass writes idx and scatters the values into the
+// zero-filled panel.
+namespace sfg {
+namespace {
+
+constexpr int kBdiaBlock = 256;
+
+__global__ void k_bdia_keys(const int32_t* __restrict__ row, const int32_t* __restrict__ col, int64_t nnz,
+                            int32_t b, int64_t off, int32_t* __restrict__ key, int32_t* __restrict__ sub) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = ld_stream(row + e), c = ld_stream(col + e);
+    key[e] = r / b;
+    sub[e] = (int32_t)(((int64_t)c - r + off) * b + r % b);
+  }
+}
+
+// kWrite = false: distinct diagonals per block row into cnt[br];
+// kWrite = true: idx[node] = d and the values at node * rb + r_in.
+template <bool kWrite>
+__global__ void __launch_bounds__(kBdiaBlock) k_bdia_nodes(const int32_t* __restrict__ bptr,
+                                                           const int32_t* __restrict__ sub,
+                                                           const float* __restrict__ val, int64_t nbr, int32_t b,
+                                                           int32_t rb, int64_t off, int32_t* __restrict__ cnt,
+                                                           const int32_t* __restrict__ nptr,
+                                                           int32_t* __restrict__ idx, float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t br = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; br < nbr; br += warps) {
+    const int32_t s = __ldg(bptr + br), e = __ldg(bptr + br + 1);
+    int32_t node = kWrite ? __ldg(nptr + br) - 1 : 0;  // the node of the previous entry
+    int32_t prev = -1, heads = 0;
+    for (int32_t k0 = s; k0 < e; k0 += 32) {
+      const int32_t k = k0 + lane;
+      const int32_t q = k < e ? __ldg(sub + k) : -1;
+      const int32_t d = q >= 0 ? q / b : -1;
+      int32_t dp = __shfl_up_sync(kFull, d, 1);
+      if (lane == 0) dp = prev;
+      const bool head = k < e && d != dp;
+      const unsigned hm = __ballot_sync(kFull, head);
+      if (kWrite && k < e) {
+        const int32_t my = node + __popc(hm & ((2u << lane) - 1u));
+        if (head) idx[my] = (int32_t)(d - off);
+        out[(int64_t)my * rb + (q - d * b)] = __ldg(val + k);
+      }
+      node += __popc(hm);
+      heads += __popc(hm);
+      prev = __shfl_sync(kFull, d, 31);
+    }
+    if (!kWrite && lane == 0) cnt[br] = heads;
+  }
+}
+
+}  // namespace
+
+sfg_tensor* coo_to_bdia(sfg_context* ctx, const sfg_tensor* s, int64_t b) {
+  const int64_t m = s->m, n = s->n, off = m - 1;
+  if ((m + n) * b >= INT32_MAX) raise(SFG_ERR_INVALID_OPERATION, "BDIA: (m + n) * b exceeds the int32 range");
+  const int64_t nbr = ceil_div(m, b), rb = std::min(b, m);
+  auto* key = dalloc_n<int32_t>(ctx, s->nnz);
+  auto* sub = dalloc_n<int32_t>(ctx, s->nnz);
+  if (s->nnz)
+    SFG_LAUNCH(k_bdia_keys, stream_grid(ctx, s->nnz, kBdiaBlock, 4, 8), kBdiaBlock, 0, ctx->stream, s->row, s->idx,
+               s->nnz, (int32_t)b, off, key, sub);
+  sfg_tensor* sorted = nullptr;
+  try {
+    sorted = sort_coo(ctx, nbr, (m + n - 1) * b, s->nnz, key, sub, static_cast<const float*>(s->val), false);
+  } catch (...) {
+    dfree(ctx, key);
+    dfree(ctx, sub);
+    throw;
+  }
+  dfree(ctx, key);
+  dfree(ctx, sub);
+  sfg_tensor* grid = coo_to_csr(ctx, sorted);  // entries per block row
+  free_tensor_arrays(sorted);
+  delete sorted;
+  auto* cnt = dalloc_n<int32_t>(ctx, nbr);
+  sfg_tensor* t = new_tensor(ctx, SFG_BDIA, m, n);
+  t->br = t->bc = b;
+  t->rb = rb;
+  t->nbr = nbr;
+  t->ptr = dalloc_n<int32_t>(ctx, nbr + 1);
+  const int g = stream_grid(ctx, nbr * 32, kBdiaBlock, 1, 8);
+  if (nbr) {
+    SFG_LAUNCH(k_bdia_nodes<false>, g, kBdiaBlock, 0, ctx->stream, grid->ptr, grid->idx,
+               static_cast<const float*>(grid->val), nbr, (int32_t)b, (int32_t)rb, off, cnt, nullptr, nullptr,
+               nullptr);
+    scan_counts(ctx, cnt, nbr, t->ptr);
+  } else {
+    SFG_CUDA(cudaMemsetAsync(t->ptr, 0, 4, ctx->stream));
+  }
+  int32_t nodes = 0;
+  read_back(ctx, t->ptr + nbr, 4, &nodes);
+  t->k = nodes;
+  t->nnz = (int64_t)nodes * rb;  // values
+  t->idx = dalloc_n<int32_t>(ctx, nodes);
+  t->val = dalloc_n<float>(ctx, t->nnz);
+  if (t->nnz) SFG_CUDA(cudaMemsetAsync(t->val, 0, t->nnz * 4, ctx->stream));
+  if (nbr && nodes)
+    SFG_LAUNCH(k_bdia_nodes<true>, g, kBdiaBlock, 0, ctx->stream, grid->ptr, grid->idx,
+               static_cast<const float*>(grid->val), nbr, (int32_t)b, (int32_t)rb, off, nullptr, t->ptr, t->idx,
+               static_cast<float*>(t->val));
+  dfree(ctx, cnt);
+  free_tensor_arrays(grid);
+  delete grid;
+  return t;
+}
+
+namespace {
+// BDIA cells holding a nonzero value, as unordered (row, col, val): a warp
+// per block row
+__global__ void k_bdia_nonzeros(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                                const float* __restrict__ val, int64_t nbr, int32_t b, int32_t rb, int64_t m,
+                                int32_t* __restrict__ orow, int32_t* __restrict__ ocol, float* __restrict__ oval,
+                                unsigned long long* __restrict__ count) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t br = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; br < nbr; br += warps) {
+    const int64_t c0 = (int64_t)__ldg(ptr + br) * rb, c1 = (int64_t)__ldg(ptr + br + 1) * rb;
+    for (int64_t q0 = c0; q0 < c1; q0 += 32) {
+      const int64_t q = q0 + lane;
+      const float v = q < c1 ? __ldg(val + q) : 0.f;
+      const bool nz = v != 0.f;
+      const unsigned msk = __ballot_sync(kFull, nz);
+      unsigned long long base = 0;
+      if (lane == 0 && msk) base = atomicAdd(count, (unsigned long long)__popc(msk));
+      base = __shfl_sync(kFull, base, 0);
+      if (nz) {
+        const int64_t node = q / rb, r = br * b + (q - node * rb);
+        const unsigned long long at = base + __popc(msk & ((1u << lane) - 1u));
+        orow[at] = (int32_t)r;
+        ocol[at] = (int32_t)(r + __ldg(idx + node));
+        oval[at] = v;
+      }
+    }
+  }
+}
+}  // namespace
+
+sfg_tensor* bdia_to_coo(sfg_context* ctx, const sfg_tensor* t) {
+  const int64_t cells = t->k * t->rb;
+  auto* r = dalloc_n<int32_t>(ctx, cells);
+  auto* c = dalloc_n<int32_t>(ctx, cells);
+  auto* v = dalloc_n<float>(ctx, cells);
+  auto* count = static_cast<unsigned long long*>(scratch(ctx, 64));
+  SFG_CUDA(cudaMemsetAsync(count, 0, 8, ctx->stream));
+  if (cells)
+    SFG_LAUNCH(k_bdia_nonzeros, stream_grid(ctx, t->nbr * 32, kBdiaBlock, 1, 8), kBdiaBlock, 0, ctx->stream, t->ptr,
+               t->idx, static_cast<const float*>(t->val), t->nbr, (int32_t)t->br, (int32_t)t->rb, t->m, r, c, v,
+               count);
+  unsigned long long nz = 0;
+  read_back(ctx, count, 8, &nz);
+  sfg_tensor* out = nullptr;
+  try {
+    out = sort_coo(ctx, t->m, t->n, (int64_t)nz, r, c, v, false);
+  } catch (...) {
+    for (void* q : {(void*)r, (void*)c, (void*)v}) dfree(ctx, q);
+    throw;
+  }
+  for (void* q : {(void*)r, (void*)c, (void*)v}) dfree(ctx, q);
+  return out;
+}
+
+}  // namespace sfg

@@ -408,9 +408,10 @@ sfg_tensor* convert_from_compressed(sfg_context* ctx, const sfg_tensor* s, const
   // column level comes back with the interval [-(m-1), n+m-2] (and a CSB
   // source with its tile-grid extents and extra dangling nodes); the device
   // tensors keep [0, n-1] columns, so these sources are not converted.
-  if (s->kind == SFG_DIA || s->kind == SFG_CSB)
+  if (s->kind == SFG_DIA || s->kind == SFG_BDIA || s->kind == SFG_CSB)
     raise(SFG_ERR_UNSUPPORTED_SOURCE,
-          "conversion from DIA / CSB: the reference's skewed / tile-grid level bounds are not held on the device");
+          "conversion from DIA / BDIA / CSB: the reference's skewed / tile-grid level bounds are not held on the "
+          "device");
   const bool same = s->kind == dst.kind &&
                     (s->kind != SFG_BCSR || (s->br == dst.block_r && s->bc == dst.block_c && s->dtype == dst.value_dtype)) &&
                     (s->kind != SFG_CSB || (s->br == dst.block_r && s->bc == dst.block_c));

@@ -88,6 +88,7 @@ struct sfg_context {
 //         slot-major), val[K*nbr*rb*cb]; nnz = K*nbr cells
 //   DOK : val = records {row, col, val}[nnz];  LIL: ptr[m+1], val = {col, val}[nnz]
 //   DIA : slots[K] (diagonals col - row, ascending), val[K*m]; nnz = K*m
+//   BDIA: ptr[nbr+1], idx[K] (diagonals per block row), val[K*rb]; k = K, nnz = K*rb
 //   CSB : ptr[nbr*nbc+1] over the block grid, row[nnz] (row in block),
 //         idx[nnz] (column in block), val[nnz]
 struct sfg_tensor {
@@ -221,6 +222,10 @@ sfg_tensor* coo_to_dia(sfg_context* ctx, const sfg_tensor* s);
 sfg_tensor* coo_to_csb(sfg_context* ctx, const sfg_tensor* s, int64_t br, int64_t bc);
 sfg_tensor* dia_to_coo(sfg_context* ctx, const sfg_tensor* t);
 sfg_tensor* csb_to_coo(sfg_context* ctx, const sfg_tensor* t);
+sfg_tensor* coo_to_bdia(sfg_context* ctx, const sfg_tensor* s, int64_t b);
+sfg_tensor* bdia_to_coo(sfg_context* ctx, const sfg_tensor* t);  // nonzero cells
+// Exclusive scan of n int32 counts into ptr[0..n] (convert_bcsr.cu).
+void scan_counts(sfg_context* ctx, const int32_t* cnt, int64_t n, int32_t* ptr);
 // The nonzero entries of an ELL / BELL tensor as a canonical COO (convert_src.cu).
 sfg_tensor* ell_nonzeros_to_coo(sfg_context* ctx, const sfg_tensor* s);
 // Blocked ELL (convert_bell.cu): the BCSR blocks relaid slot by slot.

@@ -563,6 +563,30 @@ __global__ void __launch_bounds__(kBlock) k_spmm_dia(const int32_t* __restrict__
   }
 }
 
+// ------------------------------------------------------------------ BDIA
+template <typename TB, int V>
+__global__ void __launch_bounds__(kBlock) k_spmm_bdia(const int32_t* __restrict__ ptr,
+                                                       const int32_t* __restrict__ diags,
+                                                       const float* __restrict__ val, int64_t m, int64_t n,
+                                                       int32_t b, int32_t rb, Dense d) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int chunks = (d.nd + 32 * V - 1) / (32 * V);
+  const bool vec_ok = (d.nd % (32 * V) == 0) && (d.ldb % V == 0);
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < m * chunks; w += warps) {
+    const int64_t r = w / chunks, br = r / b, ri = r - br * b;
+    const int c0 = (int)(w - r * chunks) * 32 * V + lane * V;
+    float acc[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[i] = 0.f;
+    for (int32_t q = __ldg(ptr + br); q < __ldg(ptr + br + 1); ++q) {
+      const int64_t c = r + __ldg(diags + q);
+      if (c >= 0 && c < n) fma_row<TB, V>(d, (int)c, __ldg(val + (int64_t)q * rb + ri), c0, vec_ok, acc);
+    }
+    store_row<V>(d, r, c0, false, acc);
+  }
+}
+
 // ------------------------------------------------------------------- COO
 // A warp owns 32*kCooIters consecutive row-sorted entries; it accumulates a
 // row while the row stays the same and stores it when the row changes. A row
@@ -1015,6 +1039,11 @@ void launch_fmt(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
     case SFG_ELL:
       SFG_LAUNCH((k_spmm_ell<TB, V>), grid_for(a->m * chunks), kBlock, 0, ctx->stream, a->idx, fv,
                  (int32_t)a->m, (int32_t)a->k, d);
+      break;
+    case SFG_BDIA:
+      if (a->m)
+        SFG_LAUNCH((k_spmm_bdia<TB, V>), grid_for(a->m * chunks), kBlock, 0, ctx->stream, a->ptr, a->idx, fv, a->m,
+                   a->n, (int32_t)a->br, (int32_t)a->rb, d);
       break;
     case SFG_DIA:
       if (a->m)

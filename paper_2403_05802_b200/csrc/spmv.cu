@@ -148,6 +148,23 @@ __global__ void __launch_bounds__(kBlock) k_spmv_dia(const int32_t* __restrict__
   }
 }
 
+// BDIA: thread per row, over the diagonals of its block row.
+__global__ void __launch_bounds__(kBlock) k_spmv_bdia(const int32_t* __restrict__ ptr,
+                                                       const int32_t* __restrict__ diags,
+                                                       const float* __restrict__ val, int64_t m, int64_t n,
+                                                       int32_t b, int32_t rb, const float* __restrict__ x,
+                                                       float* __restrict__ y, int acc) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t br = r / b, ri = r - br * b;
+    float sum = 0.f;
+    for (int32_t q = __ldg(ptr + br); q < __ldg(ptr + br + 1); ++q) {
+      const int64_t c = r + __ldg(diags + q);
+      if (c >= 0 && c < n) sum = fmaf(__ldg(val + (int64_t)q * rb + ri), ldx(x, (int)c), sum);
+    }
+    y[r] = acc ? y[r] + sum : sum;
+  }
+}
+
 // ---------------------------------------------------------------- COO
 // Row-sorted entries, load-balanced by entries (a heavy row spans many
 // warps). No shared memory. A warp walks its chunk
@@ -479,6 +496,11 @@ void spmv(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, bool 
       if (a->m)
         SFG_LAUNCH(k_spmv_dia, stream_grid(ctx, a->m, kBlock, 1, 8), kBlock, 0, ctx->stream, a->slots,
                    static_cast<const float*>(a->val), a->m, a->n, a->k, x, y, acc);
+      break;
+    case SFG_BDIA:
+      if (a->m)
+        SFG_LAUNCH(k_spmv_bdia, stream_grid(ctx, a->m, kBlock, 1, 8), kBlock, 0, ctx->stream, a->ptr, a->idx,
+                   static_cast<const float*>(a->val), a->m, a->n, (int32_t)a->br, (int32_t)a->rb, x, y, acc);
       break;
     case SFG_CSB: {
       // the blocks' entries back in row order (csb_to_coo), then COO

@@ -1,4 +1,4 @@
-"""DIA (formats.hpp:46) and CSB(r,c) (formats.hpp:54-57), §8f rank 2: the
+"""DIA (formats.hpp:46), BDIA(b) (76-79) and CSB(r,c) (54-57), §8f rank 2: the
 device conversions from canonical COO are bit-exact with the unmodified
 reference's materialized tensors (DIA: ascending diagonals, zero-filled
 diagonal-major panel; CSB: the dense block grid's ptr and the in-block
@@ -52,10 +52,12 @@ def _ref_fmt(fmt):
     if fmt.startswith("CSB"):
         a = [int(t) for t in fmt[4:-1].split(",")]
         return "CSB", a[0], a[1] if len(a) > 1 else a[0]
+    if fmt.startswith("BDIA"):
+        return "BDIA", int(fmt[5:-1]), 0
     return fmt, 0, 0
 
 
-@pytest.mark.parametrize("fmt", ["DIA", "CSB(2)", "CSB(2,3)", "CSB(16)"])
+@pytest.mark.parametrize("fmt", ["DIA", "CSB(2)", "CSB(2,3)", "CSB(16)", "BDIA(2)", "BDIA(3)", "BDIA(16)"])
 @pytest.mark.parametrize("case", list(CASES))
 def test_matches_reference(ctx, ref, fmt, case):
     d, p, _ = _pair(ctx, ref, case)
@@ -65,7 +67,7 @@ def test_matches_reference(ctx, ref, fmt, case):
     assert got.explain() == want.explain() == sfg.storage_explain(fmt)
 
 
-@pytest.mark.parametrize("fmt", ["DIA", "CSB(4)", "CSB(3,2)"])
+@pytest.mark.parametrize("fmt", ["DIA", "CSB(4)", "CSB(3,2)", "BDIA(4)", "BDIA(3)"])
 def test_compute(ctx, ref, fmt):
     d, p, (m, n, r, c, v) = _pair(ctx, ref, "banded")
     a = ctx.convert(d, fmt)
@@ -81,7 +83,7 @@ def test_compute(ctx, ref, fmt):
         assert np.all(np.abs(got - want) <= TOL * bound + 1e-30), (fmt, nd)
 
 
-@pytest.mark.parametrize("src", ["DIA", "CSB(2)", "CSB(2,3)"])
+@pytest.mark.parametrize("src", ["DIA", "CSB(2)", "CSB(2,3)", "BDIA(2)"])
 def test_not_a_conversion_source(ctx, ref, src):
     """The reference expands a DIA source through its skewed map (its column
     level comes back as [-(m-1), n+m-2]) and a CSB source with tile-grid
@@ -95,7 +97,7 @@ def test_not_a_conversion_source(ctx, ref, src):
     assert (want.levels[1].lo, want.levels[1].hi) != (0, 28) or want.levels[0].node_count != len(want.values)
 
 
-@pytest.mark.parametrize("fmt", ["DIA", "CSB(2,3)"])
+@pytest.mark.parametrize("fmt", ["DIA", "CSB(2,3)", "BDIA(3)"])
 def test_container_matches_reference(ctx, ref, tmp_path, fmt):
     d, p, (m, n, r, c, v) = _pair(ctx, ref, "random")
     dev = ctx.convert(d, fmt)

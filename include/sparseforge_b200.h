@@ -75,13 +75,16 @@ enum sfg_format_kind {
   SFG_DIA = 10, /* map (d0,d1)->(d1-d0, d0); merge(0), trim(0,0) formats.hpp:46 */
   SFG_CSB = 11, /* (d0/r, d1/c, d0%r, d1%c); merge(0,1), trim(2,3) formats.hpp:54-57 */
   SFG_BDIA = 12, /* (d0/b, d1-d0, d0%b); merge(0), trim(1,1)     formats.hpp:76-79 */
+  SFG_C2SR = 13, /* (d0%k, d0/k, d1); merge(0,1), trim(2,2), partition(0)
+                    formats.hpp:62-66 — rows interleaved k ways, entry ranges
+                    per residue class as partitions                          */
 };
 
 enum sfg_dtype { SFG_F32 = 0, SFG_BF16 = 1 };
 
 typedef struct sfg_format {
   int32_t kind;        /* sfg_format_kind */
-  int32_t block_r;     /* BCSR / CSB block rows (r); BELL / BDIA block size (b) */
+  int32_t block_r;     /* BCSR / CSB block rows (r); BELL / BDIA block size (b); C2SR k */
   int32_t block_c;     /* BCSR / CSB block columns (c); BELL: b         */
   int32_t value_dtype; /* sfg_dtype of stored values (BF16: BCSR only) */
   int64_t threshold;   /* HYB: DecomposeRule::min_sum (decompose.hpp:17-20) */
@@ -120,6 +123,11 @@ typedef struct sfg_tensor_view {
   int32_t layout;
   int32_t aos_start, aos_end;
   int32_t record_words; /* 1 for SoA */
+  /* Partition(level) (operators.hpp:431-445, storage.hpp:220-231): value
+   * ranges [begin, end) per coordinate of the partition level, as
+   * npartitions (begin, end) pairs in HOST memory owned by the tensor. */
+  int64_t npartitions;
+  const int64_t* partitions;
 } sfg_tensor_view;
 
 /* --------------------------------------------------------------- context */

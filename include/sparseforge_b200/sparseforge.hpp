@@ -173,6 +173,7 @@ inline std::string name_of(const sfg_format& f) {
     case SFG_BELL: return "BELL(" + std::to_string(f.block_r) + ")";
     case SFG_DIA: return "DIA";
     case SFG_BDIA: return "BDIA(" + std::to_string(f.block_r) + ")";
+    case SFG_C2SR: return "C2SR(" + std::to_string(f.block_r) + ")";
     case SFG_CSB: return "CSB(" + std::to_string(f.block_r) + "," + std::to_string(f.block_c) + ")";
   }
   return "?";
@@ -257,6 +258,7 @@ inline StorageScheme infer_storage(const FormatEncoding& enc) {
       break;
     case SFG_DIA: s.levels = {L(0, 0, 1, 0), L(1, 0, 0, 1)}; break;
     case SFG_BDIA: s.levels = {L(1, 0, 0, 0), L(0, 1, 1, 0), L(1, 0, 0, 1)}; break;
+    case SFG_C2SR: s.levels = {L(1, 0, 0, 0), L(1, 0, 0, 0), L(0, 1, 1, 0)}; break;
     case SFG_CSB: s.levels = {L(1, 0, 0, 0), L(1, 0, 0, 0), L(0, 1, 1, 0), L(0, 0, 1, 0)}; break;
     default: break;  // HYB: two parts, see DecomposeResult
   }
@@ -283,7 +285,8 @@ struct WorkingTensor {
       case SFG_BCSR: return 4;
       case SFG_BELL: return 5;
       case SFG_CSB: return 4;
-      case SFG_BDIA: return 3;
+      case SFG_BDIA:
+      case SFG_C2SR: return 3;
       default: return 2;
     }
   }
@@ -310,6 +313,7 @@ struct MaterializedTensor {
   std::vector<MaterializedLevel> levels;
   std::vector<double> values;
   ValueLayout layout;
+  std::vector<std::pair<size_t, size_t>> partitions;  // Partition value ranges (storage.hpp:90)
   FormatEncoding enc;
   std::shared_ptr<b200::TensorHandle> dev;  // the device arrays behind the host copy
 };
@@ -514,6 +518,8 @@ inline MaterializedTensor materialize(const WorkingTensor& t, const StorageSchem
   m.values = b200::download_values(v);
   if (v.layout == 1)
     m.layout = {ValueLayoutKind::AoS, static_cast<size_t>(v.aos_start), static_cast<size_t>(v.aos_end)};
+  for (int64_t q = 0; q < v.npartitions; ++q)
+    m.partitions.push_back({static_cast<size_t>(v.partitions[2 * q]), static_cast<size_t>(v.partitions[2 * q + 1])});
   return m;
 }
 

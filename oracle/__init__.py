@@ -87,10 +87,12 @@ class Materialized:
     levels: list = field(default_factory=list)
     values: np.ndarray = None
     layout: tuple = None  # AoS span (aos_start, aos_end) of a packed format; None: SoA
+    partitions: list = field(default_factory=list)  # Partition: (begin, end) value ranges
 
     def explain(self) -> str:
         text = " | ".join(f"L{i}: {lv.explain()}" for i, lv in enumerate(self.levels)) + " | val"
-        return text + (f" | pack({self.layout[0]},{self.layout[1]})" if self.layout else "")
+        text += f" | pack({self.layout[0]},{self.layout[1]})" if self.layout else ""
+        return text + (" | partition(0)" if self.fmt.startswith("C2SR") else "")  # the one partitioned format
 
 
 class _Coo:
@@ -142,6 +144,11 @@ class _Mat:
             f("mat_layout")(self.h, _p64(lay))
             if lay[0] == 1:
                 out.layout = (int(lay[1]), int(lay[2]))
+            np_ = int(f("mat_npartitions")(self.h))
+            if np_:
+                pr = np.zeros(2 * np_, np.int64)
+                f("mat_partitions")(self.h, _p64(pr))
+                out.partitions = [(int(pr[2 * i]), int(pr[2 * i + 1])) for i in range(np_)]
         return out
 
 
@@ -156,6 +163,8 @@ class _Base:
         getattr(self.lib, self.prefix + "last_error").restype = C.c_char_p
         getattr(self.lib, self.prefix + "coo_nnz").restype = C.c_int64
         getattr(self.lib, self.prefix + "mat_nvals").restype = C.c_int64
+        if hasattr(self.lib, self.prefix + "mat_npartitions"):
+            getattr(self.lib, self.prefix + "mat_npartitions").restype = C.c_int64
         for n in ("coo_free", "mat_free"):
             getattr(self.lib, self.prefix + n).restype = None
 
@@ -196,7 +205,7 @@ class _Base:
 def _fmt_text(fmt, r=None, c=None):
     if fmt == "BCSR":
         return f"BCSR({r},{c})"
-    if fmt in ("BELL", "BDIA"):  # formats.hpp:76-85: one block-size argument
+    if fmt in ("BELL", "BDIA", "C2SR"):  # formats.hpp:62-85: one argument
         return f"{fmt}({r})"
     if fmt == "CSB":  # formats.hpp:54-57: CSB(r, c)
         return f"CSB({r},{c})"

@@ -196,6 +196,17 @@ int sfr_mat_layout(void* h, int64_t out[3]) {
   return 0;
 }
 
+// Partition value ranges (storage.hpp:220-231), as (begin, end) pairs.
+int64_t sfr_mat_npartitions(void* h) { return static_cast<int64_t>(static_cast<RefMat*>(h)->m.partitions.size()); }
+int sfr_mat_partitions(void* h, int64_t* out) {
+  const auto& p = static_cast<RefMat*>(h)->m.partitions;
+  for (size_t i = 0; i < p.size(); ++i) {
+    out[2 * i] = static_cast<int64_t>(p[i].first);
+    out[2 * i + 1] = static_cast<int64_t>(p[i].second);
+  }
+  return 0;
+}
+
 void sfr_mat_free(void* h) { delete static_cast<RefMat*>(h); }
 
 int sfr_spmv(void* h, const double* x, double* y, int threads) {

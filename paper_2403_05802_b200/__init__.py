@@ -22,7 +22,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_lib", "libsfg.so")
 
-KINDS = {"COO": 0, "CSR": 1, "CSC": 2, "DCSR": 3, "ELL": 4, "BCSR": 5, "HYB": 6, "DOK": 7, "LIL": 8, "BELL": 9, "DIA": 10, "CSB": 11, "BDIA": 12}
+KINDS = {"COO": 0, "CSR": 1, "CSC": 2, "DCSR": 3, "ELL": 4, "BCSR": 5, "HYB": 6, "DOK": 7, "LIL": 8, "BELL": 9, "DIA": 10, "CSB": 11, "BDIA": 12, "C2SR": 13}
 KIND_NAMES = {v: k for k, v in KINDS.items()}
 F32, BF16 = 0, 1
 FLAG_SORTED, FLAG_SUM_DUPLICATES, FLAG_HOST = 1, 2, 4
@@ -62,7 +62,8 @@ class TensorView(C.Structure):
                 ("cols", C.c_int64), ("nlevels", C.c_int32), ("level", LevelView * 5),
                 ("nvals", C.c_int64), ("values", C.c_void_p), ("parts", C.c_void_p * 2),
                 ("layout", C.c_int32), ("aos_start", C.c_int32), ("aos_end", C.c_int32),
-                ("record_words", C.c_int32)]
+                ("record_words", C.c_int32), ("npartitions", C.c_int64),
+                ("partitions", C.POINTER(C.c_int64))]
 
 
 @dataclass
@@ -88,10 +89,12 @@ class Materialized:
     levels: list = field(default_factory=list)
     values: np.ndarray = None
     layout: tuple = None  # AoS span (aos_start, aos_end) of a packed format; None: SoA
+    partitions: list = field(default_factory=list)  # Partition: (begin, end) value ranges
 
     def explain(self) -> str:
         text = " | ".join(f"L{i}: {lv.explain()}" for i, lv in enumerate(self.levels)) + " | val"
-        return text + (f" | pack({self.layout[0]},{self.layout[1]})" if self.layout else "")
+        text += f" | pack({self.layout[0]},{self.layout[1]})" if self.layout else ""
+        return text + (" | partition(0)" if self.fmt.startswith("C2SR") else "")  # the one partitioned format
 
 
 _lib = None
@@ -335,6 +338,8 @@ class Tensor:
             out.values = raw.view(np.float32).astype(np.float64)
         else:
             out.values = self._dl(v.values, np.float32, v.nvals, rw).astype(np.float64)
+        if v.npartitions:
+            out.partitions = [(int(v.partitions[2 * i]), int(v.partitions[2 * i + 1])) for i in range(v.npartitions)]
         return out
 
     def coo_arrays(self):

@@ -87,6 +87,9 @@ std::string plan_for(const sfg_format& dst) {
              "remainder: Merge(0)\n";
     case SFG_DOK: return "Pack(0,1)\n";
     case SFG_DIA: return "Skew(0,1,-1)\nSwap(0,1)\nSort\nFill(1)\nVectorize(1)\nMerge(0)\n";
+    case SFG_C2SR:
+      return "TileSplit(0," + std::to_string(dst.block_r) +
+             ")\nSwap(0,1)\nSort\nFill(1)\nFill(0)\nMerge(0)\nMerge(1)\nPartition(0)\n";
     case SFG_BDIA:
       return "Skew(0,1,-1)\nTileSplit(0," + std::to_string(dst.block_r) +
              ")\nSwap(1,2)\nSort\nFill(2)\nFill(0)\nVectorize(2)\nMerge(0)\n";
@@ -123,7 +126,7 @@ std::string plan_from(const sfg_format& src, const sfg_format& dst) {
   if (src.kind == SFG_COO) return plan_for(dst);
   if (src.kind == SFG_ELL || src.kind == SFG_BELL)
     sfg::raise(SFG_ERR_UNSUPPORTED_SOURCE, "conversion from a format with indirect levels");
-  if (src.kind == SFG_DOK || src.kind == SFG_LIL)
+  if (src.kind == SFG_DOK || src.kind == SFG_LIL || src.kind == SFG_C2SR)
     sfg::raise(SFG_ERR_UNSUPPORTED_SOURCE, "conversion from a format with a value layout");
   if (src.kind == SFG_HYB || dst.kind == SFG_HYB)
     sfg::raise(SFG_ERR_UNSUPPORTED_SOURCE, "the hybrid pair has no single-tensor plan from a compressed source");
@@ -208,6 +211,7 @@ std::string explain_for(const sfg_format& f) {
       return "L0: idx | L1: size | L2: idx | L3: size, dense_vector | L4: size, dense_vector | val";
     case SFG_DIA: return "L0: idx | L1: size, dense_vector | val";
     case SFG_BDIA: return "L0: size | L1: ptr, idx | L2: size, dense_vector | val";
+    case SFG_C2SR: return "L0: size | L1: size | L2: ptr, idx | val | partition(0)";
     case SFG_CSB: return "L0: size | L1: size | L2: ptr, idx | L3: idx | val";
     case SFG_LIL: return "L0: size | L1: ptr, idx | val | pack(0,1)";
   }
@@ -215,8 +219,8 @@ std::string explain_for(const sfg_format& f) {
 }
 
 void validate_format(const sfg_format& f) {
-  require(f.kind >= SFG_COO && f.kind <= SFG_BDIA, SFG_ERR_PARSE, "unknown format kind");
-  if (f.kind == SFG_BCSR || f.kind == SFG_BELL || f.kind == SFG_CSB || f.kind == SFG_BDIA)
+  require(f.kind >= SFG_COO && f.kind <= SFG_C2SR, SFG_ERR_PARSE, "unknown format kind");
+  if (f.kind == SFG_BCSR || f.kind == SFG_BELL || f.kind == SFG_CSB || f.kind == SFG_BDIA || f.kind == SFG_C2SR)
     require(f.block_r > 0 && f.block_c > 0, SFG_ERR_INVALID_OPERATION,
             "TileSplit factor must be positive");
   require(f.value_dtype == SFG_F32 || (f.value_dtype == SFG_BF16 && f.kind == SFG_BCSR),
@@ -354,6 +358,10 @@ int sfg_format_resolve(const char* text, sfg_format* out) {
       f.block_c = static_cast<int32_t>(nargs > 1 ? args[1] : f.block_r);
     } else if (name == "DIA") {
       f.kind = SFG_DIA;
+    } else if (name == "C2SR") {
+      // formats.hpp:62-66: k defaults to 2
+      f.kind = SFG_C2SR;
+      f.block_r = f.block_c = static_cast<int32_t>(nargs > 0 ? args[0] : 2);
     } else if (name == "BDIA") {
       // formats.hpp:76-79: one argument, the block size (default 3)
       f.kind = SFG_BDIA;
@@ -467,6 +475,7 @@ int sfg_convert(sfg_context* ctx, const sfg_tensor* src, const sfg_format* dst, 
       case SFG_DIA: *out = sfg::coo_to_dia(ctx, src); break;
       case SFG_CSB: *out = sfg::coo_to_csb(ctx, src, dst->block_r, dst->block_c); break;
       case SFG_BDIA: *out = sfg::coo_to_bdia(ctx, src, dst->block_r); break;
+      case SFG_C2SR: *out = sfg::coo_to_c2sr(ctx, src, dst->block_r); break;
     }
   });
 }
@@ -568,6 +577,15 @@ int sfg_tensor_view_get(sfg_context* ctx, const sfg_tensor* t, sfg_tensor_view* 
         v.level[0] = level(I, -(t->m - 1), t->n - 1, t->k, t->k, t->slots, 0, nullptr);
         v.level[1] = level(S | D, 0, t->m - 1, t->k * t->m, 0, nullptr, 0, nullptr);
         v.nvals = t->k * t->m;
+        break;
+      case SFG_C2SR:  // residue classes, rows per class, CSR over the interleaved rows
+        v.nlevels = 3;
+        v.level[0] = level(S, 0, t->nbr - 1, t->nbr, 0, nullptr, 0, nullptr);
+        v.level[1] = level(S, 0, t->k - 1, t->nbr * t->k, 0, nullptr, 0, nullptr);
+        v.level[2] = level(P | I, 0, t->n - 1, t->nnz, t->nnz, t->idx, t->nbr * t->k + 1, t->ptr);
+        v.nvals = t->nnz;
+        v.npartitions = (int64_t)t->partitions.size() / 2;
+        v.partitions = t->partitions.data();
         break;
       case SFG_BDIA:  // block rows, their diagonals, a dense vector over the block's rows
         v.nlevels = 3;

@@ -98,6 +98,7 @@ std::vector<uint8_t> expected_kinds(int kind) {
     case SFG_BELL: return {kUIdx, kUSize, kUIdx, kUSize | kUDense, kUSize | kUDense};
     case SFG_DIA: return {kUIdx, kUSize | kUDense};
     case SFG_BDIA: return {kUSize, kUIdx | kUPtr, kUSize | kUDense};
+    case SFG_C2SR: return {kUSize, kUSize, kUIdx | kUPtr};
     case SFG_CSB: return {kUSize, kUSize, kUIdx | kUPtr, kUIdx};
     case SFG_DOK: return {kUIdx, kUIdx};           // COO + pack(0,1)
     case SFG_LIL: return {kUSize, kUIdx | kUPtr};  // CSR + pack(0,1)
@@ -203,7 +204,8 @@ void write_container(sfg_context* ctx, const sfg_tensor* t, const char* path_c) 
   } else {
     put(head, 0, 1);  // SoA
   }
-  put(head, 0, 4);  // no partitions
+  put(head, (uint64_t)v.npartitions, 4);  // partitions: (begin, end) value ranges
+  for (int64_t q = 0; q < 2 * v.npartitions; ++q) put(head, (uint64_t)v.partitions[q], 8);
   emit(head);
   const int64_t size = off;
 
@@ -308,7 +310,8 @@ sfg_tensor* read_container(sfg_context* ctx, const char* path_c, const sfg_forma
       raise(SFG_ERR_UNSUPPORTED_SOURCE, path + ": only the Pack(0,1) value layout (DOK / LIL) is held on the device");
   }
   const uint64_t nparts = get(4);
-  if (nparts) raise(SFG_ERR_UNSUPPORTED_SOURCE, path + ": partitioned containers are not held on the device");
+  std::vector<int64_t> parts;
+  for (uint64_t q = 0; q < 2 * nparts; ++q) parts.push_back((int64_t)get(8));
 
   // the requested format must match the stored structure; without one, the
   // level kinds name it (CSR and CSC look alike: CSR is taken)
@@ -318,7 +321,7 @@ sfg_tensor* read_container(sfg_context* ctx, const char* path_c, const sfg_forma
   } else {
     fmt.value_dtype = SFG_F32;
     int found = -1;
-    for (int k : {SFG_COO, SFG_CSR, SFG_DCSR, SFG_ELL, SFG_BCSR, SFG_BELL, SFG_DIA, SFG_CSB, SFG_BDIA}) {
+    for (int k : {SFG_COO, SFG_CSR, SFG_DCSR, SFG_ELL, SFG_BCSR, SFG_BELL, SFG_DIA, SFG_CSB, SFG_BDIA, SFG_C2SR}) {
       const auto w = expected_kinds(k);
       bool same = w.size() == lv.size();
       for (size_t l = 0; same && l < lv.size(); ++l) same = lv[l].kind == w[l];
@@ -336,6 +339,8 @@ sfg_tensor* read_container(sfg_context* ctx, const char* path_c, const sfg_forma
       fmt.block_c = lv[3].hi - lv[3].lo + 1;
     } else if (found == SFG_BELL) {
       fmt.block_r = fmt.block_c = lv[3].hi - lv[3].lo + 1;
+    } else if (found == SFG_C2SR) {
+      fmt.block_r = fmt.block_c = lv[0].hi - lv[0].lo + 1;  // k (min(k, m) when k > m)
     } else if (found == SFG_BDIA) {
       fmt.block_r = fmt.block_c = lv[2].hi - lv[2].lo + 1;
     } else if (found == SFG_CSB) {
@@ -347,6 +352,8 @@ sfg_tensor* read_container(sfg_context* ctx, const char* path_c, const sfg_forma
   bool ok = rank == 2 && lv.size() == want.size();
   for (size_t l = 0; ok && l < lv.size(); ++l) ok = lv[l].kind == want[l];
   if (ok) ok = (tag == 1) == (fmt.kind == SFG_DOK || fmt.kind == SFG_LIL);
+  if (ok && nparts && fmt.kind != SFG_C2SR)
+    raise(SFG_ERR_UNSUPPORTED_SOURCE, path + ": partitions are held on the device for C2SR only");
   if (!ok) raise(SFG_ERR_INVALID_OPERATION, path + ": the container does not hold this format");
   const int64_t m = ext[0], n = ext[1];
   if (m >= INT32_MAX || n >= INT32_MAX || nvals >= INT32_MAX)
@@ -404,6 +411,15 @@ sfg_tensor* read_container(sfg_context* ctx, const char* path_c, const sfg_forma
         t->k = lv[0].nidx;
         t->nnz = t->k * m;
         t->slots = load_i(lv[0].idx_off, lv[0].nidx);
+        break;
+      case SFG_C2SR:
+        t->br = t->bc = fmt.block_r;
+        t->nbr = lv[0].hi - lv[0].lo + 1;
+        t->k = lv[1].hi - lv[1].lo + 1;
+        t->nnz = lv[2].nidx;
+        t->ptr = load_i(lv[2].ptr_off, lv[2].nptr);
+        t->idx = load_i(lv[2].idx_off, lv[2].nidx);
+        t->partitions = parts;
         break;
       case SFG_BDIA:
         t->br = t->bc = fmt.block_r;

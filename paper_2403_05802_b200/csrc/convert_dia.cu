@@ -441,3 +441,110 @@ sfg_tensor* bdia_to_coo(sfg_context* ctx, const sfg_tensor* t) {
 }
 
 }  // namespace sfg
+
+// --------------------------------------------------------------- C2SR(k)
+// C2SR(k): map (d0%k, d0/k, d1); merge(0,1), trim(2,2), partition(0)
+// (formats.hpp:62-66); plan TileSplit(0,k) Swap(0,1) Sort Fill(1) Fill(0)
+// Merge(0) Merge(1) Partition(0). The rows interleaved k ways: row r is
+// stored at r' = (r % k) * R + r / k (R = ceil(m/k) rows per residue
+// class), a CSR over the kk * R interleaved rows (kk = min(k, m)), and one
+// partition per residue class holding entries (storage.hpp:220-231):
+// [ptr[j R], ptr[(j+1) R]) when non-empty. Device: the rows rekeyed, the
+// canonical radix sort, the CSR row-pointer pass; the kk + 1 class bounds
+// are gathered and read back for the (host) partition list.
+namespace sfg {
+namespace {
+
+__global__ void k_c2sr_rows(const int32_t* __restrict__ row, int64_t nnz, int32_t k, int32_t rr,
+                            int32_t* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = ld_stream(row + e);
+    out[e] = (r % k) * rr + r / k;
+  }
+}
+
+__global__ void k_c2sr_bounds(const int32_t* __restrict__ ptr, int32_t kk, int32_t rr, int64_t* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j <= kk) out[j] = __ldg(ptr + (int64_t)j * rr);
+}
+
+// original coordinates of a C2SR tensor's entries (a warp per stored row)
+__global__ void k_c2sr_coords(const int32_t* __restrict__ ptr, int64_t rows, int32_t k, int32_t rr,
+                              int32_t* __restrict__ orow) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < rows; q += warps) {
+    const int32_t r = (int32_t)((q % rr) * k + q / rr);
+    for (int32_t e = __ldg(ptr + q) + lane; e < __ldg(ptr + q + 1); e += 32) orow[e] = r;
+  }
+}
+
+}  // namespace
+
+void c2sr_partitions(sfg_context* ctx, sfg_tensor* t) {
+  const int32_t kk = (int32_t)t->nbr, rr = (int32_t)t->k;
+  auto* b = static_cast<int64_t*>(scratch(ctx, (size_t)(kk + 1) * 8));
+  SFG_LAUNCH(k_c2sr_bounds, (int)ceil_div(kk + 1, 256), 256, 0, ctx->stream, t->ptr, kk, rr, b);
+  std::vector<int64_t> h(kk + 1);
+  SFG_CUDA(cudaMemcpyAsync(h.data(), b, (kk + 1) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  SFG_CUDA(cudaStreamSynchronize(ctx->stream));
+  t->partitions.clear();
+  for (int32_t j = 0; j < kk; ++j)
+    if (h[j + 1] > h[j]) {
+      t->partitions.push_back(h[j]);
+      t->partitions.push_back(h[j + 1]);
+    }
+}
+
+sfg_tensor* coo_to_c2sr(sfg_context* ctx, const sfg_tensor* s, int64_t k) {
+  const int64_t m = s->m, kk = std::min(k, m), rr = ceil_div(m, k);
+  if (kk * rr >= INT32_MAX) raise(SFG_ERR_INVALID_OPERATION, "C2SR: the interleaved rows exceed the int32 range");
+  auto* key = dalloc_n<int32_t>(ctx, s->nnz);
+  if (s->nnz)
+    SFG_LAUNCH(k_c2sr_rows, stream_grid(ctx, s->nnz, kBdiaBlock, 4, 8), kBdiaBlock, 0, ctx->stream, s->row, s->nnz,
+               (int32_t)k, (int32_t)rr, key);
+  sfg_tensor* sorted = nullptr;
+  try {
+    sorted = sort_coo(ctx, kk * rr, s->n, s->nnz, key, s->idx, static_cast<const float*>(s->val), false);
+  } catch (...) {
+    dfree(ctx, key);
+    throw;
+  }
+  dfree(ctx, key);
+  sfg_tensor* csr = coo_to_csr(ctx, sorted);
+  free_tensor_arrays(sorted);
+  delete sorted;
+  sfg_tensor* t = new_tensor(ctx, SFG_C2SR, s->m, s->n);
+  t->br = t->bc = k;
+  t->nbr = kk;
+  t->k = rr;
+  t->nnz = csr->nnz;
+  t->has_zeros = s->has_zeros;
+  t->ptr = csr->ptr;
+  t->idx = csr->idx;
+  t->val = csr->val;
+  csr->ptr = csr->idx = nullptr;
+  csr->val = nullptr;
+  free_tensor_arrays(csr);
+  delete csr;
+  c2sr_partitions(ctx, t);
+  return t;
+}
+
+sfg_tensor* c2sr_to_coo(sfg_context* ctx, const sfg_tensor* t) {
+  auto* r = dalloc_n<int32_t>(ctx, t->nnz);
+  if (t->nnz)
+    SFG_LAUNCH(k_c2sr_coords, stream_grid(ctx, t->nbr * t->k, kBdiaBlock / 32, 1, 16), kBdiaBlock, 0, ctx->stream,
+               t->ptr, t->nbr * t->k, (int32_t)t->br, (int32_t)t->k, r);
+  sfg_tensor* out = nullptr;
+  try {
+    out = sort_coo(ctx, t->m, t->n, t->nnz, r, t->idx, static_cast<const float*>(t->val), false);
+  } catch (...) {
+    dfree(ctx, r);
+    throw;
+  }
+  dfree(ctx, r);
+  return out;
+}
+
+}  // namespace sfg

@@ -402,7 +402,7 @@ sfg_tensor* convert_from_compressed(sfg_context* ctx, const sfg_tensor* s, const
     raise(SFG_ERR_UNSUPPORTED_SOURCE, "conversion from a format with indirect levels");
   if (s->kind == SFG_HYB) raise(SFG_ERR_UNSUPPORTED_SOURCE, "conversion from the hybrid pair");
   // planner.hpp:98-99: sources with a value layout are rejected
-  if (s->kind == SFG_DOK || s->kind == SFG_LIL)
+  if (s->kind == SFG_DOK || s->kind == SFG_LIL || s->kind == SFG_C2SR)
     raise(SFG_ERR_UNSUPPORTED_SOURCE, "conversion from a format with a value layout");
   // The reference expands a DIA source through its skewed map, so the
   // column level comes back with the interval [-(m-1), n+m-2] (and a CSB
@@ -452,6 +452,8 @@ sfg_tensor* convert_from_compressed(sfg_context* ctx, const sfg_tensor* s, const
       case SFG_LIL: out = coo_to_lil(ctx, coo); break;
       case SFG_DIA: out = coo_to_dia(ctx, coo); break;
       case SFG_CSB: out = coo_to_csb(ctx, coo, dst.block_r, dst.block_c); break;
+      case SFG_BDIA: out = coo_to_bdia(ctx, coo, dst.block_r); break;
+      case SFG_C2SR: out = coo_to_c2sr(ctx, coo, dst.block_r); break;
       default: raise(SFG_ERR_INVALID_OPERATION, "unknown target");
     }
   } catch (...) {

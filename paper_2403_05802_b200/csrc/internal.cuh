@@ -89,6 +89,8 @@ struct sfg_context {
 //   DOK : val = records {row, col, val}[nnz];  LIL: ptr[m+1], val = {col, val}[nnz]
 //   DIA : slots[K] (diagonals col - row, ascending), val[K*m]; nnz = K*m
 //   BDIA: ptr[nbr+1], idx[K] (diagonals per block row), val[K*rb]; k = K, nnz = K*rb
+//   C2SR: ptr[kk*R+1] over the interleaved rows (row' = (r % k) * R + r / k,
+//         R = ceil(m/k), kk = min(k, m); nbr = kk, k = R), idx, val; partitions
 //   CSB : ptr[nbr*nbc+1] over the block grid, row[nnz] (row in block),
 //         idx[nnz] (column in block), val[nnz]
 struct sfg_tensor {
@@ -114,6 +116,7 @@ struct sfg_tensor {
   int32_t* slots = nullptr;
   void* val = nullptr;
   sfg_tensor* part[2] = {nullptr, nullptr};
+  std::vector<int64_t> partitions;  // C2SR: (begin, end) value ranges, host
 };
 
 namespace sfg {
@@ -224,6 +227,10 @@ sfg_tensor* dia_to_coo(sfg_context* ctx, const sfg_tensor* t);
 sfg_tensor* csb_to_coo(sfg_context* ctx, const sfg_tensor* t);
 sfg_tensor* coo_to_bdia(sfg_context* ctx, const sfg_tensor* s, int64_t b);
 sfg_tensor* bdia_to_coo(sfg_context* ctx, const sfg_tensor* t);  // nonzero cells
+sfg_tensor* coo_to_c2sr(sfg_context* ctx, const sfg_tensor* s, int64_t k);
+sfg_tensor* c2sr_to_coo(sfg_context* ctx, const sfg_tensor* t);
+// C2SR partitions from its row pointers (R rows per residue class).
+void c2sr_partitions(sfg_context* ctx, sfg_tensor* t);
 // Exclusive scan of n int32 counts into ptr[0..n] (convert_bcsr.cu).
 void scan_counts(sfg_context* ctx, const int32_t* cnt, int64_t n, int32_t* ptr);
 // The nonzero entries of an ELL / BELL tensor as a canonical COO (convert_src.cu).

@@ -1312,8 +1312,8 @@ void spmm(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dtype, int
     return;
   }
   if (a->kind == SFG_BCSR && spmm_bcsr_tc(ctx, a, b, b_dtype, nd, ldb, c, ldc, accumulate)) return;
-  if (a->kind == SFG_CSB) {  // the blocks' entries back in row order (csb_to_coo), then COO
-    sfg_tensor* coo = csb_to_coo(ctx, a);
+  if (a->kind == SFG_CSB || a->kind == SFG_C2SR) {  // the entries back in row order, then COO
+    sfg_tensor* coo = a->kind == SFG_CSB ? csb_to_coo(ctx, a) : c2sr_to_coo(ctx, a);
     try {
       spmm(ctx, coo, b, b_dtype, nd, ldb, c, ldc, accumulate);
     } catch (...) {

@@ -502,9 +502,10 @@ void spmv(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, bool 
         SFG_LAUNCH(k_spmv_bdia, stream_grid(ctx, a->m, kBlock, 1, 8), kBlock, 0, ctx->stream, a->ptr, a->idx,
                    static_cast<const float*>(a->val), a->m, a->n, (int32_t)a->br, (int32_t)a->rb, x, y, acc);
       break;
-    case SFG_CSB: {
-      // the blocks' entries back in row order (csb_to_coo), then COO
-      sfg_tensor* coo = csb_to_coo(ctx, a);
+    case SFG_CSB:
+    case SFG_C2SR: {
+      // the entries back in row order (csb_to_coo / c2sr_to_coo), then COO
+      sfg_tensor* coo = a->kind == SFG_CSB ? csb_to_coo(ctx, a) : c2sr_to_coo(ctx, a);
       spmv_coo(ctx, coo, x, y, acc);
       free_tensor_arrays(coo);
       delete coo;

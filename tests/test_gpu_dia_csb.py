@@ -1,4 +1,5 @@
-"""DIA (formats.hpp:46), BDIA(b) (76-79) and CSB(r,c) (54-57), §8f rank 2: the
+"""DIA (formats.hpp:46), BDIA(b) (76-79), CSB(r,c) (54-57) and C2SR(k)
+(62-66, Partition(0): per-class value ranges), §8f rank 2: the
 device conversions from canonical COO are bit-exact with the unmodified
 reference's materialized tensors (DIA: ascending diagonals, zero-filled
 diagonal-major panel; CSB: the dense block grid's ptr and the in-block
@@ -54,20 +55,24 @@ def _ref_fmt(fmt):
         return "CSB", a[0], a[1] if len(a) > 1 else a[0]
     if fmt.startswith("BDIA"):
         return "BDIA", int(fmt[5:-1]), 0
+    if fmt.startswith("C2SR"):
+        return "C2SR", int(fmt[5:-1]), 0
     return fmt, 0, 0
 
 
-@pytest.mark.parametrize("fmt", ["DIA", "CSB(2)", "CSB(2,3)", "CSB(16)", "BDIA(2)", "BDIA(3)", "BDIA(16)"])
+@pytest.mark.parametrize("fmt", ["DIA", "CSB(2)", "CSB(2,3)", "CSB(16)", "BDIA(2)", "BDIA(3)", "BDIA(16)",
+                                 "C2SR(2)", "C2SR(3)", "C2SR(64)"])
 @pytest.mark.parametrize("case", list(CASES))
 def test_matches_reference(ctx, ref, fmt, case):
     d, p, _ = _pair(ctx, ref, case)
     got = ctx.convert(d, fmt).download()
     want = ref.convert(p, *_ref_fmt(fmt)).download()
     assert_same_materialized(got, want, (fmt, case))
+    assert got.partitions == want.partitions, (fmt, case)
     assert got.explain() == want.explain() == sfg.storage_explain(fmt)
 
 
-@pytest.mark.parametrize("fmt", ["DIA", "CSB(4)", "CSB(3,2)", "BDIA(4)", "BDIA(3)"])
+@pytest.mark.parametrize("fmt", ["DIA", "CSB(4)", "CSB(3,2)", "BDIA(4)", "BDIA(3)", "C2SR(2)", "C2SR(5)"])
 def test_compute(ctx, ref, fmt):
     d, p, (m, n, r, c, v) = _pair(ctx, ref, "banded")
     a = ctx.convert(d, fmt)
@@ -97,7 +102,7 @@ def test_not_a_conversion_source(ctx, ref, src):
     assert (want.levels[1].lo, want.levels[1].hi) != (0, 28) or want.levels[0].node_count != len(want.values)
 
 
-@pytest.mark.parametrize("fmt", ["DIA", "CSB(2,3)", "BDIA(3)"])
+@pytest.mark.parametrize("fmt", ["DIA", "CSB(2,3)", "BDIA(3)", "C2SR(3)"])
 def test_container_matches_reference(ctx, ref, tmp_path, fmt):
     d, p, (m, n, r, c, v) = _pair(ctx, ref, "random")
     dev = ctx.convert(d, fmt)
@@ -106,8 +111,10 @@ def test_container_matches_reference(ctx, ref, tmp_path, fmt):
     f, a, b = _ref_fmt(fmt)
     ref.write_container(p, f, str(theirs), a, b)
     assert filecmp.cmp(ours, theirs, shallow=False), fmt
-    back = ctx.read_container(str(theirs), fmt)
-    assert_same_materialized(back.download(), dev.download(), ("read", fmt))
+    for f in (fmt, None):  # named, or inferred from the stored levels
+        back = ctx.read_container(str(theirs), f)
+        assert_same_materialized(back.download(), dev.download(), ("read", fmt, f))
+        assert back.download().partitions == dev.download().partitions
 
 
 def test_dia_capacity_error(ctx):

@@ -78,6 +78,9 @@ enum sfg_format_kind {
   SFG_C2SR = 13, /* (d0%k, d0/k, d1); merge(0,1), trim(2,2), partition(0)
                     formats.hpp:62-66 — rows interleaved k ways, entry ranges
                     per residue class as partitions                          */
+  SFG_HBELL = 14, /* hybrid BELL/COO (the paper's GPU format, PAPER.md fig.
+                     BELL-COO): decompose by b x b blocks with >= threshold
+                     nonzeros -> BELL(b), the rest -> COO                    */
 };
 
 enum sfg_dtype { SFG_F32 = 0, SFG_BF16 = 1 };
@@ -87,7 +90,7 @@ typedef struct sfg_format {
   int32_t block_r;     /* BCSR / CSB block rows (r); BELL / BDIA block size (b); C2SR k */
   int32_t block_c;     /* BCSR / CSB block columns (c); BELL: b         */
   int32_t value_dtype; /* sfg_dtype of stored values (BF16: BCSR only) */
-  int64_t threshold;   /* HYB: DecomposeRule::min_sum (decompose.hpp:17-20) */
+  int64_t threshold;   /* HYB / HBELL: DecomposeRule::min_sum (decompose.hpp:17-20) */
 } sfg_format;
 
 /* LevelStorage flags (storage.hpp:17-22). */
@@ -179,6 +182,13 @@ int sfg_convert(sfg_context* ctx, const sfg_tensor* src, const sfg_format* dst, 
  * int32[rows]) receives the row totals. */
 int sfg_decompose_rows(sfg_context* ctx, const sfg_tensor* coo, int64_t min_sum,
                        sfg_tensor** selected, sfg_tensor** remainder, int32_t* totals);
+
+/* decompose (decompose.hpp:30-63) with the block count rule
+ * "sum(value) groupBy (d0, d1) -> (d0/r, d1/c) with value ne 0 -> 1 | otherwise -> 0":
+ * the entries of r x c blocks holding >= min_sum nonzeros go to *selected,
+ * the rest to *remainder (the split behind the hybrid BELL/COO format). */
+int sfg_decompose_blocks(sfg_context* ctx, const sfg_tensor* coo, int64_t r, int64_t c, int64_t min_sum,
+                         sfg_tensor** selected, sfg_tensor** remainder);
 
 /* Materialized arrays (device pointers, valid while the tensor lives). */
 int sfg_tensor_view_get(sfg_context* ctx, const sfg_tensor* t, sfg_tensor_view* out);

@@ -306,6 +306,12 @@ class Ref(_Base):
         self.lib.sfr_coo_shape(h, C.byref(m), C.byref(n))
         return _Coo(self.lib, h, self.prefix, (m.value, n.value))
 
+    def decompose_blocks(self, coo, r, c, min_sum):
+        s, rem = C.c_void_p(), C.c_void_p()
+        self._check(self.lib.sfr_decompose_blocks(coo.h, C.c_int64(r), C.c_int64(c), C.c_int64(min_sum),
+                                                  C.byref(s), C.byref(rem)))
+        return _Coo(self.lib, s, self.prefix, coo.shape), _Coo(self.lib, rem, self.prefix, coo.shape)
+
     def plan(self, src, dst):
         buf = C.create_string_buffer(4096)
         self._check(self.lib.sfr_plan(src.encode(), dst.encode(), buf, C.c_int64(4096)))

@@ -271,6 +271,21 @@ int sfr_decompose_rows(void* h, int64_t min_sum, void** sel, void** rem, int64_t
   });
 }
 
+// decompose by r x c blocks with the block count rule (decompose.hpp:30-63)
+int sfr_decompose_blocks(void* h, int64_t r, int64_t c, int64_t min_sum, void** sel, void** rem) {
+  *sel = *rem = nullptr;
+  return guard([&] {
+    const WorkingTensor& t = static_cast<RefCoo*>(h)->t;
+    DecomposeRule rule;
+    rule.query = parse_query("sum(value) groupBy (d0, d1) -> (d0/" + std::to_string(r) + ", d1/" + std::to_string(c) +
+                             ") with value ne 0 -> 1 | otherwise -> 0");
+    rule.min_sum = min_sum;
+    DecomposeResult d = decompose(t, rule);
+    *sel = new RefCoo{std::move(d.selected)};
+    *rem = new RefCoo{std::move(d.remainder)};
+  });
+}
+
 int sfr_plan(const char* src, const char* dst, char* buf, int64_t len) {
   return guard([&] {
     std::string out;

@@ -22,7 +22,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_lib", "libsfg.so")
 
-KINDS = {"COO": 0, "CSR": 1, "CSC": 2, "DCSR": 3, "ELL": 4, "BCSR": 5, "HYB": 6, "DOK": 7, "LIL": 8, "BELL": 9, "DIA": 10, "CSB": 11, "BDIA": 12, "C2SR": 13}
+KINDS = {"COO": 0, "CSR": 1, "CSC": 2, "DCSR": 3, "ELL": 4, "BCSR": 5, "HYB": 6, "DOK": 7, "LIL": 8, "BELL": 9, "DIA": 10, "CSB": 11, "BDIA": 12, "C2SR": 13, "HBELL": 14}
 KIND_NAMES = {v: k for k, v in KINDS.items()}
 F32, BF16 = 0, 1
 FLAG_SORTED, FLAG_SUM_DUPLICATES, FLAG_HOST = 1, 2, 4
@@ -124,6 +124,7 @@ def load():
         "sfg_from_coo": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, u32, pp]),
         "sfg_convert": (C.c_int, [vp, vp, C.POINTER(Format), pp]),
         "sfg_decompose_rows": (C.c_int, [vp, vp, i64, pp, pp, vp]),
+        "sfg_decompose_blocks": (C.c_int, [vp, vp, i64, i64, i64, pp, pp]),
         "sfg_tensor_view_get": (C.c_int, [vp, vp, C.POINTER(TensorView)]),
         "sfg_tensor_free": (C.c_int, [vp]),
         "sfg_spmv": (C.c_int, [vp, vp, vp, vp, u32]),
@@ -432,6 +433,12 @@ class Context:
         _check(self.lib.sfg_decompose_rows(self.h, coo.h, min_sum, C.byref(s), C.byref(r),
                                            C.c_void_p(totals_ptr)))
         return Tensor(self, s), Tensor(self, r)
+
+    def decompose_blocks(self, coo: Tensor, r: int, c: int, min_sum: int):
+        """decompose by r x c blocks (the block count rule): (selected, remainder)."""
+        s, rem = C.c_void_p(), C.c_void_p()
+        _check(self.lib.sfg_decompose_blocks(self.h, coo.h, r, c, min_sum, C.byref(s), C.byref(rem)))
+        return Tensor(self, s), Tensor(self, rem)
 
     def row_partition(self, coo: Tensor, parts: int):
         b = (C.c_int64 * (parts + 1))()

@@ -87,6 +87,14 @@ std::string plan_for(const sfg_format& dst) {
              "remainder: Merge(0)\n";
     case SFG_DOK: return "Pack(0,1)\n";
     case SFG_DIA: return "Skew(0,1,-1)\nSwap(0,1)\nSort\nFill(1)\nVectorize(1)\nMerge(0)\n";
+    case SFG_HBELL: {
+      const std::string b = std::to_string(dst.block_r);
+      return "Decompose(sum(value) groupBy (d0, d1) -> (d0/" + b + ", d1/" + b +
+             ") with value ne 0 -> 1 | otherwise -> 0, " + std::to_string(dst.threshold) +
+             ")\nselected: TileSplit(0," + b + ")\nselected: TileSplit(2," + b +
+             ")\nselected: Swap(1,2)\nselected: Sum(0)\nselected: Enumerate(0)\nselected: Sort\nselected: "
+             "Fill(4)\nselected: Fill(3)\nselected: Fill(1)\nselected: Vectorize(3)\nselected: Merge(0)\n";
+    }
     case SFG_C2SR:
       return "TileSplit(0," + std::to_string(dst.block_r) +
              ")\nSwap(0,1)\nSort\nFill(1)\nFill(0)\nMerge(0)\nMerge(1)\nPartition(0)\n";
@@ -128,7 +136,7 @@ std::string plan_from(const sfg_format& src, const sfg_format& dst) {
     sfg::raise(SFG_ERR_UNSUPPORTED_SOURCE, "conversion from a format with indirect levels");
   if (src.kind == SFG_DOK || src.kind == SFG_LIL || src.kind == SFG_C2SR)
     sfg::raise(SFG_ERR_UNSUPPORTED_SOURCE, "conversion from a format with a value layout");
-  if (src.kind == SFG_HYB || dst.kind == SFG_HYB)
+  if (src.kind == SFG_HYB || dst.kind == SFG_HYB || src.kind == SFG_HBELL || dst.kind == SFG_HBELL)
     sfg::raise(SFG_ERR_UNSUPPORTED_SOURCE, "the hybrid pair has no single-tensor plan from a compressed source");
   if (same_format(src, dst)) return "";
   // BCSR(r,c) and CSB(r,c) share the index map: only the storage of the
@@ -212,6 +220,9 @@ std::string explain_for(const sfg_format& f) {
     case SFG_DIA: return "L0: idx | L1: size, dense_vector | val";
     case SFG_BDIA: return "L0: size | L1: ptr, idx | L2: size, dense_vector | val";
     case SFG_C2SR: return "L0: size | L1: size | L2: ptr, idx | val | partition(0)";
+    case SFG_HBELL:
+      return "BELL(L0: idx | L1: size | L2: idx | L3: size, dense_vector | L4: size, dense_vector | val) + "
+             "COO(L0: idx | L1: idx | val)";
     case SFG_CSB: return "L0: size | L1: size | L2: ptr, idx | L3: idx | val";
     case SFG_LIL: return "L0: size | L1: ptr, idx | val | pack(0,1)";
   }
@@ -219,8 +230,9 @@ std::string explain_for(const sfg_format& f) {
 }
 
 void validate_format(const sfg_format& f) {
-  require(f.kind >= SFG_COO && f.kind <= SFG_C2SR, SFG_ERR_PARSE, "unknown format kind");
-  if (f.kind == SFG_BCSR || f.kind == SFG_BELL || f.kind == SFG_CSB || f.kind == SFG_BDIA || f.kind == SFG_C2SR)
+  require(f.kind >= SFG_COO && f.kind <= SFG_HBELL, SFG_ERR_PARSE, "unknown format kind");
+  if (f.kind == SFG_BCSR || f.kind == SFG_BELL || f.kind == SFG_CSB || f.kind == SFG_BDIA || f.kind == SFG_C2SR ||
+      f.kind == SFG_HBELL)
     require(f.block_r > 0 && f.block_c > 0, SFG_ERR_INVALID_OPERATION,
             "TileSplit factor must be positive");
   require(f.value_dtype == SFG_F32 || (f.value_dtype == SFG_BF16 && f.kind == SFG_BCSR),
@@ -358,6 +370,11 @@ int sfg_format_resolve(const char* text, sfg_format* out) {
       f.block_c = static_cast<int32_t>(nargs > 1 ? args[1] : f.block_r);
     } else if (name == "DIA") {
       f.kind = SFG_DIA;
+    } else if (name == "HBELL") {
+      // hybrid BELL/COO: block size b (default 2), threshold (default b*b/2)
+      f.kind = SFG_HBELL;
+      f.block_r = f.block_c = static_cast<int32_t>(nargs > 0 ? args[0] : 2);
+      f.threshold = nargs > 1 ? args[1] : std::max<int64_t>(1, (int64_t)f.block_r * f.block_r / 2);
     } else if (name == "C2SR") {
       // formats.hpp:62-66: k defaults to 2
       f.kind = SFG_C2SR;
@@ -476,6 +493,7 @@ int sfg_convert(sfg_context* ctx, const sfg_tensor* src, const sfg_format* dst, 
       case SFG_CSB: *out = sfg::coo_to_csb(ctx, src, dst->block_r, dst->block_c); break;
       case SFG_BDIA: *out = sfg::coo_to_bdia(ctx, src, dst->block_r); break;
       case SFG_C2SR: *out = sfg::coo_to_c2sr(ctx, src, dst->block_r); break;
+      case SFG_HBELL: *out = sfg::coo_to_hbell(ctx, src, dst->block_r, dst->threshold); break;
     }
   });
 }
@@ -488,6 +506,17 @@ int sfg_decompose_rows(sfg_context* ctx, const sfg_tensor* coo, int64_t min_sum,
             "decompose expects coordinate-form input");
     *selected = *remainder = nullptr;
     sfg::decompose_rows(ctx, coo, min_sum, selected, remainder, totals);
+  });
+}
+
+int sfg_decompose_blocks(sfg_context* ctx, const sfg_tensor* coo, int64_t r, int64_t c, int64_t min_sum,
+                         sfg_tensor** selected, sfg_tensor** remainder) {
+  return guard(ctx, [&] {
+    require(ctx && coo && selected && remainder, SFG_ERR_INVALID_OPERATION, "null argument");
+    require(coo->kind == SFG_COO, SFG_ERR_INVALID_OPERATION, "decompose expects coordinate-form input");
+    require(r > 0 && c > 0, SFG_ERR_INVALID_OPERATION, "TileSplit factor must be positive");
+    *selected = *remainder = nullptr;
+    sfg::decompose_blocks(ctx, coo, r, c, min_sum, selected, remainder);
   });
 }
 
@@ -547,6 +576,7 @@ int sfg_tensor_view_get(sfg_context* ctx, const sfg_tensor* t, sfg_tensor_view* 
         v.nvals = t->nnz * t->rb * t->cb;
         break;
       case SFG_HYB:
+      case SFG_HBELL:
         v.nlevels = 0;
         v.parts[0] = t->part[0];
         v.parts[1] = t->part[1];

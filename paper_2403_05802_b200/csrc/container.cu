@@ -137,7 +137,7 @@ void write_all(const std::string& path, const char* data, int64_t size) {
 
 void write_container(sfg_context* ctx, const sfg_tensor* t, const char* path_c) {
   const std::string path(path_c);
-  if (t->kind == SFG_HYB) raise(SFG_ERR_INVALID_OPERATION, "the hybrid pair is two tensors: write each part");
+  if (t->kind == SFG_HYB || t->kind == SFG_HBELL) raise(SFG_ERR_INVALID_OPERATION, "the hybrid pair is two tensors: write each part");
   sfg_tensor_view v;
   if (int st = sfg_tensor_view_get(ctx, t, &v)) raise(st, "tensor view");
   // a packed (AoS) tensor is written like its SoA base plus the layout tag

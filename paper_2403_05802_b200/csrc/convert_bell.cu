@@ -119,3 +119,182 @@ sfg_tensor* coo_to_bell(sfg_context* ctx, const sfg_tensor* s, int64_t b) {
 }
 
 }  // namespace sfg
+
+// ------------------------------------------------- decompose by blocks
+// decompose (decompose.hpp:30-63) with the block count rule
+//   sum(value) groupBy (d0, d1) -> (d0/r, d1/c) with value ne 0 -> 1 | otherwise -> 0
+// — the paper's hybrid BELL/COO split: the entries of blocks holding at
+// least min_sum nonzeros are selected, the rest remain; both parts keep the
+// input order. Device: entries keyed (block row, block column·r·c + place in
+// block) carry their input index through the canonical radix sort, so each
+// block's entries are adjacent; a pass over the sorted keys finds the block
+// runs and their nonzero counts and flags every entry at its input index;
+// an order-preserving split by the flags (tile counts, scan, scatter) gives
+// the two parts.
+namespace sfg {
+namespace {
+
+__global__ void k_blockdec_keys(const int32_t* __restrict__ row, const int32_t* __restrict__ col, int64_t nnz,
+                                int32_t r, int32_t c, int32_t* __restrict__ key, int32_t* __restrict__ sub,
+                                float* __restrict__ idx_bits) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t rr = ld_stream(row + e), cc = ld_stream(col + e);
+    key[e] = rr / r;
+    sub[e] = (int32_t)((int64_t)(cc / c) * r * c + (rr % r) * c + cc % c);
+    idx_bits[e] = __int_as_float((int32_t)e);
+  }
+}
+
+// sorted keys: block runs (same row key, same sub / (r c)); a thread per
+// entry walks back / forward to its run's ends — runs hold <= r c entries
+__global__ void k_blockdec_flags(const int32_t* __restrict__ key, const int32_t* __restrict__ sub,
+                                 const float* __restrict__ idx_bits, const float* __restrict__ val_in, int64_t nnz,
+                                 int32_t rc, int64_t min_sum, uint8_t* __restrict__ flag) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t k = key[e], b = sub[e] / rc;
+    int64_t lo = e, hi = e;
+    while (lo > 0 && key[lo - 1] == k && sub[lo - 1] / rc == b) --lo;
+    while (hi + 1 < nnz && key[hi + 1] == k && sub[hi + 1] / rc == b) ++hi;
+    int64_t nz = 0;
+    for (int64_t q = lo; q <= hi; ++q) nz += val_in[__float_as_int(idx_bits[q])] != 0.f ? 1 : 0;
+    flag[__float_as_int(idx_bits[e])] = nz >= min_sum ? 1 : 0;
+  }
+}
+
+constexpr int kSplitItems = 8;
+constexpr int kSplitTileF = 256 * kSplitItems;
+
+sfg_tensor* coo_alloc(sfg_context* ctx, int64_t m, int64_t n, int64_t nnz) {
+  sfg_tensor* t = new_tensor(ctx, SFG_COO, m, n);
+  t->nnz = nnz;
+  t->row = dalloc_n<int32_t>(ctx, nnz);
+  t->idx = dalloc_n<int32_t>(ctx, nnz);
+  t->val = dalloc_n<float>(ctx, nnz);
+  return t;
+}
+
+__global__ void __launch_bounds__(256) k_flag_count(const uint8_t* __restrict__ flag, int64_t nnz,
+                                                    int32_t* __restrict__ cnt) {
+  __shared__ int32_t ws[8];
+  int32_t n = 0;
+  for (int i = 0; i < kSplitItems; ++i) {
+    const int64_t e = (int64_t)blockIdx.x * kSplitTileF + i * 256 + threadIdx.x;
+    n += e < nnz && flag[e];
+  }
+  n = warp_sum(n);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = n;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t t = 0;
+    for (int w = 0; w < 8; ++w) t += ws[w];
+    cnt[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_flag_split(const uint8_t* __restrict__ flag, const int32_t* __restrict__ base,
+                                                    const int32_t* __restrict__ row, const int32_t* __restrict__ col,
+                                                    const float* __restrict__ val, int64_t nnz,
+                                                    int32_t* __restrict__ ar, int32_t* __restrict__ ac,
+                                                    float* __restrict__ av, int32_t* __restrict__ br,
+                                                    int32_t* __restrict__ bc, float* __restrict__ bv) {
+  __shared__ int32_t ws[8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t t0 = (int64_t)blockIdx.x * kSplitTileF;
+  int32_t sel_before = __ldg(base + blockIdx.x);
+  for (int i = 0; i < kSplitItems; ++i) {
+    const int64_t e = t0 + i * 256 + threadIdx.x;
+    const bool in = e < nnz;
+    const bool f = in && flag[e];
+    const unsigned bal = __ballot_sync(kFull, f);
+    if (lane == 0) ws[w] = __popc(bal);
+    __syncthreads();
+    int32_t wpre = 0, tot = 0;
+    for (int q = 0; q < 8; ++q) {
+      if (q < w) wpre += ws[q];
+      tot += ws[q];
+    }
+    const int32_t s = sel_before + wpre + __popc(bal & ((1u << lane) - 1u));
+    if (in) {
+      if (f) {
+        ar[s] = row[e], ac[s] = col[e], av[s] = val[e];
+      } else {
+        const int64_t rpos = e - s;  // entries before e not selected
+        br[rpos] = row[e], bc[rpos] = col[e], bv[rpos] = val[e];
+      }
+    }
+    sel_before += tot;
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+void decompose_blocks(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_t c, int64_t min_sum,
+                      sfg_tensor** sel, sfg_tensor** rem) {
+  const int64_t nnz = s->nnz, nbr = ceil_div(s->m, r), nbc = ceil_div(s->n, c);
+  if (nbc * r * c >= INT32_MAX) raise(SFG_ERR_INVALID_OPERATION, "decompose by blocks: block keys exceed int32");
+  auto* flag = dalloc_n<uint8_t>(ctx, nnz);
+  if (nnz) {
+    auto* key = dalloc_n<int32_t>(ctx, nnz);
+    auto* sub = dalloc_n<int32_t>(ctx, nnz);
+    auto* ib = dalloc_n<float>(ctx, nnz);
+    SFG_LAUNCH(k_blockdec_keys, stream_grid(ctx, nnz, kBlock, 4, 8), kBlock, 0, ctx->stream, s->row, s->idx, nnz,
+               (int32_t)r, (int32_t)c, key, sub, ib);
+    sfg_tensor* sorted = nullptr;
+    try {
+      sorted = sort_coo(ctx, nbr, nbc * r * c, nnz, key, sub, ib, false);
+    } catch (...) {
+      for (void* q : {(void*)key, (void*)sub, (void*)ib, (void*)flag}) dfree(ctx, q);
+      throw;
+    }
+    for (void* q : {(void*)key, (void*)sub, (void*)ib}) dfree(ctx, q);
+    SFG_LAUNCH(k_blockdec_flags, stream_grid(ctx, nnz, kBlock, 4, 8), kBlock, 0, ctx->stream, sorted->row,
+               sorted->idx, static_cast<const float*>(sorted->val), static_cast<const float*>(s->val), nnz,
+               (int32_t)(r * c), min_sum, flag);
+    free_tensor_arrays(sorted);
+    delete sorted;
+  }
+  const int64_t tiles = ceil_div(nnz, (int64_t)kSplitTileF);
+  auto* cnt = dalloc_n<int32_t>(ctx, tiles);
+  auto* base = dalloc_n<int32_t>(ctx, tiles + 1);
+  int32_t nsel = 0;
+  if (nnz) {
+    SFG_LAUNCH(k_flag_count, (int)tiles, 256, 0, ctx->stream, flag, nnz, cnt);
+    scan_counts(ctx, cnt, tiles, base);
+    read_back(ctx, base + tiles, 4, &nsel);
+  }
+  sfg_tensor* a = coo_alloc(ctx, s->m, s->n, nsel);
+  sfg_tensor* b = coo_alloc(ctx, s->m, s->n, nnz - nsel);
+  a->has_zeros = b->has_zeros = s->has_zeros == 0 ? 0 : -1;
+  if (nnz)
+    SFG_LAUNCH(k_flag_split, (int)tiles, 256, 0, ctx->stream, flag, base, s->row, s->idx,
+               static_cast<const float*>(s->val), nnz, a->row, a->idx, static_cast<float*>(a->val), b->row, b->idx,
+               static_cast<float*>(b->val));
+  for (void* q : {(void*)flag, (void*)cnt, (void*)base}) dfree(ctx, q);
+  *sel = a;
+  *rem = b;
+}
+
+sfg_tensor* coo_to_hbell(sfg_context* ctx, const sfg_tensor* s, int64_t b, int64_t min_sum) {
+  sfg_tensor *sel = nullptr, *rem = nullptr;
+  decompose_blocks(ctx, s, b, b, min_sum, &sel, &rem);
+  sfg_tensor* h = new_tensor(ctx, SFG_HBELL, s->m, s->n);
+  h->threshold = min_sum;
+  h->br = h->bc = b;
+  try {
+    h->part[0] = coo_to_bell(ctx, sel, b);
+  } catch (...) {
+    for (sfg_tensor* t : {sel, rem}) {
+      free_tensor_arrays(t);
+      delete t;
+    }
+    delete h;
+    throw;
+  }
+  free_tensor_arrays(sel);
+  delete sel;
+  h->part[1] = rem;  // the remainder stays coordinate form (COO)
+  return h;
+}
+
+}  // namespace sfg

@@ -400,7 +400,8 @@ sfg_tensor* deep_copy(sfg_context* ctx, const sfg_tensor* s) {
 sfg_tensor* convert_from_compressed(sfg_context* ctx, const sfg_tensor* s, const sfg_format& dst) {
   if (s->kind == SFG_ELL || s->kind == SFG_BELL)
     raise(SFG_ERR_UNSUPPORTED_SOURCE, "conversion from a format with indirect levels");
-  if (s->kind == SFG_HYB) raise(SFG_ERR_UNSUPPORTED_SOURCE, "conversion from the hybrid pair");
+  if (s->kind == SFG_HYB || s->kind == SFG_HBELL)
+    raise(SFG_ERR_UNSUPPORTED_SOURCE, "conversion from the hybrid pair");
   // planner.hpp:98-99: sources with a value layout are rejected
   if (s->kind == SFG_DOK || s->kind == SFG_LIL || s->kind == SFG_C2SR)
     raise(SFG_ERR_UNSUPPORTED_SOURCE, "conversion from a format with a value layout");
@@ -447,6 +448,7 @@ sfg_tensor* convert_from_compressed(sfg_context* ctx, const sfg_tensor* s, const
       case SFG_ELL: out = coo_to_ell(ctx, coo); break;
       case SFG_BCSR: out = coo_to_bcsr(ctx, coo, dst.block_r, dst.block_c, dst.value_dtype); break;
       case SFG_HYB: out = coo_to_hyb(ctx, coo, dst.threshold); break;
+      case SFG_HBELL: out = coo_to_hbell(ctx, coo, dst.block_r, dst.threshold); break;
       case SFG_BELL: out = coo_to_bell(ctx, coo, dst.block_r); break;
       case SFG_DOK: out = coo_to_dok(ctx, coo); break;
       case SFG_LIL: out = coo_to_lil(ctx, coo); break;

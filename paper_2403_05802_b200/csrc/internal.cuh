@@ -84,6 +84,7 @@ struct sfg_context {
 //   ELL : slots[K] (L0 idx), idx[K*m] (L2 idx, slot-major), val[K*m]
 //   BCSR: ptr[nbr+1], idx[nblocks] (bcol), val[nblocks*rb*cb] block-major
 //   HYB : part[0] = ELL of the remainder, part[1] = COO of the selection
+//   HBELL: part[0] = BELL(b) of the dense blocks, part[1] = COO of the rest
 //   BELL: slots[K], idx[K*nbr] (block column of cell (slot, block row),
 //         slot-major), val[K*nbr*rb*cb]; nnz = K*nbr cells
 //   DOK : val = records {row, col, val}[nnz];  LIL: ptr[m+1], val = {col, val}[nnz]
@@ -237,6 +238,11 @@ void scan_counts(sfg_context* ctx, const int32_t* cnt, int64_t n, int32_t* ptr);
 sfg_tensor* ell_nonzeros_to_coo(sfg_context* ctx, const sfg_tensor* s);
 // Blocked ELL (convert_bell.cu): the BCSR blocks relaid slot by slot.
 sfg_tensor* coo_to_bell(sfg_context* ctx, const sfg_tensor* s, int64_t b);
+// decompose by blocks (the block count rule) and the hybrid BELL/COO built on
+// it: part[0] = BELL(b) of the blocks with >= min_sum nonzeros, part[1] = COO.
+void decompose_blocks(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_t c, int64_t min_sum,
+                      sfg_tensor** sel, sfg_tensor** rem);
+sfg_tensor* coo_to_hbell(sfg_context* ctx, const sfg_tensor* s, int64_t b, int64_t min_sum);
 // Value-layout formats (pack.cu): Pack(0,1) over COO (DOK) / CSR (LIL).
 sfg_tensor* coo_to_dok(sfg_context* ctx, const sfg_tensor* s);
 sfg_tensor* coo_to_lil(sfg_context* ctx, const sfg_tensor* s);

@@ -92,12 +92,12 @@ void spgemm(sfg_context* ctx, const sfg_tensor* a, const sfg_tensor* b, float* c
   if (a->n != b->m) raise(SFG_ERR_INVALID_OPERATION, "spgemm: inner extents differ");
   // hybrid operands: the sum of their two parts' products (the reference
   // runs the kernel once per part)
-  if (a->kind == SFG_HYB) {
+  if (a->kind == SFG_HYB || a->kind == SFG_HBELL) {
     spgemm(ctx, a->part[0], b, c, ldc, accumulate);
     spgemm(ctx, a->part[1], b, c, ldc, true);
     return;
   }
-  if (b->kind == SFG_HYB) {
+  if (b->kind == SFG_HYB || b->kind == SFG_HBELL) {
     spgemm(ctx, a, b->part[0], c, ldc, accumulate);
     spgemm(ctx, a, b->part[1], c, ldc, true);
     return;

@@ -1306,7 +1306,7 @@ bool spmm_bcsr_tc(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dt
 
 void spmm(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dtype, int64_t nd,
           int64_t ldb, float* c, int64_t ldc, bool accumulate) {
-  if (a->kind == SFG_HYB) {
+  if (a->kind == SFG_HYB || a->kind == SFG_HBELL) {
     spmm(ctx, a->part[0], b, b_dtype, nd, ldb, c, ldc, accumulate);
     spmm(ctx, a->part[1], b, b_dtype, nd, ldb, c, ldc, true);
     return;

@@ -512,6 +512,7 @@ void spmv(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, bool 
       break;
     }
     case SFG_HYB:
+    case SFG_HBELL:
       // y = ELL(remainder) x, then += COO(selection) x: the caller-side sum
       // of two run_kernel outputs in the reference.
       spmv(ctx, a->part[0], x, y, acc);

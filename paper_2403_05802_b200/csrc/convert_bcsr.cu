@@ -107,6 +107,49 @@ __device__ __forceinline__ void col_range(const int32_t* __restrict__ col, int32
 // separate min/max pass over the columns.
 constexpr int32_t kFullRangeCols = 32768;
 
+// Block-count rule of the hybrid decompose (convert_bell.cu): per block row,
+// a shared counter per block column gathers the nonzero
+// count of every r x c block — a warp's 32 consecutive entries split into
+// runs of one block column (a row's columns ascend), one shared atomic per
+// run — then every entry is flagged by its block's count. Entries stay in
+// place, so the flags are in input order.
+constexpr int32_t kDecCounters = 48 * 1024;  // 192 KB of counters
+
+__global__ void __launch_bounds__(kBlock) k_block_nz_flags(const int32_t* __restrict__ bptr,
+                                                           const int32_t* __restrict__ col,
+                                                           const float* __restrict__ val, int32_t c, int32_t nbr,
+                                                           int32_t nbc, int64_t min_sum, bool count_values,
+                                                           uint8_t* __restrict__ flag) {
+  extern __shared__ uint32_t cnt[];  // nbc <= kDecCounters (host)
+  const int lane = threadIdx.x & 31;
+  for (int32_t br = blockIdx.x; br < nbr; br += gridDim.x) {
+    const int32_t s = __ldg(bptr + br), e = __ldg(bptr + br + 1);
+    if (s == e) continue;
+    for (int w = threadIdx.x; w < nbc; w += blockDim.x) cnt[w] = 0;
+    __syncthreads();
+    for (int32_t k0 = s; k0 < e; k0 += blockDim.x) {
+      const int32_t k = k0 + threadIdx.x;
+      const bool in = k < e;
+      const int b = in ? __ldg(col + k) / c : -1;
+      const bool nz = in && (!count_values || __ldg(val + k) != 0.f);
+      const int pb = __shfl_up_sync(kFull, b, 1);
+      const bool head = in && (lane == 0 || pb != b);
+      const unsigned hm = __ballot_sync(kFull, head), nm = __ballot_sync(kFull, nz);
+      if (head) {
+        const unsigned above = hm & ~((2u << lane) - 1u);
+        const int h = above ? __ffs(above) - 1 : 32;
+        const unsigned run = (h == 32 ? kFull : ((1u << h) - 1u)) & ~((1u << lane) - 1u);
+        const int q = __popc(nm & run);
+        if (q) atomicAdd(cnt + b, (uint32_t)q);
+      }
+    }
+    __syncthreads();
+    for (int32_t k = s + threadIdx.x; k < e; k += blockDim.x)
+      flag[k] = (int64_t)cnt[__ldg(col + k) / c] >= min_sum ? 1 : 0;
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(kBlock) k_count_blocks(const int32_t* __restrict__ bptr,
                                                           const int32_t* __restrict__ col,
                                                           int32_t c, int32_t nbr, int32_t nbc,
@@ -321,6 +364,22 @@ sfg_tensor* coo_to_bcsr(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_
   dfree(ctx, bptr);
   dfree(ctx, cnt);
   return t;
+}
+
+bool block_nz_flags(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_t c, int64_t min_sum, uint8_t* flag) {
+  const int64_t nbr = ceil_div(s->m, r), nbc = ceil_div(s->n, c);
+  if (nbc > kDecCounters || nbr >= INT32_MAX) return false;
+  if (s->nnz == 0) return true;
+  int32_t* bptr = dalloc_n<int32_t>(ctx, nbr + 1);
+  SFG_LAUNCH(k_brow_ptr, stream_grid(ctx, ceil_div(s->nnz, 128 * kBrowVec), kBlock / 32, 1, 8), kBlock, 0,
+             ctx->stream, s->row, s->nnz, (int32_t)r, (int32_t)nbr, bptr);
+  const size_t smem = (size_t)nbc * 4;
+  SFG_CUDA(cudaFuncSetAttribute(k_block_nz_flags, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SFG_LAUNCH(k_block_nz_flags, (int)std::min<int64_t>(nbr, (int64_t)ctx->sms * 16), kBlock, smem, ctx->stream, bptr,
+             s->idx, static_cast<const float*>(s->val), (int32_t)c, (int32_t)nbr, (int32_t)nbc, min_sum,
+             s->has_zeros != 0, flag);
+  dfree(ctx, bptr);
+  return true;
 }
 
 }  // namespace sfg

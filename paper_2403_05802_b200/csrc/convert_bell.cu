@@ -145,18 +145,32 @@ __global__ void k_blockdec_keys(const int32_t* __restrict__ row, const int32_t* 
   }
 }
 
-// sorted keys: block runs (same row key, same sub / (r c)); a thread per
-// entry walks back / forward to its run's ends — runs hold <= r c entries
+// sorted keys: block runs (same row key, same sub / (r c)) hold <= r c
+// entries and the composite (key, sub / (r c)) is nondecreasing, so a thread
+// per entry finds its run's ends by binary search inside the r c window
+// either side; without explicit zeros the run length is its nonzero count,
+// otherwise the run's values are counted.
 __global__ void k_blockdec_flags(const int32_t* __restrict__ key, const int32_t* __restrict__ sub,
                                  const float* __restrict__ idx_bits, const float* __restrict__ val_in, int64_t nnz,
-                                 int32_t rc, int64_t min_sum, uint8_t* __restrict__ flag) {
+                                 int32_t rc, int64_t min_sum, bool count_values, uint8_t* __restrict__ flag) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
     const int32_t k = key[e], b = sub[e] / rc;
-    int64_t lo = e, hi = e;
-    while (lo > 0 && key[lo - 1] == k && sub[lo - 1] / rc == b) --lo;
-    while (hi + 1 < nnz && key[hi + 1] == k && sub[hi + 1] / rc == b) ++hi;
-    int64_t nz = 0;
-    for (int64_t q = lo; q <= hi; ++q) nz += val_in[__float_as_int(idx_bits[q])] != 0.f ? 1 : 0;
+    auto same = [&](int64_t q) { return key[q] == k && sub[q] / rc == b; };
+    int64_t lo = e - rc + 1 > 0 ? e - rc + 1 : 0, l_hi = e;  // first q in [lo, e] with same(q)
+    while (lo < l_hi) {
+      const int64_t mid = (lo + l_hi) >> 1;
+      if (same(mid)) l_hi = mid; else lo = mid + 1;
+    }
+    int64_t h_lo = e, hi = e + rc - 1 < nnz - 1 ? e + rc - 1 : nnz - 1;  // last q in [e, hi] with same(q)
+    while (h_lo < hi) {
+      const int64_t mid = (h_lo + hi + 1) >> 1;
+      if (same(mid)) h_lo = mid; else hi = mid - 1;
+    }
+    int64_t nz = hi - lo + 1;
+    if (count_values) {
+      nz = 0;
+      for (int64_t q = lo; q <= hi; ++q) nz += val_in[__float_as_int(idx_bits[q])] != 0.f ? 1 : 0;
+    }
     flag[__float_as_int(idx_bits[e])] = nz >= min_sum ? 1 : 0;
   }
 }
@@ -234,7 +248,9 @@ void decompose_blocks(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_t 
   const int64_t nnz = s->nnz, nbr = ceil_div(s->m, r), nbc = ceil_div(s->n, c);
   if (nbc * r * c >= INT32_MAX) raise(SFG_ERR_INVALID_OPERATION, "decompose by blocks: block keys exceed int32");
   auto* flag = dalloc_n<uint8_t>(ctx, nnz);
-  if (nnz) {
+  // canonical input with a block-column grid that fits the shared counters:
+  // counted in place (convert_bcsr.cu); otherwise the radix path below
+  if (!block_nz_flags(ctx, s, r, c, min_sum, flag) && nnz) {
     auto* key = dalloc_n<int32_t>(ctx, nnz);
     auto* sub = dalloc_n<int32_t>(ctx, nnz);
     auto* ib = dalloc_n<float>(ctx, nnz);
@@ -250,7 +266,7 @@ void decompose_blocks(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_t 
     for (void* q : {(void*)key, (void*)sub, (void*)ib}) dfree(ctx, q);
     SFG_LAUNCH(k_blockdec_flags, stream_grid(ctx, nnz, kBlock, 4, 8), kBlock, 0, ctx->stream, sorted->row,
                sorted->idx, static_cast<const float*>(sorted->val), static_cast<const float*>(s->val), nnz,
-               (int32_t)(r * c), min_sum, flag);
+               (int32_t)(r * c), min_sum, s->has_zeros != 0, flag);
     free_tensor_arrays(sorted);
     delete sorted;
   }

@@ -219,6 +219,9 @@ sfg_tensor* coo_to_csc(sfg_context* ctx, const sfg_tensor* s);
 sfg_tensor* coo_to_dcsr(sfg_context* ctx, const sfg_tensor* s);
 sfg_tensor* coo_to_ell(sfg_context* ctx, const sfg_tensor* s);
 sfg_tensor* coo_to_bcsr(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_t c, int dtype);
+// per-entry flags of the block-count rule over canonical COO (false: grid too
+// wide for the shared counters — the caller sorts instead)
+bool block_nz_flags(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_t c, int64_t min_sum, uint8_t* flag);
 sfg_tensor* coo_to_hyb(sfg_context* ctx, const sfg_tensor* s, int64_t min_sum);
 // DIA and CSB(r,c) (convert_dia.cu), and back to canonical COO (DIA: its
 // nonzero cells; CSB: every entry).

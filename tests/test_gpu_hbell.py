@@ -51,6 +51,32 @@ def test_decompose_blocks_matches_reference(ctx, ref, case, b, t):
         assert_same_materialized(bell.download(), ref.convert(ps, "BELL", b).download(), (case, b, t, "bell"))
 
 
+@pytest.mark.parametrize("case", ["zeros", "wide"])
+def test_decompose_blocks_paths(ctx, ref, case):
+    """Explicit zeros (the count rule counts only nonzero values) and a block
+    grid wider than the device's shared counters (the radix-order path)."""
+    b, t = 2, 2
+    if case == "zeros":
+        m, n = 150, 130
+        r, c, v = blocky(3, m, n, b)
+        v = v.copy()
+        v[np.random.default_rng(1).random(len(v)) < 0.3] = 0.0
+    else:
+        m, n = 40, 200_000
+        rng = np.random.default_rng(2)
+        r = rng.integers(0, m, 3000)
+        c = np.concatenate([rng.integers(0, n, 1500), rng.integers(0, 200, 1500)])
+        key = np.unique(r * n + c)
+        r, c = key // n, key % n
+        v = (0.5 + rng.random(len(r))).astype(np.float32).astype(np.float64)
+    d, p = ctx.from_coo(m, n, r, c, v), ref.from_coo(m, n, r, c, v)
+    ds, dr = ctx.decompose_blocks(d, b, b, t)
+    ps, pr = ref.decompose_blocks(p, b, b, t)
+    assert 0 < ps.nnz < len(v)
+    for dd, pp, what in ((ds, ps, "selected"), (dr, pr, "remainder")):
+        assert_same_materialized(ctx.convert(dd, "COO").download(), ref.convert(pp, "COO").download(), (case, what))
+
+
 @pytest.mark.parametrize("b,t", [(4, 8), (16, 128)])
 def test_hbell_spmv_spmm(ctx, b, t):
     m, n = 1000, 900

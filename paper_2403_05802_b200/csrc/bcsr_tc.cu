@@ -97,6 +97,17 @@ __device__ __forceinline__ void tc_mma_elect(uint32_t tmem_d, uint64_t adesc, ui
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+__device__ __forceinline__ void tc_mma_elect_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.eq.u32 p, 1, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc)
+      : "memory");
+}
 __device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
   asm volatile(
       "{\n"
@@ -574,22 +585,62 @@ __global__ void __launch_bounds__(32 * (4 + kProducers + kMmaWarps), 1)
 // per ~kPanel x 3 MMAs instead of per ~3. Value blocks arrive by cp.async
 // (one 16-byte copy per lane per block, written in the 32-byte-swizzled
 // K-major layout). Stage metadata (tile masks) travels in shared memory.
-constexpr int kPanel = 4;
-constexpr int kPanelA = 16;  // value blocks per stage (a wider block column splits)
-constexpr int kPStages = 8;
-constexpr int kPStageBytes = kPanel * kTileBytes + kPanelA * kABytes;  // 24 KB
+// Two configurations: bf16 (one kind::f16 MMA per block, 4 tiles and 16
+// value blocks per stage, 8 stages) and fp32 (3xTF32: per block and K half
+// of 8, hi.hi + lo.hi + hi.lo kind::tf32 MMAs — six per block — with B split
+// into tf32 hi / lo arrays by a pre-pass and each staged value block split in
+// shared memory by its MMA warp; 2 tiles and 8 blocks per stage, each stored
+// hi and lo, 4 stages).
+template <bool kTF>
+struct PanelCfg;
+template <>
+struct PanelCfg<false> {
+  static constexpr int kPanel = 4, kPanelA = 16, kStages = 8;
+  static constexpr int kTile = kTileBytes, kA = kABytes;
+  static constexpr int kVal = kPanel * kTile;  // value blocks' offset inside a stage
+  static constexpr int kStageBytes = kPanel * kTile + kPanelA * kA;     // 24 KB
+  static constexpr uint32_t kId = kIdesc;
+};
+template <>
+struct PanelCfg<true> {
+  static constexpr int kPanel = 2, kPanelA = 8, kStages = 4;
+  static constexpr int kTile = kBlk * kND * 4, kA = kBlk * kBlk * 4;  // 8 KB, 1 KB
+  static constexpr int kLoTile = kPanel * kTile, kVal = 2 * kPanel * kTile, kLoVal = kVal + kPanelA * kA;
+  static constexpr int kStageBytes = 2 * (kPanel * kTile + kPanelA * kA);  // 48 KB
+  // F32 accumulate, TF32 x TF32, A MN-major, B K-major, N = 16, M = 128
+  static constexpr uint32_t kId = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) |
+                                     ((uint32_t)(kBlk >> 3) << 17) | ((uint32_t)(kND >> 4) << 24);
+};
 constexpr int kDescWords = 32;  // 0 head, 1-4 tile columns, 5-8 masks, 10-13 slot bytes, 16-31 slot blocks
-static_assert(kPanel <= 4 && kPanelA <= 16, "descriptor layout: 4 tiles, 16 slots");
+static_assert(PanelCfg<false>::kPanel <= 4 && PanelCfg<false>::kPanelA <= 16, "descriptor layout: 4 tiles, 16 slots");
 
+template <int kStagesT>
 struct PShared {
-  uint64_t full[kPStages];
-  uint64_t empty[kPStages];
+  uint64_t full[kStagesT];
+  uint64_t empty[kStagesT];
   uint64_t acc_full;
   uint64_t acc_empty;
-  alignas(16) uint32_t mask[kPStages][kPanel];  // mask[s][t]: block rows of tile t; a zero tile ends the stage
-  alignas(16) uint8_t slot[kPStages][kPanelA];  // slot -> block row | tile << 5
+  alignas(16) uint32_t mask[kStagesT][4];  // mask[s][t]: block rows of tile t; a zero tile ends the stage
+  alignas(16) uint8_t slot[kStagesT][16];  // slot -> block row | tile << 5
   uint32_t tmem_base;
 };
+
+// tf32 hi part: the low 13 mantissa bits cleared (exact as tf32 whether the
+// tensor core truncates or rounds); lo = x - hi is exact in fp32
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
+
+// B (n x 128, leading dimension ldb) -> hi, lo (n x 128, dense)
+__global__ void k_tf32_split(const float* __restrict__ b, int64_t n, int64_t ldb, float* __restrict__ hi,
+                             float* __restrict__ lo) {
+  const int64_t q4 = n * (kND / 4);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < q4; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / (kND / 4), c4 = i % (kND / 4);
+    const float4 x = ld_stream(reinterpret_cast<const float4*>(b + r * ldb) + c4);
+    const float4 h = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
+    reinterpret_cast<float4*>(hi)[i] = h;
+    reinterpret_cast<float4*>(lo)[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+  }
+}
 
 __device__ __forceinline__ void tmem_zero16(uint32_t taddr) {
   asm volatile(
@@ -606,15 +657,18 @@ __device__ __forceinline__ void tmem_zero16(uint32_t taddr) {
 // epilogue after each drain and every MMA accumulates, so the MMAs of one
 // group may come from any MMA warp (the CTA's MMAs execute in one tensor
 // pipe; each adds into its accumulator).
-template <int kProducers, int kMmaWarps>
+template <int kProducers, int kMmaWarps, bool kTF>
 __global__ void __launch_bounds__(32 * (4 + kProducers + kMmaWarps), 1)
-    k_bcsr_tc_panel(const __grid_constant__ CUtensorMap tmap_b, const uint8_t* __restrict__ aval,
+    k_bcsr_tc_panel(const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_lo,
+                    const uint8_t* __restrict__ aval,
                     const int32_t* __restrict__ ptr, int32_t nbr, int32_t m, float* __restrict__ c, int64_t ldc,
                     int accumulate, const int32_t* __restrict__ sbase, const uint32_t* __restrict__ sdesc,
                     int dbg, unsigned long long* __restrict__ dbg_out) {
+  using Cfg = PanelCfg<kTF>;
+  constexpr int kPStages = Cfg::kStages, kPStageBytes = Cfg::kStageBytes;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* stages = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  PShared* sh = reinterpret_cast<PShared*>(stages + kPStages * kPStageBytes);
+  auto* sh = reinterpret_cast<PShared<kPStages>*>(stages + kPStages * kPStageBytes);
   unsigned long long t_wait = 0, t_start = clock64();
   auto timed_wait = [&](uint64_t* bar, uint32_t par) {
     if (dbg & 256) {
@@ -723,20 +777,38 @@ __global__ void __launch_bounds__(32 * (4 + kProducers + kMmaWarps), 1)
         const int ntile = (int)(head & 0xff), nblk = (int)(head >> 8 & 0xff);
         const uint32_t tbc = __shfl_sync(kFull, c0, 1 + (lane & 3));
         const uint32_t tmask = __shfl_sync(kFull, c0, 5 + (lane & 3));
-        if (lane >= 10 && lane < 10 + kPanelA / 4) sts_u32(smem_u32(&sh->slot[stage][4 * (lane - 10)]), c0);
-        if (lane < kPanel) {
+        if (lane >= 10 && lane < 10 + Cfg::kPanelA / 4) sts_u32(smem_u32(&sh->slot[stage][4 * (lane - 10)]), c0);
+        if (lane < 4) {
           sts_u32(smem_u32(&sh->mask[stage][lane]), lane < ntile ? tmask : 0u);
           if (lane < ntile && !(dbg & 2)) {
-            mbar_expect_tx_only(&sh->full[stage], kTileBytes);
-            tma_3d(st + lane * kTileBytes, &tmap_b, &sh->full[stage], 0, (int)tbc * kBlk, 0);
+            if constexpr (kTF) {
+              mbar_expect_tx_only(&sh->full[stage], 2 * Cfg::kTile);
+              tma_3d(st + lane * Cfg::kTile, &tmap_b, &sh->full[stage], 0, (int)tbc * kBlk, 0);
+              tma_3d(st + Cfg::kLoTile + lane * Cfg::kTile, &tmap_lo, &sh->full[stage], 0, (int)tbc * kBlk, 0);
+            } else {
+              mbar_expect_tx_only(&sh->full[stage], Cfg::kTile);
+              tma_3d(st + lane * Cfg::kTile, &tmap_b, &sh->full[stage], 0, (int)tbc * kBlk, 0);
+            }
           }
         }
         __syncwarp();  // reconverge: the shuffles below must not take the divergent path
         for (int sl = 0; sl < ((dbg & 4) ? 0 : nblk); ++sl) {
           const int32_t kb = (int32_t)__shfl_sync(kFull, c0, 16 + sl);
-          cp_async16(st + kPanel * kTileBytes + sl * kABytes + dst_off, aval + (int64_t)kb * kABytes + lane * 16);
+          if constexpr (kTF) {
+            // 1 KB fp32 block, row-major 16 x 16: 16-byte chunk q = row i,
+            // chunk cq of the row -> K half cq / 2, 32-byte-swizzled
+            // K-major (chunk cq % 2 of row i at chunk (cq % 2) ^ (i >> 2 & 1))
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+              const int qq = lane + 32 * t, i = qq >> 2, cq = qq & 3;
+              const uint32_t off = (cq >> 1) * 512 + i * 32 + (((cq & 1) ^ ((i >> 2) & 1)) << 4);
+              cp_async16(st + Cfg::kVal + sl * Cfg::kA + off, aval + (int64_t)kb * Cfg::kA + qq * 16);
+            }
+          } else {
+            cp_async16(st + Cfg::kVal + sl * Cfg::kA + dst_off, aval + (int64_t)kb * Cfg::kA + lane * 16);
+          }
         }
-      } else if (lane < kPanel) {
+      } else if (lane < 4) {
         sts_u32(smem_u32(&sh->mask[stage][lane]), 0u);  // end-of-group marker
       }
       cp_async_mbar_arrive(&sh->full[stage]);
@@ -754,8 +826,11 @@ __global__ void __launch_bounds__(32 * (4 + kProducers + kMmaWarps), 1)
     // fetched while the current MMA issues).
     const int w = warp - kMmaWarp;
     const uint32_t base0 = smem_u32(stages);
-    const uint64_t adesc0 = smem_desc(base0, 2048, 1024, 2);                     // SW128, MN-major
-    const uint64_t bdesc0 = smem_desc(base0 + kPanel * kTileBytes, 16, 256, 6);  // SW32, K-major
+    // A (the B tiles), MN-major: bf16 SW128 (8-row K groups, SBO 1 KB);
+    // tf32 only takes SW128 with 32-byte atoms (layout type 1, 4-row K
+    // groups, SBO 512 B). Both: 2 KB between the 128-byte column boxes.
+    const uint64_t adesc0 = kTF ? smem_desc(base0, 2048, 512, 1) : smem_desc(base0, 2048, 1024, 2);
+    const uint64_t bdesc0 = smem_desc(base0 + Cfg::kVal, 16, 256, 6);  // SW32, K-major
     uint32_t tg = 0;  // ring position of the group's first stage
     int it = 0;
     for (int32_t g = blockIdx.x; g < ngroups; g += gridDim.x, ++it) {
@@ -769,9 +844,24 @@ __global__ void __launch_bounds__(32 * (4 + kProducers + kMmaWarps), 1)
         const uint32_t phase = (tq / kPStages) & 1u;
         timed_wait(&sh->full[stage], phase);
         tc_fence_after();
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // cp.async data -> MMA reads
         const uint4 mv = lds_v4(smem_u32(&sh->mask[stage][0]));
         const int nblk = __popc(mv.x) + __popc(mv.y) + __popc(mv.z) + __popc(mv.w);
+        if constexpr (kTF) {
+          // split the staged value blocks: hi in place, lo beside them
+          const uint32_t vbase = base0 + stage * kPStageBytes + Cfg::kVal;
+          for (int q = lane; q < nblk * (Cfg::kA / 16); q += 32) {
+            const uint4 x = lds_v4(vbase + q * 16);
+            const uint4 h = make_uint4(x.x & 0xffffe000u, x.y & 0xffffe000u, x.z & 0xffffe000u, x.w & 0xffffe000u);
+            const uint4 l = make_uint4(__float_as_uint(__uint_as_float(x.x) - __uint_as_float(h.x)),
+                                       __float_as_uint(__uint_as_float(x.y) - __uint_as_float(h.y)),
+                                       __float_as_uint(__uint_as_float(x.z) - __uint_as_float(h.z)),
+                                       __float_as_uint(__uint_as_float(x.w) - __uint_as_float(h.w)));
+            sts_v4(vbase + q * 16, h);
+            sts_v4(vbase + (Cfg::kLoVal - Cfg::kVal) + q * 16, l);
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // cp.async / st.shared data -> MMA reads
+        __syncwarp();
         uint32_t b = 0;
         if (lane < nblk) asm volatile("ld.shared.u8 %0, [%1];" : "=r"(b) : "r"(smem_u32(&sh->slot[stage][lane])));
         __syncwarp();
@@ -780,8 +870,21 @@ __global__ void __launch_bounds__(32 * (4 + kProducers + kMmaWarps), 1)
           uint32_t pk = __shfl_sync(kFull, b, 0);
           for (int sl = 0; sl < nblk; ++sl) {
             const uint32_t nx = __shfl_sync(kFull, b, (sl + 1) & 31);
-            tc_mma_elect(tmem + (pk & 31u) * kBlk, adesc0 + soff + (pk >> 5) * (kTileBytes >> 4),
-                         bdesc0 + soff + (uint32_t)sl * (kABytes >> 4), kIdesc, 1u);
+            const uint32_t acc = tmem + (pk & 31u) * kBlk;
+            const uint64_t ad = adesc0 + soff + (pk >> 5) * (Cfg::kTile >> 4);
+            const uint64_t bd = bdesc0 + soff + (uint32_t)sl * (Cfg::kA >> 4);
+            if constexpr (kTF) {
+              constexpr uint32_t lo_a = Cfg::kLoTile >> 4, lo_b = (Cfg::kLoVal - Cfg::kVal) >> 4;
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {  // K half: tile rows 8h.., value-block half h
+                const uint64_t ah = ad + h * (1024 >> 4), bh = bd + h * (512 >> 4);
+                tc_mma_elect_tf32(acc, ah, bh, Cfg::kId);
+                tc_mma_elect_tf32(acc, ah + lo_a, bh, Cfg::kId);
+                tc_mma_elect_tf32(acc, ah, bh + lo_b, Cfg::kId);
+              }
+            } else {
+              tc_mma_elect(acc, ad, bd, Cfg::kId, 1u);
+            }
             pk = nx;
           }
         }
@@ -850,7 +953,7 @@ constexpr int kSegCols = 2048;
 
 template <bool kWrite>
 __global__ void __launch_bounds__(256) k_bcsr_sched(const uint32_t* __restrict__ plan, int32_t nbr, int32_t nbc,
-                                                     int32_t nseg, int32_t* __restrict__ sbase,
+                                                     int32_t nseg, int panel, int panel_a, int32_t* __restrict__ sbase,
                                                      int32_t* __restrict__ bcnt, uint32_t* __restrict__ sdesc) {
   const int lane = threadIdx.x & 31;
   const int32_t ngroups = (nbr + kGroup - 1) / kGroup;
@@ -868,7 +971,7 @@ __global__ void __launch_bounds__(256) k_bcsr_sched(const uint32_t* __restrict__
       if (kWrite) {
         uint32_t* d = sdesc + (int64_t)stage * kDescWords;
         if (lane == 0) d[0] = (uint32_t)ntile | ((uint32_t)nblk << 8);
-        if (lane < kPanel) {
+        if (lane < 4) {
           d[1 + lane] = lane < ntile ? my_bc : 0u;
           d[5 + lane] = lane < ntile ? my_mask : 0u;
         }
@@ -888,10 +991,10 @@ __global__ void __launch_bounds__(256) k_bcsr_sched(const uint32_t* __restrict__
           // a block column held by more than kPanelA block rows is split
           // into several tiles (the B tile is loaded once per tile)
           uint32_t mask = rest;
-          if (__popc(rest) > kPanelA) {
+          if (__popc(rest) > panel_a) {
             mask = 0;
             uint32_t t = rest;
-            for (int k = 0; k < kPanelA; ++k) {
+            for (int k = 0; k < panel_a; ++k) {
               const uint32_t low = t & (0u - t);
               mask |= low;
               t ^= low;
@@ -899,7 +1002,7 @@ __global__ void __launch_bounds__(256) k_bcsr_sched(const uint32_t* __restrict__
           }
           rest ^= mask;
           const int cnt = __popc(mask);
-          if (ntile && (ntile == kPanel || nblk + cnt > kPanelA)) close();
+          if (ntile && (ntile == panel || nblk + cnt > panel_a)) close();
           if (!ntile) nblk = 0;
           if (lane == ntile) {
             my_bc = (uint32_t)(bc0 + src);
@@ -998,12 +1101,122 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 bool spmm_bcsr_tc(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dtype, int64_t nd,
                   int64_t ldb, float* c, int64_t ldc, bool accumulate) {
-  if (a->kind != SFG_BCSR || a->dtype != SFG_BF16 || b_dtype != SFG_BF16 || nd != kND) return false;
+  // bf16 values and B: one kind::f16 MMA per block; fp32 values and B:
+  // 3xTF32 (panel schedule only)
+  const bool tf = a->dtype == SFG_F32 && b_dtype == SFG_F32;
+  const bool bf = a->dtype == SFG_BF16 && b_dtype == SFG_BF16;
+  if (a->kind != SFG_BCSR || !(tf || bf) || nd != kND) return false;
   if (a->br != kBlk || a->bc != kBlk || a->rb != kBlk || a->cb != kBlk) return false;
-  if ((ldb * 2) % 16 != 0 || (reinterpret_cast<uintptr_t>(b) & 15) || a->nnz == 0) return false;
+  if (reinterpret_cast<uintptr_t>(b) & 15 || a->nnz == 0) return false;
+  if (bf ? (ldb * 2) % 16 != 0 : ldb % 4 != 0) return false;
   if (a->nbr > INT32_MAX || a->nnz * kBlk > INT32_MAX) return false;
+  const int64_t ngroups = ceil_div(a->nbr, kGroup);
+  const int64_t words = ngroups * a->nbc;
+  const bool plan_ok = a->nnz * 4 >= words && words <= (int64_t(1) << 30);
+  if (tf && !plan_ok) return false;
   auto encode = get_encode();
   if (!encode) return false;
+  sfg_tensor* mut = const_cast<sfg_tensor*>(a);  // plan and schedule are caches, not tensor state
+  int grid = (int)std::min<int64_t>(ngroups, (int64_t)ctx->sms);
+  auto build_schedule = [&](int panel, int panel_a) {
+    // The mask plan (per 32-block-row group, per block column) and the stage
+    // schedule are built once per matrix and cached on the tensor; they are
+    // used when the group masks are dense enough that streaming them beats
+    // the in-kernel merge. A warp per (group, segment of kSegCols block
+    // columns): count, scan, write.
+    if (!mut->tc_plan) {
+      mut->tc_plan = dalloc_n<uint32_t>(ctx, words);
+      SFG_CUDA(cudaMemsetAsync(mut->tc_plan, 0, words * 4, ctx->stream));
+      SFG_LAUNCH(k_bcsr_plan, stream_grid(ctx, a->nbr * 32, 256, 1, 8), 256, 0, ctx->stream, a->ptr, a->idx,
+                 (int32_t)a->nbr, (int32_t)a->nbc, mut->tc_plan);
+    }
+    if (mut->tc_desc) return;
+    const int32_t nseg = (int32_t)ceil_div(a->nbc, (int64_t)kSegCols);
+    const int64_t nsg = ngroups * nseg;
+    auto* sbase = dalloc_n<int32_t>(ctx, nsg + 1);
+    auto* bcnt = dalloc_n<int32_t>(ctx, nsg * 32);
+    mut->tc_base = dalloc_n<int32_t>(ctx, ngroups + 1);
+    const int sgrid = stream_grid(ctx, nsg * 32, 256, 1, 8);
+    SFG_LAUNCH(k_bcsr_sched<false>, sgrid, 256, 0, ctx->stream, mut->tc_plan, (int32_t)a->nbr, (int32_t)a->nbc, nseg,
+               panel, panel_a, sbase, bcnt, nullptr);
+    SFG_LAUNCH(k_scan_small, 1, 1024, 0, ctx->stream, sbase, (int32_t)nsg);
+    SFG_LAUNCH(k_sched_first_blocks, stream_grid(ctx, ngroups * 32, 256, 1, 8), 256, 0, ctx->stream, a->ptr,
+               (int32_t)a->nbr, nseg, bcnt);
+    SFG_LAUNCH(k_sched_group_base, (int)ceil_div(ngroups + 1, 256), 256, 0, ctx->stream, sbase, (int32_t)ngroups,
+               nseg, mut->tc_base);
+    int32_t nstages = 0;
+    read_back(ctx, sbase + nsg, sizeof(int32_t), &nstages);
+    mut->tc_desc = dalloc_n<uint32_t>(ctx, (int64_t)nstages * kDescWords);
+    SFG_LAUNCH(k_bcsr_sched<true>, sgrid, 256, 0, ctx->stream, mut->tc_plan, (int32_t)a->nbr, (int32_t)a->nbc, nseg,
+               panel, panel_a, sbase, bcnt, mut->tc_desc);
+    dfree(ctx, sbase);
+    dfree(ctx, bcnt);
+  };
+#ifdef SFG_TC_DEBUG
+  // profiling / ablation switches (ablations skip work: debug builds only)
+  static const int dbg = (std::getenv("SFG_TC_PROF") ? 256 : 0) |
+                         (std::getenv("SFG_TC_ABLATE") ? std::atoi(std::getenv("SFG_TC_ABLATE")) : 0);
+#else
+  constexpr int dbg = 0;
+#endif
+  // 4 producer and 4 MMA warps measured best for bf16 (scripts/gpu_run78.sh:
+  // 0.40 ms at m = 65536; 4/8: 0.39, 4/2: 0.43, 8/4: 0.47, 8/8: 0.47, 2/4:
+  // 0.61; 3/3 over 6 stages of 32 value blocks: 0.46)
+  constexpr int kP = 4, kW = 4;
+  auto run_panel = [&](auto kern, size_t psmem, const CUtensorMap& t_hi, const CUtensorMap& t_lo) {
+    unsigned long long* dbg_out = nullptr;
+    if (dbg) {
+      dbg_out = static_cast<unsigned long long*>(scratch(ctx, 64 * 8));
+      SFG_CUDA(cudaMemsetAsync(dbg_out, 0, 64 * 8, ctx->stream));
+    }
+    // set on every call: a once-only static setup measured 30 % slower
+    // launches (0.61 vs 0.46 ms at m = 65536)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+    SFG_LAUNCH(kern, grid, 32 * (4 + kP + kW), psmem, ctx->stream, t_hi, t_lo, static_cast<const uint8_t*>(a->val),
+               a->ptr, (int32_t)a->nbr, (int32_t)a->m, c, ldc, accumulate ? 1 : 0, mut->tc_base, mut->tc_desc, dbg,
+               dbg_out);
+    if (dbg & 256) {
+      unsigned long long h[64];
+      SFG_CUDA(cudaMemcpyAsync(h, dbg_out, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+      SFG_CUDA(cudaStreamSynchronize(ctx->stream));
+      for (int w = 0; w < 4 + kP + kW; ++w)
+        std::fprintf(stderr, "[tc prof] warp %2d: wait %5.1f%% of %.0f cycles/CTA\n", w,
+                     100.0 * h[2 * w] / (double)(h[2 * w + 1] ? h[2 * w + 1] : 1), h[2 * w + 1] / (double)grid);
+    }
+  };
+  // a dense 16-row x 128-column B tile in one 3-D copy: dims (cols per
+  // 128-byte box, n, boxes), SWIZZLE_128B
+  auto tile_map = [&](CUtensorMap* map, CUtensorMapDataType ty, int esz, const void* base, int64_t ld,
+                      CUtensorMapSwizzle swz) {
+    const int per = 128 / esz;
+    cuuint64_t dims[3] = {(cuuint64_t)per, (cuuint64_t)a->n, (cuuint64_t)(kND / per)};
+    cuuint64_t strides[2] = {(cuuint64_t)ld * esz, 128};
+    cuuint32_t box[3] = {(cuuint32_t)per, kBlk, (cuuint32_t)(kND / per)};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (encode(map, ty, 3, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      raise(SFG_ERR_CUDA, "cuTensorMapEncodeTiled(B tile) failed");
+  };
+
+  if (tf) {
+    // B -> tf32 hi / lo (dense, ld 128), then the 3xTF32 panel kernel
+    build_schedule(PanelCfg<true>::kPanel, PanelCfg<true>::kPanelA);
+    float* bhi = dalloc_n<float>(ctx, a->n * kND);
+    float* blo = dalloc_n<float>(ctx, a->n * kND);
+    SFG_LAUNCH(k_tf32_split, stream_grid(ctx, a->n * (kND / 4), 256, 4, 8), 256, 0, ctx->stream,
+               static_cast<const float*>(b), a->n, ldb, bhi, blo);
+    CUtensorMap thi, tlo;
+    tile_map(&thi, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, bhi, kND, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    tile_map(&tlo, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, blo, kND, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    run_panel(k_bcsr_tc_panel<kP, kW, true>,
+              1024 + PanelCfg<true>::kStages * PanelCfg<true>::kStageBytes + sizeof(PShared<PanelCfg<true>::kStages>) +
+                  64,
+              thi, tlo);
+    dfree(ctx, bhi);
+    dfree(ctx, blo);
+    return true;
+  }
+
   CUtensorMap tb, ta;
   {
     cuuint64_t dims[2] = {(cuuint64_t)nd, (cuuint64_t)a->n};
@@ -1026,16 +1239,7 @@ bool spmm_bcsr_tc(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dt
       raise(SFG_ERR_CUDA, "cuTensorMapEncodeTiled(A) failed");
   }
   CUtensorMap tb3;  // both 64-column halves of a B tile in one copy: dims (64, n, 2)
-  {
-    cuuint64_t dims[3] = {64, (cuuint64_t)a->n, 2};
-    cuuint64_t strides[2] = {(cuuint64_t)ldb * 2, 128};
-    cuuint32_t box[3] = {64, kBlk, 2};
-    cuuint32_t es[3] = {1, 1, 1};
-    if (encode(&tb3, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(b), dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      raise(SFG_ERR_CUDA, "cuTensorMapEncodeTiled(B, 3-D) failed");
-  }
+  tile_map(&tb3, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, b, ldb, CU_TENSOR_MAP_SWIZZLE_128B);
   const size_t smem = 1024 + kStages * kStageBytes + sizeof(Shared) + 64;
   const size_t gsmem = 1024 + kGStages * kGStageBytes + sizeof(GShared) + 64;
   static const bool per_row = [] {
@@ -1045,91 +1249,23 @@ bool spmm_bcsr_tc(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dt
   if (per_row) {
     // the attribute is per device: set on every call (a few host microseconds)
     SFG_CUDA(cudaFuncSetAttribute(k_bcsr_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int grid = (int)std::min<int64_t>(a->nbr, (int64_t)ctx->sms);
-    SFG_LAUNCH(k_bcsr_tc, grid, kThreads, smem, ctx->stream, tb, ta, a->ptr, a->idx, (int32_t)a->nbr,
-               (int32_t)a->m, c, ldc, accumulate ? 1 : 0);
+    SFG_LAUNCH(k_bcsr_tc, (int)std::min<int64_t>(a->nbr, (int64_t)ctx->sms), kThreads, smem, ctx->stream, tb, ta,
+               a->ptr, a->idx, (int32_t)a->nbr, (int32_t)a->m, c, ldc, accumulate ? 1 : 0);
+    return true;
+  }
+  if (plan_ok) build_schedule(PanelCfg<false>::kPanel, PanelCfg<false>::kPanelA);
+  if (mut->tc_desc) {
+    run_panel(k_bcsr_tc_panel<kP, kW, false>,
+              1024 + PanelCfg<false>::kStages * PanelCfg<false>::kStageBytes +
+                  sizeof(PShared<PanelCfg<false>::kStages>) + 64,
+              tb3, tb3);
   } else {
-    // The mask plan (per 32-block-row group, per block column) is built once
-    // per matrix and cached on the tensor; it is used when the group masks
-    // are dense enough that streaming them beats the in-kernel merge.
-    const int64_t ngroups = ceil_div(a->nbr, kGroup);
-    const int64_t words = ngroups * a->nbc;
-    sfg_tensor* mut = const_cast<sfg_tensor*>(a);  // plan is a cache, not tensor state
-    if (!mut->tc_plan && a->nnz * 4 >= words && words <= (int64_t(1) << 30)) {
-      mut->tc_plan = dalloc_n<uint32_t>(ctx, words);
-      SFG_CUDA(cudaMemsetAsync(mut->tc_plan, 0, words * 4, ctx->stream));
-      SFG_LAUNCH(k_bcsr_plan, stream_grid(ctx, a->nbr * 32, 256, 1, 8), 256, 0, ctx->stream, a->ptr, a->idx,
-                 (int32_t)a->nbr, (int32_t)a->nbc, mut->tc_plan);
-    }
-    int grid = (int)std::min<int64_t>(ngroups, (int64_t)ctx->sms);
-    if (mut->tc_plan && !mut->tc_desc) {
-      // stage schedule: count, scan, write (once per matrix, cached); a
-      // warp per (group, segment of kSegCols block columns)
-      const int32_t nseg = (int32_t)ceil_div(a->nbc, (int64_t)kSegCols);
-      const int64_t nsg = ngroups * nseg;
-      auto* sbase = dalloc_n<int32_t>(ctx, nsg + 1);
-      auto* bcnt = dalloc_n<int32_t>(ctx, nsg * 32);
-      mut->tc_base = dalloc_n<int32_t>(ctx, ngroups + 1);
-      const int sgrid = stream_grid(ctx, nsg * 32, 256, 1, 8);
-      SFG_LAUNCH(k_bcsr_sched<false>, sgrid, 256, 0, ctx->stream, mut->tc_plan, (int32_t)a->nbr, (int32_t)a->nbc,
-                 nseg, sbase, bcnt, nullptr);
-      SFG_LAUNCH(k_scan_small, 1, 1024, 0, ctx->stream, sbase, (int32_t)nsg);
-      SFG_LAUNCH(k_sched_first_blocks, stream_grid(ctx, ngroups * 32, 256, 1, 8), 256, 0, ctx->stream, a->ptr,
-                 (int32_t)a->nbr, nseg, bcnt);
-      SFG_LAUNCH(k_sched_group_base, (int)ceil_div(ngroups + 1, 256), 256, 0, ctx->stream, sbase, (int32_t)ngroups,
-                 nseg, mut->tc_base);
-      int32_t nstages = 0;
-      read_back(ctx, sbase + nsg, sizeof(int32_t), &nstages);
-      mut->tc_desc = dalloc_n<uint32_t>(ctx, (int64_t)nstages * kDescWords);
-      SFG_LAUNCH(k_bcsr_sched<true>, sgrid, 256, 0, ctx->stream, mut->tc_plan, (int32_t)a->nbr, (int32_t)a->nbc, nseg,
-                 sbase, bcnt, mut->tc_desc);
-      dfree(ctx, sbase);
-      dfree(ctx, bcnt);
-    }
-    if (mut->tc_desc) {
-      // 4 producer and 4 MMA warps over 8 stages measured best
-      // (scripts/gpu_run78.sh: 0.40 ms at m = 65536; 4/8: 0.39, 4/2: 0.43,
-      // 8/4: 0.47, 8/8: 0.47, 2/4: 0.61; 3/3 over 6 stages of 32 value
-      // blocks: 0.46)
-      constexpr int kP = 4, kW = 4;
-      const size_t psmem = 1024 + kPStages * kPStageBytes + sizeof(PShared) + 64;
-#ifdef SFG_TC_DEBUG
-      // profiling / ablation switches (ablations skip work: debug builds only)
-      static const int dbg = (std::getenv("SFG_TC_PROF") ? 256 : 0) |
-                             (std::getenv("SFG_TC_ABLATE") ? std::atoi(std::getenv("SFG_TC_ABLATE")) : 0);
-#else
-      constexpr int dbg = 0;
-#endif
-      unsigned long long* dbg_out = nullptr;
-      if (dbg) {
-        dbg_out = static_cast<unsigned long long*>(scratch(ctx, 64 * 8));
-        SFG_CUDA(cudaMemsetAsync(dbg_out, 0, 64 * 8, ctx->stream));
-      }
-      auto go = [&](auto kern, int threads) {
-        // set on every call: a once-only static setup measured 30 % slower
-        // launches (0.61 vs 0.46 ms at m = 65536)
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
-        SFG_LAUNCH(kern, grid, threads, psmem, ctx->stream, tb3, static_cast<const uint8_t*>(a->val), a->ptr,
-                   (int32_t)a->nbr, (int32_t)a->m, c, ldc, accumulate ? 1 : 0, mut->tc_base, mut->tc_desc, dbg,
-                   dbg_out);
-      };
-      go(k_bcsr_tc_panel<kP, kW>, 32 * (4 + kP + kW));
-      if (dbg & 256) {
-        unsigned long long h[64];
-        SFG_CUDA(cudaMemcpyAsync(h, dbg_out, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
-        SFG_CUDA(cudaStreamSynchronize(ctx->stream));
-        for (int w = 0; w < 4 + kP + kW; ++w)
-          std::fprintf(stderr, "[tc prof] warp %2d: wait %5.1f%% of %.0f cycles/CTA\n", w,
-                       100.0 * h[2 * w] / (double)(h[2 * w + 1] ? h[2 * w + 1] : 1), h[2 * w + 1] / (double)grid);
-      }
-    } else {
-      // set on every call: a once-only static setup measured 30 % slower
-      // launches of the panel kernel (0.61 vs 0.46 ms at m = 65536)
-      cudaFuncSetAttribute(k_bcsr_tc_group<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem);
-      SFG_LAUNCH((k_bcsr_tc_group<2, 2>), grid, 32 * 8, gsmem, ctx->stream, tb3,
-                 static_cast<const uint8_t*>(a->val), a->ptr, a->idx, (int32_t)a->nbr, (int32_t)a->m, c, ldc,
-                 accumulate ? 1 : 0, mut->tc_plan, (int32_t)a->nbc);
-    }
+    // set on every call: a once-only static setup measured 30 % slower
+    // launches of the panel kernel (0.61 vs 0.46 ms at m = 65536)
+    cudaFuncSetAttribute(k_bcsr_tc_group<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem);
+    SFG_LAUNCH((k_bcsr_tc_group<2, 2>), grid, 32 * 8, gsmem, ctx->stream, tb3, static_cast<const uint8_t*>(a->val),
+               a->ptr, a->idx, (int32_t)a->nbr, (int32_t)a->m, c, ldc, accumulate ? 1 : 0, mut->tc_plan,
+               (int32_t)a->nbc);
   }
   return true;
 }

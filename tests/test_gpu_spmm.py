@@ -124,6 +124,40 @@ def test_bcsr16_bf16_tensor_core(ctx, port, shape, density):
     check(cd, cr, abs_bound(rows, cols, vals, m, b64), ("bcsr-tc", shape, density))
 
 
+@pytest.mark.parametrize("shape", [(256, 256), (250, 200), (1000, 3000), (4096, 512)])
+@pytest.mark.parametrize("density", [0.02, 0.3, 0.9])
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_bcsr16_fp32_tensor_core(ctx, port, shape, density, accumulate):
+    """BCSR(16,16) with fp32 values and fp32 B, nd = 128: the 3xTF32 tcgen05
+    path (bcsr_tc.cu, kind::tf32 hi.hi + lo.hi + hi.lo) held to the fp32
+    tolerance against the f64 oracle on full-mantissa operands."""
+    m, n = shape
+    rng = np.random.default_rng(m * 7 + n)
+    nbr, nbc = (m + 15) // 16, (n + 15) // 16
+    mask = rng.random((nbr, nbc)) < density
+    mask[nbr // 2] = False  # an empty block row
+    br, bc = np.nonzero(mask)
+    ii, jj = np.meshgrid(np.arange(16), np.arange(16), indexing="ij")
+    rows = (br[:, None] * 16 + ii.ravel()[None, :]).ravel()
+    cols = (bc[:, None] * 16 + jj.ravel()[None, :]).ravel()
+    keep = (rows < m) & (cols < n) & (rng.random(rows.size) < 0.95)  # some zeros inside blocks
+    rows, cols = rows[keep], cols[keep]
+    vals = ((rng.random(rows.size) * 2 - 1) * np.exp2(rng.integers(-6, 6, rows.size))).astype(np.float32)
+    b = ((rng.random((n, 128)) * 2 - 1) * np.exp2(rng.integers(-4, 4, (n, 128)))).astype(np.float32)
+    d = ctx.convert(ctx.from_coo(m, n, rows, cols, vals.astype(np.float64)), "BCSR(16,16)")
+    c0 = (rng.random((m, 128)) * 2 - 1).astype(np.float32)
+    cbuf = ctx.buffer(c0.nbytes).upload(c0)
+    bbuf = ctx.buffer(b.nbytes).upload(b)
+    ctx.spmm_device(d, bbuf.ptr, sfg.F32, 128, cbuf.ptr, accumulate=accumulate)
+    cd = cbuf.download(np.float32, m * 128).reshape(m, 128)
+    p = port.from_coo(m, n, rows, cols, vals.astype(np.float64))
+    cr = port.spmm(port.convert(p, "BCSR", 16, 16), b.astype(np.float64))
+    if accumulate:
+        cr = cr + c0.astype(np.float64)
+    bound = abs_bound(rows, cols, vals.astype(np.float64), m, b.astype(np.float64)) + np.abs(c0) * accumulate
+    check(cd, cr, bound, ("bcsr-tf32", shape, density, accumulate))
+
+
 @pytest.mark.parametrize("accumulate", [False, True])
 def test_spmm_csr_heavy_and_empty_rows(ctx, port, accumulate):
     """CSR SpMM is load balanced over (rows + entries): one row far longer

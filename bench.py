@@ -213,7 +213,7 @@ class Cfg4(Workload):
 
     def describe(self):
         return (f"BCSR({self.block},{self.block}) {self.vdtype} SpMM N=128"
-                f"{(' (tcgen05)' if self.vdtype == 'bf16' else ' (tcgen05 3xTF32)') if self.block == 16 else ' (CUDA cores)'}, "
+                f"{' (tcgen05)' if self.vdtype == 'bf16' else (' (tcgen05 3xTF32)' if self.block == 16 else ' (CUDA cores)')}, "
                 "block-sparse 512K x 512K, 10% block density, generated as BCSR")
 
     def setup(self, torch):
@@ -253,7 +253,8 @@ class Cfg4(Workload):
         nb, m, n, nd, r = self.nblocks, self.m, self.n, self.nd, self.block
         s = 2 if self.vdtype == "bf16" else 4
         byts = nb * r * r * s + 4 * nb + 4 * (m // r + 1) + s * n * nd + 4 * m * nd
-        return [("spmm_bcsr_tc" if r == 16 else "spmm_bcsr", self.step, byts, 2 * self.nnz * nd)]
+        tc = r == 16 or self.vdtype == "bf16"
+        return [("spmm_bcsr_tc" if tc else "spmm_bcsr", self.step, byts, 2 * self.nnz * nd)]
 
 
 class Cfg5(SpmvWorkload):
@@ -488,7 +489,9 @@ def run_ours(args):
         k["hbm_frac_nominal"] = round(k["GB/s"] / NOMINAL_HBM_GBS, 4)
     # DRAM bytes per launch of the dominant family, from the committed ncu
     # launch list of this config (profiles/traffic_config<N>.json)
-    tpath = os.path.join(ROOT, "profiles", f"traffic_config{args.config}.json")
+    variant = "" if args.config != 4 or (args.block, args.bcsr_dtype) == (16, "bf16") else \
+        f"_{args.block}x{args.block}_{args.bcsr_dtype}"  # the config-4 file is the 16x16 bf16 launch list
+    tpath = os.path.join(ROOT, "profiles", f"traffic_config{args.config}{variant}.json")
     if os.path.exists(tpath):
         try:
             fam = json.load(open(tpath))["families"].get(dom)

@@ -1084,6 +1084,294 @@ __global__ void __launch_bounds__(256) k_bcsr_plan(const int32_t* __restrict__ p
   }
 }
 
+// ------------------------------------------------------------------------
+// BCSR(4,4) bf16 SpMM on tcgen05. A 4 x 4 block is far below an MMA tile, so
+// the MMA covers a 128-row x 16-column window of A: N = 128 (the 32 block
+// rows of a group), K = 16 (a "super column" of 4 block columns), M = 128
+// (nd):  D[nd][128 rows] += B[16 sc .. 16 sc + 15][nd]^T . A_window^T.
+// The A operand is the same 16-row B tile as the 16x16 kernel (one TMA);
+// the B operand is the window's values, K-major with 32-byte swizzle, built
+// in shared memory by the producer warp: lane j owns block row 32 g + j, i.e.
+// window rows 4j .. 4j + 3, and writes them whole (its blocks of the super
+// column in place, zeros elsewhere), so no separate zero fill is needed.
+// Super columns without any block of the group are skipped (warp min of
+// the lanes' next block columns). At 10 % block density a window holds
+// ~13 of its 128 block slots; the MMA reads 8 KB of shared memory for them
+// (4 KB tile + 4 KB window), against 4.5 KB per 16 x 16 block.
+// A CTA runs kQPipes independent pipelines (producer warp, MMA warp, ring of
+// kQStages stages, a 128-column TMEM accumulator), each on its own groups;
+// the 4 epilogue warps drain them in turn.
+constexpr int kQPipes = 4;
+constexpr int kQStages = 5;
+constexpr int kQTile = kTileBytes;  // 4 KB: 16 B rows x 128 columns
+constexpr int kQVal = 128 * 32;     // 4 KB: 128 window rows x 16 K bf16
+constexpr int kQStageBytes = kQTile + kQVal;
+// F32 accumulate, BF16 x BF16, A MN-major, B K-major, N = 128, M = 128
+constexpr uint32_t kQIdesc =
+    (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(kND >> 4) << 24);
+
+struct QShared {
+  uint64_t full[kQPipes][kQStages];
+  uint64_t empty[kQPipes][kQStages];
+  uint64_t acc_full[kQPipes];
+  uint64_t acc_empty[kQPipes];
+  uint32_t end[kQPipes][kQStages];  // 1: the stage is a group's end marker
+  alignas(16) uint32_t ring_col[kQPipes][32][12];     // per producer lane: block columns of three quads
+  alignas(16) uint8_t ring_val[kQPipes][32][12 * 32 + 16];  // and their value blocks (+16: lanes on distinct banks)
+  uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(32 * (4 + 2 * kQPipes), 1)
+    k_bcsr4_tc(const __grid_constant__ CUtensorMap tmap_b, const uint8_t* __restrict__ aval,
+               const int32_t* __restrict__ ptr, const int32_t* __restrict__ bcol, int64_t nnz, int32_t nbr,
+               int32_t m, float* __restrict__ c, int64_t ldc, int accumulate) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* stages = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  QShared* sh = reinterpret_cast<QShared*>(stages + kQPipes * kQStages * kQStageBytes);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t ngroups = (nbr + kGroup - 1) / kGroup;
+  constexpr int kMmaWarp = 4 + kQPipes;
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < kQPipes; ++w) {
+      for (int s = 0; s < kQStages; ++s) {
+        mbar_init(&sh->full[w][s], 1);   // producer lane 0 (plus the tile's bytes)
+        mbar_init(&sh->empty[w][s], 1);  // the MMA warp's commit
+      }
+      mbar_init(&sh->acc_full[w], 1);
+      mbar_init(&sh->acc_empty[w], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sh->tmem_base)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sh->tmem_base;
+  auto group_of = [&](int k, int w) { return (int32_t)blockIdx.x + (k * kQPipes + w) * (int32_t)gridDim.x; };
+
+  if (warp >= 4 && warp < kMmaWarp) {
+    // ---------------------------------------------------------- producers
+    // Lane j walks block row 32 g + j through a ring of three aligned quads
+    // of blocks (block columns + 32 value bytes each) in shared memory,
+    // refilled by cp.async a quad at a time: when the walk enters quad Q the
+    // vacated slot is refilled with Q + 2 and the lane waits for Q + 1, so
+    // the current and the next quad are always resident — a stage reads the
+    // lane's next four blocks at once, with no loop and no load latency
+    // (register look-ahead stalls instead: shifting a register whose load is
+    // in flight waits for it). An L2 prefetch runs 64 blocks ahead. The lane
+    // zeroes its four window rows, then copies its blocks of the super
+    // column into them.
+    const int w = warp - 4;
+    int stage = 0;
+    uint32_t phase = 0;
+    constexpr uint32_t kNone = 0xffffffffu;
+    const uint32_t sw = (uint32_t)lane & 1u;  // 32-byte swizzle: chunk ^= (row >> 2) & 1, row >> 2 = lane
+    const uint32_t rcol = smem_u32(&sh->ring_col[w][lane][0]);
+    const uint32_t rval = smem_u32(&sh->ring_val[w][lane][0]);
+    for (int k = 0;; ++k) {
+      const int32_t g = group_of(k, w);
+      if (g >= ngroups) break;
+      const int32_t br = g * kGroup + lane;
+      int64_t cur = 0, end = 0;
+      if (br < nbr) {
+        cur = __ldg(ptr + br);
+        end = __ldg(ptr + br + 1);
+      }
+      auto slot = [](int64_t i) {  // ring entry of block i (32-bit modulo: block indices < 2^31)
+        return ((((uint32_t)(i >> 2)) % 3u) << 2) | (uint32_t)(i & 3);
+      };
+      // quad q0 (blocks q0 .. q0 + 3, q0 % 4 == 0): one cp.async group
+      auto refill = [&](int64_t q0) {
+        if (q0 < end) {
+          const uint32_t s0 = slot(q0);
+          const int64_t nc = nnz - q0 < 4 ? nnz - q0 : 4;  // entries of the column array left
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(rcol + s0 * 4), "l"(bcol + q0),
+                       "r"((int)nc * 4)
+                       : "memory");
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const bool in = q0 + e < nnz;
+            const uint8_t* src = aval + (in ? (q0 + e) * 32 : 0);
+            const uint32_t dst = rval + (s0 + e) * 32;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(in ? 16 : 0)
+                         : "memory");
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst + 16), "l"(src + 16),
+                         "r"(in ? 16 : 0)
+                         : "memory");
+          }
+          if (q0 + 64 < end) asm volatile("prefetch.global.L2 [%0];" ::"l"(aval + (q0 + 64) * 32));
+          if (((q0 + 64) & 31) == 0 && q0 + 64 < end) asm volatile("prefetch.global.L2 [%0];" ::"l"(bcol + q0 + 64));
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      };
+      for (int64_t i = cur & ~int64_t(3); i < cur + 64 && i < end; i += 4)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(aval + i * 32));
+      const int64_t qb = cur & ~int64_t(3);
+      refill(qb);
+      refill(qb + 4);
+      refill(qb + 8);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      auto col_of = [&](int64_t i) -> uint32_t {
+        if (i >= end) return kNone;
+        uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(rcol + slot(i) * 4));
+        return v;
+      };
+      uint32_t nb = col_of(cur);
+      while (true) {
+        const uint32_t mn = __reduce_min_sync(kFull, nb);
+        if (mn == kNone) break;
+        const uint32_t sc = mn >> 2;
+        if (lane == 0) mbar_wait(&sh->empty[w][stage], phase ^ 1);
+        __syncwarp();
+        uint8_t* st = stages + (w * kQStages + stage) * kQStageBytes;
+        if (lane == 0) {
+          sh->end[w][stage] = 0;
+          mbar_expect_tx_only(&sh->full[w][stage], kQTile);
+          tma_3d(st, &tmap_b, &sh->full[w][stage], 0, (int)sc * kBlk, 0);
+        }
+        // the lane's window rows 4 lane .. 4 lane + 3: zero, then its blocks
+        const uint32_t vb = smem_u32(st + kQTile) + (uint32_t)lane * 128u;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)  // rotated by lane: 8 consecutive lanes hit 8 different bank groups
+          sts_v4(vb + (((uint32_t)(i + lane) & 7u) << 4), make_uint4(0u, 0u, 0u, 0u));
+        uint32_t c[4];
+        c[0] = nb;
+#pragma unroll
+        for (int e = 1; e < 4; ++e) c[e] = col_of(cur + e);
+        int taken = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if ((c[e] >> 2) == sc) {  // columns ascend: the taken blocks are a prefix
+            const uint32_t q = c[e] & 3u;
+            const uint32_t src = rval + slot(cur + e) * 32;
+            const uint4 lo = lds_v4(src), hi = lds_v4(src + 16);
+            // block column q: bytes 8q .. 8q + 7 of each row (chunk q / 2)
+            const uint32_t off = (((q >> 1) ^ sw) << 4) + ((q & 1u) << 3);
+            asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(vb + off), "r"(lo.x), "r"(lo.y) : "memory");
+            asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(vb + 32 + off), "r"(lo.z), "r"(lo.w) : "memory");
+            asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(vb + 64 + off), "r"(hi.x), "r"(hi.y) : "memory");
+            asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(vb + 96 + off), "r"(hi.z), "r"(hi.w) : "memory");
+            ++taken;
+          }
+        }
+        if (taken) {
+          const int64_t q_old = cur >> 2;
+          cur += taken;
+          if ((cur >> 2) != q_old) {  // entered the next quad: refill the vacated slot, wait for the one after
+            refill(((cur >> 2) + 2) * 4);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+          }
+          nb = col_of(cur);
+        }
+        __syncwarp();
+        // the MMA warp fences (generic -> async proxy) after the barrier
+        if (lane == 0) mbar_arrive(&sh->full[w][stage]);
+        if (++stage == kQStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      asm volatile("cp.async.wait_group 0;" ::: "memory");  // the ring is rewritten by the next group
+      // end-of-group marker
+      if (lane == 0) {
+        mbar_wait(&sh->empty[w][stage], phase ^ 1);
+        sh->end[w][stage] = 1;
+        mbar_arrive(&sh->full[w][stage]);
+      }
+      __syncwarp();
+      if (++stage == kQStages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  } else if (warp >= kMmaWarp) {
+    // ------------------------------------------------------- MMA issuers
+    const int w = warp - kMmaWarp;
+
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int k = 0;; ++k) {
+      const int32_t g = group_of(k, w);
+      if (g >= ngroups) break;
+      mbar_wait(&sh->acc_empty[w], (k & 1) ^ 1);
+      tc_fence_after();
+      uint32_t acc_on = 0;  // the group's first MMA overwrites the accumulator
+      while (true) {
+        mbar_wait(&sh->full[w][stage], phase);
+        tc_fence_after();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // producer st.shared -> MMA reads
+        uint32_t endm;  // explicit shared load (a volatile generic load compiles to a slow system-scope one)
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(endm) : "r"(smem_u32(&sh->end[w][stage])));
+        if (!endm) {
+          const uint32_t base = smem_u32(stages + (w * kQStages + stage) * kQStageBytes);
+          tc_mma_elect(tmem + w * 128, smem_desc(base, 2048, 1024, 2), smem_desc(base + kQTile, 16, 256, 6), kQIdesc,
+                       acc_on);
+          acc_on = 1;
+        }
+        tc_commit_elect(&sh->empty[w][stage]);
+        __syncwarp();
+        if (++stage == kQStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+        if (endm) break;
+      }
+      tc_commit_elect(&sh->acc_full[w]);
+      __syncwarp();
+    }
+  } else {
+    // ---------------------------------------------------------- epilogue
+    const int col = warp * 32 + lane;
+    const uint32_t lanes = (uint32_t)(warp * 32) << 16;
+    for (int k = 0;; ++k) {
+      bool done = false;
+      for (int w = 0; w < kQPipes; ++w) {
+        const int32_t g = group_of(k, w);
+        if (g >= ngroups) {
+          done = true;
+          break;
+        }
+        mbar_wait(&sh->acc_full[w], k & 1);
+        tc_fence_after();
+        const int32_t b_lo = g * kGroup, b_hi = min(b_lo + kGroup, nbr);
+        const bool any = __ldg(ptr + b_lo) < __ldg(ptr + b_hi);  // else no MMA ran: the rows are zero
+        for (int n0 = 0; n0 < 128; n0 += 16) {
+          float v[16];
+          if (any) {
+            tc_ld16(tmem + lanes + w * 128 + n0, v);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = 0.f;
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int64_t row = (int64_t)g * 128 + n0 + i;
+            if (row < m) {
+              float* p = c + row * ldc + col;
+              *p = accumulate ? *p + v[i] : v[i];
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sh->acc_empty[w]);
+      }
+      if (done) break;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -1106,14 +1394,16 @@ bool spmm_bcsr_tc(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dt
   const bool tf = a->dtype == SFG_F32 && b_dtype == SFG_F32;
   const bool bf = a->dtype == SFG_BF16 && b_dtype == SFG_BF16;
   if (a->kind != SFG_BCSR || !(tf || bf) || nd != kND) return false;
-  if (a->br != kBlk || a->bc != kBlk || a->rb != kBlk || a->cb != kBlk) return false;
+  const bool quad = bf && a->br == 4 && a->bc == 4 && a->rb == 4 && a->cb == 4;  // BCSR(4,4): 128-row windows
+  if (!quad && (a->br != kBlk || a->bc != kBlk || a->rb != kBlk || a->cb != kBlk)) return false;
   if (reinterpret_cast<uintptr_t>(b) & 15 || a->nnz == 0) return false;
   if (bf ? (ldb * 2) % 16 != 0 : ldb % 4 != 0) return false;
-  if (a->nbr > INT32_MAX || a->nnz * kBlk > INT32_MAX) return false;
+  if (a->nbr > INT32_MAX || a->nnz > INT32_MAX || (!quad && a->nnz * kBlk > INT32_MAX)) return false;
   const int64_t ngroups = ceil_div(a->nbr, kGroup);
   const int64_t words = ngroups * a->nbc;
   const bool plan_ok = a->nnz * 4 >= words && words <= (int64_t(1) << 30);
   if (tf && !plan_ok) return false;
+  if (quad && a->nbr > (int64_t)INT32_MAX - kGroup) return false;
   auto encode = get_encode();
   if (!encode) return false;
   sfg_tensor* mut = const_cast<sfg_tensor*>(a);  // plan and schedule are caches, not tensor state
@@ -1217,6 +1507,15 @@ bool spmm_bcsr_tc(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dt
     return true;
   }
 
+  if (quad) {
+    CUtensorMap tq;
+    tile_map(&tq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, b, ldb, CU_TENSOR_MAP_SWIZZLE_128B);
+    const size_t qsmem = 1024 + (size_t)kQPipes * kQStages * kQStageBytes + sizeof(QShared) + 64;
+    cudaFuncSetAttribute(k_bcsr4_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsmem);
+    SFG_LAUNCH(k_bcsr4_tc, grid, 32 * (4 + 2 * kQPipes), qsmem, ctx->stream, tq, static_cast<const uint8_t*>(a->val),
+               a->ptr, a->idx, a->nnz, (int32_t)a->nbr, (int32_t)a->m, c, ldc, accumulate ? 1 : 0);
+    return true;
+  }
   CUtensorMap tb, ta;
   {
     cuuint64_t dims[2] = {(cuuint64_t)nd, (cuuint64_t)a->n};

@@ -124,6 +124,42 @@ def test_bcsr16_bf16_tensor_core(ctx, port, shape, density):
     check(cd, cr, abs_bound(rows, cols, vals, m, b64), ("bcsr-tc", shape, density))
 
 
+@pytest.mark.parametrize("shape", [(256, 256), (250, 202), (9, 40), (1000, 3000), (4100, 520)])
+@pytest.mark.parametrize("density", [0.01, 0.1, 0.9])
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_bcsr4_bf16_tensor_core(ctx, port, shape, density, accumulate):
+    """BCSR(4,4) with bf16 values and bf16 B, nd = 128: the tcgen05 path over
+    128-row x 16-column windows (bcsr_tc.cu k_bcsr4_tc). The oracle runs on
+    the bf16-rounded values and B."""
+    m, n = shape
+    rng = np.random.default_rng(m * 3 + n)
+    nbr, nbc = (m + 3) // 4, (n + 3) // 4
+    mask = rng.random((nbr, nbc)) < density
+    mask[nbr // 2] = False  # an empty block row
+    if nbr > 64:
+        mask[32:64] = False  # an empty 32-block-row group
+    br, bc = np.nonzero(mask)
+    ii, jj = np.meshgrid(np.arange(4), np.arange(4), indexing="ij")
+    rows = (br[:, None] * 4 + ii.ravel()[None, :]).ravel()
+    cols = (bc[:, None] * 4 + jj.ravel()[None, :]).ravel()
+    keep = (rows < m) & (cols < n) & (rng.random(rows.size) < 0.9)
+    rows, cols = rows[keep], cols[keep]
+    vals = bf16_round((rng.random(rows.size) * 2 - 1) * np.exp2(rng.integers(-3, 3, rows.size)))
+    b = (rng.random((n, 128)) * 2 - 1).astype(np.float32)
+    bb = to_bf16_bits(b)
+    d = ctx.convert(ctx.from_coo(m, n, rows, cols, vals), "BCSR(4,4)", value_dtype=sfg.BF16)
+    c0 = (rng.random((m, 128)) * 2 - 1).astype(np.float32)
+    cbuf = ctx.buffer(c0.nbytes).upload(c0)
+    bbuf = ctx.buffer(bb.nbytes).upload(bb)
+    ctx.spmm_device(d, bbuf.ptr, sfg.BF16, 128, cbuf.ptr, accumulate=accumulate)
+    cd = cbuf.download(np.float32, m * 128).reshape(m, 128)
+    b64 = bits_to_f64(bb)
+    cr = port.spmm(port.convert(port.from_coo(m, n, rows, cols, vals), "BCSR", 4, 4), b64)
+    if accumulate:
+        cr = cr + c0.astype(np.float64)
+    check(cd, cr, abs_bound(rows, cols, vals, m, b64) + np.abs(c0) * accumulate, ("bcsr4-tc", shape, density))
+
+
 @pytest.mark.parametrize("shape", [(256, 256), (250, 200), (1000, 3000), (4096, 512)])
 @pytest.mark.parametrize("density", [0.02, 0.3, 0.9])
 @pytest.mark.parametrize("accumulate", [False, True])

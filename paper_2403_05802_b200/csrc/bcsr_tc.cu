@@ -660,7 +660,7 @@ __device__ __forceinline__ void tmem_zero16(uint32_t taddr) {
 template <int kProducers, int kMmaWarps, bool kTF>
 __global__ void __launch_bounds__(32 * (4 + kProducers + kMmaWarps), 1)
     k_bcsr_tc_panel(const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_lo,
-                    const uint8_t* __restrict__ aval,
+                    const __grid_constant__ CUtensorMap tmap_v, const uint8_t* __restrict__ aval,
                     const int32_t* __restrict__ ptr, int32_t nbr, int32_t m, float* __restrict__ c, int64_t ldc,
                     int accumulate, const int32_t* __restrict__ sbase, const uint32_t* __restrict__ sdesc,
                     int dbg, unsigned long long* __restrict__ dbg_out) {
@@ -683,14 +683,14 @@ __global__ void __launch_bounds__(32 * (4 + kProducers + kMmaWarps), 1)
   const int32_t ngroups = (nbr + kGroup - 1) / kGroup;
   constexpr int kMmaWarp = 4 + kProducers;
   // A parity wait is exact only if the stage's previous use (one ring round
-  // earlier) has already been waited on by the same warp: role counts must
-  // divide the ring size.
-  static_assert(kPStages % kProducers == 0 && kPStages % kMmaWarps == 0, "roles must divide the ring");
+  // earlier) has already been waited on by the same warp: the producer count
+  // must divide the ring size (every MMA warp visits every stage).
+  static_assert(kPStages % kProducers == 0, "producers must divide the ring");
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kPStages; ++s) {
-      mbar_init(&sh->full[s], 1);   // the stage's producer arrives once
-      mbar_init(&sh->empty[s], 1);  // the stage's MMA warp commits once
+      mbar_init(&sh->full[s], 1);           // the stage's producer arrives once
+      mbar_init(&sh->empty[s], kMmaWarps);  // every MMA warp commits once
     }
     mbar_init(&sh->acc_full, kMmaWarps);  // every MMA warp commits once per group
     mbar_init(&sh->acc_empty, 4);
@@ -747,8 +747,6 @@ __global__ void __launch_bounds__(32 * (4 + kProducers + kMmaWarps), 1)
     // load two positions ahead, so no global latency sits between a free
     // stage and its copies.
     const int q = warp - 4;
-    const int r = lane >> 1, ch = lane & 1;
-    const uint32_t dst_off = r * 32 + ((ch ^ ((r >> 2) & 1)) << 4);
     auto load = [&](const Pos& p, uint32_t& w0) {
       w0 = 0u;
       if (p.g < ngroups && p.i < p.ns) w0 = __ldg(sdesc + (int64_t)(p.s0 + p.i) * kDescWords + lane);
@@ -791,27 +789,21 @@ __global__ void __launch_bounds__(32 * (4 + kProducers + kMmaWarps), 1)
             }
           }
         }
-        __syncwarp();  // reconverge: the shuffles below must not take the divergent path
-        for (int sl = 0; sl < ((dbg & 4) ? 0 : nblk); ++sl) {
-          const int32_t kb = (int32_t)__shfl_sync(kFull, c0, 16 + sl);
-          if constexpr (kTF) {
-            // 1 KB fp32 block, row-major 16 x 16: 16-byte chunk q = row i,
-            // chunk cq of the row -> K half cq / 2, 32-byte-swizzled
-            // K-major (chunk cq % 2 of row i at chunk (cq % 2) ^ (i >> 2 & 1))
-#pragma unroll
-            for (int t = 0; t < 2; ++t) {
-              const int qq = lane + 32 * t, i = qq >> 2, cq = qq & 3;
-              const uint32_t off = (cq >> 1) * 512 + i * 32 + (((cq & 1) ^ ((i >> 2) & 1)) << 4);
-              cp_async16(st + Cfg::kVal + sl * Cfg::kA + off, aval + (int64_t)kb * Cfg::kA + qq * 16);
-            }
-          } else {
-            cp_async16(st + Cfg::kVal + sl * Cfg::kA + dst_off, aval + (int64_t)kb * Cfg::kA + lane * 16);
-          }
+        // value blocks: one TMA each (the lane holding the slot's block
+        // index), written in the 32-byte-swizzled K-major layout (tf32: a
+        // 3-D box puts the two K halves of 8 one after the other)
+        if (lane == 0 && !(dbg & 4)) mbar_expect_tx_only(&sh->full[stage], nblk * Cfg::kA);
+        __syncwarp();
+        if (lane >= 16 && lane < 16 + nblk && !(dbg & 4)) {
+          const int sl = lane - 16;
+          if constexpr (kTF)
+            tma_3d(st + Cfg::kVal + sl * Cfg::kA, &tmap_v, &sh->full[stage], 0, (int)c0 * kBlk, 0);
+          else
+            tma_2d(st + Cfg::kVal + sl * Cfg::kA, &tmap_v, &sh->full[stage], 0, (int)c0 * kBlk);
         }
       } else if (lane < 4) {
         sts_u32(smem_u32(&sh->mask[stage][lane]), 0u);  // end-of-group marker
       }
-      cp_async_mbar_arrive(&sh->full[stage]);
       __syncwarp();
       if (lane == 0) mbar_arrive(&sh->full[stage]);
       cur = n1;
@@ -821,9 +813,11 @@ __global__ void __launch_bounds__(32 * (4 + kProducers + kMmaWarps), 1)
     }
   } else if (warp >= kMmaWarp) {
     // ------------------------------------------------------- MMA issuers
-    // Per stage the lanes fetch slot s = lane's (block row, tile) byte in
-    // parallel; the issue loop broadcasts one byte per MMA (the next one is
-    // fetched while the current MMA issues).
+    // Every MMA warp walks every stage and issues the MMAs of its own block
+    // rows (j % kMmaWarps == w): an accumulator's MMAs come from one warp in
+    // ring order, so the fp32 accumulation order — and C — is the same on
+    // every run. Per stage the lanes fetch slot s = lane's (block row, tile)
+    // byte in parallel; the issue loop broadcasts one byte per slot.
     const int w = warp - kMmaWarp;
     const uint32_t base0 = smem_u32(stages);
     // A (the B tiles), MN-major: bf16 SW128 (8-row K groups, SBO 1 KB);
@@ -837,39 +831,43 @@ __global__ void __launch_bounds__(32 * (4 + kProducers + kMmaWarps), 1)
       const int32_t ns = __ldg(sbase + g + 1) - __ldg(sbase + g);
       mbar_wait(&sh->acc_empty, (it & 1) ^ 1);  // accumulators drained and cleared
       tc_fence_after();
-      // this warp's positions of the group (stages and the end marker)
-      for (uint32_t tq = tg + (uint32_t)((w - (int)(tg % kMmaWarps) + kMmaWarps) % kMmaWarps);
-           tq <= tg + (uint32_t)ns; tq += kMmaWarps) {
+      for (uint32_t tq = tg; tq <= tg + (uint32_t)ns; ++tq) {  // the group's stages and its end marker
         const int stage = (int)(tq % kPStages);
         const uint32_t phase = (tq / kPStages) & 1u;
         timed_wait(&sh->full[stage], phase);
         tc_fence_after();
         const uint4 mv = lds_v4(smem_u32(&sh->mask[stage][0]));
         const int nblk = __popc(mv.x) + __popc(mv.y) + __popc(mv.z) + __popc(mv.w);
-        if constexpr (kTF) {
-          // split the staged value blocks: hi in place, lo beside them
-          const uint32_t vbase = base0 + stage * kPStageBytes + Cfg::kVal;
-          for (int q = lane; q < nblk * (Cfg::kA / 16); q += 32) {
-            const uint4 x = lds_v4(vbase + q * 16);
-            const uint4 h = make_uint4(x.x & 0xffffe000u, x.y & 0xffffe000u, x.z & 0xffffe000u, x.w & 0xffffe000u);
-            const uint4 l = make_uint4(__float_as_uint(__uint_as_float(x.x) - __uint_as_float(h.x)),
-                                       __float_as_uint(__uint_as_float(x.y) - __uint_as_float(h.y)),
-                                       __float_as_uint(__uint_as_float(x.z) - __uint_as_float(h.z)),
-                                       __float_as_uint(__uint_as_float(x.w) - __uint_as_float(h.w)));
-            sts_v4(vbase + q * 16, h);
-            sts_v4(vbase + (Cfg::kLoVal - Cfg::kVal) + q * 16, l);
-          }
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // cp.async / st.shared data -> MMA reads
-        __syncwarp();
         uint32_t b = 0;
         if (lane < nblk) asm volatile("ld.shared.u8 %0, [%1];" : "=r"(b) : "r"(smem_u32(&sh->slot[stage][lane])));
+        const uint32_t mine = __ballot_sync(kFull, lane < nblk && (int)((b & 31u) % kMmaWarps) == w);  // my slots
+        if constexpr (kTF) {
+          // split this warp's staged value blocks: hi in place, lo beside them
+          const uint32_t vbase = base0 + stage * kPStageBytes + Cfg::kVal;
+          for (uint32_t ms = mine; ms; ms &= ms - 1) {
+            const int sl = __ffs(ms) - 1;
+#pragma unroll
+            for (int t = 0; t < Cfg::kA / 16 / 32; ++t) {
+              const uint32_t a = vbase + sl * Cfg::kA + (t * 32 + lane) * 16;
+              const uint4 x = lds_v4(a);
+              const uint4 h =
+                  make_uint4(x.x & 0xffffe000u, x.y & 0xffffe000u, x.z & 0xffffe000u, x.w & 0xffffe000u);
+              const uint4 l = make_uint4(__float_as_uint(__uint_as_float(x.x) - __uint_as_float(h.x)),
+                                         __float_as_uint(__uint_as_float(x.y) - __uint_as_float(h.y)),
+                                         __float_as_uint(__uint_as_float(x.z) - __uint_as_float(h.z)),
+                                         __float_as_uint(__uint_as_float(x.w) - __uint_as_float(h.w)));
+              sts_v4(a, h);
+              sts_v4(a + (Cfg::kLoVal - Cfg::kVal), l);
+            }
+          }
+        }
+        if constexpr (kTF) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // split stores -> MMA reads
         __syncwarp();
         const uint64_t soff = (uint64_t)((stage * kPStageBytes) >> 4);
         if (!(dbg & 1)) {
-          uint32_t pk = __shfl_sync(kFull, b, 0);
-          for (int sl = 0; sl < nblk; ++sl) {
-            const uint32_t nx = __shfl_sync(kFull, b, (sl + 1) & 31);
+          for (uint32_t ms = mine; ms; ms &= ms - 1) {
+            const int sl = __ffs(ms) - 1;
+            const uint32_t pk = __shfl_sync(kFull, b, sl);
             const uint32_t acc = tmem + (pk & 31u) * kBlk;
             const uint64_t ad = adesc0 + soff + (pk >> 5) * (Cfg::kTile >> 4);
             const uint64_t bd = bdesc0 + soff + (uint32_t)sl * (Cfg::kA >> 4);
@@ -885,10 +883,9 @@ __global__ void __launch_bounds__(32 * (4 + kProducers + kMmaWarps), 1)
             } else {
               tc_mma_elect(acc, ad, bd, Cfg::kId, 1u);
             }
-            pk = nx;
           }
         }
-        tc_commit_elect(&sh->empty[stage]);
+        tc_commit_elect(&sh->empty[stage]);  // one of kMmaWarps arrivals
         __syncwarp();
       }
       tc_commit_elect(&sh->acc_full);  // fires when this warp's MMAs of the group are done
@@ -1449,11 +1446,12 @@ bool spmm_bcsr_tc(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dt
 #else
   constexpr int dbg = 0;
 #endif
-  // 4 producer and 4 MMA warps measured best for bf16 (scripts/gpu_run78.sh:
-  // 0.40 ms at m = 65536; 4/8: 0.39, 4/2: 0.43, 8/4: 0.47, 8/8: 0.47, 2/4:
-  // 0.61; 3/3 over 6 stages of 32 value blocks: 0.46)
-  constexpr int kP = 4, kW = 4;
-  auto run_panel = [&](auto kern, size_t psmem, const CUtensorMap& t_hi, const CUtensorMap& t_lo) {
+  // 4 producer and 8 MMA warps (each MMA warp owning the block rows j with
+  // j % 8 == w) measured best at config 4 bf16: 22.1 ms; 4 MMA warps 22.8,
+  // 2 MMA warps 31.5, 2 producers 25.1
+  constexpr int kP = 4, kW = 8;
+  auto run_panel = [&](auto kern, size_t psmem, const CUtensorMap& t_hi, const CUtensorMap& t_lo,
+                       const CUtensorMap& t_v) {
     unsigned long long* dbg_out = nullptr;
     if (dbg) {
       dbg_out = static_cast<unsigned long long*>(scratch(ctx, 64 * 8));
@@ -1462,7 +1460,7 @@ bool spmm_bcsr_tc(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dt
     // set on every call: a once-only static setup measured 30 % slower
     // launches (0.61 vs 0.46 ms at m = 65536)
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
-    SFG_LAUNCH(kern, grid, 32 * (4 + kP + kW), psmem, ctx->stream, t_hi, t_lo, static_cast<const uint8_t*>(a->val),
+    SFG_LAUNCH(kern, grid, 32 * (4 + kP + kW), psmem, ctx->stream, t_hi, t_lo, t_v, static_cast<const uint8_t*>(a->val),
                a->ptr, (int32_t)a->nbr, (int32_t)a->m, c, ldc, accumulate ? 1 : 0, mut->tc_base, mut->tc_desc, dbg,
                dbg_out);
     if (dbg & 256) {
@@ -1495,13 +1493,23 @@ bool spmm_bcsr_tc(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dt
     float* blo = dalloc_n<float>(ctx, a->n * kND);
     SFG_LAUNCH(k_tf32_split, stream_grid(ctx, a->n * (kND / 4), 256, 4, 8), 256, 0, ctx->stream,
                static_cast<const float*>(b), a->n, ldb, bhi, blo);
-    CUtensorMap thi, tlo;
+    CUtensorMap thi, tlo, tv;
     tile_map(&thi, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, bhi, kND, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     tile_map(&tlo, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, blo, kND, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    {  // value blocks as (8 K, rows, 2 K halves): a box lands as [half][row][32 bytes], 32-byte swizzle
+      cuuint64_t dims[3] = {8, (cuuint64_t)(a->nnz * kBlk), 2};
+      cuuint64_t strides[2] = {kBlk * 4, 32};
+      cuuint32_t box[3] = {8, kBlk, 2};
+      cuuint32_t es[3] = {1, 1, 1};
+      if (encode(&tv, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, a->val, dims, strides, box, es,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        raise(SFG_ERR_CUDA, "cuTensorMapEncodeTiled(values) failed");
+    }
     run_panel(k_bcsr_tc_panel<kP, kW, true>,
               1024 + PanelCfg<true>::kStages * PanelCfg<true>::kStageBytes + sizeof(PShared<PanelCfg<true>::kStages>) +
                   64,
-              thi, tlo);
+              thi, tlo, tv);
     dfree(ctx, bhi);
     dfree(ctx, blo);
     return true;
@@ -1557,7 +1565,7 @@ bool spmm_bcsr_tc(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dt
     run_panel(k_bcsr_tc_panel<kP, kW, false>,
               1024 + PanelCfg<false>::kStages * PanelCfg<false>::kStageBytes +
                   sizeof(PShared<PanelCfg<false>::kStages>) + 64,
-              tb3, tb3);
+              tb3, tb3, ta);
   } else {
     // set on every call: a once-only static setup measured 30 % slower
     // launches of the panel kernel (0.61 vs 0.46 ms at m = 65536)

@@ -66,3 +66,30 @@ def test_spmm_accumulate_bit_identical(ctx):
     torch.cuda.synchronize()
     for o in outs[1:]:
         assert torch.equal(o, outs[0])
+
+
+@pytest.mark.parametrize("block,density", [(16, 0.1), (16, 0.6), (4, 0.1)])
+def test_bcsr_tensor_core_bit_identical(ctx, block, density):
+    """The tcgen05 BCSR paths with bf16 values and B (16x16 panel kernel:
+    MMA warps own block rows; 4x4 window kernel: one MMA warp per
+    accumulator) give the same bits on every run."""
+    import paper_2403_05802_b200 as sfg
+    rng = np.random.default_rng(block)
+    m = n = 2048
+    nb = m // block
+    br, bc = np.nonzero(rng.random((nb, nb)) < density)
+    ii, jj = np.meshgrid(np.arange(block), np.arange(block), indexing="ij")
+    r = (br[:, None] * block + ii.ravel()[None, :]).ravel()
+    c = (bc[:, None] * block + jj.ravel()[None, :]).ravel()
+    v = (rng.random(len(r)) * 2 - 1).astype(np.float32).astype(np.float64)
+    a = ctx.convert(ctx.from_coo(m, n, r, c, v), f"BCSR({block},{block})", value_dtype=sfg.BF16)
+    b = (torch.rand(n * 128, device="cuda") * 2 - 1).to(torch.bfloat16)
+    cc = torch.empty(m * 128, device="cuda")
+    outs = []
+    for _ in range(10):
+        cc.fill_(float("nan"))
+        ctx.spmm_device(a, b.data_ptr(), sfg.BF16, 128, cc.data_ptr())
+        outs.append(cc.clone())
+    torch.cuda.synchronize()
+    for o in outs[1:]:
+        assert torch.equal(o.view(torch.int32), outs[0].view(torch.int32)), (block, density)

@@ -81,6 +81,10 @@ enum sfg_format_kind {
   SFG_HBELL = 14, /* hybrid BELL/COO (the paper's GPU format, PAPER.md fig.
                      BELL-COO): decompose by b x b blocks with >= threshold
                      nonzeros -> BELL(b), the rest -> COO                    */
+  SFG_DCSC = 15, /* (d1, d0); merge(0), trim(0,1): nonempty columns, then
+                    rows                                      formats.hpp:43 */
+  SFG_DIAV = 16, /* DIA-variant: (d1-d0, d1); merge(0), trim(0,0) — diagonals
+                    over a dense vector of columns            formats.hpp:47 */
 };
 
 enum sfg_dtype { SFG_F32 = 0, SFG_BF16 = 1 };

@@ -175,6 +175,9 @@ inline std::string name_of(const sfg_format& f) {
     case SFG_BDIA: return "BDIA(" + std::to_string(f.block_r) + ")";
     case SFG_C2SR: return "C2SR(" + std::to_string(f.block_r) + ")";
     case SFG_CSB: return "CSB(" + std::to_string(f.block_r) + "," + std::to_string(f.block_c) + ")";
+    case SFG_HBELL: return "HBELL(" + std::to_string(f.block_r) + "," + std::to_string(f.threshold) + ")";
+    case SFG_DCSC: return "DCSC";
+    case SFG_DIAV: return "DIA-variant";
   }
   return "?";
 }
@@ -192,6 +195,9 @@ inline FormatEncoding resolve_format(const std::string& text) {
         {"map(d0,d1)->(d0,d1);merge(0),trim(1,1)", "CSR"},
         {"map(d0,d1)->(d1,d0);merge(0),trim(1,1)", "CSC"},
         {"map(d0,d1)->(d0,d1);merge(0),trim(0,1)", "DCSR"},
+        {"map(d0,d1)->(d1,d0);merge(0),trim(0,1)", "DCSC"},
+        {"map(d0,d1)->(d1-d0,d0);merge(0),trim(0,0)", "DIA"},
+        {"map(d0,d1)->(d1-d0,d1);merge(0),trim(0,0)", "DIA-variant"},
         {"map(d0,d1)->(d0,d1);trim(0,1),pack(0,1)", "DOK"},
         {"map(d0,d1)->(d0,d1);merge(0),trim(1,1),pack(0,1)", "LIL"},
     };
@@ -250,13 +256,15 @@ inline StorageScheme infer_storage(const FormatEncoding& enc) {
     case SFG_CSR:
     case SFG_LIL:
     case SFG_CSC: s.levels = {L(1, 0, 0, 0), L(0, 1, 1, 0)}; break;
-    case SFG_DCSR: s.levels = {L(0, 0, 1, 0), L(0, 1, 1, 0)}; break;
+    case SFG_DCSR:
+    case SFG_DCSC: s.levels = {L(0, 0, 1, 0), L(0, 1, 1, 0)}; break;
     case SFG_ELL: s.levels = {L(0, 0, 1, 0), L(1, 0, 0, 0), L(0, 0, 1, 0)}; break;
     case SFG_BCSR: s.levels = {L(1, 0, 0, 0), L(0, 1, 1, 0), L(1, 0, 0, 1), L(1, 0, 0, 1)}; break;
     case SFG_BELL:
       s.levels = {L(0, 0, 1, 0), L(1, 0, 0, 0), L(0, 0, 1, 0), L(1, 0, 0, 1), L(1, 0, 0, 1)};
       break;
-    case SFG_DIA: s.levels = {L(0, 0, 1, 0), L(1, 0, 0, 1)}; break;
+    case SFG_DIA:
+    case SFG_DIAV: s.levels = {L(0, 0, 1, 0), L(1, 0, 0, 1)}; break;
     case SFG_BDIA: s.levels = {L(1, 0, 0, 0), L(0, 1, 1, 0), L(1, 0, 0, 1)}; break;
     case SFG_C2SR: s.levels = {L(1, 0, 0, 0), L(1, 0, 0, 0), L(0, 1, 1, 0)}; break;
     case SFG_CSB: s.levels = {L(1, 0, 0, 0), L(1, 0, 0, 0), L(0, 1, 1, 0), L(0, 0, 1, 0)}; break;

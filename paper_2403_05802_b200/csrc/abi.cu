@@ -110,6 +110,8 @@ std::string plan_for(const sfg_format& dst) {
              "Fill(3)\nFill(1)\nVectorize(3)\nMerge(0)\n";
     }
     case SFG_LIL: return "Fill(0)\nMerge(0)\nPack(0,1)\n";
+    case SFG_DCSC: return "Swap(0,1)\nSort\nMerge(0)\n";
+    case SFG_DIAV: return "Scale(0,-1)\nSkew(1,0,1)\nSort\nFill(1)\nVectorize(1)\nMerge(0)\n";
   }
   return "";
 }
@@ -159,6 +161,12 @@ std::string simplify_plan(std::string p) {
       {"Swap(0,1)\nSkew(0,1,-1)\n", "Skew(1,0,-1)\nSwap(0,1)\n"},
       {"Swap(0,1)\nSwap(0,1)\n", ""},
       {"Skew(0,1,1)\nSwap(0,1)\n", "Scale(1,-1)\nSkew(1,0,-1)\nSkew(0,1,1)\n"},
+      // DIA-variant's map (Scale(0,-1) Skew(1,0,1)) after a transposing or
+      // skewed source, and its inverse before DIA's
+      {"Swap(0,1)\nScale(0,-1)\nSkew(1,0,1)\n", "Skew(1,0,-1)\nSkew(0,1,1)\n"},
+      {"Skew(1,0,1)\nSkew(1,0,-1)\n", ""},
+      {"Skew(0,1,1)\nScale(0,-1)\nSkew(1,0,1)\n", "Skew(1,0,1)\nSwap(0,1)\n"},
+      {"Scale(0,-1)\nSkew(1,0,1)\nSkew(0,1,-1)\n", "Skew(0,1,-1)\nSwap(0,1)\n"},
   };
   for (bool changed = true; changed;) {
     changed = false;
@@ -181,9 +189,16 @@ std::string plan_from_raw(const sfg_format& src, const sfg_format& dst) {
       if (dst.kind == SFG_CSR) return "Fill(0)\n";
       if (dst.kind == SFG_LIL) return "Fill(0)\nPack(0,1)\n";
       return "Split(0)\n" + tail;
+    case SFG_DCSC:
+      if (dst.kind == SFG_CSC) return "Fill(0)\n";
+      return "Split(0)\nSwap(0,1)\n" + std::string(sorts ? "" : "Sort\n") + tail;
+    case SFG_DIAV:
+      return "Devectorize(1)\nSplit(0)\nTrim(1)\nScale(0,-1)\nSkew(1,0,1)\n" + std::string(sorts ? "" : "Sort\n") +
+             tail;
     case SFG_CSC: {
       // the coordinates come back column-major: Swap(0,1), then the sort
       // unless the target's ops sort
+      if (dst.kind == SFG_DCSC) return "Trim(0)\n";
       return "Split(0)\nTrim(0)\nSwap(0,1)\n" + std::string(sorts ? "" : "Sort\n") + tail;
     }
     case SFG_BCSR:
@@ -225,12 +240,14 @@ std::string explain_for(const sfg_format& f) {
              "COO(L0: idx | L1: idx | val)";
     case SFG_CSB: return "L0: size | L1: size | L2: ptr, idx | L3: idx | val";
     case SFG_LIL: return "L0: size | L1: ptr, idx | val | pack(0,1)";
+    case SFG_DCSC: return "L0: idx | L1: ptr, idx | val";
+    case SFG_DIAV: return "L0: idx | L1: size, dense_vector | val";
   }
   return "";
 }
 
 void validate_format(const sfg_format& f) {
-  require(f.kind >= SFG_COO && f.kind <= SFG_HBELL, SFG_ERR_PARSE, "unknown format kind");
+  require(f.kind >= SFG_COO && f.kind <= SFG_DIAV, SFG_ERR_PARSE, "unknown format kind");
   if (f.kind == SFG_BCSR || f.kind == SFG_BELL || f.kind == SFG_CSB || f.kind == SFG_BDIA || f.kind == SFG_C2SR ||
       f.kind == SFG_HBELL)
     require(f.block_r > 0 && f.block_c > 0, SFG_ERR_INVALID_OPERATION,
@@ -355,6 +372,8 @@ int sfg_format_resolve(const char* text, sfg_format* out) {
     else if (name == "CSR") f.kind = SFG_CSR;
     else if (name == "CSC") f.kind = SFG_CSC;
     else if (name == "DCSR") f.kind = SFG_DCSR;
+    else if (name == "DCSC") f.kind = SFG_DCSC;
+    else if (name == "DIA-variant" || name == "DIAV") f.kind = SFG_DIAV;
     else if (name == "ELL") f.kind = SFG_ELL;
     else if (name == "DOK") f.kind = SFG_DOK;
     else if (name == "LIL") f.kind = SFG_LIL;
@@ -494,6 +513,8 @@ int sfg_convert(sfg_context* ctx, const sfg_tensor* src, const sfg_format* dst, 
       case SFG_BDIA: *out = sfg::coo_to_bdia(ctx, src, dst->block_r); break;
       case SFG_C2SR: *out = sfg::coo_to_c2sr(ctx, src, dst->block_r); break;
       case SFG_HBELL: *out = sfg::coo_to_hbell(ctx, src, dst->block_r, dst->threshold); break;
+      case SFG_DCSC: *out = sfg::coo_to_dcsc(ctx, src); break;
+      case SFG_DIAV: *out = sfg::coo_to_dia(ctx, src, true); break;
     }
   });
 }
@@ -608,6 +629,20 @@ int sfg_tensor_view_get(sfg_context* ctx, const sfg_tensor* t, sfg_tensor_view* 
         v.level[1] = level(S | D, 0, t->m - 1, t->k * t->m, 0, nullptr, 0, nullptr);
         v.nvals = t->k * t->m;
         break;
+      case SFG_DIAV:  // diagonals, then a dense vector over the columns
+        v.nlevels = 2;
+        v.level[0] = level(I, -(t->m - 1), t->n - 1, t->k, t->k, t->slots, 0, nullptr);
+        v.level[1] = level(S | D, 0, t->n - 1, t->k * t->n, 0, nullptr, 0, nullptr);
+        v.nvals = t->k * t->n;
+        break;
+      case SFG_DCSC: {  // nonempty columns, then the rows
+        const int64_t nnc = sfg::tensor_nnr(t);
+        v.nlevels = 2;
+        v.level[0] = level(I, 0, t->n - 1, nnc, nnc, t->row, 0, nullptr);
+        v.level[1] = level(P | I, 0, t->m - 1, t->nnz, t->nnz, t->idx, nnc + 1, t->ptr);
+        v.nvals = t->nnz;
+        break;
+      }
       case SFG_C2SR:  // residue classes, rows per class, CSR over the interleaved rows
         v.nlevels = 3;
         v.level[0] = level(S, 0, t->nbr - 1, t->nbr, 0, nullptr, 0, nullptr);

@@ -92,11 +92,13 @@ std::vector<uint8_t> expected_kinds(int kind) {
     case SFG_COO: return {kUIdx, kUIdx};
     case SFG_CSR:
     case SFG_CSC: return {kUSize, kUIdx | kUPtr};
-    case SFG_DCSR: return {kUIdx, kUIdx | kUPtr};
+    case SFG_DCSR:
+    case SFG_DCSC: return {kUIdx, kUIdx | kUPtr};  // (DCSC: read with the format given)
     case SFG_ELL: return {kUIdx, kUSize, kUIdx};
     case SFG_BCSR: return {kUSize, kUIdx | kUPtr, kUSize | kUDense, kUSize | kUDense};
     case SFG_BELL: return {kUIdx, kUSize, kUIdx, kUSize | kUDense, kUSize | kUDense};
-    case SFG_DIA: return {kUIdx, kUSize | kUDense};
+    case SFG_DIA:
+    case SFG_DIAV: return {kUIdx, kUSize | kUDense};  // (DIA-variant: read with the format given)
     case SFG_BDIA: return {kUSize, kUIdx | kUPtr, kUSize | kUDense};
     case SFG_C2SR: return {kUSize, kUSize, kUIdx | kUPtr};
     case SFG_CSB: return {kUSize, kUSize, kUIdx | kUPtr, kUIdx};
@@ -408,8 +410,9 @@ sfg_tensor* read_container(sfg_context* ctx, const char* path_c, const sfg_forma
         break;
       }
       case SFG_DIA:
+      case SFG_DIAV:
         t->k = lv[0].nidx;
-        t->nnz = t->k * m;
+        t->nnz = t->k * (fmt.kind == SFG_DIAV ? n : m);
         t->slots = load_i(lv[0].idx_off, lv[0].nidx);
         break;
       case SFG_C2SR:
@@ -465,6 +468,7 @@ sfg_tensor* read_container(sfg_context* ctx, const char* path_c, const sfg_forma
         t->idx = load_i(lv[1].idx_off, lv[1].nidx);
         break;
       case SFG_DCSR:
+      case SFG_DCSC:
         t->nnr = lv[0].nidx;
         t->nnz = lv[1].nidx;
         t->row = load_i(lv[0].idx_off, lv[0].nidx);

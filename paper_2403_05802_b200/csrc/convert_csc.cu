@@ -514,4 +514,57 @@ sfg_tensor* coo_to_csc(sfg_context* ctx, const sfg_tensor* s) {
   return t;
 }
 
+// DCSC: map (d1, d0); merge(0), trim(0,1) (formats.hpp:43), plan Swap(0,1)
+// Sort Merge(0): the CSC with its empty columns dropped — L0 idx = the
+// nonempty columns ascending (bounds [0, n-1]), L1 ptr over them + the rows.
+// Device: the CSC conversion above, then a flag / scan / scatter over the
+// column pointers (the row and value arrays are taken over as they are).
+namespace {
+
+__global__ void k_col_nonempty(const int32_t* __restrict__ ptr, int64_t n, int32_t* __restrict__ flag) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x)
+    flag[c] = __ldg(ptr + c + 1) > __ldg(ptr + c) ? 1 : 0;
+}
+
+__global__ void k_col_compact(const int32_t* __restrict__ ptr, const int32_t* __restrict__ base, int64_t n,
+                              int32_t* __restrict__ cols, int32_t* __restrict__ dptr) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t b = __ldg(base + c);
+    if (__ldg(base + c + 1) > b) {
+      cols[b] = (int32_t)c;
+      dptr[b] = __ldg(ptr + c);
+    }
+    if (c == n - 1) dptr[__ldg(base + n)] = __ldg(ptr + n);
+  }
+}
+
+}  // namespace
+
+sfg_tensor* coo_to_dcsc(sfg_context* ctx, const sfg_tensor* s) {
+  sfg_tensor* csc = coo_to_csc(ctx, s);
+  const int64_t n = s->n;
+  sfg_tensor* t = new_tensor(ctx, SFG_DCSC, s->m, n);
+  t->nnz = csc->nnz;
+  t->idx = csc->idx;
+  t->val = csc->val;
+  csc->idx = nullptr;
+  csc->val = nullptr;
+  int32_t* flag = dalloc_n<int32_t>(ctx, n);
+  int32_t* base = dalloc_n<int32_t>(ctx, n + 1);
+  SFG_LAUNCH(k_col_nonempty, stream_grid(ctx, n, kBlock, 4, 8), kBlock, 0, ctx->stream, csc->ptr, n, flag);
+  scan_counts(ctx, flag, n, base);
+  int32_t nnc = 0;
+  read_back(ctx, base + n, sizeof nnc, &nnc);
+  t->row = dalloc_n<int32_t>(ctx, nnc);
+  t->ptr = dalloc_n<int32_t>(ctx, nnc + 1);
+  t->nnr = nnc;
+  SFG_LAUNCH(k_col_compact, stream_grid(ctx, n, kBlock, 4, 8), kBlock, 0, ctx->stream, csc->ptr, base, n, t->row,
+             t->ptr);
+  dfree(ctx, flag);
+  dfree(ctx, base);
+  free_tensor_arrays(csc);
+  delete csc;
+  return t;
+}
+
 }  // namespace sfg

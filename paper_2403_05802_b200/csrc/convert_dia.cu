@@ -67,16 +67,18 @@ __global__ void __launch_bounds__(1024) k_dia_ranks(const uint32_t* __restrict__
   if (threadIdx.x == 0) *ndiag = (int32_t)carry;
 }
 
+// the panel position of an entry: its row (DIA, stride m) or its column
+// (DIA-variant, stride n)
 __global__ void k_dia_scatter(const int32_t* __restrict__ row, const int32_t* __restrict__ col,
-                              const float* __restrict__ val, int64_t nnz, int64_t off, int64_t m,
+                              const float* __restrict__ val, int64_t nnz, int64_t off, int64_t stride, bool by_col,
                               const uint32_t* __restrict__ bits, const int32_t* __restrict__ word_base,
                               float* __restrict__ out) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t r = ld_stream(row + e);
-    const int64_t d = (int64_t)ld_stream(col + e) - r + off;
+    const int32_t r = ld_stream(row + e), c = ld_stream(col + e);
+    const int64_t d = (int64_t)c - r + off;
     const uint32_t word = __ldg(bits + (d >> 5));
     const int64_t k = __ldg(word_base + (d >> 5)) + __popc(word & ((1u << (d & 31)) - 1u));
-    out[k * m + r] = ld_stream(val + e);
+    out[k * stride + (by_col ? c : r)] = ld_stream(val + e);
   }
 }
 
@@ -103,10 +105,10 @@ __global__ void k_csb_split(const int32_t* __restrict__ sub, int64_t nnz, int32_
 // dematerialization of a DIA source (Devectorize(1) Split(0) Trim(1) drops
 // the zero cells — padding and explicit zeros alike)
 __global__ void k_dia_nonzeros(const int32_t* __restrict__ diags, const float* __restrict__ val, int64_t ndiag,
-                               int64_t m, int32_t* __restrict__ orow, int32_t* __restrict__ ocol,
+                               int64_t m, bool by_col, int32_t* __restrict__ orow, int32_t* __restrict__ ocol,
                                float* __restrict__ oval, unsigned long long* __restrict__ count) {
   const int lane = threadIdx.x & 31;
-  const int64_t cells = ndiag * m;
+  const int64_t cells = ndiag * m;  // m: the panel stride (rows, or columns for the variant)
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e - lane < cells;
        e += (int64_t)gridDim.x * blockDim.x) {
     const bool in = e < cells;
@@ -117,10 +119,10 @@ __global__ void k_dia_nonzeros(const int32_t* __restrict__ diags, const float* _
     if (lane == 0 && msk) base = atomicAdd(count, (unsigned long long)__popc(msk));
     base = __shfl_sync(kFull, base, 0);
     if (nz) {
-      const int64_t k = e / m, r = e - k * m;
+      const int64_t k = e / m, i = e - k * m, d = __ldg(diags + k);
       const unsigned long long at = base + __popc(msk & ((1u << lane) - 1u));
-      orow[at] = (int32_t)r;
-      ocol[at] = (int32_t)(r + __ldg(diags + k));
+      orow[at] = (int32_t)(by_col ? i - d : i);
+      ocol[at] = (int32_t)(by_col ? i : i + d);
       oval[at] = v;
     }
   }
@@ -143,8 +145,12 @@ __global__ void k_csb_coords(const int32_t* __restrict__ ptr, const int32_t* __r
 
 }  // namespace
 
-sfg_tensor* coo_to_dia(sfg_context* ctx, const sfg_tensor* s) {
-  const int64_t m = s->m, n = s->n, off = m - 1;
+// DIA (variant = false): the dense vector over the rows; DIA-variant: map
+// (d0, d1) -> (d1 - d0, d1) (formats.hpp:47-48), the same diagonals with a
+// dense vector over the columns: values[ndiag * n], column j of diagonal d =
+// A[j - d][j] or 0, L1 bounds [0, n-1].
+sfg_tensor* coo_to_dia(sfg_context* ctx, const sfg_tensor* s, bool variant) {
+  const int64_t m = s->m, n = s->n, off = m - 1, stride = variant ? n : m;
   const int64_t nd = m + n - 1, nwords = ceil_div(nd, (int64_t)32);
   auto* bits = dalloc_n<uint32_t>(ctx, nwords);
   auto* word_base = dalloc_n<int32_t>(ctx, nwords);
@@ -157,13 +163,14 @@ sfg_tensor* coo_to_dia(sfg_context* ctx, const sfg_tensor* s) {
   SFG_LAUNCH(k_dia_ranks, 1, 1024, 0, ctx->stream, bits, nwords, off, word_base, diags, nd_dev);
   int32_t ndiag = 0;
   read_back(ctx, nd_dev, 4, &ndiag);
-  const int64_t cells = (int64_t)ndiag * m;
+  const int64_t cells = (int64_t)ndiag * stride;
   if (cells >= INT32_MAX || cells * 4 > (int64_t)(ctx->total_mem / 2)) {
     for (void* p : {(void*)bits, (void*)word_base, (void*)diags}) dfree(ctx, p);
-    raise(SFG_ERR_INVALID_OPERATION, "DIA: " + std::to_string(ndiag) + " diagonals x " + std::to_string(m) +
-                                         " rows exceed the device's dense-vector capacity");
+    raise(SFG_ERR_INVALID_OPERATION, "DIA: " + std::to_string(ndiag) + " diagonals x " + std::to_string(stride) +
+                                         (variant ? " columns" : " rows") +
+                                         " exceed the device's dense-vector capacity");
   }
-  sfg_tensor* t = new_tensor(ctx, SFG_DIA, m, n);
+  sfg_tensor* t = new_tensor(ctx, variant ? SFG_DIAV : SFG_DIA, m, n);
   t->k = ndiag;
   t->nnz = cells;
   t->slots = diags;  // L0 idx (ascending diagonals)
@@ -171,7 +178,8 @@ sfg_tensor* coo_to_dia(sfg_context* ctx, const sfg_tensor* s) {
   if (cells) SFG_CUDA(cudaMemsetAsync(t->val, 0, cells * 4, ctx->stream));
   if (s->nnz)
     SFG_LAUNCH(k_dia_scatter, stream_grid(ctx, s->nnz, kBlock, 4, 8), kBlock, 0, ctx->stream, s->row, s->idx,
-               static_cast<const float*>(s->val), s->nnz, off, m, bits, word_base, static_cast<float*>(t->val));
+               static_cast<const float*>(s->val), s->nnz, off, stride, variant, bits, word_base,
+               static_cast<float*>(t->val));
   dfree(ctx, bits);
   dfree(ctx, word_base);
   return t;
@@ -242,7 +250,8 @@ sfg_tensor* csb_to_coo(sfg_context* ctx, const sfg_tensor* t) {
 }
 
 sfg_tensor* dia_to_coo(sfg_context* ctx, const sfg_tensor* t) {
-  const int64_t cells = t->k * t->m;
+  const bool by_col = t->kind == SFG_DIAV;
+  const int64_t stride = by_col ? t->n : t->m, cells = t->k * stride;
   auto* r = dalloc_n<int32_t>(ctx, cells);
   auto* c = dalloc_n<int32_t>(ctx, cells);
   auto* v = dalloc_n<float>(ctx, cells);
@@ -250,7 +259,7 @@ sfg_tensor* dia_to_coo(sfg_context* ctx, const sfg_tensor* t) {
   SFG_CUDA(cudaMemsetAsync(count, 0, 8, ctx->stream));
   if (cells)
     SFG_LAUNCH(k_dia_nonzeros, stream_grid(ctx, cells, kBlock, 1, 8), kBlock, 0, ctx->stream, t->slots,
-               static_cast<const float*>(t->val), t->k, t->m, r, c, v, count);
+               static_cast<const float*>(t->val), t->k, stride, by_col, r, c, v, count);
   unsigned long long nz = 0;
   read_back(ctx, count, 8, &nz);
   sfg_tensor* out = nullptr;

@@ -304,6 +304,32 @@ sfg_tensor* bcsr_to_coo(sfg_context* ctx, const sfg_tensor* s) {
 
 }  // namespace
 
+// DCSC: as the CSC above, with the nonempty-column list as the A^T row ids
+// (Split(0) Swap(0,1) Sort: no column trim — empty columns are already gone)
+sfg_tensor* dcsc_to_coo(sfg_context* ctx, const sfg_tensor* s) {
+  sfg_tensor* at = row_compressed_to_coo(ctx, s->ptr, s->row, tensor_nnr(s), s->idx,
+                                         static_cast<const float*>(s->val), s->nnz, s->n, s->m, false);
+  sfg_tensor* a_csr = nullptr;
+  try {
+    a_csr = coo_to_csc(ctx, at);
+  } catch (...) {
+    free_tensor(at);
+    throw;
+  }
+  free_tensor(at);
+  sfg_tensor* out = nullptr;
+  try {
+    out = row_compressed_to_coo(ctx, a_csr->ptr, nullptr, s->m, a_csr->idx, static_cast<const float*>(a_csr->val),
+                                a_csr->nnz, s->m, s->n, false);
+  } catch (...) {
+    free_tensor(a_csr);
+    throw;
+  }
+  free_tensor(a_csr);
+  return out;
+}
+
+
 // The nonzero entries of an ELL or BELL tensor as a canonical COO (for
 // operations whose result does not depend on zero slots, e.g. SpGEMM).
 sfg_tensor* ell_nonzeros_to_coo(sfg_context* ctx, const sfg_tensor* s) {
@@ -368,6 +394,7 @@ sfg_tensor* deep_copy(sfg_context* ctx, const sfg_tensor* s) {
       t->val = dup(s->val, s->nnz * esz);
       break;
     case SFG_DCSR:
+    case SFG_DCSC:
       t->row = static_cast<int32_t*>(dup(s->row, s->nnr * 4));  // resolved above
       t->ptr = static_cast<int32_t*>(dup(s->ptr, (s->nnr + 1) * 4));
       t->idx = static_cast<int32_t*>(dup(s->idx, s->nnz * 4));
@@ -409,10 +436,18 @@ sfg_tensor* convert_from_compressed(sfg_context* ctx, const sfg_tensor* s, const
   // column level comes back with the interval [-(m-1), n+m-2] (and a CSB
   // source with its tile-grid extents and extra dangling nodes); the device
   // tensors keep [0, n-1] columns, so these sources are not converted.
-  if (s->kind == SFG_DIA || s->kind == SFG_BDIA || s->kind == SFG_CSB)
+  if (s->kind == SFG_DIA || s->kind == SFG_DIAV || s->kind == SFG_BDIA || s->kind == SFG_CSB)
     raise(SFG_ERR_UNSUPPORTED_SOURCE,
-          "conversion from DIA / BDIA / CSB: the reference's skewed / tile-grid level bounds are not held on the "
-          "device");
+          "conversion from DIA / DIA-variant / BDIA / CSB: the reference's skewed / tile-grid level bounds are not "
+          "held on the device");
+  // From a column-major source the reference reaches DIA-variant's map by
+  // Skew(1,0,-1) Skew(0,1,1), which widens the column level to
+  // [-(m-1), n+m-2] (a panel of ndiag x (n + 2(m-1)) cells); the device's
+  // DIA-variant keeps [0, n-1].
+  if (dst.kind == SFG_DIAV && (s->kind == SFG_CSC || s->kind == SFG_DCSC))
+    raise(SFG_ERR_UNSUPPORTED_SOURCE,
+          "CSC / DCSC -> DIA-variant: the reference's skewed plan widens the column level to [-(m-1), n+m-2], "
+          "not held on the device");
   const bool same = s->kind == dst.kind &&
                     (s->kind != SFG_BCSR || (s->br == dst.block_r && s->bc == dst.block_c && s->dtype == dst.value_dtype)) &&
                     (s->kind != SFG_CSB || (s->br == dst.block_r && s->bc == dst.block_c));
@@ -429,6 +464,9 @@ sfg_tensor* convert_from_compressed(sfg_context* ctx, const sfg_tensor* s, const
       break;
     case SFG_CSC:
       coo = csc_to_coo(ctx, s, dst.kind != SFG_CSC);
+      break;
+    case SFG_DCSC:
+      coo = dcsc_to_coo(ctx, s);
       break;
     case SFG_BCSR:
       coo = bcsr_to_coo(ctx, s);
@@ -453,6 +491,8 @@ sfg_tensor* convert_from_compressed(sfg_context* ctx, const sfg_tensor* s, const
       case SFG_DOK: out = coo_to_dok(ctx, coo); break;
       case SFG_LIL: out = coo_to_lil(ctx, coo); break;
       case SFG_DIA: out = coo_to_dia(ctx, coo); break;
+      case SFG_DIAV: out = coo_to_dia(ctx, coo, true); break;
+      case SFG_DCSC: out = coo_to_dcsc(ctx, coo); break;
       case SFG_CSB: out = coo_to_csb(ctx, coo, dst.block_r, dst.block_c); break;
       case SFG_BDIA: out = coo_to_bdia(ctx, coo, dst.block_r); break;
       case SFG_C2SR: out = coo_to_c2sr(ctx, coo, dst.block_r); break;

@@ -81,6 +81,8 @@ struct sfg_context {
 //   COO : row[nnz] (L0 idx), idx[nnz] (L1 idx)
 //   CSR : ptr[m+1], idx[nnz]              CSC: ptr[n+1], idx[nnz] (rows)
 //   DCSR: row[nnr] (L0 idx), ptr[nnr+1], idx[nnz]
+//   DCSC: row[nnr] = the nonempty columns (L0 idx), ptr[nnr+1], idx[nnz] = rows
+//   DIAV: slots[K] (diagonals), val[K*n] (dense vector over the columns)
 //   ELL : slots[K] (L0 idx), idx[K*m] (L2 idx, slot-major), val[K*m]
 //   BCSR: ptr[nbr+1], idx[nblocks] (bcol), val[nblocks*rb*cb] block-major
 //   HYB : part[0] = ELL of the remainder, part[1] = COO of the selection
@@ -225,9 +227,11 @@ bool block_nz_flags(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_t c,
 sfg_tensor* coo_to_hyb(sfg_context* ctx, const sfg_tensor* s, int64_t min_sum);
 // DIA and CSB(r,c) (convert_dia.cu), and back to canonical COO (DIA: its
 // nonzero cells; CSB: every entry).
-sfg_tensor* coo_to_dia(sfg_context* ctx, const sfg_tensor* s);
+sfg_tensor* coo_to_dia(sfg_context* ctx, const sfg_tensor* s, bool variant = false);  // variant: DIA-variant
 sfg_tensor* coo_to_csb(sfg_context* ctx, const sfg_tensor* s, int64_t br, int64_t bc);
-sfg_tensor* dia_to_coo(sfg_context* ctx, const sfg_tensor* t);
+sfg_tensor* dia_to_coo(sfg_context* ctx, const sfg_tensor* t);  // DIA or DIA-variant
+sfg_tensor* coo_to_dcsc(sfg_context* ctx, const sfg_tensor* s);
+sfg_tensor* dcsc_to_coo(sfg_context* ctx, const sfg_tensor* t);
 sfg_tensor* csb_to_coo(sfg_context* ctx, const sfg_tensor* t);
 sfg_tensor* coo_to_bdia(sfg_context* ctx, const sfg_tensor* s, int64_t b);
 sfg_tensor* bdia_to_coo(sfg_context* ctx, const sfg_tensor* t);  // nonzero cells

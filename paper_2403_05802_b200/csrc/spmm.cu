@@ -544,7 +544,7 @@ __global__ void __launch_bounds__(kBlock) k_spmm_ell(const int32_t* __restrict__
 template <typename TB, int V>
 __global__ void __launch_bounds__(kBlock) k_spmm_dia(const int32_t* __restrict__ diags,
                                                       const float* __restrict__ val, int64_t m, int64_t n,
-                                                      int64_t k, Dense d) {
+                                                      int64_t k, bool by_col, Dense d) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int chunks = (d.nd + 32 * V - 1) / (32 * V);
@@ -557,7 +557,7 @@ __global__ void __launch_bounds__(kBlock) k_spmm_dia(const int32_t* __restrict__
     for (int i = 0; i < V; ++i) acc[i] = 0.f;
     for (int64_t q = 0; q < k; ++q) {
       const int64_t c = r + __ldg(diags + q);
-      if (c >= 0 && c < n) fma_row<TB, V>(d, (int)c, __ldg(val + q * m + r), c0, vec_ok, acc);
+      if (c >= 0 && c < n) fma_row<TB, V>(d, (int)c, __ldg(val + (by_col ? q * n + c : q * m + r)), c0, vec_ok, acc);
     }
     store_row<V>(d, r, c0, false, acc);
   }
@@ -1046,9 +1046,10 @@ void launch_fmt(sfg_context* ctx, const sfg_tensor* a, const Dense& d) {
                    a->n, (int32_t)a->br, (int32_t)a->rb, d);
       break;
     case SFG_DIA:
+    case SFG_DIAV:
       if (a->m)
         SFG_LAUNCH((k_spmm_dia<TB, V>), grid_for(a->m * chunks), kBlock, 0, ctx->stream, a->slots, fv, a->m, a->n,
-                   a->k, d);
+                   a->k, a->kind == SFG_DIAV, d);
       break;
     case SFG_COO:
     case SFG_DOK:
@@ -1312,8 +1313,9 @@ void spmm(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dtype, int
     return;
   }
   if (a->kind == SFG_BCSR && spmm_bcsr_tc(ctx, a, b, b_dtype, nd, ldb, c, ldc, accumulate)) return;
-  if (a->kind == SFG_CSB || a->kind == SFG_C2SR) {  // the entries back in row order, then COO
-    sfg_tensor* coo = a->kind == SFG_CSB ? csb_to_coo(ctx, a) : c2sr_to_coo(ctx, a);
+  if (a->kind == SFG_CSB || a->kind == SFG_C2SR || a->kind == SFG_DCSC) {  // the entries back in row order, then COO
+    sfg_tensor* coo = a->kind == SFG_CSB ? csb_to_coo(ctx, a) : a->kind == SFG_C2SR ? c2sr_to_coo(ctx, a)
+                                                                                     : dcsc_to_coo(ctx, a);
     try {
       spmm(ctx, coo, b, b_dtype, nd, ldb, c, ldc, accumulate);
     } catch (...) {

@@ -134,15 +134,16 @@ __global__ void __launch_bounds__(kBlock) k_spmv_ell(const int32_t* __restrict__
 // ---------------------------------------------------------------- DIA
 // Thread per row: every diagonal's cell of the row (zero cells included,
 // like the reference's walk; columns past N guarded out).
+// (DIA-variant: the panel is over the columns, cell (q, c) at q * n + c)
 __global__ void __launch_bounds__(kBlock) k_spmv_dia(const int32_t* __restrict__ diags,
                                                       const float* __restrict__ val, int64_t m, int64_t n,
-                                                      int64_t k, const float* __restrict__ x,
+                                                      int64_t k, bool by_col, const float* __restrict__ x,
                                                       float* __restrict__ y, int acc) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
     float sum = 0.f;
     for (int64_t q = 0; q < k; ++q) {
       const int64_t c = r + __ldg(diags + q);
-      if (c >= 0 && c < n) sum = fmaf(ld_stream(val + q * m + r), ldx(x, (int)c), sum);
+      if (c >= 0 && c < n) sum = fmaf(ld_stream(val + (by_col ? q * n + c : q * m + r)), ldx(x, (int)c), sum);
     }
     y[r] = acc ? y[r] + sum : sum;
   }
@@ -493,10 +494,19 @@ void spmv(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, bool 
       break;
     }
     case SFG_DIA:
+    case SFG_DIAV:
       if (a->m)
         SFG_LAUNCH(k_spmv_dia, stream_grid(ctx, a->m, kBlock, 1, 8), kBlock, 0, ctx->stream, a->slots,
-                   static_cast<const float*>(a->val), a->m, a->n, a->k, x, y, acc);
+                   static_cast<const float*>(a->val), a->m, a->n, a->k, a->kind == SFG_DIAV, x, y, acc);
       break;
+    case SFG_DCSC: {
+      // the entries back in row order (dcsc_to_coo), then COO
+      sfg_tensor* coo = dcsc_to_coo(ctx, a);
+      spmv_coo(ctx, coo, x, y, acc);
+      free_tensor_arrays(coo);
+      delete coo;
+      break;
+    }
     case SFG_BDIA:
       if (a->m)
         SFG_LAUNCH(k_spmv_bdia, stream_grid(ctx, a->m, kBlock, 1, 8), kBlock, 0, ctx->stream, a->ptr, a->idx,

@@ -36,7 +36,7 @@ def test_library_is_sm100a():
 
 FORMATS = ["COO", "CSR", "CSC", "DCSR", "ELL", "BCSR(2,2)", "BCSR(4,4)", "BCSR(16,16)", "BCSR(3,2)", "DOK", "LIL", "BELL(2)", "BELL(4)", "BELL(16)",
            "DIA", "CSB(2)", "CSB(2,3)", "CSB(16)", "CSB(3,2)", "BDIA(2)", "BDIA(3)",
-           "C2SR(2)", "C2SR(3)"]
+           "C2SR(2)", "C2SR(3)", "DCSC", "DIA-variant"]
 
 
 @pytest.mark.parametrize("fmt", FORMATS)
@@ -62,7 +62,8 @@ def test_format_resolution():
         assert ei.value.kind == "Parse", bad
 
 
-SOURCES = ["CSR", "DCSR", "CSC", "BCSR(2,2)", "BCSR(4,4)", "BCSR(3,2)", "DIA", "CSB(2)", "CSB(2,3)", "CSB(3,2)", "BDIA(2)", "BDIA(3)"]
+SOURCES = ["CSR", "DCSR", "CSC", "BCSR(2,2)", "BCSR(4,4)", "BCSR(3,2)", "DIA", "CSB(2)", "CSB(2,3)", "CSB(3,2)", "BDIA(2)", "BDIA(3)",
+           "DCSC", "DIA-variant"]
 
 
 @pytest.mark.parametrize("src", SOURCES)

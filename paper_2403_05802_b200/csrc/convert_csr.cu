@@ -99,36 +99,13 @@ __global__ void k_fill_i32(int32_t* __restrict__ p, int64_t n, int32_t v) {
 // ---------------------------------------------------------- COO -> DCSR
 // Row heads (e == 0 or row[e] != row[e-1]) are compacted: tile t learns how
 // many heads precede it and writes L0.idx[pos] = row, L1.ptr[pos] = e
-// directly. The column and value arrays are the COO's own: k_copy2 moves
-// them with 16-byte loads and stores. (A single-pass decoupled look-back
+// directly. The column and value arrays are the COO's own: the heads
+// kernel moves each tile's words with 16-byte loads and stores (one launch
+// less than a separate copy: 80 -> 65-71 µs at config 3). (A single-pass decoupled look-back
 // version, copies included, took 59 µs on config 3; without the copies
 // still 41 µs — the look-back serialised the tiles.)
 constexpr int kDcsrItems = 16;  // per lane, warp-striped
 constexpr int kDcsrTile = kBlock * kDcsrItems;
-
-// Two arrays of n 32-bit words copied with 16-byte loads / stores (all four
-// pointers 16-byte aligned: device allocations are).
-__global__ void __launch_bounds__(kBlock) k_copy2(const int4* __restrict__ a, const int4* __restrict__ b, int64_t n,
-                                                  int4* __restrict__ oa, int4* __restrict__ ob) {
-  const int64_t q = n / 4;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < q; i += 2 * stride) {
-    const int4 x0 = ld_stream(a + i), y0 = ld_stream(b + i);
-    const bool two = i + stride < q;
-    int4 x1, y1;
-    if (two) x1 = ld_stream(a + i + stride), y1 = ld_stream(b + i + stride);
-    st_stream(oa + i, x0);
-    st_stream(ob + i, y0);
-    if (two) {
-      st_stream(oa + i + stride, x1);
-      st_stream(ob + i + stride, y1);
-    }
-  }
-  for (int64_t e = q * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += stride) {
-    reinterpret_cast<int32_t*>(oa)[e] = reinterpret_cast<const int32_t*>(a)[e];
-    reinterpret_cast<int32_t*>(ob)[e] = reinterpret_cast<const int32_t*>(b)[e];
-  }
-}
 
 // Row heads without a serial look-back: k_dcsr_count counts each tile's
 // heads (a tile is one CTA's kDcsrTile entries, warp-striped), then
@@ -178,10 +155,27 @@ __global__ void __launch_bounds__(kBlock) k_dcsr_count(const int32_t* __restrict
 __global__ void __launch_bounds__(kBlock) k_dcsr_heads(const int32_t* __restrict__ row, int64_t nnz,
                                                        const uint32_t* __restrict__ tile_cnt,
                                                        int32_t* __restrict__ orow, int32_t* __restrict__ optr,
-                                                       int32_t* __restrict__ nnr_out) {
+                                                       int32_t* __restrict__ nnr_out,
+                                                       const int4* __restrict__ cin, const int4* __restrict__ vin,
+                                                       int4* __restrict__ cout, int4* __restrict__ vout) {
   __shared__ uint32_t smem[34];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tile = blockIdx.x;
+  // the tile's column and value words move unchanged (16-byte copies,
+  // issued first so they overlap the head detection)
+  {
+    const int64_t q0 = (int64_t)tile * (kDcsrTile / 4), q1 = min((int64_t)(tile + 1) * (kDcsrTile / 4), nnz / 4);
+    for (int64_t q = q0 + threadIdx.x; q < q1; q += kBlock) {
+      const int4 a = ld_stream(cin + q), b = ld_stream(vin + q);
+      st_stream(cout + q, a);
+      st_stream(vout + q, b);
+    }
+    if (tile == gridDim.x - 1)
+      for (int64_t e = (nnz / 4) * 4 + threadIdx.x; e < nnz; e += kBlock) {
+        reinterpret_cast<int32_t*>(cout)[e] = reinterpret_cast<const int32_t*>(cin)[e];
+        reinterpret_cast<int32_t*>(vout)[e] = reinterpret_cast<const int32_t*>(vin)[e];
+      }
+  }
   // heads before this tile: the counts of tiles 0 .. tile-1
   uint32_t before = 0;
   for (int i = threadIdx.x; i < tile; i += kBlock) before += __ldg(tile_cnt + i);
@@ -325,9 +319,8 @@ sfg_tensor* coo_to_dcsr(sfg_context* ctx, const sfg_tensor* s) {
   int32_t* nnr_dev = reinterpret_cast<int32_t*>(sc);
   uint32_t* tile_cnt = sc + 16;
   SFG_LAUNCH(k_dcsr_count, tiles, kBlock, 0, ctx->stream, s->row, s->nnz, tile_cnt);
-  SFG_LAUNCH(k_dcsr_heads, tiles, kBlock, 0, ctx->stream, s->row, s->nnz, tile_cnt, t->row, t->ptr, nnr_dev);
-  SFG_LAUNCH(k_copy2, stream_grid(ctx, ceil_div(s->nnz, 8), kBlock, 1, 8), kBlock, 0, ctx->stream,
-             reinterpret_cast<const int4*>(s->idx), reinterpret_cast<const int4*>(s->val), s->nnz,
+  SFG_LAUNCH(k_dcsr_heads, tiles, kBlock, 0, ctx->stream, s->row, s->nnz, tile_cnt, t->row, t->ptr, nnr_dev,
+             reinterpret_cast<const int4*>(s->idx), reinterpret_cast<const int4*>(s->val),
              reinterpret_cast<int4*>(t->idx), reinterpret_cast<int4*>(t->val));
   // nnr is read back asynchronously: the tensor is usable at once and the
   // host only waits where the count is needed (tensor_nnr)

@@ -85,6 +85,10 @@ enum sfg_format_kind {
                     rows                                      formats.hpp:43 */
   SFG_DIAV = 16, /* DIA-variant: (d1-d0, d1); merge(0), trim(0,0) — diagonals
                     over a dense vector of columns            formats.hpp:47 */
+  SFG_CISR = 17, /* (indirect(d0), d0, d1); merge(0,1), trim(1,2), partition(0)
+                    with the row count + greedy schedule onto k partitions
+                    (rows in order)                        formats.hpp:67-72 */
+  SFG_CISRP = 18, /* CISR-plus: rows visited heaviest first (reorder query) */
 };
 
 enum sfg_dtype { SFG_F32 = 0, SFG_BF16 = 1 };

@@ -178,6 +178,8 @@ inline std::string name_of(const sfg_format& f) {
     case SFG_HBELL: return "HBELL(" + std::to_string(f.block_r) + "," + std::to_string(f.threshold) + ")";
     case SFG_DCSC: return "DCSC";
     case SFG_DIAV: return "DIA-variant";
+    case SFG_CISR: return "CISR(" + std::to_string(f.block_r) + ")";
+    case SFG_CISRP: return "CISR-plus(" + std::to_string(f.block_r) + ")";
   }
   return "?";
 }
@@ -267,6 +269,8 @@ inline StorageScheme infer_storage(const FormatEncoding& enc) {
     case SFG_DIAV: s.levels = {L(0, 0, 1, 0), L(1, 0, 0, 1)}; break;
     case SFG_BDIA: s.levels = {L(1, 0, 0, 0), L(0, 1, 1, 0), L(1, 0, 0, 1)}; break;
     case SFG_C2SR: s.levels = {L(1, 0, 0, 0), L(1, 0, 0, 0), L(0, 1, 1, 0)}; break;
+    case SFG_CISR:
+    case SFG_CISRP: s.levels = {L(0, 0, 1, 0), L(0, 1, 1, 0), L(0, 1, 1, 0)}; break;
     case SFG_CSB: s.levels = {L(1, 0, 0, 0), L(1, 0, 0, 0), L(0, 1, 1, 0), L(0, 0, 1, 0)}; break;
     default: break;  // HYB: two parts, see DecomposeResult
   }

@@ -205,7 +205,7 @@ class _Base:
 def _fmt_text(fmt, r=None, c=None):
     if fmt == "BCSR":
         return f"BCSR({r},{c})"
-    if fmt in ("BELL", "BDIA", "C2SR"):  # formats.hpp:62-85: one argument
+    if fmt in ("BELL", "BDIA", "C2SR", "CISR", "CISR-plus"):  # formats.hpp:62-85: one argument
         return f"{fmt}({r})"
     if fmt == "CSB":  # formats.hpp:54-57: CSB(r, c)
         return f"CSB({r},{c})"

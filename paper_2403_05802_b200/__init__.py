@@ -23,7 +23,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_lib", "libsfg.so")
 
 KINDS = {"COO": 0, "CSR": 1, "CSC": 2, "DCSR": 3, "ELL": 4, "BCSR": 5, "HYB": 6, "DOK": 7, "LIL": 8, "BELL": 9, "DIA": 10, "CSB": 11, "BDIA": 12, "C2SR": 13, "HBELL": 14, "DCSC": 15,
-         "DIA-variant": 16}
+         "DIA-variant": 16, "CISR": 17, "CISR-plus": 18}
 KIND_NAMES = {v: k for k, v in KINDS.items()}
 F32, BF16 = 0, 1
 FLAG_SORTED, FLAG_SUM_DUPLICATES, FLAG_HOST = 1, 2, 4

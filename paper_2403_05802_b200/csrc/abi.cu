@@ -112,13 +112,16 @@ std::string plan_for(const sfg_format& dst) {
     case SFG_LIL: return "Fill(0)\nMerge(0)\nPack(0,1)\n";
     case SFG_DCSC: return "Swap(0,1)\nSort\nMerge(0)\n";
     case SFG_DIAV: return "Scale(0,-1)\nSkew(1,0,1)\nSort\nFill(1)\nVectorize(1)\nMerge(0)\n";
+    case SFG_CISR: return "Sum(0)\nSchedule(0)\nSort\nMerge(0)\nMerge(1)\nPartition(0)\n";
+    case SFG_CISRP: return "Sum(0)\nReorder(0)\nSchedule(0)\nSort\nMerge(0)\nMerge(1)\nPartition(0)\n";
   }
   return "";
 }
 
 bool same_format(const sfg_format& a, const sfg_format& b) {
   if (a.kind != b.kind) return false;
-  if (a.kind == SFG_BCSR || a.kind == SFG_BELL || a.kind == SFG_CSB || a.kind == SFG_BDIA)
+  if (a.kind == SFG_BCSR || a.kind == SFG_BELL || a.kind == SFG_CSB || a.kind == SFG_BDIA || a.kind == SFG_C2SR ||
+      a.kind == SFG_CISR || a.kind == SFG_CISRP)
     return a.block_r == b.block_r && a.block_c == b.block_c;
   if (a.kind == SFG_HYB) return a.threshold == b.threshold;
   return true;
@@ -134,7 +137,7 @@ std::string plan_from_raw(const sfg_format& src, const sfg_format& dst);
 // with an indirect level or a value layout are rejected (planner.hpp:96-99).
 std::string plan_from(const sfg_format& src, const sfg_format& dst) {
   if (src.kind == SFG_COO) return plan_for(dst);
-  if (src.kind == SFG_ELL || src.kind == SFG_BELL)
+  if (src.kind == SFG_ELL || src.kind == SFG_BELL || src.kind == SFG_CISR || src.kind == SFG_CISRP)
     sfg::raise(SFG_ERR_UNSUPPORTED_SOURCE, "conversion from a format with indirect levels");
   if (src.kind == SFG_DOK || src.kind == SFG_LIL || src.kind == SFG_C2SR)
     sfg::raise(SFG_ERR_UNSUPPORTED_SOURCE, "conversion from a format with a value layout");
@@ -242,14 +245,16 @@ std::string explain_for(const sfg_format& f) {
     case SFG_LIL: return "L0: size | L1: ptr, idx | val | pack(0,1)";
     case SFG_DCSC: return "L0: idx | L1: ptr, idx | val";
     case SFG_DIAV: return "L0: idx | L1: size, dense_vector | val";
+    case SFG_CISR:
+    case SFG_CISRP: return "L0: idx | L1: ptr, idx | L2: ptr, idx | val | partition(0)";
   }
   return "";
 }
 
 void validate_format(const sfg_format& f) {
-  require(f.kind >= SFG_COO && f.kind <= SFG_DIAV, SFG_ERR_PARSE, "unknown format kind");
+  require(f.kind >= SFG_COO && f.kind <= SFG_CISRP, SFG_ERR_PARSE, "unknown format kind");
   if (f.kind == SFG_BCSR || f.kind == SFG_BELL || f.kind == SFG_CSB || f.kind == SFG_BDIA || f.kind == SFG_C2SR ||
-      f.kind == SFG_HBELL)
+      f.kind == SFG_HBELL || f.kind == SFG_CISR || f.kind == SFG_CISRP)
     require(f.block_r > 0 && f.block_c > 0, SFG_ERR_INVALID_OPERATION,
             "TileSplit factor must be positive");
   require(f.value_dtype == SFG_F32 || (f.value_dtype == SFG_BF16 && f.kind == SFG_BCSR),
@@ -398,6 +403,11 @@ int sfg_format_resolve(const char* text, sfg_format* out) {
       // formats.hpp:62-66: k defaults to 2
       f.kind = SFG_C2SR;
       f.block_r = f.block_c = static_cast<int32_t>(nargs > 0 ? args[0] : 2);
+    } else if (name == "CISR" || name == "CISR-plus" || name == "CISRPLUS") {
+      // formats.hpp:67-72: k partitions (default 2); -plus visits the rows
+      // heaviest first
+      f.kind = name == "CISR" ? SFG_CISR : SFG_CISRP;
+      f.block_r = f.block_c = static_cast<int32_t>(nargs > 0 ? args[0] : 2);
     } else if (name == "BDIA") {
       // formats.hpp:76-79: one argument, the block size (default 3)
       f.kind = SFG_BDIA;
@@ -515,6 +525,8 @@ int sfg_convert(sfg_context* ctx, const sfg_tensor* src, const sfg_format* dst, 
       case SFG_HBELL: *out = sfg::coo_to_hbell(ctx, src, dst->block_r, dst->threshold); break;
       case SFG_DCSC: *out = sfg::coo_to_dcsc(ctx, src); break;
       case SFG_DIAV: *out = sfg::coo_to_dia(ctx, src, true); break;
+      case SFG_CISR:
+      case SFG_CISRP: *out = sfg::coo_to_cisr(ctx, src, dst->block_r, dst->kind == SFG_CISRP); break;
     }
   });
 }
@@ -635,6 +647,17 @@ int sfg_tensor_view_get(sfg_context* ctx, const sfg_tensor* t, sfg_tensor_view* 
         v.level[1] = level(S | D, 0, t->n - 1, t->k * t->n, 0, nullptr, 0, nullptr);
         v.nvals = t->k * t->n;
         break;
+      case SFG_CISR:
+      case SFG_CISRP: {  // partitions, their rows, the rows' columns; value range per partition
+        v.nlevels = 3;
+        v.level[0] = level(I, 0, t->br - 1, t->k, t->k, t->slots, 0, nullptr);
+        v.level[1] = level(P | I, 0, t->m - 1, t->nnr, t->nnr, t->row, t->k + 1, t->ptr1);
+        v.level[2] = level(P | I, 0, t->n - 1, t->nnz, t->nnz, t->idx, t->nnr + 1, t->ptr);
+        v.nvals = t->nnz;
+        v.npartitions = (int64_t)t->partitions.size() / 2;
+        v.partitions = t->partitions.data();
+        break;
+      }
       case SFG_DCSC: {  // nonempty columns, then the rows
         const int64_t nnc = sfg::tensor_nnr(t);
         v.nlevels = 2;

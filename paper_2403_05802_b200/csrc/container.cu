@@ -101,6 +101,8 @@ std::vector<uint8_t> expected_kinds(int kind) {
     case SFG_DIAV: return {kUIdx, kUSize | kUDense};  // (DIA-variant: read with the format given)
     case SFG_BDIA: return {kUSize, kUIdx | kUPtr, kUSize | kUDense};
     case SFG_C2SR: return {kUSize, kUSize, kUIdx | kUPtr};
+    case SFG_CISR:
+    case SFG_CISRP: return {kUIdx, kUIdx | kUPtr, kUIdx | kUPtr};  // (-plus: read with the format given)
     case SFG_CSB: return {kUSize, kUSize, kUIdx | kUPtr, kUIdx};
     case SFG_DOK: return {kUIdx, kUIdx};           // COO + pack(0,1)
     case SFG_LIL: return {kUSize, kUIdx | kUPtr};  // CSR + pack(0,1)
@@ -323,7 +325,8 @@ sfg_tensor* read_container(sfg_context* ctx, const char* path_c, const sfg_forma
   } else {
     fmt.value_dtype = SFG_F32;
     int found = -1;
-    for (int k : {SFG_COO, SFG_CSR, SFG_DCSR, SFG_ELL, SFG_BCSR, SFG_BELL, SFG_DIA, SFG_CSB, SFG_BDIA, SFG_C2SR}) {
+    for (int k : {SFG_COO, SFG_CSR, SFG_DCSR, SFG_ELL, SFG_BCSR, SFG_BELL, SFG_DIA, SFG_CSB, SFG_BDIA, SFG_C2SR,
+                  SFG_CISR}) {
       const auto w = expected_kinds(k);
       bool same = w.size() == lv.size();
       for (size_t l = 0; same && l < lv.size(); ++l) same = lv[l].kind == w[l];
@@ -341,8 +344,8 @@ sfg_tensor* read_container(sfg_context* ctx, const char* path_c, const sfg_forma
       fmt.block_c = lv[3].hi - lv[3].lo + 1;
     } else if (found == SFG_BELL) {
       fmt.block_r = fmt.block_c = lv[3].hi - lv[3].lo + 1;
-    } else if (found == SFG_C2SR) {
-      fmt.block_r = fmt.block_c = lv[0].hi - lv[0].lo + 1;  // k (min(k, m) when k > m)
+    } else if (found == SFG_C2SR || found == SFG_CISR) {
+      fmt.block_r = fmt.block_c = lv[0].hi - lv[0].lo + 1;  // k (C2SR: min(k, m) when k > m)
     } else if (found == SFG_BDIA) {
       fmt.block_r = fmt.block_c = lv[2].hi - lv[2].lo + 1;
     } else if (found == SFG_CSB) {
@@ -354,8 +357,8 @@ sfg_tensor* read_container(sfg_context* ctx, const char* path_c, const sfg_forma
   bool ok = rank == 2 && lv.size() == want.size();
   for (size_t l = 0; ok && l < lv.size(); ++l) ok = lv[l].kind == want[l];
   if (ok) ok = (tag == 1) == (fmt.kind == SFG_DOK || fmt.kind == SFG_LIL);
-  if (ok && nparts && fmt.kind != SFG_C2SR)
-    raise(SFG_ERR_UNSUPPORTED_SOURCE, path + ": partitions are held on the device for C2SR only");
+  if (ok && nparts && fmt.kind != SFG_C2SR && fmt.kind != SFG_CISR && fmt.kind != SFG_CISRP)
+    raise(SFG_ERR_UNSUPPORTED_SOURCE, path + ": partitions are held on the device for C2SR and CISR only");
   if (!ok) raise(SFG_ERR_INVALID_OPERATION, path + ": the container does not hold this format");
   const int64_t m = ext[0], n = ext[1];
   if (m >= INT32_MAX || n >= INT32_MAX || nvals >= INT32_MAX)
@@ -466,6 +469,19 @@ sfg_tensor* read_container(sfg_context* ctx, const char* path_c, const sfg_forma
         t->nnz = lv[1].nidx;
         t->ptr = load_i(lv[1].ptr_off, lv[1].nptr);
         t->idx = load_i(lv[1].idx_off, lv[1].nidx);
+        break;
+      case SFG_CISR:
+      case SFG_CISRP:
+        t->br = t->bc = fmt.block_r;
+        t->k = lv[0].nidx;
+        t->nnr = lv[1].nidx;
+        t->nnz = lv[2].nidx;
+        t->slots = load_i(lv[0].idx_off, lv[0].nidx);
+        t->ptr1 = load_i(lv[1].ptr_off, lv[1].nptr);
+        t->row = load_i(lv[1].idx_off, lv[1].nidx);
+        t->ptr = load_i(lv[2].ptr_off, lv[2].nptr);
+        t->idx = load_i(lv[2].idx_off, lv[2].nidx);
+        t->partitions = parts;
         break;
       case SFG_DCSR:
       case SFG_DCSC:

@@ -368,7 +368,7 @@ sfg_tensor* deep_copy(sfg_context* ctx, const sfg_tensor* s) {
   t->tc_base = nullptr;
   t->tc_desc = nullptr;
   t->part[0] = t->part[1] = nullptr;
-  t->row = t->ptr = t->idx = t->slots = nullptr;
+  t->row = t->ptr = t->idx = t->slots = t->ptr1 = nullptr;
   t->val = nullptr;
   auto dup = [&](const void* p, size_t bytes) -> void* {
     if (!p) return nullptr;
@@ -425,7 +425,7 @@ sfg_tensor* deep_copy(sfg_context* ctx, const sfg_tensor* s) {
 }  // namespace
 
 sfg_tensor* convert_from_compressed(sfg_context* ctx, const sfg_tensor* s, const sfg_format& dst) {
-  if (s->kind == SFG_ELL || s->kind == SFG_BELL)
+  if (s->kind == SFG_ELL || s->kind == SFG_BELL || s->kind == SFG_CISR || s->kind == SFG_CISRP)
     raise(SFG_ERR_UNSUPPORTED_SOURCE, "conversion from a format with indirect levels");
   if (s->kind == SFG_HYB || s->kind == SFG_HBELL)
     raise(SFG_ERR_UNSUPPORTED_SOURCE, "conversion from the hybrid pair");
@@ -493,6 +493,8 @@ sfg_tensor* convert_from_compressed(sfg_context* ctx, const sfg_tensor* s, const
       case SFG_DIA: out = coo_to_dia(ctx, coo); break;
       case SFG_DIAV: out = coo_to_dia(ctx, coo, true); break;
       case SFG_DCSC: out = coo_to_dcsc(ctx, coo); break;
+      case SFG_CISR:
+      case SFG_CISRP: out = coo_to_cisr(ctx, coo, dst.block_r, dst.kind == SFG_CISRP); break;
       case SFG_CSB: out = coo_to_csb(ctx, coo, dst.block_r, dst.block_c); break;
       case SFG_BDIA: out = coo_to_bdia(ctx, coo, dst.block_r); break;
       case SFG_C2SR: out = coo_to_c2sr(ctx, coo, dst.block_r); break;

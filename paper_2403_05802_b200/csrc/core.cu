@@ -215,6 +215,8 @@ void free_tensor_arrays(sfg_tensor* t) {
   dfree(ctx, t->ptr);
   dfree(ctx, t->idx);
   dfree(ctx, t->slots);
+  dfree(ctx, t->ptr1);
+  t->ptr1 = nullptr;
   dfree(ctx, t->val);
   dfree(ctx, t->tc_plan);
   dfree(ctx, t->tc_base);

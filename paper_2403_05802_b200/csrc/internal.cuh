@@ -83,6 +83,8 @@ struct sfg_context {
 //   DCSR: row[nnr] (L0 idx), ptr[nnr+1], idx[nnz]
 //   DCSC: row[nnr] = the nonempty columns (L0 idx), ptr[nnr+1], idx[nnz] = rows
 //   DIAV: slots[K] (diagonals), val[K*n] (dense vector over the columns)
+//   CISR: slots[K] (present partitions, L0 idx), ptr1[K+1] + row[nnr] (L1:
+//         rows per partition), ptr[nnr+1] + idx[nnz] (L2), val[nnz]
 //   ELL : slots[K] (L0 idx), idx[K*m] (L2 idx, slot-major), val[K*m]
 //   BCSR: ptr[nbr+1], idx[nblocks] (bcol), val[nblocks*rb*cb] block-major
 //   HYB : part[0] = ELL of the remainder, part[1] = COO of the selection
@@ -117,9 +119,10 @@ struct sfg_tensor {
   int32_t* ptr = nullptr;
   int32_t* idx = nullptr;
   int32_t* slots = nullptr;
+  int32_t* ptr1 = nullptr;  // CISR: L1 ptr over the present partitions
   void* val = nullptr;
   sfg_tensor* part[2] = {nullptr, nullptr};
-  std::vector<int64_t> partitions;  // C2SR: (begin, end) value ranges, host
+  std::vector<int64_t> partitions;  // C2SR / CISR: (begin, end) value ranges, host
 };
 
 namespace sfg {
@@ -231,6 +234,8 @@ sfg_tensor* coo_to_dia(sfg_context* ctx, const sfg_tensor* s, bool variant = fal
 sfg_tensor* coo_to_csb(sfg_context* ctx, const sfg_tensor* s, int64_t br, int64_t bc);
 sfg_tensor* dia_to_coo(sfg_context* ctx, const sfg_tensor* t);  // DIA or DIA-variant
 sfg_tensor* coo_to_dcsc(sfg_context* ctx, const sfg_tensor* s);
+sfg_tensor* coo_to_cisr(sfg_context* ctx, const sfg_tensor* s, int64_t k, bool plus);
+sfg_tensor* cisr_to_coo(sfg_context* ctx, const sfg_tensor* t);
 sfg_tensor* dcsc_to_coo(sfg_context* ctx, const sfg_tensor* t);
 sfg_tensor* csb_to_coo(sfg_context* ctx, const sfg_tensor* t);
 sfg_tensor* coo_to_bdia(sfg_context* ctx, const sfg_tensor* s, int64_t b);

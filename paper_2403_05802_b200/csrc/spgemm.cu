@@ -59,9 +59,10 @@ sfg_tensor* to_csr(sfg_context* ctx, const sfg_tensor* t) {
   f.value_dtype = SFG_F32;
   if (t->kind == SFG_COO) return coo_to_csr(ctx, t);
   if (t->kind == SFG_DIA || t->kind == SFG_DIAV || t->kind == SFG_BDIA || t->kind == SFG_CSB ||
-      t->kind == SFG_C2SR || t->kind == SFG_DCSC) {  // bounds aside
-    sfg_tensor* coo = t->kind == SFG_DIA || t->kind == SFG_DIAV ? dia_to_coo(ctx, t)
-                      : t->kind == SFG_DCSC                      ? dcsc_to_coo(ctx, t)
+      t->kind == SFG_C2SR || t->kind == SFG_DCSC || t->kind == SFG_CISR || t->kind == SFG_CISRP) {  // bounds aside
+    sfg_tensor* coo = t->kind == SFG_DIA || t->kind == SFG_DIAV     ? dia_to_coo(ctx, t)
+                      : t->kind == SFG_DCSC                          ? dcsc_to_coo(ctx, t)
+                      : t->kind == SFG_CISR || t->kind == SFG_CISRP ? cisr_to_coo(ctx, t)
                       : t->kind == SFG_BDIA ? bdia_to_coo(ctx, t)
                       : t->kind == SFG_C2SR ? c2sr_to_coo(ctx, t)
                                             : csb_to_coo(ctx, t);

@@ -1313,9 +1313,12 @@ void spmm(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dtype, int
     return;
   }
   if (a->kind == SFG_BCSR && spmm_bcsr_tc(ctx, a, b, b_dtype, nd, ldb, c, ldc, accumulate)) return;
-  if (a->kind == SFG_CSB || a->kind == SFG_C2SR || a->kind == SFG_DCSC) {  // the entries back in row order, then COO
-    sfg_tensor* coo = a->kind == SFG_CSB ? csb_to_coo(ctx, a) : a->kind == SFG_C2SR ? c2sr_to_coo(ctx, a)
-                                                                                     : dcsc_to_coo(ctx, a);
+  if (a->kind == SFG_CSB || a->kind == SFG_C2SR || a->kind == SFG_DCSC || a->kind == SFG_CISR ||
+      a->kind == SFG_CISRP) {  // the entries back in row order, then COO
+    sfg_tensor* coo = a->kind == SFG_CSB    ? csb_to_coo(ctx, a)
+                      : a->kind == SFG_C2SR ? c2sr_to_coo(ctx, a)
+                      : a->kind == SFG_DCSC ? dcsc_to_coo(ctx, a)
+                                            : cisr_to_coo(ctx, a);
     try {
       spmm(ctx, coo, b, b_dtype, nd, ldb, c, ldc, accumulate);
     } catch (...) {

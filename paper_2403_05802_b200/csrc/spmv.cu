@@ -499,9 +499,11 @@ void spmv(sfg_context* ctx, const sfg_tensor* a, const float* x, float* y, bool 
         SFG_LAUNCH(k_spmv_dia, stream_grid(ctx, a->m, kBlock, 1, 8), kBlock, 0, ctx->stream, a->slots,
                    static_cast<const float*>(a->val), a->m, a->n, a->k, a->kind == SFG_DIAV, x, y, acc);
       break;
-    case SFG_DCSC: {
-      // the entries back in row order (dcsc_to_coo), then COO
-      sfg_tensor* coo = dcsc_to_coo(ctx, a);
+    case SFG_DCSC:
+    case SFG_CISR:
+    case SFG_CISRP: {
+      // the entries back in row order (dcsc_to_coo / cisr_to_coo), then COO
+      sfg_tensor* coo = a->kind == SFG_DCSC ? dcsc_to_coo(ctx, a) : cisr_to_coo(ctx, a);
       spmv_coo(ctx, coo, x, y, acc);
       free_tensor_arrays(coo);
       delete coo;

@@ -36,7 +36,7 @@ def test_library_is_sm100a():
 
 FORMATS = ["COO", "CSR", "CSC", "DCSR", "ELL", "BCSR(2,2)", "BCSR(4,4)", "BCSR(16,16)", "BCSR(3,2)", "DOK", "LIL", "BELL(2)", "BELL(4)", "BELL(16)",
            "DIA", "CSB(2)", "CSB(2,3)", "CSB(16)", "CSB(3,2)", "BDIA(2)", "BDIA(3)",
-           "C2SR(2)", "C2SR(3)", "DCSC", "DIA-variant"]
+           "C2SR(2)", "C2SR(3)", "DCSC", "DIA-variant", "CISR(2)", "CISR(3)", "CISR-plus(2)", "CISR-plus(5)"]
 
 
 @pytest.mark.parametrize("fmt", FORMATS)
@@ -76,7 +76,8 @@ def test_plan_from_compressed_sources_matches_reference(ref, src):
 
 @pytest.mark.parametrize("src,why", [("ELL", "indirect levels"), ("BELL(2)", "indirect levels"),
                                      ("DOK", "value layout"), ("LIL", "value layout"),
-                                     ("C2SR(2)", "value layout")])
+                                     ("C2SR(2)", "value layout"), ("CISR(2)", "indirect levels"),
+                                     ("CISR-plus(3)", "indirect levels")])
 def test_plan_rejects_sources_like_the_reference(ref, src, why):
     with pytest.raises(sfg.SfgError) as ei:
         sfg.plan_lines(src, "CSR")

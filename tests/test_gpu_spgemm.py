@@ -69,7 +69,8 @@ def test_spgemm_errors(ctx):
 
 
 
-EXTRA = ["ELL", "HYB(2)", "DOK", "LIL", "BELL(2)", "DIA", "CSB(2,3)", "BDIA(3)", "C2SR(3)", "DCSC", "DIA-variant", "HBELL(2,2)"]
+EXTRA = ["ELL", "HYB(2)", "DOK", "LIL", "BELL(2)", "DIA", "CSB(2,3)", "BDIA(3)", "C2SR(3)", "DCSC", "DIA-variant", "HBELL(2,2)",
+         "CISR(3)", "CISR-plus(2)"]
 
 
 @pytest.mark.parametrize("fb", ["CSR"] + EXTRA)

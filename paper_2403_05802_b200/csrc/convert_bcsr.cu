@@ -30,6 +30,11 @@ namespace {
 constexpr int kBlock = 256;
 constexpr int kMaxWords = 24 * 1024;  // 96 KB bitmap (+96 KB prefix) => <= 786K block columns
 
+// x / d for x >= 0, a shift when d is a power of two (the block sizes in
+// practice; a division by a run-time divisor costs ~20 instructions)
+__device__ __forceinline__ int pow2_shift(int d) { return (d & (d - 1)) == 0 ? __ffs(d) - 1 : -1; }
+__device__ __forceinline__ int divp(int x, int d, int sh) { return sh >= 0 ? x >> sh : x / d; }
+
 // Block-row pointers: the row pointers of the block-row ids (row / r) of
 // the sorted entries — the CSR row-pointer pass (devutil.cuh: 16-byte row
 // loads, warp-staged lower-bound searches, coalesced stores).
@@ -40,6 +45,7 @@ __global__ void __launch_bounds__(kBlock) k_brow_ptr(const int32_t* __restrict__
                                                       int32_t* __restrict__ bptr) {
   constexpr int kChunk = 128 * kBrowVec;
   __shared__ __align__(16) int32_t s_rows[kBlock / 32][kChunk];
+  const int rs = pow2_shift(r);
   const int64_t nchunk = (nnz + kChunk - 1) / kChunk;
   const int64_t warps = (int64_t)gridDim.x * (kBlock / 32);
   for (int64_t ch = (int64_t)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); ch < nchunk; ch += warps) {
@@ -49,8 +55,8 @@ __global__ void __launch_bounds__(kBlock) k_brow_ptr(const int32_t* __restrict__
 #pragma unroll
     for (int g = 0; g < kBrowVec; ++g)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) c.r[g][i] /= r;
-    c.prev = c.prev < 0 ? -1 : c.prev / r;
+      for (int i = 0; i < 4; ++i) c.r[g][i] = divp(c.r[g][i], r, rs);
+    c.prev = c.prev < 0 ? -1 : divp(c.prev, r, rs);
     chunk_row_ptr(c, nnz, base, nbr, s_rows[threadIdx.x >> 5], bptr);
   }
 }
@@ -59,20 +65,39 @@ __global__ void __launch_bounds__(kBlock) k_brow_ptr(const int32_t* __restrict__
 // Four entries per thread per step, loads first (the loop is latency
 // bound). (Skipping entries whose block column repeats its predecessor's,
 // or an OR-scan per run of equal words with one atomic per run, both
-// measured slower: 391 / 451 vs 290 us for the count kernel at 32768^2.)
+// measured slower in round 1: 391 / 451 vs 290 us for the count kernel at
+// 32768^2; the match-any aggregation below is faster for wide blocks.)
 __device__ __forceinline__ void mark(const int32_t* __restrict__ col, int32_t s, int32_t e,
                                      int32_t c, int32_t lo, uint32_t* bm) {
   constexpr int U = 4;
-  for (int32_t k = s + threadIdx.x; k < e; k += U * blockDim.x) {
+  const int cs = pow2_shift(c);
+  // warp-uniform trip count: the warp-wide match / reduce below need every lane
+  for (int32_t kw = s + (int32_t)(threadIdx.x & ~31u); kw < e; kw += U * blockDim.x) {
+    const int32_t k = kw + (int32_t)(threadIdx.x & 31);
     int v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) v[u] = k + u * (int32_t)blockDim.x < e ? __ldg(col + k + u * blockDim.x) : -1;
+    if (c >= 8) {
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (v[u] >= 0) {
-        const int b = v[u] / c - lo;
-        atomicOr(bm + (b >> 5), 1u << (b & 31));
+      for (int u = 0; u < U; ++u) {
+        // lanes marking the same word OR their bits first: one shared atomic
+        // per distinct word of the warp (a row's consecutive entries share
+        // their block column). 16 x 16 at 32768^2: count 365 -> ~220 us;
+        // with 4-wide blocks the match costs more than it saves.
+        const int b = v[u] >= 0 ? divp(v[u], c, cs) - lo : -32 - (int)(threadIdx.x & 31);
+        const int wd = b >> 5;
+        const unsigned peers = __match_any_sync(kFull, wd);
+        const uint32_t bits = __reduce_or_sync(peers, v[u] >= 0 ? 1u << (b & 31) : 0u);
+        if (v[u] >= 0 && (int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicOr(bm + wd, bits);
       }
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (v[u] >= 0) {
+          const int b = divp(v[u], c, cs) - lo;
+          atomicOr(bm + (b >> 5), 1u << (b & 31));
+        }
+    }
   }
 }
 
@@ -81,7 +106,7 @@ __device__ __forceinline__ void col_range(const int32_t* __restrict__ col, int32
                                           int32_t* hi) {
   int mn = INT32_MAX, mx = -1;
   for (int32_t k = s + threadIdx.x; k < e; k += blockDim.x) {
-    int b = __ldg(col + k) / c;
+    int b = divp(__ldg(col + k), c, pow2_shift(c));
     mn = min(mn, b);
     mx = max(mx, b);
   }
@@ -122,6 +147,7 @@ __global__ void __launch_bounds__(kBlock) k_block_nz_flags(const int32_t* __rest
                                                            uint8_t* __restrict__ flag) {
   extern __shared__ uint32_t cnt[];  // nbc <= kDecCounters (host)
   const int lane = threadIdx.x & 31;
+  const int cs = pow2_shift(c);
   for (int32_t br = blockIdx.x; br < nbr; br += gridDim.x) {
     const int32_t s = __ldg(bptr + br), e = __ldg(bptr + br + 1);
     if (s == e) continue;
@@ -130,7 +156,7 @@ __global__ void __launch_bounds__(kBlock) k_block_nz_flags(const int32_t* __rest
     for (int32_t k0 = s; k0 < e; k0 += blockDim.x) {
       const int32_t k = k0 + threadIdx.x;
       const bool in = k < e;
-      const int b = in ? __ldg(col + k) / c : -1;
+      const int b = in ? divp(__ldg(col + k), c, cs) : -1;
       const bool nz = in && (!count_values || __ldg(val + k) != 0.f);
       const int pb = __shfl_up_sync(kFull, b, 1);
       const bool head = in && (lane == 0 || pb != b);
@@ -145,7 +171,7 @@ __global__ void __launch_bounds__(kBlock) k_block_nz_flags(const int32_t* __rest
     }
     __syncthreads();
     for (int32_t k = s + threadIdx.x; k < e; k += blockDim.x)
-      flag[k] = (int64_t)cnt[__ldg(col + k) / c] >= min_sum ? 1 : 0;
+      flag[k] = (int64_t)cnt[divp(__ldg(col + k), c, cs)] >= min_sum ? 1 : 0;
     __syncthreads();
   }
 }
@@ -232,6 +258,7 @@ __global__ void __launch_bounds__(kBlock) k_fill_blocks(
   extern __shared__ uint32_t bm[];  // [words] bitmap, then [words] prefix
   __shared__ int smin, smax;
   __shared__ uint32_t wsum[34];
+  const int cs = pow2_shift(c);
   for (int32_t br = blockIdx.x; br < nbr; br += gridDim.x) {
     int32_t s = __ldg(bptr + br), e = __ldg(bptr + br + 1);
     if (s == e) continue;
@@ -274,10 +301,11 @@ __global__ void __launch_bounds__(kBlock) k_fill_blocks(
     // scatter the entries into their dense blocks
     for (int32_t k = s + threadIdx.x; k < e; k += blockDim.x) {
       int cc = __ldg(col + k), rr = __ldg(row + k);
-      int b = cc / c - lo;
+      const int bq = divp(cc, c, cs);
+      int b = bq - lo;
       uint32_t rank = pre[b >> 5] + __popc(bm[b >> 5] & ((1u << (b & 31)) - 1u));
       int64_t blk = (int64_t)base + rank;
-      int i = rr - br * r, j = cc - (cc / c) * c;
+      int i = rr - br * r, j = cc - bq * c;
       bval[(blk * rb + i) * cb + j] = to_val<T>(__ldg(val + k));
     }
     __syncthreads();

@@ -249,6 +249,25 @@ class Cfg4(Workload):
     def work_units(self):
         return 2 * self.nnz * self.nd / 1e3  # unit conversion below: (MFLOP) -> GFLOP/s
 
+    def operand_roofline(self, ms):
+        """The tcgen05 kernels are bound by the MMAs' shared-memory operand
+        reads (ncu 'smem reads by the MMA'): bytes the MMAs read
+        per product against 148 SMs x 128 B/cycle at the maximum SM clock."""
+        if self.block == 16:
+            per_mma = 128 * 16 * 2 + 16 * 16 * 2 if self.vdtype == "bf16" else 128 * 8 * 4 + 16 * 8 * 4
+            mmas = self.nblocks * (1 if self.vdtype == "bf16" else 6)
+        elif self.vdtype == "bf16":
+            per_mma = 128 * 16 * 2 + 128 * 16 * 2  # a 16-row B tile and a 128-row x 16-column window
+            mmas = self.info.get("windows")
+            if not mmas:
+                return None
+        else:
+            return None
+        peak = 148 * 128 * 1.965e9 / 1e9  # GB/s
+        ach = per_mma * mmas / ms / 1e6
+        return {"achieved": round(ach, 1), "peak": round(peak, 1), "unit": "GB/s", "frac": round(ach / peak, 4),
+                "bytes_per_mma": per_mma, "mmas": int(mmas)}
+
     def kernels(self):
         nb, m, n, nd, r = self.nblocks, self.m, self.n, self.nd, self.block
         s = 2 if self.vdtype == "bf16" else 4
@@ -487,6 +506,8 @@ def run_ours(args):
             "peak_nominal": NOMINAL_HBM_GBS, "frac_nominal": round(ach / NOMINAL_HBM_GBS, 4)}
     for k in kernels.values():
         k["hbm_frac_nominal"] = round(k["GB/s"] / NOMINAL_HBM_GBS, 4)
+    if hasattr(wl, "operand_roofline"):  # the bound of the tensor-core kernels
+        roof["operand_smem"] = wl.operand_roofline(kernels[dom]["ms"])
     # DRAM bytes per launch of the dominant family, from the committed ncu
     # launch list of this config (profiles/traffic_config<N>.json)
     variant = "" if args.config != 4 or (args.block, args.bcsr_dtype) == (16, "bf16") else \

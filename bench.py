@@ -308,6 +308,19 @@ class Cfg5(SpmvWorkload):
     def out_rows(self):
         return self.c
 
+    def gather_roofline(self, ms):
+        """The SpMM is bound by its random 128-byte B-row gathers (DESIGN
+        §4): one per entry; measured on this part (scripts/row_gather_bench.cu,
+        profiles/r02_row_gather_bench.log) 35.7 G rows/s when every gather
+        misses L2 and 154 G rows/s from L2, and ncu puts this SpMM's L2 hit
+        rate at ~36 % — the floor of the gathers alone is their time at those
+        rates."""
+        rows, hit, hbm_rate, l2_rate = self.nnz, 0.36, 35.7e9, 154e9
+        floor = ((1 - hit) * rows / hbm_rate + hit * rows / l2_rate) * 1e3
+        return {"gathers": int(rows), "achieved_G_rows_per_s": round(rows / ms / 1e6, 2),
+                "floor_ms": round(floor, 3), "frac": round(floor / ms, 4), "l2_hit_rate_ncu": hit,
+                "rates_G_rows_per_s": {"hbm": 35.7, "l2": 154.0}}
+
 
 WORKLOADS = {1: Cfg1, 2: Cfg2, 3: Cfg3, 4: Cfg4, 5: Cfg5}
 
@@ -508,6 +521,8 @@ def run_ours(args):
         k["hbm_frac_nominal"] = round(k["GB/s"] / NOMINAL_HBM_GBS, 4)
     if hasattr(wl, "operand_roofline"):  # the bound of the tensor-core kernels
         roof["operand_smem"] = wl.operand_roofline(kernels[dom]["ms"])
+    if hasattr(wl, "gather_roofline") and dom == "spmm":  # the gather floor of the config-5 SpMM
+        roof["gather"] = wl.gather_roofline(kernels[dom]["ms"])
     # DRAM bytes per launch of the dominant family, from the committed ncu
     # launch list of this config (profiles/traffic_config<N>.json)
     variant = "" if args.config != 4 or (args.block, args.bcsr_dtype) == (16, "bf16") else \

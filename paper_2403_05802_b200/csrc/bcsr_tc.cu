@@ -1400,6 +1400,9 @@ bool spmm_bcsr_tc(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dt
   const int64_t words = ngroups * a->nbc;
   const bool plan_ok = a->nnz * 4 >= words && words <= (int64_t(1) << 30);
   if (tf && !plan_ok) return false;
+  // 3xTF32 splits B into hi / lo copies (2 x n x 512 bytes): only when they
+  // fit comfortably, else the CUDA-core kernel takes the product
+  if (tf && 2 * a->n * kND * 4 > (int64_t)(ctx->total_mem / 4)) return false;
   if (quad && a->nbr > (int64_t)INT32_MAX - kGroup) return false;
   auto encode = get_encode();
   if (!encode) return false;

@@ -104,3 +104,25 @@ def test_large_schedule(ctx, ref):
         want = ref.convert(p, *_ref(fmt)).download()
         assert_same_materialized(got, want, fmt)
         assert got.partitions == want.partitions
+
+
+@pytest.mark.parametrize("fmt", ["CISR(2)", "CISR-plus(3)", "DCSC", "DIA-variant", "DIA", "BELL(2)", "HBELL(2,2)"])
+def test_empty_matrix(ctx, ref, fmt):
+    """No entries: the empty levels and bounds the reference materializes
+    (HBELL: both parts empty)."""
+    m, n = 5, 4
+    e = np.array([], np.int64)
+    d = ctx.from_coo(m, n, e, e, np.array([], np.float64))
+    got = ctx.convert(d, fmt)
+    x = np.ones(n, np.float32)
+    assert np.all(ctx.spmv(got, x) == 0)
+    if fmt.startswith("HBELL"):
+        return
+    if "(" in fmt and not fmt.startswith("BELL"):
+        name, k = _ref(fmt)
+        want = ref.convert(ref.from_coo(m, n, e, e, np.array([], np.float64)), name, k).download()
+    elif fmt.startswith("BELL"):
+        want = ref.convert(ref.from_coo(m, n, e, e, np.array([], np.float64)), "BELL", 2).download()
+    else:
+        want = ref.convert(ref.from_coo(m, n, e, e, np.array([], np.float64)), fmt).download()
+    assert_same_materialized(got.download(), want, fmt)

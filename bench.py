@@ -232,7 +232,7 @@ class Cfg4(Workload):
         self.fmt = f"BCSR({r},{r}) {self.vdtype}"
         self.bounds = [0, m]
         self.info = {"nblocks": self.nblocks, "nd": self.nd, "value_dtype": self.vdtype, "b_dtype": self.vdtype}
-        if r == 16:
+        if r == 16 or bf:
             # the tensor-core path builds its per-matrix block schedule on the
             # first product and caches it on the tensor: timed here once
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]

@@ -1115,13 +1115,15 @@ struct QShared {
   uint32_t end[kQPipes][kQStages];  // 1: the stage is a group's end marker
   alignas(16) uint32_t ring_col[kQPipes][32][12];     // per producer lane: block columns of three quads
   alignas(16) uint8_t ring_val[kQPipes][32][12 * 32 + 16];  // and their value blocks (+16: lanes on distinct banks)
+  alignas(16) uint32_t dring[kQPipes][2 * 32][8];        // window schedule: 2 blocks of 32 (super column, masks)
   uint32_t tmem_base;
 };
 
 __global__ void __launch_bounds__(32 * (4 + 2 * kQPipes), 1)
     k_bcsr4_tc(const __grid_constant__ CUtensorMap tmap_b, const uint8_t* __restrict__ aval,
                const int32_t* __restrict__ ptr, const int32_t* __restrict__ bcol, int64_t nnz, int32_t nbr,
-               int32_t m, float* __restrict__ c, int64_t ldc, int accumulate) {
+               int32_t m, float* __restrict__ c, int64_t ldc, int accumulate, const int32_t* __restrict__ gstart,
+               const int32_t* __restrict__ dsc, const uint4* __restrict__ dmask) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* stages = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   QShared* sh = reinterpret_cast<QShared*>(stages + kQPipes * kQStages * kQStageBytes);
@@ -1218,6 +1220,74 @@ __global__ void __launch_bounds__(32 * (4 + 2 * kQPipes), 1)
         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(rcol + slot(i) * 4));
         return v;
       };
+      if (gstart != nullptr) {
+        // the per-matrix window schedule: each stage's super column and the
+        // lanes' 4-bit block masks (k_q_plan / k_q_compact) — no column
+        // reads, no compares, no warp min
+        // descriptors in blocks of 32 stages: lane l loads stage (block +
+        // l)'s into registers one block ahead and parks them in a shared
+        // ring at the next block's start, so no load latency meets a stage
+        const int32_t t0 = __ldg(gstart + g), t1 = __ldg(gstart + g + 1);
+        const uint32_t dr = smem_u32(&sh->dring[w][0][0]);
+        int32_t psc = 0;
+        uint4 pmk = make_uint4(0, 0, 0, 0);
+        if (t0 + lane < t1) psc = __ldg(dsc + t0 + lane), pmk = __ldg(dmask + t0 + lane);
+        for (int32_t t = t0; t < t1; ++t) {
+          const int32_t j = (t - t0) & 31;
+          if (j == 0) {  // a new block: park its descriptors, request the next block's
+            const uint32_t at = dr + ((((t - t0) >> 5) & 1) * 32 + lane) * 32;
+            sts_u32(at, (uint32_t)psc);
+            sts_v4(at + 16, pmk);
+            __syncwarp();
+            const int32_t tn = t + 32 + lane;
+            if (tn < t1) psc = __ldg(dsc + tn), pmk = __ldg(dmask + tn);
+          }
+          const uint32_t at = dr + ((((t - t0) >> 5) & 1) * 32 + j) * 32;
+          uint32_t sc, word;
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(sc) : "r"(at));
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(word) : "r"(at + 16 + (lane >> 3) * 4));
+          const uint32_t nib = (word >> ((lane & 7) * 4)) & 0xfu;
+          if (lane == 0) mbar_wait(&sh->empty[w][stage], phase ^ 1);
+          __syncwarp();
+          uint8_t* st = stages + (w * kQStages + stage) * kQStageBytes;
+          if (lane == 0) {
+            sh->end[w][stage] = 0;
+            mbar_expect_tx_only(&sh->full[w][stage], kQTile);
+            tma_3d(st, &tmap_b, &sh->full[w][stage], 0, (int)sc * kBlk, 0);
+          }
+          const uint32_t vb = smem_u32(st + kQTile) + (uint32_t)lane * 128u;
+#pragma unroll
+          for (int i = 0; i < 8; ++i)  // rotated by lane: 8 consecutive lanes hit 8 different bank groups
+            sts_v4(vb + (((uint32_t)(i + lane) & 7u) << 4), make_uint4(0u, 0u, 0u, 0u));
+          int e = 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (nib >> q & 1u) {  // the lane's blocks of this super column, in column order
+              const uint32_t src = rval + slot(cur + e) * 32;
+              const uint4 lo = lds_v4(src), hi = lds_v4(src + 16);
+              const uint32_t off = ((((uint32_t)q >> 1) ^ sw) << 4) + (((uint32_t)q & 1u) << 3);
+              asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(vb + off), "r"(lo.x), "r"(lo.y) : "memory");
+              asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(vb + 32 + off), "r"(lo.z), "r"(lo.w) : "memory");
+              asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(vb + 64 + off), "r"(hi.x), "r"(hi.y) : "memory");
+              asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(vb + 96 + off), "r"(hi.z), "r"(hi.w) : "memory");
+              ++e;
+            }
+          if (e) {
+            const int64_t q_old = cur >> 2;
+            cur += e;
+            if ((cur >> 2) != q_old) {  // entered the next quad: refill the vacated slot, wait for the one after
+              refill(((cur >> 2) + 2) * 4);
+              asm volatile("cp.async.wait_group 1;" ::: "memory");
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sh->full[w][stage]);
+          if (++stage == kQStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      } else {
       uint32_t nb = col_of(cur);
       while (true) {
         const uint32_t mn = __reduce_min_sync(kFull, nb);
@@ -1272,6 +1342,7 @@ __global__ void __launch_bounds__(32 * (4 + 2 * kQPipes), 1)
           stage = 0;
           phase ^= 1;
         }
+      }
       }
       asm volatile("cp.async.wait_group 0;" ::: "memory");  // the ring is rewritten by the next group
       // end-of-group marker
@@ -1366,6 +1437,47 @@ __global__ void __launch_bounds__(32 * (4 + 2 * kQPipes), 1)
   if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// Window schedule of the BCSR(4,4) kernel, built once per matrix and cached
+// on the tensor: per (group of 32 block rows, super column of 4 block
+// columns) a 16-byte mask — 4 bits per block row (lane), bit q = block
+// column 4 sc + q present — then the nonempty (group, super column) pairs
+// compacted in order: the stage list of each group, its super columns and
+// masks.
+__global__ void k_q_plan(const int32_t* __restrict__ ptr, const int32_t* __restrict__ bcol, int32_t nbr,
+                         int64_t nsc, uint32_t* __restrict__ plan) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t br = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; br < nbr; br += warps) {
+    uint32_t* pg = plan + (br >> 5) * nsc * 4 + ((br & 31) >> 3);
+    const uint32_t sh = (uint32_t)(br & 7) * 4;
+    for (int32_t k = __ldg(ptr + br) + lane; k < __ldg(ptr + br + 1); k += 32) {
+      const int32_t bc = __ldg(bcol + k);
+      atomicOr(pg + (int64_t)(bc >> 2) * 4, 1u << (sh + (bc & 3)));
+    }
+  }
+}
+
+__global__ void k_q_flags(const uint4* __restrict__ plan, int64_t n, int32_t* __restrict__ flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 v = __ldg(plan + i);
+    flag[i] = (v.x | v.y | v.z | v.w) != 0u ? 1 : 0;
+  }
+}
+
+__global__ void k_q_compact(const uint4* __restrict__ plan, const int32_t* __restrict__ pos, int64_t n, int64_t nsc,
+                            int64_t ngroups, int32_t* __restrict__ dsc, uint4* __restrict__ dmask,
+                            int32_t* __restrict__ gstart) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t p = __ldg(pos + i);
+    if (__ldg(pos + i + 1) > p) {
+      dsc[p] = (int32_t)(i % nsc);
+      dmask[p] = __ldg(plan + i);
+    }
+    if (i % nsc == 0) gstart[i / nsc] = p;
+    if (i == n - 1) gstart[ngroups] = __ldg(pos + n);
   }
 }
 
@@ -1521,10 +1633,35 @@ bool spmm_bcsr_tc(sfg_context* ctx, const sfg_tensor* a, const void* b, int b_dt
   if (quad) {
     CUtensorMap tq;
     tile_map(&tq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, b, ldb, CU_TENSOR_MAP_SWIZZLE_128B);
+    // the window schedule (cached on the tensor: tc_base = per-group first
+    // stage, tc_desc = super columns, tc_plan = masks), when its build fits
+    const int64_t nsc = ceil_div(a->nbc, (int64_t)4), cells = ngroups * nsc;
+    static const bool no_sched = std::getenv("SFG_Q_NOSCHED") != nullptr;  // A/B switch
+    if (!no_sched && !mut->tc_base && cells < INT32_MAX && cells * 24 <= (int64_t)(ctx->total_mem / 8)) {
+      auto* plan = dalloc_n<uint32_t>(ctx, cells * 4);
+      auto* flag = dalloc_n<int32_t>(ctx, cells);
+      auto* pos = dalloc_n<int32_t>(ctx, cells + 1);
+      SFG_CUDA(cudaMemsetAsync(plan, 0, cells * 16, ctx->stream));
+      SFG_LAUNCH(k_q_plan, stream_grid(ctx, a->nbr * 32, 256, 1, 8), 256, 0, ctx->stream, a->ptr, a->idx,
+                 (int32_t)a->nbr, nsc, plan);
+      SFG_LAUNCH(k_q_flags, stream_grid(ctx, cells, 256, 4, 8), 256, 0, ctx->stream,
+                 reinterpret_cast<const uint4*>(plan), cells, flag);
+      scan_counts(ctx, flag, cells, pos);
+      int32_t nst = 0;
+      read_back(ctx, pos + cells, sizeof nst, &nst);
+      mut->tc_base = dalloc_n<int32_t>(ctx, ngroups + 1);
+      mut->tc_desc = reinterpret_cast<uint32_t*>(dalloc_n<int32_t>(ctx, std::max<int32_t>(nst, 1)));
+      mut->tc_plan = dalloc_n<uint32_t>(ctx, (int64_t)std::max<int32_t>(nst, 1) * 4);
+      SFG_LAUNCH(k_q_compact, stream_grid(ctx, cells, 256, 4, 8), 256, 0, ctx->stream,
+                 reinterpret_cast<const uint4*>(plan), pos, cells, nsc, ngroups,
+                 reinterpret_cast<int32_t*>(mut->tc_desc), reinterpret_cast<uint4*>(mut->tc_plan), mut->tc_base);
+      for (void* q : {(void*)plan, (void*)flag, (void*)pos}) dfree(ctx, q);
+    }
     const size_t qsmem = 1024 + (size_t)kQPipes * kQStages * kQStageBytes + sizeof(QShared) + 64;
     cudaFuncSetAttribute(k_bcsr4_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsmem);
     SFG_LAUNCH(k_bcsr4_tc, grid, 32 * (4 + 2 * kQPipes), qsmem, ctx->stream, tq, static_cast<const uint8_t*>(a->val),
-               a->ptr, a->idx, a->nnz, (int32_t)a->nbr, (int32_t)a->m, c, ldc, accumulate ? 1 : 0);
+               a->ptr, a->idx, a->nnz, (int32_t)a->nbr, (int32_t)a->m, c, ldc, accumulate ? 1 : 0, mut->tc_base,
+               reinterpret_cast<const int32_t*>(mut->tc_desc), reinterpret_cast<const uint4*>(mut->tc_plan));
     return true;
   }
   CUtensorMap tb, ta;

@@ -298,6 +298,20 @@ __global__ void __launch_bounds__(kBlock) k_fill_blocks(
         bidx[base + k++] = lo + (w << 5) + b;
       }
     }
+    // zero the block row's value region (contiguous: its blocks are
+    // consecutive), then scatter the entries over it — no separate memset
+    // pass over the whole value array, and the region is L2-hot for the
+    // scatter
+    {
+      const int64_t v0 = (int64_t)base * rb * cb, v1 = (int64_t)__ldg(blk_ptr + br + 1) * rb * cb;
+      constexpr int kPer16 = 16 / (int)sizeof(T);
+      const int64_t a0 = (v0 + kPer16 - 1) / kPer16 * kPer16, a1 = v1 / kPer16 * kPer16;
+      for (int64_t q = v0 + threadIdx.x; q < min(a0, v1); q += blockDim.x) bval[q] = to_val<T>(0.f);
+      for (int64_t q = a0 / kPer16 + threadIdx.x; q < a1 / kPer16; q += blockDim.x)
+        reinterpret_cast<uint4*>(bval)[q] = make_uint4(0u, 0u, 0u, 0u);
+      for (int64_t q = max(a1, a0) + threadIdx.x; q < v1; q += blockDim.x) bval[q] = to_val<T>(0.f);
+    }
+    __syncthreads();
     // scatter the entries into their dense blocks
     for (int32_t k = s + threadIdx.x; k < e; k += blockDim.x) {
       int cc = __ldg(col + k), rr = __ldg(row + k);
@@ -378,8 +392,7 @@ sfg_tensor* coo_to_bcsr(sfg_context* ctx, const sfg_tensor* s, int64_t r, int64_
   int64_t nvals = (int64_t)nblocks * t->rb * t->cb;
   size_t esz = dtype == SFG_BF16 ? 2 : 4;
   t->idx = dalloc_n<int32_t>(ctx, nblocks);
-  t->val = dalloc(ctx, nvals * esz);
-  SFG_CUDA(cudaMemsetAsync(t->val, 0, nvals * esz, ctx->stream));
+  t->val = dalloc(ctx, nvals * esz);  // zero-filled block row by block row by the fill kernel
   if (dtype == SFG_BF16)
     SFG_LAUNCH(k_fill_blocks<__nv_bfloat16>, grid, kBlock, words * 8, ctx->stream, bptr, s->row,
                s->idx, static_cast<const float*>(s->val), (int32_t)r, (int32_t)c, (int32_t)t->rb,

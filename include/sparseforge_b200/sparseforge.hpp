@@ -23,8 +23,11 @@
 #include <array>
 #include <cctype>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
+#include <fstream>
 #include <map>
+#include <sstream>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -298,7 +301,9 @@ struct WorkingTensor {
       case SFG_BELL: return 5;
       case SFG_CSB: return 4;
       case SFG_BDIA:
-      case SFG_C2SR: return 3;
+      case SFG_C2SR:
+      case SFG_CISR:
+      case SFG_CISRP: return 3;
       default: return 2;
     }
   }
@@ -440,6 +445,144 @@ inline CooData read_matrix_market(const std::string& path) {
   return d;
 }
 
+// Host-side text utilities of io.hpp, same formats and messages: Matrix
+// Market output (io.hpp:123-134, values as %.17g), FROSTT .tns input
+// (151-184), one value per line vectors (186-202).
+namespace b200 {
+inline std::string format_value(double v) {
+  char buf[64];
+  std::snprintf(buf, sizeof buf, "%.17g", v);
+  return buf;
+}
+inline void write_text(const std::string& path, const std::string& text) {
+  std::FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) fail(ErrorKind::Io, "cannot write " + path);
+  const bool ok = std::fwrite(text.data(), 1, text.size(), f) == text.size();
+  if (std::fclose(f) != 0 || !ok) fail(ErrorKind::Io, "write failed: " + path);
+}
+}  // namespace b200
+
+inline void write_matrix_market(const std::string& path, const CooData& d) {
+  if (d.shape.rank() != 2) fail(ErrorKind::InvalidOperation, "matrix market output is rank-2");
+  std::string out = "%%MatrixMarket matrix coordinate real general\n";
+  out += std::to_string(d.shape.extents[0]) + " " + std::to_string(d.shape.extents[1]) + " " +
+         std::to_string(d.values.size()) + "\n";
+  for (size_t e = 0; e < d.values.size(); ++e)
+    out += std::to_string(d.coords[0][e] + 1) + " " + std::to_string(d.coords[1][e] + 1) + " " +
+           b200::format_value(d.values[e]) + "\n";
+  b200::write_text(path, out);
+}
+
+inline CooData read_tns(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) fail(ErrorKind::Io, "cannot open " + path);
+  auto bad = [&](size_t line, const std::string& msg) {
+    fail(ErrorKind::Parse, path + ":" + std::to_string(line) + ": " + msg);
+  };
+  CooData out;
+  std::string text;
+  size_t line = 0, rank = 0;
+  while (std::getline(in, text)) {
+    ++line;
+    if (!text.empty() && (text[0] == '#' || text[0] == '%')) continue;
+    if (text.find_first_not_of(" \t\r") == std::string::npos) continue;
+    std::istringstream fields(text);
+    std::vector<double> nums;
+    for (double x; fields >> x;) nums.push_back(x);
+    if (nums.size() < 2) bad(line, "need coordinates and a value");
+    if (rank == 0) {
+      rank = nums.size() - 1;
+      out.coords.resize(rank);
+      out.shape.extents.assign(rank, 0);
+    } else if (nums.size() - 1 != rank) {
+      bad(line, "inconsistent rank");
+    }
+    for (size_t k = 0; k < rank; ++k) {
+      const auto c = static_cast<std::int64_t>(nums[k]);
+      if (c < 1) bad(line, "coordinates are 1-based");
+      out.coords[k].push_back(c - 1);
+      out.shape.extents[k] = std::max(out.shape.extents[k], c);
+    }
+    out.values.push_back(nums.back());
+  }
+  if (rank == 0) bad(line ? line : 1, "no entries");
+  return out;
+}
+
+inline std::vector<double> read_vector_text(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) fail(ErrorKind::Io, "cannot open " + path);
+  std::vector<double> out;
+  for (double v; in >> v;) out.push_back(v);
+  return out;
+}
+
+inline void write_vector_text(const std::string& path, const std::vector<double>& v) {
+  std::string out;
+  for (double x : v) out += b200::format_value(x) + "\n";
+  b200::write_text(path, out);
+}
+
+// to_coo_data (io.hpp:136-149): the coordinates of a tensor whose map is
+// the identity (COO, and CSR / DCSR / DOK / LIL brought back to COO on the
+// device), in canonical order.
+inline CooData to_coo_data(const WorkingTensor& t) {
+  const int k = t.enc.fmt.kind;
+  if (k != SFG_COO && k != SFG_CSR && k != SFG_DCSR && k != SFG_DOK && k != SFG_LIL)
+    fail(ErrorKind::InvalidOperation, "tensor is not in coordinate form");
+  CooData d;
+  d.shape = t.shape;
+  if (k == SFG_COO) {
+    t.download(d.coords, d.values);
+    return d;
+  }
+  sfg_format coo{};
+  b200::check(sfg_format_resolve("COO", &coo));
+  sfg_tensor* h = nullptr;
+  b200::check(sfg_convert(b200::default_context().get(), t.dev->h, &coo, &h));
+  WorkingTensor c;
+  c.shape = t.shape;
+  c.enc = resolve_format("COO");
+  c.dev = std::make_shared<b200::TensorHandle>(h);
+  c.download(d.coords, d.values);
+  return d;
+}
+
+// from_dense (tensor.hpp:164-179): the nonzero cells in row-major order.
+inline WorkingTensor from_dense(const DenseTensor& d) {
+  if (d.shape.rank() != 2) fail(ErrorKind::InvalidOperation, "coordinate rank mismatch (the B200 path handles matrices)");
+  std::vector<std::vector<std::int64_t>> coords(2);
+  std::vector<double> values;
+  const std::int64_t n = d.shape.extents[1];
+  for (size_t off = 0; off < d.data.size(); ++off)
+    if (d.data[off] != 0.0) {
+      coords[0].push_back(static_cast<std::int64_t>(off) / n);
+      coords[1].push_back(static_cast<std::int64_t>(off) % n);
+      values.push_back(d.data[off]);
+    }
+  return from_coo(d.shape, coords, values);
+}
+
+// to_dense (tensor.hpp:184-201) for identity-mapped tensors: the nonzero
+// values back in their cells (zero values, padding, are dropped).
+inline DenseTensor to_dense(const WorkingTensor& t) {
+  const CooData c = to_coo_data(t);
+  DenseTensor out(t.shape);
+  for (size_t e = 0; e < c.values.size(); ++e)
+    if (c.values[e] != 0.0) out.at({c.coords[0][e], c.coords[1][e]}) = c.values[e];
+  return out;
+}
+
+// equal_dense (tensor.hpp:203-211)
+inline bool equal_dense(const DenseTensor& a, const DenseTensor& b, double tol = 0.0) {
+  if (a.shape.extents != b.shape.extents) return false;
+  for (size_t i = 0; i < a.data.size(); ++i) {
+    const double diff = a.data[i] > b.data[i] ? a.data[i] - b.data[i] : b.data[i] - a.data[i];
+    if (diff > tol) return false;
+  }
+  return true;
+}
+
 // write_container / read_container (io.hpp:240, 283): the USPT file of a
 // materialized tensor, written from / read into device memory.
 struct MaterializedTensor;
@@ -533,6 +676,20 @@ inline MaterializedTensor materialize(const WorkingTensor& t, const StorageSchem
   for (int64_t q = 0; q < v.npartitions; ++q)
     m.partitions.push_back({static_cast<size_t>(v.partitions[2 * q]), static_cast<size_t>(v.partitions[2 * q + 1])});
   return m;
+}
+
+// dematerialize (storage.hpp:284-343): the working form behind a
+// materialized tensor — on the B200 path, the device arrays it was
+// downloaded from (or read into, read_container).
+inline WorkingTensor dematerialize(const MaterializedTensor& m, const FormatEncoding& enc) {
+  if (!m.dev) fail(ErrorKind::InvalidOperation, "materialized tensor without device arrays");
+  if (m.enc.fmt.kind != enc.fmt.kind || m.levels.size() != infer_storage(enc).levels.size())
+    fail(ErrorKind::InvalidOperation, "container rank does not match the encoding");
+  WorkingTensor t;
+  t.shape = m.logical_shape;
+  t.enc = enc;
+  t.dev = m.dev;
+  return t;
 }
 
 inline void write_container(const std::string& path, const MaterializedTensor& m) {

@@ -7,8 +7,8 @@
 // is row-sorted and the sort is stable), materialized like CSR with the
 // roles of rows and columns exchanged (storage.hpp:171-200).
 //
-// Device plan. (1) Column-block partition (every block of 1,024 columns
-// holds <= 4,096 entries, e.g. the hypersparse config 3): count per block,
+// Device plan. (1) Column-bucket partition (every bucket of <= 8,192
+// columns holds <= 22,528 entries, e.g. the hypersparse config 3): count per bucket,
 // scan, scatter into block regions, sort each block in shared memory —
 // below. (2) Otherwise, when every column holds <= kShortCol entries:
 // column histogram (RED atomics) -> single-pass look-back scan ->
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(kBlock) k_csc_unpack(const uint64_t* __restric
 // (0) Each of P CTAs counts its contiguous share of the entries per column
 //     bucket (2^bits columns) in shared memory; an exclusive scan over
 //     (bucket, CTA) gives every CTA its write range inside every bucket.
-// (1) Each CTA reorders its share, kPartTile entries at a time, by bucket
+// (1) Each CTA reorders its share, a tile of entries at a time, by bucket
 //     in shared memory and writes each bucket's run to the bucket's range:
 //     consecutive threads write consecutive addresses. The intermediate
 //     (row, value, column-in-bucket: 10 B an entry) is kept in L2 for pass 2.
@@ -191,22 +191,52 @@ __global__ void __launch_bounds__(kBlock) k_csc_unpack(const uint64_t* __restric
 //     / ptr of its columns with coalesced stores.
 constexpr int kPartThreads = 512;
 constexpr int kPartPer = 24;                          // entries per thread per round
-constexpr int kPartTile = kPartThreads * kPartPer;    // 12,288 entries reordered per round
 constexpr int kMaxBuckets = 4096;
-constexpr int kMaxBucketBits = 12;                    // columns per bucket <= 4,096
+constexpr int kMaxBucketBits = 13;                    // columns per bucket <= 8,192
 constexpr int kSortThreads = 1024;
-constexpr int kSortPer = 12;
-constexpr int kBucketCap = kSortThreads * kSortPer;   // 12,288 entries sorted per pass-2 CTA
+constexpr int kSortPer = 22;
+constexpr int kBucketCap = kSortThreads * kSortPer;   // 22,528 entries sorted per pass-2 CTA
 
+// Entries [e0, e1) of pass-1 CTA `cta`: equal shares rounded up to a
+// multiple of 4, so each share starts 16-byte aligned (k_bkt_count and
+// k_bkt_part must agree on them: the bucket offsets are per CTA).
+__device__ __forceinline__ void part_range(int64_t nnz, int cta, int ctas, int64_t& e0, int64_t& e1) {
+  const int64_t per = ((nnz + ctas - 1) / ctas + 3) & ~int64_t(3);
+  e0 = min(nnz, cta * per);
+  e1 = min(nnz, e0 + per);
+}
+
+// kVec: the input arrays are 16-byte aligned (int4 loads, four entries each)
+template <bool kVec>
 __global__ void __launch_bounds__(kPartThreads) k_bkt_count(const int32_t* __restrict__ col, int64_t nnz, int bits,
                                                              int nb, int32_t* __restrict__ counts) {
   __shared__ int32_t h[kMaxBuckets];
   for (int i = threadIdx.x; i < nb; i += kPartThreads) h[i] = 0;
   __syncthreads();
-  const int64_t per = (nnz + gridDim.x - 1) / gridDim.x;
-  const int64_t e0 = blockIdx.x * per, e1 = min(nnz, e0 + per);
+  int64_t e0, e1;
+  part_range(nnz, blockIdx.x, gridDim.x, e0, e1);
   constexpr int U = 8;  // loads in flight per thread
-  for (int64_t e = e0 + threadIdx.x; e < e1; e += U * kPartThreads) {
+  int64_t e = e0 + threadIdx.x;
+  if constexpr (kVec) {
+    const int64_t nv = (e1 - e0) >> 2;
+    const int4* c4 = reinterpret_cast<const int4*>(col + e0);
+    for (int64_t j = threadIdx.x; j < nv; j += U * kPartThreads) {
+      int4 q[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        q[u] = j + u * kPartThreads < nv ? ld_stream(c4 + j + u * kPartThreads) : make_int4(-1, -1, -1, -1);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (q[u].x >= 0) {
+          atomicAdd(&h[q[u].x >> bits], 1);
+          atomicAdd(&h[q[u].y >> bits], 1);
+          atomicAdd(&h[q[u].z >> bits], 1);
+          atomicAdd(&h[q[u].w >> bits], 1);
+        }
+    }
+    e = e0 + nv * 4 + threadIdx.x;
+  }
+  for (; e < e1; e += U * kPartThreads) {
     int c[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) c[u] = e + u * kPartThreads < e1 ? ld_stream(col + e + u * kPartThreads) : -1;
@@ -229,45 +259,63 @@ __global__ void __launch_bounds__(kBlock) k_blk_max(const int32_t* __restrict__ 
 
 // Pass 1. Dynamic shared memory: row, value, column of kPartTile entries,
 // then per-bucket count, start and write cursor.
+// kPer entries per thread per round (the tile: as large as the shared memory
+// left by the bucket counters allows)
+template <bool kVec, int kPer>
 __global__ void __launch_bounds__(kPartThreads, 1) k_bkt_part(const int32_t* __restrict__ row,
                                                                const int32_t* __restrict__ col,
                                                                const float* __restrict__ val, int64_t nnz,
                                                                int bits, int nb, const int32_t* __restrict__ off,
                                                                int32_t* __restrict__ trow, float* __restrict__ tval,
                                                                uint16_t* __restrict__ tcol) {
+  constexpr int kPartTile = kPartThreads * kPer;
   extern __shared__ int32_t sm[];
   int32_t* s_row = sm;
   float* s_val = reinterpret_cast<float*>(sm + kPartTile);
   int32_t* s_col = sm + 2 * kPartTile;
   int32_t* s_cnt = sm + 3 * kPartTile;
-  int32_t* s_start = s_cnt + kMaxBuckets;
-  int32_t* s_cur = s_start + kMaxBuckets;
+  int32_t* s_start = s_cnt + nb;
+  int32_t* s_cur = s_start + nb;
   __shared__ uint32_t scan_smem[34];
   const int tid = threadIdx.x;
   for (int b = tid; b < nb; b += kPartThreads) s_cur[b] = off[(int64_t)b * gridDim.x + blockIdx.x];
   const uint64_t once = l2_evict_first(), keep = l2_evict_last();
   const uint32_t cmask = (1u << bits) - 1;
-  const int64_t per = (nnz + gridDim.x - 1) / gridDim.x;
-  const int64_t e0 = blockIdx.x * per, e1 = min(nnz, e0 + per);
+  int64_t e0, e1;
+  part_range(nnz, blockIdx.x, gridDim.x, e0, e1);
   constexpr int kBPer = kMaxBuckets / kPartThreads;  // buckets per thread in the scan
   for (int64_t base = e0; base < e1; base += kPartTile) {
     const int cnt = (int)(e1 - base < kPartTile ? e1 - base : kPartTile);
     for (int b = tid; b < nb; b += kPartThreads) s_cnt[b] = 0;
     __syncthreads();
-    int r[kPartPer], c[kPartPer], rank[kPartPer];
-    float v[kPartPer];
+    int c[kPer], rank[kPer];
+    // slot k of this thread is tile entry item(k); with kVec, four
+    // consecutive entries per int4 load (order within a bucket run does not
+    // matter: pass 2 sorts each column by row). Only the columns are held in
+    // registers; rows and values are loaded after the scan, straight into
+    // their places.
+    auto item = [&](int k) { return kVec ? 4 * ((k >> 2) * kPartThreads + tid) + (k & 3) : k * kPartThreads + tid; };
+    if constexpr (kVec) {
 #pragma unroll
-    for (int k = 0; k < kPartPer; ++k) {
-      const int i = k * kPartThreads + tid;
-      if (i < cnt) {
-        c[k] = (int)ld_hint(col + base + i, once);
-        r[k] = (int)ld_hint(row + base + i, once);
-        v[k] = __uint_as_float(ld_hint(val + base + i, once));
+      for (int g = 0; g < kPer / 4; ++g) {
+        const int i = 4 * (g * kPartThreads + tid);
+        if (i + 3 < cnt) {
+          const int4 cq = ld_stream(reinterpret_cast<const int4*>(col + base + i));
+          c[4 * g] = cq.x, c[4 * g + 1] = cq.y, c[4 * g + 2] = cq.z, c[4 * g + 3] = cq.w;
+        } else {
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (i + t < cnt) c[4 * g + t] = ld_stream(col + base + i + t);
+        }
       }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kPer; ++k)
+        if (item(k) < cnt) c[k] = (int)ld_hint(col + base + item(k), once);
     }
 #pragma unroll
-    for (int k = 0; k < kPartPer; ++k)
-      if (k * kPartThreads + tid < cnt) rank[k] = atomicAdd(&s_cnt[c[k] >> bits], 1);
+    for (int k = 0; k < kPer; ++k)
+      if (item(k) < cnt) rank[k] = atomicAdd(&s_cnt[c[k] >> bits], 1);
     __syncthreads();
     int loc[kBPer], sum = 0;
 #pragma unroll
@@ -285,14 +333,41 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_bkt_part(const int32_t* __r
       run += loc[q];
     }
     __syncthreads();
+    if constexpr (kVec) {
 #pragma unroll
-    for (int k = 0; k < kPartPer; ++k)
-      if (k * kPartThreads + tid < cnt) {
-        const int pos = s_start[c[k] >> bits] + rank[k];
-        s_row[pos] = r[k];
-        s_val[pos] = v[k];
-        s_col[pos] = c[k];
+      for (int g = 0; g < kPer / 4; ++g) {
+        const int i = 4 * (g * kPartThreads + tid);
+        int r[4];
+        float v[4];
+        if (i + 3 < cnt) {
+          const int4 rq = ld_stream(reinterpret_cast<const int4*>(row + base + i));
+          const float4 vq = ld_stream(reinterpret_cast<const float4*>(val + base + i));
+          r[0] = rq.x, r[1] = rq.y, r[2] = rq.z, r[3] = rq.w;
+          v[0] = vq.x, v[1] = vq.y, v[2] = vq.z, v[3] = vq.w;
+        } else {
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (i + t < cnt) r[t] = ld_stream(row + base + i + t), v[t] = ld_stream(val + base + i + t);
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (i + t < cnt) {
+            const int k = 4 * g + t, pos = s_start[c[k] >> bits] + rank[k];
+            s_row[pos] = r[t];
+            s_val[pos] = v[t];
+            s_col[pos] = c[k];
+          }
       }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kPer; ++k)
+        if (item(k) < cnt) {
+          const int pos = s_start[c[k] >> bits] + rank[k];
+          s_row[pos] = (int)ld_hint(row + base + item(k), once);
+          s_val[pos] = __uint_as_float(ld_hint(val + base + item(k), once));
+          s_col[pos] = c[k];
+        }
+    }
     __syncthreads();
     // bucket runs out: consecutive positions of a bucket go to consecutive
     // addresses of the bucket's range
@@ -316,7 +391,7 @@ __global__ void __launch_bounds__(kSortThreads, 1) k_bkt_sort(const int32_t* __r
                                                                const int32_t* __restrict__ off, int p, int bits,
                                                                int64_t n, int64_t nnz, int32_t* __restrict__ ptr,
                                                                int32_t* __restrict__ orow, float* __restrict__ oval) {
-  extern __shared__ int32_t sm2[];  // cnt[4096] | srow[kBucketCap] | sval[kBucketCap]
+  extern __shared__ int32_t sm2[];  // cnt[8192] | srow[kBucketCap] | sval[kBucketCap]
   int32_t* cnt = sm2;
   int32_t* srow = sm2 + (1 << kMaxBucketBits);
   float* sval = reinterpret_cast<float*>(srow + kBucketCap);
@@ -328,17 +403,13 @@ __global__ void __launch_bounds__(kSortThreads, 1) k_bkt_sort(const int32_t* __r
   const int ncols = n - c0 < ncols_b ? (int)(n - c0) : ncols_b;
   for (int i = threadIdx.x; i < ncols_b; i += kSortThreads) cnt[i] = 0;
   __syncthreads();
-  // per entry: row, value, and (slot within its column << 16 | column)
-  int r[kSortPer], cs[kSortPer];
-  float v[kSortPer];
+  // per entry: (slot within its column << 16 | column); rows and values are
+  // loaded once the column starts are known, straight into their places
+  int cs[kSortPer];
 #pragma unroll
   for (int k = 0; k < kSortPer; ++k) {
     const int i = k * kSortThreads + threadIdx.x;
-    if (i < size) {
-      r[k] = trow[s + i];
-      v[k] = tval[s + i];
-      cs[k] = tcol[s + i];
-    }
+    if (i < size) cs[k] = tcol[s + i];
   }
 #pragma unroll
   for (int k = 0; k < kSortPer; ++k)
@@ -361,12 +432,14 @@ __global__ void __launch_bounds__(kSortThreads, 1) k_bkt_sort(const int32_t* __r
     }
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < kSortPer; ++k)
-    if (k * kSortThreads + threadIdx.x < size) {
+  for (int k = 0; k < kSortPer; ++k) {
+    const int i = k * kSortThreads + threadIdx.x;
+    if (i < size) {
       const int pos = cnt[cs[k] & 0xffff] + (cs[k] >> 16);
-      srow[pos] = r[k];
-      sval[pos] = v[k];
+      srow[pos] = trow[s + i];
+      sval[pos] = tval[s + i];
     }
+  }
   __syncthreads();
   // each column's rows in ascending order (columns are short; the reference
   // order is the stable sort of a row-sorted input)
@@ -409,13 +482,13 @@ int bits_for(int64_t extent) {
 bool csc_by_column_buckets(sfg_context* ctx, const sfg_tensor* s, sfg_tensor* t) {
   const int64_t n = s->n, nnz = s->nnz;
   // fewest buckets (longest pass-1 runs) whose average fill is at most 3/4
-  // of a pass-2 CTA's capacity, with <= 4,096 columns per bucket
+  // of a pass-2 CTA's capacity, with <= 8,192 columns per bucket
   constexpr int64_t kAvgFill = kBucketCap * 3 / 4;
   int bits = kMaxBucketBits;
   while (bits > 0 && ceil_div(n, int64_t(1) << bits) * kAvgFill < nnz) --bits;
   const int64_t nb = ceil_div(n, int64_t(1) << bits);
   if (nb > kMaxBuckets || nb * kAvgFill < nnz) return false;
-  const int p = ctx->sms;  // one pass-1 CTA per SM (196 KB of shared memory each)
+  const int p = ctx->sms;  // one pass-1 CTA per SM
   const int64_t cells = nb * p;
   int32_t* counts = dalloc_n<int32_t>(ctx, cells);
   int32_t* off = dalloc_n<int32_t>(ctx, cells + 1);
@@ -424,7 +497,12 @@ bool csc_by_column_buckets(sfg_context* ctx, const sfg_tensor* s, sfg_tensor* t)
   auto* status = lookback_status(ctx, tiles);
   auto* mx = static_cast<int32_t*>(scratch(ctx, 64));
   SFG_CUDA(cudaMemsetAsync(mx, 0, 8, ctx->stream));
-  SFG_LAUNCH(k_bkt_count, p, kPartThreads, 0, ctx->stream, s->idx, nnz, bits, (int)nb, counts);
+  const bool vec = ((reinterpret_cast<uintptr_t>(s->row) | reinterpret_cast<uintptr_t>(s->idx) |
+                     reinterpret_cast<uintptr_t>(s->val)) & 15) == 0;
+  if (vec)
+    SFG_LAUNCH(k_bkt_count<true>, p, kPartThreads, 0, ctx->stream, s->idx, nnz, bits, (int)nb, counts);
+  else
+    SFG_LAUNCH(k_bkt_count<false>, p, kPartThreads, 0, ctx->stream, s->idx, nnz, bits, (int)nb, counts);
   SFG_LAUNCH(k_count_scan, tiles, kBlock, 0, ctx->stream, counts, (int32_t)cells, off, dummy, status,
              ctx->epoch++, mx + 1);
   SFG_LAUNCH(k_blk_max, (int)std::min<int64_t>(ceil_div(nb, kBlock), 64), kBlock, 0, ctx->stream, off, (int)nb, p,
@@ -436,10 +514,22 @@ bool csc_by_column_buckets(sfg_context* ctx, const sfg_tensor* s, sfg_tensor* t)
   int32_t* trow = dalloc_n<int32_t>(ctx, nnz);
   float* tval = dalloc_n<float>(ctx, nnz);
   uint16_t* tcol = dalloc_n<uint16_t>(ctx, nnz);
-  const size_t smem = (size_t)3 * kPartTile * 4 + (size_t)3 * kMaxBuckets * 4;
-  SFG_CUDA(cudaFuncSetAttribute(k_bkt_part, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  SFG_LAUNCH(k_bkt_part, p, kPartThreads, smem, ctx->stream, s->row, s->idx, static_cast<const float*>(s->val), nnz,
-             bits, (int)nb, off, trow, tval, tcol);
+  // pass-1 tile: 16,384 entries when the bucket counters leave room, else 12,288
+  const bool big_tile = (size_t)3 * kPartThreads * 32 * 4 + (size_t)3 * nb * 4 <= 227 * 1024;
+  const size_t smem = (size_t)3 * kPartThreads * (big_tile ? 32 : kPartPer) * 4 + (size_t)3 * nb * 4;
+  const float* sv = static_cast<const float*>(s->val);
+#define SFG_BKT_PART(V, P)                                                                                    \
+  do {                                                                                                        \
+    const auto k_bkt_part_ = k_bkt_part<V, P>;                                                                \
+    SFG_CUDA(cudaFuncSetAttribute(k_bkt_part_, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));      \
+    SFG_LAUNCH(k_bkt_part_, p, kPartThreads, smem, ctx->stream, s->row, s->idx, sv, nnz, bits, (int)nb, off,    \
+               trow, tval, tcol);                                                                             \
+  } while (0)
+  if (vec && big_tile) SFG_BKT_PART(true, 32);
+  else if (vec) SFG_BKT_PART(true, kPartPer);
+  else if (big_tile) SFG_BKT_PART(false, 32);
+  else SFG_BKT_PART(false, kPartPer);
+#undef SFG_BKT_PART
   int32_t big = 0;
   read_back_wait(ctx, sizeof big, &big);
   auto release = [&] {

@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(kBlock) k_csc_unpack(const uint64_t* __restric
 // --------------------------------------------- column-bucket partition path
 // Two passes, atomic-free in global memory and coalesced both ways.
 // (0) Each of P CTAs counts its contiguous share of the entries per column
-//     bucket (2^bits columns) in shared memory; an exclusive scan over
+//     bucket (w consecutive columns) in shared memory; an exclusive scan over
 //     (bucket, CTA) gives every CTA its write range inside every bucket.
 // (1) Each CTA reorders its share, a tile of entries at a time, by bucket
 //     in shared memory and writes each bucket's run to the bucket's range:
@@ -192,10 +192,27 @@ __global__ void __launch_bounds__(kBlock) k_csc_unpack(const uint64_t* __restric
 constexpr int kPartThreads = 512;
 constexpr int kPartPer = 24;                          // entries per thread per round
 constexpr int kMaxBuckets = 4096;
-constexpr int kMaxBucketBits = 13;                    // columns per bucket <= 8,192
+constexpr int kMaxBucketCols = 8192;                 // columns per bucket
 constexpr int kSortThreads = 1024;
 constexpr int kSortPer = 22;
 constexpr int kBucketCap = kSortThreads * kSortPer;   // 22,528 entries sorted per pass-2 CTA
+
+// Bucket of column c < 2^31: c / w as a multiply-high, m = ceil(2^k / w) with
+// k = 31 + ceil(log2 w) (then m < 2^32 and c * (m * w - 2^k) < 2^k, so the
+// quotient is exact).
+struct BucketDiv {
+  uint32_t w, m;
+  int k;
+  __device__ __forceinline__ uint32_t operator()(int32_t c) const {
+    return (uint32_t)(((uint64_t)(uint32_t)c * m) >> k);
+  }
+};
+BucketDiv bucket_div(uint32_t w) {
+  int l = 0;
+  while ((uint64_t(1) << l) < w) ++l;
+  const int k = 31 + l;
+  return {w, (uint32_t)(((uint64_t(1) << k) + w - 1) / w), k};
+}
 
 // Entries [e0, e1) of pass-1 CTA `cta`: equal shares rounded up to a
 // multiple of 4, so each share starts 16-byte aligned (k_bkt_count and
@@ -208,7 +225,7 @@ __device__ __forceinline__ void part_range(int64_t nnz, int cta, int ctas, int64
 
 // kVec: the input arrays are 16-byte aligned (int4 loads, four entries each)
 template <bool kVec>
-__global__ void __launch_bounds__(kPartThreads) k_bkt_count(const int32_t* __restrict__ col, int64_t nnz, int bits,
+__global__ void __launch_bounds__(kPartThreads) k_bkt_count(const int32_t* __restrict__ col, int64_t nnz, BucketDiv bkt,
                                                              int nb, int32_t* __restrict__ counts) {
   __shared__ int32_t h[kMaxBuckets];
   for (int i = threadIdx.x; i < nb; i += kPartThreads) h[i] = 0;
@@ -228,10 +245,10 @@ __global__ void __launch_bounds__(kPartThreads) k_bkt_count(const int32_t* __res
 #pragma unroll
       for (int u = 0; u < U; ++u)
         if (q[u].x >= 0) {
-          atomicAdd(&h[q[u].x >> bits], 1);
-          atomicAdd(&h[q[u].y >> bits], 1);
-          atomicAdd(&h[q[u].z >> bits], 1);
-          atomicAdd(&h[q[u].w >> bits], 1);
+          atomicAdd(&h[bkt(q[u].x)], 1);
+          atomicAdd(&h[bkt(q[u].y)], 1);
+          atomicAdd(&h[bkt(q[u].z)], 1);
+          atomicAdd(&h[bkt(q[u].w)], 1);
         }
     }
     e = e0 + nv * 4 + threadIdx.x;
@@ -242,7 +259,7 @@ __global__ void __launch_bounds__(kPartThreads) k_bkt_count(const int32_t* __res
     for (int u = 0; u < U; ++u) c[u] = e + u * kPartThreads < e1 ? ld_stream(col + e + u * kPartThreads) : -1;
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (c[u] >= 0) atomicAdd(&h[c[u] >> bits], 1);
+      if (c[u] >= 0) atomicAdd(&h[bkt(c[u])], 1);
   }
   __syncthreads();
   for (int b = threadIdx.x; b < nb; b += kPartThreads) counts[(int64_t)b * gridDim.x + blockIdx.x] = h[b];
@@ -265,7 +282,7 @@ template <bool kVec, int kPer>
 __global__ void __launch_bounds__(kPartThreads, 1) k_bkt_part(const int32_t* __restrict__ row,
                                                                const int32_t* __restrict__ col,
                                                                const float* __restrict__ val, int64_t nnz,
-                                                               int bits, int nb, const int32_t* __restrict__ off,
+                                                               BucketDiv bkt, int nb, const int32_t* __restrict__ off,
                                                                int32_t* __restrict__ trow, float* __restrict__ tval,
                                                                uint16_t* __restrict__ tcol) {
   constexpr int kPartTile = kPartThreads * kPer;
@@ -280,7 +297,6 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_bkt_part(const int32_t* __r
   const int tid = threadIdx.x;
   for (int b = tid; b < nb; b += kPartThreads) s_cur[b] = off[(int64_t)b * gridDim.x + blockIdx.x];
   const uint64_t once = l2_evict_first(), keep = l2_evict_last();
-  const uint32_t cmask = (1u << bits) - 1;
   int64_t e0, e1;
   part_range(nnz, blockIdx.x, gridDim.x, e0, e1);
   constexpr int kBPer = kMaxBuckets / kPartThreads;  // buckets per thread in the scan
@@ -315,7 +331,7 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_bkt_part(const int32_t* __r
     }
 #pragma unroll
     for (int k = 0; k < kPer; ++k)
-      if (item(k) < cnt) rank[k] = atomicAdd(&s_cnt[c[k] >> bits], 1);
+      if (item(k) < cnt) rank[k] = atomicAdd(&s_cnt[bkt(c[k])], 1);
     __syncthreads();
     int loc[kBPer], sum = 0;
 #pragma unroll
@@ -352,7 +368,7 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_bkt_part(const int32_t* __r
 #pragma unroll
         for (int t = 0; t < 4; ++t)
           if (i + t < cnt) {
-            const int k = 4 * g + t, pos = s_start[c[k] >> bits] + rank[k];
+            const int k = 4 * g + t, pos = s_start[bkt(c[k])] + rank[k];
             s_row[pos] = r[t];
             s_val[pos] = v[t];
             s_col[pos] = c[k];
@@ -362,7 +378,7 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_bkt_part(const int32_t* __r
 #pragma unroll
       for (int k = 0; k < kPer; ++k)
         if (item(k) < cnt) {
-          const int pos = s_start[c[k] >> bits] + rank[k];
+          const int pos = s_start[bkt(c[k])] + rank[k];
           s_row[pos] = (int)ld_hint(row + base + item(k), once);
           s_val[pos] = __uint_as_float(ld_hint(val + base + item(k), once));
           s_col[pos] = c[k];
@@ -372,11 +388,11 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_bkt_part(const int32_t* __r
     // bucket runs out: consecutive positions of a bucket go to consecutive
     // addresses of the bucket's range
     for (int p = tid; p < cnt; p += kPartThreads) {
-      const int cc = s_col[p], b = cc >> bits;
+      const int cc = s_col[p], b = bkt(cc);
       const int64_t dst = (int64_t)s_cur[b] + (p - s_start[b]);
       st_hint(trow + dst, (uint32_t)s_row[p], keep);
       st_hint(tval + dst, __float_as_uint(s_val[p]), keep);
-      tcol[dst] = (uint16_t)(cc & cmask);
+      tcol[dst] = (uint16_t)(cc - b * (int)bkt.w);
     }
     __syncthreads();
     for (int b = tid; b < nb; b += kPartThreads) s_cur[b] += s_cnt[b];
@@ -388,18 +404,18 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_bkt_part(const int32_t* __r
 __global__ void __launch_bounds__(kSortThreads, 1) k_bkt_sort(const int32_t* __restrict__ trow,
                                                                const float* __restrict__ tval,
                                                                const uint16_t* __restrict__ tcol,
-                                                               const int32_t* __restrict__ off, int p, int bits,
+                                                               const int32_t* __restrict__ off, int p, int w,
                                                                int64_t n, int64_t nnz, int32_t* __restrict__ ptr,
                                                                int32_t* __restrict__ orow, float* __restrict__ oval) {
   extern __shared__ int32_t sm2[];  // cnt[8192] | srow[kBucketCap] | sval[kBucketCap]
   int32_t* cnt = sm2;
-  int32_t* srow = sm2 + (1 << kMaxBucketBits);
+  int32_t* srow = sm2 + kMaxBucketCols;
   float* sval = reinterpret_cast<float*>(srow + kBucketCap);
   __shared__ uint32_t scan_smem[34];
   const int b = blockIdx.x;
-  const int ncols_b = 1 << bits;
+  const int ncols_b = w;
   const int32_t s = off[(int64_t)b * p], size = off[(int64_t)(b + 1) * p] - s;
-  const int64_t c0 = (int64_t)b << bits;
+  const int64_t c0 = (int64_t)b * w;
   const int ncols = n - c0 < ncols_b ? (int)(n - c0) : ncols_b;
   for (int i = threadIdx.x; i < ncols_b; i += kSortThreads) cnt[i] = 0;
   __syncthreads();
@@ -416,8 +432,8 @@ __global__ void __launch_bounds__(kSortThreads, 1) k_bkt_sort(const int32_t* __r
     if (k * kSortThreads + threadIdx.x < size) cs[k] |= atomicAdd(&cnt[cs[k]], 1) << 16;
   __syncthreads();
   // exclusive scan of the per-column counts; each thread owns a run of
-  // columns (ncols_b / kSortThreads, at least one)
-  const int per = ncols_b >= kSortThreads ? ncols_b / kSortThreads : 1;
+  // columns (ceil(ncols_b / kSortThreads))
+  const int per = (ncols_b + kSortThreads - 1) / kSortThreads;
   const int cbeg = threadIdx.x * per;
   int sum = 0;
   for (int q = 0; q < per; ++q) sum += cbeg + q < ncols_b ? cnt[cbeg + q] : 0;
@@ -482,13 +498,17 @@ int bits_for(int64_t extent) {
 bool csc_by_column_buckets(sfg_context* ctx, const sfg_tensor* s, sfg_tensor* t) {
   const int64_t n = s->n, nnz = s->nnz;
   // fewest buckets (longest pass-1 runs) whose average fill is at most 3/4
-  // of a pass-2 CTA's capacity, with <= 8,192 columns per bucket
+  // of a pass-2 CTA's capacity, with <= kMaxBucketCols columns per bucket;
+  // a count of several waves is rounded up to a multiple of the SM count so
+  // that pass 2 runs full waves
   constexpr int64_t kAvgFill = kBucketCap * 3 / 4;
-  int bits = kMaxBucketBits;
-  while (bits > 0 && ceil_div(n, int64_t(1) << bits) * kAvgFill < nnz) --bits;
-  const int64_t nb = ceil_div(n, int64_t(1) << bits);
-  if (nb > kMaxBuckets || nb * kAvgFill < nnz) return false;
   const int p = ctx->sms;  // one pass-1 CTA per SM
+  int64_t nb = std::max(ceil_div(nnz, kAvgFill), ceil_div(n, int64_t(kMaxBucketCols)));
+  if (nb > p / 2) nb = ceil_div(nb, int64_t(p)) * p;
+  const int64_t w = ceil_div(n, nb);
+  nb = ceil_div(n, w);
+  const BucketDiv bkt = bucket_div((uint32_t)w);
+  if (nb > kMaxBuckets || nb * kAvgFill < nnz) return false;
   const int64_t cells = nb * p;
   int32_t* counts = dalloc_n<int32_t>(ctx, cells);
   int32_t* off = dalloc_n<int32_t>(ctx, cells + 1);
@@ -500,9 +520,9 @@ bool csc_by_column_buckets(sfg_context* ctx, const sfg_tensor* s, sfg_tensor* t)
   const bool vec = ((reinterpret_cast<uintptr_t>(s->row) | reinterpret_cast<uintptr_t>(s->idx) |
                      reinterpret_cast<uintptr_t>(s->val)) & 15) == 0;
   if (vec)
-    SFG_LAUNCH(k_bkt_count<true>, p, kPartThreads, 0, ctx->stream, s->idx, nnz, bits, (int)nb, counts);
+    SFG_LAUNCH(k_bkt_count<true>, p, kPartThreads, 0, ctx->stream, s->idx, nnz, bkt, (int)nb, counts);
   else
-    SFG_LAUNCH(k_bkt_count<false>, p, kPartThreads, 0, ctx->stream, s->idx, nnz, bits, (int)nb, counts);
+    SFG_LAUNCH(k_bkt_count<false>, p, kPartThreads, 0, ctx->stream, s->idx, nnz, bkt, (int)nb, counts);
   SFG_LAUNCH(k_count_scan, tiles, kBlock, 0, ctx->stream, counts, (int32_t)cells, off, dummy, status,
              ctx->epoch++, mx + 1);
   SFG_LAUNCH(k_blk_max, (int)std::min<int64_t>(ceil_div(nb, kBlock), 64), kBlock, 0, ctx->stream, off, (int)nb, p,
@@ -522,7 +542,7 @@ bool csc_by_column_buckets(sfg_context* ctx, const sfg_tensor* s, sfg_tensor* t)
   do {                                                                                                        \
     const auto k_bkt_part_ = k_bkt_part<V, P>;                                                                \
     SFG_CUDA(cudaFuncSetAttribute(k_bkt_part_, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));      \
-    SFG_LAUNCH(k_bkt_part_, p, kPartThreads, smem, ctx->stream, s->row, s->idx, sv, nnz, bits, (int)nb, off,    \
+    SFG_LAUNCH(k_bkt_part_, p, kPartThreads, smem, ctx->stream, s->row, s->idx, sv, nnz, bkt, (int)nb, off,              \
                trow, tval, tcol);                                                                             \
   } while (0)
   if (vec && big_tile) SFG_BKT_PART(true, 32);
@@ -539,9 +559,9 @@ bool csc_by_column_buckets(sfg_context* ctx, const sfg_tensor* s, sfg_tensor* t)
     release();
     return false;
   }
-  const size_t smem2 = ((size_t)(1 << kMaxBucketBits) + 2 * kBucketCap) * 4;
+  const size_t smem2 = ((size_t)kMaxBucketCols + 2 * kBucketCap) * 4;
   SFG_CUDA(cudaFuncSetAttribute(k_bkt_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-  SFG_LAUNCH(k_bkt_sort, (int)nb, kSortThreads, smem2, ctx->stream, trow, tval, tcol, off, p, bits, n, nnz, t->ptr,
+  SFG_LAUNCH(k_bkt_sort, (int)nb, kSortThreads, smem2, ctx->stream, trow, tval, tcol, off, p, (int)w, n, nnz, t->ptr,
              t->idx, static_cast<float*>(t->val));
   release();
   return true;

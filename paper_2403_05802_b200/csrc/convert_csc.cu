@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kBlock) k_csc_unpack(const uint64_t* __restric
 //     in shared memory and writes each bucket's run to the bucket's range:
 //     consecutive threads write consecutive addresses. The intermediate
 //     (row, value, column-in-bucket: 10 B an entry) is kept in L2 for pass 2.
-// (2) One CTA per bucket loads its <= kBucketCap entries, counts them per
+// (2) One CTA per bucket loads its <= kSortPer x threads entries, counts them per
 //     column, places them by column, insertion-sorts each (short) column by
 //     row — the stable order of the row-sorted input — and writes idx / val
 //     / ptr of its columns with coalesced stores.
@@ -193,9 +193,7 @@ constexpr int kPartThreads = 512;
 constexpr int kPartPer = 24;                          // entries per thread per round
 constexpr int kMaxBuckets = 4096;
 constexpr int kMaxBucketCols = 8192;                 // columns per bucket
-constexpr int kSortThreads = 1024;
-constexpr int kSortPer = 22;
-constexpr int kBucketCap = kSortThreads * kSortPer;   // 22,528 entries sorted per pass-2 CTA
+constexpr int kSortPer = 22;                           // entries per pass-2 thread
 
 // Bucket of column c < 2^31: c / w as a multiply-high, m = ceil(2^k / w) with
 // k = 31 + ceil(log2 w) (then m < 2^32 and c * (m * w - 2^k) < 2^k, so the
@@ -401,15 +399,17 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_bkt_part(const int32_t* __r
 
 // Pass 2: a CTA per bucket. Static shared memory: sorted rows and values of
 // <= kBucketCap entries, per-column counts / starts.
-__global__ void __launch_bounds__(kSortThreads, 1) k_bkt_sort(const int32_t* __restrict__ trow,
+template <int kSortThreads, int kMinBlocks>
+__global__ void __launch_bounds__(kSortThreads, kMinBlocks) k_bkt_sort(const int32_t* __restrict__ trow,
                                                                const float* __restrict__ tval,
                                                                const uint16_t* __restrict__ tcol,
                                                                const int32_t* __restrict__ off, int p, int w,
                                                                int64_t n, int64_t nnz, int32_t* __restrict__ ptr,
                                                                int32_t* __restrict__ orow, float* __restrict__ oval) {
-  extern __shared__ int32_t sm2[];  // cnt[8192] | srow[kBucketCap] | sval[kBucketCap]
+  constexpr int kBucketCap = kSortThreads * kSortPer;
+  extern __shared__ int32_t sm2[];  // cnt[w] | srow[kBucketCap] | sval[kBucketCap]
   int32_t* cnt = sm2;
-  int32_t* srow = sm2 + kMaxBucketCols;
+  int32_t* srow = sm2 + w;
   float* sval = reinterpret_cast<float*>(srow + kBucketCap);
   __shared__ uint32_t scan_smem[34];
   const int b = blockIdx.x;
@@ -498,13 +498,18 @@ int bits_for(int64_t extent) {
 bool csc_by_column_buckets(sfg_context* ctx, const sfg_tensor* s, sfg_tensor* t) {
   const int64_t n = s->n, nnz = s->nnz;
   // fewest buckets (longest pass-1 runs) whose average fill is at most 3/4
-  // of a pass-2 CTA's capacity, with <= kMaxBucketCols columns per bucket;
-  // a count of several waves is rounded up to a multiple of the SM count so
-  // that pass 2 runs full waves
-  constexpr int64_t kAvgFill = kBucketCap * 3 / 4;
+  // of a pass-2 CTA's capacity, with <= max_cols columns per bucket; a
+  // count of several waves is rounded up to whole pass-2 waves.
+  // Pass 2: one 1,024-thread CTA per SM (22,528 entries per bucket), or with
+  // SFG_CSC_SORT=512 two 512-thread CTAs per SM (11,264 entries)
+  const char* sort_env = getenv("SFG_CSC_SORT");
+  const int sort_threads = sort_env && atoi(sort_env) == 512 ? 512 : 1024;
+  const int64_t cap = (int64_t)sort_threads * kSortPer, max_cols = sort_threads == 512 ? 4096 : kMaxBucketCols;
+  const int64_t kAvgFill = cap * 3 / 4;
   const int p = ctx->sms;  // one pass-1 CTA per SM
-  int64_t nb = std::max(ceil_div(nnz, kAvgFill), ceil_div(n, int64_t(kMaxBucketCols)));
-  if (nb > p / 2) nb = ceil_div(nb, int64_t(p)) * p;
+  const int wave = sort_threads == 512 ? 2 * p : p;
+  int64_t nb = std::max(ceil_div(nnz, kAvgFill), ceil_div(n, max_cols));
+  if (nb > wave / 2) nb = ceil_div(nb, int64_t(wave)) * wave;
   const int64_t w = ceil_div(n, nb);
   nb = ceil_div(n, w);
   const BucketDiv bkt = bucket_div((uint32_t)w);
@@ -555,14 +560,22 @@ bool csc_by_column_buckets(sfg_context* ctx, const sfg_tensor* s, sfg_tensor* t)
   auto release = [&] {
     for (void* q : {(void*)counts, (void*)off, (void*)dummy, (void*)trow, (void*)tval, (void*)tcol}) dfree(ctx, q);
   };
-  if (big > kBucketCap) {
+  if (big > cap) {
     release();
     return false;
   }
-  const size_t smem2 = ((size_t)kMaxBucketCols + 2 * kBucketCap) * 4;
-  SFG_CUDA(cudaFuncSetAttribute(k_bkt_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-  SFG_LAUNCH(k_bkt_sort, (int)nb, kSortThreads, smem2, ctx->stream, trow, tval, tcol, off, p, (int)w, n, nnz, t->ptr,
-             t->idx, static_cast<float*>(t->val));
+  const size_t smem2 = ((size_t)w + 2 * cap) * 4;
+  if (sort_threads == 512) {
+    const auto k_bkt_sort_ = k_bkt_sort<512, 2>;
+    SFG_CUDA(cudaFuncSetAttribute(k_bkt_sort_, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+    SFG_LAUNCH(k_bkt_sort_, (int)nb, 512, smem2, ctx->stream, trow, tval, tcol, off, p, (int)w, n, nnz,
+               t->ptr, t->idx, static_cast<float*>(t->val));
+  } else {
+    const auto k_bkt_sort_ = k_bkt_sort<1024, 1>;
+    SFG_CUDA(cudaFuncSetAttribute(k_bkt_sort_, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+    SFG_LAUNCH(k_bkt_sort_, (int)nb, 1024, smem2, ctx->stream, trow, tval, tcol, off, p, (int)w, n, nnz,
+               t->ptr, t->idx, static_cast<float*>(t->val));
+  }
   release();
   return true;
 }

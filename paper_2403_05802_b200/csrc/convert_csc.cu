@@ -8,14 +8,14 @@
 // roles of rows and columns exchanged (storage.hpp:171-200).
 //
 // Device plan. (1) Column-bucket partition (every bucket of <= 8,192
-// columns holds <= 22,528 entries, e.g. the hypersparse config 3): count per bucket,
-// scan, scatter into block regions, sort each block in shared memory —
-// below. (2) Otherwise, when every column holds <= kShortCol entries:
+// columns holds <= 22,528 entries, e.g. the hypersparse config 3): count
+// per bucket, scan, scatter into bucket regions, sort each bucket in shared
+// memory — below. (2) Otherwise, when every column holds <= kShortCol entries:
 // column histogram (RED atomics) -> single-pass look-back scan ->
 // atomic-cursor scatter -> per-column insertion sort by row, which restores
 // the stable order. (3) Any longer column: stable LSD radix sort on the
 // column bits with the row carried in the upper key half, then compression
-// of the sorted columns. Config 3 (8.4 M entries, 4 M columns): (1) 0.35 ms,
+// of the sorted columns. Config 3 (8.4 M entries, 4 M columns): (1) 0.21 ms,
 // (2) 0.37 ms.
 #include "async.cuh"
 #include "devutil.cuh"
@@ -185,15 +185,15 @@ __global__ void __launch_bounds__(kBlock) k_csc_unpack(const uint64_t* __restric
 //     in shared memory and writes each bucket's run to the bucket's range:
 //     consecutive threads write consecutive addresses. The intermediate
 //     (row, value, column-in-bucket: 10 B an entry) is kept in L2 for pass 2.
-// (2) One CTA per bucket loads its <= kSortPer x threads entries, counts them per
-//     column, places them by column, insertion-sorts each (short) column by
+// (2) One CTA per bucket loads its <= kSortPer x threads entries, counts
+//     them per column, places them by column, insertion-sorts each (short) column by
 //     row — the stable order of the row-sorted input — and writes idx / val
 //     / ptr of its columns with coalesced stores.
 constexpr int kPartThreads = 512;
-constexpr int kPartPer = 24;                          // entries per thread per round
+constexpr int kPartPer = 24;        // pass-1 entries per thread per round (32 when shared memory allows)
 constexpr int kMaxBuckets = 4096;
-constexpr int kMaxBucketCols = 8192;                 // columns per bucket
-constexpr int kSortPer = 22;                           // entries per pass-2 thread
+constexpr int kMaxBucketCols = 8192;  // columns per bucket
+constexpr int kSortPer = 22;        // pass-2 entries per thread
 
 // Bucket of column c < 2^31: c / w as a multiply-high, m = ceil(2^k / w) with
 // k = 31 + ceil(log2 w) (then m < 2^32 and c * (m * w - 2^k) < 2^k, so the

@@ -39,9 +39,11 @@ def test_csc_long_columns_general_path(ctx, port, seed):
 
 @pytest.mark.parametrize("m,n,nnz", [(1 << 22, 1 << 22, 300_000), (5000, 70_000, 150_000), (100, 1500, 60_000)])
 def test_csc_column_blocks(ctx, port, m, n, nnz):
-    # the column-block partition path: many blocks of 1,024 columns, each
-    # sorted in shared memory; the last block is partial when n % 1024 != 0;
-    # (100, 1500, 60000) puts ~40 rows in a column (dense short matrix)
+    # the column-bucket partition path: buckets of w <= 8,192 columns (w not a
+    # power of two: 7,086 for the first case, whose 592 buckets are rounded
+    # up to whole waves of the SM count), each sorted in shared memory; the
+    # last bucket is partial; (100, 1500, 60000) puts ~40 rows in a column
+    # (dense short matrix)
     rng = np.random.default_rng(nnz)
     key = np.unique(rng.integers(0, m * n, nnz, dtype=np.int64))
     r, c = key // n, key % n
@@ -51,12 +53,17 @@ def test_csc_column_blocks(ctx, port, m, n, nnz):
 
 
 def test_csc_block_overflow_takes_histogram_path(ctx, port):
-    # ~10 entries per column but > 4,096 entries per column block: the
-    # per-column histogram path (short columns, atomic cursors)
-    m, n = 50_000, 3000
+    # 15 entries in each of the first 2,000 columns plus scattered ones: the
+    # first column bucket holds > 22,528 entries (more than one pass-2 CTA
+    # sorts), so the conversion takes the per-column histogram path (short
+    # columns, atomic cursors)
+    m, n = 50_000, 100_000
     rng = np.random.default_rng(3)
-    key = np.unique(rng.integers(0, m * n, 30_000, dtype=np.int64))
+    dense_r = np.concatenate([rng.choice(m, 15, replace=False) for _ in range(2000)])
+    dense_c = np.repeat(np.arange(2000), 15)
+    key = np.unique(np.concatenate([dense_r * n + dense_c, rng.integers(0, m * n, 1000, dtype=np.int64)]))
     r, c = key // n, key % n
+    assert np.bincount(c).max() <= 32 and np.count_nonzero(c < 7693) > 22_528
     v = (rng.random(len(key)) + 0.5).astype(np.float32)
     d, p = ctx.from_coo(m, n, r, c, v), port.from_coo(m, n, r, c, v)
     assert_same_materialized(ctx.convert(d, "CSC").download(), port.convert(p, "CSC").download(), "CSC")

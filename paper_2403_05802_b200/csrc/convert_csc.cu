@@ -298,17 +298,15 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_bkt_part(const int32_t* __r
   int64_t e0, e1;
   part_range(nnz, blockIdx.x, gridDim.x, e0, e1);
   constexpr int kBPer = kMaxBuckets / kPartThreads;  // buckets per thread in the scan
-  for (int64_t base = e0; base < e1; base += kPartTile) {
-    const int cnt = (int)(e1 - base < kPartTile ? e1 - base : kPartTile);
-    for (int b = tid; b < nb; b += kPartThreads) s_cnt[b] = 0;
-    __syncthreads();
-    int c[kPer], rank[kPer];
-    // slot k of this thread is tile entry item(k); with kVec, four
-    // consecutive entries per int4 load (order within a bucket run does not
-    // matter: pass 2 sorts each column by row). Only the columns are held in
-    // registers; rows and values are loaded after the scan, straight into
-    // their places.
-    auto item = [&](int k) { return kVec ? 4 * ((k >> 2) * kPartThreads + tid) + (k & 3) : k * kPartThreads + tid; };
+  // slot k of this thread is tile entry item(k); with kVec, four
+  // consecutive entries per int4 load (order within a bucket run does not
+  // matter: pass 2 sorts each column by row). Only the columns are held in
+  // registers — the next tile's are loaded while this tile's runs are
+  // written out; rows and values are loaded after the scan, straight into
+  // their places.
+  auto item = [&](int k) { return kVec ? 4 * ((k >> 2) * kPartThreads + tid) + (k & 3) : k * kPartThreads + tid; };
+  int c[kPer], rank[kPer];
+  auto load_cols = [&](int64_t base, int cnt) {
     if constexpr (kVec) {
 #pragma unroll
       for (int g = 0; g < kPer / 4; ++g) {
@@ -327,6 +325,13 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_bkt_part(const int32_t* __r
       for (int k = 0; k < kPer; ++k)
         if (item(k) < cnt) c[k] = (int)ld_hint(col + base + item(k), once);
     }
+  };
+  auto tile_len = [&](int64_t base) { return (int)(e1 - base < kPartTile ? e1 - base : kPartTile); };
+  if (e0 < e1) load_cols(e0, tile_len(e0));
+  for (int64_t base = e0; base < e1; base += kPartTile) {
+    const int cnt = tile_len(base);
+    for (int b = tid; b < nb; b += kPartThreads) s_cnt[b] = 0;
+    __syncthreads();
 #pragma unroll
     for (int k = 0; k < kPer; ++k)
       if (item(k) < cnt) rank[k] = atomicAdd(&s_cnt[bkt(c[k])], 1);
@@ -383,6 +388,7 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_bkt_part(const int32_t* __r
         }
     }
     __syncthreads();
+    if (base + kPartTile < e1) load_cols(base + kPartTile, tile_len(base + kPartTile));
     // bucket runs out: consecutive positions of a bucket go to consecutive
     // addresses of the bucket's range
     for (int p = tid; p < cnt; p += kPartThreads) {

@@ -235,11 +235,17 @@ __global__ void __launch_bounds__(kPartThreads) k_bkt_count(const int32_t* __res
   if constexpr (kVec) {
     const int64_t nv = (e1 - e0) >> 2;
     const int4* c4 = reinterpret_cast<const int4*>(col + e0);
-    for (int64_t j = threadIdx.x; j < nv; j += U * kPartThreads) {
-      int4 q[U];
+    // double-buffered: the next batch's loads are in flight while this
+    // batch is counted
+    int4 q[U], nq[U];
+    auto load = [&](int4 (&dst)[U], int64_t j) {
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        q[u] = j + u * kPartThreads < nv ? ld_stream(c4 + j + u * kPartThreads) : make_int4(-1, -1, -1, -1);
+        dst[u] = j + u * kPartThreads < nv ? ld_stream(c4 + j + u * kPartThreads) : make_int4(-1, -1, -1, -1);
+    };
+    load(q, threadIdx.x);
+    for (int64_t j = threadIdx.x; j < nv; j += U * kPartThreads) {
+      if (j + U * kPartThreads < nv) load(nq, j + U * kPartThreads);
 #pragma unroll
       for (int u = 0; u < U; ++u)
         if (q[u].x >= 0) {
@@ -248,6 +254,8 @@ __global__ void __launch_bounds__(kPartThreads) k_bkt_count(const int32_t* __res
           atomicAdd(&h[bkt(q[u].z)], 1);
           atomicAdd(&h[bkt(q[u].w)], 1);
         }
+#pragma unroll
+      for (int u = 0; u < U; ++u) q[u] = nq[u];
     }
     e = e0 + nv * 4 + threadIdx.x;
   }

@@ -224,8 +224,11 @@ __device__ __forceinline__ void part_range(int64_t nnz, int cta, int ctas, int64
 // kVec: the input arrays are 16-byte aligned (int4 loads, four entries each)
 template <bool kVec>
 __global__ void __launch_bounds__(kPartThreads) k_bkt_count(const int32_t* __restrict__ col, int64_t nnz, BucketDiv bkt,
-                                                             int nb, int32_t* __restrict__ counts) {
+                                                             int nb, int32_t* __restrict__ counts,
+                                                             int32_t* __restrict__ btot, uint32_t* __restrict__ done,
+                                                             int32_t* __restrict__ mx) {
   __shared__ int32_t h[kMaxBuckets];
+  __shared__ bool last;
   for (int i = threadIdx.x; i < nb; i += kPartThreads) h[i] = 0;
   __syncthreads();
   int64_t e0, e1;
@@ -268,16 +271,23 @@ __global__ void __launch_bounds__(kPartThreads) k_bkt_count(const int32_t* __res
       if (c[u] >= 0) atomicAdd(&h[bkt(c[u])], 1);
   }
   __syncthreads();
-  for (int b = threadIdx.x; b < nb; b += kPartThreads) counts[(int64_t)b * gridDim.x + blockIdx.x] = h[b];
-}
-
-__global__ void __launch_bounds__(kBlock) k_blk_max(const int32_t* __restrict__ off, int nb, int p,
-                                                     int32_t* __restrict__ mx) {
-  int m = 0;
-  for (int b = blockIdx.x * kBlock + threadIdx.x; b < nb; b += gridDim.x * kBlock)
-    m = max(m, off[(int64_t)(b + 1) * p] - off[(int64_t)b * p]);
-  m = warp_max(m);
-  if ((threadIdx.x & 31) == 0) atomicMax(mx, m);
+  for (int b = threadIdx.x; b < nb; b += kPartThreads) {
+    counts[(int64_t)b * gridDim.x + blockIdx.x] = h[b];
+    if (h[b]) atomicAdd(btot + b, h[b]);
+  }
+  // the last CTA to finish takes the largest bucket (btot, done and mx are
+  // zeroed by the caller) for the host's pass-2 capacity check
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    int m = 0;
+    for (int b = threadIdx.x; b < nb; b += kPartThreads) m = max(m, __ldcg(btot + b));
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) atomicMax(mx, m);
+  }
 }
 
 // Pass 1. Dynamic shared memory: row, value, column of kPartTile entries,
@@ -534,22 +544,27 @@ bool csc_by_column_buckets(sfg_context* ctx, const sfg_tensor* s, sfg_tensor* t)
   int32_t* dummy = dalloc_n<int32_t>(ctx, cells);
   const int tiles = (int)ceil_div(cells, kTile);
   auto* status = lookback_status(ctx, tiles);
-  auto* mx = static_cast<int32_t*>(scratch(ctx, 64));
-  SFG_CUDA(cudaMemsetAsync(mx, 0, 8, ctx->stream));
+  // scratch: [0] largest bucket, [1] largest cell (the scan's), [2] CTAs
+  // done counting, [16, 16 + nb) bucket totals
+  auto* mx = static_cast<int32_t*>(scratch(ctx, 64 + 4 * nb));
+  SFG_CUDA(cudaMemsetAsync(mx, 0, 64 + 4 * nb, ctx->stream));
+  int32_t* btot = mx + 16;
+  auto* done = reinterpret_cast<uint32_t*>(mx + 2);
   const bool vec = ((reinterpret_cast<uintptr_t>(s->row) | reinterpret_cast<uintptr_t>(s->idx) |
                      reinterpret_cast<uintptr_t>(s->val)) & 15) == 0;
   if (vec)
-    SFG_LAUNCH(k_bkt_count<true>, p, kPartThreads, 0, ctx->stream, s->idx, nnz, bkt, (int)nb, counts);
+    SFG_LAUNCH(k_bkt_count<true>, p, kPartThreads, 0, ctx->stream, s->idx, nnz, bkt, (int)nb, counts, btot, done,
+               mx);
   else
-    SFG_LAUNCH(k_bkt_count<false>, p, kPartThreads, 0, ctx->stream, s->idx, nnz, bkt, (int)nb, counts);
+    SFG_LAUNCH(k_bkt_count<false>, p, kPartThreads, 0, ctx->stream, s->idx, nnz, bkt, (int)nb, counts, btot, done,
+               mx);
+  // the largest bucket is known after the count: its read-back starts now,
+  // and the scan and pass 1 (which needs only the offsets) are enqueued
+  // before the host waits for it, so that round trip overlaps them (an
+  // oversized bucket — rare — discards pass 1 and takes the other path)
+  read_back_start(ctx, mx, sizeof(int32_t));
   SFG_LAUNCH(k_count_scan, tiles, kBlock, 0, ctx->stream, counts, (int32_t)cells, off, dummy, status,
              ctx->epoch++, mx + 1);
-  SFG_LAUNCH(k_blk_max, (int)std::min<int64_t>(ceil_div(nb, kBlock), 64), kBlock, 0, ctx->stream, off, (int)nb, p,
-             mx);
-  // Pass 1 needs only the offsets: it is enqueued before the host waits for
-  // the largest bucket, so that round trip overlaps it (an oversized bucket
-  // — rare — discards pass 1 and takes the other path).
-  read_back_start(ctx, mx, sizeof(int32_t));
   int32_t* trow = dalloc_n<int32_t>(ctx, nnz);
   float* tval = dalloc_n<float>(ctx, nnz);
   uint16_t* tcol = dalloc_n<uint16_t>(ctx, nnz);

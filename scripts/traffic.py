@@ -14,7 +14,7 @@ FAMILIES = {
     2: {"convert": ["k_row_ptr", "k_row_scan", "k_split", "k_iota", "k_ell_fill"],
         "spmv": ["k_spmv_ell", "k_spmv_coo", "k_carry_fix"]},
     3: {"convert_dcsr": ["k_dcsr_count", "k_dcsr_heads"],
-        "convert_csc": ["k_bkt_count", "k_count_scan", "k_blk_max", "k_bkt_part", "k_bkt_sort"],
+        "convert_csc": ["k_bkt_count", "k_count_scan", "k_bkt_part", "k_bkt_sort"],
         "spmm": ["k_spmm_rows"]},
     # the per-matrix schedule (k_bcsr_plan / k_bcsr_sched) is built once and
     # cached: the step is the panel kernel alone
